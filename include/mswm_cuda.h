@@ -1,0 +1,207 @@
+/*
+ * mswm_cuda.h — C ABI of the B200-native LTS3 / TRiSK shallow-water path.
+ *
+ * This is the drop-in boundary for the reference (`mswm`, arXiv:2106.07154
+ * re-creation under /root/reference/proj).  Every entry point below replaces
+ * one reference interface; the citation after each declaration names it.
+ * Plain pointers and sizes only: no C++ or torch types cross this boundary,
+ * no exceptions escape it.  Every call returns an mswm_status; the message of
+ * the last failure on a context is available from mswm_cuda_last_error().
+ *
+ * Ids at this boundary are always the caller's ("original") ids.  The
+ * library may renumber entities internally for locality; it translates at
+ * the boundary.  All calls are synchronous with respect to the host unless
+ * they say otherwise.
+ */
+#ifndef MSWM_CUDA_H
+#define MSWM_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  Map 1:1 onto the reference exception hierarchy
+ * (proj/include/mswm/errors.hpp:9-49). */
+typedef enum {
+  MSWM_OK = 0,
+  MSWM_E_CONFIG = 1,     /* ConfigError   (errors.hpp:17-19) */
+  MSWM_E_USAGE = 2,      /* UsageError    (errors.hpp:40-43) */
+  MSWM_E_TOPOLOGY = 3,   /* TopologyError (errors.hpp:22-24) */
+  MSWM_E_DRY_VERTEX = 4, /* DryVertexError{vertex} (errors.hpp:45-49) */
+  MSWM_E_CUDA = 5,       /* CUDA runtime failure (no reference analogue) */
+  MSWM_E_NCCL = 6,       /* NCCL failure (no reference analogue) */
+  MSWM_E_NOMEM = 7       /* allocation failure */
+} mswm_status;
+
+/* Element-group bits (proj/include/mswm/integrators.hpp:43-61). */
+enum {
+  MSWM_CELLS_FINE_PLAIN = 1u << 0,
+  MSWM_CELLS_UF1 = 1u << 1,
+  MSWM_CELLS_UF2 = 1u << 2,
+  MSWM_CELLS_IF1 = 1u << 3,
+  MSWM_CELLS_IF2 = 1u << 4,
+  MSWM_CELLS_COARSE = 1u << 5,
+  MSWM_EDGES_FINE_PLAIN = 1u << 6,
+  MSWM_EDGES_UFINE = 1u << 7,
+  MSWM_EDGES_IF1 = 1u << 8,
+  MSWM_EDGES_IF2 = 1u << 9,
+  MSWM_EDGES_COARSE = 1u << 10,
+  MSWM_CELLS_ALL = 0x3Fu,
+  MSWM_EDGES_ALL = 0x7C0u,
+  MSWM_MASK_ALL = 0x7FFu
+};
+
+/* Time-stepping schemes (proj/include/mswm/integrators.hpp:26). */
+typedef enum {
+  MSWM_SSPRK2 = 0,
+  MSWM_SSPRK3 = 1,
+  MSWM_RK4 = 2,
+  MSWM_LTS2 = 3,
+  MSWM_LTS3 = 4
+} mswm_scheme;
+
+/* Closure kinds of one masked evaluation: the dependency sets the reference
+ * marks in shallow_water_tendencies (proj/src/operators.cpp:35-58) and keeps
+ * in TendencyScratch::{flux,qt,cell,vertex}_ids (operators.hpp:32). */
+typedef enum {
+  MSWM_CLOSURE_FLUX = 0,
+  MSWM_CLOSURE_QT = 1,
+  MSWM_CLOSURE_K = 2,
+  MSWM_CLOSURE_PV = 3
+} mswm_closure_kind;
+
+/* SoA views of the VoronoiMesh tables (proj/include/mswm/mesh.hpp:31-68).
+ * The caller owns the memory; mswm_cuda_create copies what it needs.
+ * Ring convention, ascending edge_cells/edge_vertices and sign rules are
+ * the reference's (mesh.hpp:26-30). */
+typedef struct mswm_mesh_desc {
+  int32_t n_cells, n_edges, n_vertices;
+  const int32_t* cell_offset;      /* [n_cells+1]  mesh.hpp:44 */
+  const int32_t* cell_edges;       /* [cell_offset[n_cells]] mesh.hpp:45 */
+  const int32_t* cell_vertices;    /* [cell_offset[n_cells]] mesh.hpp:46 */
+  const int32_t* cell_cells;       /* [cell_offset[n_cells]] mesh.hpp:47 */
+  const int32_t* edge_cells;       /* [n_edges][2] ascending, mesh.hpp:49 */
+  const int32_t* edge_vertices;    /* [n_edges][2] ascending, mesh.hpp:50 */
+  const int32_t* vertex_cells;     /* [n_vertices][3] mesh.hpp:51 */
+  const int32_t* vertex_edges;     /* [n_vertices][3] mesh.hpp:52 */
+  const int32_t* edge_edge_offset; /* [n_edges+1] mesh.hpp:56 */
+  const int32_t* edge_edges;       /* [edge_edge_offset[n_edges]] mesh.hpp:57 */
+  const int8_t* edge_cell_sign;    /* [n_edges][2] mesh.hpp:68 */
+  const int8_t* edge_vertex_sign;  /* [n_edges][2] mesh.hpp:69 */
+  const double* edge_len;          /* [n_edges] l_e  mesh.hpp:60 */
+  const double* edge_dual_len;     /* [n_edges] d_e  mesh.hpp:61 */
+  const double* cell_area;         /* [n_cells] A_i  mesh.hpp:62 */
+  const double* vertex_area;       /* [n_vertices] A_v mesh.hpp:63 */
+  const double* vertex_kite;       /* [n_vertices][3] mesh.hpp:65 */
+  const double* edge_weight;       /* aligned with edge_edges, mesh.hpp:70 */
+} mswm_mesh_desc;
+
+typedef struct mswm_cuda_ctx mswm_cuda_ctx;
+
+/* Renumbering policy for mswm_cuda_create (internal layout only; results are
+ * bitwise independent of it because per-element operation order is kept). */
+typedef enum {
+  MSWM_ORDER_INPUT = 0,   /* keep the caller's numbering */
+  MSWM_ORDER_HILBERT = 1  /* space-filling-curve order from cell adjacency */
+} mswm_order;
+
+/* Create a context on CUDA device `device`: validates and uploads the mesh,
+ * builds the device tables.  Replaces constructing SerialEvaluator
+ * (proj/src/integrators.cpp:297-314, minus b/f which come from
+ * mswm_cuda_set_fields).  On failure *out is NULL and the message is
+ * available from mswm_cuda_last_error(NULL). */
+int mswm_cuda_create(const mswm_mesh_desc* mesh, int device, int order,
+                     mswm_cuda_ctx** out);
+void mswm_cuda_destroy(mswm_cuda_ctx* ctx);
+/* Last error message of ctx, or of the last failed create when ctx is NULL. */
+const char* mswm_cuda_last_error(const mswm_cuda_ctx* ctx);
+
+/* Bottom topography b[n_cells], Coriolis f[n_vertices], gravity — the
+ * evaluator's constant inputs (SerialEvaluator ctor, integrators.hpp:79-81). */
+int mswm_cuda_set_fields(mswm_cuda_ctx* ctx, const double* b,
+                         const double* f_vertex, double gravity);
+
+/* Region classification on device from a host-evaluated fine predicate
+ * (fine_mask[n_cells] != 0 means fine).  Replaces make_regions
+ * (proj/src/regions.cpp:164-171 = label_cells :69-105 + label_underline_fine
+ * :107-139 + label_edges :141-162 + rebuild_groups :35-67).  Outputs (any may
+ * be NULL): labels with the reference's enum values (regions.hpp:12-21) and
+ * the 11 group sizes in GroupBit order.  Warnings of label_underline_fine
+ * are returned as bits in *warnings (1: uf1 empty, 2: uf2 empty,
+ * 4: no plain fine cells), may be NULL. */
+int mswm_cuda_set_regions(mswm_cuda_ctx* ctx, const uint8_t* fine_mask,
+                          int interface_width, uint8_t* cell_label,
+                          uint8_t* cell_sublabel, uint8_t* edge_label,
+                          int64_t group_size[11], int* warnings);
+
+/* Ascending original ids of group g (GroupBit index 0..10), the
+ * RegionMap::cells_* / edges_* lists (regions.hpp:35-42). */
+int mswm_cuda_get_group(mswm_cuda_ctx* ctx, int group, int32_t* ids);
+
+/* Closure set of a masked evaluation (operators.cpp:35-58), ascending
+ * original ids.  ids may be NULL to query the size only. */
+int mswm_cuda_get_closure(mswm_cuda_ctx* ctx, unsigned mask, int kind,
+                          int32_t* ids, int64_t* n);
+
+/* TendencyEvaluator::eval (proj/include/mswm/integrators.hpp:68-73):
+ * h[n_cells], u[n_edges] full host arrays; writes dh/du only on the masked
+ * groups, leaves every other entry untouched.  Without regions only
+ * MSWM_MASK_ALL is legal (UsageError, integrators.cpp:139-142).  Returns
+ * MSWM_E_DRY_VERTEX (see mswm_cuda_dry_vertex) like the reference throws
+ * DryVertexError (operators.cpp:82-84). */
+int mswm_cuda_eval(mswm_cuda_ctx* ctx, const double* h, const double* u,
+                   unsigned mask, double* dh, double* du);
+
+/* Device-resident prognostic state (State, integrators.hpp:18-24). */
+int mswm_cuda_state_upload(mswm_cuda_ctx* ctx, const double* h,
+                           const double* u, double time);
+int mswm_cuda_state_download(mswm_cuda_ctx* ctx, double* h, double* u,
+                             double* time);
+
+/* n_steps of Stepper::step (integrators.cpp:577-596) on the device state:
+ * scheme in mswm_scheme, dt the coarse step for LTS and the global step
+ * otherwise, M the substep count (LTS only).  LTS3 = lts_step(3)
+ * (:412-575), RK4 = rk4_step (:370-410), SSPRK3 = ssprk_step(3) (:337-368).
+ * Steps are replayed from a captured CUDA graph.  Asynchronous when
+ * `sync` is 0 (errors then surface at the next synchronous call). */
+int mswm_cuda_step(mswm_cuda_ctx* ctx, int scheme, double dt, int M,
+                   int64_t n_steps, int sync);
+
+/* WorkLedger counters (proj/include/mswm/ledger.hpp:25-60): cell_evals and
+ * edge_evals are [4 regions][4 stages] row-major; steps may be NULL. */
+int mswm_cuda_ledger(mswm_cuda_ctx* ctx, int64_t cell_evals[16],
+                     int64_t edge_evals[16], int64_t* steps);
+int mswm_cuda_ledger_reset(mswm_cuda_ctx* ctx);
+
+/* Original id of the vertex of the last DryVertexError, -1 if none; and the
+ * 1-based step of the batch in which it occurred (0 for mswm_cuda_eval). */
+int mswm_cuda_dry_vertex(const mswm_cuda_ctx* ctx, int64_t* step);
+
+/* Synchronise the context's stream; returns any pending error. */
+int mswm_cuda_sync(mswm_cuda_ctx* ctx);
+/* The cudaStream_t every kernel of ctx is launched on (for event timing). */
+void* mswm_cuda_stream(mswm_cuda_ctx* ctx);
+
+/* Per-evaluation device timing of the most recent step (profiling aid for
+ * the roofline).  Enable before mswm_cuda_step; the captured step then
+ * brackets every tendency evaluation with CUDA events.  After a step,
+ * mswm_cuda_eval_profile fills up to `cap` entries: eval_ms[k] the device
+ * time of evaluation k of the last replayed step, out_cells/out_edges its
+ * output set sizes; returns the count in *n. */
+int mswm_cuda_set_profiling(mswm_cuda_ctx* ctx, int enable);
+int mswm_cuda_eval_profile(mswm_cuda_ctx* ctx, float* eval_ms,
+                           int64_t* out_cells, int64_t* out_edges, int cap,
+                           int* n);
+
+/* Device diagnostics: total_mass (proj/src/harness.cpp:99-105) of the
+ * device state, summed in ascending original cell id order (bitwise equal
+ * to the reference). */
+int mswm_cuda_total_mass(mswm_cuda_ctx* ctx, double* mass);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MSWM_CUDA_H */
