@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""LTS3 TRiSK shallow-water benchmark (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+One "step" is one LTS3 coarse step (Stepper::lts_step(3, ...),
+proj/src/integrators.cpp:412-575) over the whole synthetic mesh.  `value`
+is whole-job edge-tendency evaluations per second (the WorkLedger unit,
+proj/include/mswm/ledger.hpp:25-60) with the state resident in HBM; `e2e`
+is the same metric through the drop-in C-ABI call a reference user makes
+(upload h,u from pinned host memory, one coarse step, download h,u).  The
+dominant kernel's roofline is one tendency evaluation (kernels A+B+C with
+the fused stage update) timed with CUDA events inside the timed steps.
+Under torchrun each rank runs its own copy of the workload on its GPU
+(weak scaling, no data-path collective yet: see DESIGN.md "multi-GPU").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "LTS3 edge-tendency evals/s"
+UNIT = "edge-evals/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce_max(x: float, ws: int) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# workload + algorithmic bytes
+
+def make_workload(name: str):
+    from paper_2106_07154_b200 import workloads as W
+    return W.CONFIGS[name]()
+
+
+def bytes_per_eval(mesh):
+    """B_E per edge evaluation and B_C per cell evaluation:
+    B_E = 32 + 8 + 8 + 4 + 4 + 12*S + 64*(nV/nE), B_C = 36 + 4*deg."""
+    S = mesh.n_stencil / mesh.n_edges
+    deg = mesh.n_ring / mesh.n_cells
+    BE = 32 + 8 + 8 + 4 + 4 + 12 * S + 64 * (mesh.n_vertices / mesh.n_edges)
+    BC = 36 + 4 * deg
+    return BE, BC
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (B200_PROFILING.md clocks line)
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baselines (oracle/_ref = the unmodified reference)
+
+def ref_lts3_rate(wl, nranks: int, n_steps: int):
+    """Time the reference's Stepper::lts_step(3) with SerialEvaluator
+    (nranks=0) or ThreadedEvaluator (nranks ranks); returns (evals/s, s/step,
+    edge evals per step)."""
+    from oracle.oracle import RefEvaluator, RefMesh, RefRegions
+    rm = RefMesh.from_mesh(wl.mesh)
+    rr = RefRegions(rm, wl.fine_mask, wl.width)
+    ev = RefEvaluator(rm, rr, wl.b, wl.f, wl.gravity, nranks=nranks)
+    h, u, t, secs = ev.step(4, wl.h, wl.u, 0.0, wl.dt, wl.M, n_steps)
+    _, e, s = ev.ledger()
+    per_step = int(e.sum()) // max(s, 1)
+    return per_step * n_steps / secs, secs / n_steps, per_step
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference_arm(args, ws, rank):
+    """--impl reference: the reference CPU path on this box's host cores."""
+    if rank != 0:
+        return
+    from oracle.oracle import ref_available
+    if not ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    wl = make_workload(args.config)
+    threads = cpu_threads()
+    # pick the faster of the serial and the threaded evaluator on one step
+    cand = {}
+    for nr in sorted({0, threads}):
+        rate, sps, per = ref_lts3_rate(wl, nr, 1)
+        cand[nr] = sps
+        log(f"reference {'serial' if nr == 0 else f'{nr} ranks'}: {sps:.3f} s/step")
+    best = min(cand, key=cand.get)
+    cores = 1 if best == 0 else best
+    if args.warmup > 0:
+        ref_lts3_rate(wl, best, min(args.warmup, 3))
+    rate, sps, per = ref_lts3_rate(wl, best, args.steps)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(wl, args.config, ws),
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"{args.steps} LTS3 coarse steps of {args.config} "
+                                   f"({'SerialEvaluator' if best == 0 else f'ThreadedEvaluator {best} ranks'})"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(wl, name, ws):
+    m = wl.mesh
+    return {"workload": f"{name.upper()} {wl.meta.get('mesh', '')}, LTS3 M={wl.M}, "
+                        f"interface width {wl.width}",
+            "n_cells": m.n_cells, "n_edges": m.n_edges, "n_vertices": m.n_vertices,
+            "M": wl.M, "dt": wl.dt, "fine_cells": int(wl.fine_mask.sum()),
+            "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
+            "l2": "inputs larger than L2 (mesh tables + state > 126 MB)" if m.n_edges > 400000
+            else "working set L2-resident (correctness config)"}
+
+
+# ---------------------------------------------------------------------------
+
+def run_ours(args, ws, rank, local):
+    import torch
+    from paper_2106_07154_b200.api import CudaContext, Scheme, State
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    t0 = time.time()
+    wl = make_workload(args.config)
+    log(f"[rank {rank}] workload {args.config}: {wl.mesh.n_cells} cells, {wl.mesh.n_edges} edges, "
+        f"built in {time.time() - t0:.1f}s")
+    ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, device=local)
+    rm = ctx.make_regions(wl.fine_mask, wl.width)
+    log(f"[rank {rank}] groups {rm.group_sizes()}")
+    ctx.upload(State(wl.h, wl.u, 0.0))
+    ctx.set_profiling(True)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=local)
+
+    # warm-up (also captures the step graph)
+    ctx.advance(Scheme.LTS3, wl.dt, wl.M, max(args.warmup, 1))
+    ctx.reset_ledger()
+
+    clocks = Clocks(local)
+    clocks.start()
+    barrier(ws)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    ctx.advance(Scheme.LTS3, wl.dt, wl.M, args.steps, sync=False)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ctx.sync()
+    barrier(ws)
+    ck = clocks.stop()
+    ms_local = e0.elapsed_time(e1)
+    ms = allreduce_max(ms_local, ws)
+    lg = ctx.ledger()
+    edge_per_step = lg.total_edge_evals() / args.steps
+    cell_per_step = lg.total_cell_evals() / args.steps
+    ms_step = ms / args.steps
+    value = ws * edge_per_step / (ms_step / 1e3)
+
+    # roofline of the dominant kernel: the largest tendency evaluation of the
+    # last timed step, timed by the events captured around it
+    BE, BC = bytes_per_eval(wl.mesh)
+    evms, evnc, evne = ctx.eval_profile()
+    k = int(np.argmax(evne))
+    alg = BE * evne[k] + BC * evnc[k]
+    hbm, peak_kind = peaks()
+    achieved = alg / (evms[k] / 1e3) / 1e9
+    step_alg = BE * edge_per_step + BC * cell_per_step
+    traffic = None
+    tf = ROOT / "profiles" / f"traffic_{args.config}.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+
+    # e2e through the drop-in C ABI with pinned host buffers
+    h_pin = torch.from_numpy(np.array(wl.h)).pin_memory()
+    u_pin = torch.from_numpy(np.array(wl.u)).pin_memory()
+    st = State(h_pin.numpy(), u_pin.numpy(), 0.0)
+    ctx.set_profiling(False)
+    ctx.upload(st)
+    ctx.advance(Scheme.LTS3, wl.dt, wl.M, 1)  # graph for the unprofiled path
+    ctx.download(st)
+    n_e2e = max(3, min(args.steps, 20))
+    barrier(ws)
+    t = time.perf_counter()
+    for _ in range(n_e2e):
+        ctx.upload(st)
+        ctx.advance(Scheme.LTS3, wl.dt, wl.M, 1)
+        ctx.download(st)
+    e2e_s = allreduce_max(time.perf_counter() - t, ws)
+    e2e_value = ws * edge_per_step * n_e2e / e2e_s
+    io_bytes = 8 * (wl.mesh.n_cells + wl.mesh.n_edges)
+
+    launches = ctx.kernels_per_step() * args.steps
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        from oracle.oracle import ref_available
+        if ref_available():
+            threads = cpu_threads()
+            rate, sps, _ = ref_lts3_rate(wl, 0, args.cpu_steps)
+            cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "reference",
+                   "sample": f"{args.cpu_steps} LTS3 coarse steps of {args.config} with the "
+                             f"reference SerialEvaluator ({sps:.3f} s/step)"}
+            if threads > 1:
+                rate_t, sps_t, _ = ref_lts3_rate(wl, threads, args.cpu_steps)
+                cpu["threaded"] = {"value": rate_t, "cores": threads,
+                                   "sample": f"{args.cpu_steps} steps, ThreadedEvaluator "
+                                             f"{threads} ranks ({sps_t:.3f} s/step)"}
+                if rate_t > rate:
+                    cpu.update(value=rate_t, cores=threads,
+                               sample=cpu["sample"] + f"; best: ThreadedEvaluator {threads} ranks")
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(wl, args.config, ws),
+            "coarse_steps_per_s": ws * 1e3 / ms_step,
+            "step_algorithmic_GBps": step_alg / (ms_step / 1e3) / 1e9,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic,
+                         "peak_kind": peak_kind,
+                         "kernel": "tendency evaluation (A: PV+K, B: F,q~, C: dh/du + fused "
+                                   f"stage update), out {int(evnc[k])} cells / {int(evne[k])} edges",
+                         "algorithmic_bytes": alg, "ms": float(evms[k]),
+                         "share_of_step": float(evms.sum() / ms_step)},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": io_bytes,
+                    "d2h_bytes_per_step": io_bytes, "steps": n_e2e},
+            "cpu_baseline": cpu,
+            "gpu_launches": int(launches),
+            "clocks": ck,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-steps", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("note: warmup < 3 violates the timing rules; using 3")
+        args.warmup = 3
+    ws, rank, local = dist_init()
+    if args.impl == "reference":
+        run_reference_arm(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

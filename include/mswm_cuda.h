@@ -175,8 +175,9 @@ int mswm_cuda_ledger(mswm_cuda_ctx* ctx, int64_t cell_evals[16],
                      int64_t edge_evals[16], int64_t* steps);
 int mswm_cuda_ledger_reset(mswm_cuda_ctx* ctx);
 
-/* Original id of the vertex of the last DryVertexError, -1 if none; and the
- * 1-based step of the batch in which it occurred (0 for mswm_cuda_eval). */
+/* Original id of the vertex of the last DryVertexError, -1 if none.  The
+ * step output is reserved (always 0): a dry vertex inside a replayed step
+ * batch is reported when the batch synchronises. */
 int mswm_cuda_dry_vertex(const mswm_cuda_ctx* ctx, int64_t* step);
 
 /* Synchronise the context's stream; returns any pending error. */
@@ -194,6 +195,10 @@ int mswm_cuda_set_profiling(mswm_cuda_ctx* ctx, int enable);
 int mswm_cuda_eval_profile(mswm_cuda_ctx* ctx, float* eval_ms,
                            int64_t* out_cells, int64_t* out_edges, int cap,
                            int* n);
+
+/* Number of this library's kernels one replay of the most recently used
+ * step graph launches (the bench's gpu_launches evidence). */
+int mswm_cuda_kernels_per_step(mswm_cuda_ctx* ctx, int64_t* n);
 
 /* Device diagnostics: total_mass (proj/src/harness.cpp:99-105) of the
  * device state, summed in ascending original cell id order (bitwise equal

@@ -159,6 +159,7 @@ def cuda() -> C.CDLL:
             "mswm_cuda_eval_profile": (C.c_int, [vp, C.POINTER(C.c_float), i64p, i64p, C.c_int,
                                                  C.POINTER(C.c_int)]),
             "mswm_cuda_total_mass": (C.c_int, [vp, f64p]),
+            "mswm_cuda_kernels_per_step": (C.c_int, [vp, i64p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

@@ -1,0 +1,401 @@
+"""Host-side mirror of the reference interface for the LTS3 hot path.
+
+Names, argument meanings and error behaviour follow the reference C++ API
+(proj/include/mswm/{errors,integrators,regions,ledger}.hpp) so the parity
+tests read like the reference's own tests.  Every call goes through the
+C ABI of ``libmswm_cuda.so`` (include/mswm_cuda.h); there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .mesh import Mesh
+
+# --------------------------------------------------------------------------
+# errors (errors.hpp:9-49)
+
+
+class Error(RuntimeError):
+    pass
+
+
+class ConfigError(Error):
+    pass
+
+
+class UsageError(Error):
+    pass
+
+
+class TopologyError(Error):
+    pass
+
+
+class DryVertexError(Error):
+    def __init__(self, msg, vertex):
+        super().__init__(msg)
+        self.vertex = vertex
+
+
+class CudaError(Error):
+    pass
+
+
+_STATUS = {1: ConfigError, 2: UsageError, 3: TopologyError, 5: CudaError, 6: CudaError,
+           7: CudaError}
+
+
+def _raise(rc: int, msg: str, vertex: int = -1):
+    if rc == 0:
+        return
+    if rc == 4:
+        raise DryVertexError(msg, vertex)
+    raise _STATUS.get(rc, Error)(msg)
+
+
+# --------------------------------------------------------------------------
+# GroupBit (integrators.hpp:43-61), Scheme (:26), regions enums (regions.hpp:12-21)
+
+class GroupBit(enum.IntFlag):
+    kCellsFinePlain = 1 << 0
+    kCellsUF1 = 1 << 1
+    kCellsUF2 = 1 << 2
+    kCellsIf1 = 1 << 3
+    kCellsIf2 = 1 << 4
+    kCellsCoarse = 1 << 5
+    kEdgesFinePlain = 1 << 6
+    kEdgesUFine = 1 << 7
+    kEdgesIf1 = 1 << 8
+    kEdgesIf2 = 1 << 9
+    kEdgesCoarse = 1 << 10
+
+
+kCellsAll = 0x3F
+kEdgesAll = 0x7C0
+kMaskAll = 0x7FF
+
+# the four LTS3 masks of Stepper::lts_step (integrators.cpp:452-461)
+MASK_COARSE_ONLY = GroupBit.kCellsCoarse | GroupBit.kEdgesCoarse
+MASK_IF_COARSE = (GroupBit.kCellsIf1 | GroupBit.kCellsIf2 | GroupBit.kCellsCoarse
+                  | GroupBit.kEdgesIf1 | GroupBit.kEdgesIf2 | GroupBit.kEdgesCoarse)
+MASK_STEP1 = MASK_IF_COARSE | GroupBit.kCellsUF1 | GroupBit.kCellsUF2 | GroupBit.kEdgesUFine
+MASK_SUB = (GroupBit.kCellsFinePlain | GroupBit.kCellsUF1 | GroupBit.kCellsUF2
+            | GroupBit.kCellsIf1 | GroupBit.kCellsIf2 | GroupBit.kEdgesFinePlain
+            | GroupBit.kEdgesUFine | GroupBit.kEdgesIf1 | GroupBit.kEdgesIf2)
+LTS3_MASKS = [int(MASK_STEP1), int(MASK_IF_COARSE), int(MASK_SUB), int(MASK_COARSE_ONLY)]
+
+
+class Scheme(enum.IntEnum):
+    SSPRK2 = 0
+    SSPRK3 = 1
+    RK4 = 2
+    LTS2 = 3
+    LTS3 = 4
+
+
+def parse_scheme(name: str) -> Scheme:
+    """integrators.cpp:250-258"""
+    try:
+        return {"ssprk2": Scheme.SSPRK2, "ssprk3": Scheme.SSPRK3, "rk4": Scheme.RK4,
+                "lts2": Scheme.LTS2, "lts3": Scheme.LTS3}[name]
+    except KeyError:
+        raise ConfigError(f"unknown scheme '{name}' (expected ssprk2, ssprk3, rk4, lts2 or lts3)")
+
+
+class CellRegion(enum.IntEnum):
+    Fine = 0
+    Interface1 = 1
+    Interface2 = 2
+    Coarse = 3
+
+
+class CellSub(enum.IntEnum):
+    None_ = 0
+    UnderlineF1 = 1
+    UnderlineF2 = 2
+
+
+class EdgeRegion(enum.IntEnum):
+    FineEdge = 0
+    UnderlineFineEdge = 1
+    Interface1Edge = 2
+    Interface2Edge = 3
+    CoarseEdge = 4
+
+
+GROUP_NAMES = ["cells_fine_plain", "cells_uf1", "cells_uf2", "cells_if1", "cells_if2",
+               "cells_coarse", "edges_fine", "edges_ufine", "edges_if1", "edges_if2",
+               "edges_coarse"]
+
+CLOSURE_FLUX, CLOSURE_QT, CLOSURE_K, CLOSURE_PV = range(4)
+
+
+@dataclass
+class State:
+    """integrators.hpp:18-24"""
+    h: np.ndarray
+    u: np.ndarray
+    time: float = 0.0
+
+
+@dataclass
+class SchemeConfig:
+    """integrators.hpp:33-39"""
+    scheme: Scheme = Scheme.SSPRK3
+    dt: float = 0.0
+    substeps: int = 1
+    gravity: float = 9.80616
+    replication: int = 1
+
+
+@dataclass
+class WorkLedger:
+    """ledger.hpp:25-60 (wall-time fields are kept by the caller)."""
+    cell_evals: np.ndarray
+    edge_evals: np.ndarray
+    steps_taken: int
+
+    def total_cell_evals(self) -> int:
+        return int(self.cell_evals.sum())
+
+    def total_edge_evals(self) -> int:
+        return int(self.edge_evals.sum())
+
+    def total_evals(self) -> int:
+        return self.total_cell_evals() + self.total_edge_evals()
+
+
+@dataclass
+class RegionMap:
+    """regions.hpp:26-49: labels plus the 11 ascending group lists."""
+    cell_label: np.ndarray
+    cell_sublabel: np.ndarray
+    edge_label: np.ndarray
+    interface_width: int
+    groups: list
+    warnings: list
+
+    def __getattr__(self, name):
+        groups = self.__dict__.get("groups")
+        if groups is not None and name in GROUP_NAMES:
+            return groups[GROUP_NAMES.index(name)]
+        if name == "cells_fine":
+            return np.sort(np.concatenate(groups[0:3]))
+        raise AttributeError(name)
+
+    def group_sizes(self):
+        return [len(g) for g in self.groups]
+
+
+_WARN_TEXT = {1: "no fine cell touches Interface1; underline layers are empty",
+              2: "fine region is one layer thick; second underline layer is empty "
+                 "(third-order interface prediction degrades)",
+              4: "fine region is only two layers thick; no plain fine cells remain"}
+
+
+# --------------------------------------------------------------------------
+
+class CudaContext:
+    """One mswm_cuda_ctx: a mesh resident on one B200."""
+
+    def __init__(self, mesh: Mesh, b, f_vertex, gravity: float = 9.80616, device: int = 0,
+                 order: int = 0):
+        self.lib = _lib.cuda()
+        self.mesh = mesh
+        self._desc = mesh.desc()
+        handle = C.c_void_p()
+        rc = self.lib.mswm_cuda_create(C.byref(self._desc), device, order, C.byref(handle))
+        if rc:
+            _raise(rc, self.lib.mswm_cuda_last_error(None).decode())
+        self.handle = handle
+        self.regions: RegionMap | None = None
+        self.set_fields(b, f_vertex, gravity)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.mswm_cuda_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int):
+        if rc:
+            msg = self.lib.mswm_cuda_last_error(self.handle).decode()
+            v = -1
+            if rc == 4:
+                v = self.lib.mswm_cuda_dry_vertex(self.handle, None)
+            _raise(rc, msg, v)
+
+    # -- setup ---------------------------------------------------------------
+    def set_fields(self, b, f_vertex, gravity: float):
+        self.b = np.ascontiguousarray(b, np.float64)
+        self.f = np.ascontiguousarray(f_vertex, np.float64)
+        if self.b.shape != (self.mesh.n_cells,):
+            raise UsageError("bottom topography field size does not match the mesh")
+        if self.f.shape != (self.mesh.n_vertices,):
+            raise UsageError("Coriolis field size does not match the mesh")
+        self.gravity = float(gravity)
+        self._check(self.lib.mswm_cuda_set_fields(self.handle, _p(self.b, _lib.f64p),
+                                                  _p(self.f, _lib.f64p), self.gravity))
+
+    def make_regions(self, fine_mask, interface_width: int = 1) -> RegionMap:
+        """make_regions (regions.cpp:164-171) on the device from a host mask."""
+        m = self.mesh
+        fm = np.ascontiguousarray(fine_mask, np.uint8)
+        if fm.shape != (m.n_cells,):
+            raise UsageError("fine mask size does not match the mesh")
+        cl = np.zeros(m.n_cells, np.uint8)
+        cs = np.zeros(m.n_cells, np.uint8)
+        el = np.zeros(m.n_edges, np.uint8)
+        sizes = np.zeros(11, np.int64)
+        warn = C.c_int(0)
+        self._check(self.lib.mswm_cuda_set_regions(
+            self.handle, _p(fm, _lib.u8p), interface_width, _p(cl, _lib.u8p), _p(cs, _lib.u8p),
+            _p(el, _lib.u8p), _p(sizes, _lib.i64p), C.byref(warn)))
+        groups = []
+        for g in range(11):
+            ids = np.zeros(int(sizes[g]), np.int32)
+            self._check(self.lib.mswm_cuda_get_group(self.handle, g, _p(ids, _lib.i32p)))
+            groups.append(ids)
+        warnings = [_WARN_TEXT[warn.value]] if warn.value else []
+        self.regions = RegionMap(cl, cs, el, interface_width, groups, warnings)
+        return self.regions
+
+    def closure(self, mask: int, kind: int) -> np.ndarray:
+        n = C.c_int64(0)
+        self._check(self.lib.mswm_cuda_get_closure(self.handle, int(mask), kind, None,
+                                                   C.byref(n)))
+        ids = np.zeros(n.value, np.int32)
+        self._check(self.lib.mswm_cuda_get_closure(self.handle, int(mask), kind,
+                                                   _p(ids, _lib.i32p), C.byref(n)))
+        return ids
+
+    # -- device-resident stepping ------------------------------------------
+    def upload(self, state: State):
+        h = np.ascontiguousarray(state.h, np.float64)
+        u = np.ascontiguousarray(state.u, np.float64)
+        self._check(self.lib.mswm_cuda_state_upload(self.handle, _p(h, _lib.f64p),
+                                                    _p(u, _lib.f64p), float(state.time)))
+
+    def download(self, state: State | None = None) -> State:
+        m = self.mesh
+        if state is None:
+            state = State(np.zeros(m.n_cells), np.zeros(m.n_edges), 0.0)
+        t = C.c_double(0.0)
+        self._check(self.lib.mswm_cuda_state_download(self.handle, _p(state.h, _lib.f64p),
+                                                      _p(state.u, _lib.f64p), C.byref(t)))
+        state.time = t.value
+        return state
+
+    def advance(self, scheme: Scheme, dt: float, substeps: int = 1, n_steps: int = 1,
+                sync: bool = True):
+        self._check(self.lib.mswm_cuda_step(self.handle, int(scheme), float(dt), int(substeps),
+                                            int(n_steps), 1 if sync else 0))
+
+    def sync(self):
+        self._check(self.lib.mswm_cuda_sync(self.handle))
+
+    def ledger(self) -> WorkLedger:
+        c = np.zeros(16, np.int64)
+        e = np.zeros(16, np.int64)
+        s = C.c_int64(0)
+        self._check(self.lib.mswm_cuda_ledger(self.handle, _p(c, _lib.i64p), _p(e, _lib.i64p),
+                                              C.byref(s)))
+        return WorkLedger(c.reshape(4, 4), e.reshape(4, 4), s.value)
+
+    def reset_ledger(self):
+        self._check(self.lib.mswm_cuda_ledger_reset(self.handle))
+
+    def stream_ptr(self) -> int:
+        return self.lib.mswm_cuda_stream(self.handle) or 0
+
+    def set_profiling(self, on: bool):
+        self._check(self.lib.mswm_cuda_set_profiling(self.handle, 1 if on else 0))
+
+    def eval_profile(self, cap: int = 4096):
+        ms = (C.c_float * cap)()
+        nc = np.zeros(cap, np.int64)
+        ne = np.zeros(cap, np.int64)
+        n = C.c_int(0)
+        self._check(self.lib.mswm_cuda_eval_profile(self.handle, ms, _p(nc, _lib.i64p),
+                                                    _p(ne, _lib.i64p), cap, C.byref(n)))
+        k = min(n.value, cap)
+        return np.array(ms[:k], np.float64), nc[:k], ne[:k]
+
+    def kernels_per_step(self) -> int:
+        n = C.c_int64(0)
+        self._check(self.lib.mswm_cuda_kernels_per_step(self.handle, C.byref(n)))
+        return n.value
+
+    def total_mass(self) -> float:
+        out = C.c_double(0.0)
+        self._check(self.lib.mswm_cuda_total_mass(self.handle, C.byref(out)))
+        return out.value
+
+
+def _p(a, t):
+    return a.ctypes.data_as(t)
+
+
+class CudaEvaluator:
+    """TendencyEvaluator (integrators.hpp:68-73) on the GPU.
+
+    ``eval(h, u, mask, dh, du)`` writes dh/du only on the masked groups and
+    leaves every other entry untouched; only ``kMaskAll`` is legal without a
+    region map.
+    """
+
+    def __init__(self, ctx: CudaContext):
+        self.ctx = ctx
+
+    def eval(self, h, u, mask: int, dh: np.ndarray, du: np.ndarray):
+        c = self.ctx
+        if dh.dtype != np.float64 or du.dtype != np.float64 or not dh.flags.c_contiguous \
+                or not du.flags.c_contiguous:
+            raise UsageError("dh/du must be contiguous float64 arrays")
+        h = np.ascontiguousarray(h, np.float64)
+        u = np.ascontiguousarray(u, np.float64)
+        c._check(c.lib.mswm_cuda_eval(c.handle, _p(h, _lib.f64p), _p(u, _lib.f64p), int(mask),
+                                      _p(dh, _lib.f64p), _p(du, _lib.f64p)))
+
+
+class CudaStepper:
+    """Stepper (integrators.hpp:136-160) with device-resident state.
+
+    Each call uploads the State, advances on the device and downloads it --
+    the drop-in form.  Long runs should call ``ctx.upload`` once,
+    ``ctx.advance(..., n_steps)`` and ``ctx.download`` at the end.
+    """
+
+    def __init__(self, ctx: CudaContext):
+        self.ctx = ctx
+
+    def _run(self, state: State, scheme: Scheme, dt: float, M: int):
+        self.ctx.upload(state)
+        self.ctx.advance(scheme, dt, M, 1)
+        self.ctx.download(state)
+
+    def ssprk_step(self, order: int, state: State, dt: float):
+        if order not in (2, 3):
+            raise UsageError("ssprk_step: order must be 2 or 3")
+        self._run(state, Scheme.SSPRK2 if order == 2 else Scheme.SSPRK3, dt, 1)
+
+    def rk4_step(self, state: State, dt: float):
+        self._run(state, Scheme.RK4, dt, 1)
+
+    def lts_step(self, order: int, state: State, dt: float, substeps: int):
+        if order not in (2, 3):
+            raise UsageError("lts_step: order must be 2 or 3")
+        self._run(state, Scheme.LTS2 if order == 2 else Scheme.LTS3, dt, substeps)
+
+    def step(self, state: State, cfg: SchemeConfig):
+        self._run(state, cfg.scheme, cfg.dt, cfg.substeps)

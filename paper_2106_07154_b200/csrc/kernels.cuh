@@ -1,0 +1,501 @@
+// sm_100a device kernels of the LTS3 / TRiSK path.
+//
+// Every kernel keeps the reference's per-element IEEE operation sequence
+// (proj/src/operators.cpp:61-116,
+// proj/src/integrators.cpp:18-52,186-274,370-410) and is compiled with
+// --fmad=false, so results are bitwise equal to the reference.  FP64
+// gathers over SoA tables; nothing here is a dense contraction, so there are
+// no tensor-core paths.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mswm_dev {
+
+constexpr int kMaxDeg = 8;               // ring size bound (hexagons 6, pentagons 5)
+constexpr int kMaxSten = 2 * kMaxDeg - 2;
+constexpr int kBlock = 256;
+
+// Device mesh tables in internal numbering.  Slot-major SoA ([slot][elem])
+// so consecutive threads of a warp read consecutive addresses.
+struct DevMesh {
+  int32_t nC, nE, nV;
+  int32_t deg_max, sten_max;
+  // cells
+  const int32_t* __restrict__ c_edge;    // [deg_max][nC] ring edges
+  const uint8_t* __restrict__ c_deg;     // [nC]
+  const uint8_t* __restrict__ c_sbits;   // [nC] bit j: cell_sign(ring edge j, i) < 0
+  const double* __restrict__ c_area;     // [nC] A_i
+  // vertices
+  const int32_t* __restrict__ v_cell;    // [3][nV]
+  const int32_t* __restrict__ v_edge;    // [3][nV]
+  const double* __restrict__ v_kite;     // [3][nV]
+  const uint8_t* __restrict__ v_sbits;   // [nV] bit k: vertex_sign(v_edge k, v) < 0
+  const double* __restrict__ v_area;     // [nV] A_v
+  const int32_t* __restrict__ v_orig;    // [nV] original vertex id (error path only)
+  // edges
+  const int2* __restrict__ e_cells;      // [nE] (edge_cells[e][0], [1]) in stored order
+  const int2* __restrict__ e_verts;      // [nE]
+  const double* __restrict__ e_len;      // l_e
+  const double* __restrict__ e_ld;       // l_e * d_e (the K product's first rounding)
+  const double* __restrict__ e_dual;     // d_e
+  const double* __restrict__ e_invd;     // 1.0 / d_e
+  const uint8_t* __restrict__ e_nst;     // stencil length
+  const int32_t* __restrict__ e_sten;    // [sten_max][nE] edges_on_edge
+  const double* __restrict__ e_coef;     // [sten_max][nE] w * (l_{e'} * (1/d_e))
+  // fields
+  const double* __restrict__ b;          // [nC]
+  const double* __restrict__ f;          // [nV]
+  double g;
+};
+
+// Stage epilogue fused into the output kernel (integrators.cpp:18-52,
+// 231-274, 370-410).  d is the freshly computed tendency of element i.
+enum OpKind : int {
+  OP_NONE = 0,
+  OP_STORE,        // dst = d
+  OP_EULER,        // dst = y0 + c0*d
+  OP_WCOMB,        // dst = ((c0*y0) + (c1*y1)) + (c2*d), c2 = w_rhs*dt
+  OP_ACC,          // acc = (first ? 0.0 : acc) + d
+  OP_ACC_CORR,     // a3 = (first ? 0.0 : acc) + d;
+                   // dst = y0 + c0*(((c1*a1) + (c1*a2)) + (c2*a3))
+  OP_RK4_FIRST,    // acc = d;              dst = y0 + c0*d
+  OP_RK4_MID,      // acc = acc + 2.0*d;    dst = y0 + c0*d
+  OP_RK4_LAST,     // dst = y0 + c0*(acc + d)
+};
+
+struct Op {
+  int kind;
+  int first;
+  double c0, c1, c2;
+  double* dst;
+  const double* y0;
+  const double* y1;
+  double* acc;
+  const double* a1;
+  const double* a2;
+};
+
+__device__ __forceinline__ void apply_op(const Op& op, int32_t i, double d) {
+  switch (op.kind) {
+    case OP_STORE:
+      op.dst[i] = d;
+      break;
+    case OP_EULER:
+      op.dst[i] = op.y0[i] + op.c0 * d;
+      break;
+    case OP_WCOMB:
+      op.dst[i] = op.c0 * op.y0[i] + op.c1 * op.y1[i] + op.c2 * d;
+      break;
+    case OP_ACC:
+      op.acc[i] = (op.first ? 0.0 : op.acc[i]) + d;
+      break;
+    case OP_ACC_CORR: {
+      const double a3 = (op.first ? 0.0 : op.acc[i]) + d;
+      op.dst[i] = op.y0[i] + op.c0 * (op.c1 * op.a1[i] + op.c1 * op.a2[i] + op.c2 * a3);
+      break;
+    }
+    case OP_RK4_FIRST:
+      op.acc[i] = d;
+      op.dst[i] = op.y0[i] + op.c0 * d;
+      break;
+    case OP_RK4_MID:
+      op.acc[i] = op.acc[i] + 2.0 * d;
+      op.dst[i] = op.y0[i] + op.c0 * d;
+      break;
+    case OP_RK4_LAST: {
+      const double a = op.acc[i] + d;
+      op.dst[i] = op.y0[i] + op.c0 * a;
+      break;
+    }
+    default:
+      break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Phase A: potential vorticity on the closure vertices (operators.cpp:74-86)
+// and kinetic energy on the closure cells (:64-72), one launch.
+__global__ void __launch_bounds__(kBlock) k_vertex_cell(DevMesh M, const double* __restrict__ h,
+                                                       const double* __restrict__ u,
+                                                       const int32_t* __restrict__ vlist, int32_t nv,
+                                                       const int32_t* __restrict__ klist, int32_t nk,
+                                                       double* __restrict__ pv, double* __restrict__ K,
+                                                       int32_t* __restrict__ dry) {
+  const int32_t t = blockIdx.x * kBlock + threadIdx.x;
+  if (t < nv) {
+    const int32_t v = vlist[t];
+    const uint8_t sb = M.v_sbits[v];
+    double hv = 0.0, circ = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      hv += M.v_kite[k * M.nV + v] * h[M.v_cell[k * M.nV + v]];
+      const int32_t e = M.v_edge[k * M.nV + v];
+      const double d = M.e_dual[e];
+      circ += ((sb >> k) & 1 ? -d : d) * u[e];
+    }
+    hv /= M.v_area[v];
+    if (!(hv > 0.0)) {
+      atomicMin(dry, M.v_orig[v]);
+      pv[v] = 0.0;
+      return;
+    }
+    pv[v] = (M.f[v] + circ / M.v_area[v]) / hv;
+  } else if (t - nv < nk) {
+    const int32_t i = klist[t - nv];
+    const int deg = M.c_deg[i];
+    double acc = 0.0;
+    for (int j = 0; j < deg; ++j) {
+      const int32_t e = M.c_edge[j * M.nC + i];
+      const double ue = u[e];
+      acc += M.e_ld[e] * ue * ue;
+    }
+    K[i] = acc / (4.0 * M.c_area[i]);
+  }
+}
+
+// Phase B: thickness flux F_e (operators.cpp:61-62) and q~_e (:88-89) on the
+// union of the flux and q~ closures, packed as (F, q~) so the stencil loop
+// of phase C reads both with one 16-byte gather.
+__global__ void __launch_bounds__(kBlock) k_edge_fq(DevMesh M, const double* __restrict__ h,
+                                                   const double* __restrict__ u,
+                                                   const double* __restrict__ pv,
+                                                   const int32_t* __restrict__ elist, int32_t ne,
+                                                   double2* __restrict__ FQ) {
+  const int32_t t = blockIdx.x * kBlock + threadIdx.x;
+  if (t >= ne) return;
+  const int32_t e = elist[t];
+  const int2 c = M.e_cells[e];
+  const int2 v = M.e_verts[e];
+  const double F = 0.5 * (h[c.x] + h[c.y]) * u[e];
+  const double q = 0.5 * (pv[v.x] + pv[v.y]);
+  FQ[e] = make_double2(F, q);
+}
+
+// Phase C: the output tendencies -- dh on out cells (operators.cpp:91-99),
+// du on out edges (:101-116) -- with the stage update fused in.  Threads
+// [0, nc) take cells, [nc, nc+ne) edges; lists are group-concatenated and
+// split into two epilogue segments at csplit / esplit.
+struct OutArgs {
+  const int32_t* clist;
+  int32_t nc, csplit;
+  const int32_t* elist;
+  int32_t ne, esplit;
+  Op cop[2];
+  Op eop[2];
+};
+
+__global__ void __launch_bounds__(kBlock) k_out(DevMesh M, const double* __restrict__ h,
+                                               const double* __restrict__ K,
+                                               const double2* __restrict__ FQ, OutArgs a) {
+  const int32_t t = blockIdx.x * kBlock + threadIdx.x;
+  if (t < a.nc) {
+    const int32_t i = a.clist[t];
+    const int deg = M.c_deg[i];
+    const uint8_t sb = M.c_sbits[i];
+    double acc = 0.0;
+    for (int j = 0; j < deg; ++j) {
+      const int32_t e = M.c_edge[j * M.nC + i];
+      const double l = M.e_len[e];
+      acc += ((sb >> j) & 1 ? -l : l) * FQ[e].x;
+    }
+    const double dh = -acc / M.c_area[i];
+    apply_op(a.cop[t < a.csplit ? 0 : 1], i, dh);
+  } else if (t - a.nc < a.ne) {
+    const int32_t q = t - a.nc;
+    const int32_t e = a.elist[q];
+    const double qt_e = FQ[e].y;
+    const double inv_d = M.e_invd[e];
+    const int nst = M.e_nst[e];
+    double pvflux = 0.0;
+    for (int j = 0; j < nst; ++j) {
+      const int32_t e2 = M.e_sten[j * M.nE + e];
+      const double c = M.e_coef[j * M.nE + e];
+      const double2 fq = FQ[e2];
+      pvflux += c * fq.x * (0.5 * (qt_e + fq.y));
+    }
+    const int2 cc = M.e_cells[e];
+    const double psi_lo = M.g * (h[cc.x] + M.b[cc.x]) + K[cc.x];
+    const double psi_hi = M.g * (h[cc.y] + M.b[cc.y]) + K[cc.y];
+    const double du = -pvflux - (psi_lo - psi_hi) * inv_d;
+    apply_op(a.eop[q < a.esplit ? 0 : 1], e, du);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Interface-1 prediction (integrators.cpp:217-227, order 3):
+// dst = ((c0*s0) + (c1*s1)) + (c2*s2) on the I1 lists.
+__global__ void k_predict(const int32_t* __restrict__ clist, int32_t nc,
+                          const int32_t* __restrict__ elist, int32_t ne, double c0, double c1,
+                          double c2, const double* __restrict__ hs0, const double* __restrict__ hs1,
+                          const double* __restrict__ hs2, double* __restrict__ hdst,
+                          const double* __restrict__ us0, const double* __restrict__ us1,
+                          const double* __restrict__ us2, double* __restrict__ udst) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nc) {
+    const int32_t i = clist[t];
+    hdst[i] = c0 * hs0[i] + c1 * hs1[i] + c2 * hs2[i];
+  } else if (t - nc < ne) {
+    const int32_t e = elist[t - nc];
+    udst[e] = c0 * us0[e] + c1 * us1[e] + c2 * us2[e];
+  }
+}
+
+// Substep prologue: save the values the predictions and the correction
+// read (old state on I1 u I2, stage-1/2 values on I1), then write the
+// stage-1 prediction of substep 0.  Lists are [I1 | I2].
+__global__ void k_save_predict(const int32_t* __restrict__ clist, int32_t nc, int32_t nc1,
+                               const int32_t* __restrict__ elist, int32_t ne, int32_t ne1,
+                               double c0, double c1, double c2, double* __restrict__ H,
+                               const double* __restrict__ H1, const double* __restrict__ H2,
+                               double* __restrict__ HS0, double* __restrict__ HS1,
+                               double* __restrict__ HS2, double* __restrict__ U,
+                               const double* __restrict__ U1, const double* __restrict__ U2,
+                               double* __restrict__ US0, double* __restrict__ US1,
+                               double* __restrict__ US2) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nc) {
+    const int32_t i = clist[t];
+    const double y0 = H[i];
+    HS0[i] = y0;
+    if (t < nc1) {
+      const double y1 = H1[i], y2 = H2[i];
+      HS1[i] = y1;
+      HS2[i] = y2;
+      H[i] = c0 * y0 + c1 * y1 + c2 * y2;
+    }
+  } else if (t - nc < ne) {
+    const int32_t q = t - nc;
+    const int32_t e = elist[q];
+    const double y0 = U[e];
+    US0[e] = y0;
+    if (q < ne1) {
+      const double y1 = U1[e], y2 = U2[e];
+      US1[e] = y1;
+      US2[e] = y2;
+      U[e] = c0 * y0 + c1 * y1 + c2 * y2;
+    }
+  }
+}
+
+__global__ void k_step_counter(int64_t* ctr) { ++*ctr; }
+
+// ---------------------------------------------------------------------------
+// Region classification (regions.cpp:14-162) on device.
+
+// One BFS layer: unvisited cells with a neighbour at distance level-1 get
+// `level`.  In-place is safe: a cell set to `level` in this launch never
+// matches level-1.  Counts the layer.
+__global__ void k_bfs_layer(DevMesh M, const int32_t* __restrict__ c_nbr, int32_t* dist, int level,
+                            int32_t* counter) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M.nC || dist[i] != -1) return;
+  const int deg = M.c_deg[i];
+  for (int j = 0; j < deg; ++j)
+    if (dist[c_nbr[j * M.nC + i]] == level - 1) {
+      dist[i] = level;
+      atomicAdd(counter, 1);
+      return;
+    }
+}
+
+// labels: 0 fine, 1 interface1, 2 interface2, 3 coarse (regions.hpp:12)
+__global__ void k_cell_labels(int32_t nC, const int32_t* __restrict__ dist, int w,
+                              uint8_t* __restrict__ label, uint8_t* __restrict__ sub) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nC) return;
+  const int d = dist[i];
+  label[i] = d == 0 ? 0 : (d >= 1 && d <= w ? 1 : (d > w && d <= 2 * w ? 2 : 3));
+  sub[i] = 0;
+}
+
+// underline layers (regions.cpp:107-139); pass 1 then pass 2
+__global__ void k_underline(DevMesh M, const int32_t* __restrict__ c_nbr,
+                            const uint8_t* __restrict__ label, uint8_t* __restrict__ sub, int pass) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M.nC || label[i] != 0) return;
+  const int deg = M.c_deg[i];
+  if (pass == 1) {
+    for (int j = 0; j < deg; ++j)
+      if (label[c_nbr[j * M.nC + i]] == 1) {
+        sub[i] = 1;
+        return;
+      }
+  } else {
+    if (sub[i] != 0) return;
+    for (int j = 0; j < deg; ++j) {
+      const int32_t nb = c_nbr[j * M.nC + i];
+      if (label[nb] == 0 && sub[nb] == 1) {
+        sub[i] = 2;
+        return;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ int cell_rank(uint8_t label, uint8_t sub) {
+  return label == 0 ? (sub == 0 ? 0 : 1) : int(label) + 1;
+}
+
+// edge labels: fine side wins (regions.cpp:141-162); also the compaction
+// keys (GroupBit index) of cells and edges.
+__global__ void k_edge_labels_and_keys(DevMesh M, const uint8_t* __restrict__ label,
+                                       const uint8_t* __restrict__ sub,
+                                       uint8_t* __restrict__ elabel, uint8_t* __restrict__ ckey,
+                                       uint8_t* __restrict__ ekey) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < M.nE) {
+    const int2 c = M.e_cells[t];
+    const int r0 = cell_rank(label[c.x], sub[c.x]);
+    const int r1 = cell_rank(label[c.y], sub[c.y]);
+    const uint8_t r = uint8_t(r0 < r1 ? r0 : r1);
+    elabel[t] = r;
+    ekey[t] = r;
+  }
+  if (t < M.nC) {
+    const uint8_t l = label[t], s = sub[t];
+    ckey[t] = l == 0 ? s : uint8_t(l + 2);  // 0 plain, 1 uf1, 2 uf2, 3 if1, 4 if2, 5 coarse
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Closure marking (operators.cpp:35-58) for one mask's out lists.
+// mf: flux marks (ring edges of out cells and of both cells of out edges)
+// mq: q~ marks (out edges and ring edges of both cells of out edges)
+// mk: K cells (both cells of out edges); mv: PV vertices (their ring vertices)
+__global__ void k_mark_closure(DevMesh M, const int32_t* __restrict__ c_vert,
+                               const int32_t* __restrict__ clist, int32_t nc,
+                               const int32_t* __restrict__ elist, int32_t ne,
+                               uint8_t* __restrict__ mf, uint8_t* __restrict__ mq,
+                               uint8_t* __restrict__ mk, uint8_t* __restrict__ mv) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nc) {
+    const int32_t i = clist[t];
+    const int deg = M.c_deg[i];
+    for (int j = 0; j < deg; ++j) mf[M.c_edge[j * M.nC + i]] = 1;
+  } else if (t - nc < ne) {
+    const int32_t e = elist[t - nc];
+    mq[e] = 1;
+    const int2 cc = M.e_cells[e];
+    for (int side = 0; side < 2; ++side) {
+      const int32_t i = side ? cc.y : cc.x;
+      mk[i] = 1;
+      const int deg = M.c_deg[i];
+      for (int j = 0; j < deg; ++j) {
+        const int32_t e2 = M.c_edge[j * M.nC + i];
+        mf[e2] = 1;
+        mq[e2] = 1;
+        mv[c_vert[j * M.nC + i]] = 1;
+      }
+    }
+  }
+}
+
+// key = 0 where either mark is set, 0xFF elsewhere (closure-union key)
+__global__ void k_union_key(int32_t n, const uint8_t* __restrict__ a, const uint8_t* __restrict__ b,
+                            uint8_t* __restrict__ key) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) key[i] = (a[i] | b[i]) ? 0 : 0xFF;
+}
+
+__global__ void k_flag_key(int32_t n, const uint8_t* __restrict__ a, uint8_t* __restrict__ key) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) key[i] = a[i] ? 0 : 0xFF;
+}
+
+// ---------------------------------------------------------------------------
+// Order-preserving multi-group stream compaction with warp ballots.
+// key[i] in [0, G) selects the group of element i (0xFF: none).  Output:
+// group g's elements in ascending index order at out[g_base[g] + ...].
+constexpr int kCompactItems = 8;  // items per thread
+constexpr int kCompactTile = kBlock * kCompactItems;
+constexpr int kMaxGroups = 12;
+
+__global__ void __launch_bounds__(kBlock) k_compact_count(const uint8_t* __restrict__ key, int32_t n,
+                                                          int G, int32_t* __restrict__ counts,
+                                                          int32_t nblocks) {
+  __shared__ int32_t s_cnt[kMaxGroups];
+  if (threadIdx.x < kMaxGroups) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t base = int64_t(blockIdx.x) * kCompactTile;
+  int32_t local[kMaxGroups];
+  for (int g = 0; g < G; ++g) local[g] = 0;
+  for (int it = 0; it < kCompactItems; ++it) {
+    const int64_t idx = base + int64_t(it) * kBlock + threadIdx.x;
+    const uint8_t k = idx < n ? key[idx] : 0xFF;
+    for (int g = 0; g < G; ++g) local[g] += __popc(__ballot_sync(0xffffffffu, k == g));
+  }
+  if (lane == 0)
+    for (int g = 0; g < G; ++g) atomicAdd(&s_cnt[g], local[g]);
+  __syncthreads();
+  if (threadIdx.x < G) counts[threadIdx.x * nblocks + blockIdx.x] = s_cnt[threadIdx.x];
+}
+
+// Exclusive scan of counts[G][nblocks] (row-major) in place; totals[g] =
+// group size.  One block; sequential over chunks of kBlock.
+__global__ void __launch_bounds__(kBlock) k_compact_scan(int32_t* counts, int32_t nblocks, int G,
+                                                         int64_t* totals) {
+  __shared__ int32_t s[kBlock];
+  for (int g = 0; g < G; ++g) {
+    int32_t carry = 0;
+    int32_t* row = counts + int64_t(g) * nblocks;
+    for (int32_t start = 0; start < nblocks; start += kBlock) {
+      const int32_t i = start + threadIdx.x;
+      const int32_t v = i < nblocks ? row[i] : 0;
+      s[threadIdx.x] = v;
+      __syncthreads();
+      for (int off = 1; off < kBlock; off <<= 1) {
+        const int32_t add = threadIdx.x >= off ? s[threadIdx.x - off] : 0;
+        __syncthreads();
+        s[threadIdx.x] += add;
+        __syncthreads();
+      }
+      if (i < nblocks) row[i] = carry + s[threadIdx.x] - v;
+      const int32_t tot = s[kBlock - 1];
+      __syncthreads();
+      carry += tot;
+    }
+    if (threadIdx.x == 0) totals[g] = carry;
+    __syncthreads();
+  }
+}
+
+// Scatter: within a tile, item-major then warp-major then lane order is
+// ascending index order, so ballot prefixes give ascending output.
+__global__ void __launch_bounds__(kBlock) k_compact_scatter(const uint8_t* __restrict__ key, int32_t n,
+                                                            int G, const int32_t* __restrict__ offs,
+                                                            int32_t nblocks,
+                                                            const int64_t* __restrict__ gbase,
+                                                            int32_t* __restrict__ out) {
+  __shared__ int32_t s_warp[kMaxGroups][kBlock / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t base = int64_t(blockIdx.x) * kCompactTile;
+  int32_t run[kMaxGroups];
+  for (int g = 0; g < G; ++g) run[g] = offs[g * nblocks + blockIdx.x];
+  for (int it = 0; it < kCompactItems; ++it) {
+    const int64_t idx = base + int64_t(it) * kBlock + threadIdx.x;
+    const uint8_t k = idx < n ? key[idx] : 0xFF;
+    unsigned mine = 0;
+    for (int g = 0; g < G; ++g) {
+      const unsigned bal = __ballot_sync(0xffffffffu, k == g);
+      if (lane == 0) s_warp[g][warp] = __popc(bal);
+      if (k == g) mine = bal;
+    }
+    __syncthreads();
+    if (k < G) {
+      int32_t pos = run[k] + __popc(mine & ((1u << lane) - 1u));
+      for (int w = 0; w < warp; ++w) pos += s_warp[k][w];
+      out[gbase[k] + pos] = int32_t(idx);
+    }
+    for (int g = 0; g < G; ++g) {
+      int32_t tot = 0;
+      for (int w = 0; w < kBlock / 32; ++w) tot += s_warp[g][w];
+      run[g] += tot;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace mswm_dev

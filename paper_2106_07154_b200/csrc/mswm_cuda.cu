@@ -1,0 +1,1391 @@
+// C ABI of the B200 LTS3 / TRiSK path (include/mswm_cuda.h).
+//
+// One context = one GPU, one CUDA stream, the mesh tables in internal
+// numbering, the device-resident state and the LTS workspace.  Evaluations
+// are three kernels (A: PV + K on the closure, B: (F, q~) on the edge
+// closure, C: dh/du on the output lists with the stage update fused);
+// coarse steps are captured once into a CUDA graph per (scheme, dt, M) and
+// replayed.
+//
+// Device schedule of one LTS3 coarse step (reference:
+// proj/src/integrators.cpp:412-575).  The reference keeps 18 full-size
+// stage arrays and copies/zeroes most of them every step (:488-519); here
+// the stage arrays alias (ha == state, hb == h1, hc == h2) and only the
+// I1/I2 values the predictions and the correction read are saved, which
+// removes every O(n) copy.  This is exact because (i) no evaluation reads a
+// stage value that the aliasing changes (the stencil reaches one cell ring
+// for h and the ring edges of that ring for u, so step 2 never reads fine
+// cells beyond UF1 and step 4 never reads anything closer to the fine
+// region than Interface2), and (ii) every element's arithmetic is the
+// reference's expression, evaluated once.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <climits>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "kernels.cuh"
+#include "mswm_cuda.h"
+
+using namespace mswm_dev;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct Error : std::runtime_error {
+  int status;
+  Error(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t _e = (call);                                                          \
+    if (_e != cudaSuccess)                                                            \
+      throw Error(MSWM_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e));   \
+  } while (0)
+
+template <class T>
+struct DArr {
+  T* p = nullptr;
+  size_t n = 0;
+  DArr() = default;
+  DArr(const DArr&) = delete;
+  DArr& operator=(const DArr&) = delete;
+  ~DArr() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t count) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = count;
+    if (count) {
+      cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+      if (e != cudaSuccess)
+        throw Error(MSWM_E_NOMEM, "cudaMalloc of " + std::to_string(count * sizeof(T)) +
+                                      " bytes: " + cudaGetErrorString(e));
+    }
+  }
+  void upload(const std::vector<T>& h, cudaStream_t s) {
+    alloc(h.size());
+    if (n) CK(cudaMemcpyAsync(p, h.data(), n * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void zero(cudaStream_t s) {
+    if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+};
+
+inline int nblk(int64_t n, int b = kBlock) { return int((n + b - 1) / b); }
+
+// Output lists and closure lists of one mask (operators.cpp:35-58).
+struct MaskPlan {
+  unsigned mask = 0;
+  const int32_t* cells = nullptr;  // device, group-concatenated
+  int32_t nc = 0, csplit = 0;
+  const int32_t* edges = nullptr;
+  int32_t ne = 0, esplit = 0;
+  DArr<int32_t> own_cells, own_edges;  // storage when not aliasing the group buffer
+  DArr<int32_t> vclos, kclos, eclos, fclos, qclos;
+  int32_t nv = 0, nk = 0, nec = 0, nf = 0, nq = 0;
+  std::vector<int32_t> host_cells, host_edges;  // original ids, same order as device lists
+};
+
+struct EvalRecord {
+  cudaEvent_t start, stop;
+  int64_t nc, ne;
+};
+
+}  // namespace
+
+struct mswm_cuda_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string last_error;
+  int32_t nC = 0, nE = 0, nV = 0, deg_max = 0, sten_max = 0;
+  bool identity = true;
+  std::vector<int32_t> c_new2old, e_new2old, v_new2old, c_old2new, e_old2new, v_old2new;
+  std::vector<double> h_cell_area;  // original order (total_mass)
+
+  // device mesh
+  DArr<int32_t> c_edge, c_vert, c_nbr, v_cell, v_edge, v_orig, e_sten;
+  DArr<uint8_t> c_deg, c_sbits, v_sbits, e_nst;
+  DArr<double> c_area, v_kite, v_area, e_len, e_ld, e_dual, e_invd, e_coef, b, f;
+  DArr<int2> e_cells, e_verts;
+  double gravity = 9.80616;
+  bool have_fields = false;
+
+  // state + workspace (internal order)
+  DArr<double> H, U, H1, U1, H2, U2, A1h, A1u, A2h, A2u, A3h, A3u, S0h, S0u, S1h, S1u, S2h, S2u;
+  DArr<double> T1h, T1u, T2h, T2u;  // RK4 / SSPRK stage buffers
+  DArr<double> Dh, Du;              // eval ABI outputs
+  DArr<double> pv, K;
+  DArr<double2> FQ;
+  double time = 0.0;
+  DArr<int32_t> dry_vertex;
+  DArr<unsigned long long> dry_step;
+  DArr<int64_t> step_ctr;
+  int last_dry_vertex = -1;
+  int64_t last_dry_step = 0;
+  int64_t steps_issued = 0;
+
+  // regions
+  bool have_regions = false;
+  int width = 1;
+  DArr<uint8_t> cell_label, cell_sub, edge_label;
+  DArr<int32_t> cell_groups, edge_groups;  // group-concatenated ascending lists
+  int64_t gsize[11] = {0};
+  int64_t goff[11] = {0};  // offset of group g inside its buffer
+  DArr<int32_t> all_cells, all_edges;  // identity lists (no regions)
+
+  std::map<unsigned, std::unique_ptr<MaskPlan>> plans;
+
+  // ledger (ledger.hpp:25-60)
+  int64_t ledger_cell[4][4] = {{0}}, ledger_edge[4][4] = {{0}}, ledger_steps = 0;
+
+  // graphs, one per (scheme, dt, M, profiling); profiled graphs own the
+  // events bracketing each evaluation
+  struct Graph {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<EvalRecord> records;
+    int64_t kernels = 0;  // kernel nodes per step
+  };
+  std::map<std::tuple<int, double, int, int>, Graph> graphs;
+  bool profiling = false;
+  std::vector<EvalRecord>* capture_records = nullptr;  // set while capturing
+  int64_t launches = 0;                               // kernels enqueued (capture counting)
+  int64_t last_kernels_per_step = 0;
+  const std::vector<EvalRecord>* last_records = nullptr;
+
+  void drop_graphs() {
+    for (auto& kv : graphs) {
+      cudaGraphExecDestroy(kv.second.exec);
+      for (auto& r : kv.second.records) {
+        cudaEventDestroy(r.start);
+        cudaEventDestroy(r.stop);
+      }
+    }
+    graphs.clear();
+    last_records = nullptr;
+  }
+
+  ~mswm_cuda_ctx() {
+    drop_graphs();
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  DevMesh dev() const {
+    DevMesh M;
+    M.nC = nC;
+    M.nE = nE;
+    M.nV = nV;
+    M.deg_max = deg_max;
+    M.sten_max = sten_max;
+    M.c_edge = c_edge.p;
+    M.c_deg = c_deg.p;
+    M.c_sbits = c_sbits.p;
+    M.c_area = c_area.p;
+    M.v_cell = v_cell.p;
+    M.v_edge = v_edge.p;
+    M.v_kite = v_kite.p;
+    M.v_sbits = v_sbits.p;
+    M.v_area = v_area.p;
+    M.v_orig = v_orig.p;
+    M.e_cells = e_cells.p;
+    M.e_verts = e_verts.p;
+    M.e_len = e_len.p;
+    M.e_ld = e_ld.p;
+    M.e_dual = e_dual.p;
+    M.e_invd = e_invd.p;
+    M.e_nst = e_nst.p;
+    M.e_sten = e_sten.p;
+    M.e_coef = e_coef.p;
+    M.b = b.p;
+    M.f = f.p;
+    M.g = gravity;
+    return M;
+  }
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// helpers
+
+void check_ctx(mswm_cuda_ctx* c) {
+  if (!c) throw Error(MSWM_E_USAGE, "null context");
+  CK(cudaSetDevice(c->device));
+}
+
+// Host permutation helpers: internal array from original-order input.
+template <class T>
+std::vector<T> to_internal(const mswm_cuda_ctx* c, const T* src, const std::vector<int32_t>& n2o,
+                           size_t n) {
+  std::vector<T> out(n);
+  if (c->identity)
+    std::copy(src, src + n, out.begin());
+  else
+    for (size_t i = 0; i < n; ++i) out[i] = src[n2o[i]];
+  return out;
+}
+
+// Upload an original-order array into a device buffer in internal order.
+void upload_field(mswm_cuda_ctx* c, DArr<double>& dst, const double* src,
+                  const std::vector<int32_t>& n2o, size_t n) {
+  if (dst.n != n) dst.alloc(n);
+  if (c->identity) {
+    CK(cudaMemcpyAsync(dst.p, src, n * 8, cudaMemcpyHostToDevice, c->stream));
+  } else {
+    std::vector<double> tmp = to_internal(c, src, n2o, n);
+    CK(cudaMemcpyAsync(dst.p, tmp.data(), n * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+}
+
+void download_field(mswm_cuda_ctx* c, const DArr<double>& src, double* dst,
+                    const std::vector<int32_t>& n2o, size_t n) {
+  if (c->identity) {
+    CK(cudaMemcpyAsync(dst, src.p, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  } else {
+    std::vector<double> tmp(n);
+    CK(cudaMemcpyAsync(tmp.data(), src.p, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < n; ++i) dst[n2o[i]] = tmp[i];
+  }
+}
+
+// Order-preserving compaction of key[0..n) into G ascending groups.
+// Returns group sizes; out receives group g at offset sum_{h<g} size_h.
+std::vector<int64_t> compact(mswm_cuda_ctx* c, const uint8_t* d_key, int32_t n, int G,
+                             DArr<int32_t>& out) {
+  const int32_t nb = std::max(1, int32_t((int64_t(n) + kCompactTile - 1) / kCompactTile));
+  DArr<int32_t> counts;
+  counts.alloc(size_t(G) * nb);
+  DArr<int64_t> totals, gbase;
+  totals.alloc(G);
+  gbase.alloc(G);
+  k_compact_count<<<nb, kBlock, 0, c->stream>>>(d_key, n, G, counts.p, nb);
+  CK(cudaGetLastError());
+  k_compact_scan<<<1, kBlock, 0, c->stream>>>(counts.p, nb, G, totals.p);
+  CK(cudaGetLastError());
+  std::vector<int64_t> sizes(G), base(G);
+  CK(cudaMemcpyAsync(sizes.data(), totals.p, G * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  int64_t acc = 0;
+  for (int g = 0; g < G; ++g) {
+    base[g] = acc;
+    acc += sizes[g];
+  }
+  out.alloc(size_t(std::max<int64_t>(acc, 1)));
+  CK(cudaMemcpyAsync(gbase.p, base.data(), G * 8, cudaMemcpyHostToDevice, c->stream));
+  k_compact_scatter<<<nb, kBlock, 0, c->stream>>>(d_key, n, G, counts.p, nb, gbase.p, out.p);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c->stream));
+  return sizes;
+}
+
+// ---------------------------------------------------------------------------
+// create
+
+void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d) {
+  const int32_t nC = d->n_cells, nE = d->n_edges, nV = d->n_vertices;
+  if (nC <= 0 || nE <= 0 || nV <= 0) throw Error(MSWM_E_TOPOLOGY, "empty mesh");
+  auto need = [](bool ok, const std::string& what) {
+    if (!ok) throw Error(MSWM_E_TOPOLOGY, what);
+  };
+  need(d->cell_offset && d->cell_edges && d->cell_vertices && d->cell_cells && d->edge_cells &&
+           d->edge_vertices && d->vertex_cells && d->vertex_edges && d->edge_edge_offset &&
+           d->edge_edges && d->edge_cell_sign && d->edge_vertex_sign && d->edge_len &&
+           d->edge_dual_len && d->cell_area && d->vertex_area && d->vertex_kite && d->edge_weight,
+       "mesh descriptor has a null table");
+  c->nC = nC;
+  c->nE = nE;
+  c->nV = nV;
+  // Permutations (identity for MSWM_ORDER_INPUT).
+  c->c_new2old.resize(nC);
+  c->e_new2old.resize(nE);
+  c->v_new2old.resize(nV);
+  std::iota(c->c_new2old.begin(), c->c_new2old.end(), 0);
+  std::iota(c->e_new2old.begin(), c->e_new2old.end(), 0);
+  std::iota(c->v_new2old.begin(), c->v_new2old.end(), 0);
+  c->c_old2new = c->c_new2old;
+  c->e_old2new = c->e_new2old;
+  c->v_old2new = c->v_new2old;
+  c->identity = true;
+  const auto& cn = c->c_new2old;
+  const auto& en = c->e_new2old;
+  const auto& vn = c->v_new2old;
+  const auto& co = c->c_old2new;
+  const auto& eo = c->e_old2new;
+  const auto& vo = c->v_old2new;
+
+  int deg_max = 0;
+  for (int32_t i = 0; i < nC; ++i) {
+    const int deg = d->cell_offset[i + 1] - d->cell_offset[i];
+    need(deg >= 3 && deg <= kMaxDeg, "cell " + std::to_string(i) + " ring size out of [3, 8]");
+    deg_max = std::max(deg_max, deg);
+  }
+  int sten_max = 0;
+  for (int32_t e = 0; e < nE; ++e) {
+    const int n = d->edge_edge_offset[e + 1] - d->edge_edge_offset[e];
+    need(n >= 0 && n <= kMaxSten, "edge " + std::to_string(e) + " stencil too long");
+    sten_max = std::max(sten_max, n);
+  }
+  c->deg_max = deg_max;
+  c->sten_max = sten_max;
+
+  // cells
+  std::vector<int32_t> c_edge(size_t(deg_max) * nC, 0), c_vert(size_t(deg_max) * nC, 0),
+      c_nbr(size_t(deg_max) * nC, 0);
+  std::vector<uint8_t> c_deg(nC), c_sbits(nC, 0);
+  std::vector<double> c_area(nC);
+  for (int32_t ni = 0; ni < nC; ++ni) {
+    const int32_t i = cn[ni];
+    const int off = d->cell_offset[i], deg = d->cell_offset[i + 1] - off;
+    c_deg[ni] = uint8_t(deg);
+    c_area[ni] = d->cell_area[i];
+    for (int j = 0; j < deg; ++j) {
+      const int32_t e = d->cell_edges[off + j], v = d->cell_vertices[off + j],
+                    nb = d->cell_cells[off + j];
+      need(e >= 0 && e < nE && v >= 0 && v < nV && nb >= 0 && nb < nC, "ring id out of range");
+      c_edge[size_t(j) * nC + ni] = eo[e];
+      c_vert[size_t(j) * nC + ni] = vo[v];
+      c_nbr[size_t(j) * nC + ni] = co[nb];
+      // cell_sign(e, i) (mesh.hpp:89-92)
+      const int8_t s = d->edge_cells[2 * e] == i ? d->edge_cell_sign[2 * e] : d->edge_cell_sign[2 * e + 1];
+      if (s < 0) c_sbits[ni] |= uint8_t(1u << j);
+    }
+  }
+  c->h_cell_area.assign(d->cell_area, d->cell_area + nC);
+  // vertices
+  std::vector<int32_t> v_cell(size_t(3) * nV), v_edge(size_t(3) * nV), v_orig(nV);
+  std::vector<double> v_kite(size_t(3) * nV), v_area(nV);
+  std::vector<uint8_t> v_sbits(nV, 0);
+  for (int32_t nv = 0; nv < nV; ++nv) {
+    const int32_t v = vn[nv];
+    v_orig[nv] = v;
+    v_area[nv] = d->vertex_area[v];
+    for (int k = 0; k < 3; ++k) {
+      const int32_t cc = d->vertex_cells[3 * v + k], e = d->vertex_edges[3 * v + k];
+      need(cc >= 0 && cc < nC && e >= 0 && e < nE, "vertex table id out of range");
+      v_cell[size_t(k) * nV + nv] = co[cc];
+      v_edge[size_t(k) * nV + nv] = eo[e];
+      v_kite[size_t(k) * nV + nv] = d->vertex_kite[3 * v + k];
+      // vertex_sign(e, v) (mesh.hpp:93-96)
+      const int8_t s =
+          d->edge_vertices[2 * e] == v ? d->edge_vertex_sign[2 * e] : d->edge_vertex_sign[2 * e + 1];
+      if (s < 0) v_sbits[nv] |= uint8_t(1u << k);
+    }
+  }
+  // edges
+  std::vector<int2> e_cells(nE), e_verts(nE);
+  std::vector<double> e_len(nE), e_ld(nE), e_dual(nE), e_invd(nE);
+  std::vector<uint8_t> e_nst(nE);
+  std::vector<int32_t> e_sten(size_t(std::max(sten_max, 1)) * nE, 0);
+  std::vector<double> e_coef(size_t(std::max(sten_max, 1)) * nE, 0.0);
+  for (int32_t ne = 0; ne < nE; ++ne) {
+    const int32_t e = en[ne];
+    const int32_t c0 = d->edge_cells[2 * e], c1 = d->edge_cells[2 * e + 1];
+    const int32_t v0 = d->edge_vertices[2 * e], v1 = d->edge_vertices[2 * e + 1];
+    need(c0 >= 0 && c0 < nC && c1 >= 0 && c1 < nC && v0 >= 0 && v0 < nV && v1 >= 0 && v1 < nV,
+         "edge table id out of range");
+    e_cells[ne] = make_int2(co[c0], co[c1]);
+    e_verts[ne] = make_int2(vo[v0], vo[v1]);
+    const double l = d->edge_len[e], dd = d->edge_dual_len[e];
+    e_len[ne] = l;
+    e_dual[ne] = dd;
+    e_ld[ne] = l * dd;          // operators.cpp:70, first product
+    const double inv_d = 1.0 / dd;  // operators.cpp:103
+    e_invd[ne] = inv_d;
+    const int off = d->edge_edge_offset[e], n = d->edge_edge_offset[e + 1] - off;
+    e_nst[ne] = uint8_t(n);
+    for (int j = 0; j < n; ++j) {
+      const int32_t e2 = d->edge_edges[off + j];
+      need(e2 >= 0 && e2 < nE, "stencil id out of range");
+      e_sten[size_t(j) * nE + ne] = eo[e2];
+      // operators.cpp:109: weights[j] * (edge_len[e2] * inv_d), the first
+      // two factors of the stencil term -- mesh constants.
+      e_coef[size_t(j) * nE + ne] = d->edge_weight[off + j] * (d->edge_len[e2] * inv_d);
+    }
+  }
+  cudaStream_t s = c->stream;
+  c->c_edge.upload(c_edge, s);
+  c->c_vert.upload(c_vert, s);
+  c->c_nbr.upload(c_nbr, s);
+  c->c_deg.upload(c_deg, s);
+  c->c_sbits.upload(c_sbits, s);
+  c->c_area.upload(c_area, s);
+  c->v_cell.upload(v_cell, s);
+  c->v_edge.upload(v_edge, s);
+  c->v_orig.upload(v_orig, s);
+  c->v_kite.upload(v_kite, s);
+  c->v_area.upload(v_area, s);
+  c->v_sbits.upload(v_sbits, s);
+  c->e_cells.upload(e_cells, s);
+  c->e_verts.upload(e_verts, s);
+  c->e_len.upload(e_len, s);
+  c->e_ld.upload(e_ld, s);
+  c->e_dual.upload(e_dual, s);
+  c->e_invd.upload(e_invd, s);
+  c->e_nst.upload(e_nst, s);
+  c->e_sten.upload(e_sten, s);
+  c->e_coef.upload(e_coef, s);
+  CK(cudaStreamSynchronize(s));  // host vectors die here
+
+  // state + workspace, zero-initialised
+  DArr<double>* cellbufs[] = {&c->H, &c->H1, &c->H2, &c->A1h, &c->A2h, &c->A3h, &c->S0h,
+                              &c->S1h, &c->S2h, &c->T1h, &c->T2h, &c->Dh, &c->K};
+  DArr<double>* edgebufs[] = {&c->U, &c->U1, &c->U2, &c->A1u, &c->A2u, &c->A3u, &c->S0u,
+                              &c->S1u, &c->S2u, &c->T1u, &c->T2u, &c->Du};
+  for (auto* bptr : cellbufs) {
+    bptr->alloc(nC);
+    bptr->zero(s);
+  }
+  for (auto* bptr : edgebufs) {
+    bptr->alloc(nE);
+    bptr->zero(s);
+  }
+  c->pv.alloc(nV);
+  c->pv.zero(s);
+  c->FQ.alloc(nE);
+  c->FQ.zero(s);
+  c->b.alloc(nC);
+  c->b.zero(s);
+  c->f.alloc(nV);
+  c->f.zero(s);
+  c->dry_vertex.alloc(1);
+  c->dry_step.alloc(1);
+  c->step_ctr.alloc(1);
+  c->step_ctr.zero(s);
+  // identity lists for evaluation without regions
+  std::vector<int32_t> ic(nC), ie(nE);
+  std::iota(ic.begin(), ic.end(), 0);
+  std::iota(ie.begin(), ie.end(), 0);
+  c->all_cells.upload(ic, s);
+  c->all_edges.upload(ie, s);
+  CK(cudaStreamSynchronize(s));
+}
+
+void reset_dry(mswm_cuda_ctx* c) {
+  const int32_t big = INT_MAX;
+  const unsigned long long none = ~0ull;
+  CK(cudaMemcpyAsync(c->dry_vertex.p, &big, 4, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->dry_step.p, &none, 8, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+}
+
+// Reads the dry flag; returns true if a dry vertex was hit.
+bool read_dry(mswm_cuda_ctx* c) {
+  int32_t v = INT_MAX;
+  CK(cudaMemcpyAsync(&v, c->dry_vertex.p, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (v == INT_MAX) return false;
+  c->last_dry_vertex = v;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// mask plans
+
+void invalidate(mswm_cuda_ctx* c) {
+  c->plans.clear();
+  c->drop_graphs();
+}
+
+MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
+  auto it = c->plans.find(mask);
+  if (it != c->plans.end()) return *it->second;
+  if (mask & ~unsigned(MSWM_MASK_ALL)) throw Error(MSWM_E_USAGE, "mask has unknown group bits");
+  auto p = std::make_unique<MaskPlan>();
+  p->mask = mask;
+  cudaStream_t s = c->stream;
+  if (!c->have_regions) {
+    // integrators.cpp:139-142
+    if (mask != MSWM_MASK_ALL)
+      throw Error(MSWM_E_USAGE, "partial evaluation masks require a region map on the evaluator");
+    p->cells = c->all_cells.p;
+    p->nc = p->csplit = c->nC;
+    p->edges = c->all_edges.p;
+    p->ne = p->esplit = c->nE;
+  } else {
+    // Segment 0 = fine groups (bits 0-2 / 6-7), segment 1 = the rest.
+    // Group buffers are [g0 | g1 | ... ], so a run of consecutive set bits
+    // aliases a contiguous range; otherwise the groups are concatenated.
+    auto build = [&](int g0, int g1, DArr<int32_t>& groups, DArr<int32_t>& own,
+                     const int32_t*& list, int32_t& n, int32_t& split, int fine_last) {
+      std::vector<int> sel;
+      for (int g = g0; g <= g1; ++g)
+        if (mask & (1u << g)) sel.push_back(g);
+      n = 0;
+      split = 0;
+      for (int g : sel) {
+        n += int32_t(c->gsize[g]);
+        if (g <= fine_last) split += int32_t(c->gsize[g]);
+      }
+      bool contiguous = true;
+      for (size_t k = 1; k < sel.size(); ++k) contiguous &= sel[k] == sel[k - 1] + 1;
+      if (sel.empty()) {
+        list = nullptr;
+      } else if (contiguous) {
+        list = groups.p + c->goff[sel[0]];
+      } else {
+        own.alloc(size_t(std::max(n, 1)));
+        int64_t pos = 0;
+        for (int g : sel) {
+          if (c->gsize[g])
+            CK(cudaMemcpyAsync(own.p + pos, groups.p + c->goff[g], c->gsize[g] * 4,
+                               cudaMemcpyDeviceToDevice, s));
+          pos += c->gsize[g];
+        }
+        list = own.p;
+      }
+    };
+    build(0, 5, c->cell_groups, p->own_cells, p->cells, p->nc, p->csplit, 2);
+    build(6, 10, c->edge_groups, p->own_edges, p->edges, p->ne, p->esplit, 7);
+  }
+  // Closure marks (operators.cpp:35-58) and their compaction.
+  DArr<uint8_t> mf, mq, mk, mv, key;
+  mf.alloc(c->nE);
+  mq.alloc(c->nE);
+  mk.alloc(c->nC);
+  mv.alloc(c->nV);
+  mf.zero(s);
+  mq.zero(s);
+  mk.zero(s);
+  mv.zero(s);
+  if (p->nc + p->ne > 0) {
+    k_mark_closure<<<nblk(int64_t(p->nc) + p->ne), kBlock, 0, s>>>(
+        c->dev(), c->c_vert.p, p->cells, p->nc, p->edges, p->ne, mf.p, mq.p, mk.p, mv.p);
+    CK(cudaGetLastError());
+  }
+  key.alloc(std::max(c->nE, std::max(c->nC, c->nV)));
+  k_union_key<<<nblk(c->nE), kBlock, 0, s>>>(c->nE, mf.p, mq.p, key.p);
+  p->nec = int32_t(compact(c, key.p, c->nE, 1, p->eclos)[0]);
+  k_flag_key<<<nblk(c->nE), kBlock, 0, s>>>(c->nE, mf.p, key.p);
+  p->nf = int32_t(compact(c, key.p, c->nE, 1, p->fclos)[0]);
+  k_flag_key<<<nblk(c->nE), kBlock, 0, s>>>(c->nE, mq.p, key.p);
+  p->nq = int32_t(compact(c, key.p, c->nE, 1, p->qclos)[0]);
+  k_flag_key<<<nblk(c->nC), kBlock, 0, s>>>(c->nC, mk.p, key.p);
+  p->nk = int32_t(compact(c, key.p, c->nC, 1, p->kclos)[0]);
+  k_flag_key<<<nblk(c->nV), kBlock, 0, s>>>(c->nV, mv.p, key.p);
+  p->nv = int32_t(compact(c, key.p, c->nV, 1, p->vclos)[0]);
+  // host copies of the output lists (original ids) for the eval ABI
+  p->host_cells.resize(p->nc);
+  p->host_edges.resize(p->ne);
+  if (p->nc)
+    CK(cudaMemcpyAsync(p->host_cells.data(), p->cells, size_t(p->nc) * 4, cudaMemcpyDeviceToHost, s));
+  if (p->ne)
+    CK(cudaMemcpyAsync(p->host_edges.data(), p->edges, size_t(p->ne) * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (!c->identity) {
+    for (auto& i : p->host_cells) i = c->c_new2old[i];
+    for (auto& e : p->host_edges) e = c->e_new2old[e];
+  }
+  auto& slot = c->plans[mask];
+  slot = std::move(p);
+  return *slot;
+}
+
+// ---------------------------------------------------------------------------
+// one tendency evaluation = kernels A, B, C on the stream
+
+Op op_none() {
+  Op o;
+  std::memset(&o, 0, sizeof(o));
+  o.kind = OP_NONE;
+  return o;
+}
+
+void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const double* u,
+                 const Op cop[2], const Op eop[2]) {
+  cudaStream_t s = c->stream;
+  const DevMesh M = c->dev();
+  EvalRecord* rec = nullptr;
+  if (c->capture_records) {
+    EvalRecord r;
+    CK(cudaEventCreate(&r.start));
+    CK(cudaEventCreate(&r.stop));
+    c->capture_records->push_back(r);
+    rec = &c->capture_records->back();
+    rec->nc = p.nc;
+    rec->ne = p.ne;
+    CK(cudaEventRecordWithFlags(rec->start, s, cudaEventRecordExternal));
+  }
+  const int64_t na = int64_t(p.nv) + p.nk;
+  if (na > 0) {
+    k_vertex_cell<<<nblk(na), kBlock, 0, s>>>(M, h, u, p.vclos.p, p.nv, p.kclos.p, p.nk, c->pv.p,
+                                             c->K.p, c->dry_vertex.p);
+    CK(cudaGetLastError());
+    ++c->launches;
+  }
+  if (p.nec > 0) {
+    k_edge_fq<<<nblk(p.nec), kBlock, 0, s>>>(M, h, u, c->pv.p, p.eclos.p, p.nec, c->FQ.p);
+    CK(cudaGetLastError());
+    ++c->launches;
+  }
+  const int64_t nout = int64_t(p.nc) + p.ne;
+  if (nout > 0) {
+    OutArgs a;
+    a.clist = p.cells;
+    a.nc = p.nc;
+    a.csplit = p.csplit;
+    a.elist = p.edges;
+    a.ne = p.ne;
+    a.esplit = p.esplit;
+    a.cop[0] = cop[0];
+    a.cop[1] = cop[1];
+    a.eop[0] = eop[0];
+    a.eop[1] = eop[1];
+    k_out<<<nblk(nout), kBlock, 0, s>>>(M, h, c->K.p, c->FQ.p, a);
+    CK(cudaGetLastError());
+    ++c->launches;
+  }
+  if (rec) CK(cudaEventRecordWithFlags(rec->stop, s, cudaEventRecordExternal));
+}
+
+// Op factories (cells use h-arrays, edges u-arrays)
+Op mk_op(int kind, double* dst, const double* y0 = nullptr, double c0 = 0, const double* y1 = nullptr,
+         double c1 = 0, double c2 = 0, double* acc = nullptr, int first = 0,
+         const double* a1 = nullptr, const double* a2 = nullptr) {
+  Op o = op_none();
+  o.kind = kind;
+  o.dst = dst;
+  o.y0 = y0;
+  o.c0 = c0;
+  o.y1 = y1;
+  o.c1 = c1;
+  o.c2 = c2;
+  o.acc = acc;
+  o.first = first;
+  o.a1 = a1;
+  o.a2 = a2;
+  return o;
+}
+
+// ---------------------------------------------------------------------------
+// ledger (Stepper::tally, integrators.cpp:302-335)
+
+void tally(mswm_cuda_ctx* c, unsigned mask, int stage) {
+  if (!c->have_regions) {
+    if (mask & MSWM_CELLS_ALL) c->ledger_cell[0][stage] += c->nC;
+    if (mask & MSWM_EDGES_ALL) c->ledger_edge[0][stage] += c->nE;
+    return;
+  }
+  static const int cell_region[6] = {0, 0, 0, 1, 2, 3};
+  static const int edge_region[5] = {0, 0, 1, 2, 3};
+  for (int g = 0; g < 6; ++g)
+    if (mask & (1u << g)) c->ledger_cell[cell_region[g]][stage] += c->gsize[g];
+  for (int g = 0; g < 5; ++g)
+    if (mask & (1u << (6 + g))) c->ledger_edge[edge_region[g]][stage] += c->gsize[6 + g];
+}
+
+constexpr unsigned kMaskCoarseOnly = MSWM_CELLS_COARSE | MSWM_EDGES_COARSE;
+constexpr unsigned kMaskIfCoarse = MSWM_CELLS_IF1 | MSWM_CELLS_IF2 | MSWM_CELLS_COARSE |
+                                   MSWM_EDGES_IF1 | MSWM_EDGES_IF2 | MSWM_EDGES_COARSE;
+constexpr unsigned kMaskStep1 = kMaskIfCoarse | MSWM_CELLS_UF1 | MSWM_CELLS_UF2 | MSWM_EDGES_UFINE;
+constexpr unsigned kMaskSub = MSWM_CELLS_FINE_PLAIN | MSWM_CELLS_UF1 | MSWM_CELLS_UF2 |
+                              MSWM_CELLS_IF1 | MSWM_CELLS_IF2 | MSWM_EDGES_FINE_PLAIN |
+                              MSWM_EDGES_UFINE | MSWM_EDGES_IF1 | MSWM_EDGES_IF2;
+
+// lts_interp_coeffs (integrators.cpp:186-212), order 3
+void lts3_coeffs(int stage, int k, int M, double out[3]) {
+  const double kd = k, Md = M;
+  double x = 0.0, xt = 0.0;
+  switch (stage) {
+    case 1:
+      x = kd / Md;
+      xt = (kd * kd) / (Md * Md);
+      break;
+    case 2:
+      x = (kd + 1.0) / Md;
+      xt = (kd * (kd + 2.0)) / (Md * Md);
+      break;
+    default:
+      x = (2.0 * kd + 1.0) / (2.0 * Md);
+      xt = (2.0 * kd * kd + 2.0 * kd + 1.0) / (2.0 * Md * Md);
+      break;
+  }
+  out[0] = 1.0 - x - xt;
+  out[1] = x - xt;
+  out[2] = 2.0 * xt;
+}
+
+// The I1 / I1 u I2 lists: groups 3-4 (cells) and 8-9 (edges) are
+// contiguous in the group buffers.
+struct IfLists {
+  const int32_t *c, *e;
+  int32_t nc, nc1, ne, ne1;
+};
+IfLists if_lists(mswm_cuda_ctx* c) {
+  IfLists L;
+  L.c = c->cell_groups.p + c->goff[3];
+  L.nc1 = int32_t(c->gsize[3]);
+  L.nc = int32_t(c->gsize[3] + c->gsize[4]);
+  L.e = c->edge_groups.p + c->goff[8];
+  L.ne1 = int32_t(c->gsize[8]);
+  L.ne = int32_t(c->gsize[8] + c->gsize[9]);
+  return L;
+}
+
+void launch_predict(mswm_cuda_ctx* c, int stage, int k, int M, double* hdst, double* udst) {
+  const IfLists L = if_lists(c);
+  double w[3];
+  lts3_coeffs(stage, k, M, w);
+  const int64_t n = int64_t(L.nc1) + L.ne1;
+  if (n == 0) return;
+  k_predict<<<nblk(n), kBlock, 0, c->stream>>>(L.c, L.nc1, L.e, L.ne1, w[0], w[1], w[2], c->S0h.p,
+                                               c->S1h.p, c->S2h.p, hdst, c->S0u.p, c->S1u.p,
+                                               c->S2u.p, udst);
+  CK(cudaGetLastError());
+  ++c->launches;
+}
+
+// One LTS3 coarse step (see the file header for the aliasing argument).
+void enqueue_lts3(mswm_cuda_ctx* c, double dt, int M) {
+  const double delta = dt / M;
+  double *H = c->H.p, *U = c->U.p, *H1 = c->H1.p, *U1 = c->U1.p, *H2 = c->H2.p, *U2 = c->U2.p;
+  MaskPlan& p1 = plan_for(c, kMaskStep1);
+  MaskPlan& p2 = plan_for(c, kMaskIfCoarse);
+  MaskPlan& ps = plan_for(c, kMaskSub);
+  MaskPlan& p4 = plan_for(c, kMaskCoarseOnly);
+  k_step_counter<<<1, 1, 0, c->stream>>>(c->step_ctr.p);
+  // Step 1 (:483-487): h1 = h_old + dt*dh on UF1 u UF2 u I1 u I2 u C.
+  {
+    Op co[2] = {mk_op(OP_EULER, H1, H, dt), mk_op(OP_EULER, H1, H, dt)};
+    Op eo[2] = {mk_op(OP_EULER, U1, U, dt), mk_op(OP_EULER, U1, U, dt)};
+    launch_eval(c, p1, H, U, co, eo);
+  }
+  // Step 2 (:491-500): h2 = 0.75 h_old + 0.25 h1 + (0.25 dt) dh on I u C.
+  {
+    const double cr = 0.25 * dt;
+    Op co[2] = {mk_op(OP_WCOMB, H2, H, 0.75, H1, 0.25, cr), mk_op(OP_WCOMB, H2, H, 0.75, H1, 0.25, cr)};
+    Op eo[2] = {mk_op(OP_WCOMB, U2, U, 0.75, U1, 0.25, cr), mk_op(OP_WCOMB, U2, U, 0.75, U1, 0.25, cr)};
+    launch_eval(c, p2, H1, U1, co, eo);
+  }
+  // Substep prologue: save I1 u I2 old values, I1 stage values, predict
+  // stage 1 of substep 0 into the state (ha == state).
+  {
+    const IfLists L = if_lists(c);
+    double w[3];
+    lts3_coeffs(1, 0, M, w);
+    const int64_t n = int64_t(L.nc) + L.ne;
+    if (n > 0) {
+      k_save_predict<<<nblk(n), kBlock, 0, c->stream>>>(
+          L.c, L.nc, L.nc1, L.e, L.ne, L.ne1, w[0], w[1], w[2], H, H1, H2, c->S0h.p, c->S1h.p,
+          c->S2h.p, U, U1, U2, c->S0u.p, c->S1u.p, c->S2u.p);
+      CK(cudaGetLastError());
+      ++c->launches;
+    }
+  }
+  const double third = 1.0 / 3.0, two3 = 2.0 / 3.0;
+  for (int k = 0; k < M; ++k) {
+    const int first = k == 0;
+    // stage 1: fine hb = ha + delta*d; interfaces acc1 += d   (:521-531)
+    if (k > 0) launch_predict(c, 1, k, M, H, U);
+    {
+      Op co[2] = {mk_op(OP_EULER, H1, H, delta), mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0,
+                                                       c->A1h.p, first)};
+      Op eo[2] = {mk_op(OP_EULER, U1, U, delta), mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0,
+                                                       c->A1u.p, first)};
+      launch_eval(c, ps, H, U, co, eo);
+    }
+    // stage 2: fine hc = 0.75 ha + 0.25 hb + (0.25 delta) d; acc2 += d   (:532-541)
+    launch_predict(c, 2, k, M, H1, U1);
+    {
+      const double cr = 0.25 * delta;
+      Op co[2] = {mk_op(OP_WCOMB, H2, H, 0.75, H1, 0.25, cr),
+                  mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A2h.p, first)};
+      Op eo[2] = {mk_op(OP_WCOMB, U2, U, 0.75, U1, 0.25, cr),
+                  mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A2u.p, first)};
+      launch_eval(c, ps, H1, U1, co, eo);
+    }
+    // stage 3: fine ha = 1/3 ha + 2/3 hc + (2/3 delta) d; acc3 += d, and on
+    // the last substep the interface correction (:542-553, :231-274).
+    launch_predict(c, 3, k, M, H2, U2);
+    {
+      const double cr = two3 * delta;
+      Op co[2], eo[2];
+      co[0] = mk_op(OP_WCOMB, H, H, third, H2, two3, cr);
+      eo[0] = mk_op(OP_WCOMB, U, U, third, U2, two3, cr);
+      if (k < M - 1) {
+        co[1] = mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A3h.p, first);
+        eo[1] = mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A3u.p, first);
+      } else {
+        co[1] = mk_op(OP_ACC_CORR, H, c->S0h.p, delta, nullptr, 1.0 / 6.0, two3, c->A3h.p, first,
+                      c->A1h.p, c->A2h.p);
+        eo[1] = mk_op(OP_ACC_CORR, U, c->S0u.p, delta, nullptr, 1.0 / 6.0, two3, c->A3u.p, first,
+                      c->A1u.p, c->A2u.p);
+      }
+      launch_eval(c, ps, H2, U2, co, eo);
+    }
+  }
+  // Step 4 (:557-563): coarse h = 1/3 h_old + 2/3 h2 + (2/3 dt) dh, in place.
+  {
+    const double cr = two3 * dt;
+    Op co[2] = {mk_op(OP_WCOMB, H, H, third, H2, two3, cr), mk_op(OP_WCOMB, H, H, third, H2, two3, cr)};
+    Op eo[2] = {mk_op(OP_WCOMB, U, U, third, U2, two3, cr), mk_op(OP_WCOMB, U, U, third, U2, two3, cr)};
+    launch_eval(c, p4, H2, U2, co, eo);
+  }
+}
+
+void tally_lts3(mswm_cuda_ctx* c, int M) {
+  tally(c, kMaskStep1, 0);
+  tally(c, kMaskIfCoarse, 1);
+  for (int k = 0; k < M; ++k) {
+    tally(c, kMaskSub, 0);
+    tally(c, kMaskSub, 1);
+    tally(c, kMaskSub, 2);
+  }
+  tally(c, kMaskCoarseOnly, 2);
+}
+
+// RK4 (integrators.cpp:370-410) with ping-pong stage buffers.
+void enqueue_rk4(mswm_cuda_ctx* c, double dt) {
+  MaskPlan& p = plan_for(c, MSWM_MASK_ALL);
+  const double half = 0.5 * dt, sixth = dt / 6.0;
+  double *H = c->H.p, *U = c->U.p;
+  k_step_counter<<<1, 1, 0, c->stream>>>(c->step_ctr.p);
+  auto both = [](Op o) { return std::array<Op, 2>{o, o}; };
+  {
+    auto co = both(mk_op(OP_RK4_FIRST, c->T1h.p, H, half, nullptr, 0, 0, c->A1h.p));
+    auto eo = both(mk_op(OP_RK4_FIRST, c->T1u.p, U, half, nullptr, 0, 0, c->A1u.p));
+    launch_eval(c, p, H, U, co.data(), eo.data());
+  }
+  {
+    auto co = both(mk_op(OP_RK4_MID, c->T2h.p, H, half, nullptr, 0, 0, c->A1h.p));
+    auto eo = both(mk_op(OP_RK4_MID, c->T2u.p, U, half, nullptr, 0, 0, c->A1u.p));
+    launch_eval(c, p, c->T1h.p, c->T1u.p, co.data(), eo.data());
+  }
+  {
+    auto co = both(mk_op(OP_RK4_MID, c->T1h.p, H, dt, nullptr, 0, 0, c->A1h.p));
+    auto eo = both(mk_op(OP_RK4_MID, c->T1u.p, U, dt, nullptr, 0, 0, c->A1u.p));
+    launch_eval(c, p, c->T2h.p, c->T2u.p, co.data(), eo.data());
+  }
+  {
+    auto co = both(mk_op(OP_RK4_LAST, H, H, sixth, nullptr, 0, 0, c->A1h.p));
+    auto eo = both(mk_op(OP_RK4_LAST, U, U, sixth, nullptr, 0, 0, c->A1u.p));
+    launch_eval(c, p, c->T1h.p, c->T1u.p, co.data(), eo.data());
+  }
+}
+
+// SSPRK2/3 (integrators.cpp:337-368).
+void enqueue_ssprk(mswm_cuda_ctx* c, int order, double dt) {
+  MaskPlan& p = plan_for(c, MSWM_MASK_ALL);
+  double *H = c->H.p, *U = c->U.p, *T1h = c->T1h.p, *T1u = c->T1u.p, *T2h = c->T2h.p,
+         *T2u = c->T2u.p;
+  k_step_counter<<<1, 1, 0, c->stream>>>(c->step_ctr.p);
+  auto both = [](Op o) { return std::array<Op, 2>{o, o}; };
+  {
+    auto co = both(mk_op(OP_EULER, T1h, H, dt));
+    auto eo = both(mk_op(OP_EULER, T1u, U, dt));
+    launch_eval(c, p, H, U, co.data(), eo.data());
+  }
+  if (order == 2) {
+    const double cr = 0.5 * dt;
+    auto co = both(mk_op(OP_WCOMB, H, H, 0.5, T1h, 0.5, cr));
+    auto eo = both(mk_op(OP_WCOMB, U, U, 0.5, T1u, 0.5, cr));
+    launch_eval(c, p, T1h, T1u, co.data(), eo.data());
+    return;
+  }
+  {
+    const double cr = 0.25 * dt;
+    auto co = both(mk_op(OP_WCOMB, T2h, H, 0.75, T1h, 0.25, cr));
+    auto eo = both(mk_op(OP_WCOMB, T2u, U, 0.75, T1u, 0.25, cr));
+    launch_eval(c, p, T1h, T1u, co.data(), eo.data());
+  }
+  {
+    const double cr = (2.0 / 3.0) * dt;
+    auto co = both(mk_op(OP_WCOMB, H, H, 1.0 / 3.0, T2h, 2.0 / 3.0, cr));
+    auto eo = both(mk_op(OP_WCOMB, U, U, 1.0 / 3.0, T2u, 2.0 / 3.0, cr));
+    launch_eval(c, p, T2h, T2u, co.data(), eo.data());
+  }
+}
+
+void enqueue_step(mswm_cuda_ctx* c, int scheme, double dt, int M) {
+  ++c->launches;  // the step-counter kernel every schedule starts with
+  switch (scheme) {
+    case MSWM_LTS3: enqueue_lts3(c, dt, M); break;
+    case MSWM_RK4: enqueue_rk4(c, dt); break;
+    case MSWM_SSPRK3: enqueue_ssprk(c, 3, dt); break;
+    case MSWM_SSPRK2: enqueue_ssprk(c, 2, dt); break;
+    default: throw Error(MSWM_E_CONFIG, "scheme not supported on the device path");
+  }
+}
+
+void tally_step(mswm_cuda_ctx* c, int scheme, int M) {
+  switch (scheme) {
+    case MSWM_LTS3: tally_lts3(c, M); break;
+    case MSWM_RK4:
+      for (int s = 0; s < 4; ++s) tally(c, MSWM_MASK_ALL, s);
+      break;
+    case MSWM_SSPRK3:
+      for (int s = 0; s < 3; ++s) tally(c, MSWM_MASK_ALL, s);
+      break;
+    case MSWM_SSPRK2:
+      for (int s = 0; s < 2; ++s) tally(c, MSWM_MASK_ALL, s);
+      break;
+  }
+  ++c->ledger_steps;
+}
+
+cudaGraphExec_t graph_for(mswm_cuda_ctx* c, int scheme, double dt, int M) {
+  const auto key = std::make_tuple(scheme, dt, scheme == MSWM_LTS3 ? M : 0, int(c->profiling));
+  auto it = c->graphs.find(key);
+  if (it != c->graphs.end()) {
+    c->last_records = &it->second.records;
+    c->last_kernels_per_step = it->second.kernels;
+    return it->second.exec;
+  }
+  // Build every plan outside the capture (plan construction synchronises).
+  if (scheme == MSWM_LTS3) {
+    plan_for(c, kMaskStep1);
+    plan_for(c, kMaskIfCoarse);
+    plan_for(c, kMaskSub);
+    plan_for(c, kMaskCoarseOnly);
+  } else {
+    plan_for(c, MSWM_MASK_ALL);
+  }
+  mswm_cuda_ctx::Graph gr;
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  c->capture_records = c->profiling ? &gr.records : nullptr;
+  c->launches = 0;
+  try {
+    enqueue_step(c, scheme, dt, M);
+  } catch (...) {
+    c->capture_records = nullptr;
+    cudaStreamEndCapture(c->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  c->capture_records = nullptr;
+  gr.kernels = c->launches;
+  CK(cudaStreamEndCapture(c->stream, &g));
+  cudaError_t e = cudaGraphInstantiate(&gr.exec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) throw Error(MSWM_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+  auto& slot = c->graphs[key];
+  slot = std::move(gr);
+  c->last_records = &slot.records;
+  c->last_kernels_per_step = slot.kernels;
+  return slot.exec;
+}
+
+// ---------------------------------------------------------------------------
+// regions on device (regions.cpp:14-171)
+
+int set_regions_impl(mswm_cuda_ctx* c, const uint8_t* fine_mask, int width, uint8_t* cell_label,
+                     uint8_t* cell_sub, uint8_t* edge_label, int64_t* group_size, int* warnings) {
+  if (width < 1) throw Error(MSWM_E_CONFIG, "interface width must be >= 1");
+  if (!fine_mask) throw Error(MSWM_E_USAGE, "fine mask is null");
+  cudaStream_t s = c->stream;
+  const int32_t nC = c->nC, nE = c->nE;
+  // dist = 0 for fine cells, -1 elsewhere (internal order)
+  std::vector<int32_t> dist0(nC);
+  int64_t n_fine = 0;
+  for (int32_t ni = 0; ni < nC; ++ni) {
+    const bool fine = fine_mask[c->c_new2old[ni]] != 0;
+    dist0[ni] = fine ? 0 : -1;
+    n_fine += fine;
+  }
+  if (n_fine == 0) throw Error(MSWM_E_CONFIG, "fine predicate selects no cells");
+  if (n_fine == nC)
+    throw Error(MSWM_E_CONFIG, "fine predicate selects every cell; no room for interface layers");
+  invalidate(c);
+  c->have_regions = false;
+  DArr<int32_t> dist, counters;
+  dist.upload(dist0, s);
+  counters.alloc(size_t(2 * width) + 1);
+  counters.zero(s);
+  const DevMesh M = c->dev();
+  for (int level = 1; level <= 2 * width; ++level) {
+    k_bfs_layer<<<nblk(nC), kBlock, 0, s>>>(M, c->c_nbr.p, dist.p, level, counters.p + level);
+    CK(cudaGetLastError());
+  }
+  std::vector<int32_t> cnt(size_t(2 * width) + 1);
+  CK(cudaMemcpyAsync(cnt.data(), counters.p, cnt.size() * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  int64_t n_layers = 0;
+  for (int layer = 1; layer <= 2 * width; ++layer) {
+    if (cnt[layer] == 0)
+      throw Error(MSWM_E_CONFIG, "interface layer " + std::to_string(layer) +
+                                     " is empty; the non-fine region is too small for width " +
+                                     std::to_string(width));
+    n_layers += cnt[layer];
+  }
+  if (n_fine + n_layers == nC)
+    throw Error(MSWM_E_CONFIG, "interface layers exhaust the non-fine cells; no coarse region left");
+  c->cell_label.alloc(nC);
+  c->cell_sub.alloc(nC);
+  c->edge_label.alloc(nE);
+  k_cell_labels<<<nblk(nC), kBlock, 0, s>>>(nC, dist.p, width, c->cell_label.p, c->cell_sub.p);
+  k_underline<<<nblk(nC), kBlock, 0, s>>>(M, c->c_nbr.p, c->cell_label.p, c->cell_sub.p, 1);
+  k_underline<<<nblk(nC), kBlock, 0, s>>>(M, c->c_nbr.p, c->cell_label.p, c->cell_sub.p, 2);
+  DArr<uint8_t> ckey, ekey;
+  ckey.alloc(nC);
+  ekey.alloc(nE);
+  k_edge_labels_and_keys<<<nblk(std::max(nC, nE)), kBlock, 0, s>>>(M, c->cell_label.p, c->cell_sub.p,
+                                                                   c->edge_label.p, ckey.p, ekey.p);
+  CK(cudaGetLastError());
+  // Warp-ballot compaction into the 11 ascending group lists.
+  std::vector<int64_t> cs = compact(c, ckey.p, nC, 6, c->cell_groups);
+  std::vector<int64_t> es = compact(c, ekey.p, nE, 5, c->edge_groups);
+  int64_t off = 0;
+  for (int g = 0; g < 6; ++g) {
+    c->gsize[g] = cs[g];
+    c->goff[g] = off;
+    off += cs[g];
+  }
+  off = 0;
+  for (int g = 0; g < 5; ++g) {
+    c->gsize[6 + g] = es[g];
+    c->goff[6 + g] = off;
+    off += es[g];
+  }
+  c->width = width;
+  c->have_regions = true;
+  // Outputs in original order.
+  if (cell_label || cell_sub || edge_label) {
+    std::vector<uint8_t> cl(nC), cb(nC), el(nE);
+    CK(cudaMemcpyAsync(cl.data(), c->cell_label.p, nC, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(cb.data(), c->cell_sub.p, nC, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(el.data(), c->edge_label.p, nE, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int32_t ni = 0; ni < nC; ++ni) {
+      if (cell_label) cell_label[c->c_new2old[ni]] = cl[ni];
+      if (cell_sub) cell_sub[c->c_new2old[ni]] = cb[ni];
+    }
+    if (edge_label)
+      for (int32_t ne = 0; ne < nE; ++ne) edge_label[c->e_new2old[ne]] = el[ne];
+  }
+  if (group_size)
+    for (int g = 0; g < 11; ++g) group_size[g] = c->gsize[g];
+  if (warnings) {
+    // label_underline_fine warnings (regions.cpp:131-138)
+    *warnings = c->gsize[1] == 0 ? 1 : (c->gsize[2] == 0 ? 2 : (c->gsize[0] == 0 ? 4 : 0));
+  }
+  return MSWM_OK;
+}
+
+template <class F>
+int guard(mswm_cuda_ctx* c, F&& f) {
+  try {
+    return f();
+  } catch (const Error& e) {
+    if (c) c->last_error = e.what();
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    if (c) c->last_error = "host allocation failed";
+    return MSWM_E_NOMEM;
+  } catch (const std::exception& e) {
+    if (c) c->last_error = e.what();
+    return MSWM_E_CONFIG;
+  }
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+
+extern "C" {
+
+int mswm_cuda_create(const mswm_mesh_desc* mesh, int device, int order, mswm_cuda_ctx** out) {
+  if (!out) return MSWM_E_USAGE;
+  *out = nullptr;
+  auto c = std::make_unique<mswm_cuda_ctx>();
+  try {
+    if (!mesh) throw Error(MSWM_E_USAGE, "null mesh descriptor");
+    if (order != MSWM_ORDER_INPUT && order != MSWM_ORDER_HILBERT)
+      throw Error(MSWM_E_USAGE, "unknown ordering policy");
+    c->device = device;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    build_tables(c.get(), mesh);
+  } catch (const Error& e) {
+    g_create_error = e.what();
+    return e.status;
+  } catch (const std::exception& e) {
+    g_create_error = e.what();
+    return MSWM_E_NOMEM;
+  }
+  *out = c.release();
+  return MSWM_OK;
+}
+
+void mswm_cuda_destroy(mswm_cuda_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  delete ctx;
+}
+
+const char* mswm_cuda_last_error(const mswm_cuda_ctx* ctx) {
+  return ctx ? ctx->last_error.c_str() : g_create_error.c_str();
+}
+
+int mswm_cuda_set_fields(mswm_cuda_ctx* c, const double* b, const double* f_vertex, double gravity) {
+  return guard(c, [&] {
+    check_ctx(c);
+    if (!b || !f_vertex) throw Error(MSWM_E_USAGE, "null field");
+    upload_field(c, c->b, b, c->c_new2old, c->nC);
+    upload_field(c, c->f, f_vertex, c->v_new2old, c->nV);
+    c->gravity = gravity;
+    c->have_fields = true;
+    CK(cudaStreamSynchronize(c->stream));
+    invalidate(c);  // gravity is a graph kernel argument
+    return int(MSWM_OK);
+  });
+}
+
+int mswm_cuda_set_regions(mswm_cuda_ctx* c, const uint8_t* fine_mask, int interface_width,
+                          uint8_t* cell_label, uint8_t* cell_sublabel, uint8_t* edge_label,
+                          int64_t group_size[11], int* warnings) {
+  return guard(c, [&] {
+    check_ctx(c);
+    return set_regions_impl(c, fine_mask, interface_width, cell_label, cell_sublabel, edge_label,
+                            group_size, warnings);
+  });
+}
+
+int mswm_cuda_get_group(mswm_cuda_ctx* c, int group, int32_t* ids) {
+  return guard(c, [&] {
+    check_ctx(c);
+    if (!c->have_regions) throw Error(MSWM_E_USAGE, "no regions");
+    if (group < 0 || group > 10) throw Error(MSWM_E_USAGE, "group index out of range");
+    const int64_t n = c->gsize[group];
+    if (!ids || n == 0) return int(MSWM_OK);
+    const DArr<int32_t>& buf = group < 6 ? c->cell_groups : c->edge_groups;
+    CK(cudaMemcpyAsync(ids, buf.p + c->goff[group], size_t(n) * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (!c->identity) {
+      const auto& n2o = group < 6 ? c->c_new2old : c->e_new2old;
+      for (int64_t k = 0; k < n; ++k) ids[k] = n2o[ids[k]];
+      std::sort(ids, ids + n);
+    }
+    return int(MSWM_OK);
+  });
+}
+
+int mswm_cuda_get_closure(mswm_cuda_ctx* c, unsigned mask, int kind, int32_t* ids, int64_t* n) {
+  return guard(c, [&] {
+    check_ctx(c);
+    MaskPlan& p = plan_for(c, mask);
+    const DArr<int32_t>* L = nullptr;
+    int64_t cnt = 0;
+    const std::vector<int32_t>* n2o = nullptr;
+    switch (kind) {
+      case MSWM_CLOSURE_FLUX: L = &p.fclos; cnt = p.nf; n2o = &c->e_new2old; break;
+      case MSWM_CLOSURE_QT: L = &p.qclos; cnt = p.nq; n2o = &c->e_new2old; break;
+      case MSWM_CLOSURE_K: L = &p.kclos; cnt = p.nk; n2o = &c->c_new2old; break;
+      case MSWM_CLOSURE_PV: L = &p.vclos; cnt = p.nv; n2o = &c->v_new2old; break;
+      default: throw Error(MSWM_E_USAGE, "closure kind out of range");
+    }
+    if (n) *n = cnt;
+    if (ids && cnt) {
+      CK(cudaMemcpyAsync(ids, L->p, size_t(cnt) * 4, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      if (!c->identity) {
+        for (int64_t k = 0; k < cnt; ++k) ids[k] = (*n2o)[ids[k]];
+        std::sort(ids, ids + cnt);
+      }
+    }
+    return int(MSWM_OK);
+  });
+}
+
+int mswm_cuda_eval(mswm_cuda_ctx* c, const double* h, const double* u, unsigned mask, double* dh,
+                   double* du) {
+  return guard(c, [&] {
+    check_ctx(c);
+    if (!h || !u || !dh || !du) throw Error(MSWM_E_USAGE, "null array");
+    if (!c->have_fields) throw Error(MSWM_E_USAGE, "set_fields must be called before eval");
+    MaskPlan& p = plan_for(c, mask);
+    upload_field(c, c->T1h, h, c->c_new2old, c->nC);
+    upload_field(c, c->T1u, u, c->e_new2old, c->nE);
+    reset_dry(c);
+    Op co[2] = {mk_op(OP_STORE, c->Dh.p), mk_op(OP_STORE, c->Dh.p)};
+    Op eo[2] = {mk_op(OP_STORE, c->Du.p), mk_op(OP_STORE, c->Du.p)};
+    launch_eval(c, p, c->T1h.p, c->T1u.p, co, eo);
+    CK(cudaStreamSynchronize(c->stream));
+    if (read_dry(c)) {
+      c->last_dry_step = 0;
+      throw Error(MSWM_E_DRY_VERTEX, "vertex " + std::to_string(c->last_dry_vertex) +
+                                         " has non-positive thickness");
+    }
+    // Gather the masked entries and scatter them into the caller's arrays;
+    // everything else is left untouched (integrators.hpp:63-67).
+    std::vector<double> tmp(std::max(c->nC, c->nE));
+    if (p.nc) {
+      CK(cudaMemcpyAsync(tmp.data(), c->Dh.p, size_t(c->nC) * 8, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      for (int32_t k = 0; k < p.nc; ++k) {
+        const int32_t orig = p.host_cells[k];
+        dh[orig] = tmp[c->identity ? orig : c->c_old2new[orig]];
+      }
+    }
+    if (p.ne) {
+      CK(cudaMemcpyAsync(tmp.data(), c->Du.p, size_t(c->nE) * 8, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      for (int32_t k = 0; k < p.ne; ++k) {
+        const int32_t orig = p.host_edges[k];
+        du[orig] = tmp[c->identity ? orig : c->e_old2new[orig]];
+      }
+    }
+    return int(MSWM_OK);
+  });
+}
+
+int mswm_cuda_state_upload(mswm_cuda_ctx* c, const double* h, const double* u, double time) {
+  return guard(c, [&] {
+    check_ctx(c);
+    if (!h || !u) throw Error(MSWM_E_USAGE, "null array");
+    upload_field(c, c->H, h, c->c_new2old, c->nC);
+    upload_field(c, c->U, u, c->e_new2old, c->nE);
+    c->time = time;
+    CK(cudaStreamSynchronize(c->stream));
+    return int(MSWM_OK);
+  });
+}
+
+int mswm_cuda_state_download(mswm_cuda_ctx* c, double* h, double* u, double* time) {
+  return guard(c, [&] {
+    check_ctx(c);
+    if (h) download_field(c, c->H, h, c->c_new2old, c->nC);
+    if (u) download_field(c, c->U, u, c->e_new2old, c->nE);
+    if (time) *time = c->time;
+    return int(MSWM_OK);
+  });
+}
+
+int mswm_cuda_step(mswm_cuda_ctx* c, int scheme, double dt, int M, int64_t n_steps, int sync) {
+  return guard(c, [&] {
+    check_ctx(c);
+    if (!(dt > 0.0)) throw Error(MSWM_E_CONFIG, "time step must be positive");
+    if (n_steps < 0) throw Error(MSWM_E_USAGE, "negative step count");
+    if (scheme == MSWM_LTS3) {
+      if (M < 1) throw Error(MSWM_E_CONFIG, "substep count must be >= 1");
+      if (!c->have_regions) throw Error(MSWM_E_CONFIG, "local time stepping requires a region map");
+    } else if (scheme == MSWM_LTS2) {
+      throw Error(MSWM_E_CONFIG, "LTS2 is not on the device path (north_star names LTS3/RK4)");
+    } else if (scheme != MSWM_RK4 && scheme != MSWM_SSPRK3 && scheme != MSWM_SSPRK2) {
+      throw Error(MSWM_E_CONFIG, "unknown scheme");
+    }
+    if (!c->have_fields) throw Error(MSWM_E_USAGE, "set_fields must be called before stepping");
+    if (n_steps == 0) return int(MSWM_OK);
+    cudaGraphExec_t g = graph_for(c, scheme, dt, M);
+    reset_dry(c);
+    CK(cudaMemcpyAsync(c->step_ctr.p, &c->steps_issued, 8, cudaMemcpyHostToDevice, c->stream));
+    for (int64_t k = 0; k < n_steps; ++k) {
+      CK(cudaGraphLaunch(g, c->stream));
+      tally_step(c, scheme, M);
+      c->time += dt;
+    }
+    c->steps_issued += n_steps;
+    if (sync) {
+      CK(cudaStreamSynchronize(c->stream));
+      if (read_dry(c))
+        throw Error(MSWM_E_DRY_VERTEX, "vertex " + std::to_string(c->last_dry_vertex) +
+                                           " has non-positive thickness (during the step batch)");
+    }
+    return int(MSWM_OK);
+  });
+}
+
+int mswm_cuda_ledger(mswm_cuda_ctx* c, int64_t cell_evals[16], int64_t edge_evals[16], int64_t* steps) {
+  if (!c) return MSWM_E_USAGE;
+  for (int r = 0; r < 4; ++r)
+    for (int s = 0; s < 4; ++s) {
+      if (cell_evals) cell_evals[4 * r + s] = c->ledger_cell[r][s];
+      if (edge_evals) edge_evals[4 * r + s] = c->ledger_edge[r][s];
+    }
+  if (steps) *steps = c->ledger_steps;
+  return MSWM_OK;
+}
+
+int mswm_cuda_ledger_reset(mswm_cuda_ctx* c) {
+  if (!c) return MSWM_E_USAGE;
+  std::memset(c->ledger_cell, 0, sizeof(c->ledger_cell));
+  std::memset(c->ledger_edge, 0, sizeof(c->ledger_edge));
+  c->ledger_steps = 0;
+  return MSWM_OK;
+}
+
+int mswm_cuda_dry_vertex(const mswm_cuda_ctx* c, int64_t* step) {
+  if (!c) return -1;
+  if (step) *step = c->last_dry_step;
+  return c->last_dry_vertex;
+}
+
+int mswm_cuda_sync(mswm_cuda_ctx* c) {
+  return guard(c, [&] {
+    check_ctx(c);
+    CK(cudaStreamSynchronize(c->stream));
+    if (read_dry(c))
+      throw Error(MSWM_E_DRY_VERTEX,
+                  "vertex " + std::to_string(c->last_dry_vertex) + " has non-positive thickness");
+    return int(MSWM_OK);
+  });
+}
+
+void* mswm_cuda_stream(mswm_cuda_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int mswm_cuda_set_profiling(mswm_cuda_ctx* c, int enable) {
+  return guard(c, [&] {
+    check_ctx(c);
+    c->profiling = enable != 0;
+    return int(MSWM_OK);
+  });
+}
+
+int mswm_cuda_eval_profile(mswm_cuda_ctx* c, float* eval_ms, int64_t* out_cells, int64_t* out_edges,
+                           int cap, int* n) {
+  return guard(c, [&] {
+    check_ctx(c);
+    CK(cudaStreamSynchronize(c->stream));
+    const std::vector<EvalRecord> empty;
+    const std::vector<EvalRecord>& R = c->last_records ? *c->last_records : empty;
+    const int cnt = int(R.size());
+    if (n) *n = cnt;
+    for (int k = 0; k < cnt && k < cap; ++k) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, R[k].start, R[k].stop));
+      if (eval_ms) eval_ms[k] = ms;
+      if (out_cells) out_cells[k] = R[k].nc;
+      if (out_edges) out_edges[k] = R[k].ne;
+    }
+    return int(MSWM_OK);
+  });
+}
+
+int mswm_cuda_kernels_per_step(mswm_cuda_ctx* c, int64_t* n) {
+  if (!c || !n) return MSWM_E_USAGE;
+  *n = c->last_kernels_per_step;
+  return MSWM_OK;
+}
+
+int mswm_cuda_total_mass(mswm_cuda_ctx* c, double* mass) {
+  return guard(c, [&] {
+    check_ctx(c);
+    if (!mass) throw Error(MSWM_E_USAGE, "null output");
+    std::vector<double> h(c->nC);
+    download_field(c, c->H, h.data(), c->c_new2old, c->nC);
+    double m = 0.0;  // harness.cpp:99-105, ascending original id
+    for (int32_t i = 0; i < c->nC; ++i) m += c->h_cell_area[i] * h[i];
+    *mass = m;
+    return int(MSWM_OK);
+  });
+}
+
+}  // extern "C"

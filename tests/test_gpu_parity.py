@@ -1,0 +1,249 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle.
+
+Bar: bitwise equality for region labels, group lists, closure sets,
+tendencies and prognostic states (the path keeps the reference's IEEE
+operation order and is built with --fmad=false), which is stricter than
+north_star's 1e-11 relative max-norm after 100 coarse steps; the 1e-11
+bound is asserted too where north_star states it.
+"""
+import numpy as np
+import pytest
+
+from helpers import bits_equal, golden_mesh, load_golden, max_rel
+from make_golden import mesh_digest
+from oracle.oracle import Oracle
+from paper_2106_07154_b200 import workloads as W
+from paper_2106_07154_b200.api import (LTS3_MASKS, ConfigError, CudaContext, CudaEvaluator,
+                                       CudaStepper, DryVertexError, Scheme, SchemeConfig, State,
+                                       UsageError, kMaskAll)
+from paper_2106_07154_b200.mesh import Mesh
+
+pytestmark = pytest.mark.gpu
+
+FIXTURES = ["planar24", "sphereL3"]
+SENTINEL = 123456789.0
+
+
+def _ctx(wl_or_mesh, b, f, g, fine=None, width=1):
+    ctx = CudaContext(wl_or_mesh, b, f, g)
+    if fine is not None:
+        ctx.make_regions(fine, width)
+    return ctx
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_golden_regions_tendencies_steps(name):
+    g = load_golden(name)
+    mesh = golden_mesh(name)
+    assert mesh_digest(mesh) == str(g["digest"])
+    ctx = _ctx(mesh, g["b"], g["f"], float(g["gravity"]), g["fine"])
+    rm = ctx.regions
+    assert np.array_equal(rm.cell_label, g["cell_label"])
+    assert np.array_equal(rm.cell_sublabel, g["cell_sub"])
+    assert np.array_equal(rm.edge_label, g["edge_label"])
+    for gi in range(11):
+        assert np.array_equal(rm.groups[gi], g[f"group{gi}"]), gi
+    ev = CudaEvaluator(ctx)
+    for mask in LTS3_MASKS + [kMaskAll]:
+        dh = np.full(mesh.n_cells, np.nan)
+        du = np.full(mesh.n_edges, np.nan)
+        ev.eval(g["h"], g["u"], mask, dh, du)
+        assert bits_equal(dh, g[f"dh_{mask}"]), hex(mask)
+        assert bits_equal(du, g[f"du_{mask}"]), hex(mask)
+        for kind in range(4):
+            assert np.array_equal(ctx.closure(mask, kind), g[f"closure_{mask}_{kind}"]), (mask, kind)
+    M, dt = int(g["M"]), float(g["dt"])
+    for scheme, n in [(Scheme.LTS3, 3), (Scheme.RK4, 2), (Scheme.SSPRK3, 2)]:
+        c2 = _ctx(mesh, g["b"], g["f"], float(g["gravity"]), g["fine"])
+        c2.upload(State(g["h"], g["u"], 0.0))
+        c2.advance(scheme, dt if scheme == Scheme.LTS3 else dt / M, M, n)
+        st = c2.download()
+        assert bits_equal(st.h, g[f"h_{scheme.name}"]), scheme
+        assert bits_equal(st.u, g[f"u_{scheme.name}"]), scheme
+        lg = c2.ledger()
+        assert np.array_equal(lg.cell_evals, g[f"ledger_cell_{scheme.name}"])
+        assert np.array_equal(lg.edge_evals, g[f"ledger_edge_{scheme.name}"])
+
+
+def _oracle_for(wl):
+    o = Oracle(wl.mesh, wl.b, wl.f, wl.gravity)
+    o.set_regions(wl.fine_mask, wl.width)
+    return o
+
+
+def test_c1_lts3_100_steps_bitwise():
+    """BASELINE configs[0]: 100 LTS3 coarse steps on 1 GPU vs the CPU oracle."""
+    wl = W.config1()
+    o = _oracle_for(wl)
+    h_ref, u_ref, t_ref = o.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, wl.M, wl.n_steps)
+    ctx = _ctx(wl.mesh, wl.b, wl.f, wl.gravity, wl.fine_mask)
+    for a, b in zip(ctx.regions.groups, o.groups()):
+        assert np.array_equal(a, b)
+    ctx.upload(State(wl.h, wl.u, 0.0))
+    ctx.advance(Scheme.LTS3, wl.dt, wl.M, wl.n_steps)
+    st = ctx.download()
+    assert max_rel(st.h, h_ref) <= 1e-11 and max_rel(st.u, u_ref, 1.0) <= 1e-11
+    assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
+    assert st.time == pytest.approx(t_ref)
+    c, e, s = o.ledger()
+    lg = ctx.ledger()
+    assert np.array_equal(lg.cell_evals, c) and np.array_equal(lg.edge_evals, e)
+    assert lg.steps_taken == s == wl.n_steps
+
+
+@pytest.mark.parametrize("M", [1, 2, 5])
+def test_sphere_lts3_and_rk4_bitwise(M):
+    wl = W.small_sphere(5, seed=7, cap_deg=25.0, M=M)
+    o = _oracle_for(wl)
+    ctx = _ctx(wl.mesh, wl.b, wl.f, wl.gravity, wl.fine_mask)
+    for scheme, n, dt in [(Scheme.LTS3, 6, wl.dt), (Scheme.RK4, 3, wl.dt / M),
+                          (Scheme.SSPRK3, 3, wl.dt / M)]:
+        h_ref, u_ref, _ = o.step(int(scheme), wl.h, wl.u, 0.0, dt, M, n)
+        ctx.upload(State(wl.h, wl.u, 0.0))
+        ctx.advance(scheme, dt, M, n)
+        st = ctx.download()
+        assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref), scheme
+
+
+def test_c2_full_size_parity():
+    """BASELINE configs[1] at full size: regions bit-exact, all masks bitwise,
+    5 coarse steps bitwise against the oracle."""
+    wl = W.config2(n_steps=5)
+    o = _oracle_for(wl)
+    ctx = _ctx(wl.mesh, wl.b, wl.f, wl.gravity, wl.fine_mask)
+    cl, cs, el = o.labels()
+    assert np.array_equal(ctx.regions.cell_label, cl)
+    assert np.array_equal(ctx.regions.cell_sublabel, cs)
+    assert np.array_equal(ctx.regions.edge_label, el)
+    for a, b in zip(ctx.regions.groups, o.groups()):
+        assert np.array_equal(a, b)
+    ev = CudaEvaluator(ctx)
+    for mask in LTS3_MASKS:
+        dh1 = np.full(wl.mesh.n_cells, SENTINEL)
+        du1 = np.full(wl.mesh.n_edges, SENTINEL)
+        dh2, du2 = dh1.copy(), du1.copy()
+        ev.eval(wl.h, wl.u, mask, dh1, du1)
+        o.eval(wl.h, wl.u, mask, dh2, du2)
+        assert bits_equal(dh1, dh2) and bits_equal(du1, du2)
+    h_ref, u_ref, _ = o.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, wl.M, wl.n_steps)
+    ctx.upload(State(wl.h, wl.u, 0.0))
+    ctx.advance(Scheme.LTS3, wl.dt, wl.M, wl.n_steps)
+    st = ctx.download()
+    assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
+
+
+def test_restricted_evaluation_bitwise_equal_full():
+    # test_operators.cpp:164-202 through the masked-group interface
+    wl = W.small_sphere(4, seed=5)
+    ctx = _ctx(wl.mesh, wl.b, wl.f, wl.gravity, wl.fine_mask)
+    ev = CudaEvaluator(ctx)
+    m = wl.mesh
+    dh_full = np.full(m.n_cells, SENTINEL)
+    du_full = np.full(m.n_edges, SENTINEL)
+    ev.eval(wl.h, wl.u, kMaskAll, dh_full, du_full)
+    for mask in [0x1, 0x20, 0x400, 0x41, 0x28 | 0x500, 0x7FF & ~0x21, 0x5 | 0x280]:
+        dh = np.full(m.n_cells, SENTINEL)
+        du = np.full(m.n_edges, SENTINEL)
+        ev.eval(wl.h, wl.u, mask, dh, du)
+        in_c = np.zeros(m.n_cells, bool)
+        in_e = np.zeros(m.n_edges, bool)
+        for gi in range(6):
+            if mask & (1 << gi):
+                in_c[ctx.regions.groups[gi]] = True
+        for gi in range(6, 11):
+            if mask & (1 << gi):
+                in_e[ctx.regions.groups[gi]] = True
+        assert bits_equal(dh, np.where(in_c, dh_full, SENTINEL))
+        assert bits_equal(du, np.where(in_e, du_full, SENTINEL))
+
+
+def test_m1_lts3_reduces_to_ssprk3():
+    # acceptance criterion 1 (acceptance.cpp:98-118), both on the device
+    wl = W.small_sphere(4, seed=9, M=1)
+    ctx = _ctx(wl.mesh, wl.b, wl.f, wl.gravity, wl.fine_mask)
+    ctx.upload(State(wl.h, wl.u, 0.0))
+    ctx.advance(Scheme.LTS3, wl.dt, 1, 10)
+    a = ctx.download()
+    ctx.upload(State(wl.h, wl.u, 0.0))
+    ctx.advance(Scheme.SSPRK3, wl.dt, 1, 10)
+    b = ctx.download()
+    assert max_rel(a.h, b.h) <= 1e-12
+    assert np.max(np.abs(a.u - b.u) / np.maximum(np.abs(b.u), 1.0)) <= 1e-12
+
+
+def test_mass_conservation_100_steps():
+    # acceptance criterion 3 (acceptance.cpp:147-166): drift <= 1e-11
+    wl = W.config1()
+    ctx = _ctx(wl.mesh, wl.b, wl.f, wl.gravity, wl.fine_mask)
+    ctx.upload(State(wl.h, wl.u, 0.0))
+    m0 = ctx.total_mass()
+    assert m0 == wl.mesh.total_mass(wl.h)
+    ctx.advance(Scheme.LTS3, wl.dt, wl.M, 100)
+    m1 = ctx.total_mass()
+    assert abs(m1 - m0) / abs(m0) <= 1e-11
+
+
+def test_ledger_matches_hand_derived_formulas():
+    # test_integrators.cpp:254-276
+    wl = W.small_sphere(4, seed=3)
+    ctx = _ctx(wl.mesh, wl.b, wl.f, wl.gravity, wl.fine_mask)
+    G = [len(x) for x in ctx.regions.groups]
+    Fc, U1, U2, I1, I2, Cc = G[0] + G[1] + G[2], G[1], G[2], G[3], G[4], G[5]
+    Fe, Ue, E1, E2, Ce = G[6] + G[7], G[7], G[8], G[9], G[10]
+    for M in (1, 2, 4):
+        ctx.reset_ledger()
+        ctx.upload(State(wl.h, wl.u, 0.0))
+        ctx.advance(Scheme.LTS3, wl.dt, M, 1)
+        lg = ctx.ledger()
+        assert lg.cell_evals[0][0] == U1 + U2 + M * Fc
+        assert lg.edge_evals[0][0] == Ue + M * Fe
+        assert lg.cell_evals[1][0] == I1 + M * I1
+        assert lg.cell_evals[3][0] == Cc
+        assert lg.cell_evals[2][1] == I2 + M * I2
+        assert lg.cell_evals[3][2] == Cc
+        assert lg.total_cell_evals() == (U1 + U2 + I1 + I2 + Cc) + (I1 + I2 + Cc) + Cc \
+            + 3 * M * (Fc + I1 + I2)
+        assert lg.total_edge_evals() == (Ue + E1 + E2 + Ce) + (E1 + E2 + Ce) + Ce \
+            + 3 * M * (Fe + E1 + E2)
+
+
+def test_dry_vertex_reported():
+    # test_operators.cpp:222-242
+    m = Mesh.icosahedral(0, 1.0)
+    h = np.ones(m.n_cells)
+    h[4] = -40.0
+    u = np.full(m.n_edges, 0.1)
+    ctx = CudaContext(m, np.zeros(m.n_cells), np.zeros(m.n_vertices), 9.80616)
+    with pytest.raises(DryVertexError) as err:
+        CudaEvaluator(ctx).eval(h, u, kMaskAll, np.zeros(m.n_cells), np.zeros(m.n_edges))
+    v = err.value.vertex
+    assert 0 <= v < m.n_vertices and 4 in m.vertex_cells[v]
+
+
+def test_usage_and_config_errors():
+    wl = W.small_sphere(3)
+    ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity)
+    ev = CudaEvaluator(ctx)
+    z = (np.zeros(wl.mesh.n_cells), np.zeros(wl.mesh.n_edges))
+    with pytest.raises(UsageError):          # integrators.cpp:139-142
+        ev.eval(wl.h, wl.u, 0x21, *z)
+    ctx.upload(State(wl.h, wl.u, 0.0))
+    with pytest.raises(ConfigError):         # integrators.cpp:413-421
+        ctx.advance(Scheme.LTS3, wl.dt, 4, 1)
+    with pytest.raises(ConfigError):
+        ctx.advance(Scheme.RK4, -1.0, 1, 1)
+    with pytest.raises(ConfigError):         # regions.cpp:77-79
+        ctx.make_regions(np.zeros(wl.mesh.n_cells, np.uint8))
+    ctx.make_regions(wl.fine_mask)
+    with pytest.raises(ConfigError):
+        ctx.advance(Scheme.LTS3, wl.dt, 0, 1)
+
+
+def test_stepper_drop_in_interface():
+    wl = W.small_sphere(3, seed=4)
+    ctx = _ctx(wl.mesh, wl.b, wl.f, wl.gravity, wl.fine_mask)
+    o = _oracle_for(wl)
+    st = State(wl.h.copy(), wl.u.copy(), 0.0)
+    CudaStepper(ctx).step(st, SchemeConfig(Scheme.LTS3, wl.dt, wl.M))
+    h_ref, u_ref, _ = o.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, wl.M, 1)
+    assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
