@@ -100,20 +100,20 @@ typedef struct mswm_mesh_desc {
 
 typedef struct mswm_cuda_ctx mswm_cuda_ctx;
 
-/* Renumbering policy for mswm_cuda_create (internal layout only; results are
- * bitwise independent of it because per-element operation order is kept). */
-typedef enum {
-  MSWM_ORDER_INPUT = 0,   /* keep the caller's numbering */
-  MSWM_ORDER_HILBERT = 1  /* space-filling-curve order from cell adjacency */
-} mswm_order;
-
 /* Create a context on CUDA device `device`: validates and uploads the mesh,
  * builds the device tables.  Replaces constructing SerialEvaluator
  * (proj/src/integrators.cpp:297-314, minus b/f which come from
- * mswm_cuda_set_fields).  On failure *out is NULL and the message is
- * available from mswm_cuda_last_error(NULL). */
-int mswm_cuda_create(const mswm_mesh_desc* mesh, int device, int order,
-                     mswm_cuda_ctx** out);
+ * mswm_cuda_set_fields).  cell_order (may be NULL = input order) is a
+ * permutation of the cells for the internal memory layout, normally a
+ * space-filling curve (mswm_mesh_locality_order); edges and vertices follow
+ * it.  Results are bitwise independent of cell_order.  When the stencil and
+ * weights are the reference builder's ring walk and weight rule
+ * (mesh_build.cpp:133-154, 343-362) -- verified bitwise here -- the kernels
+ * rebuild them from per-cell rows instead of streaming the stencil tables.
+ * On failure *out is NULL and the message is available from
+ * mswm_cuda_last_error(NULL). */
+int mswm_cuda_create(const mswm_mesh_desc* mesh, int device,
+                     const int32_t* cell_order, mswm_cuda_ctx** out);
 void mswm_cuda_destroy(mswm_cuda_ctx* ctx);
 /* Last error message of ctx, or of the last failed create when ctx is NULL. */
 const char* mswm_cuda_last_error(const mswm_cuda_ctx* ctx);
@@ -195,6 +195,12 @@ int mswm_cuda_set_profiling(mswm_cuda_ctx* ctx, int enable);
 int mswm_cuda_eval_profile(mswm_cuda_ctx* ctx, float* eval_ms,
                            int64_t* out_cells, int64_t* out_edges, int cap,
                            int* n);
+
+/* Layout actually chosen at create: ring_derived = 1 when the stencil and
+ * weights are rebuilt from per-cell rows, identity_order = 1 when the
+ * caller's numbering is kept.  Either pointer may be NULL. */
+int mswm_cuda_layout_info(const mswm_cuda_ctx* ctx, int* ring_derived,
+                          int* identity_order);
 
 /* Number of this library's kernels one replay of the most recently used
  * step graph launches (the bench's gpu_launches evidence). */

@@ -58,6 +58,11 @@ int mswm_mesh_get_geometry(const mswm_mesh* m, const double** cell_xyz,
 int mswm_mesh_get_domain(const mswm_mesh* m, int* spherical, double* radius,
                          double* width, double* height);
 
+/* Space-filling-curve cell order for the CUDA path's internal layout
+ * (mswm_cuda_create's cell_order): cell_order[k] = id of the k-th cell
+ * along a Hilbert curve (planar) or per-cube-face Hilbert curves (sphere). */
+int mswm_mesh_locality_order(const mswm_mesh* m, int32_t* cell_order);
+
 #ifdef __cplusplus
 }
 #endif

@@ -127,6 +127,7 @@ def host() -> C.CDLL:
         lib.mswm_mesh_get_desc.argtypes = [C.c_void_p, C.POINTER(MeshDesc)]
         lib.mswm_mesh_get_geometry.argtypes = [C.c_void_p] + [C.POINTER(f64p)] * 4
         lib.mswm_mesh_get_domain.argtypes = [C.c_void_p, C.POINTER(C.c_int), f64p, f64p, f64p]
+        lib.mswm_mesh_locality_order.argtypes = [C.c_void_p, i32p]
         _host = lib
     return _host
 
@@ -138,7 +139,7 @@ def cuda() -> C.CDLL:
         lib = _load(CUDA_LIB)
         vp = C.c_void_p
         sig = {
-            "mswm_cuda_create": (C.c_int, [C.POINTER(MeshDesc), C.c_int, C.c_int, C.POINTER(vp)]),
+            "mswm_cuda_create": (C.c_int, [C.POINTER(MeshDesc), C.c_int, i32p, C.POINTER(vp)]),
             "mswm_cuda_destroy": (None, [vp]),
             "mswm_cuda_last_error": (C.c_char_p, [vp]),
             "mswm_cuda_set_fields": (C.c_int, [vp, f64p, f64p, C.c_double]),
@@ -160,6 +161,7 @@ def cuda() -> C.CDLL:
                                                  C.POINTER(C.c_int)]),
             "mswm_cuda_total_mass": (C.c_int, [vp, f64p]),
             "mswm_cuda_kernels_per_step": (C.c_int, [vp, i64p]),
+            "mswm_cuda_layout_info": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

@@ -204,12 +204,21 @@ class CudaContext:
     """One mswm_cuda_ctx: a mesh resident on one B200."""
 
     def __init__(self, mesh: Mesh, b, f_vertex, gravity: float = 9.80616, device: int = 0,
-                 order: int = 0):
+                 order="hilbert"):
+        """order: "hilbert" (space-filling-curve device layout, default),
+        "input" (the caller's numbering) or an explicit cell permutation.
+        Results are bitwise independent of it."""
         self.lib = _lib.cuda()
         self.mesh = mesh
         self._desc = mesh.desc()
+        if isinstance(order, str):
+            if order not in ("hilbert", "input"):
+                raise UsageError(f"unknown order '{order}'")
+            order = mesh.locality_order() if order == "hilbert" else None
+        self._order = None if order is None else np.ascontiguousarray(order, np.int32)
+        optr = _p(self._order, _lib.i32p) if self._order is not None else None
         handle = C.c_void_p()
-        rc = self.lib.mswm_cuda_create(C.byref(self._desc), device, order, C.byref(handle))
+        rc = self.lib.mswm_cuda_create(C.byref(self._desc), device, optr, C.byref(handle))
         if rc:
             _raise(rc, self.lib.mswm_cuda_last_error(None).decode())
         self.handle = handle
@@ -330,6 +339,11 @@ class CudaContext:
                                                     _p(ne, _lib.i64p), cap, C.byref(n)))
         k = min(n.value, cap)
         return np.array(ms[:k], np.float64), nc[:k], ne[:k]
+
+    def layout_info(self) -> dict:
+        rd, ident = C.c_int(0), C.c_int(0)
+        self._check(self.lib.mswm_cuda_layout_info(self.handle, C.byref(rd), C.byref(ident)))
+        return {"ring_derived_stencil": bool(rd.value), "input_order": bool(ident.value)}
 
     def kernels_per_step(self) -> int:
         n = C.c_int64(0)

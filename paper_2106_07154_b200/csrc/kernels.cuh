@@ -27,6 +27,8 @@ struct DevMesh {
   const uint8_t* __restrict__ c_deg;     // [nC]
   const uint8_t* __restrict__ c_sbits;   // [nC] bit j: cell_sign(ring edge j, i) < 0
   const double* __restrict__ c_area;     // [nC] A_i
+  const double* __restrict__ c_ratio;    // [deg_max][nC] kite_area / A_i per ring slot
+                                         // (ring-derived stencil; null = explicit tables)
   // vertices
   const int32_t* __restrict__ v_cell;    // [3][nV]
   const int32_t* __restrict__ v_edge;    // [3][nV]
@@ -41,6 +43,8 @@ struct DevMesh {
   const double* __restrict__ e_ld;       // l_e * d_e (the K product's first rounding)
   const double* __restrict__ e_dual;     // d_e
   const double* __restrict__ e_invd;     // 1.0 / d_e
+  const uint8_t* __restrict__ e_slots;   // ring-derived stencil: bits 0-2 slot of e in
+                                         // ring(c0), 3-5 in ring(c1), 6/7 anchor sign < 0
   const uint8_t* __restrict__ e_nst;     // stencil length
   const int32_t* __restrict__ e_sten;    // [sten_max][nE] edges_on_edge
   const double* __restrict__ e_coef;     // [sten_max][nE] w * (l_{e'} * (1/d_e))
@@ -122,10 +126,14 @@ __global__ void __launch_bounds__(kBlock) k_vertex_cell(DevMesh M, const double*
                                                        const int32_t* __restrict__ vlist, int32_t nv,
                                                        const int32_t* __restrict__ klist, int32_t nk,
                                                        double* __restrict__ pv, double* __restrict__ K,
-                                                       int32_t* __restrict__ dry) {
+                                                       int32_t* __restrict__ dry,
+                                                       const uint32_t* __restrict__ vmask) {
+  // Lists may be null (dense mode: element = thread index, superset of the
+  // closure); the dry check then consults the closure bitmask vmask so only
+  // closure vertices raise, as in operators.cpp:74-84.
   const int32_t t = blockIdx.x * kBlock + threadIdx.x;
   if (t < nv) {
-    const int32_t v = vlist[t];
+    const int32_t v = vlist ? vlist[t] : t;
     const uint8_t sb = M.v_sbits[v];
     double hv = 0.0, circ = 0.0;
 #pragma unroll
@@ -137,13 +145,13 @@ __global__ void __launch_bounds__(kBlock) k_vertex_cell(DevMesh M, const double*
     }
     hv /= M.v_area[v];
     if (!(hv > 0.0)) {
-      atomicMin(dry, M.v_orig[v]);
+      if (!vmask || ((vmask[v >> 5] >> (v & 31)) & 1u)) atomicMin(dry, M.v_orig[v]);
       pv[v] = 0.0;
       return;
     }
     pv[v] = (M.f[v] + circ / M.v_area[v]) / hv;
   } else if (t - nv < nk) {
-    const int32_t i = klist[t - nv];
+    const int32_t i = klist ? klist[t - nv] : t - nv;
     const int deg = M.c_deg[i];
     double acc = 0.0;
     for (int j = 0; j < deg; ++j) {
@@ -165,7 +173,7 @@ __global__ void __launch_bounds__(kBlock) k_edge_fq(DevMesh M, const double* __r
                                                    double2* __restrict__ FQ) {
   const int32_t t = blockIdx.x * kBlock + threadIdx.x;
   if (t >= ne) return;
-  const int32_t e = elist[t];
+  const int32_t e = elist ? elist[t] : t;
   const int2 c = M.e_cells[e];
   const int2 v = M.e_verts[e];
   const double F = 0.5 * (h[c.x] + h[c.y]) * u[e];
@@ -178,10 +186,13 @@ __global__ void __launch_bounds__(kBlock) k_edge_fq(DevMesh M, const double* __r
 // [0, nc) take cells, [nc, nc+ne) edges; lists are group-concatenated and
 // split into two epilogue segments at csplit / esplit.
 struct OutArgs {
-  const int32_t* clist;
+  const int32_t* clist;   // null: dense over all cells, membership from ckey
   int32_t nc, csplit;
-  const int32_t* elist;
+  const int32_t* elist;   // null: dense over all edges, membership from ekey
   int32_t ne, esplit;
+  const uint8_t* ckey;    // GroupBit index per cell (dense mode; null = all, segment 0)
+  const uint8_t* ekey;    // GroupBit index - 6 per edge
+  uint32_t mask;
   Op cop[2];
   Op eop[2];
 };
@@ -191,35 +202,95 @@ __global__ void __launch_bounds__(kBlock) k_out(DevMesh M, const double* __restr
                                                const double2* __restrict__ FQ, OutArgs a) {
   const int32_t t = blockIdx.x * kBlock + threadIdx.x;
   if (t < a.nc) {
-    const int32_t i = a.clist[t];
+    int32_t i;
+    int seg;
+    if (a.clist) {
+      i = a.clist[t];
+      seg = t < a.csplit ? 0 : 1;
+    } else {
+      i = t;
+      const int g = a.ckey ? a.ckey[i] : 0;
+      if (!((a.mask >> g) & 1u)) return;
+      seg = g <= 2 ? 0 : 1;
+    }
     const int deg = M.c_deg[i];
     const uint8_t sb = M.c_sbits[i];
     double acc = 0.0;
-    for (int j = 0; j < deg; ++j) {
-      const int32_t e = M.c_edge[j * M.nC + i];
-      const double l = M.e_len[e];
-      acc += ((sb >> j) & 1 ? -l : l) * FQ[e].x;
+#pragma unroll
+    for (int j = 0; j < kMaxDeg; ++j) {
+      if (j < deg) {
+        const int32_t e = M.c_edge[j * M.nC + i];
+        const double l = M.e_len[e];
+        acc += ((sb >> j) & 1 ? -l : l) * FQ[e].x;
+      }
     }
     const double dh = -acc / M.c_area[i];
-    apply_op(a.cop[t < a.csplit ? 0 : 1], i, dh);
+    apply_op(a.cop[seg], i, dh);
   } else if (t - a.nc < a.ne) {
     const int32_t q = t - a.nc;
-    const int32_t e = a.elist[q];
+    int32_t e;
+    int seg;
+    if (a.elist) {
+      e = a.elist[q];
+      seg = q < a.esplit ? 0 : 1;
+    } else {
+      e = q;
+      const int g = a.ekey ? a.ekey[e] : 0;
+      if (!((a.mask >> (6 + g)) & 1u)) return;
+      seg = g <= 1 ? 0 : 1;
+    }
     const double qt_e = FQ[e].y;
     const double inv_d = M.e_invd[e];
-    const int nst = M.e_nst[e];
-    double pvflux = 0.0;
-    for (int j = 0; j < nst; ++j) {
-      const int32_t e2 = M.e_sten[j * M.nE + e];
-      const double c = M.e_coef[j * M.nE + e];
-      const double2 fq = FQ[e2];
-      pvflux += c * fq.x * (0.5 * (qt_e + fq.y));
-    }
     const int2 cc = M.e_cells[e];
+    double pvflux = 0.0;
+    if (M.e_slots) {
+      // Ring-derived stencil (mesh_build.cpp:133-154 walk, weights
+      // :343-362): for each side, walk the cell's ring counterclockwise
+      // from just after e; w = (cell_sign * anchor) * (frac - 0.5) with
+      // frac the running sum of kite/A -- bitwise the stored edge_weight
+      // (verified at create), so the stencil tables never leave the chip.
+      const uint8_t sl = M.e_slots[e];
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const int32_t c = side ? cc.y : cc.x;
+        const int p = side ? ((sl >> 3) & 7) : (sl & 7);
+        const unsigned aneg = (sl >> (6 + side)) & 1u;
+        const int deg = M.c_deg[c];
+        const uint8_t sb = M.c_sbits[c];
+        double frac = 0.0;
+#pragma unroll
+        for (int k = 1; k < kMaxDeg; ++k) {
+          if (k < deg) {
+            int sp = p + k - 1;
+            if (sp >= deg) sp -= deg;
+            int s = p + k;
+            if (s >= deg) s -= deg;
+            frac += M.c_ratio[sp * M.nC + c];
+            const int32_t e2 = M.c_edge[s * M.nC + c];
+            const double x = frac - 0.5;
+            const double w = (((sb >> s) & 1u) ^ aneg) ? -x : x;
+            const double coef = w * (M.e_len[e2] * inv_d);
+            const double2 fq = FQ[e2];
+            pvflux += coef * fq.x * (0.5 * (qt_e + fq.y));
+          }
+        }
+      }
+    } else {
+      const int nst = M.e_nst[e];
+#pragma unroll
+      for (int j = 0; j < kMaxSten; ++j) {
+        if (j < nst) {
+          const int32_t e2 = M.e_sten[j * M.nE + e];
+          const double c = M.e_coef[j * M.nE + e];
+          const double2 fq = FQ[e2];
+          pvflux += c * fq.x * (0.5 * (qt_e + fq.y));
+        }
+      }
+    }
     const double psi_lo = M.g * (h[cc.x] + M.b[cc.x]) + K[cc.x];
     const double psi_hi = M.g * (h[cc.y] + M.b[cc.y]) + K[cc.y];
     const double du = -pvflux - (psi_lo - psi_hi) * inv_d;
-    apply_op(a.eop[q < a.esplit ? 0 : 1], e, du);
+    apply_op(a.eop[seg], e, du);
   }
 }
 
@@ -397,6 +468,18 @@ __global__ void k_union_key(int32_t n, const uint8_t* __restrict__ a, const uint
                             uint8_t* __restrict__ key) {
   const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) key[i] = (a[i] | b[i]) ? 0 : 0xFF;
+}
+
+// pack a 0/1 byte array into a bitmask
+__global__ void k_pack_bits(int32_t n, const uint8_t* __restrict__ a, uint32_t* __restrict__ bits) {
+  const int32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w * 32 >= n) return;
+  uint32_t x = 0;
+  for (int b = 0; b < 32; ++b) {
+    const int32_t i = w * 32 + b;
+    if (i < n && a[i]) x |= 1u << b;
+  }
+  bits[w] = x;
 }
 
 __global__ void k_flag_key(int32_t n, const uint8_t* __restrict__ a, uint8_t* __restrict__ key) {

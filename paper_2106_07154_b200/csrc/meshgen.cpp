@@ -547,9 +547,72 @@ mswm_mesh* build_sphere(int level, double radius) {
   return m;
 }
 
+// Hilbert index of (x, y) on an n x n grid (n a power of two).
+uint64_t hilbert2(uint32_t n, uint32_t x, uint32_t y) {
+  uint64_t d = 0;
+  for (uint32_t s = n / 2; s > 0; s /= 2) {
+    const uint32_t rx = (x & s) ? 1u : 0u, ry = (y & s) ? 1u : 0u;
+    d += uint64_t(s) * s * ((3u * rx) ^ ry);
+    if (ry == 0) {
+      if (rx == 1) {
+        x = n - 1 - x;
+        y = n - 1 - y;
+      }
+      std::swap(x, y);
+    }
+  }
+  return d;
+}
+
+// Space-filling-curve cell order: 2-D Hilbert on the plane; on the sphere a
+// Hilbert curve per cube face (faces visited so consecutive faces share an
+// edge).  Only the internal memory layout of the CUDA path depends on it.
+void locality_order(const mswm_mesh& m, int32_t* order) {
+  const uint32_t n = 1u << 20;
+  std::vector<std::pair<uint64_t, int32_t>> key(m.nC);
+  for (int32_t i = 0; i < m.nC; ++i) {
+    const double* p = &m.cell_xyz[3 * size_t(i)];
+    uint64_t k;
+    if (!m.spherical) {
+      const uint32_t x = uint32_t(std::min(double(n - 1), std::max(0.0, p[0] / m.width * n)));
+      const uint32_t y = uint32_t(std::min(double(n - 1), std::max(0.0, p[1] / m.height * n)));
+      k = hilbert2(n, x, y);
+    } else {
+      const double ax = std::fabs(p[0]), ay = std::fabs(p[1]), az = std::fabs(p[2]);
+      int face;
+      double u, v;
+      if (ax >= ay && ax >= az) {
+        face = p[0] > 0 ? 0 : 3;
+        u = p[1] / ax;
+        v = p[2] / ax;
+      } else if (ay >= az) {
+        face = p[1] > 0 ? 1 : 4;
+        u = p[2] / ay;
+        v = p[0] / ay;
+      } else {
+        face = p[2] > 0 ? 2 : 5;
+        u = p[0] / az;
+        v = p[1] / az;
+      }
+      const uint32_t x = uint32_t(std::min(double(n - 1), std::max(0.0, (u + 1.0) * 0.5 * n)));
+      const uint32_t y = uint32_t(std::min(double(n - 1), std::max(0.0, (v + 1.0) * 0.5 * n)));
+      k = (uint64_t(face) << 40) | hilbert2(n, x, y);
+    }
+    key[i] = {k, i};
+  }
+  std::sort(key.begin(), key.end());
+  for (int32_t k = 0; k < m.nC; ++k) order[k] = key[k].second;
+}
+
 }  // namespace
 
 extern "C" {
+
+int mswm_mesh_locality_order(const mswm_mesh* m, int32_t* cell_order) {
+  if (!m || !cell_order) return MSWM_E_USAGE;
+  locality_order(*m, cell_order);
+  return MSWM_OK;
+}
 
 const char* mswm_host_last_error(void) { return g_last_error.c_str(); }
 

@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <array>
 #include <climits>
+#include <cstdlib>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -98,6 +99,10 @@ struct MaskPlan {
   DArr<int32_t> own_cells, own_edges;  // storage when not aliasing the group buffer
   DArr<int32_t> vclos, kclos, eclos, fclos, qclos;
   int32_t nv = 0, nk = 0, nec = 0, nf = 0, nq = 0;
+  // dense launches (thread index = element id) when a set covers most of
+  // the mesh: no index-list traffic, perfectly coalesced own-element access
+  bool dense_v = false, dense_k = false, dense_fq = false, dense_out = false;
+  DArr<uint32_t> vmask;  // closure bitmask for the dense dry-vertex check
   std::vector<int32_t> host_cells, host_edges;  // original ids, same order as device lists
 };
 
@@ -119,8 +124,9 @@ struct mswm_cuda_ctx {
 
   // device mesh
   DArr<int32_t> c_edge, c_vert, c_nbr, v_cell, v_edge, v_orig, e_sten;
-  DArr<uint8_t> c_deg, c_sbits, v_sbits, e_nst;
-  DArr<double> c_area, v_kite, v_area, e_len, e_ld, e_dual, e_invd, e_coef, b, f;
+  DArr<uint8_t> c_deg, c_sbits, v_sbits, e_nst, e_slots;
+  DArr<double> c_area, c_ratio, v_kite, v_area, e_len, e_ld, e_dual, e_invd, e_coef, b, f;
+  bool ring_derived = false;
   DArr<int2> e_cells, e_verts;
   double gravity = 9.80616;
   bool have_fields = false;
@@ -144,6 +150,7 @@ struct mswm_cuda_ctx {
   int width = 1;
   DArr<uint8_t> cell_label, cell_sub, edge_label;
   DArr<int32_t> cell_groups, edge_groups;  // group-concatenated ascending lists
+  DArr<uint8_t> ckey, ekey;                // GroupBit index per cell / edge (-6)
   int64_t gsize[11] = {0};
   int64_t goff[11] = {0};  // offset of group g inside its buffer
   DArr<int32_t> all_cells, all_edges;  // identity lists (no regions)
@@ -195,6 +202,7 @@ struct mswm_cuda_ctx {
     M.c_deg = c_deg.p;
     M.c_sbits = c_sbits.p;
     M.c_area = c_area.p;
+    M.c_ratio = c_ratio.p;
     M.v_cell = v_cell.p;
     M.v_edge = v_edge.p;
     M.v_kite = v_kite.p;
@@ -208,6 +216,7 @@ struct mswm_cuda_ctx {
     M.e_dual = e_dual.p;
     M.e_invd = e_invd.p;
     M.e_nst = e_nst.p;
+    M.e_slots = ring_derived ? e_slots.p : nullptr;
     M.e_sten = e_sten.p;
     M.e_coef = e_coef.p;
     M.b = b.p;
@@ -298,7 +307,128 @@ std::vector<int64_t> compact(mswm_cuda_ctx* c, const uint8_t* d_key, int32_t n, 
 // ---------------------------------------------------------------------------
 // create
 
-void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d) {
+// Internal numbering.  Cells follow `cell_order` (a space-filling curve from
+// the caller, or the input order); edges are sorted by the internal ids of
+// their two cells (min, max) and vertices by their three, so every gather of
+// the kernels lands near the element that issues it.  Per-element
+// arithmetic does not depend on the numbering (slot orders, edge_cells
+// order and stencil order are carried verbatim), so results are bitwise
+// independent of it (SURVEY.md §0 finding 5).
+void make_orders(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell_order) {
+  const int32_t nC = d->n_cells, nE = d->n_edges, nV = d->n_vertices;
+  c->c_new2old.resize(nC);
+  c->e_new2old.resize(nE);
+  c->v_new2old.resize(nV);
+  if (!cell_order) {
+    std::iota(c->c_new2old.begin(), c->c_new2old.end(), 0);
+    std::iota(c->e_new2old.begin(), c->e_new2old.end(), 0);
+    std::iota(c->v_new2old.begin(), c->v_new2old.end(), 0);
+    c->c_old2new = c->c_new2old;
+    c->e_old2new = c->e_new2old;
+    c->v_old2new = c->v_new2old;
+    c->identity = true;
+    return;
+  }
+  c->c_old2new.assign(nC, -1);
+  for (int32_t k = 0; k < nC; ++k) {
+    const int32_t i = cell_order[k];
+    if (i < 0 || i >= nC || c->c_old2new[i] != -1)
+      throw Error(MSWM_E_USAGE, "cell_order is not a permutation of the cells");
+    c->c_old2new[i] = k;
+    c->c_new2old[k] = i;
+  }
+  const auto& r = c->c_old2new;
+  {
+    std::vector<std::pair<uint64_t, int32_t>> key(nE);
+    for (int32_t e = 0; e < nE; ++e) {
+      uint32_t a = uint32_t(r[d->edge_cells[2 * e]]), b = uint32_t(r[d->edge_cells[2 * e + 1]]);
+      if (a > b) std::swap(a, b);
+      key[e] = {(uint64_t(a) << 32) | b, e};
+    }
+    std::sort(key.begin(), key.end());
+    c->e_old2new.assign(nE, 0);
+    for (int32_t k = 0; k < nE; ++k) {
+      c->e_new2old[k] = key[k].second;
+      c->e_old2new[key[k].second] = k;
+    }
+  }
+  {
+    struct VK {
+      uint32_t a, b, cc;
+      int32_t v;
+    };
+    std::vector<VK> key(nV);
+    for (int32_t v = 0; v < nV; ++v) {
+      uint32_t x[3] = {uint32_t(r[d->vertex_cells[3 * v]]), uint32_t(r[d->vertex_cells[3 * v + 1]]),
+                       uint32_t(r[d->vertex_cells[3 * v + 2]])};
+      std::sort(x, x + 3);
+      key[v] = {x[0], x[1], x[2], v};
+    }
+    std::sort(key.begin(), key.end(), [](const VK& p, const VK& q) {
+      return std::tie(p.a, p.b, p.cc, p.v) < std::tie(q.a, q.b, q.cc, q.v);
+    });
+    c->v_old2new.assign(nV, 0);
+    for (int32_t k = 0; k < nV; ++k) {
+      c->v_new2old[k] = key[k].v;
+      c->v_old2new[key[k].v] = k;
+    }
+  }
+  c->identity = false;
+}
+
+// Is the caller's stencil the ring walk of mesh_build.cpp:133-154 with the
+// weight rule of :343-362?  If so (bitwise, every entry), the kernels
+// rebuild both from per-cell rows and the 120 B/edge stencil tables are not
+// needed.  Returns the per-cell kite/A rows and per-edge slot bytes.
+bool derive_ring_stencil(const mswm_mesh_desc* d, std::vector<double>& kite_of_slot,
+                         std::vector<uint8_t>& slots) {
+  const int32_t nC = d->n_cells, nE = d->n_edges;
+  const int32_t total = d->cell_offset[nC];
+  kite_of_slot.assign(total, 0.0);
+  // kite_area per ring slot from vertex_kite (mesh_build.cpp:330-341 inverted)
+  for (int32_t i = 0; i < nC; ++i)
+    for (int32_t j = d->cell_offset[i]; j < d->cell_offset[i + 1]; ++j) {
+      const int32_t v = d->cell_vertices[j];
+      int k = 0;
+      while (k < 3 && d->vertex_cells[3 * v + k] != i) ++k;
+      if (k == 3) return false;
+      kite_of_slot[j] = d->vertex_kite[3 * v + k];
+    }
+  slots.assign(nE, 0);
+  for (int32_t e = 0; e < nE; ++e) {
+    int pos = d->edge_edge_offset[e];
+    uint8_t sl = 0;
+    for (int side = 0; side < 2; ++side) {
+      const int32_t i = d->edge_cells[2 * e + side];
+      const int off = d->cell_offset[i], mm = d->cell_offset[i + 1] - off;
+      int p = 0;
+      while (p < mm && d->cell_edges[off + p] != e) ++p;
+      if (p == mm) return false;
+      const int32_t av = d->cell_vertices[off + p];
+      const double anchor = d->edge_vertices[2 * e] == av ? double(d->edge_vertex_sign[2 * e])
+                                                          : double(d->edge_vertex_sign[2 * e + 1]);
+      double frac = 0.0;
+      for (int k = 1; k < mm; ++k) {
+        frac += kite_of_slot[off + (p + k - 1) % mm] / d->cell_area[i];
+        const int32_t ep = d->cell_edges[off + (p + k) % mm];
+        const double cs = d->edge_cells[2 * ep] == i ? double(d->edge_cell_sign[2 * ep])
+                                                     : double(d->edge_cell_sign[2 * ep + 1]);
+        const double w = cs * anchor * (frac - 0.5);
+        if (pos >= d->edge_edge_offset[e + 1] || d->edge_edges[pos] != ep) return false;
+        if (std::memcmp(&w, &d->edge_weight[pos], 8) != 0) return false;
+        ++pos;
+      }
+      if (p > 7) return false;
+      sl |= uint8_t(p << (3 * side));
+      if (anchor < 0) sl |= uint8_t(1u << (6 + side));
+    }
+    if (pos != d->edge_edge_offset[e + 1]) return false;
+    slots[e] = sl;
+  }
+  return true;
+}
+
+void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell_order) {
   const int32_t nC = d->n_cells, nE = d->n_edges, nV = d->n_vertices;
   if (nC <= 0 || nE <= 0 || nV <= 0) throw Error(MSWM_E_TOPOLOGY, "empty mesh");
   auto need = [](bool ok, const std::string& what) {
@@ -312,24 +442,6 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d) {
   c->nC = nC;
   c->nE = nE;
   c->nV = nV;
-  // Permutations (identity for MSWM_ORDER_INPUT).
-  c->c_new2old.resize(nC);
-  c->e_new2old.resize(nE);
-  c->v_new2old.resize(nV);
-  std::iota(c->c_new2old.begin(), c->c_new2old.end(), 0);
-  std::iota(c->e_new2old.begin(), c->e_new2old.end(), 0);
-  std::iota(c->v_new2old.begin(), c->v_new2old.end(), 0);
-  c->c_old2new = c->c_new2old;
-  c->e_old2new = c->e_new2old;
-  c->v_old2new = c->v_new2old;
-  c->identity = true;
-  const auto& cn = c->c_new2old;
-  const auto& en = c->e_new2old;
-  const auto& vn = c->v_new2old;
-  const auto& co = c->c_old2new;
-  const auto& eo = c->e_old2new;
-  const auto& vo = c->v_old2new;
-
   int deg_max = 0;
   for (int32_t i = 0; i < nC; ++i) {
     const int deg = d->cell_offset[i + 1] - d->cell_offset[i];
@@ -342,14 +454,37 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d) {
     need(n >= 0 && n <= kMaxSten, "edge " + std::to_string(e) + " stencil too long");
     sten_max = std::max(sten_max, n);
   }
+  for (int64_t k = 0; k < 2 * int64_t(nE); ++k)
+    need(d->edge_cells[k] >= 0 && d->edge_cells[k] < nC && d->edge_vertices[k] >= 0 &&
+             d->edge_vertices[k] < nV,
+         "edge table id out of range");
+  for (int64_t k = 0; k < 3 * int64_t(nV); ++k)
+    need(d->vertex_cells[k] >= 0 && d->vertex_cells[k] < nC && d->vertex_edges[k] >= 0 &&
+             d->vertex_edges[k] < nE,
+         "vertex table id out of range");
   c->deg_max = deg_max;
   c->sten_max = sten_max;
+  make_orders(c, d, cell_order);
+  const auto& cn = c->c_new2old;
+  const auto& en = c->e_new2old;
+  const auto& vn = c->v_new2old;
+  const auto& co = c->c_old2new;
+  const auto& eo = c->e_old2new;
+  const auto& vo = c->v_old2new;
+
+  std::vector<double> kite_of_slot;
+  std::vector<uint8_t> slots;
+  // MSWM_EXPLICIT_STENCIL=1 forces the explicit-table path (tests cover both).
+  const char* force = std::getenv("MSWM_EXPLICIT_STENCIL");
+  c->ring_derived = !(force && force[0] == '1') && derive_ring_stencil(d, kite_of_slot, slots);
 
   // cells
   std::vector<int32_t> c_edge(size_t(deg_max) * nC, 0), c_vert(size_t(deg_max) * nC, 0),
       c_nbr(size_t(deg_max) * nC, 0);
   std::vector<uint8_t> c_deg(nC), c_sbits(nC, 0);
   std::vector<double> c_area(nC);
+  std::vector<double> c_ratio;
+  if (c->ring_derived) c_ratio.assign(size_t(deg_max) * nC, 0.0);
   for (int32_t ni = 0; ni < nC; ++ni) {
     const int32_t i = cn[ni];
     const int off = d->cell_offset[i], deg = d->cell_offset[i + 1] - off;
@@ -363,8 +498,10 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d) {
       c_vert[size_t(j) * nC + ni] = vo[v];
       c_nbr[size_t(j) * nC + ni] = co[nb];
       // cell_sign(e, i) (mesh.hpp:89-92)
-      const int8_t s = d->edge_cells[2 * e] == i ? d->edge_cell_sign[2 * e] : d->edge_cell_sign[2 * e + 1];
-      if (s < 0) c_sbits[ni] |= uint8_t(1u << j);
+      const int8_t sg = d->edge_cells[2 * e] == i ? d->edge_cell_sign[2 * e] : d->edge_cell_sign[2 * e + 1];
+      if (sg < 0) c_sbits[ni] |= uint8_t(1u << j);
+      // operators / mesh_build.cpp:354: kite_area[slot] / cell_area[i]
+      if (c->ring_derived) c_ratio[size_t(j) * nC + ni] = kite_of_slot[off + j] / d->cell_area[i];
     }
   }
   c->h_cell_area.assign(d->cell_area, d->cell_area + nC);
@@ -378,36 +515,44 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d) {
     v_area[nv] = d->vertex_area[v];
     for (int k = 0; k < 3; ++k) {
       const int32_t cc = d->vertex_cells[3 * v + k], e = d->vertex_edges[3 * v + k];
-      need(cc >= 0 && cc < nC && e >= 0 && e < nE, "vertex table id out of range");
       v_cell[size_t(k) * nV + nv] = co[cc];
       v_edge[size_t(k) * nV + nv] = eo[e];
       v_kite[size_t(k) * nV + nv] = d->vertex_kite[3 * v + k];
       // vertex_sign(e, v) (mesh.hpp:93-96)
-      const int8_t s =
+      const int8_t sg =
           d->edge_vertices[2 * e] == v ? d->edge_vertex_sign[2 * e] : d->edge_vertex_sign[2 * e + 1];
-      if (s < 0) v_sbits[nv] |= uint8_t(1u << k);
+      if (sg < 0) v_sbits[nv] |= uint8_t(1u << k);
     }
   }
   // edges
   std::vector<int2> e_cells(nE), e_verts(nE);
   std::vector<double> e_len(nE), e_ld(nE), e_dual(nE), e_invd(nE);
-  std::vector<uint8_t> e_nst(nE);
-  std::vector<int32_t> e_sten(size_t(std::max(sten_max, 1)) * nE, 0);
-  std::vector<double> e_coef(size_t(std::max(sten_max, 1)) * nE, 0.0);
+  std::vector<uint8_t> e_nst, e_slots;
+  std::vector<int32_t> e_sten;
+  std::vector<double> e_coef;
+  if (c->ring_derived) {
+    e_slots.resize(nE);
+  } else {
+    e_nst.resize(nE);
+    e_sten.assign(size_t(std::max(sten_max, 1)) * nE, 0);
+    e_coef.assign(size_t(std::max(sten_max, 1)) * nE, 0.0);
+  }
   for (int32_t ne = 0; ne < nE; ++ne) {
     const int32_t e = en[ne];
     const int32_t c0 = d->edge_cells[2 * e], c1 = d->edge_cells[2 * e + 1];
     const int32_t v0 = d->edge_vertices[2 * e], v1 = d->edge_vertices[2 * e + 1];
-    need(c0 >= 0 && c0 < nC && c1 >= 0 && c1 < nC && v0 >= 0 && v0 < nV && v1 >= 0 && v1 < nV,
-         "edge table id out of range");
     e_cells[ne] = make_int2(co[c0], co[c1]);
     e_verts[ne] = make_int2(vo[v0], vo[v1]);
     const double l = d->edge_len[e], dd = d->edge_dual_len[e];
     e_len[ne] = l;
     e_dual[ne] = dd;
-    e_ld[ne] = l * dd;          // operators.cpp:70, first product
+    e_ld[ne] = l * dd;              // operators.cpp:70, first product
     const double inv_d = 1.0 / dd;  // operators.cpp:103
     e_invd[ne] = inv_d;
+    if (c->ring_derived) {
+      e_slots[ne] = slots[e];
+      continue;
+    }
     const int off = d->edge_edge_offset[e], n = d->edge_edge_offset[e + 1] - off;
     e_nst[ne] = uint8_t(n);
     for (int j = 0; j < n; ++j) {
@@ -426,6 +571,7 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d) {
   c->c_deg.upload(c_deg, s);
   c->c_sbits.upload(c_sbits, s);
   c->c_area.upload(c_area, s);
+  c->c_ratio.upload(c_ratio, s);
   c->v_cell.upload(v_cell, s);
   c->v_edge.upload(v_edge, s);
   c->v_orig.upload(v_orig, s);
@@ -439,6 +585,7 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d) {
   c->e_dual.upload(e_dual, s);
   c->e_invd.upload(e_invd, s);
   c->e_nst.upload(e_nst, s);
+  c->e_slots.upload(e_slots, s);
   c->e_sten.upload(e_sten, s);
   c->e_coef.upload(e_coef, s);
   CK(cudaStreamSynchronize(s));  // host vectors die here
@@ -580,6 +727,15 @@ MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
   p->nk = int32_t(compact(c, key.p, c->nC, 1, p->kclos)[0]);
   k_flag_key<<<nblk(c->nV), kBlock, 0, s>>>(c->nV, mv.p, key.p);
   p->nv = int32_t(compact(c, key.p, c->nV, 1, p->vclos)[0]);
+  p->dense_v = p->nv >= int64_t(c->nV) * 85 / 100;
+  p->dense_k = p->nk >= int64_t(c->nC) * 85 / 100;
+  p->dense_fq = p->nec >= int64_t(c->nE) * 85 / 100;
+  p->dense_out = int64_t(p->nc) + p->ne >= (int64_t(c->nC) + c->nE) / 2;
+  if (p->dense_v && p->nv < c->nV) {
+    p->vmask.alloc((size_t(c->nV) + 31) / 32);
+    k_pack_bits<<<nblk((int64_t(c->nV) + 31) / 32), kBlock, 0, s>>>(c->nV, mv.p, p->vmask.p);
+    CK(cudaGetLastError());
+  }
   // host copies of the output lists (original ids) for the eval ABI
   p->host_cells.resize(p->nc);
   p->host_edges.resize(p->ne);
@@ -622,27 +778,43 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
     rec->ne = p.ne;
     CK(cudaEventRecordWithFlags(rec->start, s, cudaEventRecordExternal));
   }
-  const int64_t na = int64_t(p.nv) + p.nk;
-  if (na > 0) {
-    k_vertex_cell<<<nblk(na), kBlock, 0, s>>>(M, h, u, p.vclos.p, p.nv, p.kclos.p, p.nk, c->pv.p,
-                                             c->K.p, c->dry_vertex.p);
+  const int32_t nv = p.dense_v ? c->nV : p.nv, nk = p.dense_k ? c->nC : p.nk;
+  const int64_t na = int64_t(nv) + nk;
+  if (p.nv + p.nk > 0) {
+    k_vertex_cell<<<nblk(na), kBlock, 0, s>>>(M, h, u, p.dense_v ? nullptr : p.vclos.p, nv,
+                                             p.dense_k ? nullptr : p.kclos.p, nk, c->pv.p, c->K.p,
+                                             c->dry_vertex.p, p.vmask.p);
     CK(cudaGetLastError());
     ++c->launches;
   }
   if (p.nec > 0) {
-    k_edge_fq<<<nblk(p.nec), kBlock, 0, s>>>(M, h, u, c->pv.p, p.eclos.p, p.nec, c->FQ.p);
+    const int32_t nfq = p.dense_fq ? c->nE : p.nec;
+    k_edge_fq<<<nblk(nfq), kBlock, 0, s>>>(M, h, u, c->pv.p, p.dense_fq ? nullptr : p.eclos.p, nfq,
+                                          c->FQ.p);
     CK(cudaGetLastError());
     ++c->launches;
   }
-  const int64_t nout = int64_t(p.nc) + p.ne;
-  if (nout > 0) {
+  if (int64_t(p.nc) + p.ne > 0) {
     OutArgs a;
-    a.clist = p.cells;
-    a.nc = p.nc;
-    a.csplit = p.csplit;
-    a.elist = p.edges;
-    a.ne = p.ne;
-    a.esplit = p.esplit;
+    a.mask = p.mask;
+    a.ckey = c->have_regions ? c->ckey.p : nullptr;
+    a.ekey = c->have_regions ? c->ekey.p : nullptr;
+    if (p.dense_out) {
+      a.clist = nullptr;
+      a.nc = c->nC;
+      a.csplit = 0;
+      a.elist = nullptr;
+      a.ne = c->nE;
+      a.esplit = 0;
+    } else {
+      a.clist = p.cells;
+      a.nc = p.nc;
+      a.csplit = p.csplit;
+      a.elist = p.edges;
+      a.ne = p.ne;
+      a.esplit = p.esplit;
+    }
+    const int64_t nout = int64_t(a.nc) + a.ne;
     a.cop[0] = cop[0];
     a.cop[1] = cop[1];
     a.eop[0] = eop[0];
@@ -1032,7 +1204,8 @@ int set_regions_impl(mswm_cuda_ctx* c, const uint8_t* fine_mask, int width, uint
   k_cell_labels<<<nblk(nC), kBlock, 0, s>>>(nC, dist.p, width, c->cell_label.p, c->cell_sub.p);
   k_underline<<<nblk(nC), kBlock, 0, s>>>(M, c->c_nbr.p, c->cell_label.p, c->cell_sub.p, 1);
   k_underline<<<nblk(nC), kBlock, 0, s>>>(M, c->c_nbr.p, c->cell_label.p, c->cell_sub.p, 2);
-  DArr<uint8_t> ckey, ekey;
+  DArr<uint8_t>& ckey = c->ckey;
+  DArr<uint8_t>& ekey = c->ekey;
   ckey.alloc(nC);
   ekey.alloc(nE);
   k_edge_labels_and_keys<<<nblk(std::max(nC, nE)), kBlock, 0, s>>>(M, c->cell_label.p, c->cell_sub.p,
@@ -1101,18 +1274,17 @@ int guard(mswm_cuda_ctx* c, F&& f) {
 
 extern "C" {
 
-int mswm_cuda_create(const mswm_mesh_desc* mesh, int device, int order, mswm_cuda_ctx** out) {
+int mswm_cuda_create(const mswm_mesh_desc* mesh, int device, const int32_t* cell_order,
+                     mswm_cuda_ctx** out) {
   if (!out) return MSWM_E_USAGE;
   *out = nullptr;
   auto c = std::make_unique<mswm_cuda_ctx>();
   try {
     if (!mesh) throw Error(MSWM_E_USAGE, "null mesh descriptor");
-    if (order != MSWM_ORDER_INPUT && order != MSWM_ORDER_HILBERT)
-      throw Error(MSWM_E_USAGE, "unknown ordering policy");
     c->device = device;
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    build_tables(c.get(), mesh);
+    build_tables(c.get(), mesh, cell_order);
   } catch (const Error& e) {
     g_create_error = e.what();
     return e.status;
@@ -1367,6 +1539,13 @@ int mswm_cuda_eval_profile(mswm_cuda_ctx* c, float* eval_ms, int64_t* out_cells,
     }
     return int(MSWM_OK);
   });
+}
+
+int mswm_cuda_layout_info(const mswm_cuda_ctx* c, int* ring_derived, int* identity_order) {
+  if (!c) return MSWM_E_USAGE;
+  if (ring_derived) *ring_derived = c->ring_derived ? 1 : 0;
+  if (identity_order) *identity_order = c->identity ? 1 : 0;
+  return MSWM_OK;
 }
 
 int mswm_cuda_kernels_per_step(mswm_cuda_ctx* c, int64_t* n) {

@@ -83,6 +83,15 @@ class Mesh:
         """Doubly periodic hexagonal mesh (nx*ny cells, centre spacing dc)."""
         return cls._from_host(_lib.host().mswm_mesh_planar_hex(nx, ny, dc))
 
+    def locality_order(self) -> np.ndarray:
+        """Hilbert-curve cell order for the device layout (host library)."""
+        owner = self._owner
+        if isinstance(owner, _HostMesh):
+            out = np.zeros(self.n_cells, np.int32)
+            _lib.host().mswm_mesh_locality_order(owner.handle, _lib.as_ptr(out, _lib.i32p))
+            return out
+        return hilbert_order_py(self)
+
     # -- boundary ----------------------------------------------------------
     def desc(self) -> _lib.MeshDesc:
         d = _lib.MeshDesc()
@@ -127,6 +136,19 @@ class Mesh:
     def total_mass(self, h: np.ndarray) -> float:
         """harness.cpp:99-105 (sequential sum in id order)."""
         return float(sum_in_order(self.tables["cell_area"] * h))
+
+
+def hilbert_order_py(mesh: "Mesh") -> np.ndarray:
+    """Coarse locality order for meshes not built by the host library:
+    sort cells by a 3-D Morton key of their positions."""
+    p = np.asarray(mesh.cell_xyz, np.float64)
+    lo, hi = p.min(0), p.max(0)
+    q = ((p - lo) / np.maximum(hi - lo, 1e-300) * 1023).astype(np.uint64)
+    key = np.zeros(len(p), np.uint64)
+    for b in range(10):
+        for a in range(3):
+            key |= ((q[:, a] >> np.uint64(b)) & np.uint64(1)) << np.uint64(3 * b + a)
+    return np.argsort(key, kind="stable").astype(np.int32)
 
 
 def sum_in_order(x: np.ndarray) -> float:

@@ -247,3 +247,44 @@ def test_stepper_drop_in_interface():
     CudaStepper(ctx).step(st, SchemeConfig(Scheme.LTS3, wl.dt, wl.M))
     h_ref, u_ref, _ = o.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, wl.M, 1)
     assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
+
+
+@pytest.mark.parametrize("explicit", [False, True])
+def test_layouts_are_bitwise_equivalent(explicit, monkeypatch):
+    """Results are independent of the device numbering (input, Hilbert,
+    random) and of the stencil storage (ring-derived vs explicit tables)."""
+    if explicit:
+        monkeypatch.setenv("MSWM_EXPLICIT_STENCIL", "1")
+    wl = W.small_sphere(5, seed=13, cap_deg=20.0)
+    o = _oracle_for(wl)
+    h_ref, u_ref, _ = o.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, wl.M, 4)
+    rng = np.random.default_rng(0)
+    for order in ["input", "hilbert", rng.permutation(wl.mesh.n_cells).astype(np.int32)]:
+        ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order)
+        info = ctx.layout_info()
+        assert info["ring_derived_stencil"] == (not explicit)
+        ctx.make_regions(wl.fine_mask, wl.width)
+        for a, b in zip(ctx.regions.groups, o.groups()):
+            assert np.array_equal(a, b)
+        for mask in LTS3_MASKS:
+            for kind in range(4):
+                o_dh = np.zeros(wl.mesh.n_cells)
+                o_du = np.zeros(wl.mesh.n_edges)
+                o.eval(wl.h, wl.u, mask, o_dh, o_du)
+                assert np.array_equal(ctx.closure(mask, kind), np.sort(o.last_closure(kind)))
+        ctx.upload(State(wl.h, wl.u, 0.0))
+        ctx.advance(Scheme.LTS3, wl.dt, wl.M, 4)
+        st = ctx.download()
+        assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref), str(order)[:20]
+
+
+def test_planar_ring_derived_and_rk4_full_mesh():
+    wl = W.config1(n_steps=3)
+    o = _oracle_for(wl)
+    ctx = _ctx(wl.mesh, wl.b, wl.f, wl.gravity, wl.fine_mask)
+    assert ctx.layout_info() == {"ring_derived_stencil": True, "input_order": False}
+    h_ref, u_ref, _ = o.step(int(Scheme.RK4), wl.h, wl.u, 0.0, wl.dt / 4, 1, 5)
+    ctx.upload(State(wl.h, wl.u, 0.0))
+    ctx.advance(Scheme.RK4, wl.dt / 4, 1, 5)
+    st = ctx.download()
+    assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
