@@ -352,6 +352,19 @@ __global__ void k_save_predict(const int32_t* __restrict__ clist, int32_t nc, in
 
 __global__ void k_step_counter(int64_t* ctr) { ++*ctr; }
 
+// Boundary permutations between the caller's numbering and the internal one.
+__global__ void k_gather_perm(int32_t n, const int32_t* __restrict__ n2o,
+                              const double* __restrict__ src, double* __restrict__ dst) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[n2o[i]];
+}
+__global__ void k_scatter_perm(int32_t n, const int32_t* __restrict__ n2o,
+                               const double* __restrict__ src, double* __restrict__ dst) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[n2o[i]] = src[i];
+}
+
+
 // ---------------------------------------------------------------------------
 // Region classification (regions.cpp:14-162) on device.
 

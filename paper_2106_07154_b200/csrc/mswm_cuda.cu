@@ -137,6 +137,8 @@ struct mswm_cuda_ctx {
   DArr<double> Dh, Du;              // eval ABI outputs
   DArr<double> pv, K;
   DArr<double2> FQ;
+  DArr<int32_t> d_c_n2o, d_e_n2o;  // internal -> original ids (device permutes)
+  DArr<double> io_h, io_u;          // staging for permuted uploads / downloads
   double time = 0.0;
   DArr<int32_t> dry_vertex;
   DArr<unsigned long long> dry_step;
@@ -249,16 +251,33 @@ std::vector<T> to_internal(const mswm_cuda_ctx* c, const T* src, const std::vect
 }
 
 // Upload an original-order array into a device buffer in internal order.
+// Cell and edge fields are permuted on the device (H2D into a staging
+// buffer, then a gather kernel); vertex fields (set once) on the host.
 void upload_field(mswm_cuda_ctx* c, DArr<double>& dst, const double* src,
                   const std::vector<int32_t>& n2o, size_t n) {
   if (dst.n != n) dst.alloc(n);
   if (c->identity) {
     CK(cudaMemcpyAsync(dst.p, src, n * 8, cudaMemcpyHostToDevice, c->stream));
-  } else {
-    std::vector<double> tmp = to_internal(c, src, n2o, n);
-    CK(cudaMemcpyAsync(dst.p, tmp.data(), n * 8, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    return;
   }
+  DArr<double>* stage = nullptr;
+  const int32_t* perm = nullptr;
+  if (&n2o == &c->c_new2old) {
+    stage = &c->io_h;
+    perm = c->d_c_n2o.p;
+  } else if (&n2o == &c->e_new2old) {
+    stage = &c->io_u;
+    perm = c->d_e_n2o.p;
+  }
+  if (stage) {
+    CK(cudaMemcpyAsync(stage->p, src, n * 8, cudaMemcpyHostToDevice, c->stream));
+    k_gather_perm<<<nblk(int64_t(n)), kBlock, 0, c->stream>>>(int32_t(n), perm, stage->p, dst.p);
+    CK(cudaGetLastError());
+    return;
+  }
+  std::vector<double> tmp = to_internal(c, src, n2o, n);
+  CK(cudaMemcpyAsync(dst.p, tmp.data(), n * 8, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
 }
 
 void download_field(mswm_cuda_ctx* c, const DArr<double>& src, double* dst,
@@ -266,12 +285,15 @@ void download_field(mswm_cuda_ctx* c, const DArr<double>& src, double* dst,
   if (c->identity) {
     CK(cudaMemcpyAsync(dst, src.p, n * 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-  } else {
-    std::vector<double> tmp(n);
-    CK(cudaMemcpyAsync(tmp.data(), src.p, n * 8, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    for (size_t i = 0; i < n; ++i) dst[n2o[i]] = tmp[i];
+    return;
   }
+  const bool cells = &n2o == &c->c_new2old;
+  DArr<double>& stage = cells ? c->io_h : c->io_u;
+  const int32_t* perm = cells ? c->d_c_n2o.p : c->d_e_n2o.p;
+  k_scatter_perm<<<nblk(int64_t(n)), kBlock, 0, c->stream>>>(int32_t(n), perm, src.p, stage.p);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(dst, stage.p, n * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
 }
 
 // Order-preserving compaction of key[0..n) into G ascending groups.
@@ -474,9 +496,12 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
 
   std::vector<double> kite_of_slot;
   std::vector<uint8_t> slots;
-  // MSWM_EXPLICIT_STENCIL=1 forces the explicit-table path (tests cover both).
-  const char* force = std::getenv("MSWM_EXPLICIT_STENCIL");
-  c->ring_derived = !(force && force[0] == '1') && derive_ring_stencil(d, kite_of_slot, slots);
+  // The explicit-table path is the default: on the Hilbert layout its
+  // coalesced stencil streams beat the L1-gather-bound ring walk (profiles/
+  // r1_v2_*).  MSWM_RING_DERIVED=1 selects the ring-derived path when the
+  // mesh qualifies (tests cover both).
+  const char* want = std::getenv("MSWM_RING_DERIVED");
+  c->ring_derived = (want && want[0] == '1') && derive_ring_stencil(d, kite_of_slot, slots);
 
   // cells
   std::vector<int32_t> c_edge(size_t(deg_max) * nC, 0), c_vert(size_t(deg_max) * nC, 0),
@@ -500,7 +525,7 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
       // cell_sign(e, i) (mesh.hpp:89-92)
       const int8_t sg = d->edge_cells[2 * e] == i ? d->edge_cell_sign[2 * e] : d->edge_cell_sign[2 * e + 1];
       if (sg < 0) c_sbits[ni] |= uint8_t(1u << j);
-      // operators / mesh_build.cpp:354: kite_area[slot] / cell_area[i]
+      // mesh_build.cpp:354: kite_area[slot] / cell_area[i]
       if (c->ring_derived) c_ratio[size_t(j) * nC + ni] = kite_of_slot[off + j] / d->cell_area[i];
     }
   }
@@ -607,6 +632,13 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   c->pv.zero(s);
   c->FQ.alloc(nE);
   c->FQ.zero(s);
+  if (!c->identity) {
+    c->d_c_n2o.upload(c->c_new2old, s);
+    c->d_e_n2o.upload(c->e_new2old, s);
+    c->io_h.alloc(nC);
+    c->io_u.alloc(nE);
+    CK(cudaStreamSynchronize(s));
+  }
   c->b.alloc(nC);
   c->b.zero(s);
   c->f.alloc(nV);
