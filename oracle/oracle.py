@@ -72,6 +72,7 @@ def ref() -> C.CDLL:
             "ref_regions_validate": (C.c_int, [vp, vp]),
             "ref_eval_create": (vp, [vp, vp, f64p, f64p, C.c_double, C.c_int, C.c_uint64] + E),
             "ref_eval_free": (None, [vp]),
+            "ref_cuda_eval_create": (vp, [vp, vp, f64p, f64p, C.c_double, C.c_int] + E),
             "ref_eval": (C.c_int, [vp, f64p, f64p, C.c_uint, f64p, f64p] + E
                          + [C.POINTER(C.c_int)]),
             "ref_closure": (C.c_int, [vp, f64p, f64p, C.c_uint, C.c_int, i32p, i64p] + E),
@@ -224,6 +225,22 @@ class RefEvaluator:
             raise OracleError(1, buf.value.decode())
         self.mesh, self.regions = mesh, regions
         self.stepper = None
+
+    @classmethod
+    def cuda(cls, mesh: RefMesh, regions: RefRegions | None, b, f, gravity, device=0):
+        """The reference's evaluator slot filled with mswm::CudaEvaluator
+        (oracle/drop_in_evaluator.hpp) -- the C++ drop-in over the C ABI."""
+        obj = cls.__new__(cls)
+        obj.b = np.ascontiguousarray(b, np.float64)
+        obj.f = np.ascontiguousarray(f, np.float64)
+        buf = _err()
+        obj.handle = ref().ref_cuda_eval_create(mesh.handle, regions.handle if regions else None,
+                                                _p(obj.b, f64p), _p(obj.f, f64p), gravity, device,
+                                                buf, ERRLEN)
+        if not obj.handle:
+            raise OracleError(5, buf.value.decode())
+        obj.mesh, obj.regions, obj.stepper = mesh, regions, None
+        return obj
 
     def __del__(self):
         if getattr(self, "stepper", None):

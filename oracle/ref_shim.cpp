@@ -29,6 +29,7 @@
 #include "mswm/rank_pool.hpp"
 #include "mswm/regions.hpp"
 #include "mswm_cuda.h"
+#include "drop_in_evaluator.hpp"
 
 using namespace mswm;
 
@@ -319,6 +320,28 @@ void* ref_eval_create(void* mp, void* rp, const double* b, const double* f, doub
 }
 
 void ref_eval_free(void* e) { delete static_cast<Evaluator*>(e); }
+
+// The drop-in: the reference's own Stepper driving the GPU through
+// mswm::CudaEvaluator (drop_in_evaluator.hpp) -- one C-ABI eval() per stage.
+void* ref_cuda_eval_create(void* mp, void* rp, const double* b, const double* f, double gravity,
+                           int device, char* err, int errlen) {
+  auto* m = static_cast<VoronoiMesh*>(mp);
+  auto* r = static_cast<RegionMap*>(rp);
+  Evaluator* out = nullptr;
+  guarded(err, errlen, nullptr, [&] {
+    auto ev = std::make_unique<Evaluator>();
+    ev->mesh = m;
+    ev->map = r;
+    ev->b = CellField(m->n_cells);
+    ev->f = VertexField(m->n_vertices);
+    std::copy(b, b + m->n_cells, ev->b.data.begin());
+    std::copy(f, f + m->n_vertices, ev->f.data.begin());
+    ev->gravity = gravity;
+    ev->ev = std::make_unique<CudaEvaluator>(*m, r, ev->b, ev->f, gravity, device);
+    out = ev.release();
+  });
+  return out;
+}
 
 int ref_eval(void* ep, const double* h, const double* u, unsigned mask, double* dh, double* du,
              char* err, int errlen, int* dry_vertex) {

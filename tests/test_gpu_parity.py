@@ -287,3 +287,24 @@ def test_planar_ring_derived_and_rk4_full_mesh():
     ctx.advance(Scheme.RK4, wl.dt / 4, 1, 5)
     st = ctx.download()
     assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
+
+
+def test_reference_stepper_drives_cuda_evaluator():
+    """The C++ drop-in: the reference's own Stepper::lts_step with its
+    evaluator slot filled by mswm::CudaEvaluator (oracle/drop_in_evaluator.hpp
+    over the C ABI) reproduces the reference with SerialEvaluator bitwise."""
+    from oracle.oracle import RefEvaluator, RefMesh, RefRegions, ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    wl = W.small_sphere(4, seed=17, cap_deg=30.0)
+    rm = RefMesh.from_mesh(wl.mesh)
+    rr = RefRegions(rm, wl.fine_mask, wl.width)
+    serial = RefEvaluator(rm, rr, wl.b, wl.f, wl.gravity)
+    cuda = RefEvaluator.cuda(rm, rr, wl.b, wl.f, wl.gravity)
+    for scheme, dt in [(Scheme.LTS3, wl.dt), (Scheme.RK4, wl.dt / wl.M)]:
+        h1, u1, _, _ = serial.step(int(scheme), wl.h, wl.u, 0.0, dt, wl.M, 3)
+        h2, u2, _, _ = cuda.step(int(scheme), wl.h, wl.u, 0.0, dt, wl.M, 3)
+        assert bits_equal(h1, h2) and bits_equal(u1, u2), scheme
+    c1, e1, _ = serial.ledger()
+    c2, e2, _ = cuda.ledger()
+    assert np.array_equal(c1, c2) and np.array_equal(e1, e2)
