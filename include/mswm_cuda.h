@@ -211,6 +211,48 @@ int mswm_cuda_kernels_per_step(mswm_cuda_ctx* ctx, int64_t* n);
  * to the reference). */
 int mswm_cuda_total_mass(mswm_cuda_ctx* ctx, double* mass);
 
+/* ---- multi-rank (one process per GPU, or an in-process group) ----------
+ * A rank context holds one rank's piece of the mesh (owned elements plus a
+ * two-hop halo, the reference's block plan, partition.cpp:307-403) in local
+ * numbering; outputs are the owned elements only and halo copies are
+ * refreshed before every evaluation (the device form of ThreadedEvaluator's
+ * per-eval copy-in, rank_pool.cpp:133-135). */
+
+/* Region labels from the global RegionMap (regions.hpp:27-29 values),
+ * indexed by local ids; outputs restricted to cell_owned / edge_owned
+ * (NULL = all).  Replaces mswm_cuda_set_regions on a rank context. */
+int mswm_cuda_set_labels(mswm_cuda_ctx* ctx, const uint8_t* cell_label,
+                         const uint8_t* cell_sublabel, const uint8_t* edge_label,
+                         const uint8_t* cell_owned, const uint8_t* edge_owned,
+                         int interface_width);
+
+/* Halo plan of rank `rank` of `n_ranks`: for each of n_peers peers,
+ * counts[4*j..4*j+3] = (#cells sent, #edges sent, #cells received,
+ * #edges received) and `ids` holds, peer after peer, those local ids in that
+ * order.  Both sides must list shared elements in the same order. */
+int mswm_cuda_set_halo(mswm_cuda_ctx* ctx, int rank, int n_ranks, int n_peers,
+                       const int32_t* peers, const int64_t* counts,
+                       const int32_t* ids);
+
+/* NCCL transport (one process per GPU): rank 0 creates a 128-byte unique id,
+ * the caller broadcasts it, every rank calls mswm_cuda_comm_init.  The
+ * exchange is NCCL point-to-point on the context's stream, captured in the
+ * step graph.  NCCL is resolved at run time (libnccl.so.2). */
+int mswm_cuda_nccl_unique_id(void* id_out /* 128 bytes */);
+int mswm_cuda_comm_init(mswm_cuda_ctx* ctx, const void* unique_id, int rank,
+                        int n_ranks);
+
+/* In-process group: n rank contexts on one device stepped in lockstep on
+ * one stream, halos exchanged by device copies (no kernel waits on another).
+ * members[r] must be rank r of n. */
+typedef struct mswm_cuda_group mswm_cuda_group;
+int mswm_cuda_group_create(mswm_cuda_ctx* const* members, int n,
+                           mswm_cuda_group** out);
+void mswm_cuda_group_destroy(mswm_cuda_group* group);
+int mswm_cuda_group_step(mswm_cuda_group* group, int scheme, double dt, int M,
+                         int64_t n_steps);
+const char* mswm_cuda_group_last_error(const mswm_cuda_group* group);
+
 #ifdef __cplusplus
 }
 #endif

@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kBlock) k_out(DevMesh M, const double* __restr
     } else {
       i = t;
       const int g = a.ckey ? a.ckey[i] : 0;
-      if (!((a.mask >> g) & 1u)) return;
+      if (g > 5 || !((a.mask >> g) & 1u)) return;  // 0xFF: not an output of this rank
       seg = g <= 2 ? 0 : 1;
     }
     const int deg = M.c_deg[i];
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kBlock) k_out(DevMesh M, const double* __restr
     } else {
       e = q;
       const int g = a.ekey ? a.ekey[e] : 0;
-      if (!((a.mask >> (6 + g)) & 1u)) return;
+      if (g > 4 || !((a.mask >> (6 + g)) & 1u)) return;
       seg = g <= 1 ? 0 : 1;
     }
     const double qt_e = FQ[e].y;
@@ -351,6 +351,26 @@ __global__ void k_save_predict(const int32_t* __restrict__ clist, int32_t nc, in
 }
 
 __global__ void k_step_counter(int64_t* ctr) { ++*ctr; }
+
+// Halo exchange pack/unpack: code >= 0 is a cell id (h array), code < 0 is
+// ~edge id (u array).
+__global__ void k_pack(int64_t n, const int32_t* __restrict__ code, const double* __restrict__ h,
+                       const double* __restrict__ u, double* __restrict__ buf) {
+  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int32_t c = code[k];
+  buf[k] = c >= 0 ? h[c] : u[~c];
+}
+__global__ void k_unpack(int64_t n, const int32_t* __restrict__ code, const double* __restrict__ buf,
+                         double* __restrict__ h, double* __restrict__ u) {
+  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int32_t c = code[k];
+  if (c >= 0)
+    h[c] = buf[k];
+  else
+    u[~c] = buf[k];
+}
 
 // Boundary permutations between the caller's numbering and the internal one.
 __global__ void k_gather_perm(int32_t n, const int32_t* __restrict__ n2o,

@@ -20,6 +20,8 @@
 // reference's expression, evaluated once.
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <array>
@@ -64,6 +66,20 @@ struct DArr {
   DArr() = default;
   DArr(const DArr&) = delete;
   DArr& operator=(const DArr&) = delete;
+  DArr(DArr&& o) noexcept : p(o.p), n(o.n) {
+    o.p = nullptr;
+    o.n = 0;
+  }
+  DArr& operator=(DArr&& o) noexcept {
+    if (this != &o) {
+      if (p) cudaFree(p);
+      p = o.p;
+      n = o.n;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
   ~DArr() {
     if (p) cudaFree(p);
   }
@@ -106,6 +122,65 @@ struct MaskPlan {
   std::vector<int32_t> host_cells, host_edges;  // original ids, same order as device lists
 };
 
+// Halo exchange plan of one rank: per peer slot, the owned values it sends
+// and the halo values it receives, as flat codes into the (h, u) arrays
+// (code >= 0: cell id, code < 0: ~edge id) and offsets into one send and one
+// receive buffer.
+struct Halo {
+  std::vector<int> peer;
+  std::vector<int64_t> soff, scnt, roff, rcnt;
+  DArr<int32_t> scode, rcode;
+  DArr<double> sbuf, rbuf;
+  int64_t ns = 0, nr = 0;
+  bool active() const { return !peer.empty(); }
+};
+
+// NCCL, resolved at run time from the process's libnccl.so.2 (the one torch
+// already loaded, if any), so the library has no link-time NCCL dependency.
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.why = "libnccl.so.2 not found";
+      return a;
+    }
+    auto sym = [&](const char* n) { return dlsym(h, n); };
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
+    a.Send = reinterpret_cast<decltype(a.Send)>(sym("ncclSend"));
+    a.Recv = reinterpret_cast<decltype(a.Recv)>(sym("ncclRecv"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.GroupStart && a.GroupEnd &&
+           a.Send && a.Recv && a.GetErrorString;
+    if (!a.ok) a.why = "libnccl.so.2 lacks the p2p API";
+    return a;
+  }();
+  if (!api.ok) throw Error(MSWM_E_NCCL, "NCCL unavailable: " + api.why);
+  return api;
+}
+
+void nccl_check(ncclResult_t r) {
+  if (r != ncclSuccess) throw Error(MSWM_E_NCCL, std::string("NCCL: ") + nccl().GetErrorString(r));
+}
+
 struct EvalRecord {
   cudaEvent_t start, stop;
   int64_t nc, ne;
@@ -116,6 +191,11 @@ struct EvalRecord {
 struct mswm_cuda_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t ls = nullptr;  // launch stream (== stream, or a group's stream while capturing)
+  // multi-rank: this context is rank `rank` of `n_ranks`, owning part of the mesh
+  int rank = 0, n_ranks = 1;
+  Halo halo;
+  ncclComm_t nccl_comm = nullptr;
   std::string last_error;
   int32_t nC = 0, nE = 0, nV = 0, deg_max = 0, sten_max = 0;
   bool identity = true;
@@ -190,6 +270,7 @@ struct mswm_cuda_ctx {
 
   ~mswm_cuda_ctx() {
     drop_graphs();
+    if (nccl_comm) nccl().CommDestroy(nccl_comm);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -797,7 +878,7 @@ Op op_none() {
 
 void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const double* u,
                  const Op cop[2], const Op eop[2]) {
-  cudaStream_t s = c->stream;
+  cudaStream_t s = c->ls;
   const DevMesh M = c->dev();
   EvalRecord* rec = nullptr;
   if (c->capture_records) {
@@ -948,98 +1029,169 @@ void launch_predict(mswm_cuda_ctx* c, int stage, int k, int M, double* hdst, dou
   lts3_coeffs(stage, k, M, w);
   const int64_t n = int64_t(L.nc1) + L.ne1;
   if (n == 0) return;
-  k_predict<<<nblk(n), kBlock, 0, c->stream>>>(L.c, L.nc1, L.e, L.ne1, w[0], w[1], w[2], c->S0h.p,
-                                               c->S1h.p, c->S2h.p, hdst, c->S0u.p, c->S1u.p,
-                                               c->S2u.p, udst);
+  k_predict<<<nblk(n), kBlock, 0, c->ls>>>(L.c, L.nc1, L.e, L.ne1, w[0], w[1], w[2], c->S0h.p,
+                                           c->S1h.p, c->S2h.p, hdst, c->S0u.p, c->S1u.p, c->S2u.p,
+                                           udst);
   CK(cudaGetLastError());
   ++c->launches;
 }
 
-// One LTS3 coarse step (see the file header for the aliasing argument).
-void enqueue_lts3(mswm_cuda_ctx* c, double dt, int M) {
+// ---------------------------------------------------------------------------
+// Halo exchange (multi-rank).  Before every evaluation each rank refreshes
+// the halo copies of the (h, u) stage arrays the evaluation reads -- the
+// device form of ThreadedEvaluator's per-eval copy-in (rank_pool.cpp:133-135).
+// Transports: NCCL point-to-point between processes (one GPU each), or, for
+// an in-process group of rank contexts on one device, device-to-device
+// copies.  Both are stream-ordered and capturable in the step graph.
+
+using ArrSel = DArr<double> mswm_cuda_ctx::*;
+
+void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us) {
+  bool any = false;
+  for (auto* c : cs) any |= c->halo.active();
+  if (!any) return;
+  for (auto* c : cs) {
+    Halo& x = c->halo;
+    if (x.ns > 0) {
+      k_pack<<<nblk(x.ns), kBlock, 0, c->ls>>>(x.ns, x.scode.p, (c->*hs).p, (c->*us).p, x.sbuf.p);
+      CK(cudaGetLastError());
+      ++c->launches;
+    }
+  }
+  if (cs.size() == 1) {
+    mswm_cuda_ctx* c = cs[0];
+    Halo& x = c->halo;
+    if (!c->nccl_comm) throw Error(MSWM_E_USAGE, "halo set but no communicator (mswm_cuda_comm_init)");
+    nccl_check(nccl().GroupStart());
+    for (size_t j = 0; j < x.peer.size(); ++j) {
+      if (x.scnt[j])
+        nccl_check(nccl().Send(x.sbuf.p + x.soff[j], size_t(x.scnt[j]), ncclFloat64, x.peer[j],
+                               c->nccl_comm, c->ls));
+      if (x.rcnt[j])
+        nccl_check(nccl().Recv(x.rbuf.p + x.roff[j], size_t(x.rcnt[j]), ncclFloat64, x.peer[j],
+                               c->nccl_comm, c->ls));
+    }
+    nccl_check(nccl().GroupEnd());
+  } else {
+    // in-process group: member index == rank
+    for (auto* c : cs) {
+      Halo& x = c->halo;
+      for (size_t j = 0; j < x.peer.size(); ++j) {
+        if (!x.rcnt[j]) continue;
+        mswm_cuda_ctx* src = cs[x.peer[j]];
+        const Halo& y = src->halo;
+        size_t k = 0;
+        while (k < y.peer.size() && y.peer[k] != c->rank) ++k;
+        if (k == y.peer.size() || y.scnt[k] != x.rcnt[j])
+          throw Error(MSWM_E_USAGE, "inconsistent halo plans between ranks " +
+                                        std::to_string(c->rank) + " and " + std::to_string(x.peer[j]));
+        CK(cudaMemcpyAsync(x.rbuf.p + x.roff[j], y.sbuf.p + y.soff[k], size_t(x.rcnt[j]) * 8,
+                           cudaMemcpyDeviceToDevice, c->ls));
+      }
+    }
+  }
+  for (auto* c : cs) {
+    Halo& x = c->halo;
+    if (x.nr > 0) {
+      k_unpack<<<nblk(x.nr), kBlock, 0, c->ls>>>(x.nr, x.rcode.p, x.rbuf.p, (c->*hs).p, (c->*us).p);
+      CK(cudaGetLastError());
+      ++c->launches;
+    }
+  }
+}
+
+// One LTS3 coarse step (see the file header for the aliasing argument) for
+// every rank context of the executor.
+void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
   const double delta = dt / M;
-  double *H = c->H.p, *U = c->U.p, *H1 = c->H1.p, *U1 = c->U1.p, *H2 = c->H2.p, *U2 = c->U2.p;
-  MaskPlan& p1 = plan_for(c, kMaskStep1);
-  MaskPlan& p2 = plan_for(c, kMaskIfCoarse);
-  MaskPlan& ps = plan_for(c, kMaskSub);
-  MaskPlan& p4 = plan_for(c, kMaskCoarseOnly);
-  k_step_counter<<<1, 1, 0, c->stream>>>(c->step_ctr.p);
+  const double third = 1.0 / 3.0, two3 = 2.0 / 3.0;
+  using C = mswm_cuda_ctx;
   // Step 1 (:483-487): h1 = h_old + dt*dh on UF1 u UF2 u I1 u I2 u C.
-  {
+  exchange(cs, &C::H, &C::U);
+  for (auto* c : cs) {
+    double *H = c->H.p, *U = c->U.p, *H1 = c->H1.p, *U1 = c->U1.p;
     Op co[2] = {mk_op(OP_EULER, H1, H, dt), mk_op(OP_EULER, H1, H, dt)};
     Op eo[2] = {mk_op(OP_EULER, U1, U, dt), mk_op(OP_EULER, U1, U, dt)};
-    launch_eval(c, p1, H, U, co, eo);
+    launch_eval(c, plan_for(c, kMaskStep1), H, U, co, eo);
   }
   // Step 2 (:491-500): h2 = 0.75 h_old + 0.25 h1 + (0.25 dt) dh on I u C.
-  {
+  exchange(cs, &C::H1, &C::U1);
+  for (auto* c : cs) {
+    double *H = c->H.p, *U = c->U.p, *H1 = c->H1.p, *U1 = c->U1.p, *H2 = c->H2.p, *U2 = c->U2.p;
     const double cr = 0.25 * dt;
     Op co[2] = {mk_op(OP_WCOMB, H2, H, 0.75, H1, 0.25, cr), mk_op(OP_WCOMB, H2, H, 0.75, H1, 0.25, cr)};
     Op eo[2] = {mk_op(OP_WCOMB, U2, U, 0.75, U1, 0.25, cr), mk_op(OP_WCOMB, U2, U, 0.75, U1, 0.25, cr)};
-    launch_eval(c, p2, H1, U1, co, eo);
+    launch_eval(c, plan_for(c, kMaskIfCoarse), H1, U1, co, eo);
   }
   // Substep prologue: save I1 u I2 old values, I1 stage values, predict
   // stage 1 of substep 0 into the state (ha == state).
-  {
+  for (auto* c : cs) {
     const IfLists L = if_lists(c);
     double w[3];
     lts3_coeffs(1, 0, M, w);
     const int64_t n = int64_t(L.nc) + L.ne;
     if (n > 0) {
-      k_save_predict<<<nblk(n), kBlock, 0, c->stream>>>(
-          L.c, L.nc, L.nc1, L.e, L.ne, L.ne1, w[0], w[1], w[2], H, H1, H2, c->S0h.p, c->S1h.p,
-          c->S2h.p, U, U1, U2, c->S0u.p, c->S1u.p, c->S2u.p);
+      k_save_predict<<<nblk(n), kBlock, 0, c->ls>>>(
+          L.c, L.nc, L.nc1, L.e, L.ne, L.ne1, w[0], w[1], w[2], c->H.p, c->H1.p, c->H2.p, c->S0h.p,
+          c->S1h.p, c->S2h.p, c->U.p, c->U1.p, c->U2.p, c->S0u.p, c->S1u.p, c->S2u.p);
       CK(cudaGetLastError());
       ++c->launches;
     }
   }
-  const double third = 1.0 / 3.0, two3 = 2.0 / 3.0;
   for (int k = 0; k < M; ++k) {
     const int first = k == 0;
     // stage 1: fine hb = ha + delta*d; interfaces acc1 += d   (:521-531)
-    if (k > 0) launch_predict(c, 1, k, M, H, U);
-    {
-      Op co[2] = {mk_op(OP_EULER, H1, H, delta), mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0,
-                                                       c->A1h.p, first)};
-      Op eo[2] = {mk_op(OP_EULER, U1, U, delta), mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0,
-                                                       c->A1u.p, first)};
-      launch_eval(c, ps, H, U, co, eo);
+    if (k > 0)
+      for (auto* c : cs) launch_predict(c, 1, k, M, c->H.p, c->U.p);
+    exchange(cs, &C::H, &C::U);
+    for (auto* c : cs) {
+      Op co[2] = {mk_op(OP_EULER, c->H1.p, c->H.p, delta),
+                  mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A1h.p, first)};
+      Op eo[2] = {mk_op(OP_EULER, c->U1.p, c->U.p, delta),
+                  mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A1u.p, first)};
+      launch_eval(c, plan_for(c, kMaskSub), c->H.p, c->U.p, co, eo);
     }
     // stage 2: fine hc = 0.75 ha + 0.25 hb + (0.25 delta) d; acc2 += d   (:532-541)
-    launch_predict(c, 2, k, M, H1, U1);
-    {
+    for (auto* c : cs) launch_predict(c, 2, k, M, c->H1.p, c->U1.p);
+    exchange(cs, &C::H1, &C::U1);
+    for (auto* c : cs) {
       const double cr = 0.25 * delta;
-      Op co[2] = {mk_op(OP_WCOMB, H2, H, 0.75, H1, 0.25, cr),
+      Op co[2] = {mk_op(OP_WCOMB, c->H2.p, c->H.p, 0.75, c->H1.p, 0.25, cr),
                   mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A2h.p, first)};
-      Op eo[2] = {mk_op(OP_WCOMB, U2, U, 0.75, U1, 0.25, cr),
+      Op eo[2] = {mk_op(OP_WCOMB, c->U2.p, c->U.p, 0.75, c->U1.p, 0.25, cr),
                   mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A2u.p, first)};
-      launch_eval(c, ps, H1, U1, co, eo);
+      launch_eval(c, plan_for(c, kMaskSub), c->H1.p, c->U1.p, co, eo);
     }
     // stage 3: fine ha = 1/3 ha + 2/3 hc + (2/3 delta) d; acc3 += d, and on
     // the last substep the interface correction (:542-553, :231-274).
-    launch_predict(c, 3, k, M, H2, U2);
-    {
+    for (auto* c : cs) launch_predict(c, 3, k, M, c->H2.p, c->U2.p);
+    exchange(cs, &C::H2, &C::U2);
+    for (auto* c : cs) {
       const double cr = two3 * delta;
       Op co[2], eo[2];
-      co[0] = mk_op(OP_WCOMB, H, H, third, H2, two3, cr);
-      eo[0] = mk_op(OP_WCOMB, U, U, third, U2, two3, cr);
+      co[0] = mk_op(OP_WCOMB, c->H.p, c->H.p, third, c->H2.p, two3, cr);
+      eo[0] = mk_op(OP_WCOMB, c->U.p, c->U.p, third, c->U2.p, two3, cr);
       if (k < M - 1) {
         co[1] = mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A3h.p, first);
         eo[1] = mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A3u.p, first);
       } else {
-        co[1] = mk_op(OP_ACC_CORR, H, c->S0h.p, delta, nullptr, 1.0 / 6.0, two3, c->A3h.p, first,
-                      c->A1h.p, c->A2h.p);
-        eo[1] = mk_op(OP_ACC_CORR, U, c->S0u.p, delta, nullptr, 1.0 / 6.0, two3, c->A3u.p, first,
-                      c->A1u.p, c->A2u.p);
+        co[1] = mk_op(OP_ACC_CORR, c->H.p, c->S0h.p, delta, nullptr, 1.0 / 6.0, two3, c->A3h.p,
+                      first, c->A1h.p, c->A2h.p);
+        eo[1] = mk_op(OP_ACC_CORR, c->U.p, c->S0u.p, delta, nullptr, 1.0 / 6.0, two3, c->A3u.p,
+                      first, c->A1u.p, c->A2u.p);
       }
-      launch_eval(c, ps, H2, U2, co, eo);
+      launch_eval(c, plan_for(c, kMaskSub), c->H2.p, c->U2.p, co, eo);
     }
   }
   // Step 4 (:557-563): coarse h = 1/3 h_old + 2/3 h2 + (2/3 dt) dh, in place.
-  {
+  // H2/U2 halos are current: the last exchange refreshed them and only
+  // fine/I1 entries (never read here) changed since.
+  for (auto* c : cs) {
     const double cr = two3 * dt;
+    double *H = c->H.p, *U = c->U.p, *H2 = c->H2.p, *U2 = c->U2.p;
     Op co[2] = {mk_op(OP_WCOMB, H, H, third, H2, two3, cr), mk_op(OP_WCOMB, H, H, third, H2, two3, cr)};
     Op eo[2] = {mk_op(OP_WCOMB, U, U, third, U2, two3, cr), mk_op(OP_WCOMB, U, U, third, U2, two3, cr)};
-    launch_eval(c, p4, H2, U2, co, eo);
+    launch_eval(c, plan_for(c, kMaskCoarseOnly), H2, U2, co, eo);
   }
 }
 
@@ -1055,74 +1207,75 @@ void tally_lts3(mswm_cuda_ctx* c, int M) {
 }
 
 // RK4 (integrators.cpp:370-410) with ping-pong stage buffers.
-void enqueue_rk4(mswm_cuda_ctx* c, double dt) {
-  MaskPlan& p = plan_for(c, MSWM_MASK_ALL);
+void enqueue_rk4(std::vector<mswm_cuda_ctx*>& cs, double dt) {
+  using C = mswm_cuda_ctx;
   const double half = 0.5 * dt, sixth = dt / 6.0;
-  double *H = c->H.p, *U = c->U.p;
-  k_step_counter<<<1, 1, 0, c->stream>>>(c->step_ctr.p);
   auto both = [](Op o) { return std::array<Op, 2>{o, o}; };
-  {
-    auto co = both(mk_op(OP_RK4_FIRST, c->T1h.p, H, half, nullptr, 0, 0, c->A1h.p));
-    auto eo = both(mk_op(OP_RK4_FIRST, c->T1u.p, U, half, nullptr, 0, 0, c->A1u.p));
-    launch_eval(c, p, H, U, co.data(), eo.data());
-  }
-  {
-    auto co = both(mk_op(OP_RK4_MID, c->T2h.p, H, half, nullptr, 0, 0, c->A1h.p));
-    auto eo = both(mk_op(OP_RK4_MID, c->T2u.p, U, half, nullptr, 0, 0, c->A1u.p));
-    launch_eval(c, p, c->T1h.p, c->T1u.p, co.data(), eo.data());
-  }
-  {
-    auto co = both(mk_op(OP_RK4_MID, c->T1h.p, H, dt, nullptr, 0, 0, c->A1h.p));
-    auto eo = both(mk_op(OP_RK4_MID, c->T1u.p, U, dt, nullptr, 0, 0, c->A1u.p));
-    launch_eval(c, p, c->T2h.p, c->T2u.p, co.data(), eo.data());
-  }
-  {
-    auto co = both(mk_op(OP_RK4_LAST, H, H, sixth, nullptr, 0, 0, c->A1h.p));
-    auto eo = both(mk_op(OP_RK4_LAST, U, U, sixth, nullptr, 0, 0, c->A1u.p));
-    launch_eval(c, p, c->T1h.p, c->T1u.p, co.data(), eo.data());
+  struct St {
+    ArrSel rh, ru, wh, wu;
+    int kind;
+    double c0;
+  };
+  const St stages[4] = {{&C::H, &C::U, &C::T1h, &C::T1u, OP_RK4_FIRST, half},
+                        {&C::T1h, &C::T1u, &C::T2h, &C::T2u, OP_RK4_MID, half},
+                        {&C::T2h, &C::T2u, &C::T1h, &C::T1u, OP_RK4_MID, dt},
+                        {&C::T1h, &C::T1u, &C::H, &C::U, OP_RK4_LAST, sixth}};
+  for (const St& st : stages) {
+    exchange(cs, st.rh, st.ru);
+    for (auto* c : cs) {
+      auto co = both(mk_op(st.kind, (c->*st.wh).p, c->H.p, st.c0, nullptr, 0, 0, c->A1h.p));
+      auto eo = both(mk_op(st.kind, (c->*st.wu).p, c->U.p, st.c0, nullptr, 0, 0, c->A1u.p));
+      launch_eval(c, plan_for(c, MSWM_MASK_ALL), (c->*st.rh).p, (c->*st.ru).p, co.data(), eo.data());
+    }
   }
 }
 
 // SSPRK2/3 (integrators.cpp:337-368).
-void enqueue_ssprk(mswm_cuda_ctx* c, int order, double dt) {
-  MaskPlan& p = plan_for(c, MSWM_MASK_ALL);
-  double *H = c->H.p, *U = c->U.p, *T1h = c->T1h.p, *T1u = c->T1u.p, *T2h = c->T2h.p,
-         *T2u = c->T2u.p;
-  k_step_counter<<<1, 1, 0, c->stream>>>(c->step_ctr.p);
+void enqueue_ssprk(std::vector<mswm_cuda_ctx*>& cs, int order, double dt) {
+  using C = mswm_cuda_ctx;
   auto both = [](Op o) { return std::array<Op, 2>{o, o}; };
-  {
-    auto co = both(mk_op(OP_EULER, T1h, H, dt));
-    auto eo = both(mk_op(OP_EULER, T1u, U, dt));
-    launch_eval(c, p, H, U, co.data(), eo.data());
+  exchange(cs, &C::H, &C::U);
+  for (auto* c : cs) {
+    auto co = both(mk_op(OP_EULER, c->T1h.p, c->H.p, dt));
+    auto eo = both(mk_op(OP_EULER, c->T1u.p, c->U.p, dt));
+    launch_eval(c, plan_for(c, MSWM_MASK_ALL), c->H.p, c->U.p, co.data(), eo.data());
   }
+  exchange(cs, &C::T1h, &C::T1u);
   if (order == 2) {
-    const double cr = 0.5 * dt;
-    auto co = both(mk_op(OP_WCOMB, H, H, 0.5, T1h, 0.5, cr));
-    auto eo = both(mk_op(OP_WCOMB, U, U, 0.5, T1u, 0.5, cr));
-    launch_eval(c, p, T1h, T1u, co.data(), eo.data());
+    for (auto* c : cs) {
+      const double cr = 0.5 * dt;
+      auto co = both(mk_op(OP_WCOMB, c->H.p, c->H.p, 0.5, c->T1h.p, 0.5, cr));
+      auto eo = both(mk_op(OP_WCOMB, c->U.p, c->U.p, 0.5, c->T1u.p, 0.5, cr));
+      launch_eval(c, plan_for(c, MSWM_MASK_ALL), c->T1h.p, c->T1u.p, co.data(), eo.data());
+    }
     return;
   }
-  {
+  for (auto* c : cs) {
     const double cr = 0.25 * dt;
-    auto co = both(mk_op(OP_WCOMB, T2h, H, 0.75, T1h, 0.25, cr));
-    auto eo = both(mk_op(OP_WCOMB, T2u, U, 0.75, T1u, 0.25, cr));
-    launch_eval(c, p, T1h, T1u, co.data(), eo.data());
+    auto co = both(mk_op(OP_WCOMB, c->T2h.p, c->H.p, 0.75, c->T1h.p, 0.25, cr));
+    auto eo = both(mk_op(OP_WCOMB, c->T2u.p, c->U.p, 0.75, c->T1u.p, 0.25, cr));
+    launch_eval(c, plan_for(c, MSWM_MASK_ALL), c->T1h.p, c->T1u.p, co.data(), eo.data());
   }
-  {
+  exchange(cs, &C::T2h, &C::T2u);
+  for (auto* c : cs) {
     const double cr = (2.0 / 3.0) * dt;
-    auto co = both(mk_op(OP_WCOMB, H, H, 1.0 / 3.0, T2h, 2.0 / 3.0, cr));
-    auto eo = both(mk_op(OP_WCOMB, U, U, 1.0 / 3.0, T2u, 2.0 / 3.0, cr));
-    launch_eval(c, p, T2h, T2u, co.data(), eo.data());
+    auto co = both(mk_op(OP_WCOMB, c->H.p, c->H.p, 1.0 / 3.0, c->T2h.p, 2.0 / 3.0, cr));
+    auto eo = both(mk_op(OP_WCOMB, c->U.p, c->U.p, 1.0 / 3.0, c->T2u.p, 2.0 / 3.0, cr));
+    launch_eval(c, plan_for(c, MSWM_MASK_ALL), c->T2h.p, c->T2u.p, co.data(), eo.data());
   }
 }
 
-void enqueue_step(mswm_cuda_ctx* c, int scheme, double dt, int M) {
-  ++c->launches;  // the step-counter kernel every schedule starts with
+void enqueue_step(std::vector<mswm_cuda_ctx*>& cs, int scheme, double dt, int M) {
+  for (auto* c : cs) {
+    k_step_counter<<<1, 1, 0, c->ls>>>(c->step_ctr.p);
+    CK(cudaGetLastError());
+    ++c->launches;
+  }
   switch (scheme) {
-    case MSWM_LTS3: enqueue_lts3(c, dt, M); break;
-    case MSWM_RK4: enqueue_rk4(c, dt); break;
-    case MSWM_SSPRK3: enqueue_ssprk(c, 3, dt); break;
-    case MSWM_SSPRK2: enqueue_ssprk(c, 2, dt); break;
+    case MSWM_LTS3: enqueue_lts3(cs, dt, M); break;
+    case MSWM_RK4: enqueue_rk4(cs, dt); break;
+    case MSWM_SSPRK3: enqueue_ssprk(cs, 3, dt); break;
+    case MSWM_SSPRK2: enqueue_ssprk(cs, 2, dt); break;
     default: throw Error(MSWM_E_CONFIG, "scheme not supported on the device path");
   }
 }
@@ -1143,6 +1296,65 @@ void tally_step(mswm_cuda_ctx* c, int scheme, int M) {
   ++c->ledger_steps;
 }
 
+void check_step_args(mswm_cuda_ctx* c, int scheme, double dt, int M, int64_t n_steps) {
+  if (!(dt > 0.0)) throw Error(MSWM_E_CONFIG, "time step must be positive");
+  if (n_steps < 0) throw Error(MSWM_E_USAGE, "negative step count");
+  if (scheme == MSWM_LTS3) {
+    if (M < 1) throw Error(MSWM_E_CONFIG, "substep count must be >= 1");
+    if (!c->have_regions) throw Error(MSWM_E_CONFIG, "local time stepping requires a region map");
+  } else if (scheme == MSWM_LTS2) {
+    throw Error(MSWM_E_CONFIG, "LTS2 is not on the device path (north_star names LTS3/RK4)");
+  } else if (scheme != MSWM_RK4 && scheme != MSWM_SSPRK3 && scheme != MSWM_SSPRK2) {
+    throw Error(MSWM_E_CONFIG, "unknown scheme");
+  }
+  if (!c->have_fields) throw Error(MSWM_E_USAGE, "set_fields must be called before stepping");
+}
+
+// Capture one step of every context in `cs` on `stream` into a graph.
+mswm_cuda_ctx::Graph capture_step(std::vector<mswm_cuda_ctx*>& cs, cudaStream_t stream, int scheme,
+                                  double dt, int M, bool profile) {
+  // Build every plan outside the capture (plan construction synchronises).
+  for (auto* c : cs) {
+    if (scheme == MSWM_LTS3) {
+      plan_for(c, kMaskStep1);
+      plan_for(c, kMaskIfCoarse);
+      plan_for(c, kMaskSub);
+      plan_for(c, kMaskCoarseOnly);
+    } else {
+      plan_for(c, MSWM_MASK_ALL);
+    }
+  }
+  mswm_cuda_ctx::Graph gr;
+  cudaGraph_t g = nullptr;
+  for (auto* c : cs) {
+    c->ls = stream;
+    c->launches = 0;
+  }
+  cs[0]->capture_records = profile ? &gr.records : nullptr;
+  CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    enqueue_step(cs, scheme, dt, M);
+  } catch (...) {
+    for (auto* c : cs) {
+      c->ls = c->stream;
+      c->capture_records = nullptr;
+    }
+    cudaStreamEndCapture(stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  for (auto* c : cs) {
+    gr.kernels += c->launches;
+    c->ls = c->stream;
+    c->capture_records = nullptr;
+  }
+  CK(cudaStreamEndCapture(stream, &g));
+  cudaError_t e = cudaGraphInstantiate(&gr.exec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) throw Error(MSWM_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+  return gr;
+}
+
 cudaGraphExec_t graph_for(mswm_cuda_ctx* c, int scheme, double dt, int M) {
   const auto key = std::make_tuple(scheme, dt, scheme == MSWM_LTS3 ? M : 0, int(c->profiling));
   auto it = c->graphs.find(key);
@@ -1151,36 +1363,9 @@ cudaGraphExec_t graph_for(mswm_cuda_ctx* c, int scheme, double dt, int M) {
     c->last_kernels_per_step = it->second.kernels;
     return it->second.exec;
   }
-  // Build every plan outside the capture (plan construction synchronises).
-  if (scheme == MSWM_LTS3) {
-    plan_for(c, kMaskStep1);
-    plan_for(c, kMaskIfCoarse);
-    plan_for(c, kMaskSub);
-    plan_for(c, kMaskCoarseOnly);
-  } else {
-    plan_for(c, MSWM_MASK_ALL);
-  }
-  mswm_cuda_ctx::Graph gr;
-  cudaGraph_t g = nullptr;
-  CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-  c->capture_records = c->profiling ? &gr.records : nullptr;
-  c->launches = 0;
-  try {
-    enqueue_step(c, scheme, dt, M);
-  } catch (...) {
-    c->capture_records = nullptr;
-    cudaStreamEndCapture(c->stream, &g);
-    if (g) cudaGraphDestroy(g);
-    throw;
-  }
-  c->capture_records = nullptr;
-  gr.kernels = c->launches;
-  CK(cudaStreamEndCapture(c->stream, &g));
-  cudaError_t e = cudaGraphInstantiate(&gr.exec, g, 0);
-  cudaGraphDestroy(g);
-  if (e != cudaSuccess) throw Error(MSWM_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+  std::vector<mswm_cuda_ctx*> cs{c};
   auto& slot = c->graphs[key];
-  slot = std::move(gr);
+  slot = capture_step(cs, c->stream, scheme, dt, M, c->profiling);
   c->last_records = &slot.records;
   c->last_kernels_per_step = slot.kernels;
   return slot.exec;
@@ -1316,6 +1501,7 @@ int mswm_cuda_create(const mswm_mesh_desc* mesh, int device, const int32_t* cell
     c->device = device;
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->ls = c->stream;
     build_tables(c.get(), mesh, cell_order);
   } catch (const Error& e) {
     g_create_error = e.what();
@@ -1476,17 +1662,7 @@ int mswm_cuda_state_download(mswm_cuda_ctx* c, double* h, double* u, double* tim
 int mswm_cuda_step(mswm_cuda_ctx* c, int scheme, double dt, int M, int64_t n_steps, int sync) {
   return guard(c, [&] {
     check_ctx(c);
-    if (!(dt > 0.0)) throw Error(MSWM_E_CONFIG, "time step must be positive");
-    if (n_steps < 0) throw Error(MSWM_E_USAGE, "negative step count");
-    if (scheme == MSWM_LTS3) {
-      if (M < 1) throw Error(MSWM_E_CONFIG, "substep count must be >= 1");
-      if (!c->have_regions) throw Error(MSWM_E_CONFIG, "local time stepping requires a region map");
-    } else if (scheme == MSWM_LTS2) {
-      throw Error(MSWM_E_CONFIG, "LTS2 is not on the device path (north_star names LTS3/RK4)");
-    } else if (scheme != MSWM_RK4 && scheme != MSWM_SSPRK3 && scheme != MSWM_SSPRK2) {
-      throw Error(MSWM_E_CONFIG, "unknown scheme");
-    }
-    if (!c->have_fields) throw Error(MSWM_E_USAGE, "set_fields must be called before stepping");
+    check_step_args(c, scheme, dt, M, n_steps);
     if (n_steps == 0) return int(MSWM_OK);
     cudaGraphExec_t g = graph_for(c, scheme, dt, M);
     reset_dry(c);
@@ -1597,6 +1773,217 @@ int mswm_cuda_total_mass(mswm_cuda_ctx* c, double* mass) {
     *mass = m;
     return int(MSWM_OK);
   });
+}
+
+// ---- multi-rank --------------------------------------------------------------
+
+int mswm_cuda_set_labels(mswm_cuda_ctx* c, const uint8_t* cell_label, const uint8_t* cell_sub,
+                         const uint8_t* edge_label, const uint8_t* cell_owned,
+                         const uint8_t* edge_owned, int interface_width) {
+  return guard(c, [&] {
+    check_ctx(c);
+    if (!cell_label || !cell_sub || !edge_label) throw Error(MSWM_E_USAGE, "null label array");
+    if (interface_width < 1) throw Error(MSWM_E_CONFIG, "interface width must be >= 1");
+    const int32_t nC = c->nC, nE = c->nE;
+    std::vector<uint8_t> ck(nC), ek(nE);
+    for (int32_t ni = 0; ni < nC; ++ni) {
+      const int32_t i = c->c_new2old[ni];
+      const uint8_t l = cell_label[i], sb = cell_sub[i];
+      if (l > 3 || sb > 2 || (l != 0 && sb != 0)) throw Error(MSWM_E_USAGE, "invalid cell label");
+      ck[ni] = (cell_owned && !cell_owned[i]) ? 0xFF : (l == 0 ? sb : uint8_t(l + 2));
+    }
+    for (int32_t ne = 0; ne < nE; ++ne) {
+      const int32_t e = c->e_new2old[ne];
+      if (edge_label[e] > 4) throw Error(MSWM_E_USAGE, "invalid edge label");
+      ek[ne] = (edge_owned && !edge_owned[e]) ? 0xFF : edge_label[e];
+    }
+    invalidate(c);
+    c->ckey.upload(ck, c->stream);
+    c->ekey.upload(ek, c->stream);
+    std::vector<int64_t> cs = compact(c, c->ckey.p, nC, 6, c->cell_groups);
+    std::vector<int64_t> es = compact(c, c->ekey.p, nE, 5, c->edge_groups);
+    int64_t off = 0;
+    for (int g = 0; g < 6; ++g) {
+      c->gsize[g] = cs[g];
+      c->goff[g] = off;
+      off += cs[g];
+    }
+    off = 0;
+    for (int g = 0; g < 5; ++g) {
+      c->gsize[6 + g] = es[g];
+      c->goff[6 + g] = off;
+      off += es[g];
+    }
+    c->width = interface_width;
+    c->have_regions = true;
+    return int(MSWM_OK);
+  });
+}
+
+int mswm_cuda_set_halo(mswm_cuda_ctx* c, int rank, int n_ranks, int n_peers, const int32_t* peers,
+                       const int64_t* counts, const int32_t* ids) {
+  return guard(c, [&] {
+    check_ctx(c);
+    if (n_ranks < 1 || rank < 0 || rank >= n_ranks || n_peers < 0 || n_peers > n_ranks - 1)
+      throw Error(MSWM_E_USAGE, "bad rank / peer counts");
+    if (n_peers > 0 && (!peers || !counts || !ids)) throw Error(MSWM_E_USAGE, "null halo arrays");
+    Halo h;
+    std::vector<int32_t> sc, rc;
+    const int32_t* p = ids;
+    for (int j = 0; j < n_peers; ++j) {
+      const int64_t nsc = counts[4 * j], nse = counts[4 * j + 1], nrc = counts[4 * j + 2],
+                    nre = counts[4 * j + 3];
+      if (peers[j] < 0 || peers[j] >= n_ranks || peers[j] == rank)
+        throw Error(MSWM_E_USAGE, "bad peer rank");
+      h.peer.push_back(peers[j]);
+      h.soff.push_back(int64_t(sc.size()));
+      h.scnt.push_back(nsc + nse);
+      for (int64_t k = 0; k < nsc; ++k) {
+        if (p[k] < 0 || p[k] >= c->nC) throw Error(MSWM_E_USAGE, "halo cell id out of range");
+        sc.push_back(c->c_old2new[p[k]]);
+      }
+      p += nsc;
+      for (int64_t k = 0; k < nse; ++k) {
+        if (p[k] < 0 || p[k] >= c->nE) throw Error(MSWM_E_USAGE, "halo edge id out of range");
+        sc.push_back(~c->e_old2new[p[k]]);
+      }
+      p += nse;
+      h.roff.push_back(int64_t(rc.size()));
+      h.rcnt.push_back(nrc + nre);
+      for (int64_t k = 0; k < nrc; ++k) {
+        if (p[k] < 0 || p[k] >= c->nC) throw Error(MSWM_E_USAGE, "halo cell id out of range");
+        rc.push_back(c->c_old2new[p[k]]);
+      }
+      p += nrc;
+      for (int64_t k = 0; k < nre; ++k) {
+        if (p[k] < 0 || p[k] >= c->nE) throw Error(MSWM_E_USAGE, "halo edge id out of range");
+        rc.push_back(~c->e_old2new[p[k]]);
+      }
+      p += nre;
+    }
+    h.ns = int64_t(sc.size());
+    h.nr = int64_t(rc.size());
+    h.scode.upload(sc, c->stream);
+    h.rcode.upload(rc, c->stream);
+    h.sbuf.alloc(size_t(std::max<int64_t>(h.ns, 1)));
+    h.rbuf.alloc(size_t(std::max<int64_t>(h.nr, 1)));
+    CK(cudaStreamSynchronize(c->stream));
+    c->drop_graphs();
+    c->halo = std::move(h);
+    c->rank = rank;
+    c->n_ranks = n_ranks;
+    return int(MSWM_OK);
+  });
+}
+
+int mswm_cuda_nccl_unique_id(void* id_out) {
+  try {
+    if (!id_out) return MSWM_E_USAGE;
+    ncclUniqueId id;
+    nccl_check(nccl().GetUniqueId(&id));
+    std::memcpy(id_out, &id, sizeof(id));
+    return MSWM_OK;
+  } catch (const Error& e) {
+    g_create_error = e.what();
+    return e.status;
+  }
+}
+
+int mswm_cuda_comm_init(mswm_cuda_ctx* c, const void* unique_id, int rank, int n_ranks) {
+  return guard(c, [&] {
+    check_ctx(c);
+    if (!unique_id) throw Error(MSWM_E_USAGE, "null unique id");
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof(id));
+    if (c->nccl_comm) {
+      nccl().CommDestroy(c->nccl_comm);
+      c->nccl_comm = nullptr;
+    }
+    nccl_check(nccl().CommInitRank(&c->nccl_comm, n_ranks, id, rank));
+    c->drop_graphs();
+    return int(MSWM_OK);
+  });
+}
+
+struct mswm_cuda_group {
+  std::vector<mswm_cuda_ctx*> members;
+  cudaStream_t stream = nullptr;
+  std::map<std::tuple<int, double, int>, mswm_cuda_ctx::Graph> graphs;
+  std::string last_error;
+  ~mswm_cuda_group() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+int mswm_cuda_group_create(mswm_cuda_ctx* const* members, int n, mswm_cuda_group** out) {
+  if (!out || !members || n < 1) return MSWM_E_USAGE;
+  *out = nullptr;
+  auto g = std::make_unique<mswm_cuda_group>();
+  try {
+    for (int r = 0; r < n; ++r) {
+      if (!members[r]) throw Error(MSWM_E_USAGE, "null member");
+      if (members[r]->rank != r || members[r]->n_ranks != n)
+        throw Error(MSWM_E_USAGE, "member " + std::to_string(r) + " is not rank " +
+                                      std::to_string(r) + " of " + std::to_string(n));
+      if (members[r]->device != members[0]->device)
+        throw Error(MSWM_E_USAGE, "group members must share a device");
+      g->members.push_back(members[r]);
+    }
+    CK(cudaSetDevice(members[0]->device));
+    CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+  } catch (const Error& e) {
+    g_create_error = e.what();
+    return e.status;
+  }
+  *out = g.release();
+  return MSWM_OK;
+}
+
+void mswm_cuda_group_destroy(mswm_cuda_group* g) {
+  if (!g) return;
+  cudaStreamSynchronize(g->stream);
+  delete g;
+}
+
+int mswm_cuda_group_step(mswm_cuda_group* g, int scheme, double dt, int M, int64_t n_steps) {
+  if (!g) return MSWM_E_USAGE;
+  mswm_cuda_ctx* c0 = g->members[0];
+  const int rc = guard(c0, [&] {
+    check_ctx(c0);
+    for (auto* c : g->members) {
+      check_step_args(c, scheme, dt, M, n_steps);
+      CK(cudaStreamSynchronize(c->stream));  // uploads were issued on member streams
+    }
+    if (n_steps == 0) return int(MSWM_OK);
+    const auto key = std::make_tuple(scheme, dt, scheme == MSWM_LTS3 ? M : 0);
+    auto it = g->graphs.find(key);
+    if (it == g->graphs.end()) {
+      auto gr = capture_step(g->members, g->stream, scheme, dt, M, false);
+      it = g->graphs.emplace(key, std::move(gr)).first;
+    }
+    for (auto* c : g->members) reset_dry(c);
+    for (int64_t k = 0; k < n_steps; ++k) {
+      CK(cudaGraphLaunch(it->second.exec, g->stream));
+      for (auto* c : g->members) {
+        tally_step(c, scheme, M);
+        c->time += dt;
+      }
+    }
+    CK(cudaStreamSynchronize(g->stream));
+    for (auto* c : g->members)
+      if (read_dry(c))
+        throw Error(MSWM_E_DRY_VERTEX, "rank " + std::to_string(c->rank) + ": vertex " +
+                                           std::to_string(c->last_dry_vertex) +
+                                           " has non-positive thickness (during the step batch)");
+    return int(MSWM_OK);
+  });
+  if (rc) g->last_error = c0->last_error;
+  return rc;
+}
+
+const char* mswm_cuda_group_last_error(const mswm_cuda_group* g) {
+  return g ? g->last_error.c_str() : g_create_error.c_str();
 }
 
 }  // extern "C"

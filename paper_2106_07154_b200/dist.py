@@ -1,0 +1,151 @@
+"""Multi-rank LTS3 on B200s: rank contexts, halo plans, transports.
+
+One rank = one GPU = one ``mswm_cuda_ctx`` holding the rank's piece of the
+mesh (``partition.LocalMesh``: owned cells/edges + two-hop halo, the
+reference's block plan, partition.cpp:307-403).  Region labels come from the
+global ``RegionMap`` (bit-exact with make_regions), outputs are the owned
+elements only, and halo copies of the stage arrays are refreshed before every
+evaluation.  Transports:
+
+* NCCL point-to-point (one process per GPU, ``torch.distributed`` for the
+  rendezvous): ``RankContext.init_nccl``;
+* an in-process group of rank contexts on one device (``CudaGroup``), used to
+  test the exchange path on a single GPU without kernels that wait on each
+  other.
+
+Per-rank results are bitwise identical to the single-GPU path (and to the
+reference): every owned element's arithmetic reads exactly the values the
+single-GPU evaluation reads.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .api import CudaContext, Error, State, _p, _raise
+from .mesh import Mesh
+from .partition import LocalMesh, build_local_meshes, partition_cells
+
+
+class DistributedLayout:
+    """Partition + local meshes of a global mesh with given region labels."""
+
+    def __init__(self, mesh: Mesh, cell_label, cell_sub, edge_label, n_ranks: int,
+                 order: np.ndarray | None = None):
+        self.mesh = mesh
+        self.n_ranks = n_ranks
+        self.cell_label = np.asarray(cell_label, np.uint8)
+        self.cell_sub = np.asarray(cell_sub, np.uint8)
+        self.edge_label = np.asarray(edge_label, np.uint8)
+        self.order = mesh.locality_order() if order is None else np.asarray(order)
+        self.rank_of_cell = partition_cells(self.order, self.cell_label, n_ranks)
+        self.locals: list[LocalMesh] = build_local_meshes(mesh, self.cell_label, self.cell_sub,
+                                                          self.edge_label, self.rank_of_cell,
+                                                          n_ranks)
+        hr = np.empty(mesh.n_cells, np.int64)
+        hr[self.order] = np.arange(mesh.n_cells)
+        self.hilbert_rank = hr
+
+    def local_order(self, r: int) -> np.ndarray:
+        """Device layout of rank r: local cells along the global curve."""
+        lm = self.locals[r]
+        o = np.argsort(self.hilbert_rank[lm.cells], kind="stable").astype(np.int32)
+        return np.concatenate([o, [lm.n_cells - 1]]).astype(np.int32)
+
+
+class RankContext:
+    """A CudaContext on one rank's local mesh."""
+
+    def __init__(self, layout: DistributedLayout, rank: int, b, f, gravity: float,
+                 interface_width: int = 1, device: int = 0):
+        lm = layout.locals[rank]
+        self.layout, self.rank, self.lm = layout, rank, lm
+        self.local_mesh = lm.as_mesh()
+        self.ctx = CudaContext(self.local_mesh, lm.gather_cells(np.asarray(b, np.float64)),
+                               lm.gather_vertices(np.asarray(f, np.float64)), gravity, device,
+                               order=layout.local_order(rank))
+        cl = np.concatenate([layout.cell_label[lm.cells], [3]]).astype(np.uint8)
+        cs = np.concatenate([layout.cell_sub[lm.cells], [0]]).astype(np.uint8)
+        el = np.concatenate([layout.edge_label[lm.edges], [4]]).astype(np.uint8)
+        self._labels = (cl, cs, el, lm.cell_owned, lm.edge_owned)
+        lib = self.ctx.lib
+        self.ctx._check(lib.mswm_cuda_set_labels(
+            self.ctx.handle, _p(cl, _lib.u8p), _p(cs, _lib.u8p), _p(el, _lib.u8p),
+            _p(lm.cell_owned, _lib.u8p), _p(lm.edge_owned, _lib.u8p), interface_width))
+        peers = sorted(set(lm.send_cells) | set(lm.recv_cells))
+        counts, ids = [], []
+        for q in peers:
+            parts = [lm.send_cells.get(q, np.zeros(0, np.int32)),
+                     lm.send_edges.get(q, np.zeros(0, np.int32)),
+                     lm.recv_cells.get(q, np.zeros(0, np.int32)),
+                     lm.recv_edges.get(q, np.zeros(0, np.int32))]
+            counts.extend(len(x) for x in parts)
+            ids.extend(parts)
+        self._peers = np.asarray(peers, np.int32)
+        self._counts = np.asarray(counts, np.int64)
+        self._ids = np.concatenate(ids).astype(np.int32) if ids else np.zeros(1, np.int32)
+        self.ctx._check(lib.mswm_cuda_set_halo(
+            self.ctx.handle, rank, layout.n_ranks, len(peers), _p(self._peers, _lib.i32p),
+            _p(self._counts, _lib.i64p), _p(self._ids, _lib.i32p)))
+
+    # -- NCCL transport ------------------------------------------------------
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_char * 128)()
+        rc = _lib.cuda().mswm_cuda_nccl_unique_id(C.cast(buf, C.c_void_p))
+        if rc:
+            _raise(rc, _lib.cuda().mswm_cuda_last_error(None).decode())
+        return bytes(buf)
+
+    def init_nccl(self, unique_id: bytes):
+        buf = (C.c_char * 128).from_buffer_copy(unique_id)
+        self.ctx._check(self.ctx.lib.mswm_cuda_comm_init(
+            self.ctx.handle, C.cast(buf, C.c_void_p), self.rank, self.layout.n_ranks))
+
+    # -- state ---------------------------------------------------------------
+    def upload(self, h_global, u_global, time: float = 0.0):
+        lm = self.lm
+        self.ctx.upload(State(lm.gather_cells(np.asarray(h_global, np.float64)),
+                              lm.gather_edges(np.asarray(u_global, np.float64)), time))
+
+    def download_owned(self, h_global: np.ndarray, u_global: np.ndarray) -> float:
+        """Write this rank's owned values into the global arrays."""
+        st = self.ctx.download()
+        lm = self.lm
+        h_global[lm.cells[:lm.n_owned_cells]] = st.h[:lm.n_owned_cells]
+        u_global[lm.edges[:lm.n_owned_edges]] = st.u[:lm.n_owned_edges]
+        return st.time
+
+
+class CudaGroup:
+    """All ranks of a layout as contexts on one device, stepped in lockstep."""
+
+    def __init__(self, ranks: list[RankContext]):
+        self.ranks = ranks
+        lib = _lib.cuda()
+        arr = (C.c_void_p * len(ranks))(*[r.ctx.handle.value for r in ranks])
+        h = C.c_void_p()
+        rc = lib.mswm_cuda_group_create(arr, len(ranks), C.byref(h))
+        if rc:
+            _raise(rc, lib.mswm_cuda_last_error(None).decode())
+        self.handle = h
+        self.lib = lib
+
+    def advance(self, scheme, dt: float, substeps: int = 1, n_steps: int = 1):
+        rc = self.lib.mswm_cuda_group_step(self.handle, int(scheme), float(dt), int(substeps),
+                                           int(n_steps))
+        if rc:
+            _raise(rc, self.lib.mswm_cuda_group_last_error(self.handle).decode())
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.mswm_cuda_group_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

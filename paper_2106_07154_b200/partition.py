@@ -1,0 +1,239 @@
+"""Domain decomposition for the multi-GPU LTS3 path.
+
+Restates the reference's rank/block layout for one process per GPU:
+
+* ``partition_cells`` -- per-class balanced split (partition.cpp:219-231): each
+  class (fine incl. underline, coarse, interface) is cut into N near-equal
+  consecutive runs, so every rank holds 1/N of the fine work (weighted M x by
+  the substeps) *and* 1/N of the coarse work and no rank idles in a phase
+  (PAPER.md:482-483).  The sweep order is the Hilbert curve instead of the
+  reference's BFS sweep; the boundary-refinement pass is not used.
+* ``edge_owner`` -- edge ownership rule of make_block_plan (partition.cpp:338-353):
+  the first cell of ``edge_cells`` whose class equals the edge's class.
+* ``LocalMesh`` -- owned cells plus the cells within two hops (the reference's
+  halo, partition.cpp:355-392), every ring edge and ring vertex of those cells,
+  renumbered locally; references that leave the local set point to one dummy
+  cell/edge/vertex whose values are never read by an owned output.  The halo
+  plan lists, per peer, which local halo elements that peer owns (receive) and
+  which owned elements the peer needs (send), both in ascending global id so
+  both sides agree on the order.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .mesh import Mesh
+
+# class of a cell: 0 fine (incl. underline), 1 coarse, 2 interface (partition.cpp:16-25)
+def cell_class(cell_label: np.ndarray) -> np.ndarray:
+    cl = np.asarray(cell_label)
+    return np.where(cl == 0, 0, np.where(cl == 3, 1, 2)).astype(np.int8)
+
+
+def edge_class(edge_label: np.ndarray) -> np.ndarray:
+    """partition.cpp:27-37: fine/underline-fine edges 0, coarse 1, interfaces 2."""
+    el = np.asarray(edge_label)
+    return np.where(el <= 1, 0, np.where(el == 4, 1, 2)).astype(np.int8)
+
+
+def partition_cells(order: np.ndarray, cell_label: np.ndarray, n_parts: int) -> np.ndarray:
+    """rank of every cell: position pos of t in its class's run along `order`
+    goes to part pos*N/t (partition.cpp:219-231)."""
+    n = len(order)
+    if n_parts < 1 or n_parts > n:
+        raise ValueError("n_parts out of range")
+    cls = cell_class(cell_label)[order]
+    rank = np.zeros(n, np.int32)
+    for k in range(3):
+        sel = np.nonzero(cls == k)[0]
+        t = len(sel)
+        if t == 0:
+            continue
+        pos = np.arange(t, dtype=np.int64)
+        rank[order[sel]] = (pos * n_parts // t).astype(np.int32)
+    return rank
+
+
+def edge_owner(mesh: Mesh, cell_label: np.ndarray, edge_label: np.ndarray,
+               rank_of_cell: np.ndarray) -> np.ndarray:
+    """Rank owning each edge (partition.cpp:338-353)."""
+    ec = mesh.edge_cells
+    ccls = cell_class(cell_label)
+    ecls = edge_class(edge_label)
+    first = ccls[ec[:, 0]] == ecls
+    second = ccls[ec[:, 1]] == ecls
+    if not np.all(first | second):
+        bad = int(np.nonzero(~(first | second))[0][0])
+        raise ValueError(f"edge {bad} has no adjacent cell of its own region class")
+    owner_cell = np.where(first, ec[:, 0], ec[:, 1])
+    return rank_of_cell[owner_cell].astype(np.int32)
+
+
+def ring_neighbours(mesh: Mesh):
+    co = mesh.cell_offset
+    deg = np.diff(co)
+    rows = np.repeat(np.arange(mesh.n_cells), deg)
+    return rows, mesh.cell_cells, mesh.cell_edges, mesh.cell_vertices
+
+
+@dataclass
+class LocalMesh:
+    """One rank's piece of the mesh in local numbering (plus one dummy of each)."""
+    rank: int
+    n_ranks: int
+    cells: np.ndarray          # global ids of local cells (owned first, ascending within)
+    edges: np.ndarray
+    vertices: np.ndarray
+    n_owned_cells: int
+    n_owned_edges: int
+    tables: dict               # mswm_mesh_desc tables, local ids
+    cell_owned: np.ndarray     # uint8 per local cell (dummy excluded -> 0)
+    edge_owned: np.ndarray
+    send_cells: dict = field(default_factory=dict)   # peer -> local ids (ascending global)
+    recv_cells: dict = field(default_factory=dict)
+    send_edges: dict = field(default_factory=dict)
+    recv_edges: dict = field(default_factory=dict)
+
+    @property
+    def n_cells(self):
+        return len(self.cells) + 1
+
+    @property
+    def n_edges(self):
+        return len(self.edges) + 1
+
+    @property
+    def n_vertices(self):
+        return len(self.vertices) + 1
+
+    def as_mesh(self) -> Mesh:
+        m = Mesh(self.n_cells, self.n_edges, self.n_vertices, self.tables, None, None, None, None,
+                 False)
+        return m
+
+    def gather_cells(self, x: np.ndarray) -> np.ndarray:
+        """Local view of a global cell field (dummy value 1.0)."""
+        return np.concatenate([x[self.cells], [1.0]])
+
+    def gather_edges(self, x: np.ndarray) -> np.ndarray:
+        return np.concatenate([x[self.edges], [0.0]])
+
+    def gather_vertices(self, x: np.ndarray) -> np.ndarray:
+        return np.concatenate([x[self.vertices], [0.0]])
+
+
+def _two_hop(mesh: Mesh, seed_mask: np.ndarray) -> np.ndarray:
+    rows, nbr, _, _ = ring_neighbours(mesh)
+    m = seed_mask.copy()
+    for _ in range(2):
+        hit = np.zeros(mesh.n_cells, bool)
+        hit[nbr[m[rows]]] = True
+        m |= hit
+    return m
+
+
+def build_local_meshes(mesh: Mesh, cell_label, cell_sub, edge_label, rank_of_cell: np.ndarray,
+                       n_ranks: int) -> list[LocalMesh]:
+    """Local meshes and halo plans for every rank (host setup)."""
+    own_e = edge_owner(mesh, cell_label, edge_label, rank_of_cell)
+    rows, nbr, redges, rverts = ring_neighbours(mesh)
+    co = mesh.cell_offset
+    out = []
+    for r in range(n_ranks):
+        owned_c = rank_of_cell == r
+        lc_mask = _two_hop(mesh, owned_c)
+        # cells: owned first, then halo, each ascending
+        cells = np.concatenate([np.nonzero(owned_c)[0], np.nonzero(lc_mask & ~owned_c)[0]])
+        in_ring = lc_mask[rows]
+        e_mask = np.zeros(mesh.n_edges, bool)
+        e_mask[redges[in_ring]] = True
+        v_mask = np.zeros(mesh.n_vertices, bool)
+        v_mask[rverts[in_ring]] = True
+        owned_e = (own_e == r)
+        if np.any(owned_e & ~e_mask):
+            raise AssertionError("an owned edge is not a ring edge of a local cell")
+        edges = np.concatenate([np.nonzero(owned_e)[0], np.nonzero(e_mask & ~owned_e)[0]])
+        verts = np.nonzero(v_mask)[0]
+        nC, nE, nV = len(cells) + 1, len(edges) + 1, len(verts) + 1
+        dC, dE, dV = nC - 1, nE - 1, nV - 1
+        gc = np.full(mesh.n_cells, dC, np.int32)
+        gc[cells] = np.arange(len(cells), dtype=np.int32)
+        ge = np.full(mesh.n_edges, dE, np.int32)
+        ge[edges] = np.arange(len(edges), dtype=np.int32)
+        gv = np.full(mesh.n_vertices, dV, np.int32)
+        gv[verts] = np.arange(len(verts), dtype=np.int32)
+        deg = np.diff(co)[cells]
+        # local CSR rings (dummy cell: a triangle of dummies)
+        offs = np.zeros(nC + 1, np.int32)
+        offs[1:len(cells) + 1] = np.cumsum(deg)
+        offs[nC] = offs[nC - 1] + 3
+        take = np.concatenate([np.arange(co[c], co[c + 1]) for c in cells]) if len(cells) else \
+            np.zeros(0, np.int64)
+        ring_e = np.concatenate([ge[mesh.cell_edges[take]], [dE] * 3]).astype(np.int32)
+        ring_v = np.concatenate([gv[mesh.cell_vertices[take]], [dV] * 3]).astype(np.int32)
+        ring_c = np.concatenate([gc[mesh.cell_cells[take]], [dC] * 3]).astype(np.int32)
+        eoff_g = mesh.edge_edge_offset
+        slen = np.diff(eoff_g)[edges]
+        eoff = np.zeros(nE + 1, np.int32)
+        eoff[1:len(edges) + 1] = np.cumsum(slen)
+        eoff[nE] = eoff[nE - 1]
+        stake = np.concatenate([np.arange(eoff_g[e], eoff_g[e + 1]) for e in edges]) \
+            if len(edges) else np.zeros(0, np.int64)
+        t = {
+            "cell_offset": offs,
+            "cell_edges": ring_e,
+            "cell_vertices": ring_v,
+            "cell_cells": ring_c,
+            "edge_cells": np.concatenate([gc[mesh.edge_cells[edges]], [[dC, dC]]]).astype(np.int32),
+            "edge_vertices": np.concatenate([gv[mesh.edge_vertices[edges]], [[dV, dV]]]).astype(np.int32),
+            "vertex_cells": np.concatenate([gc[mesh.vertex_cells[verts]], [[dC] * 3]]).astype(np.int32),
+            "vertex_edges": np.concatenate([ge[mesh.vertex_edges[verts]], [[dE] * 3]]).astype(np.int32),
+            "edge_edge_offset": eoff,
+            "edge_edges": ge[mesh.edge_edges[stake]].astype(np.int32),
+            "edge_cell_sign": np.concatenate([mesh.edge_cell_sign[edges], [[-1, 1]]]).astype(np.int8),
+            "edge_vertex_sign": np.concatenate([mesh.edge_vertex_sign[edges], [[-1, 1]]]).astype(np.int8),
+            "edge_len": np.concatenate([mesh.edge_len[edges], [1.0]]),
+            "edge_dual_len": np.concatenate([mesh.edge_dual_len[edges], [1.0]]),
+            "cell_area": np.concatenate([mesh.cell_area[cells], [1.0]]),
+            "vertex_area": np.concatenate([mesh.vertex_area[verts], [1.0]]),
+            "vertex_kite": np.concatenate([mesh.vertex_kite[verts], [[1.0, 1.0, 1.0]]]),
+            "edge_weight": mesh.edge_weight[stake].astype(np.float64),
+        }
+        t = {k: np.ascontiguousarray(v) for k, v in t.items()}
+        cell_owned = np.zeros(nC, np.uint8)
+        cell_owned[:int(owned_c.sum())] = 1
+        edge_owned = np.zeros(nE, np.uint8)
+        edge_owned[:int(owned_e.sum())] = 1
+        lm = LocalMesh(r, n_ranks, cells.astype(np.int64), edges.astype(np.int64),
+                       verts.astype(np.int64), int(owned_c.sum()), int(owned_e.sum()), t,
+                       cell_owned, edge_owned)
+        out.append(lm)
+    # halo plans: rank r receives halo element x from owner(x); the owner sends
+    # it.  Lists are in ascending global id on both sides.
+    for lm in out:
+        r = lm.rank
+        halo_c = lm.cells[lm.n_owned_cells:]
+        halo_e = lm.edges[lm.n_owned_edges:]
+        for p in range(n_ranks):
+            if p == r:
+                continue
+            hc = np.sort(halo_c[rank_of_cell[halo_c] == p])
+            he = np.sort(halo_e[own_e[halo_e] == p])
+            if len(hc) == 0 and len(he) == 0:
+                continue
+            lm.recv_cells[p] = _local_ids(lm.cells, hc)
+            lm.recv_edges[p] = _local_ids(lm.edges, he)
+            peer = out[p]
+            peer.send_cells[r] = _local_ids(peer.cells, hc)
+            peer.send_edges[r] = _local_ids(peer.edges, he)
+    return out
+
+
+def _local_ids(local_globals: np.ndarray, wanted: np.ndarray) -> np.ndarray:
+    idx = np.argsort(local_globals, kind="stable")
+    pos = np.searchsorted(local_globals[idx], wanted)
+    ids = idx[pos]
+    assert np.array_equal(local_globals[ids], wanted)
+    return ids.astype(np.int32)

@@ -1,0 +1,62 @@
+"""Multi-rank device path on one GPU: N rank contexts (local meshes, owned
+outputs, halo plans) stepped in lockstep by an in-process group whose halo
+exchange is device copies -- the same pack/unpack and schedule as the NCCL
+transport, without kernels that wait on one another.  Results must equal the
+single-context path and the oracle bitwise (acceptance.cpp:205-244 analogue:
+ranks bitwise = serial)."""
+import numpy as np
+import pytest
+
+from helpers import bits_equal
+from oracle.oracle import Oracle
+from paper_2106_07154_b200 import workloads as W
+from paper_2106_07154_b200.api import Scheme
+from paper_2106_07154_b200.dist import CudaGroup, DistributedLayout, RankContext
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("n_ranks", [2, 3, 4])
+@pytest.mark.parametrize("scheme", [Scheme.LTS3, Scheme.RK4])
+def test_group_ranks_bitwise_equal_oracle(n_ranks, scheme):
+    wl = W.small_sphere(5, seed=23, cap_deg=25.0)
+    o = Oracle(wl.mesh, wl.b, wl.f, wl.gravity)
+    o.set_regions(wl.fine_mask, wl.width)
+    cl, cs, el = o.labels()
+    dt = wl.dt if scheme == Scheme.LTS3 else wl.dt / wl.M
+    n = 4
+    h_ref, u_ref, _ = o.step(int(scheme), wl.h, wl.u, 0.0, dt, wl.M, n)
+    lay = DistributedLayout(wl.mesh, cl, cs, el, n_ranks)
+    ranks = [RankContext(lay, r, wl.b, wl.f, wl.gravity) for r in range(n_ranks)]
+    for rc in ranks:
+        rc.upload(wl.h, wl.u)
+    grp = CudaGroup(ranks)
+    grp.advance(scheme, dt, wl.M, n)
+    h = np.full(wl.mesh.n_cells, np.nan)
+    u = np.full(wl.mesh.n_edges, np.nan)
+    for rc in ranks:
+        rc.download_owned(h, u)
+    assert bits_equal(h, h_ref) and bits_equal(u, u_ref)
+    # the per-rank ledgers add up to the serial one
+    c_ref, e_ref, _ = o.ledger()
+    c = sum(rc.ctx.ledger().cell_evals for rc in ranks)
+    e = sum(rc.ctx.ledger().edge_evals for rc in ranks)
+    assert np.array_equal(c, c_ref) and np.array_equal(e, e_ref)
+
+
+def test_planar_group_c1():
+    wl = W.config1(n_steps=10)
+    o = Oracle(wl.mesh, wl.b, wl.f, wl.gravity)
+    o.set_regions(wl.fine_mask, wl.width)
+    cl, cs, el = o.labels()
+    h_ref, u_ref, _ = o.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, wl.M, wl.n_steps)
+    lay = DistributedLayout(wl.mesh, cl, cs, el, 4)
+    ranks = [RankContext(lay, r, wl.b, wl.f, wl.gravity) for r in range(4)]
+    for rc in ranks:
+        rc.upload(wl.h, wl.u)
+    CudaGroup(ranks).advance(Scheme.LTS3, wl.dt, wl.M, wl.n_steps)
+    h = np.full(wl.mesh.n_cells, np.nan)
+    u = np.full(wl.mesh.n_edges, np.nan)
+    for rc in ranks:
+        rc.download_owned(h, u)
+    assert bits_equal(h, h_ref) and bits_equal(u, u_ref)
