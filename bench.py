@@ -11,8 +11,9 @@ is the same metric through the drop-in C-ABI call a reference user makes
 (upload h,u from pinned host memory, one coarse step, download h,u).  The
 dominant kernel's roofline is one tendency evaluation (kernels A+B+C with
 the fused stage update) timed with CUDA events inside the timed steps.
-Under torchrun each rank runs its own copy of the workload on its GPU
-(weak scaling, no data-path collective yet: see DESIGN.md "multi-GPU").
+Under torchrun the mesh is partitioned across the ranks (strong scaling):
+per-class balanced Hilbert partition, two-hop halos, NCCL point-to-point
+halo exchange before every evaluation.
 """
 from __future__ import annotations
 
@@ -62,6 +63,17 @@ def barrier(ws):
     if ws > 1:
         import torch.distributed as dist
         dist.barrier()
+
+
+def allreduce_sum(x: float, ws: int) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
 
 
 def allreduce_max(x: float, ws: int) -> float:
@@ -215,7 +227,7 @@ def run_reference_arm(args, ws, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": ws,
         "steps": n, "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": sps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload_config(wl, args.config, ws),
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": f"{n} LTS3 coarse steps of {args.config} "
@@ -231,7 +243,8 @@ def workload_config(wl, name, ws):
                         f"interface width {wl.width}",
             "n_cells": m.n_cells, "n_edges": m.n_edges, "n_vertices": m.n_vertices,
             "M": wl.M, "dt": wl.dt, "fine_cells": int(wl.fine_mask.sum()),
-            "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
+            "parallelism": (f"{ws} GPUs: class-balanced Hilbert partition, 2-hop halos, "
+                            "NCCL p2p halo exchange before every evaluation") if ws > 1 else "1 GPU",
             "l2": "inputs larger than L2 (mesh tables + state > 126 MB)" if m.n_edges > 400000
             else "working set L2-resident (correctness config)"}
 
@@ -249,10 +262,34 @@ def run_ours(args, ws, rank, local):
     wl = make_workload(args.config)
     log(f"[rank {rank}] workload {args.config}: {wl.mesh.n_cells} cells, {wl.mesh.n_edges} edges, "
         f"built in {time.time() - t0:.1f}s")
-    ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, device=local)
-    rm = ctx.make_regions(wl.fine_mask, wl.width)
-    log(f"[rank {rank}] groups {rm.group_sizes()}")
-    ctx.upload(State(wl.h, wl.u, 0.0))
+    rc = None
+    if ws == 1:
+        ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, device=local)
+        rm = ctx.make_regions(wl.fine_mask, wl.width)
+        log(f"[rank {rank}] groups {rm.group_sizes()}")
+        ctx.upload(State(wl.h, wl.u, 0.0))
+        io_mesh = wl.mesh
+    else:
+        # partitioned (strong scaling): global labels from a device
+        # make_regions, this rank's local mesh + halo plan, NCCL p2p halos
+        import torch.distributed as dist
+        from paper_2106_07154_b200.dist import DistributedLayout, RankContext
+        g = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, device=local)
+        rm = g.make_regions(wl.fine_mask, wl.width)
+        g.close()
+        del g
+        t1 = time.time()
+        lay = DistributedLayout(wl.mesh, rm.cell_label, rm.cell_sublabel, rm.edge_label, ws,
+                                only=rank)
+        rc = RankContext(lay, rank, wl.b, wl.f, wl.gravity, wl.width, device=local)
+        uid = [RankContext.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        rc.init_nccl(uid[0])
+        rc.upload(wl.h, wl.u)
+        ctx = rc.ctx
+        io_mesh = rc.local_mesh
+        log(f"[rank {rank}] local mesh {rc.lm.n_cells} cells ({rc.lm.n_owned_cells} owned), "
+            f"{len(lay.locals[rank].send_cells)} peers, set up in {time.time() - t1:.1f}s")
     ctx.set_profiling(True)
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=local)
 
@@ -276,10 +313,10 @@ def run_ours(args, ws, rank, local):
     ms_local = e0.elapsed_time(e1)
     ms = allreduce_max(ms_local, ws)
     lg = ctx.ledger()
-    edge_per_step = lg.total_edge_evals() / args.steps
-    cell_per_step = lg.total_cell_evals() / args.steps
+    edge_per_step = allreduce_sum(lg.total_edge_evals(), ws) / args.steps
+    cell_per_step = allreduce_sum(lg.total_cell_evals(), ws) / args.steps
     ms_step = ms / args.steps
-    value = ws * edge_per_step / (ms_step / 1e3)
+    value = edge_per_step / (ms_step / 1e3)
 
     # roofline of the dominant kernel: the largest tendency evaluation of the
     # last timed step, timed by the events captured around it
@@ -295,9 +332,11 @@ def run_ours(args, ws, rank, local):
     if tf.exists():
         traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
 
-    # e2e through the drop-in C ABI with pinned host buffers
-    h_pin = torch.from_numpy(np.array(wl.h)).pin_memory()
-    u_pin = torch.from_numpy(np.array(wl.u)).pin_memory()
+    # e2e through the drop-in C ABI with pinned host buffers (the rank's
+    # local arrays when partitioned)
+    st0 = ctx.download()
+    h_pin = torch.from_numpy(np.array(st0.h)).pin_memory()
+    u_pin = torch.from_numpy(np.array(st0.u)).pin_memory()
     st = State(h_pin.numpy(), u_pin.numpy(), 0.0)
     ctx.set_profiling(False)
     ctx.upload(st)
@@ -311,8 +350,8 @@ def run_ours(args, ws, rank, local):
         ctx.advance(Scheme.LTS3, wl.dt, wl.M, 1)
         ctx.download(st)
     e2e_s = allreduce_max(time.perf_counter() - t, ws)
-    e2e_value = ws * edge_per_step * n_e2e / e2e_s
-    io_bytes = 8 * (wl.mesh.n_cells + wl.mesh.n_edges)
+    e2e_value = edge_per_step * n_e2e / e2e_s
+    io_bytes = int(allreduce_sum(8 * (io_mesh.n_cells + io_mesh.n_edges), ws))
 
     launches = ctx.kernels_per_step() * args.steps
 
@@ -337,9 +376,9 @@ def run_ours(args, ws, rank, local):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(wl, args.config, ws),
-            "coarse_steps_per_s": ws * 1e3 / ms_step,
+            "coarse_steps_per_s": 1e3 / ms_step,
             "step_algorithmic_GBps": step_alg / (ms_step / 1e3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,

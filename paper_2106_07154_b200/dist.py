@@ -33,7 +33,7 @@ class DistributedLayout:
     """Partition + local meshes of a global mesh with given region labels."""
 
     def __init__(self, mesh: Mesh, cell_label, cell_sub, edge_label, n_ranks: int,
-                 order: np.ndarray | None = None):
+                 order: np.ndarray | None = None, only: int | None = None):
         self.mesh = mesh
         self.n_ranks = n_ranks
         self.cell_label = np.asarray(cell_label, np.uint8)
@@ -43,7 +43,7 @@ class DistributedLayout:
         self.rank_of_cell = partition_cells(self.order, self.cell_label, n_ranks)
         self.locals: list[LocalMesh] = build_local_meshes(mesh, self.cell_label, self.cell_sub,
                                                           self.edge_label, self.rank_of_cell,
-                                                          n_ranks)
+                                                          n_ranks, only=only)
         hr = np.empty(mesh.n_cells, np.int64)
         hr[self.order] = np.arange(mesh.n_cells)
         self.hilbert_rank = hr

@@ -135,25 +135,32 @@ def _two_hop(mesh: Mesh, seed_mask: np.ndarray) -> np.ndarray:
 
 
 def build_local_meshes(mesh: Mesh, cell_label, cell_sub, edge_label, rank_of_cell: np.ndarray,
-                       n_ranks: int) -> list[LocalMesh]:
-    """Local meshes and halo plans for every rank (host setup)."""
+                       n_ranks: int, only: int | None = None) -> list:
+    """Local meshes and halo plans (host setup).  With ``only`` = r, the
+    tables are built for rank r alone (the others are None) -- what one
+    process of a multi-GPU run needs."""
     own_e = edge_owner(mesh, cell_label, edge_label, rank_of_cell)
     rows, nbr, redges, rverts = ring_neighbours(mesh)
     co = mesh.cell_offset
-    out = []
+    # local cell / edge sets of every rank (needed for the send lists)
+    sets = []
     for r in range(n_ranks):
         owned_c = rank_of_cell == r
         lc_mask = _two_hop(mesh, owned_c)
-        # cells: owned first, then halo, each ascending
-        cells = np.concatenate([np.nonzero(owned_c)[0], np.nonzero(lc_mask & ~owned_c)[0]])
-        in_ring = lc_mask[rows]
         e_mask = np.zeros(mesh.n_edges, bool)
-        e_mask[redges[in_ring]] = True
-        v_mask = np.zeros(mesh.n_vertices, bool)
-        v_mask[rverts[in_ring]] = True
-        owned_e = (own_e == r)
+        e_mask[redges[lc_mask[rows]]] = True
+        owned_e = own_e == r
         if np.any(owned_e & ~e_mask):
             raise AssertionError("an owned edge is not a ring edge of a local cell")
+        sets.append((owned_c, lc_mask, owned_e, e_mask))
+    build = range(n_ranks) if only is None else [only]
+    out = [None] * n_ranks
+    for r in build:
+        owned_c, lc_mask, owned_e, e_mask = sets[r]
+        # cells: owned first, then halo, each ascending
+        cells = np.concatenate([np.nonzero(owned_c)[0], np.nonzero(lc_mask & ~owned_c)[0]])
+        v_mask = np.zeros(mesh.n_vertices, bool)
+        v_mask[rverts[lc_mask[rows]]] = True
         edges = np.concatenate([np.nonzero(owned_e)[0], np.nonzero(e_mask & ~owned_e)[0]])
         verts = np.nonzero(v_mask)[0]
         nC, nE, nV = len(cells) + 1, len(edges) + 1, len(verts) + 1
@@ -169,8 +176,7 @@ def build_local_meshes(mesh: Mesh, cell_label, cell_sub, edge_label, rank_of_cel
         offs = np.zeros(nC + 1, np.int32)
         offs[1:len(cells) + 1] = np.cumsum(deg)
         offs[nC] = offs[nC - 1] + 3
-        take = np.concatenate([np.arange(co[c], co[c + 1]) for c in cells]) if len(cells) else \
-            np.zeros(0, np.int64)
+        take = csr_take(co, cells)
         ring_e = np.concatenate([ge[mesh.cell_edges[take]], [dE] * 3]).astype(np.int32)
         ring_v = np.concatenate([gv[mesh.cell_vertices[take]], [dV] * 3]).astype(np.int32)
         ring_c = np.concatenate([gc[mesh.cell_cells[take]], [dC] * 3]).astype(np.int32)
@@ -179,8 +185,7 @@ def build_local_meshes(mesh: Mesh, cell_label, cell_sub, edge_label, rank_of_cel
         eoff = np.zeros(nE + 1, np.int32)
         eoff[1:len(edges) + 1] = np.cumsum(slen)
         eoff[nE] = eoff[nE - 1]
-        stake = np.concatenate([np.arange(eoff_g[e], eoff_g[e + 1]) for e in edges]) \
-            if len(edges) else np.zeros(0, np.int64)
+        stake = csr_take(eoff_g, edges)
         t = {
             "cell_offset": offs,
             "cell_edges": ring_e,
@@ -209,26 +214,35 @@ def build_local_meshes(mesh: Mesh, cell_label, cell_sub, edge_label, rank_of_cel
         lm = LocalMesh(r, n_ranks, cells.astype(np.int64), edges.astype(np.int64),
                        verts.astype(np.int64), int(owned_c.sum()), int(owned_e.sum()), t,
                        cell_owned, edge_owned)
-        out.append(lm)
-    # halo plans: rank r receives halo element x from owner(x); the owner sends
-    # it.  Lists are in ascending global id on both sides.
-    for lm in out:
-        r = lm.rank
-        halo_c = lm.cells[lm.n_owned_cells:]
-        halo_e = lm.edges[lm.n_owned_edges:]
+        # halo plan: receive from each peer the halo elements it owns; send to
+        # each peer the owned elements inside its local set.  Ascending global
+        # id on both sides.
         for p in range(n_ranks):
             if p == r:
                 continue
-            hc = np.sort(halo_c[rank_of_cell[halo_c] == p])
-            he = np.sort(halo_e[own_e[halo_e] == p])
-            if len(hc) == 0 and len(he) == 0:
-                continue
-            lm.recv_cells[p] = _local_ids(lm.cells, hc)
-            lm.recv_edges[p] = _local_ids(lm.edges, he)
-            peer = out[p]
-            peer.send_cells[r] = _local_ids(peer.cells, hc)
-            peer.send_edges[r] = _local_ids(peer.edges, he)
+            p_owned_c, p_lc, p_owned_e, p_e = sets[p]
+            rc_ = np.nonzero(lc_mask & p_owned_c)[0]
+            re_ = np.nonzero(e_mask & p_owned_e)[0]
+            sc_ = np.nonzero(owned_c & p_lc)[0]
+            se_ = np.nonzero(owned_e & p_e)[0]
+            if len(rc_) or len(re_):
+                lm.recv_cells[p] = gc[rc_]
+                lm.recv_edges[p] = ge[re_]
+            if len(sc_) or len(se_):
+                lm.send_cells[p] = gc[sc_]
+                lm.send_edges[p] = ge[se_]
+        out[r] = lm
     return out
+
+
+def csr_take(off: np.ndarray, rows: np.ndarray) -> np.ndarray:
+    """Indices into a CSR value array for the given rows, row after row."""
+    off = np.asarray(off, np.int64)
+    lens = off[rows + 1] - off[rows]
+    if len(rows) == 0 or lens.sum() == 0:
+        return np.zeros(0, np.int64)
+    starts = np.repeat(off[rows] - np.concatenate([[0], np.cumsum(lens)[:-1]]), lens)
+    return starts + np.arange(int(lens.sum()), dtype=np.int64)
 
 
 def _local_ids(local_globals: np.ndarray, wanted: np.ndarray) -> np.ndarray:
