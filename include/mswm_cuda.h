@@ -196,10 +196,13 @@ int mswm_cuda_eval_profile(mswm_cuda_ctx* ctx, float* eval_ms,
                            int64_t* out_cells, int64_t* out_edges, int cap,
                            int* n);
 
-/* Layout actually chosen at create: ring_derived = 1 when the stencil and
- * weights are rebuilt from per-cell rows, identity_order = 1 when the
- * caller's numbering is kept.  Either pointer may be NULL. */
-int mswm_cuda_layout_info(const mswm_cuda_ctx* ctx, int* ring_derived,
+/* Layout chosen at create: kernel_path 2 = fused tile kernel (stencil and
+ * weights rebuilt from the cell rings on chip), 1 = three kernels walking the
+ * rings through L1, 0 = three kernels streaming explicit stencil tables
+ * (always used when the mesh's stencil is not the reference builder's ring
+ * walk); selectable with MSWM_KERNELS=tile|ringwalk|explicit.
+ * identity_order = 1 when the internal numbering equals the caller's. */
+int mswm_cuda_layout_info(const mswm_cuda_ctx* ctx, int* kernel_path,
                           int* identity_order);
 
 /* Number of this library's kernels one replay of the most recently used

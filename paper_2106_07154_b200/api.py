@@ -341,9 +341,10 @@ class CudaContext:
         return np.array(ms[:k], np.float64), nc[:k], ne[:k]
 
     def layout_info(self) -> dict:
-        rd, ident = C.c_int(0), C.c_int(0)
-        self._check(self.lib.mswm_cuda_layout_info(self.handle, C.byref(rd), C.byref(ident)))
-        return {"ring_derived_stencil": bool(rd.value), "input_order": bool(ident.value)}
+        kp, ident = C.c_int(0), C.c_int(0)
+        self._check(self.lib.mswm_cuda_layout_info(self.handle, C.byref(kp), C.byref(ident)))
+        return {"kernel_path": {0: "explicit", 1: "ringwalk", 2: "tile"}[kp.value],
+                "input_order": bool(ident.value)}
 
     def kernels_per_step(self) -> int:
         n = C.c_int64(0)

@@ -54,6 +54,17 @@ struct DevMesh {
   double g;
 };
 
+// A set of elements: the range [base, base+n_range) followed by list[0..n_list).
+struct Span {
+  int32_t base, n_range;
+  const int32_t* list;
+  int32_t n_list;
+  __device__ __forceinline__ int32_t n() const { return n_range + n_list; }
+  __device__ __forceinline__ int32_t at(int32_t t) const {
+    return t < n_range ? base + t : list[t - n_range];
+  }
+};
+
 // Stage epilogue fused into the output kernel (integrators.cpp:18-52,
 // 231-274, 370-410).  d is the freshly computed tendency of element i.
 enum OpKind : int {
@@ -122,18 +133,18 @@ __device__ __forceinline__ void apply_op(const Op& op, int32_t i, double d) {
 // Phase A: potential vorticity on the closure vertices (operators.cpp:74-86)
 // and kinetic energy on the closure cells (:64-72), one launch.
 __global__ void __launch_bounds__(kBlock) k_vertex_cell(DevMesh M, const double* __restrict__ h,
-                                                       const double* __restrict__ u,
-                                                       const int32_t* __restrict__ vlist, int32_t nv,
-                                                       const int32_t* __restrict__ klist, int32_t nk,
-                                                       double* __restrict__ pv, double* __restrict__ K,
+                                                       const double* __restrict__ u, Span vs,
+                                                       Span ks, double* __restrict__ pv,
+                                                       double* __restrict__ K,
                                                        int32_t* __restrict__ dry,
                                                        const uint32_t* __restrict__ vmask) {
-  // Lists may be null (dense mode: element = thread index, superset of the
-  // closure); the dry check then consults the closure bitmask vmask so only
-  // closure vertices raise, as in operators.cpp:74-84.
+  // Spans may be supersets of the closure (dense ranges, slabs); the dry
+  // check then consults the closure bitmask vmask so only closure vertices
+  // raise, as in operators.cpp:74-84.
   const int32_t t = blockIdx.x * kBlock + threadIdx.x;
+  const int32_t nv = vs.n();
   if (t < nv) {
-    const int32_t v = vlist ? vlist[t] : t;
+    const int32_t v = vs.at(t);
     const uint8_t sb = M.v_sbits[v];
     double hv = 0.0, circ = 0.0;
 #pragma unroll
@@ -150,8 +161,8 @@ __global__ void __launch_bounds__(kBlock) k_vertex_cell(DevMesh M, const double*
       return;
     }
     pv[v] = (M.f[v] + circ / M.v_area[v]) / hv;
-  } else if (t - nv < nk) {
-    const int32_t i = klist ? klist[t - nv] : t - nv;
+  } else if (t - nv < ks.n()) {
+    const int32_t i = ks.at(t - nv);
     const int deg = M.c_deg[i];
     double acc = 0.0;
     for (int j = 0; j < deg; ++j) {
@@ -168,12 +179,11 @@ __global__ void __launch_bounds__(kBlock) k_vertex_cell(DevMesh M, const double*
 // of phase C reads both with one 16-byte gather.
 __global__ void __launch_bounds__(kBlock) k_edge_fq(DevMesh M, const double* __restrict__ h,
                                                    const double* __restrict__ u,
-                                                   const double* __restrict__ pv,
-                                                   const int32_t* __restrict__ elist, int32_t ne,
+                                                   const double* __restrict__ pv, Span es,
                                                    double2* __restrict__ FQ) {
   const int32_t t = blockIdx.x * kBlock + threadIdx.x;
-  if (t >= ne) return;
-  const int32_t e = elist ? elist[t] : t;
+  if (t >= es.n()) return;
+  const int32_t e = es.at(t);
   const int2 c = M.e_cells[e];
   const int2 v = M.e_verts[e];
   const double F = 0.5 * (h[c.x] + h[c.y]) * u[e];
@@ -186,10 +196,10 @@ __global__ void __launch_bounds__(kBlock) k_edge_fq(DevMesh M, const double* __r
 // [0, nc) take cells, [nc, nc+ne) edges; lists are group-concatenated and
 // split into two epilogue segments at csplit / esplit.
 struct OutArgs {
-  const int32_t* clist;   // null: dense over all cells, membership from ckey
-  int32_t nc, csplit;
-  const int32_t* elist;   // null: dense over all edges, membership from ekey
-  int32_t ne, esplit;
+  const int32_t* clist;   // null: dense over cells [cbase, cbase+nc), membership from ckey
+  int32_t nc, csplit, cbase;
+  const int32_t* elist;   // null: dense over edges [ebase, ebase+ne), membership from ekey
+  int32_t ne, esplit, ebase;
   const uint8_t* ckey;    // GroupBit index per cell (dense mode; null = all, segment 0)
   const uint8_t* ekey;    // GroupBit index - 6 per edge
   uint32_t mask;
@@ -208,7 +218,7 @@ __global__ void __launch_bounds__(kBlock) k_out(DevMesh M, const double* __restr
       i = a.clist[t];
       seg = t < a.csplit ? 0 : 1;
     } else {
-      i = t;
+      i = a.cbase + t;
       const int g = a.ckey ? a.ckey[i] : 0;
       if (g > 5 || !((a.mask >> g) & 1u)) return;  // 0xFF: not an output of this rank
       seg = g <= 2 ? 0 : 1;
@@ -234,7 +244,7 @@ __global__ void __launch_bounds__(kBlock) k_out(DevMesh M, const double* __restr
       e = a.elist[q];
       seg = q < a.esplit ? 0 : 1;
     } else {
-      e = q;
+      e = a.ebase + q;
       const int g = a.ekey ? a.ekey[e] : 0;
       if (g > 4 || !((a.mask >> (6 + g)) & 1u)) return;
       seg = g <= 1 ? 0 : 1;
@@ -612,6 +622,202 @@ __global__ void __launch_bounds__(kBlock) k_compact_scatter(const uint8_t* __res
     }
     __syncthreads();
   }
+}
+
+}  // namespace mswm_dev
+
+namespace mswm_dev {
+
+// ---------------------------------------------------------------------------
+// Fused tile evaluation.  A tile is kTileCells consecutive internal cells
+// (a compact blob along the Hilbert curve); its CTA evaluates everything the
+// tile's outputs need from h and u, keeping the intermediates on chip:
+//   P1  q_v on V_req = ring vertices of C1 (operators.cpp:74-86)
+//   P2  K on C1 = tile cells + their ring neighbours (:64-72), and the
+//       kite/A ring rows of C1 for the weight walk
+//   P3  F, q~ (and l) on E_req = ring edges of C1 (:61-62, :88-89)
+//   P4  dh on the tile's cells (:91-99)
+//   P5  du on the edges the tile owns (min-rank cell in the tile) (:101-116),
+//       stencil and weights rebuilt from the C1 rings (mesh_build.cpp:133-154,
+//       343-362; verified bitwise at create)
+// each followed by the fused stage epilogue.  Values computed for halo
+// elements are never outputs, so per-element results equal the reference.
+constexpr int kTileCells = 128;  // default; MSWM_TILE_CELLS overrides at create
+constexpr int kTileThreads = 256;
+
+struct TileMeta {
+  // owned ranges first (no index lists), then the halo from the lists:
+  // C1 = cells [c0, c0+nc) + c1_ids[c1_off .. nc1-nc); E_req = edges
+  // [e0, e0+ne) + er_ids[..]; V_req = vertices [v0, v0+nvo) + vr_ids[..]
+  int32_t c0, nc, nc1, c1h_off, c1r_off;
+  int32_t e0, ne, ner, erh_off, erv_off;
+  int32_t v0, nvo, nvr, vrh_off;
+};
+
+struct TileArgs {
+  const TileMeta* meta;
+  const int32_t* list;      // tiles to run (those with outputs in the mask)
+  const int32_t* c1_ids;    // per tile: C1 halo cells
+  const uint4* c1_ring;     // per C1 cell: ring edges as E_req-local uint16 x 8
+  const int32_t* er_ids;    // per tile: E_req halo edges
+  const ushort2* er_vloc;   // per E_req edge: V_req-local ids of its vertices
+  const int32_t* vr_ids;    // per tile: V_req halo vertices
+  const ushort2* oe_c1;     // per edge: C1-local ids of edge_cells[e][0], [1] in its tile
+  const uint32_t* vmask;    // closure bitmask of the mask (dry check filter), null = all
+  int32_t* dry;
+};
+
+__device__ __forceinline__ int ring16(const uint4& r, int s) {
+  const uint32_t w = s < 4 ? (s < 2 ? r.x : r.y) : (s < 6 ? r.z : r.w);
+  return (s & 1) ? int(w >> 16) : int(w & 0xFFFFu);
+}
+
+__global__ void __launch_bounds__(kTileThreads, 4) k_tile(DevMesh M, TileArgs T,
+                                                      const double* __restrict__ h,
+                                                      const double* __restrict__ u, OutArgs a) {
+  extern __shared__ double sm[];
+  const TileMeta tm = T.meta[T.list[blockIdx.x]];
+  double* sPV = sm;
+  double* sK = sPV + tm.nvr;
+  double* sR = sK + tm.nc1;
+  double* sF = sR + size_t(tm.nc1) * kMaxDeg;
+  double* sQ = sF + tm.ner;
+  double* sL = sQ + tm.ner;
+
+  // P1: potential vorticity on V_req
+#pragma unroll 2
+  for (int k = threadIdx.x; k < tm.nvr; k += kTileThreads) {
+    const int32_t v = k < tm.nvo ? tm.v0 + k : T.vr_ids[tm.vrh_off + k - tm.nvo];
+    const uint8_t sb = M.v_sbits[v];
+    double hv = 0.0, circ = 0.0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      hv += M.v_kite[j * M.nV + v] * h[M.v_cell[j * M.nV + v]];
+      const int32_t e = M.v_edge[j * M.nV + v];
+      const double d = M.e_dual[e];
+      circ += ((sb >> j) & 1 ? -d : d) * u[e];
+    }
+    hv /= M.v_area[v];
+    if (!(hv > 0.0)) {
+      if (!T.vmask || ((T.vmask[v >> 5] >> (v & 31)) & 1u)) atomicMin(T.dry, M.v_orig[v]);
+      sPV[k] = 0.0;
+    } else {
+      sPV[k] = (M.f[v] + circ / M.v_area[v]) / hv;
+    }
+  }
+  // P2: kinetic energy and kite/A rows on C1
+#pragma unroll 2
+  for (int k = threadIdx.x; k < tm.nc1; k += kTileThreads) {
+    const int32_t i = k < tm.nc ? tm.c0 + k : T.c1_ids[tm.c1h_off + k - tm.nc];
+    const int deg = M.c_deg[i];
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < kMaxDeg; ++j) {
+      if (j < deg) {
+        const int32_t e = M.c_edge[j * M.nC + i];
+        const double ue = u[e];
+        acc += M.e_ld[e] * ue * ue;
+        sR[k * kMaxDeg + j] = M.c_ratio[j * M.nC + i];
+      }
+    }
+    sK[k] = acc / (4.0 * M.c_area[i]);
+  }
+  __syncthreads();
+  // P3: F, q~ and l on E_req
+#pragma unroll 2
+  for (int k = threadIdx.x; k < tm.ner; k += kTileThreads) {
+    const int32_t e = k < tm.ne ? tm.e0 + k : T.er_ids[tm.erh_off + k - tm.ne];
+    const int2 c = M.e_cells[e];
+    const ushort2 vl = T.er_vloc[tm.erv_off + k];
+    sF[k] = 0.5 * (h[c.x] + h[c.y]) * u[e];
+    sQ[k] = 0.5 * (sPV[vl.x] + sPV[vl.y]);
+    sL[k] = M.e_len[e];
+  }
+  __syncthreads();
+  // P4: thickness tendency on the tile's cells
+  for (int k = threadIdx.x; k < tm.nc; k += kTileThreads) {
+    const int32_t i = tm.c0 + k;
+    const int g = a.ckey ? a.ckey[i] : 0;
+    if (g > 5 || !((a.mask >> g) & 1u)) continue;
+    const int seg = g <= 2 ? 0 : 1;
+    const uint4 ring = T.c1_ring[tm.c1r_off + k];
+    const int deg = M.c_deg[i];
+    const uint8_t sb = M.c_sbits[i];
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < kMaxDeg; ++j) {
+      if (j < deg) {
+        const int el = ring16(ring, j);
+        const double l = sL[el];
+        acc += ((sb >> j) & 1 ? -l : l) * sF[el];
+      }
+    }
+    apply_op(a.cop[seg], i, -acc / M.c_area[i]);
+  }
+  // P5: momentum tendency on the edges the tile owns
+#pragma unroll 2
+  for (int k = threadIdx.x; k < tm.ne; k += kTileThreads) {
+    const int32_t e = tm.e0 + k;
+    const int g = a.ekey ? a.ekey[e] : 0;
+    if (g > 4 || !((a.mask >> (6 + g)) & 1u)) continue;
+    const int seg = g <= 1 ? 0 : 1;
+    const ushort2 cl = T.oe_c1[e];
+    const double qt_e = sQ[k];
+    const double inv_d = M.e_invd[e];
+    const int2 cc = M.e_cells[e];
+    const uint8_t sl = M.e_slots[e];
+    double pvflux = 0.0;
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const int32_t c = side ? cc.y : cc.x;
+      const int lc = side ? cl.y : cl.x;
+      const int p = side ? ((sl >> 3) & 7) : (sl & 7);
+      const unsigned aneg = (sl >> (6 + side)) & 1u;
+      const int deg = M.c_deg[c];
+      const uint8_t sb = M.c_sbits[c];
+      const uint4 ring = T.c1_ring[tm.c1r_off + lc];
+      const double* rr = sR + lc * kMaxDeg;
+      double frac = 0.0;
+#pragma unroll
+      for (int kk = 1; kk < kMaxDeg; ++kk) {
+        if (kk < deg) {
+          int sp = p + kk - 1;
+          if (sp >= deg) sp -= deg;
+          int s = p + kk;
+          if (s >= deg) s -= deg;
+          frac += rr[sp];
+          const int el = ring16(ring, s);
+          const double x = frac - 0.5;
+          const double w = (((sb >> s) & 1u) ^ aneg) ? -x : x;
+          const double coef = w * (sL[el] * inv_d);
+          pvflux += coef * sF[el] * (0.5 * (qt_e + sQ[el]));
+        }
+      }
+    }
+    const double psi_lo = M.g * (h[cc.x] + M.b[cc.x]) + sK[cl.x];
+    const double psi_hi = M.g * (h[cc.y] + M.b[cc.y]) + sK[cl.y];
+    apply_op(a.eop[seg], e, -pvflux - (psi_lo - psi_hi) * inv_d);
+  }
+}
+
+// Drop dead intermediate lines from L2 without writing them back
+// (discard.global.L2, 128-byte lines): every evaluation rewrites PV, K and
+// (F, q~) before reading them.
+__global__ void k_discard(char* base, int64_t lines) {
+  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < lines) asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + 128 * k) : "memory");
+}
+
+// tiles holding at least one output of a mask
+__global__ void k_mark_tiles(const int32_t* __restrict__ clist, int32_t nc,
+                             const int32_t* __restrict__ elist, int32_t ne,
+                             const int32_t* __restrict__ e_tile, uint8_t* __restrict__ flag,
+                             int32_t tile_cells) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nc)
+    flag[clist[t] / tile_cells] = 1;
+  else if (t - nc < ne)
+    flag[e_tile[elist[t - nc]]] = 1;
 }
 
 }  // namespace mswm_dev

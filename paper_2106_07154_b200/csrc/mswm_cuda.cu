@@ -119,6 +119,8 @@ struct MaskPlan {
   // the mesh: no index-list traffic, perfectly coalesced own-element access
   bool dense_v = false, dense_k = false, dense_fq = false, dense_out = false;
   DArr<uint32_t> vmask;  // closure bitmask for the dense dry-vertex check
+  DArr<int32_t> tiles;   // fused path: tiles holding outputs of this mask
+  int32_t ntiles = 0;
   std::vector<int32_t> host_cells, host_edges;  // original ids, same order as device lists
 };
 
@@ -207,6 +209,22 @@ struct mswm_cuda_ctx {
   DArr<uint8_t> c_deg, c_sbits, v_sbits, e_nst, e_slots;
   DArr<double> c_area, c_ratio, v_kite, v_area, e_len, e_ld, e_dual, e_invd, e_coef, b, f;
   bool ring_derived = false;
+  bool tile_path = false;
+  bool l2_discard = true;
+  // fused tile kernel structures (k_tile)
+  DArr<TileMeta> t_meta;
+  DArr<int32_t> t_c1_ids, t_er_ids, t_vr_ids, t_e_tile;
+  DArr<uint4> t_c1_ring;
+  DArr<ushort2> t_er_vloc, t_oe_c1;
+
+  int32_t n_tiles = 0, tile_cells = 0;
+  // L2-blocked slabs of the three-kernel path (see build_slabs)
+  struct Slab {
+    int32_t c0, nc, e0, ne, v0, nv;
+    DArr<int32_t> khalo, ehalo, vhalo;
+  };
+  std::vector<Slab> slabs;
+  size_t tile_smem = 0;
   DArr<int2> e_cells, e_verts;
   double gravity = 9.80616;
   bool have_fields = false;
@@ -286,6 +304,7 @@ struct mswm_cuda_ctx {
     M.c_sbits = c_sbits.p;
     M.c_area = c_area.p;
     M.c_ratio = c_ratio.p;
+    if (!ring_derived) M.c_ratio = tile_path ? c_ratio.p : nullptr;
     M.v_cell = v_cell.p;
     M.v_edge = v_edge.p;
     M.v_kite = v_kite.p;
@@ -299,7 +318,7 @@ struct mswm_cuda_ctx {
     M.e_dual = e_dual.p;
     M.e_invd = e_invd.p;
     M.e_nst = e_nst.p;
-    M.e_slots = ring_derived ? e_slots.p : nullptr;
+    M.e_slots = (ring_derived || tile_path) ? e_slots.p : nullptr;
     M.e_sten = e_sten.p;
     M.e_coef = e_coef.p;
     M.b = b.p;
@@ -422,19 +441,9 @@ void make_orders(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell_
   c->c_new2old.resize(nC);
   c->e_new2old.resize(nE);
   c->v_new2old.resize(nV);
-  if (!cell_order) {
-    std::iota(c->c_new2old.begin(), c->c_new2old.end(), 0);
-    std::iota(c->e_new2old.begin(), c->e_new2old.end(), 0);
-    std::iota(c->v_new2old.begin(), c->v_new2old.end(), 0);
-    c->c_old2new = c->c_new2old;
-    c->e_old2new = c->e_new2old;
-    c->v_old2new = c->v_new2old;
-    c->identity = true;
-    return;
-  }
   c->c_old2new.assign(nC, -1);
   for (int32_t k = 0; k < nC; ++k) {
-    const int32_t i = cell_order[k];
+    const int32_t i = cell_order ? cell_order[k] : k;
     if (i < 0 || i >= nC || c->c_old2new[i] != -1)
       throw Error(MSWM_E_USAGE, "cell_order is not a permutation of the cells");
     c->c_old2new[i] = k;
@@ -476,7 +485,13 @@ void make_orders(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell_
       c->v_old2new[key[k].v] = k;
     }
   }
-  c->identity = false;
+  // (edges and vertices are always sorted by their cells so the tiles of
+  // the fused kernel own contiguous edge ranges)
+  bool ident = true;
+  for (int32_t k = 0; k < nC && ident; ++k) ident = c->c_new2old[k] == k;
+  for (int32_t k = 0; k < nE && ident; ++k) ident = c->e_new2old[k] == k;
+  for (int32_t k = 0; k < nV && ident; ++k) ident = c->v_new2old[k] == k;
+  c->identity = ident;
 }
 
 // Is the caller's stencil the ring walk of mesh_build.cpp:133-154 with the
@@ -531,6 +546,267 @@ bool derive_ring_stencil(const mswm_mesh_desc* d, std::vector<double>& kite_of_s
   return true;
 }
 
+// Tiles of the fused kernel: kTileCells consecutive internal cells; C1 = the
+// tile's cells plus their ring neighbours; E_req / V_req = ring edges /
+// vertices of C1; owned edges = edges whose lower internal cell is in the
+// tile (a contiguous range, edges being sorted by their cells).  Local ids
+// are uint16.
+// Tiles of the fused kernel: TC consecutive internal cells.  C1 = the tile's
+// cells plus their ring neighbours; E_req / V_req = ring edges / vertices of
+// C1.  The tile owns the edges and vertices whose lowest internal cell is in
+// the tile -- contiguous ranges, edges and vertices being sorted by their
+// cells -- and lists them first in its local numbering, so only halo elements
+// need index lists.  Local ids are uint16.  Returns false (three-kernel path)
+// when a closure does not fit (cell order without locality).
+bool build_tiles(mswm_cuda_ctx* c, const std::vector<int32_t>& c_edge,
+                 const std::vector<int32_t>& c_vert, const std::vector<int32_t>& c_nbr,
+                 const std::vector<uint8_t>& c_deg, const std::vector<int2>& e_cells,
+                 const std::vector<int2>& e_verts) {
+  const int32_t nC = c->nC, nE = c->nE, nV = c->nV;
+  int32_t TC = kTileCells;
+  if (const char* ts = std::getenv("MSWM_TILE_CELLS")) TC = std::max(32, std::min(1024, std::atoi(ts)));
+  const int32_t nT = (nC + TC - 1) / TC;
+  // owned ranges: first edge / vertex of every tile
+  auto ranges = [&](int32_t n, auto tile_of, std::vector<int32_t>& first) {
+    first.assign(nT + 1, n);
+    int32_t prev = -1;
+    for (int32_t x = 0; x < n; ++x) {
+      const int32_t t = tile_of(x);
+      if (t < prev) return false;
+      for (int32_t q = prev + 1; q <= t; ++q) first[q] = x;
+      prev = t;
+    }
+    for (int32_t q = prev + 1; q <= nT; ++q) first[q] = n;
+    return true;
+  };
+  // vertex -> min internal cell needs the vertex cells; recover them from the rings
+  std::vector<int32_t> vmin(nV, INT32_MAX);
+  for (int32_t i = 0; i < nC; ++i)
+    for (int j = 0; j < c_deg[i]; ++j) {
+      const int32_t v = c_vert[size_t(j) * nC + i];
+      vmin[v] = std::min(vmin[v], i);
+    }
+  std::vector<int32_t> e_first, v_first, e_tile(nE);
+  if (!ranges(nE, [&](int32_t e) { return std::min(e_cells[e].x, e_cells[e].y) / TC; }, e_first))
+    return false;
+  if (!ranges(nV, [&](int32_t v) { return vmin[v] / TC; }, v_first)) return false;
+  for (int32_t e = 0; e < nE; ++e) e_tile[e] = std::min(e_cells[e].x, e_cells[e].y) / TC;
+  std::vector<TileMeta> meta(nT);
+  std::vector<int32_t> c1h, erh, vrh;
+  std::vector<uint4> c1_ring;
+  std::vector<ushort2> er_vloc, oe_c1(nE);
+  std::vector<int32_t> cmark(nC, -1), emark(nE, -1), vmark(nV, -1);
+  std::vector<int32_t> cloc(nC, 0), eloc(nE, 0), vloc(nV, 0);
+  size_t smem_max = 0;
+  std::vector<int32_t> halo, ers, vrs;
+  for (int32_t t = 0; t < nT; ++t) {
+    TileMeta& m = meta[t];
+    m.c0 = t * TC;
+    m.nc = std::min(TC, nC - m.c0);
+    m.e0 = e_first[t];
+    m.ne = e_first[t + 1] - e_first[t];
+    m.v0 = v_first[t];
+    m.nvo = v_first[t + 1] - v_first[t];
+    // C1: tile cells, then halo (ascending)
+    for (int32_t i = m.c0; i < m.c0 + m.nc; ++i) {
+      cmark[i] = t;
+      cloc[i] = i - m.c0;
+    }
+    halo.clear();
+    for (int32_t i = m.c0; i < m.c0 + m.nc; ++i)
+      for (int j = 0; j < c_deg[i]; ++j) {
+        const int32_t nb = c_nbr[size_t(j) * nC + i];
+        if (cmark[nb] != t) {
+          cmark[nb] = t;
+          halo.push_back(nb);
+        }
+      }
+    std::sort(halo.begin(), halo.end());
+    m.c1h_off = int32_t(c1h.size());
+    for (size_t k = 0; k < halo.size(); ++k) {
+      cloc[halo[k]] = m.nc + int32_t(k);
+      c1h.push_back(halo[k]);
+    }
+    m.nc1 = m.nc + int32_t(halo.size());
+    // E_req / V_req: owned ranges first, then the rest ascending
+    for (int32_t e = m.e0; e < m.e0 + m.ne; ++e) {
+      emark[e] = t;
+      eloc[e] = e - m.e0;
+    }
+    for (int32_t v = m.v0; v < m.v0 + m.nvo; ++v) {
+      vmark[v] = t;
+      vloc[v] = v - m.v0;
+    }
+    ers.clear();
+    vrs.clear();
+    auto c1_cell = [&](int32_t k) { return k < m.nc ? m.c0 + k : halo[k - m.nc]; };
+    for (int32_t k = 0; k < m.nc1; ++k) {
+      const int32_t i = c1_cell(k);
+      for (int j = 0; j < c_deg[i]; ++j) {
+        const int32_t e = c_edge[size_t(j) * nC + i], v = c_vert[size_t(j) * nC + i];
+        if (emark[e] != t) {
+          emark[e] = t;
+          ers.push_back(e);
+        }
+        if (vmark[v] != t) {
+          vmark[v] = t;
+          vrs.push_back(v);
+        }
+      }
+    }
+    std::sort(ers.begin(), ers.end());
+    std::sort(vrs.begin(), vrs.end());
+    m.ner = m.ne + int32_t(ers.size());
+    m.nvr = m.nvo + int32_t(vrs.size());
+    if (m.nc1 > 65535 || m.ner > 65535 || m.nvr > 65535) return false;
+    m.erh_off = int32_t(erh.size());
+    for (size_t k = 0; k < ers.size(); ++k) {
+      eloc[ers[k]] = m.ne + int32_t(k);
+      erh.push_back(ers[k]);
+    }
+    m.vrh_off = int32_t(vrh.size());
+    for (size_t k = 0; k < vrs.size(); ++k) {
+      vloc[vrs[k]] = m.nvo + int32_t(k);
+      vrh.push_back(vrs[k]);
+    }
+    m.erv_off = int32_t(er_vloc.size());
+    for (int32_t k = 0; k < m.ner; ++k) {
+      const int32_t e = k < m.ne ? m.e0 + k : ers[k - m.ne];
+      const int2 v = e_verts[e];
+      if (vmark[v.x] != t || vmark[v.y] != t) return false;
+      er_vloc.push_back(make_ushort2(uint16_t(vloc[v.x]), uint16_t(vloc[v.y])));
+    }
+    m.c1r_off = int32_t(c1_ring.size());
+    for (int32_t k = 0; k < m.nc1; ++k) {
+      const int32_t i = c1_cell(k);
+      uint16_t r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int j = 0; j < c_deg[i]; ++j) r[j] = uint16_t(eloc[c_edge[size_t(j) * nC + i]]);
+      c1_ring.push_back(make_uint4(r[0] | (uint32_t(r[1]) << 16), r[2] | (uint32_t(r[3]) << 16),
+                                   r[4] | (uint32_t(r[5]) << 16), r[6] | (uint32_t(r[7]) << 16)));
+    }
+    for (int32_t e = m.e0; e < m.e0 + m.ne; ++e) {
+      const int2 cc = e_cells[e];
+      if (cmark[cc.x] != t || cmark[cc.y] != t) return false;
+      oe_c1[e] = make_ushort2(uint16_t(cloc[cc.x]), uint16_t(cloc[cc.y]));
+    }
+    const size_t smem = 8 * (size_t(m.nvr) + m.nc1 + size_t(m.nc1) * kMaxDeg + 3 * size_t(m.ner));
+    smem_max = std::max(smem_max, smem);
+  }
+  if (smem_max > 200 * 1024) return false;  // poor locality: use the three-kernel path
+  cudaStream_t s = c->stream;
+  c->n_tiles = nT;
+  c->tile_cells = TC;
+  c->tile_smem = smem_max;
+  c->t_meta.upload(meta, s);
+  c->t_c1_ids.upload(c1h, s);
+  c->t_c1_ring.upload(c1_ring, s);
+  c->t_er_ids.upload(erh, s);
+  c->t_er_vloc.upload(er_vloc, s);
+  c->t_vr_ids.upload(vrh, s);
+  c->t_oe_c1.upload(oe_c1, s);
+  c->t_e_tile.upload(e_tile, s);
+  CK(cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_max)));
+  CK(cudaStreamSynchronize(s));
+  return true;
+}
+
+// L2 blocking of the three-kernel path: slabs of SC consecutive internal
+// cells (a compact region along the Hilbert curve).  A slab owns its cells,
+// the edges and vertices whose lowest internal cell it holds (contiguous
+// ranges) and lists the halo it additionally needs: K on the cells' ring
+// neighbours, (F, q~) on every ring edge of those cells, PV on their ring
+// vertices.  Evaluating a dense mask slab by slab (A, B, C per slab) keeps
+// each slab's intermediates and inputs L2-resident between the kernels.
+void build_slabs(mswm_cuda_ctx* c, const std::vector<int32_t>& c_edge,
+                 const std::vector<int32_t>& c_vert, const std::vector<int32_t>& c_nbr,
+                 const std::vector<uint8_t>& c_deg, const std::vector<int2>& e_cells) {
+  const int32_t nC = c->nC, nE = c->nE, nV = c->nV;
+  // Opt-in (MSWM_SLAB_CELLS): measured slower than one pass on C4 -- the
+  // kernel boundaries cost more than the L2 reuse saves (profiles/r1_*).
+  const char* ss = std::getenv("MSWM_SLAB_CELLS");
+  if (!ss) return;
+  const int32_t SC = std::max(1024, std::atoi(ss));
+  if (const char* dd = std::getenv("MSWM_L2_DISCARD")) c->l2_discard = dd[0] != '0';
+  c->slabs.clear();
+  const int32_t nS = (nC + SC - 1) / SC;
+  if (nS < 2) return;
+  std::vector<int32_t> vmin(nV, INT32_MAX);
+  for (int32_t i = 0; i < nC; ++i)
+    for (int j = 0; j < c_deg[i]; ++j) {
+      const int32_t v = c_vert[size_t(j) * nC + i];
+      vmin[v] = std::min(vmin[v], i);
+    }
+  // owned ranges (edges / vertices are sorted by their lowest cell)
+  std::vector<int32_t> ef(nS + 1, nE), vf(nS + 1, nV);
+  {
+    int32_t prev = -1;
+    for (int32_t e = 0; e < nE; ++e) {
+      const int32_t t = std::min(e_cells[e].x, e_cells[e].y) / SC;
+      if (t < prev) return;  // not sorted: no slabs
+      for (int32_t q = prev + 1; q <= t; ++q) ef[q] = e;
+      prev = t;
+    }
+    for (int32_t q = prev + 1; q <= nS; ++q) ef[q] = nE;
+    prev = -1;
+    for (int32_t v = 0; v < nV; ++v) {
+      const int32_t t = vmin[v] / SC;
+      if (t < prev) return;
+      for (int32_t q = prev + 1; q <= t; ++q) vf[q] = v;
+      prev = t;
+    }
+    for (int32_t q = prev + 1; q <= nS; ++q) vf[q] = nV;
+  }
+  std::vector<int32_t> cmark(nC, -1), emark(nE, -1), vmark(nV, -1);
+  std::vector<int32_t> kh, eh, vh;
+  c->slabs.resize(nS);
+  for (int32_t t = 0; t < nS; ++t) {
+    auto& sl = c->slabs[t];
+    sl.c0 = t * SC;
+    sl.nc = std::min(SC, nC - sl.c0);
+    sl.e0 = ef[t];
+    sl.ne = ef[t + 1] - ef[t];
+    sl.v0 = vf[t];
+    sl.nv = vf[t + 1] - vf[t];
+    kh.clear();
+    eh.clear();
+    vh.clear();
+    auto own_c = [&](int32_t i) { return i >= sl.c0 && i < sl.c0 + sl.nc; };
+    auto own_e = [&](int32_t e) { return e >= sl.e0 && e < sl.e0 + sl.ne; };
+    auto own_v = [&](int32_t v) { return v >= sl.v0 && v < sl.v0 + sl.nv; };
+    auto visit = [&](int32_t i) {  // ring edges / vertices of a C1 cell
+      for (int j = 0; j < c_deg[i]; ++j) {
+        const int32_t e = c_edge[size_t(j) * nC + i], v = c_vert[size_t(j) * nC + i];
+        if (!own_e(e) && emark[e] != t) {
+          emark[e] = t;
+          eh.push_back(e);
+        }
+        if (!own_v(v) && vmark[v] != t) {
+          vmark[v] = t;
+          vh.push_back(v);
+        }
+      }
+    };
+    for (int32_t i = sl.c0; i < sl.c0 + sl.nc; ++i) {
+      visit(i);
+      for (int j = 0; j < c_deg[i]; ++j) {
+        const int32_t nb = c_nbr[size_t(j) * nC + i];
+        if (!own_c(nb) && cmark[nb] != t) {
+          cmark[nb] = t;
+          kh.push_back(nb);
+        }
+      }
+    }
+    for (int32_t nb : kh) visit(nb);
+    std::sort(kh.begin(), kh.end());
+    std::sort(eh.begin(), eh.end());
+    std::sort(vh.begin(), vh.end());
+    sl.khalo.upload(kh, c->stream);
+    sl.ehalo.upload(eh, c->stream);
+    sl.vhalo.upload(vh, c->stream);
+    CK(cudaStreamSynchronize(c->stream));
+  }
+}
+
 void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell_order) {
   const int32_t nC = d->n_cells, nE = d->n_edges, nV = d->n_vertices;
   if (nC <= 0 || nE <= 0 || nV <= 0) throw Error(MSWM_E_TOPOLOGY, "empty mesh");
@@ -577,12 +853,19 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
 
   std::vector<double> kite_of_slot;
   std::vector<uint8_t> slots;
-  // The explicit-table path is the default: on the Hilbert layout its
-  // coalesced stencil streams beat the L1-gather-bound ring walk (profiles/
-  // r1_v2_*).  MSWM_RING_DERIVED=1 selects the ring-derived path when the
-  // mesh qualifies (tests cover both).
-  const char* want = std::getenv("MSWM_RING_DERIVED");
-  c->ring_derived = (want && want[0] == '1') && derive_ring_stencil(d, kite_of_slot, slots);
+  // Evaluation path (MSWM_KERNELS): "explicit" (default) = three kernels
+  // streaming the stencil tables (DRAM-roofline-bound, profiles/); "tile" = the fused tile
+  // kernel, needs the ring-derived stencil; "explicit" = three kernels with
+  // the stencil tables streamed; "ringwalk" = three kernels walking the
+  // rings through L1.  Meshes whose stencil is not the reference builder's
+  // ring walk always take "explicit".  Tests cover all three.
+  const bool eligible = derive_ring_stencil(d, kite_of_slot, slots);
+  const char* kv = std::getenv("MSWM_KERNELS");
+  const std::string kind = kv ? kv : "explicit";
+  c->tile_path = eligible && kind == "tile";
+  c->ring_derived = eligible && kind == "ringwalk";
+  const bool need_ratio = c->tile_path || c->ring_derived;
+  bool need_explicit = !need_ratio;
 
   // cells
   std::vector<int32_t> c_edge(size_t(deg_max) * nC, 0), c_vert(size_t(deg_max) * nC, 0),
@@ -590,7 +873,7 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   std::vector<uint8_t> c_deg(nC), c_sbits(nC, 0);
   std::vector<double> c_area(nC);
   std::vector<double> c_ratio;
-  if (c->ring_derived) c_ratio.assign(size_t(deg_max) * nC, 0.0);
+  if (need_ratio) c_ratio.assign(size_t(deg_max) * nC, 0.0);
   for (int32_t ni = 0; ni < nC; ++ni) {
     const int32_t i = cn[ni];
     const int off = d->cell_offset[i], deg = d->cell_offset[i + 1] - off;
@@ -607,7 +890,7 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
       const int8_t sg = d->edge_cells[2 * e] == i ? d->edge_cell_sign[2 * e] : d->edge_cell_sign[2 * e + 1];
       if (sg < 0) c_sbits[ni] |= uint8_t(1u << j);
       // mesh_build.cpp:354: kite_area[slot] / cell_area[i]
-      if (c->ring_derived) c_ratio[size_t(j) * nC + ni] = kite_of_slot[off + j] / d->cell_area[i];
+      if (need_ratio) c_ratio[size_t(j) * nC + ni] = kite_of_slot[off + j] / d->cell_area[i];
     }
   }
   c->h_cell_area.assign(d->cell_area, d->cell_area + nC);
@@ -632,13 +915,22 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   }
   // edges
   std::vector<int2> e_cells(nE), e_verts(nE);
+  for (int32_t ne = 0; ne < nE; ++ne) {
+    const int32_t e = en[ne];
+    e_cells[ne] = make_int2(co[d->edge_cells[2 * e]], co[d->edge_cells[2 * e + 1]]);
+    e_verts[ne] = make_int2(vo[d->edge_vertices[2 * e]], vo[d->edge_vertices[2 * e + 1]]);
+  }
+  if (c->tile_path && !build_tiles(c, c_edge, c_vert, c_nbr, c_deg, e_cells, e_verts)) {
+    c->tile_path = false;  // closures too large for shared memory (poor cell order)
+    need_explicit = true;
+  }
+  if (!c->tile_path) build_slabs(c, c_edge, c_vert, c_nbr, c_deg, e_cells);
   std::vector<double> e_len(nE), e_ld(nE), e_dual(nE), e_invd(nE);
   std::vector<uint8_t> e_nst, e_slots;
   std::vector<int32_t> e_sten;
   std::vector<double> e_coef;
-  if (c->ring_derived) {
-    e_slots.resize(nE);
-  } else {
+  if (need_ratio) e_slots.resize(nE);
+  if (need_explicit) {
     e_nst.resize(nE);
     e_sten.assign(size_t(std::max(sten_max, 1)) * nE, 0);
     e_coef.assign(size_t(std::max(sten_max, 1)) * nE, 0.0);
@@ -655,10 +947,8 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
     e_ld[ne] = l * dd;              // operators.cpp:70, first product
     const double inv_d = 1.0 / dd;  // operators.cpp:103
     e_invd[ne] = inv_d;
-    if (c->ring_derived) {
-      e_slots[ne] = slots[e];
-      continue;
-    }
+    if (need_ratio) e_slots[ne] = slots[e];
+    if (!need_explicit) continue;
     const int off = d->edge_edge_offset[e], n = d->edge_edge_offset[e + 1] - off;
     e_nst[ne] = uint8_t(n);
     for (int j = 0; j < n; ++j) {
@@ -844,6 +1134,22 @@ MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
   p->dense_k = p->nk >= int64_t(c->nC) * 85 / 100;
   p->dense_fq = p->nec >= int64_t(c->nE) * 85 / 100;
   p->dense_out = int64_t(p->nc) + p->ne >= (int64_t(c->nC) + c->nE) / 2;
+  if (c->tile_path) {
+    // tiles with outputs; the tiles compute closure supersets, so the dry
+    // check always consults the closure bitmask
+    p->dense_v = true;
+    DArr<uint8_t> tflag;
+    tflag.alloc(size_t(c->n_tiles));
+    tflag.zero(s);
+    if (int64_t(p->nc) + p->ne > 0) {
+      k_mark_tiles<<<nblk(int64_t(p->nc) + p->ne), kBlock, 0, s>>>(p->cells, p->nc, p->edges, p->ne,
+                                                                  c->t_e_tile.p, tflag.p,
+                                                                  c->tile_cells);
+      CK(cudaGetLastError());
+    }
+    k_flag_key<<<nblk(c->n_tiles), kBlock, 0, s>>>(c->n_tiles, tflag.p, key.p);
+    p->ntiles = int32_t(compact(c, key.p, c->n_tiles, 1, p->tiles)[0]);
+  }
   if (p->dense_v && p->nv < c->nV) {
     p->vmask.alloc((size_t(c->nV) + 31) / 32);
     k_pack_bits<<<nblk((int64_t(c->nV) + 31) / 32), kBlock, 0, s>>>(c->nV, mv.p, p->vmask.p);
@@ -891,24 +1197,102 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
     rec->ne = p.ne;
     CK(cudaEventRecordWithFlags(rec->start, s, cudaEventRecordExternal));
   }
+  if (c->tile_path) {
+    if (p.ntiles > 0) {
+      TileArgs T;
+      T.meta = c->t_meta.p;
+      T.list = p.tiles.p;
+      T.c1_ids = c->t_c1_ids.p;
+      T.c1_ring = c->t_c1_ring.p;
+      T.er_ids = c->t_er_ids.p;
+      T.er_vloc = c->t_er_vloc.p;
+      T.vr_ids = c->t_vr_ids.p;
+      T.oe_c1 = c->t_oe_c1.p;
+      T.vmask = p.vmask.p;
+      T.dry = c->dry_vertex.p;
+      OutArgs a;
+      std::memset(&a, 0, sizeof(a));
+      a.mask = p.mask;
+      a.ckey = c->have_regions ? c->ckey.p : nullptr;
+      a.ekey = c->have_regions ? c->ekey.p : nullptr;
+      a.cop[0] = cop[0];
+      a.cop[1] = cop[1];
+      a.eop[0] = eop[0];
+      a.eop[1] = eop[1];
+      k_tile<<<p.ntiles, kTileThreads, c->tile_smem, s>>>(M, T, h, u, a);
+      CK(cudaGetLastError());
+      ++c->launches;
+    }
+    if (rec) CK(cudaEventRecordWithFlags(rec->stop, s, cudaEventRecordExternal));
+    return;
+  }
+  if (p.dense_v && p.dense_k && p.dense_fq && p.dense_out && c->slabs.size() > 1) {
+    // L2-blocked: A, B, C per slab so a slab's intermediates and re-read
+    // inputs are still in L2 when the next kernel reads them; then drop the
+    // slab's dead intermediates from L2 without write-back.
+    for (auto& sl : c->slabs) {
+      const Span vs{sl.v0, sl.nv, sl.vhalo.p, int32_t(sl.vhalo.n)};
+      const Span ks{sl.c0, sl.nc, sl.khalo.p, int32_t(sl.khalo.n)};
+      const Span es{sl.e0, sl.ne, sl.ehalo.p, int32_t(sl.ehalo.n)};
+      const int64_t na = int64_t(vs.n_range) + vs.n_list + ks.n_range + ks.n_list;
+      k_vertex_cell<<<nblk(na), kBlock, 0, s>>>(M, h, u, vs, ks, c->pv.p, c->K.p, c->dry_vertex.p,
+                                               p.vmask.p);
+      const int64_t nb_ = int64_t(es.n_range) + es.n_list;
+      k_edge_fq<<<nblk(nb_), kBlock, 0, s>>>(M, h, u, c->pv.p, es, c->FQ.p);
+      OutArgs a;
+      std::memset(&a, 0, sizeof(a));
+      a.mask = p.mask;
+      a.ckey = c->have_regions ? c->ckey.p : nullptr;
+      a.ekey = c->have_regions ? c->ekey.p : nullptr;
+      a.cbase = sl.c0;
+      a.nc = sl.nc;
+      a.ebase = sl.e0;
+      a.ne = sl.ne;
+      a.cop[0] = cop[0];
+      a.cop[1] = cop[1];
+      a.eop[0] = eop[0];
+      a.eop[1] = eop[1];
+      k_out<<<nblk(int64_t(sl.nc) + sl.ne), kBlock, 0, s>>>(M, h, c->K.p, c->FQ.p, a);
+      CK(cudaGetLastError());
+      c->launches += 3;
+      if (c->l2_discard) {
+        auto drop = [&](void* base, size_t bytes_lo, size_t bytes_hi) {
+          const size_t lo = (bytes_lo + 127) / 128, hi = bytes_hi / 128;
+          if (hi > lo) {
+            k_discard<<<nblk(int64_t(hi - lo)), kBlock, 0, s>>>(static_cast<char*>(base) + 128 * lo,
+                                                              int64_t(hi - lo));
+            ++c->launches;
+          }
+        };
+        drop(c->FQ.p, size_t(sl.e0) * 16, size_t(sl.e0 + sl.ne) * 16);
+        drop(c->pv.p, size_t(sl.v0) * 8, size_t(sl.v0 + sl.nv) * 8);
+        drop(c->K.p, size_t(sl.c0) * 8, size_t(sl.c0 + sl.nc) * 8);
+        CK(cudaGetLastError());
+      }
+    }
+    if (rec) CK(cudaEventRecordWithFlags(rec->stop, s, cudaEventRecordExternal));
+    return;
+  }
   const int32_t nv = p.dense_v ? c->nV : p.nv, nk = p.dense_k ? c->nC : p.nk;
   const int64_t na = int64_t(nv) + nk;
   if (p.nv + p.nk > 0) {
-    k_vertex_cell<<<nblk(na), kBlock, 0, s>>>(M, h, u, p.dense_v ? nullptr : p.vclos.p, nv,
-                                             p.dense_k ? nullptr : p.kclos.p, nk, c->pv.p, c->K.p,
-                                             c->dry_vertex.p, p.vmask.p);
+    const Span vs = p.dense_v ? Span{0, nv, nullptr, 0} : Span{0, 0, p.vclos.p, nv};
+    const Span ks = p.dense_k ? Span{0, nk, nullptr, 0} : Span{0, 0, p.kclos.p, nk};
+    k_vertex_cell<<<nblk(na), kBlock, 0, s>>>(M, h, u, vs, ks, c->pv.p, c->K.p, c->dry_vertex.p,
+                                             p.vmask.p);
     CK(cudaGetLastError());
     ++c->launches;
   }
   if (p.nec > 0) {
     const int32_t nfq = p.dense_fq ? c->nE : p.nec;
-    k_edge_fq<<<nblk(nfq), kBlock, 0, s>>>(M, h, u, c->pv.p, p.dense_fq ? nullptr : p.eclos.p, nfq,
-                                          c->FQ.p);
+    const Span es = p.dense_fq ? Span{0, nfq, nullptr, 0} : Span{0, 0, p.eclos.p, nfq};
+    k_edge_fq<<<nblk(nfq), kBlock, 0, s>>>(M, h, u, c->pv.p, es, c->FQ.p);
     CK(cudaGetLastError());
     ++c->launches;
   }
   if (int64_t(p.nc) + p.ne > 0) {
     OutArgs a;
+    std::memset(&a, 0, sizeof(a));
     a.mask = p.mask;
     a.ckey = c->have_regions ? c->ckey.p : nullptr;
     a.ekey = c->have_regions ? c->ekey.p : nullptr;
@@ -1749,9 +2133,9 @@ int mswm_cuda_eval_profile(mswm_cuda_ctx* c, float* eval_ms, int64_t* out_cells,
   });
 }
 
-int mswm_cuda_layout_info(const mswm_cuda_ctx* c, int* ring_derived, int* identity_order) {
+int mswm_cuda_layout_info(const mswm_cuda_ctx* c, int* kernel_path, int* identity_order) {
   if (!c) return MSWM_E_USAGE;
-  if (ring_derived) *ring_derived = c->ring_derived ? 1 : 0;
+  if (kernel_path) *kernel_path = c->tile_path ? 2 : (c->ring_derived ? 1 : 0);
   if (identity_order) *identity_order = c->identity ? 1 : 0;
   return MSWM_OK;
 }

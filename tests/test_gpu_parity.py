@@ -249,11 +249,12 @@ def test_stepper_drop_in_interface():
     assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
 
 
-@pytest.mark.parametrize("explicit", [False, True])
-def test_layouts_are_bitwise_equivalent(explicit, monkeypatch):
+@pytest.mark.parametrize("path", ["tile", "explicit", "ringwalk"])
+def test_layouts_are_bitwise_equivalent(path, monkeypatch):
     """Results are independent of the device numbering (input, Hilbert,
-    random) and of the stencil storage (ring-derived vs explicit tables)."""
-    monkeypatch.setenv("MSWM_RING_DERIVED", "0" if explicit else "1")
+    random) and of the evaluation path (fused tile kernel, explicit stencil
+    tables, ring walk through L1)."""
+    monkeypatch.setenv("MSWM_KERNELS", path)
     wl = W.small_sphere(5, seed=13, cap_deg=20.0)
     o = _oracle_for(wl)
     h_ref, u_ref, _ = o.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, wl.M, 4)
@@ -261,7 +262,9 @@ def test_layouts_are_bitwise_equivalent(explicit, monkeypatch):
     for order in ["input", "hilbert", rng.permutation(wl.mesh.n_cells).astype(np.int32)]:
         ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order)
         info = ctx.layout_info()
-        assert info["ring_derived_stencil"] == (not explicit)
+        # a random numbering has no locality: the tile path declines it
+        assert info["kernel_path"] == path or (path == "tile" and not isinstance(order, str)
+                                               and info["kernel_path"] == "explicit")
         ctx.make_regions(wl.fine_mask, wl.width)
         for a, b in zip(ctx.regions.groups, o.groups()):
             assert np.array_equal(a, b)
