@@ -184,10 +184,12 @@ class RefRunner:
         self.ev = RefEvaluator(self.rm, self.rr, wl.b, wl.f, wl.gravity, nranks=nranks)
         self.h, self.u, self.t = wl.h, wl.u, 0.0
 
-    def steps(self, n: int):
-        """Run n coarse steps; returns (edge evals/s, s/step, edge evals/step)."""
+    def steps(self, n: int, scheme: int = 4, dt: float | None = None):
+        """Run n steps (LTS3 coarse steps by default); returns (edge evals/s,
+        s/step, edge evals/step)."""
         _, e0, s0 = self.ev.ledger()
-        self.h, self.u, self.t, secs = self.ev.step(4, self.h, self.u, self.t, self.wl.dt,
+        dt = self.wl.dt if dt is None else dt
+        self.h, self.u, self.t, secs = self.ev.step(scheme, self.h, self.u, self.t, dt,
                                                     self.wl.M, n)
         _, e1, s1 = self.ev.ledger()
         per = int(e1.sum() - e0.sum()) // max(s1 - s0, 1)
@@ -355,6 +357,30 @@ def run_ours(args, ws, rank, local):
 
     launches = ctx.kernels_per_step() * args.steps
 
+    # the comparison strategy (north_star): global RK4 at the fine step dt/M,
+    # M steps per coarse interval, timed the same way
+    rk4 = None
+    if not args.no_rk4:
+        ctx.reset_ledger()
+        ctx.advance(Scheme.RK4, wl.dt / wl.M, 1, wl.M)  # warm-up + graph
+        ctx.reset_ledger()
+        n_iv = max(1, min(args.steps, 20))
+        barrier(ws)
+        torch.cuda.synchronize()
+        r0 = torch.cuda.Event(enable_timing=True)
+        r1 = torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        ctx.advance(Scheme.RK4, wl.dt / wl.M, 1, wl.M * n_iv, sync=False)
+        r1.record(stream)
+        torch.cuda.synchronize()
+        ctx.sync()
+        rk_ms = allreduce_max(r0.elapsed_time(r1), ws) / n_iv
+        rk_edges = allreduce_sum(ctx.ledger().total_edge_evals(), ws) / n_iv
+        rk4 = {"scheme": "RK4 at dt/M", "ms_per_coarse_interval": rk_ms,
+               "edge_evals_per_s": rk_edges / (rk_ms / 1e3),
+               "edge_evals_per_coarse_interval": rk_edges,
+               "lts3_speedup_vs_rk4": rk_ms / ms_step, "intervals": n_iv}
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         from oracle.oracle import ref_available
@@ -370,6 +396,11 @@ def run_ours(args, ws, rank, local):
                    "sample": f"{args.cpu_steps} LTS3 coarse step(s) of {args.config} after 1 "
                              f"warm-up, reference ThreadedEvaluator {threads} ranks "
                              f"({sps:.3f} s/step)"}
+            if not args.no_rk4:
+                rrate, rsps, _ = runner.steps(1, scheme=2, dt=wl.dt / wl.M)
+                cpu["rk4_fine_dt"] = {"edge_evals_per_s": rrate, "s_per_step": rsps,
+                                      "s_per_coarse_interval": rsps * wl.M,
+                                      "sample": "1 RK4 step at dt/M, same evaluator"}
             del runner
 
     if rank == 0:
@@ -390,6 +421,7 @@ def run_ours(args, ws, rank, local):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": io_bytes,
                     "d2h_bytes_per_step": io_bytes, "steps": n_e2e},
             "cpu_baseline": cpu,
+            "rk4_fine_dt": rk4,
             "gpu_launches": int(launches),
             "clocks": ck,
         }
@@ -405,6 +437,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-rk4", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         log("note: warmup < 3 violates the timing rules; using 3")

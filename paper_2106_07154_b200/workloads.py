@@ -11,8 +11,9 @@ arrays, so parity does not depend on these choices.  Documented choices:
 * Planar fine predicates use minimum-image distance; spherical ones the
   great-circle angle (arc_angle, geometry.hpp:33-35, evaluated on the host).
 * "Geostrophic" velocities come from a vertex streamfunction
-  psi = g*eta/f: u_e = -(psi(+t end) - psi(-t end)) / l_e, which is
-  discretely non-divergent on the TRiSK grid.
+  psi = g*eta/f0: u_e = -(psi(+t end) - psi(-t end)) / l_e, which is
+  discretely non-divergent on the TRiSK grid (f0 = 1e-4 on the beta-plane,
+  whose f jumps across the periodic y-seam; 2 Omega on the sphere).
 * "Spherical-harmonic perturbation of degree <= 32" is realised as a sum of
   random 3-D plane waves cos(k.x + phi) with |k| <= 32 restricted to the
   sphere (band-limited to leading order), scaled to the stated rms.
@@ -140,7 +141,9 @@ def config3(seed: int = 3, n_steps: int = 100, nx: int = 2048) -> Workload:
     eta_c = _planar_field(mesh, mesh.cell_xyz, modes, 2.0)
     eta_v = _planar_field(mesh, mesh.vertex_xyz, modes, 2.0, ref_xy=mesh.cell_xyz)
     h = H + eta_c
-    u = _velocity_from_streamfunction(mesh, GRAVITY * eta_v / f)
+    # balance with f0: psi = g*eta/f would jump across the y-seam of the
+    # periodic beta-plane (f is discontinuous there)
+    u = _velocity_from_streamfunction(mesh, GRAVITY * eta_v / 1e-4)
     b = np.zeros(mesh.n_cells)
     centers, radii = [], []
     while len(centers) < 4:
