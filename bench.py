@@ -266,7 +266,8 @@ def run_ours(args, ws, rank, local):
         f"built in {time.time() - t0:.1f}s")
     rc = None
     if ws == 1:
-        ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, device=local)
+        ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, device=local, order=args.order,
+                          fine_mask=wl.fine_mask, interface_width=wl.width)
         rm = ctx.make_regions(wl.fine_mask, wl.width)
         log(f"[rank {rank}] groups {rm.group_sizes()}")
         ctx.upload(State(wl.h, wl.u, 0.0))
@@ -438,6 +439,8 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rk4", action="store_true")
+    ap.add_argument("--order", default="regions", choices=["regions", "hilbert", "input"],
+                    help="device layout (results are bitwise independent of it)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("note: warmup < 3 violates the timing rules; using 3")

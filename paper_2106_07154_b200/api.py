@@ -204,17 +204,24 @@ class CudaContext:
     """One mswm_cuda_ctx: a mesh resident on one B200."""
 
     def __init__(self, mesh: Mesh, b, f_vertex, gravity: float = 9.80616, device: int = 0,
-                 order="hilbert"):
+                 order="hilbert", fine_mask=None, interface_width: int = 1):
         """order: "hilbert" (space-filling-curve device layout, default),
-        "input" (the caller's numbering) or an explicit cell permutation.
-        Results are bitwise independent of it."""
+        "regions" (region-major: LTS groups contiguous, Hilbert inside; needs
+        fine_mask), "input" (the caller's numbering) or an explicit cell
+        permutation.  Results are bitwise independent of it."""
         self.lib = _lib.cuda()
         self.mesh = mesh
         self._desc = mesh.desc()
         if isinstance(order, str):
-            if order not in ("hilbert", "input"):
+            if order not in ("hilbert", "input", "regions"):
                 raise UsageError(f"unknown order '{order}'")
-            order = mesh.locality_order() if order == "hilbert" else None
+            if order == "regions":
+                if fine_mask is None:
+                    raise UsageError("order='regions' needs the fine mask")
+                from .layout import region_major_order
+                order = region_major_order(mesh, fine_mask, interface_width)
+            else:
+                order = mesh.locality_order() if order == "hilbert" else None
         self._order = None if order is None else np.ascontiguousarray(order, np.int32)
         optr = _p(self._order, _lib.i32p) if self._order is not None else None
         handle = C.c_void_p()

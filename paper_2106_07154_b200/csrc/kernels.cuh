@@ -196,14 +196,12 @@ __global__ void __launch_bounds__(kBlock) k_edge_fq(DevMesh M, const double* __r
 // [0, nc) take cells, [nc, nc+ne) edges; lists are group-concatenated and
 // split into two epilogue segments at csplit / esplit.
 struct OutArgs {
-  const int32_t* clist;   // null: dense over cells [cbase, cbase+nc), membership from ckey
-  int32_t nc, csplit, cbase;
-  const int32_t* elist;   // null: dense over edges [ebase, ebase+ne), membership from ekey
-  int32_t ne, esplit, ebase;
-  const uint8_t* ckey;    // GroupBit index per cell (dense mode; null = all, segment 0)
-  const uint8_t* ekey;    // GroupBit index - 6 per edge
+  Span cs;               // output cells (a superset is fine: membership from ckey)
+  Span es;               // output edges (membership from ekey)
+  const uint8_t* ckey;   // GroupBit index per cell (null = every cell, segment 0)
+  const uint8_t* ekey;   // GroupBit index - 6 per edge; 0xFF: not an output here
   uint32_t mask;
-  Op cop[2];
+  Op cop[2];             // segment 0 = fine groups, 1 = the rest
   Op eop[2];
 };
 
@@ -211,18 +209,12 @@ __global__ void __launch_bounds__(kBlock) k_out(DevMesh M, const double* __restr
                                                const double* __restrict__ K,
                                                const double2* __restrict__ FQ, OutArgs a) {
   const int32_t t = blockIdx.x * kBlock + threadIdx.x;
-  if (t < a.nc) {
-    int32_t i;
-    int seg;
-    if (a.clist) {
-      i = a.clist[t];
-      seg = t < a.csplit ? 0 : 1;
-    } else {
-      i = a.cbase + t;
-      const int g = a.ckey ? a.ckey[i] : 0;
-      if (g > 5 || !((a.mask >> g) & 1u)) return;  // 0xFF: not an output of this rank
-      seg = g <= 2 ? 0 : 1;
-    }
+  const int32_t ncs = a.cs.n();
+  if (t < ncs) {
+    const int32_t i = a.cs.at(t);
+    const int g = a.ckey ? a.ckey[i] : 0;
+    if (g > 5 || !((a.mask >> g) & 1u)) return;  // 0xFF: not an output of this rank
+    const int seg = g <= 2 ? 0 : 1;
     const int deg = M.c_deg[i];
     const uint8_t sb = M.c_sbits[i];
     double acc = 0.0;
@@ -236,19 +228,11 @@ __global__ void __launch_bounds__(kBlock) k_out(DevMesh M, const double* __restr
     }
     const double dh = -acc / M.c_area[i];
     apply_op(a.cop[seg], i, dh);
-  } else if (t - a.nc < a.ne) {
-    const int32_t q = t - a.nc;
-    int32_t e;
-    int seg;
-    if (a.elist) {
-      e = a.elist[q];
-      seg = q < a.esplit ? 0 : 1;
-    } else {
-      e = a.ebase + q;
-      const int g = a.ekey ? a.ekey[e] : 0;
-      if (g > 4 || !((a.mask >> (6 + g)) & 1u)) return;
-      seg = g <= 1 ? 0 : 1;
-    }
+  } else if (t - ncs < a.es.n()) {
+    const int32_t e = a.es.at(t - ncs);
+    const int g = a.ekey ? a.ekey[e] : 0;
+    if (g > 4 || !((a.mask >> (6 + g)) & 1u)) return;
+    const int seg = g <= 1 ? 0 : 1;
     const double qt_e = FQ[e].y;
     const double inv_d = M.e_invd[e];
     const int2 cc = M.e_cells[e];

@@ -115,9 +115,16 @@ struct MaskPlan {
   DArr<int32_t> own_cells, own_edges;  // storage when not aliasing the group buffer
   DArr<int32_t> vclos, kclos, eclos, fclos, qclos;
   int32_t nv = 0, nk = 0, nec = 0, nf = 0, nq = 0;
-  // dense launches (thread index = element id) when a set covers most of
-  // the mesh: no index-list traffic, perfectly coalesced own-element access
+  // launch sets: a contiguous range plus a short list (see make_span) or a
+  // dense superset; no index-list traffic for ranges, coalesced access
   bool dense_v = false, dense_k = false, dense_fq = false, dense_out = false;
+  struct HSpan {
+    int32_t base = 0, n_range = 0, n_list = 0;
+    const int32_t* list = nullptr;
+    DArr<int32_t> own;
+    Span dev() const { return Span{base, n_range, list, n_list}; }
+    int64_t n() const { return int64_t(n_range) + n_list; }
+  } sv, sk, se, sc_out, se_out;
   DArr<uint32_t> vmask;  // closure bitmask for the dense dry-vertex check
   DArr<int32_t> tiles;   // fused path: tiles holding outputs of this mask
   int32_t ntiles = 0;
@@ -1053,6 +1060,53 @@ void invalidate(mswm_cuda_ctx* c) {
   c->drop_graphs();
 }
 
+// Launch set for a sorted id list: its longest run of consecutive ids as a
+// range plus the rest as a list when the run holds >= 90 % of the ids (the
+// region-major layout makes every LTS set such a range), else a dense
+// superset [0, universe) when the list covers >= `dense_frac` of it (the
+// kernels filter outputs by group key and dry vertices by bitmask), else the
+// plain list.
+void make_span(mswm_cuda_ctx* c, const int32_t* d_list, int32_t n, int32_t universe,
+               double dense_frac, MaskPlan::HSpan& out) {
+  out = MaskPlan::HSpan();
+  if (n <= 0) return;
+  std::vector<int32_t> h(n);
+  CK(cudaMemcpyAsync(h.data(), d_list, size_t(n) * 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  std::sort(h.begin(), h.end());
+  int32_t best_lo = 0, best_len = 1;
+  for (int32_t k = 0; k < n;) {
+    int32_t j = k + 1;
+    while (j < n && h[j] == h[j - 1] + 1) ++j;
+    if (j - k > best_len) {
+      best_len = j - k;
+      best_lo = k;
+    }
+    k = j;
+  }
+  if (best_len >= int64_t(n) * 9 / 10) {
+    out.base = h[best_lo];
+    out.n_range = best_len;
+    std::vector<int32_t> rest;
+    rest.reserve(size_t(n - best_len));
+    rest.insert(rest.end(), h.begin(), h.begin() + best_lo);
+    rest.insert(rest.end(), h.begin() + best_lo + best_len, h.end());
+    out.n_list = int32_t(rest.size());
+    if (!rest.empty()) {
+      out.own.upload(rest, c->stream);
+      out.list = out.own.p;
+    }
+    return;
+  }
+  if (double(n) >= dense_frac * universe) {
+    out.n_range = universe;
+    return;
+  }
+  out.own.upload(h, c->stream);
+  out.list = out.own.p;
+  out.n_list = n;
+}
+
 MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
   auto it = c->plans.find(mask);
   if (it != c->plans.end()) return *it->second;
@@ -1134,6 +1188,13 @@ MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
   p->dense_k = p->nk >= int64_t(c->nC) * 85 / 100;
   p->dense_fq = p->nec >= int64_t(c->nE) * 85 / 100;
   p->dense_out = int64_t(p->nc) + p->ne >= (int64_t(c->nC) + c->nE) / 2;
+  make_span(c, p->vclos.p, p->nv, c->nV, 0.85, p->sv);
+  make_span(c, p->kclos.p, p->nk, c->nC, 0.85, p->sk);
+  make_span(c, p->eclos.p, p->nec, c->nE, 0.85, p->se);
+  make_span(c, p->cells, p->nc, c->nC, 0.5, p->sc_out);
+  make_span(c, p->edges, p->ne, c->nE, 0.5, p->se_out);
+  // supersets need the closure bitmask for the dry check
+  if (p->sv.n() > p->nv) p->dense_v = true;
   if (c->tile_path) {
     // tiles with outputs; the tiles compute closure supersets, so the dry
     // check always consults the closure bitmask
@@ -1244,10 +1305,8 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
       a.mask = p.mask;
       a.ckey = c->have_regions ? c->ckey.p : nullptr;
       a.ekey = c->have_regions ? c->ekey.p : nullptr;
-      a.cbase = sl.c0;
-      a.nc = sl.nc;
-      a.ebase = sl.e0;
-      a.ne = sl.ne;
+      a.cs = Span{sl.c0, sl.nc, nullptr, 0};
+      a.es = Span{sl.e0, sl.ne, nullptr, 0};
       a.cop[0] = cop[0];
       a.cop[1] = cop[1];
       a.eop[0] = eop[0];
@@ -1273,45 +1332,28 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
     if (rec) CK(cudaEventRecordWithFlags(rec->stop, s, cudaEventRecordExternal));
     return;
   }
-  const int32_t nv = p.dense_v ? c->nV : p.nv, nk = p.dense_k ? c->nC : p.nk;
-  const int64_t na = int64_t(nv) + nk;
-  if (p.nv + p.nk > 0) {
-    const Span vs = p.dense_v ? Span{0, nv, nullptr, 0} : Span{0, 0, p.vclos.p, nv};
-    const Span ks = p.dense_k ? Span{0, nk, nullptr, 0} : Span{0, 0, p.kclos.p, nk};
+  const Span vs = p.sv.dev(), ks = p.sk.dev(), es = p.se.dev();
+  const int64_t na = p.sv.n() + p.sk.n();
+  if (na > 0) {
     k_vertex_cell<<<nblk(na), kBlock, 0, s>>>(M, h, u, vs, ks, c->pv.p, c->K.p, c->dry_vertex.p,
                                              p.vmask.p);
     CK(cudaGetLastError());
     ++c->launches;
   }
-  if (p.nec > 0) {
-    const int32_t nfq = p.dense_fq ? c->nE : p.nec;
-    const Span es = p.dense_fq ? Span{0, nfq, nullptr, 0} : Span{0, 0, p.eclos.p, nfq};
-    k_edge_fq<<<nblk(nfq), kBlock, 0, s>>>(M, h, u, c->pv.p, es, c->FQ.p);
+  if (p.se.n() > 0) {
+    k_edge_fq<<<nblk(p.se.n()), kBlock, 0, s>>>(M, h, u, c->pv.p, es, c->FQ.p);
     CK(cudaGetLastError());
     ++c->launches;
   }
-  if (int64_t(p.nc) + p.ne > 0) {
+  const int64_t nout = p.sc_out.n() + p.se_out.n();
+  if (nout > 0) {
     OutArgs a;
     std::memset(&a, 0, sizeof(a));
+    a.cs = p.sc_out.dev();
+    a.es = p.se_out.dev();
     a.mask = p.mask;
     a.ckey = c->have_regions ? c->ckey.p : nullptr;
     a.ekey = c->have_regions ? c->ekey.p : nullptr;
-    if (p.dense_out) {
-      a.clist = nullptr;
-      a.nc = c->nC;
-      a.csplit = 0;
-      a.elist = nullptr;
-      a.ne = c->nE;
-      a.esplit = 0;
-    } else {
-      a.clist = p.cells;
-      a.nc = p.nc;
-      a.csplit = p.csplit;
-      a.elist = p.edges;
-      a.ne = p.ne;
-      a.esplit = p.esplit;
-    }
-    const int64_t nout = int64_t(a.nc) + a.ne;
     a.cop[0] = cop[0];
     a.cop[1] = cop[1];
     a.eop[0] = eop[0];

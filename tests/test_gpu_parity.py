@@ -259,8 +259,9 @@ def test_layouts_are_bitwise_equivalent(path, monkeypatch):
     o = _oracle_for(wl)
     h_ref, u_ref, _ = o.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, wl.M, 4)
     rng = np.random.default_rng(0)
-    for order in ["input", "hilbert", rng.permutation(wl.mesh.n_cells).astype(np.int32)]:
-        ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order)
+    for order in ["input", "hilbert", "regions",
+                  rng.permutation(wl.mesh.n_cells).astype(np.int32)]:
+        ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order, fine_mask=wl.fine_mask)
         info = ctx.layout_info()
         # a random numbering has no locality: the tile path declines it
         assert info["kernel_path"] == path or (path == "tile" and not isinstance(order, str)
