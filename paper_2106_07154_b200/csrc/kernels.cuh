@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kBlock) k_out(DevMesh M, const double* __restr
     const double inv_d = M.e_invd[e];
     const int2 cc = M.e_cells[e];
     double pvflux = 0.0;
-    if (M.e_slots) {
+    if (!M.e_sten) {  // no explicit tables: ring walk
       // Ring-derived stencil (mesh_build.cpp:133-154 walk, weights
       // :343-362): for each side, walk the cell's ring counterclockwise
       // from just after e; w = (cell_sign * anchor) * (frac - 0.5) with

@@ -128,6 +128,7 @@ struct MaskPlan {
   DArr<uint32_t> vmask;  // closure bitmask for the dense dry-vertex check
   DArr<int32_t> tiles;   // fused path: tiles holding outputs of this mask
   int32_t ntiles = 0;
+  bool use_tiles = false;
   std::vector<int32_t> host_cells, host_edges;  // original ids, same order as device lists
 };
 
@@ -217,6 +218,7 @@ struct mswm_cuda_ctx {
   DArr<double> c_area, c_ratio, v_kite, v_area, e_len, e_ld, e_dual, e_invd, e_coef, b, f;
   bool ring_derived = false;
   bool tile_path = false;
+  bool hybrid = false;
   bool l2_discard = true;
   // fused tile kernel structures (k_tile)
   DArr<TileMeta> t_meta;
@@ -310,8 +312,7 @@ struct mswm_cuda_ctx {
     M.c_deg = c_deg.p;
     M.c_sbits = c_sbits.p;
     M.c_area = c_area.p;
-    M.c_ratio = c_ratio.p;
-    if (!ring_derived) M.c_ratio = tile_path ? c_ratio.p : nullptr;
+    M.c_ratio = (ring_derived || tile_path || hybrid) ? c_ratio.p : nullptr;
     M.v_cell = v_cell.p;
     M.v_edge = v_edge.p;
     M.v_kite = v_kite.p;
@@ -325,7 +326,7 @@ struct mswm_cuda_ctx {
     M.e_dual = e_dual.p;
     M.e_invd = e_invd.p;
     M.e_nst = e_nst.p;
-    M.e_slots = (ring_derived || tile_path) ? e_slots.p : nullptr;
+    M.e_slots = (ring_derived || tile_path || hybrid) ? e_slots.p : nullptr;
     M.e_sten = e_sten.p;
     M.e_coef = e_coef.p;
     M.b = b.p;
@@ -860,7 +861,8 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
 
   std::vector<double> kite_of_slot;
   std::vector<uint8_t> slots;
-  // Evaluation path (MSWM_KERNELS): "explicit" (default) = three kernels
+  // Evaluation path (MSWM_KERNELS): "explicit" (default); "auto" = "explicit" for
+  // near-full masks and "tile" for small ones; "explicit" = three kernels
   // streaming the stencil tables (DRAM-roofline-bound, profiles/); "tile" = the fused tile
   // kernel, needs the ring-derived stencil; "explicit" = three kernels with
   // the stencil tables streamed; "ringwalk" = three kernels walking the
@@ -871,8 +873,11 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   const std::string kind = kv ? kv : "explicit";
   c->tile_path = eligible && kind == "tile";
   c->ring_derived = eligible && kind == "ringwalk";
-  const bool need_ratio = c->tile_path || c->ring_derived;
-  bool need_explicit = !need_ratio;
+  // "auto": three streamed kernels for near-full masks, the one-launch tile
+  // kernel for small masks (the LTS substeps), where launches dominate
+  c->hybrid = eligible && kind == "auto";
+  const bool need_ratio = c->tile_path || c->ring_derived || c->hybrid;
+  bool need_explicit = !(c->tile_path || c->ring_derived);
 
   // cells
   std::vector<int32_t> c_edge(size_t(deg_max) * nC, 0), c_vert(size_t(deg_max) * nC, 0),
@@ -927,8 +932,9 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
     e_cells[ne] = make_int2(co[d->edge_cells[2 * e]], co[d->edge_cells[2 * e + 1]]);
     e_verts[ne] = make_int2(vo[d->edge_vertices[2 * e]], vo[d->edge_vertices[2 * e + 1]]);
   }
-  if (c->tile_path && !build_tiles(c, c_edge, c_vert, c_nbr, c_deg, e_cells, e_verts)) {
+  if ((c->tile_path || c->hybrid) && !build_tiles(c, c_edge, c_vert, c_nbr, c_deg, e_cells, e_verts)) {
     c->tile_path = false;  // closures too large for shared memory (poor cell order)
+    c->hybrid = false;
     need_explicit = true;
   }
   if (!c->tile_path) build_slabs(c, c_edge, c_vert, c_nbr, c_deg, e_cells);
@@ -1195,7 +1201,9 @@ MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
   make_span(c, p->edges, p->ne, c->nE, 0.5, p->se_out);
   // supersets need the closure bitmask for the dry check
   if (p->sv.n() > p->nv) p->dense_v = true;
-  if (c->tile_path) {
+  p->use_tiles = c->tile_path ||
+                 (c->hybrid && int64_t(p->nc) + p->ne < (int64_t(c->nC) + c->nE) / 5);
+  if (p->use_tiles) {
     // tiles with outputs; the tiles compute closure supersets, so the dry
     // check always consults the closure bitmask
     p->dense_v = true;
@@ -1258,7 +1266,7 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
     rec->ne = p.ne;
     CK(cudaEventRecordWithFlags(rec->start, s, cudaEventRecordExternal));
   }
-  if (c->tile_path) {
+  if (p.use_tiles) {
     if (p.ntiles > 0) {
       TileArgs T;
       T.meta = c->t_meta.p;
@@ -2177,7 +2185,7 @@ int mswm_cuda_eval_profile(mswm_cuda_ctx* c, float* eval_ms, int64_t* out_cells,
 
 int mswm_cuda_layout_info(const mswm_cuda_ctx* c, int* kernel_path, int* identity_order) {
   if (!c) return MSWM_E_USAGE;
-  if (kernel_path) *kernel_path = c->tile_path ? 2 : (c->ring_derived ? 1 : 0);
+  if (kernel_path) *kernel_path = c->tile_path ? 2 : (c->ring_derived ? 1 : (c->hybrid ? 3 : 0));
   if (identity_order) *identity_order = c->identity ? 1 : 0;
   return MSWM_OK;
 }

@@ -249,7 +249,7 @@ def test_stepper_drop_in_interface():
     assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
 
 
-@pytest.mark.parametrize("path", ["tile", "explicit", "ringwalk"])
+@pytest.mark.parametrize("path", ["auto", "tile", "explicit", "ringwalk"])
 def test_layouts_are_bitwise_equivalent(path, monkeypatch):
     """Results are independent of the device numbering (input, Hilbert,
     random) and of the evaluation path (fused tile kernel, explicit stencil
@@ -264,7 +264,8 @@ def test_layouts_are_bitwise_equivalent(path, monkeypatch):
         ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order, fine_mask=wl.fine_mask)
         info = ctx.layout_info()
         # a random numbering has no locality: the tile path declines it
-        assert info["kernel_path"] == path or (path == "tile" and not isinstance(order, str)
+        assert info["kernel_path"] == path or (path in ("tile", "auto")
+                                               and not isinstance(order, str)
                                                and info["kernel_path"] == "explicit")
         ctx.make_regions(wl.fine_mask, wl.width)
         for a, b in zip(ctx.regions.groups, o.groups()):
