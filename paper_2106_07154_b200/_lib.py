@@ -14,7 +14,8 @@ import numpy as np
 
 LIB_DIR = Path(__file__).resolve().parent / "_lib"
 HOST_LIB = LIB_DIR / "libmswm_host.so"
-CUDA_LIB = LIB_DIR / "libmswm_cuda.so"
+CUDA_LIB = Path(os.environ["MSWM_CUDA_LIB"]) if os.environ.get("MSWM_CUDA_LIB") else \
+    LIB_DIR / "libmswm_cuda.so"
 
 i32p = C.POINTER(C.c_int32)
 i8p = C.POINTER(C.c_int8)
