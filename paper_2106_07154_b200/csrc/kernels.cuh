@@ -16,6 +16,24 @@ namespace mswm_dev {
 constexpr int kMaxDeg = 8;               // ring size bound (hexagons 6, pentagons 5)
 constexpr int kMaxSten = 2 * kMaxDeg - 2;
 constexpr int kBlock = 256;
+// minimum resident CTAs per SM requested from ptxas (register budget) for
+// the streamed kernels; tuned on B200 (profiles/r1_*)
+#ifndef MSWM_KA_MINB
+#define MSWM_KA_MINB 8
+#endif
+#ifndef MSWM_KOUT_MINB
+#define MSWM_KOUT_MINB 8
+#endif
+#if MSWM_KA_MINB > 0
+#define MSWM_KA_BOUNDS __launch_bounds__(kBlock, MSWM_KA_MINB)
+#else
+#define MSWM_KA_BOUNDS __launch_bounds__(kBlock)
+#endif
+#if MSWM_KOUT_MINB > 0
+#define MSWM_KOUT_BOUNDS __launch_bounds__(kBlock, MSWM_KOUT_MINB)
+#else
+#define MSWM_KOUT_BOUNDS __launch_bounds__(kBlock)
+#endif
 
 // Device mesh tables in internal numbering.  Slot-major SoA ([slot][elem])
 // so consecutive threads of a warp read consecutive addresses.
@@ -132,7 +150,7 @@ __device__ __forceinline__ void apply_op(const Op& op, int32_t i, double d) {
 // ---------------------------------------------------------------------------
 // Phase A: potential vorticity on the closure vertices (operators.cpp:74-86)
 // and kinetic energy on the closure cells (:64-72), one launch.
-__global__ void __launch_bounds__(kBlock) k_vertex_cell(DevMesh M, const double* __restrict__ h,
+__global__ void MSWM_KA_BOUNDS k_vertex_cell(DevMesh M, const double* __restrict__ h,
                                                        const double* __restrict__ u, Span vs,
                                                        Span ks, double* __restrict__ pv,
                                                        double* __restrict__ K,
@@ -205,7 +223,7 @@ struct OutArgs {
   Op eop[2];
 };
 
-__global__ void __launch_bounds__(kBlock) k_out(DevMesh M, const double* __restrict__ h,
+__global__ void MSWM_KOUT_BOUNDS k_out(DevMesh M, const double* __restrict__ h,
                                                const double* __restrict__ K,
                                                const double2* __restrict__ FQ, OutArgs a) {
   const int32_t t = blockIdx.x * kBlock + threadIdx.x;
