@@ -9,9 +9,12 @@
 #pragma once
 
 #include <cstdint>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 namespace mswm_dev {
+
+namespace cg = cooperative_groups;
 
 constexpr int kMaxDeg = 8;               // ring size bound (hexagons 6, pentagons 5)
 constexpr int kMaxSten = 2 * kMaxDeg - 2;
@@ -150,16 +153,15 @@ __device__ __forceinline__ void apply_op(const Op& op, int32_t i, double d) {
 // ---------------------------------------------------------------------------
 // Phase A: potential vorticity on the closure vertices (operators.cpp:74-86)
 // and kinetic energy on the closure cells (:64-72), one launch.
-__global__ void MSWM_KA_BOUNDS k_vertex_cell(DevMesh M, const double* __restrict__ h,
-                                                       const double* __restrict__ u, Span vs,
-                                                       Span ks, double* __restrict__ pv,
-                                                       double* __restrict__ K,
-                                                       int32_t* __restrict__ dry,
-                                                       const uint32_t* __restrict__ vmask) {
+// one element of phase A (t indexes vs then ks)
+__device__ __forceinline__ void item_vertex_cell(const DevMesh& M, const double* __restrict__ h,
+                                                 const double* __restrict__ u, const Span& vs,
+                                                 const Span& ks, double* __restrict__ pv,
+                                                 double* __restrict__ K, int32_t* __restrict__ dry,
+                                                 const uint32_t* __restrict__ vmask, int32_t t) {
   // Spans may be supersets of the closure (dense ranges, slabs); the dry
   // check then consults the closure bitmask vmask so only closure vertices
   // raise, as in operators.cpp:74-84.
-  const int32_t t = blockIdx.x * kBlock + threadIdx.x;
   const int32_t nv = vs.n();
   if (t < nv) {
     const int32_t v = vs.at(t);
@@ -192,14 +194,21 @@ __global__ void MSWM_KA_BOUNDS k_vertex_cell(DevMesh M, const double* __restrict
   }
 }
 
+__global__ void MSWM_KA_BOUNDS k_vertex_cell(DevMesh M, const double* __restrict__ h,
+                                             const double* __restrict__ u, Span vs, Span ks,
+                                             double* __restrict__ pv, double* __restrict__ K,
+                                             int32_t* __restrict__ dry,
+                                             const uint32_t* __restrict__ vmask) {
+  item_vertex_cell(M, h, u, vs, ks, pv, K, dry, vmask, blockIdx.x * kBlock + threadIdx.x);
+}
+
 // Phase B: thickness flux F_e (operators.cpp:61-62) and q~_e (:88-89) on the
 // union of the flux and q~ closures, packed as (F, q~) so the stencil loop
 // of phase C reads both with one 16-byte gather.
-__global__ void __launch_bounds__(kBlock) k_edge_fq(DevMesh M, const double* __restrict__ h,
-                                                   const double* __restrict__ u,
-                                                   const double* __restrict__ pv, Span es,
-                                                   double2* __restrict__ FQ) {
-  const int32_t t = blockIdx.x * kBlock + threadIdx.x;
+__device__ __forceinline__ void item_edge_fq(const DevMesh& M, const double* __restrict__ h,
+                                             const double* __restrict__ u,
+                                             const double* __restrict__ pv, const Span& es,
+                                             double2* __restrict__ FQ, int32_t t) {
   if (t >= es.n()) return;
   const int32_t e = es.at(t);
   const int2 c = M.e_cells[e];
@@ -207,6 +216,13 @@ __global__ void __launch_bounds__(kBlock) k_edge_fq(DevMesh M, const double* __r
   const double F = 0.5 * (h[c.x] + h[c.y]) * u[e];
   const double q = 0.5 * (pv[v.x] + pv[v.y]);
   FQ[e] = make_double2(F, q);
+}
+
+__global__ void __launch_bounds__(kBlock) k_edge_fq(DevMesh M, const double* __restrict__ h,
+                                                   const double* __restrict__ u,
+                                                   const double* __restrict__ pv, Span es,
+                                                   double2* __restrict__ FQ) {
+  item_edge_fq(M, h, u, pv, es, FQ, blockIdx.x * kBlock + threadIdx.x);
 }
 
 // Phase C: the output tendencies -- dh on out cells (operators.cpp:91-99),
@@ -223,10 +239,10 @@ struct OutArgs {
   Op eop[2];
 };
 
-__global__ void MSWM_KOUT_BOUNDS k_out(DevMesh M, const double* __restrict__ h,
-                                               const double* __restrict__ K,
-                                               const double2* __restrict__ FQ, OutArgs a) {
-  const int32_t t = blockIdx.x * kBlock + threadIdx.x;
+__device__ __forceinline__ void item_out(const DevMesh& M, const double* __restrict__ h,
+                                         const double* __restrict__ K,
+                                         const double2* __restrict__ FQ, const OutArgs& a,
+                                         int32_t t) {
   const int32_t ncs = a.cs.n();
   if (t < ncs) {
     const int32_t i = a.cs.at(t);
@@ -306,6 +322,12 @@ __global__ void MSWM_KOUT_BOUNDS k_out(DevMesh M, const double* __restrict__ h,
   }
 }
 
+__global__ void MSWM_KOUT_BOUNDS k_out(DevMesh M, const double* __restrict__ h,
+                                     const double* __restrict__ K,
+                                     const double2* __restrict__ FQ, OutArgs a) {
+  item_out(M, h, K, FQ, a, blockIdx.x * kBlock + threadIdx.x);
+}
+
 // ---------------------------------------------------------------------------
 // Interface-1 prediction (integrators.cpp:217-227, order 3):
 // dst = ((c0*s0) + (c1*s1)) + (c2*s2) on the I1 lists.
@@ -359,6 +381,69 @@ __global__ void k_save_predict(const int32_t* __restrict__ clist, int32_t nc, in
       US2[e] = y2;
       U[e] = c0 * y0 + c1 * y1 + c2 * y2;
     }
+  }
+}
+
+// Interface-1 prediction as a data structure (for the fused kernel).
+struct PredArgs {
+  const int32_t *clist, *elist;
+  int32_t nc, ne;
+  double c0, c1, c2;
+  const double *hs0, *hs1, *hs2, *us0, *us1, *us2;
+  double *hdst, *udst;
+};
+
+__device__ __forceinline__ void item_predict(const PredArgs& p, int32_t t) {
+  if (t < p.nc) {
+    const int32_t i = p.clist[t];
+    p.hdst[i] = p.c0 * p.hs0[i] + p.c1 * p.hs1[i] + p.c2 * p.hs2[i];
+  } else if (t - p.nc < p.ne) {
+    const int32_t e = p.elist[t - p.nc];
+    p.udst[e] = p.c0 * p.us0[e] + p.c1 * p.us1[e] + p.c2 * p.us2[e];
+  }
+}
+
+// A whole small evaluation in one cooperative launch: [prediction] | PV, K |
+// F, q~ | dh, du + epilogue, phases separated by grid-wide barriers (all
+// CTAs are co-resident by construction of the cooperative launch).  Used
+// for the LTS substeps, whose three-launch cost is mostly launch latency.
+struct FusedArgs {
+  DevMesh M;
+  const double* h;
+  const double* u;
+  Span vs, ks, es;
+  double *pv, *K;
+  double2* FQ;
+  int32_t* dry;
+  const uint32_t* vmask;
+  OutArgs out;
+  PredArgs pred;
+  int has_pred;
+};
+
+__global__ void __launch_bounds__(kBlock) k_fused_eval(FusedArgs f) {
+  cg::grid_group grid = cg::this_grid();
+  const int32_t stride = gridDim.x * kBlock;
+  const int32_t t0 = blockIdx.x * kBlock + threadIdx.x;
+  if (f.has_pred) {
+    const int32_t n = f.pred.nc + f.pred.ne;
+    for (int32_t t = t0; t < n; t += stride) item_predict(f.pred, t);
+    grid.sync();
+  }
+  {
+    const int32_t n = f.vs.n() + f.ks.n();
+    for (int32_t t = t0; t < n; t += stride)
+      item_vertex_cell(f.M, f.h, f.u, f.vs, f.ks, f.pv, f.K, f.dry, f.vmask, t);
+  }
+  grid.sync();
+  {
+    const int32_t n = f.es.n();
+    for (int32_t t = t0; t < n; t += stride) item_edge_fq(f.M, f.h, f.u, f.pv, f.es, f.FQ, t);
+  }
+  grid.sync();
+  {
+    const int32_t n = f.out.cs.n() + f.out.es.n();
+    for (int32_t t = t0; t < n; t += stride) item_out(f.M, f.h, f.K, f.FQ, f.out, t);
   }
 }
 

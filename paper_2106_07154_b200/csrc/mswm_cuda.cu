@@ -129,6 +129,7 @@ struct MaskPlan {
   DArr<int32_t> tiles;   // fused path: tiles holding outputs of this mask
   int32_t ntiles = 0;
   bool use_tiles = false;
+  bool use_coop = false;  // small mask: one cooperative launch (k_fused_eval)
   std::vector<int32_t> host_cells, host_edges;  // original ids, same order as device lists
 };
 
@@ -219,6 +220,7 @@ struct mswm_cuda_ctx {
   bool ring_derived = false;
   bool tile_path = false;
   bool hybrid = false;
+  int32_t coop_blocks = 0;  // co-resident CTAs of k_fused_eval (0 = disabled)
   bool l2_discard = true;
   // fused tile kernel structures (k_tile)
   DArr<TileMeta> t_meta;
@@ -1201,6 +1203,8 @@ MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
   make_span(c, p->edges, p->ne, c->nE, 0.5, p->se_out);
   // supersets need the closure bitmask for the dry check
   if (p->sv.n() > p->nv) p->dense_v = true;
+  p->use_coop = c->coop_blocks > 0 && !c->tile_path &&
+                int64_t(p->nc) + p->ne < (int64_t(c->nC) + c->nE) / 5;
   p->use_tiles = c->tile_path ||
                  (c->hybrid && int64_t(p->nc) + p->ne < (int64_t(c->nC) + c->nE) / 5);
   if (p->use_tiles) {
@@ -1252,8 +1256,15 @@ Op op_none() {
 }
 
 void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const double* u,
-                 const Op cop[2], const Op eop[2]) {
+                 const Op cop[2], const Op eop[2], const PredArgs* pred = nullptr) {
   cudaStream_t s = c->ls;
+  if (pred && !(p.use_coop && !p.use_tiles) && int64_t(pred->nc) + pred->ne > 0) {
+    k_predict<<<nblk(int64_t(pred->nc) + pred->ne), kBlock, 0, s>>>(
+        pred->clist, pred->nc, pred->elist, pred->ne, pred->c0, pred->c1, pred->c2, pred->hs0,
+        pred->hs1, pred->hs2, pred->hdst, pred->us0, pred->us1, pred->us2, pred->udst);
+    CK(cudaGetLastError());
+    ++c->launches;
+  }
   const DevMesh M = c->dev();
   EvalRecord* rec = nullptr;
   if (c->capture_records) {
@@ -1342,6 +1353,43 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
   }
   const Span vs = p.sv.dev(), ks = p.sk.dev(), es = p.se.dev();
   const int64_t na = p.sv.n() + p.sk.n();
+  if (p.use_coop) {
+    FusedArgs f;
+    std::memset(&f, 0, sizeof(f));
+    f.M = M;
+    f.h = h;
+    f.u = u;
+    f.vs = vs;
+    f.ks = ks;
+    f.es = es;
+    f.pv = c->pv.p;
+    f.K = c->K.p;
+    f.FQ = c->FQ.p;
+    f.dry = c->dry_vertex.p;
+    f.vmask = p.vmask.p;
+    f.out.cs = p.sc_out.dev();
+    f.out.es = p.se_out.dev();
+    f.out.mask = p.mask;
+    f.out.ckey = c->have_regions ? c->ckey.p : nullptr;
+    f.out.ekey = c->have_regions ? c->ekey.p : nullptr;
+    f.out.cop[0] = cop[0];
+    f.out.cop[1] = cop[1];
+    f.out.eop[0] = eop[0];
+    f.out.eop[1] = eop[1];
+    int64_t work = std::max<int64_t>(std::max<int64_t>(na, p.se.n()), p.sc_out.n() + p.se_out.n());
+    if (pred) {
+      f.pred = *pred;
+      f.has_pred = 1;
+      work = std::max<int64_t>(work, int64_t(pred->nc) + pred->ne);
+    }
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(c->coop_blocks, nblk(work))));
+    void* args[] = {&f};
+    CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_fused_eval), dim3(grid), dim3(kBlock),
+                                   args, 0, s));
+    ++c->launches;
+    if (rec) CK(cudaEventRecordWithFlags(rec->stop, s, cudaEventRecordExternal));
+    return;
+  }
   if (na > 0) {
     k_vertex_cell<<<nblk(na), kBlock, 0, s>>>(M, h, u, vs, ks, c->pv.p, c->K.p, c->dry_vertex.p,
                                              p.vmask.p);
@@ -1470,6 +1518,29 @@ void launch_predict(mswm_cuda_ctx* c, int stage, int k, int M, double* hdst, dou
   ++c->launches;
 }
 
+PredArgs make_pred(mswm_cuda_ctx* c, int stage, int k, int M, double* hdst, double* udst) {
+  const IfLists L = if_lists(c);
+  double w[3];
+  lts3_coeffs(stage, k, M, w);
+  PredArgs pa;
+  pa.clist = L.c;
+  pa.nc = L.nc1;
+  pa.elist = L.e;
+  pa.ne = L.ne1;
+  pa.c0 = w[0];
+  pa.c1 = w[1];
+  pa.c2 = w[2];
+  pa.hs0 = c->S0h.p;
+  pa.hs1 = c->S1h.p;
+  pa.hs2 = c->S2h.p;
+  pa.us0 = c->S0u.p;
+  pa.us1 = c->S1u.p;
+  pa.us2 = c->S2u.p;
+  pa.hdst = hdst;
+  pa.udst = udst;
+  return pa;
+}
+
 // ---------------------------------------------------------------------------
 // Halo exchange (multi-rank).  Before every evaluation each rank refreshes
 // the halo copies of the (h, u) stage arrays the evaluation reads -- the
@@ -1538,6 +1609,8 @@ void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us) {
 // every rank context of the executor.
 void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
   const double delta = dt / M;
+  bool fuse_pred = true;
+  for (auto* c : cs) fuse_pred &= !c->halo.active();
   const double third = 1.0 / 3.0, two3 = 2.0 / 3.0;
   using C = mswm_cuda_ctx;
   // Step 1 (:483-487): h1 = h_old + dt*dh on UF1 u UF2 u I1 u I2 u C.
@@ -1575,32 +1648,40 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
   for (int k = 0; k < M; ++k) {
     const int first = k == 0;
     // stage 1: fine hb = ha + delta*d; interfaces acc1 += d   (:521-531)
-    if (k > 0)
+    // predictions ride in the evaluation's launch unless a halo exchange
+    // has to propagate them first (multi-rank)
+    if (k > 0 && !fuse_pred)
       for (auto* c : cs) launch_predict(c, 1, k, M, c->H.p, c->U.p);
     exchange(cs, &C::H, &C::U);
     for (auto* c : cs) {
+      const PredArgs pa = make_pred(c, 1, k, M, c->H.p, c->U.p);
       Op co[2] = {mk_op(OP_EULER, c->H1.p, c->H.p, delta),
                   mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A1h.p, first)};
       Op eo[2] = {mk_op(OP_EULER, c->U1.p, c->U.p, delta),
                   mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A1u.p, first)};
-      launch_eval(c, plan_for(c, kMaskSub), c->H.p, c->U.p, co, eo);
+      launch_eval(c, plan_for(c, kMaskSub), c->H.p, c->U.p, co, eo,
+                  (k > 0 && fuse_pred) ? &pa : nullptr);
     }
     // stage 2: fine hc = 0.75 ha + 0.25 hb + (0.25 delta) d; acc2 += d   (:532-541)
-    for (auto* c : cs) launch_predict(c, 2, k, M, c->H1.p, c->U1.p);
+    if (!fuse_pred)
+      for (auto* c : cs) launch_predict(c, 2, k, M, c->H1.p, c->U1.p);
     exchange(cs, &C::H1, &C::U1);
     for (auto* c : cs) {
+      const PredArgs pa = make_pred(c, 2, k, M, c->H1.p, c->U1.p);
       const double cr = 0.25 * delta;
       Op co[2] = {mk_op(OP_WCOMB, c->H2.p, c->H.p, 0.75, c->H1.p, 0.25, cr),
                   mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A2h.p, first)};
       Op eo[2] = {mk_op(OP_WCOMB, c->U2.p, c->U.p, 0.75, c->U1.p, 0.25, cr),
                   mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A2u.p, first)};
-      launch_eval(c, plan_for(c, kMaskSub), c->H1.p, c->U1.p, co, eo);
+      launch_eval(c, plan_for(c, kMaskSub), c->H1.p, c->U1.p, co, eo, fuse_pred ? &pa : nullptr);
     }
     // stage 3: fine ha = 1/3 ha + 2/3 hc + (2/3 delta) d; acc3 += d, and on
     // the last substep the interface correction (:542-553, :231-274).
-    for (auto* c : cs) launch_predict(c, 3, k, M, c->H2.p, c->U2.p);
+    if (!fuse_pred)
+      for (auto* c : cs) launch_predict(c, 3, k, M, c->H2.p, c->U2.p);
     exchange(cs, &C::H2, &C::U2);
     for (auto* c : cs) {
+      const PredArgs pa = make_pred(c, 3, k, M, c->H2.p, c->U2.p);
       const double cr = two3 * delta;
       Op co[2], eo[2];
       co[0] = mk_op(OP_WCOMB, c->H.p, c->H.p, third, c->H2.p, two3, cr);
@@ -1614,7 +1695,7 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
         eo[1] = mk_op(OP_ACC_CORR, c->U.p, c->S0u.p, delta, nullptr, 1.0 / 6.0, two3, c->A3u.p,
                       first, c->A1u.p, c->A2u.p);
       }
-      launch_eval(c, plan_for(c, kMaskSub), c->H2.p, c->U2.p, co, eo);
+      launch_eval(c, plan_for(c, kMaskSub), c->H2.p, c->U2.p, co, eo, fuse_pred ? &pa : nullptr);
     }
   }
   // Step 4 (:557-563): coarse h = 1/3 h_old + 2/3 h2 + (2/3 dt) dh, in place.
@@ -1937,6 +2018,15 @@ int mswm_cuda_create(const mswm_mesh_desc* mesh, int device, const int32_t* cell
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->ls = c->stream;
     build_tables(c.get(), mesh, cell_order);
+    {
+      const char* cv = std::getenv("MSWM_COOP");
+      int nb = 0, nsm = 0, coop = 0;
+      CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+      CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fused_eval, kBlock, 0));
+      // opt-in (MSWM_COOP=1): measured slower than three launches (profiles/)
+      c->coop_blocks = (coop && cv && cv[0] == '1') ? nb * nsm : 0;
+    }
   } catch (const Error& e) {
     g_create_error = e.what();
     return e.status;
