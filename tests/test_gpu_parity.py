@@ -313,3 +313,23 @@ def test_reference_stepper_drives_cuda_evaluator():
     c1, e1, _ = serial.ledger()
     c2, e2, _ = cuda.ledger()
     assert np.array_equal(c1, c2) and np.array_equal(e1, e2)
+
+
+@pytest.mark.parametrize("env", [{"MSWM_COOP": "1"}, {"MSWM_SLAB_CELLS": "2000"},
+                                 {"MSWM_KERNELS": "tile", "MSWM_TILE_CELLS": "64"},
+                                 {"MSWM_KERNELS": "auto"}, {"MSWM_KERNELS": "ringwalk"}])
+def test_optional_evaluation_paths_bitwise(env, monkeypatch):
+    """Every opt-in evaluation strategy (cooperative one-launch small evals,
+    L2-blocked slabs, fused tiles, hybrid, ring walk) stays bitwise equal."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    wl = W.small_sphere(5, seed=29, cap_deg=25.0)
+    o = _oracle_for(wl)
+    ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order="regions", fine_mask=wl.fine_mask)
+    ctx.make_regions(wl.fine_mask, wl.width)
+    for scheme, n, dt in [(Scheme.LTS3, 4, wl.dt), (Scheme.RK4, 2, wl.dt / wl.M)]:
+        h_ref, u_ref, _ = o.step(int(scheme), wl.h, wl.u, 0.0, dt, wl.M, n)
+        ctx.upload(State(wl.h, wl.u, 0.0))
+        ctx.advance(scheme, dt, wl.M, n)
+        st = ctx.download()
+        assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref), (env, scheme)

@@ -1,0 +1,61 @@
+"""CPU tests of the host-side helpers: region-major layout hint (a numpy
+restatement of make_regions) and the bench contract's reference arm."""
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle.oracle import Oracle
+from paper_2106_07154_b200 import workloads as W
+from paper_2106_07154_b200.layout import region_keys, region_major_order
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+@pytest.mark.parametrize("make", [lambda: W.config1(n_steps=1),
+                                  lambda: W.small_sphere(5, cap_deg=25.0)])
+@pytest.mark.parametrize("width", [1, 2])
+def test_region_keys_match_oracle_labels(make, width):
+    wl = make()
+    o = Oracle(wl.mesh, wl.b, wl.f, wl.gravity)
+    o.set_regions(wl.fine_mask, width)
+    cl, cs, el = o.labels()
+    ref = np.where(cl == 0, cs, cl + 2)
+    assert np.array_equal(region_keys(wl.mesh, wl.fine_mask, width), ref)
+
+
+def test_region_major_order_is_grouped_permutation():
+    wl = W.small_sphere(4, cap_deg=30.0)
+    order = region_major_order(wl.mesh, wl.fine_mask)
+    assert np.array_equal(np.sort(order), np.arange(wl.mesh.n_cells))
+    keys = region_keys(wl.mesh, wl.fine_mask)[order]
+    assert np.all(np.diff(keys) >= 0)  # groups are contiguous, in GroupBit order
+
+
+def test_bench_reference_arm_json_line():
+    """`bench.py --impl reference` prints one JSON line with the contract keys."""
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--config",
+                        "c1", "--steps", "2", "--warmup", "3"], capture_output=True, text=True,
+                       timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "dtype", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "reference"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_bench_ours_fails_loudly_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--config", "c1", "--steps", "2"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode != 0 and "CUDA" in (r.stderr + r.stdout)
