@@ -731,6 +731,10 @@ namespace mswm_dev {
 // elements are never outputs, so per-element results equal the reference.
 constexpr int kTileCells = 128;  // default; MSWM_TILE_CELLS overrides at create
 constexpr int kTileThreads = 256;
+// shared-memory row stride of the per-cell kite/A rows: 9 doubles (odd) so
+// lanes reading different cells' rows hit different banks (a stride of 8
+// doubles = 16 banks folded every lane pair onto two bank groups)
+constexpr int kRStride = kMaxDeg + 1;
 
 struct TileMeta {
   // owned ranges first (no index lists), then the halo from the lists:
@@ -767,7 +771,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(DevMesh M, TileArgs T,
   double* sPV = sm;
   double* sK = sPV + tm.nvr;
   double* sR = sK + tm.nc1;
-  double* sF = sR + size_t(tm.nc1) * kMaxDeg;
+  double* sF = sR + size_t(tm.nc1) * kRStride;
   double* sQ = sF + tm.ner;
   double* sL = sQ + tm.ner;
 
@@ -804,7 +808,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(DevMesh M, TileArgs T,
         const int32_t e = M.c_edge[j * M.nC + i];
         const double ue = u[e];
         acc += M.e_ld[e] * ue * ue;
-        sR[k * kMaxDeg + j] = M.c_ratio[j * M.nC + i];
+        sR[k * kRStride + j] = M.c_ratio[j * M.nC + i];
       }
     }
     sK[k] = acc / (4.0 * M.c_area[i]);
@@ -863,7 +867,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(DevMesh M, TileArgs T,
       const int deg = M.c_deg[c];
       const uint8_t sb = M.c_sbits[c];
       const uint4 ring = T.c1_ring[tm.c1r_off + lc];
-      const double* rr = sR + lc * kMaxDeg;
+      const double* rr = sR + lc * kRStride;
       double frac = 0.0;
 #pragma unroll
       for (int kk = 1; kk < kMaxDeg; ++kk) {

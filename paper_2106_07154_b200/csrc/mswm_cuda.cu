@@ -699,7 +699,7 @@ bool build_tiles(mswm_cuda_ctx* c, const std::vector<int32_t>& c_edge,
       if (cmark[cc.x] != t || cmark[cc.y] != t) return false;
       oe_c1[e] = make_ushort2(uint16_t(cloc[cc.x]), uint16_t(cloc[cc.y]));
     }
-    const size_t smem = 8 * (size_t(m.nvr) + m.nc1 + size_t(m.nc1) * kMaxDeg + 3 * size_t(m.ner));
+    const size_t smem = 8 * (size_t(m.nvr) + m.nc1 + size_t(m.nc1) * kRStride + 3 * size_t(m.ner));
     smem_max = std::max(smem_max, smem);
   }
   if (smem_max > 200 * 1024) return false;  // poor locality: use the three-kernel path
