@@ -734,7 +734,10 @@ constexpr int kTileThreads = 256;
 // shared-memory row stride of the per-cell kite/A rows: 9 doubles (odd) so
 // lanes reading different cells' rows hit different banks (a stride of 8
 // doubles = 16 banks folded every lane pair onto two bank groups)
-constexpr int kRStride = kMaxDeg + 1;
+#ifndef MSWM_RSTRIDE
+#define MSWM_RSTRIDE (kMaxDeg + 1)
+#endif
+constexpr int kRStride = MSWM_RSTRIDE;
 
 struct TileMeta {
   // owned ranges first (no index lists), then the halo from the lists:
