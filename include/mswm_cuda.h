@@ -205,6 +205,12 @@ int mswm_cuda_eval_profile(mswm_cuda_ctx* ctx, float* eval_ms,
 int mswm_cuda_layout_info(const mswm_cuda_ctx* ctx, int* kernel_path,
                           int* identity_order);
 
+/* Dataflow evaluation (k_flow, opt-in with MSWM_FLOW=1 at create): large
+ * masks run as one persistent launch over cell slabs of slab_cells cells;
+ * all zero when disabled (the default, small meshes). */
+int mswm_cuda_flow_info(const mswm_cuda_ctx* ctx, int* slab_cells, int* n_slabs,
+                        int* lag, int* grid);
+
 /* Number of this library's kernels one replay of the most recently used
  * step graph launches (the bench's gpu_launches evidence). */
 int mswm_cuda_kernels_per_step(mswm_cuda_ctx* ctx, int64_t* n);

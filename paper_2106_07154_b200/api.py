@@ -353,6 +353,12 @@ class CudaContext:
         return {"kernel_path": {0: "explicit", 1: "ringwalk", 2: "tile", 3: "auto"}[kp.value],
                 "input_order": bool(ident.value)}
 
+    def flow_info(self) -> dict:
+        """Dataflow evaluation (k_flow) parameters; slab_cells 0 = disabled."""
+        v = [C.c_int(0) for _ in range(4)]
+        self._check(self.lib.mswm_cuda_flow_info(self.handle, *[C.byref(x) for x in v]))
+        return dict(zip(["slab_cells", "n_slabs", "lag", "grid"], [x.value for x in v]))
+
     def kernels_per_step(self) -> int:
         n = C.c_int64(0)
         self._check(self.lib.mswm_cuda_kernels_per_step(self.handle, C.byref(n)))

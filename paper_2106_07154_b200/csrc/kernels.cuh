@@ -205,6 +205,17 @@ __global__ void MSWM_KA_BOUNDS k_vertex_cell(DevMesh M, const double* __restrict
 // Phase B: thickness flux F_e (operators.cpp:61-62) and q~_e (:88-89) on the
 // union of the flux and q~ closures, packed as (F, q~) so the stencil loop
 // of phase C reads both with one 16-byte gather.
+// Loads of intermediates written earlier in the same launch (k_flow) bypass
+// L1, which is not coherent with other SMs' writes.
+template <bool CG, class T>
+__device__ __forceinline__ T ldx(const T* p) {
+  if constexpr (CG)
+    return __ldcg(p);
+  else
+    return *p;
+}
+
+template <bool CG = false>
 __device__ __forceinline__ void item_edge_fq(const DevMesh& M, const double* __restrict__ h,
                                              const double* __restrict__ u,
                                              const double* __restrict__ pv, const Span& es,
@@ -214,7 +225,7 @@ __device__ __forceinline__ void item_edge_fq(const DevMesh& M, const double* __r
   const int2 c = M.e_cells[e];
   const int2 v = M.e_verts[e];
   const double F = 0.5 * (h[c.x] + h[c.y]) * u[e];
-  const double q = 0.5 * (pv[v.x] + pv[v.y]);
+  const double q = 0.5 * (ldx<CG>(pv + v.x) + ldx<CG>(pv + v.y));
   FQ[e] = make_double2(F, q);
 }
 
@@ -239,13 +250,14 @@ struct OutArgs {
   Op eop[2];
 };
 
-__device__ __forceinline__ void item_out(const DevMesh& M, const double* __restrict__ h,
-                                         const double* __restrict__ K,
-                                         const double2* __restrict__ FQ, const OutArgs& a,
-                                         int32_t t) {
-  const int32_t ncs = a.cs.n();
+template <bool CG = false>
+__device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __restrict__ h,
+                                            const double* __restrict__ K,
+                                            const double2* __restrict__ FQ, const Span& cs,
+                                            const Span& es, const OutArgs& a, int32_t t) {
+  const int32_t ncs = cs.n();
   if (t < ncs) {
-    const int32_t i = a.cs.at(t);
+    const int32_t i = cs.at(t);
     const int g = a.ckey ? a.ckey[i] : 0;
     if (g > 5 || !((a.mask >> g) & 1u)) return;  // 0xFF: not an output of this rank
     const int seg = g <= 2 ? 0 : 1;
@@ -257,17 +269,17 @@ __device__ __forceinline__ void item_out(const DevMesh& M, const double* __restr
       if (j < deg) {
         const int32_t e = M.c_edge[j * M.nC + i];
         const double l = M.e_len[e];
-        acc += ((sb >> j) & 1 ? -l : l) * FQ[e].x;
+        acc += ((sb >> j) & 1 ? -l : l) * ldx<CG>(FQ + e).x;
       }
     }
     const double dh = -acc / M.c_area[i];
     apply_op(a.cop[seg], i, dh);
-  } else if (t - ncs < a.es.n()) {
-    const int32_t e = a.es.at(t - ncs);
+  } else if (t - ncs < es.n()) {
+    const int32_t e = es.at(t - ncs);
     const int g = a.ekey ? a.ekey[e] : 0;
     if (g > 4 || !((a.mask >> (6 + g)) & 1u)) return;
     const int seg = g <= 1 ? 0 : 1;
-    const double qt_e = FQ[e].y;
+    const double qt_e = ldx<CG>(FQ + e).y;
     const double inv_d = M.e_invd[e];
     const int2 cc = M.e_cells[e];
     double pvflux = 0.0;
@@ -298,7 +310,7 @@ __device__ __forceinline__ void item_out(const DevMesh& M, const double* __restr
             const double x = frac - 0.5;
             const double w = (((sb >> s) & 1u) ^ aneg) ? -x : x;
             const double coef = w * (M.e_len[e2] * inv_d);
-            const double2 fq = FQ[e2];
+            const double2 fq = ldx<CG>(FQ + e2);
             pvflux += coef * fq.x * (0.5 * (qt_e + fq.y));
           }
         }
@@ -310,16 +322,23 @@ __device__ __forceinline__ void item_out(const DevMesh& M, const double* __restr
         if (j < nst) {
           const int32_t e2 = M.e_sten[j * M.nE + e];
           const double c = M.e_coef[j * M.nE + e];
-          const double2 fq = FQ[e2];
+          const double2 fq = ldx<CG>(FQ + e2);
           pvflux += c * fq.x * (0.5 * (qt_e + fq.y));
         }
       }
     }
-    const double psi_lo = M.g * (h[cc.x] + M.b[cc.x]) + K[cc.x];
-    const double psi_hi = M.g * (h[cc.y] + M.b[cc.y]) + K[cc.y];
+    const double psi_lo = M.g * (h[cc.x] + M.b[cc.x]) + ldx<CG>(K + cc.x);
+    const double psi_hi = M.g * (h[cc.y] + M.b[cc.y]) + ldx<CG>(K + cc.y);
     const double du = -pvflux - (psi_lo - psi_hi) * inv_d;
     apply_op(a.eop[seg], e, du);
   }
+}
+
+__device__ __forceinline__ void item_out(const DevMesh& M, const double* __restrict__ h,
+                                         const double* __restrict__ K,
+                                         const double2* __restrict__ FQ, const OutArgs& a,
+                                         int32_t t) {
+  item_out_sp<false>(M, h, K, FQ, a.cs, a.es, a, t);
 }
 
 __global__ void MSWM_KOUT_BOUNDS k_out(DevMesh M, const double* __restrict__ h,
@@ -444,6 +463,122 @@ __global__ void __launch_bounds__(kBlock) k_fused_eval(FusedArgs f) {
   {
     const int32_t n = f.out.cs.n() + f.out.es.n();
     for (int32_t t = t0; t < n; t += stride) item_out(f.M, f.h, f.K, f.FQ, f.out, t);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Dataflow evaluation (k_flow): the three phases of one evaluation as one
+// persistent launch whose work items are (phase, cell slab) pairs.  Slab k =
+// cells [kS, (k+1)S) plus the edges and vertices whose lowest cell lies in
+// it (edges and vertices are sorted by their cells).  A warp takes items
+// from a fixed topological order, waits for the completion flags of the
+// items it reads from, and publishes its own completion:
+//   A_k (PV, K)  reads only h, u;
+//   B_k (F, q~)  reads PV of the vertices of its edges;
+//   C_k (dh, du) reads (F, q~) of the ring edges of its cells and of both
+//                cells of its edges (stencils are inside those rings), and K
+//                of both cells of its edges.
+// Dependencies are slab sets computed at create over all elements of a
+// slab, so they hold for every mask.
+// The order keeps producers a fixed lag ahead of their consumers, so PV, K
+// and (F, q~) are read back from L2 instead of HBM and the h, u and edge
+// tables the three phases share are fetched from HBM once.  Per-element
+// arithmetic is the item_* functions of the three-kernel path: bitwise the
+// same results.
+struct FlowSpan {
+  int32_t base, n_range;  // the span's range part
+  const int32_t* list;    // its list part, ascending
+  const int32_t* lofs;    // [nS+1] offsets of each slab's entries in list (null: no list)
+};
+
+__device__ __forceinline__ Span slab_span(const FlowSpan& f, int32_t lo, int32_t hi, int32_t k) {
+  Span s;
+  const int32_t a = max(f.base, lo), b = min(f.base + f.n_range, hi);
+  s.base = a;
+  s.n_range = b > a ? b - a : 0;
+  if (f.lofs) {
+    const int32_t o = f.lofs[k];
+    s.list = f.list + o;
+    s.n_list = f.lofs[k + 1] - o;
+  } else {
+    s.list = nullptr;
+    s.n_list = 0;
+  }
+  return s;
+}
+
+struct FlowArgs {
+  DevMesh M;
+  const double* h;
+  const double* u;
+  FlowSpan vs, ks, es, cs, eo;  // closure spans (A: vs, ks; B: es), outputs (C: cs, eo)
+  const int32_t* slab_v0;       // [nS+1] first vertex of each slab
+  const int32_t* slab_e0;       // [nS+1] first edge of each slab
+  const int32_t* dep_off;       // [2 nS + 1] dependencies of B_k at [k], of C_k at [nS + k]
+  const int32_t* dep;           // flag indices (A slab j: j, B slab j: nS + j)
+  const int32_t* order;         // item codes: phase << 28 | slab
+  int32_t S, nS, n_items;
+  int32_t* flags;  // [2][nS] A / B slab complete (zeroed before the launch)
+  double* pv;
+  double* K;
+  double2* FQ;
+  int32_t* dry;
+  const uint32_t* vmask;
+  OutArgs out;
+};
+
+__device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Completion protocol: a producer warp publishes flags[slab] = 1 after a
+// fence (release); a consumer warp's lanes acquire-load the flags of the
+// exact slabs its item reads (dep lists, built at create) and the warp
+// barrier orders those acquisitions before every lane's reads.
+__device__ __forceinline__ void flow_wait(const FlowArgs& f, int32_t d0, int32_t d1, int lane) {
+  for (int32_t d = d0 + lane; d < d1; d += 32) {
+    const int32_t* fl = f.flags + f.dep[d];
+    while (ld_acquire(fl) == 0) __nanosleep(64);
+  }
+  __syncwarp();
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) k_flow(const __grid_constant__ FlowArgs f) {
+  const int lane = threadIdx.x & 31;
+  const int32_t nwarps = gridDim.x * (kBlock / 32);
+  for (int32_t q = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); q < f.n_items; q += nwarps) {
+    const int32_t code = f.order[q];
+    const int ph = code >> 28;
+    const int32_t k = code & 0x0FFFFFFF;
+    const int32_t c_lo = k * f.S, c_hi = min(c_lo + f.S, f.M.nC);
+    if (ph == 0) {
+      const Span vs = slab_span(f.vs, f.slab_v0[k], f.slab_v0[k + 1], k);
+      const Span ks = slab_span(f.ks, c_lo, c_hi, k);
+      const int32_t n = vs.n() + ks.n();
+      for (int32_t t = lane; t < n; t += 32)
+        item_vertex_cell(f.M, f.h, f.u, vs, ks, f.pv, f.K, f.dry, f.vmask, t);
+    } else if (ph == 1) {
+      flow_wait(f, f.dep_off[k], f.dep_off[k + 1], lane);
+      const Span es = slab_span(f.es, f.slab_e0[k], f.slab_e0[k + 1], k);
+      const int32_t n = es.n();
+      for (int32_t t = lane; t < n; t += 32) item_edge_fq<true>(f.M, f.h, f.u, f.pv, es, f.FQ, t);
+    } else {
+      flow_wait(f, f.dep_off[f.nS + k], f.dep_off[f.nS + k + 1], lane);
+      const Span cs = slab_span(f.cs, c_lo, c_hi, k);
+      const Span eo = slab_span(f.eo, f.slab_e0[k], f.slab_e0[k + 1], k);
+      const int32_t n = cs.n() + eo.n();
+      for (int32_t t = lane; t < n; t += 32) item_out_sp<true>(f.M, f.h, f.K, f.FQ, cs, eo, f.out, t);
+    }
+    if (ph < 2) {
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        atomicExch(f.flags + ph * f.nS + k, 1);
+      }
+    }
   }
 }
 

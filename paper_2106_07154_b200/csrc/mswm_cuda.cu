@@ -122,6 +122,8 @@ struct MaskPlan {
     int32_t base = 0, n_range = 0, n_list = 0;
     const int32_t* list = nullptr;
     DArr<int32_t> own;
+    std::vector<int32_t> host_list;  // the list part, ascending
+    DArr<int32_t> lofs;              // dataflow path: per-slab offsets into list
     Span dev() const { return Span{base, n_range, list, n_list}; }
     int64_t n() const { return int64_t(n_range) + n_list; }
   } sv, sk, se, sc_out, se_out;
@@ -130,6 +132,7 @@ struct MaskPlan {
   int32_t ntiles = 0;
   bool use_tiles = false;
   bool use_coop = false;  // small mask: one cooperative launch (k_fused_eval)
+  bool use_flow = false;  // large mask: one dataflow launch (k_flow)
   std::vector<int32_t> host_cells, host_edges;  // original ids, same order as device lists
 };
 
@@ -236,6 +239,12 @@ struct mswm_cuda_ctx {
   };
   std::vector<Slab> slabs;
   size_t tile_smem = 0;
+  // dataflow evaluation (k_flow): cell slabs, dependencies, item order
+  bool flow_ok = false;
+  int32_t flow_S = 0, flow_nS = 0, flow_grid = 0, flow_lag = 0;
+  const void* flow_fn = nullptr;
+  std::vector<int32_t> h_flow_v0, h_flow_e0;
+  DArr<int32_t> flow_v0, flow_e0, flow_dep_off, flow_dep, flow_order, flow_sync;
   DArr<int2> e_cells, e_verts;
   double gravity = 9.80616;
   bool have_fields = false;
@@ -817,6 +826,124 @@ void build_slabs(mswm_cuda_ctx* c, const std::vector<int32_t>& c_edge,
   }
 }
 
+// Dataflow evaluation (k_flow, kernels.cuh): cell slabs of S cells, the
+// edge / vertex range of each slab, each B / C item's dependency slabs and
+// the item order.  Needs edges and vertices sorted by their lowest cell
+// (make_orders guarantees it).  Opt-in (MSWM_FLOW=1; MSWM_FLOW_SLAB,
+// MSWM_FLOW_LAG, MSWM_FLOW_MINB tune): measured 1.7x slower than the three
+// streamed kernels on C4 (profiles/r1_fusion_experiments.md).
+void build_flow(mswm_cuda_ctx* c, const std::vector<int32_t>& v_cell,
+                const std::vector<int2>& e_cells, const std::vector<int2>& e_verts,
+                const std::vector<int32_t>& c_edge, const std::vector<uint8_t>& c_deg) {
+  c->flow_ok = false;
+  const char* fe = std::getenv("MSWM_FLOW");
+  if (!fe || fe[0] != '1') return;
+  const int32_t nC = c->nC, nE = c->nE, nV = c->nV;
+  int32_t S = 64;
+  if (const char* ss = std::getenv("MSWM_FLOW_SLAB")) S = std::max(8, std::atoi(ss));
+  const int32_t nS = (nC + S - 1) / S;
+  if (nS < 64) return;  // small meshes: launch latency, not traffic, dominates
+  std::vector<int32_t> e0(nS + 1, nE), v0(nS + 1, nV), vslab(nV);
+  int32_t prev = -1;
+  for (int32_t e = 0; e < nE; ++e) {
+    const int32_t t = std::min(e_cells[e].x, e_cells[e].y) / S;
+    if (t < prev) return;
+    for (int32_t q = prev + 1; q <= t; ++q) e0[q] = e;
+    prev = t;
+  }
+  for (int32_t q = prev + 1; q <= nS; ++q) e0[q] = nE;
+  prev = -1;
+  for (int32_t v = 0; v < nV; ++v) {
+    const int32_t t =
+        std::min(v_cell[v], std::min(v_cell[size_t(nV) + v], v_cell[2 * size_t(nV) + v])) / S;
+    if (t < prev) return;
+    vslab[v] = t;
+    for (int32_t q = prev + 1; q <= t; ++q) v0[q] = v;
+    prev = t;
+  }
+  for (int32_t q = prev + 1; q <= nS; ++q) v0[q] = nV;
+  auto eslab = [&](int32_t e) { return std::min(e_cells[e].x, e_cells[e].y) / S; };
+  // dependency lists: B_k at [k], C_k at [nS + k]; entries are flag indices
+  std::vector<int32_t> dep_off(2 * size_t(nS) + 1, 0), dep, mark(2 * size_t(nS), -1);
+  std::vector<int32_t> maxdep(2 * size_t(nS), 0);
+  dep.reserve(12 * size_t(nS));
+  int32_t item = 0;
+  auto add = [&](int32_t flag) {
+    if (mark[flag] == item) return;
+    mark[flag] = item;
+    dep.push_back(flag);
+    maxdep[item] = std::max(maxdep[item], flag % nS);
+  };
+  for (int32_t k = 0; k < nS; ++k, ++item) {
+    dep_off[item] = int32_t(dep.size());
+    for (int32_t e = e0[k]; e < e0[k + 1]; ++e) {
+      add(vslab[e_verts[e].x]);
+      add(vslab[e_verts[e].y]);
+    }
+  }
+  auto ring = [&](int32_t i) {
+    for (int j = 0; j < c_deg[i]; ++j) add(nS + eslab(c_edge[size_t(j) * nC + i]));
+  };
+  for (int32_t k = 0; k < nS; ++k, ++item) {
+    dep_off[item] = int32_t(dep.size());
+    for (int32_t i = k * S; i < std::min(nC, (k + 1) * S); ++i) ring(i);
+    for (int32_t e = e0[k]; e < e0[k + 1]; ++e)
+      for (int32_t i : {e_cells[e].x, e_cells[e].y}) {
+        add(i / S);
+        ring(i);
+      }
+  }
+  dep_off[item] = int32_t(dep.size());
+  int per_sm = 0, n_sm = 0;
+  int minb = 8;
+  if (const char* mb = std::getenv("MSWM_FLOW_MINB")) minb = std::atoi(mb);
+  c->flow_fn = minb >= 8 ? reinterpret_cast<const void*>(k_flow<8>)
+               : minb >= 6 ? reinterpret_cast<const void*>(k_flow<6>)
+                           : reinterpret_cast<const void*>(k_flow<4>);
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->flow_fn, kBlock, 0));
+  CK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, c->device));
+  if (per_sm < 1) return;
+  c->flow_grid = per_sm * n_sm;
+  // Producers run `lag` slabs ahead of their consumers -- about a third of
+  // the warps in flight -- so a consumer's inputs are complete when it starts.
+  int32_t lag = c->flow_grid * (kBlock / 32) / 3;
+  if (const char* sl = std::getenv("MSWM_FLOW_LAG")) lag = std::max(1, std::atoi(sl));
+  lag = std::min(lag, nS);
+  // B_k follows A_{max(k, deps) + lag}; C_k follows B_{max deps + lag}
+  std::vector<std::vector<int32_t>> bq(nS), cq(nS);
+  for (int32_t k = 0; k < nS; ++k) {
+    bq[std::min(nS - 1, std::max(k, maxdep[k]) + lag)].push_back(k);
+    cq[std::min(nS - 1, std::max(k, maxdep[nS + k]) + lag)].push_back(k);
+  }
+  // B buckets are keyed by k + lag, so B slabs come out in index order and
+  // C_k, emitted right after B_m, finds every B slab <= m (and every A slab
+  // <= m, which precede B_m) already in the order: the order is topological.
+  std::vector<int32_t> order;
+  order.reserve(3 * size_t(nS));
+  for (int32_t k = 0; k < nS; ++k) {
+    order.push_back(k);
+    for (int32_t b : bq[k]) {
+      order.push_back((1 << 28) | b);
+      for (int32_t j : cq[b]) order.push_back((2 << 28) | j);
+    }
+  }
+  if (int32_t(order.size()) != 3 * nS) throw Error(MSWM_E_CONFIG, "flow order construction");
+  cudaStream_t s = c->stream;
+  c->flow_v0.upload(v0, s);
+  c->flow_e0.upload(e0, s);
+  c->flow_dep_off.upload(dep_off, s);
+  c->flow_dep.upload(dep, s);
+  c->flow_order.upload(order, s);
+  c->flow_sync.alloc(2 * size_t(nS));
+  CK(cudaStreamSynchronize(s));
+  c->h_flow_v0 = std::move(v0);
+  c->h_flow_e0 = std::move(e0);
+  c->flow_S = S;
+  c->flow_nS = nS;
+  c->flow_lag = lag;
+  c->flow_ok = true;
+}
+
 void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell_order) {
   const int32_t nC = d->n_cells, nE = d->n_edges, nV = d->n_vertices;
   if (nC <= 0 || nE <= 0 || nV <= 0) throw Error(MSWM_E_TOPOLOGY, "empty mesh");
@@ -940,6 +1067,7 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
     need_explicit = true;
   }
   if (!c->tile_path) build_slabs(c, c_edge, c_vert, c_nbr, c_deg, e_cells);
+  if (!c->tile_path) build_flow(c, v_cell, e_cells, e_verts, c_edge, c_deg);
   std::vector<double> e_len(nE), e_ld(nE), e_dual(nE), e_invd(nE);
   std::vector<uint8_t> e_nst, e_slots;
   std::vector<int32_t> e_sten;
@@ -1103,6 +1231,7 @@ void make_span(mswm_cuda_ctx* c, const int32_t* d_list, int32_t n, int32_t unive
     if (!rest.empty()) {
       out.own.upload(rest, c->stream);
       out.list = out.own.p;
+      out.host_list = std::move(rest);
     }
     return;
   }
@@ -1113,6 +1242,7 @@ void make_span(mswm_cuda_ctx* c, const int32_t* d_list, int32_t n, int32_t unive
   out.own.upload(h, c->stream);
   out.list = out.own.p;
   out.n_list = n;
+  out.host_list = std::move(h);
 }
 
 MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
@@ -1207,6 +1337,28 @@ MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
                 int64_t(p->nc) + p->ne < (int64_t(c->nC) + c->nE) / 5;
   p->use_tiles = c->tile_path ||
                  (c->hybrid && int64_t(p->nc) + p->ne < (int64_t(c->nC) + c->nE) / 5);
+  p->use_flow = c->flow_ok && !p->use_tiles && !p->use_coop && c->slabs.empty() &&
+                int64_t(p->nc) + p->ne >= (int64_t(c->nC) + c->nE) / 4;
+  if (p->use_flow) {
+    // per-slab offsets of the spans' list parts (kind 0 cells, 1 edges, 2 vertices)
+    const int32_t nS = c->flow_nS, S = c->flow_S;
+    auto lofs = [&](MaskPlan::HSpan& sp, int kind) {
+      if (!sp.n_list) return;
+      std::vector<int32_t> o(size_t(nS) + 1);
+      for (int32_t k = 0; k < nS; ++k) {
+        const int32_t bound = kind == 0 ? k * S : kind == 1 ? c->h_flow_e0[k] : c->h_flow_v0[k];
+        o[k] = int32_t(std::lower_bound(sp.host_list.begin(), sp.host_list.end(), bound) -
+                       sp.host_list.begin());
+      }
+      o[nS] = sp.n_list;
+      sp.lofs.upload(o, s);
+    };
+    lofs(p->sv, 2);
+    lofs(p->sk, 0);
+    lofs(p->se, 1);
+    lofs(p->sc_out, 0);
+    lofs(p->se_out, 1);
+  }
   if (p->use_tiles) {
     // tiles with outputs; the tiles compute closure supersets, so the dry
     // check always consults the closure bitmask
@@ -1348,6 +1500,57 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
         CK(cudaGetLastError());
       }
     }
+    if (rec) CK(cudaEventRecordWithFlags(rec->stop, s, cudaEventRecordExternal));
+    return;
+  }
+  // The dataflow launch overlaps the phases, so a stage update must not
+  // write the arrays the evaluation reads.
+  bool flow = p.use_flow;
+  for (int g = 0; g < 2 && flow; ++g)
+    for (const Op* o : {&cop[g], &eop[g]})
+      flow &= o->dst != h && o->dst != u && o->acc != h && o->acc != u;
+  if (flow) {
+    auto fspan = [](const MaskPlan::HSpan& sp) {
+      return FlowSpan{sp.base, sp.n_range, sp.list, sp.n_list ? sp.lofs.p : nullptr};
+    };
+    FlowArgs fa;
+    std::memset(&fa, 0, sizeof(fa));
+    fa.M = M;
+    fa.h = h;
+    fa.u = u;
+    fa.vs = fspan(p.sv);
+    fa.ks = fspan(p.sk);
+    fa.es = fspan(p.se);
+    fa.cs = fspan(p.sc_out);
+    fa.eo = fspan(p.se_out);
+    fa.slab_v0 = c->flow_v0.p;
+    fa.slab_e0 = c->flow_e0.p;
+    fa.dep_off = c->flow_dep_off.p;
+    fa.dep = c->flow_dep.p;
+    fa.order = c->flow_order.p;
+    fa.S = c->flow_S;
+    fa.nS = c->flow_nS;
+    fa.n_items = int32_t(c->flow_order.n);
+    fa.flags = c->flow_sync.p;
+    fa.pv = c->pv.p;
+    fa.K = c->K.p;
+    fa.FQ = c->FQ.p;
+    fa.dry = c->dry_vertex.p;
+    fa.vmask = p.vmask.p;
+    fa.out.mask = p.mask;
+    fa.out.ckey = c->have_regions ? c->ckey.p : nullptr;
+    fa.out.ekey = c->have_regions ? c->ekey.p : nullptr;
+    fa.out.cop[0] = cop[0];
+    fa.out.cop[1] = cop[1];
+    fa.out.eop[0] = eop[0];
+    fa.out.eop[1] = eop[1];
+    CK(cudaMemsetAsync(c->flow_sync.p, 0, c->flow_sync.n * sizeof(int32_t), s));
+    void* args[] = {&fa};
+    // cooperative: every CTA is resident, so a warp never waits on an item
+    // held by a CTA that has not started
+    CK(cudaLaunchCooperativeKernel(c->flow_fn, dim3(c->flow_grid), dim3(kBlock),
+                                   args, 0, s));
+    ++c->launches;
     if (rec) CK(cudaEventRecordWithFlags(rec->stop, s, cudaEventRecordExternal));
     return;
   }
@@ -2277,6 +2480,16 @@ int mswm_cuda_layout_info(const mswm_cuda_ctx* c, int* kernel_path, int* identit
   if (!c) return MSWM_E_USAGE;
   if (kernel_path) *kernel_path = c->tile_path ? 2 : (c->ring_derived ? 1 : (c->hybrid ? 3 : 0));
   if (identity_order) *identity_order = c->identity ? 1 : 0;
+  return MSWM_OK;
+}
+
+int mswm_cuda_flow_info(const mswm_cuda_ctx* c, int* slab_cells, int* n_slabs, int* lag,
+                        int* grid) {
+  if (!c) return MSWM_E_USAGE;
+  if (slab_cells) *slab_cells = c->flow_ok ? c->flow_S : 0;
+  if (n_slabs) *n_slabs = c->flow_ok ? c->flow_nS : 0;
+  if (lag) *lag = c->flow_ok ? c->flow_lag : 0;
+  if (grid) *grid = c->flow_ok ? c->flow_grid : 0;
   return MSWM_OK;
 }
 

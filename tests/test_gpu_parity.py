@@ -333,3 +333,59 @@ def test_optional_evaluation_paths_bitwise(env, monkeypatch):
         ctx.advance(scheme, dt, wl.M, n)
         st = ctx.download()
         assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref), (env, scheme)
+
+
+@pytest.mark.parametrize("slab,lag,order", [(16, 1, "hilbert"), (64, 8, "regions"),
+                                            (256, 3, "hilbert"), (32, 100000, "regions")])
+def test_dataflow_evaluation_bitwise(slab, lag, order, monkeypatch):
+    """k_flow (one persistent launch per large evaluation, phases overlapped
+    through per-slab completion flags) stays bitwise equal for any slab size,
+    producer lag and numbering -- lag 1 makes consumers wait on producers."""
+    monkeypatch.setenv("MSWM_FLOW", "1")
+    monkeypatch.setenv("MSWM_FLOW_SLAB", str(slab))
+    monkeypatch.setenv("MSWM_FLOW_LAG", str(lag))
+    wl = W.small_sphere(6, seed=31, cap_deg=20.0)
+    o = _oracle_for(wl)
+    ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order, fine_mask=wl.fine_mask)
+    info = ctx.flow_info()
+    assert info["slab_cells"] == slab and info["n_slabs"] == -(-wl.mesh.n_cells // slab)
+    ctx.make_regions(wl.fine_mask, wl.width)
+    ev = CudaEvaluator(ctx)
+    for mask in LTS3_MASKS + [kMaskAll]:
+        dh1 = np.full(wl.mesh.n_cells, SENTINEL)
+        du1 = np.full(wl.mesh.n_edges, SENTINEL)
+        dh2, du2 = dh1.copy(), du1.copy()
+        ev.eval(wl.h, wl.u, mask, dh1, du1)
+        o.eval(wl.h, wl.u, mask, dh2, du2)
+        assert bits_equal(dh1, dh2) and bits_equal(du1, du2), hex(mask)
+    for scheme, n, dt in [(Scheme.LTS3, 5, wl.dt), (Scheme.RK4, 3, wl.dt / wl.M),
+                          (Scheme.SSPRK3, 2, wl.dt / wl.M)]:
+        h_ref, u_ref, _ = o.step(int(scheme), wl.h, wl.u, 0.0, dt, wl.M, n)
+        ctx.upload(State(wl.h, wl.u, 0.0))
+        ctx.advance(scheme, dt, wl.M, n)
+        st = ctx.download()
+        assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref), scheme
+    # the large evaluations are one launch each
+    ctx.upload(State(wl.h, wl.u, 0.0))
+    ctx.advance(Scheme.LTS3, wl.dt, wl.M, 1)
+    monkeypatch.setenv("MSWM_FLOW", "0")
+    c0 = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order, fine_mask=wl.fine_mask)
+    c0.make_regions(wl.fine_mask, wl.width)
+    c0.upload(State(wl.h, wl.u, 0.0))
+    c0.advance(Scheme.LTS3, wl.dt, wl.M, 1)
+    assert ctx.kernels_per_step() < c0.kernels_per_step()
+
+
+def test_dataflow_disabled_matches(monkeypatch):
+    """Without MSWM_FLOW=1 the three-kernel path runs (same bits)."""
+    monkeypatch.delenv("MSWM_FLOW", raising=False)
+    wl = W.small_sphere(6, seed=31, cap_deg=20.0)
+    ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, fine_mask=wl.fine_mask)
+    assert ctx.flow_info()["slab_cells"] == 0
+    o = _oracle_for(wl)
+    ctx.make_regions(wl.fine_mask, wl.width)
+    h_ref, u_ref, _ = o.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, wl.M, 3)
+    ctx.upload(State(wl.h, wl.u, 0.0))
+    ctx.advance(Scheme.LTS3, wl.dt, wl.M, 3)
+    st = ctx.download()
+    assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
