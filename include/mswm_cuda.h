@@ -162,8 +162,9 @@ int mswm_cuda_state_download(mswm_cuda_ctx* ctx, double* h, double* u,
 
 /* n_steps of Stepper::step (integrators.cpp:577-596) on the device state:
  * scheme in mswm_scheme, dt the coarse step for LTS and the global step
- * otherwise, M the substep count (LTS only).  LTS3 = lts_step(3)
- * (:412-575), RK4 = rk4_step (:370-410), SSPRK3 = ssprk_step(3) (:337-368).
+ * otherwise, M the substep count (LTS only).  LTS3 / LTS2 = lts_step(3 / 2)
+ * (:412-575), RK4 = rk4_step (:370-410), SSPRK3 / SSPRK2 = ssprk_step(3 / 2)
+ * (:337-368).
  * Steps are replayed from a captured CUDA graph.  Asynchronous when
  * `sync` is 0 (errors then surface at the next synchronous call). */
 int mswm_cuda_step(mswm_cuda_ctx* ctx, int scheme, double dt, int M,

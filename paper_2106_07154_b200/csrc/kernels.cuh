@@ -96,6 +96,8 @@ enum OpKind : int {
   OP_ACC,          // acc = (first ? 0.0 : acc) + d
   OP_ACC_CORR,     // a3 = (first ? 0.0 : acc) + d;
                    // dst = y0 + c0*(((c1*a1) + (c1*a2)) + (c2*a3))
+  OP_ACC_CORR2,    // second order: a2 = (first ? 0.0 : acc) + d;
+                   // dst = y0 + c0*((c1*a1) + (c1*a2))
   OP_RK4_FIRST,    // acc = d;              dst = y0 + c0*d
   OP_RK4_MID,      // acc = acc + 2.0*d;    dst = y0 + c0*d
   OP_RK4_LAST,     // dst = y0 + c0*(acc + d)
@@ -130,6 +132,11 @@ __device__ __forceinline__ void apply_op(const Op& op, int32_t i, double d) {
     case OP_ACC_CORR: {
       const double a3 = (op.first ? 0.0 : op.acc[i]) + d;
       op.dst[i] = op.y0[i] + op.c0 * (op.c1 * op.a1[i] + op.c1 * op.a2[i] + op.c2 * a3);
+      break;
+    }
+    case OP_ACC_CORR2: {
+      const double a2 = (op.first ? 0.0 : op.acc[i]) + d;
+      op.dst[i] = op.y0[i] + op.c0 * (op.c1 * op.a1[i] + op.c1 * a2);
       break;
     }
     case OP_RK4_FIRST:
@@ -348,8 +355,9 @@ __global__ void MSWM_KOUT_BOUNDS k_out(DevMesh M, const double* __restrict__ h,
 }
 
 // ---------------------------------------------------------------------------
-// Interface-1 prediction (integrators.cpp:217-227, order 3):
-// dst = ((c0*s0) + (c1*s1)) + (c2*s2) on the I1 lists.
+// Interface-1 prediction (integrators.cpp:217-227): order 3
+// dst = ((c0*s0) + (c1*s1)) + (c2*s2), order 2 (s2 null) (c0*s0) + (c1*s1),
+// on the I1 lists.
 __global__ void k_predict(const int32_t* __restrict__ clist, int32_t nc,
                           const int32_t* __restrict__ elist, int32_t ne, double c0, double c1,
                           double c2, const double* __restrict__ hs0, const double* __restrict__ hs1,
@@ -359,16 +367,18 @@ __global__ void k_predict(const int32_t* __restrict__ clist, int32_t nc,
   const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < nc) {
     const int32_t i = clist[t];
-    hdst[i] = c0 * hs0[i] + c1 * hs1[i] + c2 * hs2[i];
+    // second order (hs2 null): w_old*y_old + w_first*y1 (integrators.cpp:221-222)
+    hdst[i] = hs2 ? c0 * hs0[i] + c1 * hs1[i] + c2 * hs2[i] : c0 * hs0[i] + c1 * hs1[i];
   } else if (t - nc < ne) {
     const int32_t e = elist[t - nc];
-    udst[e] = c0 * us0[e] + c1 * us1[e] + c2 * us2[e];
+    udst[e] = us2 ? c0 * us0[e] + c1 * us1[e] + c2 * us2[e] : c0 * us0[e] + c1 * us1[e];
   }
 }
 
 // Substep prologue: save the values the predictions and the correction
 // read (old state on I1 u I2, stage-1/2 values on I1), then write the
-// stage-1 prediction of substep 0.  Lists are [I1 | I2].
+// stage-1 prediction of substep 0.  Lists are [I1 | I2].  Second order:
+// H2 / U2 null, no second stage value, two-term prediction.
 __global__ void k_save_predict(const int32_t* __restrict__ clist, int32_t nc, int32_t nc1,
                                const int32_t* __restrict__ elist, int32_t ne, int32_t ne1,
                                double c0, double c1, double c2, double* __restrict__ H,
@@ -384,10 +394,15 @@ __global__ void k_save_predict(const int32_t* __restrict__ clist, int32_t nc, in
     const double y0 = H[i];
     HS0[i] = y0;
     if (t < nc1) {
-      const double y1 = H1[i], y2 = H2[i];
+      const double y1 = H1[i];
       HS1[i] = y1;
-      HS2[i] = y2;
-      H[i] = c0 * y0 + c1 * y1 + c2 * y2;
+      if (H2) {
+        const double y2 = H2[i];
+        HS2[i] = y2;
+        H[i] = c0 * y0 + c1 * y1 + c2 * y2;
+      } else {
+        H[i] = c0 * y0 + c1 * y1;
+      }
     }
   } else if (t - nc < ne) {
     const int32_t q = t - nc;
@@ -395,10 +410,15 @@ __global__ void k_save_predict(const int32_t* __restrict__ clist, int32_t nc, in
     const double y0 = U[e];
     US0[e] = y0;
     if (q < ne1) {
-      const double y1 = U1[e], y2 = U2[e];
+      const double y1 = U1[e];
       US1[e] = y1;
-      US2[e] = y2;
-      U[e] = c0 * y0 + c1 * y1 + c2 * y2;
+      if (U2) {
+        const double y2 = U2[e];
+        US2[e] = y2;
+        U[e] = c0 * y0 + c1 * y1 + c2 * y2;
+      } else {
+        U[e] = c0 * y0 + c1 * y1;
+      }
     }
   }
 }
@@ -415,10 +435,12 @@ struct PredArgs {
 __device__ __forceinline__ void item_predict(const PredArgs& p, int32_t t) {
   if (t < p.nc) {
     const int32_t i = p.clist[t];
-    p.hdst[i] = p.c0 * p.hs0[i] + p.c1 * p.hs1[i] + p.c2 * p.hs2[i];
+    p.hdst[i] = p.hs2 ? p.c0 * p.hs0[i] + p.c1 * p.hs1[i] + p.c2 * p.hs2[i]
+                      : p.c0 * p.hs0[i] + p.c1 * p.hs1[i];
   } else if (t - p.nc < p.ne) {
     const int32_t e = p.elist[t - p.nc];
-    p.udst[e] = p.c0 * p.us0[e] + p.c1 * p.us1[e] + p.c2 * p.us2[e];
+    p.udst[e] = p.us2 ? p.c0 * p.us0[e] + p.c1 * p.us1[e] + p.c2 * p.us2[e]
+                      : p.c0 * p.us0[e] + p.c1 * p.us1[e];
   }
 }
 

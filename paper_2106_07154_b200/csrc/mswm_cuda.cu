@@ -1668,18 +1668,18 @@ constexpr unsigned kMaskSub = MSWM_CELLS_FINE_PLAIN | MSWM_CELLS_UF1 | MSWM_CELL
                               MSWM_CELLS_IF1 | MSWM_CELLS_IF2 | MSWM_EDGES_FINE_PLAIN |
                               MSWM_EDGES_UFINE | MSWM_EDGES_IF1 | MSWM_EDGES_IF2;
 
-// lts_interp_coeffs (integrators.cpp:186-212), order 3
-void lts3_coeffs(int stage, int k, int M, double out[3]) {
+// lts_interp_coeffs (integrators.cpp:186-212)
+void lts_coeffs(int order, int stage, int k, int M, double out[3]) {
   const double kd = k, Md = M;
   double x = 0.0, xt = 0.0;
   switch (stage) {
     case 1:
       x = kd / Md;
-      xt = (kd * kd) / (Md * Md);
+      xt = (order == 3) ? (kd * kd) / (Md * Md) : 0.0;
       break;
     case 2:
       x = (kd + 1.0) / Md;
-      xt = (kd * (kd + 2.0)) / (Md * Md);
+      xt = (order == 3) ? (kd * (kd + 2.0)) / (Md * Md) : 0.0;
       break;
     default:
       x = (2.0 * kd + 1.0) / (2.0 * Md);
@@ -1708,23 +1708,26 @@ IfLists if_lists(mswm_cuda_ctx* c) {
   return L;
 }
 
-void launch_predict(mswm_cuda_ctx* c, int stage, int k, int M, double* hdst, double* udst) {
+void launch_predict(mswm_cuda_ctx* c, int stage, int k, int M, double* hdst, double* udst,
+                    int order = 3) {
   const IfLists L = if_lists(c);
   double w[3];
-  lts3_coeffs(stage, k, M, w);
+  lts_coeffs(order, stage, k, M, w);
   const int64_t n = int64_t(L.nc1) + L.ne1;
   if (n == 0) return;
+  const bool o3 = order == 3;
   k_predict<<<nblk(n), kBlock, 0, c->ls>>>(L.c, L.nc1, L.e, L.ne1, w[0], w[1], w[2], c->S0h.p,
-                                           c->S1h.p, c->S2h.p, hdst, c->S0u.p, c->S1u.p, c->S2u.p,
-                                           udst);
+                                           c->S1h.p, o3 ? c->S2h.p : nullptr, hdst, c->S0u.p,
+                                           c->S1u.p, o3 ? c->S2u.p : nullptr, udst);
   CK(cudaGetLastError());
   ++c->launches;
 }
 
-PredArgs make_pred(mswm_cuda_ctx* c, int stage, int k, int M, double* hdst, double* udst) {
+PredArgs make_pred(mswm_cuda_ctx* c, int stage, int k, int M, double* hdst, double* udst,
+                   int order = 3) {
   const IfLists L = if_lists(c);
   double w[3];
-  lts3_coeffs(stage, k, M, w);
+  lts_coeffs(order, stage, k, M, w);
   PredArgs pa;
   pa.clist = L.c;
   pa.nc = L.nc1;
@@ -1735,10 +1738,10 @@ PredArgs make_pred(mswm_cuda_ctx* c, int stage, int k, int M, double* hdst, doub
   pa.c2 = w[2];
   pa.hs0 = c->S0h.p;
   pa.hs1 = c->S1h.p;
-  pa.hs2 = c->S2h.p;
+  pa.hs2 = order == 3 ? c->S2h.p : nullptr;
   pa.us0 = c->S0u.p;
   pa.us1 = c->S1u.p;
-  pa.us2 = c->S2u.p;
+  pa.us2 = order == 3 ? c->S2u.p : nullptr;
   pa.hdst = hdst;
   pa.udst = udst;
   return pa;
@@ -1838,7 +1841,7 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
   for (auto* c : cs) {
     const IfLists L = if_lists(c);
     double w[3];
-    lts3_coeffs(1, 0, M, w);
+    lts_coeffs(3, 1, 0, M, w);
     const int64_t n = int64_t(L.nc) + L.ne;
     if (n > 0) {
       k_save_predict<<<nblk(n), kBlock, 0, c->ls>>>(
@@ -1910,6 +1913,100 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
     Op co[2] = {mk_op(OP_WCOMB, H, H, third, H2, two3, cr), mk_op(OP_WCOMB, H, H, third, H2, two3, cr)};
     Op eo[2] = {mk_op(OP_WCOMB, U, U, third, U2, two3, cr), mk_op(OP_WCOMB, U, U, third, U2, two3, cr)};
     launch_eval(c, plan_for(c, kMaskCoarseOnly), H2, U2, co, eo);
+  }
+}
+
+// One LTS2 coarse step (Stepper::lts_step(2, ...), integrators.cpp:412-575
+// with order 2) on the LTS3 aliasing: ha = state, hb = h1.  Step 2 -- the
+// coarse finalisation h = 0.5 h_old + 0.5 h1 + (0.5 dt) dh -- runs after the
+// substeps, in place: it reads h1 only on interface-2 / coarse elements,
+// which the substeps never write, and the substeps read the state's coarse
+// entries as h_old, which it overwrites.  Evaluations are pure functions of
+// their inputs, so the reordering changes no bits.
+void enqueue_lts2(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
+  const double delta = dt / M;
+  bool fuse_pred = true;
+  for (auto* c : cs) fuse_pred &= !c->halo.active();
+  using C = mswm_cuda_ctx;
+  // Step 1 (:483-487): h1 = h_old + dt*dh on I1 u I2 u C.
+  exchange(cs, &C::H, &C::U);
+  for (auto* c : cs) {
+    double *H = c->H.p, *U = c->U.p, *H1 = c->H1.p, *U1 = c->U1.p;
+    Op co[2] = {mk_op(OP_EULER, H1, H, dt), mk_op(OP_EULER, H1, H, dt)};
+    Op eo[2] = {mk_op(OP_EULER, U1, U, dt), mk_op(OP_EULER, U1, U, dt)};
+    launch_eval(c, plan_for(c, kMaskIfCoarse), H, U, co, eo);
+  }
+  // Substep prologue: save I1 u I2 old values and I1 stage-1 values, predict
+  // stage 1 of substep 0 (two-term) into the state.
+  for (auto* c : cs) {
+    const IfLists L = if_lists(c);
+    double w[3];
+    lts_coeffs(2, 1, 0, M, w);
+    const int64_t n = int64_t(L.nc) + L.ne;
+    if (n > 0) {
+      k_save_predict<<<nblk(n), kBlock, 0, c->ls>>>(
+          L.c, L.nc, L.nc1, L.e, L.ne, L.ne1, w[0], w[1], w[2], c->H.p, c->H1.p, nullptr, c->S0h.p,
+          c->S1h.p, nullptr, c->U.p, c->U1.p, nullptr, c->S0u.p, c->S1u.p, nullptr);
+      CK(cudaGetLastError());
+      ++c->launches;
+    }
+  }
+  for (int k = 0; k < M; ++k) {
+    const int first = k == 0;
+    // stage 1: fine hb = ha + delta*d; interfaces acc1 += d   (:521-531)
+    if (k > 0 && !fuse_pred)
+      for (auto* c : cs) launch_predict(c, 1, k, M, c->H.p, c->U.p, 2);
+    exchange(cs, &C::H, &C::U);
+    for (auto* c : cs) {
+      const PredArgs pa = make_pred(c, 1, k, M, c->H.p, c->U.p, 2);
+      Op co[2] = {mk_op(OP_EULER, c->H1.p, c->H.p, delta),
+                  mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A1h.p, first)};
+      Op eo[2] = {mk_op(OP_EULER, c->U1.p, c->U.p, delta),
+                  mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A1u.p, first)};
+      launch_eval(c, plan_for(c, kMaskSub), c->H.p, c->U.p, co, eo,
+                  (k > 0 && fuse_pred) ? &pa : nullptr);
+    }
+    // stage 2: fine ha = 0.5 ha + 0.5 hb + (0.5 delta) d; acc2 += d, and on
+    // the last substep the interface correction (:532-541 order 2, :231-274)
+    if (!fuse_pred)
+      for (auto* c : cs) launch_predict(c, 2, k, M, c->H1.p, c->U1.p, 2);
+    exchange(cs, &C::H1, &C::U1);
+    for (auto* c : cs) {
+      const PredArgs pa = make_pred(c, 2, k, M, c->H1.p, c->U1.p, 2);
+      const double cr = 0.5 * delta;
+      Op co[2], eo[2];
+      co[0] = mk_op(OP_WCOMB, c->H.p, c->H.p, 0.5, c->H1.p, 0.5, cr);
+      eo[0] = mk_op(OP_WCOMB, c->U.p, c->U.p, 0.5, c->U1.p, 0.5, cr);
+      if (k < M - 1) {
+        co[1] = mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A2h.p, first);
+        eo[1] = mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A2u.p, first);
+      } else {
+        co[1] = mk_op(OP_ACC_CORR2, c->H.p, c->S0h.p, delta, nullptr, 0.5, 0, c->A2h.p, first,
+                      c->A1h.p);
+        eo[1] = mk_op(OP_ACC_CORR2, c->U.p, c->S0u.p, delta, nullptr, 0.5, 0, c->A2u.p, first,
+                      c->A1u.p);
+      }
+      launch_eval(c, plan_for(c, kMaskSub), c->H1.p, c->U1.p, co, eo, fuse_pred ? &pa : nullptr);
+    }
+  }
+  // Step 2 (:491-497): coarse h = 0.5 h_old + 0.5 h1 + (0.5 dt) dh, in place.
+  // H1/U1 halos are current: the last exchange refreshed them and only the
+  // state changed since.
+  for (auto* c : cs) {
+    const double cr = 0.5 * dt;
+    double *H = c->H.p, *U = c->U.p, *H1 = c->H1.p, *U1 = c->U1.p;
+    Op co[2] = {mk_op(OP_WCOMB, H, H, 0.5, H1, 0.5, cr), mk_op(OP_WCOMB, H, H, 0.5, H1, 0.5, cr)};
+    Op eo[2] = {mk_op(OP_WCOMB, U, U, 0.5, U1, 0.5, cr), mk_op(OP_WCOMB, U, U, 0.5, U1, 0.5, cr)};
+    launch_eval(c, plan_for(c, kMaskCoarseOnly), H1, U1, co, eo);
+  }
+}
+
+void tally_lts2(mswm_cuda_ctx* c, int M) {
+  tally(c, kMaskIfCoarse, 0);
+  tally(c, kMaskCoarseOnly, 1);
+  for (int k = 0; k < M; ++k) {
+    tally(c, kMaskSub, 0);
+    tally(c, kMaskSub, 1);
   }
 }
 
@@ -1991,6 +2088,7 @@ void enqueue_step(std::vector<mswm_cuda_ctx*>& cs, int scheme, double dt, int M)
   }
   switch (scheme) {
     case MSWM_LTS3: enqueue_lts3(cs, dt, M); break;
+    case MSWM_LTS2: enqueue_lts2(cs, dt, M); break;
     case MSWM_RK4: enqueue_rk4(cs, dt); break;
     case MSWM_SSPRK3: enqueue_ssprk(cs, 3, dt); break;
     case MSWM_SSPRK2: enqueue_ssprk(cs, 2, dt); break;
@@ -2001,6 +2099,7 @@ void enqueue_step(std::vector<mswm_cuda_ctx*>& cs, int scheme, double dt, int M)
 void tally_step(mswm_cuda_ctx* c, int scheme, int M) {
   switch (scheme) {
     case MSWM_LTS3: tally_lts3(c, M); break;
+    case MSWM_LTS2: tally_lts2(c, M); break;
     case MSWM_RK4:
       for (int s = 0; s < 4; ++s) tally(c, MSWM_MASK_ALL, s);
       break;
@@ -2017,11 +2116,9 @@ void tally_step(mswm_cuda_ctx* c, int scheme, int M) {
 void check_step_args(mswm_cuda_ctx* c, int scheme, double dt, int M, int64_t n_steps) {
   if (!(dt > 0.0)) throw Error(MSWM_E_CONFIG, "time step must be positive");
   if (n_steps < 0) throw Error(MSWM_E_USAGE, "negative step count");
-  if (scheme == MSWM_LTS3) {
+  if (scheme == MSWM_LTS3 || scheme == MSWM_LTS2) {
     if (M < 1) throw Error(MSWM_E_CONFIG, "substep count must be >= 1");
     if (!c->have_regions) throw Error(MSWM_E_CONFIG, "local time stepping requires a region map");
-  } else if (scheme == MSWM_LTS2) {
-    throw Error(MSWM_E_CONFIG, "LTS2 is not on the device path (north_star names LTS3/RK4)");
   } else if (scheme != MSWM_RK4 && scheme != MSWM_SSPRK3 && scheme != MSWM_SSPRK2) {
     throw Error(MSWM_E_CONFIG, "unknown scheme");
   }
@@ -2033,8 +2130,8 @@ mswm_cuda_ctx::Graph capture_step(std::vector<mswm_cuda_ctx*>& cs, cudaStream_t 
                                   double dt, int M, bool profile) {
   // Build every plan outside the capture (plan construction synchronises).
   for (auto* c : cs) {
-    if (scheme == MSWM_LTS3) {
-      plan_for(c, kMaskStep1);
+    if (scheme == MSWM_LTS3 || scheme == MSWM_LTS2) {
+      if (scheme == MSWM_LTS3) plan_for(c, kMaskStep1);
       plan_for(c, kMaskIfCoarse);
       plan_for(c, kMaskSub);
       plan_for(c, kMaskCoarseOnly);
@@ -2074,7 +2171,7 @@ mswm_cuda_ctx::Graph capture_step(std::vector<mswm_cuda_ctx*>& cs, cudaStream_t 
 }
 
 cudaGraphExec_t graph_for(mswm_cuda_ctx* c, int scheme, double dt, int M) {
-  const auto key = std::make_tuple(scheme, dt, scheme == MSWM_LTS3 ? M : 0, int(c->profiling));
+  const auto key = std::make_tuple(scheme, dt, (scheme == MSWM_LTS3 || scheme == MSWM_LTS2) ? M : 0, int(c->profiling));
   auto it = c->graphs.find(key);
   if (it != c->graphs.end()) {
     c->last_records = &it->second.records;
@@ -2693,7 +2790,7 @@ int mswm_cuda_group_step(mswm_cuda_group* g, int scheme, double dt, int M, int64
       CK(cudaStreamSynchronize(c->stream));  // uploads were issued on member streams
     }
     if (n_steps == 0) return int(MSWM_OK);
-    const auto key = std::make_tuple(scheme, dt, scheme == MSWM_LTS3 ? M : 0);
+    const auto key = std::make_tuple(scheme, dt, (scheme == MSWM_LTS3 || scheme == MSWM_LTS2) ? M : 0);
     auto it = g->graphs.find(key);
     if (it == g->graphs.end()) {
       auto gr = capture_step(g->members, g->stream, scheme, dt, M, false);

@@ -17,13 +17,13 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("n_ranks", [2, 3, 4])
-@pytest.mark.parametrize("scheme", [Scheme.LTS3, Scheme.RK4])
+@pytest.mark.parametrize("scheme", [Scheme.LTS3, Scheme.RK4, Scheme.LTS2])
 def test_group_ranks_bitwise_equal_oracle(n_ranks, scheme):
     wl = W.small_sphere(5, seed=23, cap_deg=25.0)
     o = Oracle(wl.mesh, wl.b, wl.f, wl.gravity)
     o.set_regions(wl.fine_mask, wl.width)
     cl, cs, el = o.labels()
-    dt = wl.dt if scheme == Scheme.LTS3 else wl.dt / wl.M
+    dt = wl.dt if scheme in (Scheme.LTS3, Scheme.LTS2) else wl.dt / wl.M
     n = 4
     h_ref, u_ref, _ = o.step(int(scheme), wl.h, wl.u, 0.0, dt, wl.M, n)
     lay = DistributedLayout(wl.mesh, cl, cs, el, n_ranks)

@@ -97,12 +97,32 @@ def test_sphere_lts3_and_rk4_bitwise(M):
     o = _oracle_for(wl)
     ctx = _ctx(wl.mesh, wl.b, wl.f, wl.gravity, wl.fine_mask)
     for scheme, n, dt in [(Scheme.LTS3, 6, wl.dt), (Scheme.RK4, 3, wl.dt / M),
-                          (Scheme.SSPRK3, 3, wl.dt / M)]:
+                          (Scheme.SSPRK3, 3, wl.dt / M), (Scheme.LTS2, 6, wl.dt),
+                          (Scheme.SSPRK2, 3, wl.dt / M)]:
         h_ref, u_ref, _ = o.step(int(scheme), wl.h, wl.u, 0.0, dt, M, n)
         ctx.upload(State(wl.h, wl.u, 0.0))
         ctx.advance(scheme, dt, M, n)
         st = ctx.download()
         assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref), scheme
+
+
+def test_c1_lts2_bitwise():
+    """Second-order LTS (Stepper::lts_step(2, ...)) on the device: coarse
+    steps and the ledger against the oracle (40 steps: at C1's LTS3 time step
+    the second-order scheme dries a vertex by step 100)."""
+    wl = W.config1(n_steps=40)
+    o = _oracle_for(wl)
+    h_ref, u_ref, t_ref = o.step(int(Scheme.LTS2), wl.h, wl.u, 0.0, wl.dt, wl.M, wl.n_steps)
+    ctx = _ctx(wl.mesh, wl.b, wl.f, wl.gravity, wl.fine_mask)
+    ctx.upload(State(wl.h, wl.u, 0.0))
+    ctx.advance(Scheme.LTS2, wl.dt, wl.M, wl.n_steps)
+    st = ctx.download()
+    assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
+    assert st.time == pytest.approx(t_ref)
+    c, e, s = o.ledger()
+    lg = ctx.ledger()
+    assert np.array_equal(lg.cell_evals, c) and np.array_equal(lg.edge_evals, e)
+    assert lg.steps_taken == s == wl.n_steps
 
 
 def test_c2_full_size_parity():
@@ -359,7 +379,7 @@ def test_dataflow_evaluation_bitwise(slab, lag, order, monkeypatch):
         o.eval(wl.h, wl.u, mask, dh2, du2)
         assert bits_equal(dh1, dh2) and bits_equal(du1, du2), hex(mask)
     for scheme, n, dt in [(Scheme.LTS3, 5, wl.dt), (Scheme.RK4, 3, wl.dt / wl.M),
-                          (Scheme.SSPRK3, 2, wl.dt / wl.M)]:
+                          (Scheme.SSPRK3, 2, wl.dt / wl.M), (Scheme.LTS2, 3, wl.dt)]:
         h_ref, u_ref, _ = o.step(int(scheme), wl.h, wl.u, 0.0, dt, wl.M, n)
         ctx.upload(State(wl.h, wl.u, 0.0))
         ctx.advance(scheme, dt, wl.M, n)
