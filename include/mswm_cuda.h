@@ -221,6 +221,21 @@ int mswm_cuda_kernels_per_step(mswm_cuda_ctx* ctx, int64_t* n);
  * to the reference). */
 int mswm_cuda_total_mass(mswm_cuda_ctx* ctx, double* mass);
 
+/* total_mass and total_energy (harness.cpp:99-123) of the device state from
+ * per-cell terms computed on the device in the reference's operation order.
+ * exact = 1: summed sequentially in ascending caller cell id (bitwise the
+ * reference); exact = 0: a fixed-shape device tree sum (deterministic, not
+ * the sequential rounding).  A rank context sums its owned cells. */
+int mswm_cuda_diagnostics(mswm_cuda_ctx* ctx, int exact, double* mass,
+                          double* energy);
+
+/* courant_numbers (integrators.cpp:632-659) of the device velocity: max of
+ * step |u_e| / d_e over fine + underline-fine edges (step dt / M) and over
+ * interface + coarse edges (step dt); without a region map every edge at dt
+ * and coarse = fine. */
+int mswm_cuda_courant(mswm_cuda_ctx* ctx, double dt, int M, double* fine,
+                      double* coarse);
+
 /* ---- multi-rank (one process per GPU, or an in-process group) ----------
  * A rank context holds one rank's piece of the mesh (owned elements plus a
  * two-hop halo, the reference's block plan, partition.cpp:307-403) in local

@@ -65,6 +65,9 @@ def ref() -> C.CDLL:
             "ref_mesh_rederive": (C.c_int, [vp] + E),
             "ref_mesh_validate": (C.c_int, [vp] + E),
             "ref_total_mass": (C.c_double, [vp, f64p]),
+            "ref_total_energy": (C.c_double, [vp, f64p, f64p, f64p, C.c_double]),
+            "ref_courant": (C.c_int, [vp, vp, f64p, C.c_double, C.c_int, f64p, C.c_char_p,
+                                      C.c_int]),
             "ref_regions_make": (vp, [vp, u8p, C.c_int] + E + [C.POINTER(C.c_int)]),
             "ref_regions_free": (None, [vp]),
             "ref_regions_labels": (None, [vp, u8p, u8p, u8p]),
@@ -171,6 +174,21 @@ class RefMesh:
     def total_mass(self, h):
         h = np.ascontiguousarray(h, np.float64)
         return ref().ref_total_mass(self.handle, _p(h, f64p))
+
+    def total_energy(self, h, u, b, gravity):
+        """harness.cpp:107-123 (the reference itself)."""
+        return ref().ref_total_energy(self.handle, _p(np.ascontiguousarray(h, np.float64), f64p),
+                                      _p(np.ascontiguousarray(u, np.float64), f64p),
+                                      _p(np.ascontiguousarray(b, np.float64), f64p), gravity)
+
+    def courant(self, regions, u, dt, M):
+        """integrators.cpp:632-659 (the reference itself); regions may be None."""
+        out = np.zeros(2)
+        buf = _err()
+        _check(ref().ref_courant(self.handle, regions.handle if regions is not None else None,
+                                 _p(np.ascontiguousarray(u, np.float64), f64p), dt, M,
+                                 _p(out, f64p), buf, ERRLEN), buf)
+        return float(out[0]), float(out[1])
 
 
 class RefRegions:
@@ -356,6 +374,9 @@ def orc() -> C.CDLL:
             "orc_step": (C.c_int, [vp, C.c_int, f64p, f64p, f64p, C.c_double, C.c_int,
                                    C.c_int64]),
             "orc_ledger": (None, [vp, i64p, i64p, i64p]),
+            "orc_total_mass": (C.c_double, [vp, f64p]),
+            "orc_total_energy": (C.c_double, [vp, f64p, f64p]),
+            "orc_courant": (C.c_int, [vp, f64p, C.c_double, C.c_int, f64p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -435,6 +456,19 @@ class Oracle:
         self._rc(orc().orc_step(self.handle, scheme, _p(h, f64p), _p(u, f64p), C.byref(t), dt, M,
                                 n_steps))
         return h, u, t.value
+
+    def total_mass(self, h):
+        return orc().orc_total_mass(self.handle, _p(np.ascontiguousarray(h, np.float64), f64p))
+
+    def total_energy(self, h, u):
+        return orc().orc_total_energy(self.handle, _p(np.ascontiguousarray(h, np.float64), f64p),
+                                      _p(np.ascontiguousarray(u, np.float64), f64p))
+
+    def courant(self, u, dt, M):
+        out = np.zeros(2)
+        self._rc(orc().orc_courant(self.handle, _p(np.ascontiguousarray(u, np.float64), f64p), dt,
+                                   M, _p(out, f64p)))
+        return float(out[0]), float(out[1])
 
     def ledger(self):
         c = np.zeros(16, np.int64)

@@ -244,6 +244,29 @@ double ref_total_mass(void* mp, const double* h) {
   return total_mass(*m, f);
 }
 
+double ref_total_energy(void* mp, const double* h, const double* u, const double* b, double g) {
+  auto* m = static_cast<VoronoiMesh*>(mp);
+  State st(m->n_cells, m->n_edges);
+  std::copy(h, h + m->n_cells, st.h.data.begin());
+  std::copy(u, u + m->n_edges, st.u.data.begin());
+  CellField bf(m->n_cells);
+  std::copy(b, b + m->n_cells, bf.data.begin());
+  return total_energy(*m, st, bf, g);
+}
+
+// rp may be null (no region map)
+int ref_courant(void* mp, void* rp, const double* u, double dt, int M, double* out, char* err,
+                int errlen) {
+  auto* m = static_cast<VoronoiMesh*>(mp);
+  return guarded(err, errlen, nullptr, [&] {
+    EdgeField uf(m->n_edges);
+    std::copy(u, u + m->n_edges, uf.data.begin());
+    const CourantNumbers c = courant_numbers(*m, static_cast<const RegionMap*>(rp), uf, dt, M);
+    out[0] = c.fine;
+    out[1] = c.coarse;
+  });
+}
+
 // ---- regions ----------------------------------------------------------------
 
 void* ref_regions_make(void* mp, const uint8_t* fine_mask, int width, char* err, int errlen,

@@ -161,6 +161,8 @@ def cuda() -> C.CDLL:
             "mswm_cuda_eval_profile": (C.c_int, [vp, C.POINTER(C.c_float), i64p, i64p, C.c_int,
                                                  C.POINTER(C.c_int)]),
             "mswm_cuda_total_mass": (C.c_int, [vp, f64p]),
+            "mswm_cuda_diagnostics": (C.c_int, [vp, C.c_int, f64p, f64p]),
+            "mswm_cuda_courant": (C.c_int, [vp, C.c_double, C.c_int, f64p, f64p]),
             "mswm_cuda_kernels_per_step": (C.c_int, [vp, i64p]),
             "mswm_cuda_layout_info": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
             "mswm_cuda_flow_info": (C.c_int, [vp] + [C.POINTER(C.c_int)] * 4),

@@ -369,6 +369,25 @@ class CudaContext:
         self._check(self.lib.mswm_cuda_total_mass(self.handle, C.byref(out)))
         return out.value
 
+    def diagnostics(self, exact: bool = True) -> tuple[float, float]:
+        """(total_mass, total_energy) of the device state (harness.cpp:99-123);
+        exact: the reference's sequential summation order, else a
+        deterministic device tree sum."""
+        m, e = C.c_double(0.0), C.c_double(0.0)
+        self._check(self.lib.mswm_cuda_diagnostics(self.handle, int(exact), C.byref(m),
+                                                   C.byref(e)))
+        return m.value, e.value
+
+    def total_energy(self, exact: bool = True) -> float:
+        return self.diagnostics(exact)[1]
+
+    def courant(self, dt: float, substeps: int = 1) -> tuple[float, float]:
+        """courant_numbers (integrators.cpp:632-659): (fine, coarse)."""
+        f, c = C.c_double(0.0), C.c_double(0.0)
+        self._check(self.lib.mswm_cuda_courant(self.handle, float(dt), int(substeps), C.byref(f),
+                                               C.byref(c)))
+        return f.value, c.value
+
 
 def _p(a, t):
     return a.ctypes.data_as(t)

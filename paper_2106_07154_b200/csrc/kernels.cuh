@@ -757,6 +757,87 @@ __global__ void k_union_key(int32_t n, const uint8_t* __restrict__ a, const uint
   if (i < n) key[i] = (a[i] | b[i]) ? 0 : 0xFF;
 }
 
+// ---------------------------------------------------------------------------
+// Diagnostics (harness.cpp:99-123, integrators.cpp:632-659).
+
+// Per-cell terms of total_mass and total_energy in the reference's per-cell
+// operation order; cells with ckey 0xFF (not owned by this rank) give 0.
+__global__ void k_cell_diag(DevMesh M, const double* __restrict__ h, const double* __restrict__ u,
+                            const uint8_t* __restrict__ ckey, double* __restrict__ mass_t,
+                            double* __restrict__ energy_t) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M.nC) return;
+  if (ckey && ckey[i] > 5) {
+    mass_t[i] = 0.0;
+    energy_t[i] = 0.0;
+    return;
+  }
+  const int deg = M.c_deg[i];
+  double k = 0.0;
+  for (int j = 0; j < deg; ++j) {
+    const int32_t e = M.c_edge[j * M.nC + i];
+    const double ue = u[e];
+    k += M.e_ld[e] * ue * ue;  // ((l d) u) u
+  }
+  const double A = M.c_area[i];
+  k /= 4.0 * A;
+  const double hi = h[i];
+  mass_t[i] = A * hi;
+  energy_t[i] = A * (hi * k + 0.5 * M.g * hi * (hi + 2.0 * M.b[i]));
+}
+
+// Fixed-shape two-level sum (deterministic for a given n, not the
+// sequential rounding): block b sums [b*chunk, (b+1)*chunk) as a strided
+// per-thread sum and a shared-memory tree; then one block sums the partials.
+__global__ void __launch_bounds__(kBlock) k_sum_chunks(int32_t n, int32_t chunk,
+                                                       const double* __restrict__ x,
+                                                       double* __restrict__ partial) {
+  __shared__ double sm[kBlock];
+  const int32_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+  double acc = 0.0;
+  for (int32_t i = lo + threadIdx.x; i < hi; i += kBlock) acc += x[i];
+  sm[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = kBlock / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sm[threadIdx.x] += sm[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sm[0];
+}
+
+// Courant numbers: max of step |u_e| / d_e over fine (edge groups 6-7, step
+// dt/M) and coarse (8-10, step dt) edges; without regions every edge at dt
+// into slot 0.  Non-negative doubles order like their bit patterns, so the
+// maxima are exact atomicMax results; NaNs never win (c > target is false).
+__global__ void __launch_bounds__(kBlock) k_courant(DevMesh M, const double* __restrict__ u,
+                                                    const uint8_t* __restrict__ ekey, double dt,
+                                                    double dt_fine,
+                                                    unsigned long long* __restrict__ out) {
+  const int32_t e = blockIdx.x * kBlock + threadIdx.x;
+  double cf = 0.0, cc = 0.0;
+  if (e < M.nE) {
+    const int g = ekey ? ekey[e] : 0;
+    if (g <= 4) {
+      const bool fine = ekey && g <= 1;
+      const double c = (ekey ? (fine ? dt_fine : dt) : dt) * fabs(u[e]) / M.e_dual[e];
+      if (c > 0.0) {
+        if (fine || !ekey)
+          cf = c;
+        else
+          cc = c;
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    cf = fmax(cf, __shfl_xor_sync(0xffffffffu, cf, o));
+    cc = fmax(cc, __shfl_xor_sync(0xffffffffu, cc, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (cf > 0.0) atomicMax(out, __double_as_longlong(cf));
+    if (cc > 0.0) atomicMax(out + 1, __double_as_longlong(cc));
+  }
+}
+
 // pack a 0/1 byte array into a bitmask
 __global__ void k_pack_bits(int32_t n, const uint8_t* __restrict__ a, uint32_t* __restrict__ bits) {
   const int32_t w = blockIdx.x * blockDim.x + threadIdx.x;

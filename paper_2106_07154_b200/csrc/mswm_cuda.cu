@@ -2596,15 +2596,85 @@ int mswm_cuda_kernels_per_step(mswm_cuda_ctx* c, int64_t* n) {
   return MSWM_OK;
 }
 
+// Per-cell diagnostics terms of the device state; exact: sequential sums in
+// ascending caller cell id on the host (the reference's order), else the
+// fixed-shape device sum.
+void diagnostics(mswm_cuda_ctx* c, bool exact, double* mass, double* energy) {
+  cudaStream_t s = c->stream;
+  DArr<double> mt, et;
+  mt.alloc(c->nC);
+  et.alloc(c->nC);
+  const uint8_t* ckey = (c->have_regions && c->n_ranks > 1) ? c->ckey.p : nullptr;
+  k_cell_diag<<<nblk(c->nC), kBlock, 0, s>>>(c->dev(), c->H.p, c->U.p, ckey, mt.p, et.p);
+  CK(cudaGetLastError());
+  if (exact) {
+    std::vector<double> hm(c->nC), he(c->nC);
+    CK(cudaMemcpyAsync(hm.data(), mt.p, size_t(c->nC) * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(he.data(), et.p, size_t(c->nC) * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    double m = 0.0, e = 0.0;
+    for (int32_t i = 0; i < c->nC; ++i) {  // harness.cpp:103, :110-122: ascending id
+      const int32_t k = c->identity ? i : c->c_old2new[i];
+      m += hm[k];
+      e += he[k];
+    }
+    if (mass) *mass = m;
+    if (energy) *energy = e;
+    return;
+  }
+  const int32_t chunk = 8192;
+  const int32_t nb = (c->nC + chunk - 1) / chunk;
+  DArr<double> part, tot;
+  part.alloc(2 * size_t(nb));
+  tot.alloc(2);
+  k_sum_chunks<<<nb, kBlock, 0, s>>>(c->nC, chunk, mt.p, part.p);
+  k_sum_chunks<<<nb, kBlock, 0, s>>>(c->nC, chunk, et.p, part.p + nb);
+  k_sum_chunks<<<1, kBlock, 0, s>>>(nb, nb, part.p, tot.p);
+  k_sum_chunks<<<1, kBlock, 0, s>>>(nb, nb, part.p + nb, tot.p + 1);
+  CK(cudaGetLastError());
+  double r[2];
+  CK(cudaMemcpyAsync(r, tot.p, 16, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (mass) *mass = r[0];
+  if (energy) *energy = r[1];
+}
+
 int mswm_cuda_total_mass(mswm_cuda_ctx* c, double* mass) {
   return guard(c, [&] {
     check_ctx(c);
     if (!mass) throw Error(MSWM_E_USAGE, "null output");
-    std::vector<double> h(c->nC);
-    download_field(c, c->H, h.data(), c->c_new2old, c->nC);
-    double m = 0.0;  // harness.cpp:99-105, ascending original id
-    for (int32_t i = 0; i < c->nC; ++i) m += c->h_cell_area[i] * h[i];
-    *mass = m;
+    diagnostics(c, true, mass, nullptr);
+    return int(MSWM_OK);
+  });
+}
+
+int mswm_cuda_diagnostics(mswm_cuda_ctx* c, int exact, double* mass, double* energy) {
+  return guard(c, [&] {
+    check_ctx(c);
+    if (!c->have_fields) throw Error(MSWM_E_USAGE, "set_fields must be called first");
+    diagnostics(c, exact != 0, mass, energy);
+    return int(MSWM_OK);
+  });
+}
+
+int mswm_cuda_courant(mswm_cuda_ctx* c, double dt, int M, double* fine, double* coarse) {
+  return guard(c, [&] {
+    check_ctx(c);
+    if (M < 1) throw Error(MSWM_E_USAGE, "substep count must be >= 1");  // integrators.cpp:636
+    cudaStream_t s = c->stream;
+    DArr<unsigned long long> out;
+    out.alloc(2);
+    out.zero(s);
+    const uint8_t* ekey = c->have_regions ? c->ekey.p : nullptr;
+    k_courant<<<nblk(c->nE), kBlock, 0, s>>>(c->dev(), c->U.p, ekey, dt, dt / M, out.p);
+    CK(cudaGetLastError());
+    unsigned long long r[2];
+    CK(cudaMemcpyAsync(r, out.p, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    double v[2];
+    std::memcpy(v, r, 16);
+    if (fine) *fine = v[0];
+    if (coarse) *coarse = ekey ? v[1] : v[0];
     return int(MSWM_OK);
   });
 }

@@ -409,3 +409,27 @@ def test_dataflow_disabled_matches(monkeypatch):
     ctx.advance(Scheme.LTS3, wl.dt, wl.M, 3)
     st = ctx.download()
     assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
+
+
+@pytest.mark.parametrize("order", ["hilbert", "input"])
+def test_device_diagnostics(order):
+    """total_mass / total_energy (harness.cpp:99-123) and courant_numbers
+    (integrators.cpp:632-659) of the device state: exact mode and Courant
+    numbers bitwise the oracle, the device tree sum within 1e-13."""
+    wl = W.small_sphere(5, seed=41, cap_deg=25.0)
+    o = _oracle_for(wl)
+    h, u, _ = o.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, wl.M, 3)
+    ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order)
+    ctx.upload(State(h, u, 0.0))
+    o_nomap = Oracle(wl.mesh, wl.b, wl.f, wl.gravity)
+    assert ctx.courant(wl.dt, 4) == o_nomap.courant(u, wl.dt, 4)
+    ctx.make_regions(wl.fine_mask, wl.width)
+    m, e = ctx.diagnostics(exact=True)
+    assert m == o.total_mass(h) and e == o.total_energy(h, u)
+    assert ctx.total_mass() == m
+    mf, ef = ctx.diagnostics(exact=False)
+    assert abs(mf - m) <= 1e-13 * abs(m) and abs(ef - e) <= 1e-13 * abs(e)
+    for M in (1, 4, 7):
+        assert ctx.courant(wl.dt, M) == o.courant(u, wl.dt, M)
+    with pytest.raises(UsageError):
+        ctx.courant(wl.dt, 0)

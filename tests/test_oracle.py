@@ -130,3 +130,20 @@ def test_restatement_dry_vertex(ref_lib):
         ev.eval(h, u, kMaskAll, np.zeros(mesh.n_cells), np.zeros(mesh.n_edges))
     assert e1.value.vertex == e2.value.vertex
     assert 4 in mesh.vertex_cells[e1.value.vertex]
+
+
+@pytest.mark.parametrize("make", [lambda: W.config1(n_steps=4), lambda: W.small_sphere(4)])
+def test_diagnostics_match_reference(ref_lib, make):
+    """total_mass / total_energy (harness.cpp:99-123) and courant_numbers
+    (integrators.cpp:632-659), with and without a region map."""
+    wl = make()
+    rm, rr, ev, o = _both(wl)
+    h, u, _ = o.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, wl.M, 2)
+    assert o.total_mass(h) == rm.total_mass(h)
+    assert o.total_energy(h, u) == rm.total_energy(h, u, wl.b, wl.gravity)
+    for M in (1, 4):
+        assert o.courant(u, wl.dt, M) == rm.courant(rr, u, wl.dt, M)
+    o2 = Oracle(wl.mesh, wl.b, wl.f, wl.gravity)
+    assert o2.courant(u, wl.dt, 3) == rm.courant(None, u, wl.dt, 3)
+    f, c = o2.courant(u, wl.dt, 3)
+    assert f == c > 0
