@@ -188,7 +188,9 @@ void* mswm_cuda_stream(mswm_cuda_ctx* ctx);
 
 /* Per-evaluation device timing of the most recent step (profiling aid for
  * the roofline).  Enable before mswm_cuda_step; the captured step then
- * brackets every tendency evaluation with CUDA events.  After a step,
+ * brackets every tendency evaluation (enable = 1), or only the first one
+ * whose outputs cover at least half the mesh (enable = 2: two event nodes
+ * per step instead of two per evaluation), with CUDA events.  After a step,
  * mswm_cuda_eval_profile fills up to `cap` entries: eval_ms[k] the device
  * time of evaluation k of the last replayed step, out_cells/out_edges its
  * output set sizes; returns the count in *n. */

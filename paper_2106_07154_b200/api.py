@@ -334,8 +334,10 @@ class CudaContext:
     def stream_ptr(self) -> int:
         return self.lib.mswm_cuda_stream(self.handle) or 0
 
-    def set_profiling(self, on: bool):
-        self._check(self.lib.mswm_cuda_set_profiling(self.handle, 1 if on else 0))
+    def set_profiling(self, on):
+        """True/1: time every evaluation of the captured step; 2: only the first
+        evaluation covering half the mesh (cheaper inside timed steps)."""
+        self._check(self.lib.mswm_cuda_set_profiling(self.handle, int(on)))
 
     def eval_profile(self, cap: int = 4096):
         ms = (C.c_float * cap)()

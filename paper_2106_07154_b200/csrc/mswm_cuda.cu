@@ -288,7 +288,7 @@ struct mswm_cuda_ctx {
     int64_t kernels = 0;  // kernel nodes per step
   };
   std::map<std::tuple<int, double, int, int>, Graph> graphs;
-  bool profiling = false;
+  int profiling = 0;  // 1: every evaluation bracketed by events, 2: only the first large one
   std::vector<EvalRecord>* capture_records = nullptr;  // set while capturing
   int64_t launches = 0;                               // kernels enqueued (capture counting)
   int64_t last_kernels_per_step = 0;
@@ -1419,7 +1419,9 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
   }
   const DevMesh M = c->dev();
   EvalRecord* rec = nullptr;
-  if (c->capture_records) {
+  if (c->capture_records &&
+      (c->profiling != 2 || (c->capture_records->empty() &&
+                             2 * (int64_t(p.nc) + p.ne) >= int64_t(c->nC) + c->nE))) {
     EvalRecord r;
     CK(cudaEventCreate(&r.start));
     CK(cudaEventCreate(&r.stop));
@@ -2548,7 +2550,8 @@ void* mswm_cuda_stream(mswm_cuda_ctx* c) { return c ? (void*)c->stream : nullptr
 int mswm_cuda_set_profiling(mswm_cuda_ctx* c, int enable) {
   return guard(c, [&] {
     check_ctx(c);
-    c->profiling = enable != 0;
+    if (enable < 0 || enable > 2) throw Error(MSWM_E_USAGE, "profiling level must be 0, 1 or 2");
+    c->profiling = enable;
     return int(MSWM_OK);
   });
 }

@@ -39,7 +39,8 @@ def main():
                               fine_mask=wl.fine_mask, interface_width=wl.width)
             ctx.make_regions(wl.fine_mask, wl.width)
             ctx.upload(State(wl.h, wl.u, 0.0))
-            ctx.set_profiling(True)
+            prof = os.environ.get("SWEEP_PROF", "1") == "1"
+            ctx.set_profiling(prof)
             stream = torch.cuda.ExternalStream(ctx.stream_ptr())
             ctx.advance(Scheme.LTS3, wl.dt, wl.M, 3)
             torch.cuda.synchronize()
@@ -51,7 +52,7 @@ def main():
             torch.cuda.synchronize()
             ctx.sync()
             ms = e0.elapsed_time(e1) / steps
-            evms, evnc, evne = ctx.eval_profile()
+            evms, evnc, evne = ctx.eval_profile() if prof else ([0.0] * 3, [0], [0])
             k = int(np.argmax(evne))
             print(f"{setting:40s} ms/step {ms:8.3f}  big-eval ms {evms[k]:.3f}  "
                   f"evals {' '.join(f'{x:.3f}' for x in evms[:3])}  kernels {ctx.kernels_per_step()}"

@@ -433,3 +433,26 @@ def test_device_diagnostics(order):
         assert ctx.courant(wl.dt, M) == o.courant(u, wl.dt, M)
     with pytest.raises(UsageError):
         ctx.courant(wl.dt, 0)
+
+
+def test_eval_profile_levels():
+    """set_profiling(1) brackets all 3M+3 evaluations of an LTS3 step with
+    events, set_profiling(2) only the first one covering half the mesh (the
+    bench's roofline kernel); profiling never changes the results."""
+    wl = W.small_sphere(5, seed=43, cap_deg=25.0)
+    ref = None
+    for level, n_evals in [(0, 0), (1, 3 * wl.M + 3), (2, 1)]:
+        ctx = _ctx(wl.mesh, wl.b, wl.f, wl.gravity, wl.fine_mask)
+        ctx.set_profiling(level)
+        ctx.upload(State(wl.h, wl.u, 0.0))
+        ctx.advance(Scheme.LTS3, wl.dt, wl.M, 2)
+        ms, nc, ne = ctx.eval_profile()
+        assert len(ms) == n_evals and np.all(ms > 0)
+        if level == 2:
+            assert 2 * (nc[0] + ne[0]) >= wl.mesh.n_cells + wl.mesh.n_edges
+        st = ctx.download()
+        if ref is None:
+            ref = st
+        assert bits_equal(st.h, ref.h) and bits_equal(st.u, ref.u)
+    with pytest.raises(UsageError):
+        ctx.set_profiling(3)
