@@ -206,7 +206,9 @@ __global__ void MSWM_KA_BOUNDS k_vertex_cell(DevMesh M, const double* __restrict
                                              double* __restrict__ pv, double* __restrict__ K,
                                              int32_t* __restrict__ dry,
                                              const uint32_t* __restrict__ vmask) {
-  item_vertex_cell(M, h, u, vs, ks, pv, K, dry, vmask, blockIdx.x * kBlock + threadIdx.x);
+  const int32_t n = vs.n() + ks.n();
+  for (int32_t t = blockIdx.x * kBlock + threadIdx.x; t < n; t += gridDim.x * kBlock)
+    item_vertex_cell(M, h, u, vs, ks, pv, K, dry, vmask, t);
 }
 
 // Phase B: thickness flux F_e (operators.cpp:61-62) and q~_e (:88-89) on the
@@ -240,7 +242,9 @@ __global__ void __launch_bounds__(kBlock) k_edge_fq(DevMesh M, const double* __r
                                                    const double* __restrict__ u,
                                                    const double* __restrict__ pv, Span es,
                                                    double2* __restrict__ FQ) {
-  item_edge_fq(M, h, u, pv, es, FQ, blockIdx.x * kBlock + threadIdx.x);
+  const int32_t n = es.n();
+  for (int32_t t = blockIdx.x * kBlock + threadIdx.x; t < n; t += gridDim.x * kBlock)
+    item_edge_fq(M, h, u, pv, es, FQ, t);
 }
 
 // Phase C: the output tendencies -- dh on out cells (operators.cpp:91-99),
@@ -351,7 +355,9 @@ __device__ __forceinline__ void item_out(const DevMesh& M, const double* __restr
 __global__ void MSWM_KOUT_BOUNDS k_out(DevMesh M, const double* __restrict__ h,
                                      const double* __restrict__ K,
                                      const double2* __restrict__ FQ, OutArgs a) {
-  item_out(M, h, K, FQ, a, blockIdx.x * kBlock + threadIdx.x);
+  const int32_t n = a.cs.n() + a.es.n();
+  for (int32_t t = blockIdx.x * kBlock + threadIdx.x; t < n; t += gridDim.x * kBlock)
+    item_out(M, h, K, FQ, a, t);
 }
 
 // ---------------------------------------------------------------------------
