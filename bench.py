@@ -288,6 +288,9 @@ def run_ours(args, ws, rank, local):
         uid = [RankContext.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         rc.init_nccl(uid[0])
+        # exchange only what each evaluation reads (setup-time position swap)
+        from paper_2106_07154_b200.api import LTS3_MASKS, kMaskAll
+        rc.restrict_halos(LTS3_MASKS + [kMaskAll])
         rc.upload(wl.h, wl.u)
         ctx = rc.ctx
         io_mesh = rc.local_mesh

@@ -261,6 +261,23 @@ int mswm_cuda_set_halo(mswm_cuda_ctx* ctx, int rank, int n_ranks, int n_peers,
                        const int32_t* peers, const int64_t* counts,
                        const int32_t* ids);
 
+/* Halo restriction per mask: the halo entries the
+ * evaluation with `mask` reads, as positions within each peer's receive list
+ * of mswm_cuda_set_halo (cells then edges), peers in set_halo order:
+ * counts[j] entries for peer j, concatenated in pos (NULL: counts only).
+ * Builds the mask's closure (as mswm_cuda_eval would). */
+int mswm_cuda_halo_needs(mswm_cuda_ctx* ctx, unsigned mask, int64_t* counts,
+                         int32_t* pos);
+
+/* Install the restriction for `mask`: send_pos = positions within each
+ * peer's send list that the peer needs (that peer's halo_needs for this
+ * rank), recv_pos = this rank's own halo_needs.  The step graph then
+ * exchanges only these entries before evaluations with `mask`, plus one
+ * coarse-mask refresh before the coarse-only stage. */
+int mswm_cuda_set_halo_mask(mswm_cuda_ctx* ctx, unsigned mask,
+                            const int64_t* send_counts, const int32_t* send_pos,
+                            const int64_t* recv_counts, const int32_t* recv_pos);
+
 /* NCCL transport (one process per GPU): rank 0 creates a 128-byte unique id,
  * the caller broadcasts it, every rank calls mswm_cuda_comm_init.  The
  * exchange is NCCL point-to-point on the context's stream, captured in the

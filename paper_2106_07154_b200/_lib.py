@@ -163,6 +163,8 @@ def cuda() -> C.CDLL:
             "mswm_cuda_total_mass": (C.c_int, [vp, f64p]),
             "mswm_cuda_diagnostics": (C.c_int, [vp, C.c_int, f64p, f64p]),
             "mswm_cuda_courant": (C.c_int, [vp, C.c_double, C.c_int, f64p, f64p]),
+            "mswm_cuda_halo_needs": (C.c_int, [vp, C.c_uint, i64p, i32p]),
+            "mswm_cuda_set_halo_mask": (C.c_int, [vp, C.c_uint, i64p, i32p, i64p, i32p]),
             "mswm_cuda_kernels_per_step": (C.c_int, [vp, i64p]),
             "mswm_cuda_layout_info": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
             "mswm_cuda_flow_info": (C.c_int, [vp] + [C.POINTER(C.c_int)] * 4),

@@ -756,6 +756,46 @@ __global__ void k_mark_closure(DevMesh M, const int32_t* __restrict__ c_vert,
   }
 }
 
+// Elements whose h (cells) or u (edges) one masked evaluation reads
+// (operators.cpp:61-86 over the closure lists): cells and edges of the PV
+// vertices, ring edges of the K cells, flux edges and their cells, and the
+// cells of the output edges (psi).  Outputs' own values are the rank's.
+__global__ void k_mark_reads(DevMesh M, const int32_t* __restrict__ vl, int32_t nv,
+                             const int32_t* __restrict__ kl, int32_t nk,
+                             const int32_t* __restrict__ fl, int32_t nf,
+                             const int32_t* __restrict__ ol, int32_t no,
+                             uint8_t* __restrict__ cread, uint8_t* __restrict__ eread) {
+  int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nv) {
+    const int32_t v = vl[t];
+    for (int k = 0; k < 3; ++k) {
+      cread[M.v_cell[k * M.nV + v]] = 1;
+      eread[M.v_edge[k * M.nV + v]] = 1;
+    }
+    return;
+  }
+  t -= nv;
+  if (t < nk) {
+    const int32_t i = kl[t];
+    for (int j = 0; j < M.c_deg[i]; ++j) eread[M.c_edge[j * M.nC + i]] = 1;
+    return;
+  }
+  t -= nk;
+  if (t < nf) {
+    const int32_t e = fl[t];
+    eread[e] = 1;
+    cread[M.e_cells[e].x] = 1;
+    cread[M.e_cells[e].y] = 1;
+    return;
+  }
+  t -= nf;
+  if (t < no) {
+    const int32_t e = ol[t];
+    cread[M.e_cells[e].x] = 1;
+    cread[M.e_cells[e].y] = 1;
+  }
+}
+
 // key = 0 where either mark is set, 0xFF elsewhere (closure-union key)
 __global__ void k_union_key(int32_t n, const uint8_t* __restrict__ a, const uint8_t* __restrict__ b,
                             uint8_t* __restrict__ key) {

@@ -143,6 +143,7 @@ struct MaskPlan {
 struct Halo {
   std::vector<int> peer;
   std::vector<int64_t> soff, scnt, roff, rcnt;
+  std::vector<int32_t> h_scode, h_rcode;  // host copies (per-mask subsets)
   DArr<int32_t> scode, rcode;
   DArr<double> sbuf, rbuf;
   int64_t ns = 0, nr = 0;
@@ -209,6 +210,9 @@ struct mswm_cuda_ctx {
   // multi-rank: this context is rank `rank` of `n_ranks`, owning part of the mesh
   int rank = 0, n_ranks = 1;
   Halo halo;
+  // per-mask restrictions of `halo` to what that evaluation reads (SURVEY
+  // §8(e)); masks without one exchange the full halo
+  std::map<unsigned, Halo> halo_mask;
   ncclComm_t nccl_comm = nullptr;
   std::string last_error;
   int32_t nC = 0, nE = 0, nV = 0, deg_max = 0, sten_max = 0;
@@ -1773,12 +1777,23 @@ PredArgs make_pred(mswm_cuda_ctx* c, int stage, int k, int M, double* hdst, doub
 
 using ArrSel = DArr<double> mswm_cuda_ctx::*;
 
-void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us) {
+Halo& halo_for(mswm_cuda_ctx* c, unsigned mask) {
+  auto it = c->halo_mask.find(mask);
+  return it == c->halo_mask.end() ? c->halo : it->second;
+}
+
+bool restricted(const std::vector<mswm_cuda_ctx*>& cs) {
+  for (auto* c : cs)
+    if (!c->halo_mask.empty()) return true;
+  return false;
+}
+
+void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us, unsigned mask) {
   bool any = false;
   for (auto* c : cs) any |= c->halo.active();
   if (!any) return;
   for (auto* c : cs) {
-    Halo& x = c->halo;
+    Halo& x = halo_for(c, mask);
     if (x.ns > 0) {
       k_pack<<<nblk(x.ns), kBlock, 0, c->ls>>>(x.ns, x.scode.p, (c->*hs).p, (c->*us).p, x.sbuf.p);
       CK(cudaGetLastError());
@@ -1787,7 +1802,7 @@ void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us) {
   }
   if (cs.size() == 1) {
     mswm_cuda_ctx* c = cs[0];
-    Halo& x = c->halo;
+    Halo& x = halo_for(c, mask);
     if (!c->nccl_comm) throw Error(MSWM_E_USAGE, "halo set but no communicator (mswm_cuda_comm_init)");
     nccl_check(nccl().GroupStart());
     for (size_t j = 0; j < x.peer.size(); ++j) {
@@ -1802,11 +1817,11 @@ void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us) {
   } else {
     // in-process group: member index == rank
     for (auto* c : cs) {
-      Halo& x = c->halo;
+      Halo& x = halo_for(c, mask);
       for (size_t j = 0; j < x.peer.size(); ++j) {
         if (!x.rcnt[j]) continue;
         mswm_cuda_ctx* src = cs[x.peer[j]];
-        const Halo& y = src->halo;
+        const Halo& y = halo_for(src, mask);
         size_t k = 0;
         while (k < y.peer.size() && y.peer[k] != c->rank) ++k;
         if (k == y.peer.size() || y.scnt[k] != x.rcnt[j])
@@ -1818,7 +1833,7 @@ void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us) {
     }
   }
   for (auto* c : cs) {
-    Halo& x = c->halo;
+    Halo& x = halo_for(c, mask);
     if (x.nr > 0) {
       k_unpack<<<nblk(x.nr), kBlock, 0, c->ls>>>(x.nr, x.rcode.p, x.rbuf.p, (c->*hs).p, (c->*us).p);
       CK(cudaGetLastError());
@@ -1836,7 +1851,7 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
   const double third = 1.0 / 3.0, two3 = 2.0 / 3.0;
   using C = mswm_cuda_ctx;
   // Step 1 (:483-487): h1 = h_old + dt*dh on UF1 u UF2 u I1 u I2 u C.
-  exchange(cs, &C::H, &C::U);
+  exchange(cs, &C::H, &C::U, kMaskStep1);
   for (auto* c : cs) {
     double *H = c->H.p, *U = c->U.p, *H1 = c->H1.p, *U1 = c->U1.p;
     Op co[2] = {mk_op(OP_EULER, H1, H, dt), mk_op(OP_EULER, H1, H, dt)};
@@ -1844,7 +1859,7 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
     launch_eval(c, plan_for(c, kMaskStep1), H, U, co, eo);
   }
   // Step 2 (:491-500): h2 = 0.75 h_old + 0.25 h1 + (0.25 dt) dh on I u C.
-  exchange(cs, &C::H1, &C::U1);
+  exchange(cs, &C::H1, &C::U1, kMaskIfCoarse);
   for (auto* c : cs) {
     double *H = c->H.p, *U = c->U.p, *H1 = c->H1.p, *U1 = c->U1.p, *H2 = c->H2.p, *U2 = c->U2.p;
     const double cr = 0.25 * dt;
@@ -1874,7 +1889,7 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
     // has to propagate them first (multi-rank)
     if (k > 0 && !fuse_pred)
       for (auto* c : cs) launch_predict(c, 1, k, M, c->H.p, c->U.p);
-    exchange(cs, &C::H, &C::U);
+    exchange(cs, &C::H, &C::U, kMaskSub);
     for (auto* c : cs) {
       const PredArgs pa = make_pred(c, 1, k, M, c->H.p, c->U.p);
       Op co[2] = {mk_op(OP_EULER, c->H1.p, c->H.p, delta),
@@ -1887,7 +1902,7 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
     // stage 2: fine hc = 0.75 ha + 0.25 hb + (0.25 delta) d; acc2 += d   (:532-541)
     if (!fuse_pred)
       for (auto* c : cs) launch_predict(c, 2, k, M, c->H1.p, c->U1.p);
-    exchange(cs, &C::H1, &C::U1);
+    exchange(cs, &C::H1, &C::U1, kMaskSub);
     for (auto* c : cs) {
       const PredArgs pa = make_pred(c, 2, k, M, c->H1.p, c->U1.p);
       const double cr = 0.25 * delta;
@@ -1901,7 +1916,7 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
     // the last substep the interface correction (:542-553, :231-274).
     if (!fuse_pred)
       for (auto* c : cs) launch_predict(c, 3, k, M, c->H2.p, c->U2.p);
-    exchange(cs, &C::H2, &C::U2);
+    exchange(cs, &C::H2, &C::U2, kMaskSub);
     for (auto* c : cs) {
       const PredArgs pa = make_pred(c, 3, k, M, c->H2.p, c->U2.p);
       const double cr = two3 * delta;
@@ -1921,8 +1936,10 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
     }
   }
   // Step 4 (:557-563): coarse h = 1/3 h_old + 2/3 h2 + (2/3 dt) dh, in place.
-  // H2/U2 halos are current: the last exchange refreshed them and only
-  // fine/I1 entries (never read here) changed since.
+  // With full halos the H2/U2 copies are current (the last exchange
+  // refreshed them; only fine/I1 entries, never read here, changed since);
+  // restricted halos refreshed only the substep's read set.
+  if (restricted(cs)) exchange(cs, &C::H2, &C::U2, kMaskCoarseOnly);
   for (auto* c : cs) {
     const double cr = two3 * dt;
     double *H = c->H.p, *U = c->U.p, *H2 = c->H2.p, *U2 = c->U2.p;
@@ -1945,7 +1962,7 @@ void enqueue_lts2(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
   for (auto* c : cs) fuse_pred &= !c->halo.active();
   using C = mswm_cuda_ctx;
   // Step 1 (:483-487): h1 = h_old + dt*dh on I1 u I2 u C.
-  exchange(cs, &C::H, &C::U);
+  exchange(cs, &C::H, &C::U, kMaskIfCoarse);
   for (auto* c : cs) {
     double *H = c->H.p, *U = c->U.p, *H1 = c->H1.p, *U1 = c->U1.p;
     Op co[2] = {mk_op(OP_EULER, H1, H, dt), mk_op(OP_EULER, H1, H, dt)};
@@ -1972,7 +1989,7 @@ void enqueue_lts2(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
     // stage 1: fine hb = ha + delta*d; interfaces acc1 += d   (:521-531)
     if (k > 0 && !fuse_pred)
       for (auto* c : cs) launch_predict(c, 1, k, M, c->H.p, c->U.p, 2);
-    exchange(cs, &C::H, &C::U);
+    exchange(cs, &C::H, &C::U, kMaskSub);
     for (auto* c : cs) {
       const PredArgs pa = make_pred(c, 1, k, M, c->H.p, c->U.p, 2);
       Op co[2] = {mk_op(OP_EULER, c->H1.p, c->H.p, delta),
@@ -1986,7 +2003,7 @@ void enqueue_lts2(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
     // the last substep the interface correction (:532-541 order 2, :231-274)
     if (!fuse_pred)
       for (auto* c : cs) launch_predict(c, 2, k, M, c->H1.p, c->U1.p, 2);
-    exchange(cs, &C::H1, &C::U1);
+    exchange(cs, &C::H1, &C::U1, kMaskSub);
     for (auto* c : cs) {
       const PredArgs pa = make_pred(c, 2, k, M, c->H1.p, c->U1.p, 2);
       const double cr = 0.5 * delta;
@@ -2006,8 +2023,10 @@ void enqueue_lts2(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
     }
   }
   // Step 2 (:491-497): coarse h = 0.5 h_old + 0.5 h1 + (0.5 dt) dh, in place.
-  // H1/U1 halos are current: the last exchange refreshed them and only the
-  // state changed since.
+  // With full halos the H1/U1 copies are current (the last exchange
+  // refreshed them and only the state changed since); restricted halos
+  // refreshed only the substep's read set.
+  if (restricted(cs)) exchange(cs, &C::H1, &C::U1, kMaskCoarseOnly);
   for (auto* c : cs) {
     const double cr = 0.5 * dt;
     double *H = c->H.p, *U = c->U.p, *H1 = c->H1.p, *U1 = c->U1.p;
@@ -2052,7 +2071,7 @@ void enqueue_rk4(std::vector<mswm_cuda_ctx*>& cs, double dt) {
                         {&C::T2h, &C::T2u, &C::T1h, &C::T1u, OP_RK4_MID, dt},
                         {&C::T1h, &C::T1u, &C::H, &C::U, OP_RK4_LAST, sixth}};
   for (const St& st : stages) {
-    exchange(cs, st.rh, st.ru);
+    exchange(cs, st.rh, st.ru, MSWM_MASK_ALL);
     for (auto* c : cs) {
       auto co = both(mk_op(st.kind, (c->*st.wh).p, c->H.p, st.c0, nullptr, 0, 0, c->A1h.p));
       auto eo = both(mk_op(st.kind, (c->*st.wu).p, c->U.p, st.c0, nullptr, 0, 0, c->A1u.p));
@@ -2065,13 +2084,13 @@ void enqueue_rk4(std::vector<mswm_cuda_ctx*>& cs, double dt) {
 void enqueue_ssprk(std::vector<mswm_cuda_ctx*>& cs, int order, double dt) {
   using C = mswm_cuda_ctx;
   auto both = [](Op o) { return std::array<Op, 2>{o, o}; };
-  exchange(cs, &C::H, &C::U);
+  exchange(cs, &C::H, &C::U, MSWM_MASK_ALL);
   for (auto* c : cs) {
     auto co = both(mk_op(OP_EULER, c->T1h.p, c->H.p, dt));
     auto eo = both(mk_op(OP_EULER, c->T1u.p, c->U.p, dt));
     launch_eval(c, plan_for(c, MSWM_MASK_ALL), c->H.p, c->U.p, co.data(), eo.data());
   }
-  exchange(cs, &C::T1h, &C::T1u);
+  exchange(cs, &C::T1h, &C::T1u, MSWM_MASK_ALL);
   if (order == 2) {
     for (auto* c : cs) {
       const double cr = 0.5 * dt;
@@ -2087,7 +2106,7 @@ void enqueue_ssprk(std::vector<mswm_cuda_ctx*>& cs, int order, double dt) {
     auto eo = both(mk_op(OP_WCOMB, c->T2u.p, c->U.p, 0.75, c->T1u.p, 0.25, cr));
     launch_eval(c, plan_for(c, MSWM_MASK_ALL), c->T1h.p, c->T1u.p, co.data(), eo.data());
   }
-  exchange(cs, &C::T2h, &C::T2u);
+  exchange(cs, &C::T2h, &C::T2u, MSWM_MASK_ALL);
   for (auto* c : cs) {
     const double cr = (2.0 / 3.0) * dt;
     auto co = both(mk_op(OP_WCOMB, c->H.p, c->H.p, 1.0 / 3.0, c->T2h.p, 2.0 / 3.0, cr));
@@ -2786,13 +2805,99 @@ int mswm_cuda_set_halo(mswm_cuda_ctx* c, int rank, int n_ranks, int n_peers, con
     h.nr = int64_t(rc.size());
     h.scode.upload(sc, c->stream);
     h.rcode.upload(rc, c->stream);
+    h.h_scode = std::move(sc);
+    h.h_rcode = std::move(rc);
     h.sbuf.alloc(size_t(std::max<int64_t>(h.ns, 1)));
     h.rbuf.alloc(size_t(std::max<int64_t>(h.nr, 1)));
     CK(cudaStreamSynchronize(c->stream));
     c->drop_graphs();
     c->halo = std::move(h);
+    c->halo_mask.clear();
     c->rank = rank;
     c->n_ranks = n_ranks;
+    return int(MSWM_OK);
+  });
+}
+
+int mswm_cuda_halo_needs(mswm_cuda_ctx* c, unsigned mask, int64_t* counts, int32_t* pos) {
+  return guard(c, [&] {
+    check_ctx(c);
+    if (!counts) throw Error(MSWM_E_USAGE, "null counts");
+    const Halo& x = c->halo;
+    MaskPlan& p = plan_for(c, mask);
+    cudaStream_t s = c->stream;
+    DArr<uint8_t> cr, er;
+    cr.alloc(c->nC);
+    er.alloc(c->nE);
+    cr.zero(s);
+    er.zero(s);
+    const int64_t n = int64_t(p.nv) + p.nk + p.nf + p.ne;
+    if (n > 0) {
+      k_mark_reads<<<nblk(n), kBlock, 0, s>>>(c->dev(), p.vclos.p, p.nv, p.kclos.p, p.nk, p.fclos.p,
+                                              p.nf, p.edges, p.ne, cr.p, er.p);
+      CK(cudaGetLastError());
+    }
+    std::vector<uint8_t> hc(c->nC), he(c->nE);
+    CK(cudaMemcpyAsync(hc.data(), cr.p, size_t(c->nC), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(he.data(), er.p, size_t(c->nE), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int64_t at = 0;
+    for (size_t j = 0; j < x.peer.size(); ++j) {
+      int64_t k = 0;
+      for (int64_t q = 0; q < x.rcnt[j]; ++q) {
+        const int32_t code = x.h_rcode[size_t(x.roff[j] + q)];
+        if (code >= 0 ? hc[code] : he[~code]) {
+          if (pos) pos[at + k] = int32_t(q);
+          ++k;
+        }
+      }
+      counts[j] = k;
+      at += k;
+    }
+    return int(MSWM_OK);
+  });
+}
+
+int mswm_cuda_set_halo_mask(mswm_cuda_ctx* c, unsigned mask, const int64_t* send_counts,
+                            const int32_t* send_pos, const int64_t* recv_counts,
+                            const int32_t* recv_pos) {
+  return guard(c, [&] {
+    check_ctx(c);
+    const Halo& x = c->halo;
+    const size_t np = x.peer.size();
+    if (np && (!send_counts || !recv_counts)) throw Error(MSWM_E_USAGE, "null halo counts");
+    Halo h;
+    h.peer = x.peer;
+    std::vector<int32_t> sc, rc;
+    const int32_t* sp = send_pos;
+    const int32_t* rp = recv_pos;
+    for (size_t j = 0; j < np; ++j) {
+      h.soff.push_back(int64_t(sc.size()));
+      h.scnt.push_back(send_counts[j]);
+      for (int64_t k = 0; k < send_counts[j]; ++k) {
+        if (sp[k] < 0 || sp[k] >= x.scnt[j]) throw Error(MSWM_E_USAGE, "send position out of range");
+        sc.push_back(x.h_scode[size_t(x.soff[j] + sp[k])]);
+      }
+      sp += send_counts[j];
+      h.roff.push_back(int64_t(rc.size()));
+      h.rcnt.push_back(recv_counts[j]);
+      for (int64_t k = 0; k < recv_counts[j]; ++k) {
+        if (rp[k] < 0 || rp[k] >= x.rcnt[j]) throw Error(MSWM_E_USAGE, "recv position out of range");
+        rc.push_back(x.h_rcode[size_t(x.roff[j] + rp[k])]);
+      }
+      rp += recv_counts[j];
+    }
+    h.ns = int64_t(sc.size());
+    h.nr = int64_t(rc.size());
+    h.scode.upload(sc, c->stream);
+    h.rcode.upload(rc, c->stream);
+    h.sbuf.alloc(size_t(std::max<int64_t>(h.ns, 1)));
+    h.rbuf.alloc(size_t(std::max<int64_t>(h.nr, 1)));
+    CK(cudaStreamSynchronize(c->stream));
+    h.h_scode = std::move(sc);
+    h.h_rcode = std::move(rc);
+    c->drop_graphs();
+    c->halo_mask[mask] = std::move(h);
     return int(MSWM_OK);
   });
 }

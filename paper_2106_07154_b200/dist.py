@@ -29,6 +29,16 @@ from .mesh import Mesh
 from .partition import LocalMesh, build_local_meshes, partition_cells
 
 
+def swap_needs(rank: int, n_ranks: int, needs: dict) -> dict:
+    """Setup-time metadata swap over torch.distributed: given this rank's
+    {peer: positions it needs from peer}, return {peer: positions peer needs
+    from this rank}."""
+    import torch.distributed as dist
+    allv = [None] * n_ranks
+    dist.all_gather_object(allv, {int(q): np.asarray(v, np.int32) for q, v in needs.items()})
+    return {int(q): allv[int(q)].get(rank, np.zeros(0, np.int32)) for q in needs}
+
+
 class DistributedLayout:
     """Partition + local meshes of a global mesh with given region labels."""
 
@@ -90,6 +100,46 @@ class RankContext:
             self.ctx.handle, rank, layout.n_ranks, len(peers), _p(self._peers, _lib.i32p),
             _p(self._counts, _lib.i64p), _p(self._ids, _lib.i32p)))
 
+    # -- halo restriction per mask --------------------------
+    def halo_needs(self, mask: int) -> dict[int, np.ndarray]:
+        """Positions within each peer's receive list that the evaluation with
+        `mask` reads: {peer rank: positions}."""
+        lib = self.ctx.lib
+        counts = np.zeros(max(len(self._peers), 1), np.int64)
+        self.ctx._check(lib.mswm_cuda_halo_needs(self.ctx.handle, mask, _p(counts, _lib.i64p), None))
+        pos = np.zeros(max(int(counts.sum()), 1), np.int32)
+        self.ctx._check(lib.mswm_cuda_halo_needs(self.ctx.handle, mask, _p(counts, _lib.i64p),
+                                                 _p(pos, _lib.i32p)))
+        out, at = {}, 0
+        for j, q in enumerate(self._peers):
+            out[int(q)] = pos[at:at + counts[j]].copy()
+            at += counts[j]
+        return out
+
+    def set_halo_mask(self, mask: int, send: dict[int, np.ndarray], recv: dict[int, np.ndarray]):
+        """Install the restriction: send[q] = positions in my send list to q
+        (q's needs from me), recv[q] = my needs from q."""
+        empty = np.zeros(0, np.int32)
+        sc = np.array([len(send.get(int(q), empty)) for q in self._peers] or [0], np.int64)
+        rc = np.array([len(recv.get(int(q), empty)) for q in self._peers] or [0], np.int64)
+        sp = np.concatenate([send.get(int(q), empty) for q in self._peers] + [np.zeros(1, np.int32)])
+        rp = np.concatenate([recv.get(int(q), empty) for q in self._peers] + [np.zeros(1, np.int32)])
+        sp, rp = sp.astype(np.int32), rp.astype(np.int32)
+        self.ctx._check(self.ctx.lib.mswm_cuda_set_halo_mask(
+            self.ctx.handle, mask, _p(sc, _lib.i64p), _p(sp, _lib.i32p), _p(rc, _lib.i64p),
+            _p(rp, _lib.i32p)))
+
+    def restrict_halos(self, masks, exchange=None):
+        """Per-mask halo restriction for this rank.  `exchange(needs)` maps this
+        rank's {peer: positions} to {peer: that peer's positions for me}; by
+        default torch.distributed all_gather_object (setup time only)."""
+        if exchange is None:
+            def exchange(needs):
+                return swap_needs(self.rank, self.layout.n_ranks, needs)
+        for m in masks:
+            needs = self.halo_needs(int(m))
+            self.set_halo_mask(int(m), exchange(needs), needs)
+
     # -- NCCL transport ------------------------------------------------------
     @staticmethod
     def nccl_unique_id() -> bytes:
@@ -132,6 +182,14 @@ class CudaGroup:
             _raise(rc, lib.mswm_cuda_last_error(None).decode())
         self.handle = h
         self.lib = lib
+
+    def restrict_halos(self, masks):
+        """Per-mask halo restriction of every member (in-process peers)."""
+        for m in masks:
+            needs = [rc.halo_needs(int(m)) for rc in self.ranks]
+            for r, rc in enumerate(self.ranks):
+                send = {q: needs[q].get(r, np.zeros(0, np.int32)) for q in needs[r]}
+                rc.set_halo_mask(int(m), send, needs[r])
 
     def advance(self, scheme, dt: float, substeps: int = 1, n_steps: int = 1):
         rc = self.lib.mswm_cuda_group_step(self.handle, int(scheme), float(dt), int(substeps),

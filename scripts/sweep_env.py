@@ -39,7 +39,7 @@ def main():
                               fine_mask=wl.fine_mask, interface_width=wl.width)
             ctx.make_regions(wl.fine_mask, wl.width)
             ctx.upload(State(wl.h, wl.u, 0.0))
-            prof = os.environ.get("SWEEP_PROF", "1") == "1"
+            prof = int(os.environ.get("SWEEP_PROF", "1"))
             ctx.set_profiling(prof)
             stream = torch.cuda.ExternalStream(ctx.stream_ptr())
             ctx.advance(Scheme.LTS3, wl.dt, wl.M, 3)
@@ -55,8 +55,8 @@ def main():
             evms, evnc, evne = ctx.eval_profile() if prof else ([0.0] * 3, [0], [0])
             k = int(np.argmax(evne))
             print(f"{setting:40s} ms/step {ms:8.3f}  big-eval ms {evms[k]:.3f}  "
-                  f"evals {' '.join(f'{x:.3f}' for x in evms[:3])}  kernels {ctx.kernels_per_step()}"
-                  f"  flow {ctx.flow_info()}", flush=True)
+                  f"evals {' '.join(f'{x:.3f}' for x in evms[:16])}  kernels {ctx.kernels_per_step()}",
+                  flush=True)
             ctx.close()
             del ctx
         except Exception as ex:  # keep sweeping

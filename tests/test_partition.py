@@ -154,6 +154,127 @@ def _gloo_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
+def _read_sets(lm, lo):
+    """h-read cells and u-read edges of the oracle's last local evaluation
+    (operators.cpp:61-86 over its closure lists): the per-mask halo
+    restriction keeps exactly the halo entries in these sets."""
+    m = lm.as_mesh()
+    flux, _, kcells, verts = (lo.last_closure(k) for k in range(4))
+    cells = np.zeros(m.n_cells, bool)
+    edges = np.zeros(m.n_edges, bool)
+    cells[m.vertex_cells[verts].ravel()] = True
+    edges[m.vertex_edges[verts].ravel()] = True
+    for i in kcells:
+        edges[m.cell_edges[m.cell_offset[i]:m.cell_offset[i + 1]]] = True
+    edges[flux] = True
+    cells[m.edge_cells[flux].ravel()] = True
+    return cells, edges
+
+
+def _gloo_restricted_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    from paper_2106_07154_b200.api import MASK_SUB
+    from paper_2106_07154_b200.dist import swap_needs
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        wl = W.small_sphere(4, seed=5, cap_deg=30.0)
+        o, (cl, cs, el) = _labels(wl)
+        groups = o.groups()
+        lay = DistributedLayout(wl.mesh, cl, cs, el, world)
+        lm = lay.locals[rank]
+        rng = np.random.default_rng(2)
+        h = 1000.0 + rng.normal(size=wl.mesh.n_cells)
+        u = rng.normal(size=wl.mesh.n_edges)
+        results = []
+        for mask in (kMaskAll, int(MASK_SUB)):
+            in_c = np.zeros(wl.mesh.n_cells, bool)
+            in_e = np.zeros(wl.mesh.n_edges, bool)
+            for g in range(6):
+                if mask >> g & 1:
+                    in_c[groups[g]] = True
+            for g in range(5):
+                if mask >> (6 + g) & 1:
+                    in_e[groups[6 + g]] = True
+            cells = np.flatnonzero(in_c[lm.cells[:lm.n_owned_cells]]).astype(np.int32)
+            edges = np.flatnonzero(in_e[lm.edges[:lm.n_owned_edges]]).astype(np.int32)
+            lo = Oracle(lm.as_mesh(), lm.gather_cells(wl.b), lm.gather_vertices(wl.f), wl.gravity)
+            # closure of this rank's outputs (values irrelevant here)
+            lo.tendencies(np.ones(lm.n_cells) * 1000.0, np.zeros(lm.n_edges), cells, edges,
+                          np.zeros(lm.n_cells), np.zeros(lm.n_edges))
+            rc_, re_ = _read_sets(lm, lo)
+            peers = sorted(set(lm.send_cells) | set(lm.recv_cells))
+            needs = {}
+            for p in peers:
+                rl = np.concatenate([rc_[lm.recv_cells[p]], re_[lm.recv_edges[p]]])
+                needs[p] = np.flatnonzero(rl).astype(np.int32)
+            give = swap_needs(rank, world, needs)
+            # restricted exchange; everything not exchanged stays NaN
+            hc = np.full(lm.n_cells, np.nan)
+            ue = np.full(lm.n_edges, np.nan)
+            hc[:lm.n_owned_cells] = h[lm.cells[:lm.n_owned_cells]]
+            ue[:lm.n_owned_edges] = u[lm.edges[:lm.n_owned_edges]]
+            reqs, bufs = [], {}
+            for p in peers:
+                full = np.concatenate([hc[lm.send_cells[p]], ue[lm.send_edges[p]]])
+                sbuf = torch.from_numpy(np.ascontiguousarray(full[give[p]]))
+                rbuf = torch.empty(len(needs[p]), dtype=torch.float64)
+                bufs[p] = rbuf
+                reqs.append(dist.isend(sbuf, p))
+                reqs.append(dist.irecv(rbuf, p))
+            for r in reqs:
+                r.wait()
+            for p, rbuf in bufs.items():
+                nc = len(lm.recv_cells[p])
+                pos = needs[p]
+                v = rbuf.numpy()
+                hc[lm.recv_cells[p][pos[pos < nc]]] = v[pos < nc]
+                ue[lm.recv_edges[p][pos[pos >= nc] - nc]] = v[pos >= nc]
+            hc[-1] = 1.0
+            ue[-1] = 0.0
+            dh = np.zeros(lm.n_cells)
+            du = np.zeros(lm.n_edges)
+            lo.tendencies(hc, ue, cells, edges, dh, du)
+            dh_g = np.zeros(wl.mesh.n_cells)
+            du_g = np.zeros(wl.mesh.n_edges)
+            o.eval(h, u, mask, dh_g, du_g)
+            n_needed = sum(len(v) for v in needs.values())
+            n_full = sum(len(lm.recv_cells[p]) + len(lm.recv_edges[p]) for p in peers)
+            results.append((bool(bits_equal(dh[cells], dh_g[lm.cells[cells]])
+                                 and bits_equal(du[edges], du_g[lm.edges[edges]])),
+                            n_needed, n_full))
+        q.put((rank, results))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_two_rank_restricted_halos():
+    """Per-mask halo restriction: each rank exchanges only
+    the halo entries its masked evaluation reads (positions swapped with
+    dist.swap_needs over gloo); NaN elsewhere; results stay bitwise."""
+    import multiprocessing as mp
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_restricted_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(r[0] for r in res) == [0, 1]
+    for _, results in res:
+        (ok_all, n_all, full), (ok_sub, n_sub, _) = results
+        assert ok_all and ok_sub
+        assert n_sub < n_all <= full
+
+
 def test_gloo_two_rank_halo_exchange_and_evaluation():
     import multiprocessing as mp
     import socket
