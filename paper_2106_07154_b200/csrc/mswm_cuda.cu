@@ -233,7 +233,7 @@ struct mswm_cuda_ctx {
   // full occupancy at 32 registers) looping over their elements: 3.7 % faster
   // C4 steps than one CTA per 256 elements (CTA churn capped occupancy at
   // ~70 %); MSWM_PERSIST=0 restores one element per thread
-  int persist_ctas = 8, n_sm = 148;
+  int persist_ctas[3] = {8, 8, 8}, n_sm = 148;  // kernels A, B, C
   // fused tile kernel structures (k_tile)
   DArr<TileMeta> t_meta;
   DArr<int32_t> t_c1_ids, t_er_ids, t_vr_ids, t_e_tile;
@@ -1006,7 +1006,11 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   // the stencil tables streamed; "ringwalk" = three kernels walking the
   // rings through L1.  Meshes whose stencil is not the reference builder's
   // ring walk always take "explicit".  Tests cover all three.
-  if (const char* pe = std::getenv("MSWM_PERSIST")) c->persist_ctas = std::max(0, std::atoi(pe));
+  if (const char* pe = std::getenv("MSWM_PERSIST")) {  // "n" or "a,b,c"
+    int v[3];
+    const int k = std::sscanf(pe, "%d,%d,%d", &v[0], &v[1], &v[2]);
+    for (int j = 0; j < 3; ++j) c->persist_ctas[j] = std::max(0, k == 3 ? v[j] : v[0]);
+  }
   CK(cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, c->device));
   const bool eligible = derive_ring_stencil(d, kite_of_slot, slots);
   const char* kv = std::getenv("MSWM_KERNELS");
@@ -1413,9 +1417,10 @@ MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
 
 // Grid of a streamed kernel: one element per thread, or at most
 // `persist_ctas` CTAs per SM looping over the elements (MSWM_PERSIST).
-int sgrid(const mswm_cuda_ctx* c, int64_t n) {
+int sgrid(const mswm_cuda_ctx* c, int64_t n, int kernel) {
   const int64_t b = nblk(n);
-  return int(c->persist_ctas > 0 ? std::min<int64_t>(b, int64_t(c->persist_ctas) * c->n_sm) : b);
+  const int p = c->persist_ctas[kernel];
+  return int(p > 0 ? std::min<int64_t>(b, int64_t(p) * c->n_sm) : b);
 }
 
 Op op_none() {
@@ -1614,13 +1619,13 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
     return;
   }
   if (na > 0) {
-    k_vertex_cell<<<sgrid(c, na), kBlock, 0, s>>>(M, h, u, vs, ks, c->pv.p, c->K.p,
+    k_vertex_cell<<<sgrid(c, na, 0), kBlock, 0, s>>>(M, h, u, vs, ks, c->pv.p, c->K.p,
                                                  c->dry_vertex.p, p.vmask.p);
     CK(cudaGetLastError());
     ++c->launches;
   }
   if (p.se.n() > 0) {
-    k_edge_fq<<<sgrid(c, p.se.n()), kBlock, 0, s>>>(M, h, u, c->pv.p, es, c->FQ.p);
+    k_edge_fq<<<sgrid(c, p.se.n(), 1), kBlock, 0, s>>>(M, h, u, c->pv.p, es, c->FQ.p);
     CK(cudaGetLastError());
     ++c->launches;
   }
@@ -1637,7 +1642,7 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
     a.cop[1] = cop[1];
     a.eop[0] = eop[0];
     a.eop[1] = eop[1];
-    k_out<<<sgrid(c, nout), kBlock, 0, s>>>(M, h, c->K.p, c->FQ.p, a);
+    k_out<<<sgrid(c, nout, 2), kBlock, 0, s>>>(M, h, c->K.p, c->FQ.p, a);
     CK(cudaGetLastError());
     ++c->launches;
   }
