@@ -456,3 +456,34 @@ def test_eval_profile_levels():
         assert bits_equal(st.h, ref.h) and bits_equal(st.u, ref.u)
     with pytest.raises(UsageError):
         ctx.set_profiling(3)
+
+
+@pytest.mark.parametrize("width", [2, 3])
+def test_wide_interfaces_bitwise(width):
+    """Interface bands of `width` layers each (make_regions width,
+    regions.cpp:69-105; the paper widens them to tens of layers): regions,
+    every LTS3 mask, LTS3 and LTS2 steps bitwise against the oracle, in the
+    Hilbert and region-major layouts."""
+    wl = W.small_sphere(5, seed=47, cap_deg=20.0)
+    o = Oracle(wl.mesh, wl.b, wl.f, wl.gravity)
+    o.set_regions(wl.fine_mask, width)
+    for order in ["hilbert", "regions"]:
+        ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order, fine_mask=wl.fine_mask,
+                          interface_width=width)
+        ctx.make_regions(wl.fine_mask, width)
+        for a, b in zip(ctx.regions.groups, o.groups()):
+            assert np.array_equal(a, b)
+        ev = CudaEvaluator(ctx)
+        for mask in LTS3_MASKS:
+            dh1 = np.full(wl.mesh.n_cells, SENTINEL)
+            du1 = np.full(wl.mesh.n_edges, SENTINEL)
+            dh2, du2 = dh1.copy(), du1.copy()
+            ev.eval(wl.h, wl.u, mask, dh1, du1)
+            o.eval(wl.h, wl.u, mask, dh2, du2)
+            assert bits_equal(dh1, dh2) and bits_equal(du1, du2), hex(mask)
+        for scheme in (Scheme.LTS3, Scheme.LTS2):
+            h_ref, u_ref, _ = o.step(int(scheme), wl.h, wl.u, 0.0, wl.dt, wl.M, 3)
+            ctx.upload(State(wl.h, wl.u, 0.0))
+            ctx.advance(scheme, wl.dt, wl.M, 3)
+            st = ctx.download()
+            assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref), (order, scheme)

@@ -147,3 +147,21 @@ def test_diagnostics_match_reference(ref_lib, make):
     assert o2.courant(u, wl.dt, 3) == rm.courant(None, u, wl.dt, 3)
     f, c = o2.courant(u, wl.dt, 3)
     assert f == c > 0
+
+
+@pytest.mark.parametrize("width", [2, 3])
+def test_restatement_wide_interfaces_match_reference(ref_lib, width):
+    """make_regions with interface bands of `width` layers (regions.cpp:69-105)
+    and the LTS steps on them: restatement = reference, bitwise."""
+    from oracle.oracle import RefEvaluator, RefMesh, RefRegions
+    wl = W.small_sphere(4, seed=9, cap_deg=35.0)
+    rm = RefMesh.from_mesh(wl.mesh)
+    rr = RefRegions(rm, wl.fine_mask, width)
+    ev = RefEvaluator(rm, rr, wl.b, wl.f, wl.gravity)
+    o = Oracle(wl.mesh, wl.b, wl.f, wl.gravity)
+    o.set_regions(wl.fine_mask, width)
+    assert all(np.array_equal(a, b) for a, b in zip(rr.groups(), o.groups()))
+    for scheme in (Scheme.LTS3, Scheme.LTS2):
+        h1, u1, _, _ = ev.step(int(scheme), wl.h, wl.u, 0.0, wl.dt, wl.M, 3)
+        h2, u2, _ = o.step(int(scheme), wl.h, wl.u, 0.0, wl.dt, wl.M, 3)
+        assert bits_equal(h1, h2) and bits_equal(u1, u2), scheme
