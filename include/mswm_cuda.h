@@ -208,6 +208,12 @@ int mswm_cuda_eval_profile(mswm_cuda_ctx* ctx, float* eval_ms,
 int mswm_cuda_layout_info(const mswm_cuda_ctx* ctx, int* kernel_path,
                           int* identity_order);
 
+/* Explicit stencil tables: offsets16 = 1 when the stencil ids are stored as
+ * 16-bit offsets e' - e (20 B/edge; MSWM_ST16=0 at create disables them);
+ * n_wide = edges with an offset outside int16, whose warps read the int32
+ * table instead (edges_on_edge, mesh.hpp:60-61). */
+int mswm_cuda_stencil_info(const mswm_cuda_ctx* ctx, int* offsets16, int64_t* n_wide);
+
 /* Dataflow evaluation (k_flow, opt-in with MSWM_FLOW=1 at create): large
  * masks run as one persistent launch over cell slabs of slab_cells cells;
  * all zero when disabled (the default, small meshes). */

@@ -355,6 +355,12 @@ class CudaContext:
         return {"kernel_path": {0: "explicit", 1: "ringwalk", 2: "tile", 3: "auto"}[kp.value],
                 "input_order": bool(ident.value)}
 
+    def stencil_info(self) -> dict:
+        """16-bit stencil offsets in use, and the edges that need the int32 table."""
+        o, n = C.c_int(0), C.c_int64(0)
+        self._check(self.lib.mswm_cuda_stencil_info(self.handle, C.byref(o), C.byref(n)))
+        return {"offsets16": bool(o.value), "n_wide": n.value}
+
     def flow_info(self) -> dict:
         """Dataflow evaluation (k_flow) parameters; slab_cells 0 = disabled."""
         v = [C.c_int(0) for _ in range(4)]

@@ -18,11 +18,18 @@ namespace cg = cooperative_groups;
 
 constexpr int kMaxDeg = 8;               // ring size bound (hexagons 6, pentagons 5)
 constexpr int kMaxSten = 2 * kMaxDeg - 2;
+// hexagon/pentagon meshes (every mesh of BASELINE.json): ring tables of 6
+// slots, stencils of at most 10 -- the kernels' straight-line fast paths
+constexpr int kFastDeg = 6;
+constexpr int kFastSten = 10;
 constexpr int kBlock = 256;
 // minimum resident CTAs per SM requested from ptxas (register budget) for
 // the streamed kernels; tuned on B200 (profiles/r1_*)
 #ifndef MSWM_KA_MINB
 #define MSWM_KA_MINB 8
+#endif
+#ifndef MSWM_KOUT_BATCH
+#define MSWM_KOUT_BATCH 5
 #endif
 #ifndef MSWM_KOUT_MINB
 #define MSWM_KOUT_MINB 8
@@ -66,8 +73,10 @@ struct DevMesh {
   const double* __restrict__ e_invd;     // 1.0 / d_e
   const uint8_t* __restrict__ e_slots;   // ring-derived stencil: bits 0-2 slot of e in
                                          // ring(c0), 3-5 in ring(c1), 6/7 anchor sign < 0
-  const uint8_t* __restrict__ e_nst;     // stencil length
+  const uint8_t* __restrict__ e_nst;     // stencil length; bit 7: some e' - e outside int16
   const int32_t* __restrict__ e_sten;    // [sten_max][nE] edges_on_edge
+  const uint32_t* __restrict__ e_st16;   // [(sten_max+1)/2][nE] e' - e as int16 pairs, entry
+                                         // 2k in the low half of word k (null: int32 only)
   const double* __restrict__ e_coef;     // [sten_max][nE] w * (l_{e'} * (1/d_e))
   // fields
   const double* __restrict__ b;          // [nC]
@@ -192,10 +201,25 @@ __device__ __forceinline__ void item_vertex_cell(const DevMesh& M, const double*
     const int32_t i = ks.at(t - nv);
     const int deg = M.c_deg[i];
     double acc = 0.0;
-    for (int j = 0; j < deg; ++j) {
-      const int32_t e = M.c_edge[j * M.nC + i];
-      const double ue = u[e];
-      acc += M.e_ld[e] * ue * ue;
+    if (M.deg_max == kFastDeg) {
+      // all ring ids first, then all gathers: the loads of one cell are
+      // independent and issue back to back (padding slots hold id 0, a
+      // valid edge, and are not accumulated)
+      int32_t ce[kFastDeg];
+#pragma unroll
+      for (int j = 0; j < kFastDeg; ++j) ce[j] = M.c_edge[j * M.nC + i];
+#pragma unroll
+      for (int j = 0; j < kFastDeg; ++j) {
+        const double ue = u[ce[j]];
+        const double x = M.e_ld[ce[j]] * ue * ue;
+        if (j < deg) acc += x;
+      }
+    } else {
+      for (int j = 0; j < deg; ++j) {
+        const int32_t e = M.c_edge[j * M.nC + i];
+        const double ue = u[e];
+        acc += M.e_ld[e] * ue * ue;
+      }
     }
     K[i] = acc / (4.0 * M.c_area[i]);
   }
@@ -275,12 +299,24 @@ __device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __re
     const int deg = M.c_deg[i];
     const uint8_t sb = M.c_sbits[i];
     double acc = 0.0;
+    if (M.deg_max == kFastDeg) {
+      int32_t ce[kFastDeg];
 #pragma unroll
-    for (int j = 0; j < kMaxDeg; ++j) {
-      if (j < deg) {
-        const int32_t e = M.c_edge[j * M.nC + i];
-        const double l = M.e_len[e];
-        acc += ((sb >> j) & 1 ? -l : l) * ldx<CG>(FQ + e).x;
+      for (int j = 0; j < kFastDeg; ++j) ce[j] = M.c_edge[j * M.nC + i];
+#pragma unroll
+      for (int j = 0; j < kFastDeg; ++j) {
+        const double l = M.e_len[ce[j]];
+        const double x = ((sb >> j) & 1 ? -l : l) * ldx<CG>(FQ + ce[j]).x;
+        if (j < deg) acc += x;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kMaxDeg; ++j) {
+        if (j < deg) {
+          const int32_t e = M.c_edge[j * M.nC + i];
+          const double l = M.e_len[e];
+          acc += ((sb >> j) & 1 ? -l : l) * ldx<CG>(FQ + e).x;
+        }
       }
     }
     const double dh = -acc / M.c_area[i];
@@ -327,14 +363,55 @@ __device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __re
         }
       }
     } else {
-      const int nst = M.e_nst[e];
+      // Stencil ids as 16-bit offsets from e (20 B/edge instead of 40 B);
+      // a warp holding any edge whose offsets do not fit (bit 7 of e_nst:
+      // ~1 % of edges, along the curve's seams) reads the int32 table
+      // instead.  The vote keeps the path warp-uniform, so the ten gathers
+      // stay back to back.
+      const int nstw = M.e_nst[e];
+      const int nst = nstw & 0x7f;
+      const bool wide = !M.e_st16 || __any_sync(__activemask(), nstw & 0x80);
+      if (!wide && M.sten_max == kFastSten) {
+        // straight line: five packed id words, then coefficients and
+        // gathers, predicated accumulation (padding entries hold valid ids
+        // and are skipped)
+        uint32_t w[kFastSten / 2];
 #pragma unroll
-      for (int j = 0; j < kMaxSten; ++j) {
-        if (j < nst) {
-          const int32_t e2 = M.e_sten[j * M.nE + e];
-          const double c = M.e_coef[j * M.nE + e];
-          const double2 fq = ldx<CG>(FQ + e2);
-          pvflux += c * fq.x * (0.5 * (qt_e + fq.y));
+        for (int k = 0; k < kFastSten / 2; ++k) w[k] = M.e_st16[k * M.nE + e];
+        // batches of MSWM_KOUT_BATCH entries: every load of a batch is
+        // issued before the first of its products
+#pragma unroll
+        for (int j0 = 0; j0 < kFastSten; j0 += MSWM_KOUT_BATCH) {
+          double c[MSWM_KOUT_BATCH];
+          double2 fq[MSWM_KOUT_BATCH];
+#pragma unroll
+          for (int b = 0; b < MSWM_KOUT_BATCH; ++b) {
+            const int j = j0 + b;
+            if (j < kFastSten) {
+              const int32_t e2 = e + (j & 1 ? int32_t(w[j >> 1]) >> 16
+                                            : int32_t(w[j >> 1] << 16) >> 16);
+              c[b] = M.e_coef[j * M.nE + e];
+              fq[b] = ldx<CG>(FQ + e2);
+            }
+          }
+#pragma unroll
+          for (int b = 0; b < MSWM_KOUT_BATCH; ++b) {
+            const int j = j0 + b;
+            if (j < kFastSten) {
+              const double x = c[b] * fq[b].x * (0.5 * (qt_e + fq[b].y));
+              if (j < nst) pvflux += x;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < kMaxSten; ++j) {
+          if (j < nst) {
+            const int32_t e2 = M.e_sten[j * M.nE + e];
+            const double c = M.e_coef[j * M.nE + e];
+            const double2 fq = ldx<CG>(FQ + e2);
+            pvflux += c * fq.x * (0.5 * (qt_e + fq.y));
+          }
         }
       }
     }

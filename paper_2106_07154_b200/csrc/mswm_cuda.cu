@@ -222,6 +222,8 @@ struct mswm_cuda_ctx {
 
   // device mesh
   DArr<int32_t> c_edge, c_vert, c_nbr, v_cell, v_edge, v_orig, e_sten;
+  DArr<uint32_t> e_st16;
+  int64_t n_sten_wide = 0;
   DArr<uint8_t> c_deg, c_sbits, v_sbits, e_nst, e_slots;
   DArr<double> c_area, c_ratio, v_kite, v_area, e_len, e_ld, e_dual, e_invd, e_coef, b, f;
   bool ring_derived = false;
@@ -348,6 +350,7 @@ struct mswm_cuda_ctx {
     M.e_nst = e_nst.p;
     M.e_slots = (ring_derived || tile_path || hybrid) ? e_slots.p : nullptr;
     M.e_sten = e_sten.p;
+    M.e_st16 = e_st16.p;
     M.e_coef = e_coef.p;
     M.b = b.p;
     M.f = f.p;
@@ -1086,12 +1089,18 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   std::vector<double> e_len(nE), e_ld(nE), e_dual(nE), e_invd(nE);
   std::vector<uint8_t> e_nst, e_slots;
   std::vector<int32_t> e_sten;
+  std::vector<uint32_t> e_st16;
   std::vector<double> e_coef;
+  // 16-bit stencil offsets (kernels.cuh item_out_sp); MSWM_ST16=0 keeps the
+  // int32 table only (A/B runs)
+  const char* s16 = std::getenv("MSWM_ST16");
+  const bool use16 = sten_max < 0x80 && !(s16 && s16[0] == '0');
   if (need_ratio) e_slots.resize(nE);
   if (need_explicit) {
     e_nst.resize(nE);
     e_sten.assign(size_t(std::max(sten_max, 1)) * nE, 0);
     e_coef.assign(size_t(std::max(sten_max, 1)) * nE, 0.0);
+    if (use16) e_st16.assign(size_t((std::max(sten_max, 1) + 1) / 2) * nE, 0u);
   }
   for (int32_t ne = 0; ne < nE; ++ne) {
     const int32_t e = en[ne];
@@ -1113,6 +1122,11 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
       const int32_t e2 = d->edge_edges[off + j];
       need(e2 >= 0 && e2 < nE, "stencil id out of range");
       e_sten[size_t(j) * nE + ne] = eo[e2];
+      const int32_t dlt = eo[e2] - ne;
+      if (dlt < INT16_MIN || dlt > INT16_MAX)
+        e_nst[ne] |= 0x80;
+      else if (use16)
+        e_st16[size_t(j / 2) * nE + ne] |= (uint32_t(dlt) & 0xFFFFu) << (16 * (j & 1));
       // operators.cpp:109: weights[j] * (edge_len[e2] * inv_d), the first
       // two factors of the stencil term -- mesh constants.
       e_coef[size_t(j) * nE + ne] = d->edge_weight[off + j] * (d->edge_len[e2] * inv_d);
@@ -1141,6 +1155,9 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   c->e_nst.upload(e_nst, s);
   c->e_slots.upload(e_slots, s);
   c->e_sten.upload(e_sten, s);
+  c->e_st16.upload(e_st16, s);
+  c->n_sten_wide = 0;
+  for (const uint8_t x : e_nst) c->n_sten_wide += x >> 7;
   c->e_coef.upload(e_coef, s);
   CK(cudaStreamSynchronize(s));  // host vectors die here
 
@@ -2618,6 +2635,13 @@ int mswm_cuda_layout_info(const mswm_cuda_ctx* c, int* kernel_path, int* identit
   if (!c) return MSWM_E_USAGE;
   if (kernel_path) *kernel_path = c->tile_path ? 2 : (c->ring_derived ? 1 : (c->hybrid ? 3 : 0));
   if (identity_order) *identity_order = c->identity ? 1 : 0;
+  return MSWM_OK;
+}
+
+int mswm_cuda_stencil_info(const mswm_cuda_ctx* c, int* offsets16, int64_t* n_wide) {
+  if (!c) return MSWM_E_USAGE;
+  if (offsets16) *offsets16 = c->e_st16.p ? 1 : 0;
+  if (n_wide) *n_wide = c->n_sten_wide;
   return MSWM_OK;
 }
 

@@ -487,3 +487,34 @@ def test_wide_interfaces_bitwise(width):
             ctx.advance(scheme, wl.dt, wl.M, 3)
             st = ctx.download()
             assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref), (order, scheme)
+
+
+@pytest.mark.parametrize("st16", ["1", "0"])
+def test_stencil_offsets16_bitwise(st16, monkeypatch):
+    """16-bit stencil offsets (default) with edges whose offsets overflow
+    int16 (a random numbering of a level-6 sphere: 123k edges, most offsets
+    wide, warps mixing both kinds) and the int32-only table: bitwise equal."""
+    monkeypatch.setenv("MSWM_ST16", st16)
+    wl = W.small_sphere(6, seed=31, cap_deg=20.0)
+    o = _oracle_for(wl)
+    h_ref, u_ref, _ = o.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, wl.M, 2)
+    rng = np.random.default_rng(3)
+    for order in ["regions", rng.permutation(wl.mesh.n_cells).astype(np.int32)]:
+        ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order, fine_mask=wl.fine_mask)
+        info = ctx.stencil_info()
+        assert info["offsets16"] == (st16 == "1")
+        if not isinstance(order, str):
+            assert 0 < info["n_wide"] < wl.mesh.n_edges
+        ctx.make_regions(wl.fine_mask, wl.width)
+        ev = CudaEvaluator(ctx)
+        for mask in LTS3_MASKS:
+            dh1 = np.full(wl.mesh.n_cells, SENTINEL)
+            du1 = np.full(wl.mesh.n_edges, SENTINEL)
+            dh2, du2 = dh1.copy(), du1.copy()
+            ev.eval(wl.h, wl.u, mask, dh1, du1)
+            o.eval(wl.h, wl.u, mask, dh2, du2)
+            assert bits_equal(dh1, dh2) and bits_equal(du1, du2)
+        ctx.upload(State(wl.h, wl.u, 0.0))
+        ctx.advance(Scheme.LTS3, wl.dt, wl.M, 2)
+        st = ctx.download()
+        assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
