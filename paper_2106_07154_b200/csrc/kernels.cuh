@@ -28,8 +28,14 @@ constexpr int kBlock = 256;
 #ifndef MSWM_KA_MINB
 #define MSWM_KA_MINB 8
 #endif
+#ifndef MSWM_VCE
+#define MSWM_VCE 1
+#endif
+#ifndef MSWM_KITE01
+#define MSWM_KITE01 0
+#endif
 #ifndef MSWM_KOUT_BATCH
-#define MSWM_KOUT_BATCH 5
+#define MSWM_KOUT_BATCH 3   // coefficient pairs per batch
 #endif
 #ifndef MSWM_KOUT_MINB
 #define MSWM_KOUT_MINB 8
@@ -75,9 +81,17 @@ struct DevMesh {
                                          // ring(c0), 3-5 in ring(c1), 6/7 anchor sign < 0
   const uint8_t* __restrict__ e_nst;     // stencil length; bit 7: some e' - e outside int16
   const int32_t* __restrict__ e_sten;    // [sten_max][nE] edges_on_edge
-  const uint32_t* __restrict__ e_st16;   // [(sten_max+1)/2][nE] e' - e as int16 pairs, entry
-                                         // 2k in the low half of word k (null: int32 only)
-  const double* __restrict__ e_coef;     // [sten_max][nE] w * (l_{e'} * (1/d_e))
+  const uint2* __restrict__ e_st16;      // [(W+1)/2][nE], W = (sten_max+1)/2 u32 words of
+                                         // e' - e as int16 pairs (entry 2k in the low half
+                                         // of word k), two words per load (null: int32 only)
+  const double2* __restrict__ e_coef2;   // [(sten_max+1)/2][nE] w * (l_{e'} * (1/d_e)) for
+                                         // entries (2k, 2k+1): one 16 B load per pair
+  // packed copies for the streamed kernels (fewer load instructions, same
+  // coalescing: consecutive threads still read consecutive 8/16 B)
+  const int2* __restrict__ c_edge2;      // [(deg_max+1)/2][nC] ring edges (2k, 2k+1)
+  const int2* __restrict__ v_ce;         // [3][nV] (vertex_cells k, vertex_edges k)
+  const double2* __restrict__ v_kite01;  // [nV] (kite 0, kite 1); kite 2 in v_kite
+  const double2* __restrict__ v_af;      // [nV] (A_v, f_v)
   // fields
   const double* __restrict__ b;          // [nC]
   const double* __restrict__ f;          // [nV]
@@ -168,7 +182,8 @@ __device__ __forceinline__ void apply_op(const Op& op, int32_t i, double d) {
 
 // ---------------------------------------------------------------------------
 // Phase A: potential vorticity on the closure vertices (operators.cpp:74-86)
-// and kinetic energy on the closure cells (:64-72), one launch.
+// and kinetic energy -> Bernoulli potential psi on the closure cells
+// (:64-72, :112-113), one launch.
 // one element of phase A (t indexes vs then ks)
 __device__ __forceinline__ void item_vertex_cell(const DevMesh& M, const double* __restrict__ h,
                                                  const double* __restrict__ u, const Span& vs,
@@ -182,21 +197,37 @@ __device__ __forceinline__ void item_vertex_cell(const DevMesh& M, const double*
   if (t < nv) {
     const int32_t v = vs.at(t);
     const uint8_t sb = M.v_sbits[v];
+    int2 ce[3];
+#if MSWM_VCE
+#pragma unroll
+    for (int k = 0; k < 3; ++k) ce[k] = M.v_ce[k * M.nV + v];
+#else
+#pragma unroll
+    for (int k = 0; k < 3; ++k) ce[k] = make_int2(M.v_cell[k * M.nV + v], M.v_edge[k * M.nV + v]);
+#endif
     double hv = 0.0, circ = 0.0;
+#if MSWM_KITE01
+    const double2 k01 = M.v_kite01[v];
+    const double kite[3] = {k01.x, k01.y, M.v_kite[2 * M.nV + v]};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) hv += kite[k] * h[ce[k].x];
+#else
+#pragma unroll
+    for (int k = 0; k < 3; ++k) hv += M.v_kite[k * M.nV + v] * h[ce[k].x];
+#endif
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      hv += M.v_kite[k * M.nV + v] * h[M.v_cell[k * M.nV + v]];
-      const int32_t e = M.v_edge[k * M.nV + v];
-      const double d = M.e_dual[e];
-      circ += ((sb >> k) & 1 ? -d : d) * u[e];
+      const double d = M.e_dual[ce[k].y];
+      circ += ((sb >> k) & 1 ? -d : d) * u[ce[k].y];
     }
-    hv /= M.v_area[v];
+    const double2 af = M.v_af[v];
+    hv /= af.x;
     if (!(hv > 0.0)) {
       if (!vmask || ((vmask[v >> 5] >> (v & 31)) & 1u)) atomicMin(dry, M.v_orig[v]);
       pv[v] = 0.0;
       return;
     }
-    pv[v] = (M.f[v] + circ / M.v_area[v]) / hv;
+    pv[v] = (af.y + circ / af.x) / hv;
   } else if (t - nv < ks.n()) {
     const int32_t i = ks.at(t - nv);
     const int deg = M.c_deg[i];
@@ -207,7 +238,11 @@ __device__ __forceinline__ void item_vertex_cell(const DevMesh& M, const double*
       // valid edge, and are not accumulated)
       int32_t ce[kFastDeg];
 #pragma unroll
-      for (int j = 0; j < kFastDeg; ++j) ce[j] = M.c_edge[j * M.nC + i];
+      for (int k = 0; k < kFastDeg / 2; ++k) {
+        const int2 p = M.c_edge2[k * M.nC + i];
+        ce[2 * k] = p.x;
+        ce[2 * k + 1] = p.y;
+      }
 #pragma unroll
       for (int j = 0; j < kFastDeg; ++j) {
         const double ue = u[ce[j]];
@@ -221,7 +256,11 @@ __device__ __forceinline__ void item_vertex_cell(const DevMesh& M, const double*
         acc += M.e_ld[e] * ue * ue;
       }
     }
-    K[i] = acc / (4.0 * M.c_area[i]);
+    // the Bernoulli potential psi_i = g (h_i + b_i) + K_i (operators.cpp:112-113),
+    // formed here once per closure cell instead of twice per output edge
+    // in phase C (same operations, same order: bitwise the reference's)
+    const double Ki = acc / (4.0 * M.c_area[i]);
+    K[i] = M.g * (h[i] + M.b[i]) + Ki;
   }
 }
 
@@ -302,7 +341,11 @@ __device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __re
     if (M.deg_max == kFastDeg) {
       int32_t ce[kFastDeg];
 #pragma unroll
-      for (int j = 0; j < kFastDeg; ++j) ce[j] = M.c_edge[j * M.nC + i];
+      for (int k = 0; k < kFastDeg / 2; ++k) {
+        const int2 p = M.c_edge2[k * M.nC + i];
+        ce[2 * k] = p.x;
+        ce[2 * k + 1] = p.y;
+      }
 #pragma unroll
       for (int j = 0; j < kFastDeg; ++j) {
         const double l = M.e_len[ce[j]];
@@ -372,33 +415,36 @@ __device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __re
       const int nst = nstw & 0x7f;
       const bool wide = !M.e_st16 || __any_sync(__activemask(), nstw & 0x80);
       if (!wide && M.sten_max == kFastSten) {
-        // straight line: five packed id words, then coefficients and
-        // gathers, predicated accumulation (padding entries hold valid ids
-        // and are skipped)
-        uint32_t w[kFastSten / 2];
+        // straight line: three 8 B loads of packed id words, then batches
+        // of coefficient pairs (16 B) and (F, q~) gathers, predicated
+        // accumulation (padding entries hold valid ids and are skipped)
+        uint32_t w[kFastSten / 2 + 1];
 #pragma unroll
-        for (int k = 0; k < kFastSten / 2; ++k) w[k] = M.e_st16[k * M.nE + e];
-        // batches of MSWM_KOUT_BATCH entries: every load of a batch is
-        // issued before the first of its products
+        for (int k = 0; k < (kFastSten / 2 + 1) / 2; ++k) {
+          const uint2 p = M.e_st16[k * M.nE + e];
+          w[2 * k] = p.x;
+          w[2 * k + 1] = p.y;
+        }
 #pragma unroll
-        for (int j0 = 0; j0 < kFastSten; j0 += MSWM_KOUT_BATCH) {
-          double c[MSWM_KOUT_BATCH];
-          double2 fq[MSWM_KOUT_BATCH];
+        for (int j0 = 0; j0 < kFastSten; j0 += 2 * MSWM_KOUT_BATCH) {
+          double2 c[MSWM_KOUT_BATCH];
+          double2 fq[2 * MSWM_KOUT_BATCH];
 #pragma unroll
-          for (int b = 0; b < MSWM_KOUT_BATCH; ++b) {
+          for (int b = 0; b < 2 * MSWM_KOUT_BATCH; ++b) {
             const int j = j0 + b;
             if (j < kFastSten) {
+              if (!(b & 1)) c[b >> 1] = M.e_coef2[(j >> 1) * M.nE + e];
               const int32_t e2 = e + (j & 1 ? int32_t(w[j >> 1]) >> 16
                                             : int32_t(w[j >> 1] << 16) >> 16);
-              c[b] = M.e_coef[j * M.nE + e];
               fq[b] = ldx<CG>(FQ + e2);
             }
           }
 #pragma unroll
-          for (int b = 0; b < MSWM_KOUT_BATCH; ++b) {
+          for (int b = 0; b < 2 * MSWM_KOUT_BATCH; ++b) {
             const int j = j0 + b;
             if (j < kFastSten) {
-              const double x = c[b] * fq[b].x * (0.5 * (qt_e + fq[b].y));
+              const double cj = b & 1 ? c[b >> 1].y : c[b >> 1].x;
+              const double x = cj * fq[b].x * (0.5 * (qt_e + fq[b].y));
               if (j < nst) pvflux += x;
             }
           }
@@ -408,15 +454,16 @@ __device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __re
         for (int j = 0; j < kMaxSten; ++j) {
           if (j < nst) {
             const int32_t e2 = M.e_sten[j * M.nE + e];
-            const double c = M.e_coef[j * M.nE + e];
+            const double2 cp = M.e_coef2[(j >> 1) * M.nE + e];
+            const double c = j & 1 ? cp.y : cp.x;
             const double2 fq = ldx<CG>(FQ + e2);
             pvflux += c * fq.x * (0.5 * (qt_e + fq.y));
           }
         }
       }
     }
-    const double psi_lo = M.g * (h[cc.x] + M.b[cc.x]) + ldx<CG>(K + cc.x);
-    const double psi_hi = M.g * (h[cc.y] + M.b[cc.y]) + ldx<CG>(K + cc.y);
+    const double psi_lo = ldx<CG>(K + cc.x);  // psi (phase A)
+    const double psi_hi = ldx<CG>(K + cc.y);
     const double du = -pvflux - (psi_lo - psi_hi) * inv_d;
     apply_op(a.eop[seg], e, du);
   }

@@ -105,6 +105,11 @@ struct DArr {
 
 inline int nblk(int64_t n, int b = kBlock) { return int((n + b - 1) / b); }
 
+__global__ void k_fill_af(int32_t n, const double* __restrict__ f, double2* __restrict__ af) {
+  const int32_t v = blockIdx.x * kBlock + threadIdx.x;
+  if (v < n) af[v].y = f[v];
+}
+
 // Output lists and closure lists of one mask (operators.cpp:35-58).
 struct MaskPlan {
   unsigned mask = 0;
@@ -222,7 +227,9 @@ struct mswm_cuda_ctx {
 
   // device mesh
   DArr<int32_t> c_edge, c_vert, c_nbr, v_cell, v_edge, v_orig, e_sten;
-  DArr<uint32_t> e_st16;
+  DArr<uint2> e_st16;
+  DArr<double2> e_coef2, v_kite01, v_af;
+  DArr<int2> c_edge2, v_ce;
   int64_t n_sten_wide = 0;
   DArr<uint8_t> c_deg, c_sbits, v_sbits, e_nst, e_slots;
   DArr<double> c_area, c_ratio, v_kite, v_area, e_len, e_ld, e_dual, e_invd, e_coef, b, f;
@@ -351,7 +358,11 @@ struct mswm_cuda_ctx {
     M.e_slots = (ring_derived || tile_path || hybrid) ? e_slots.p : nullptr;
     M.e_sten = e_sten.p;
     M.e_st16 = e_st16.p;
-    M.e_coef = e_coef.p;
+    M.e_coef2 = e_coef2.p;
+    M.c_edge2 = c_edge2.p;
+    M.v_ce = v_ce.p;
+    M.v_kite01 = v_kite01.p;
+    M.v_af = v_af.p;
     M.b = b.p;
     M.f = f.p;
     M.g = gravity;
@@ -1091,6 +1102,7 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   std::vector<int32_t> e_sten;
   std::vector<uint32_t> e_st16;
   std::vector<double> e_coef;
+  const int n_words = (std::max(sten_max, 1) + 1) / 2;
   // 16-bit stencil offsets (kernels.cuh item_out_sp); MSWM_ST16=0 keeps the
   // int32 table only (A/B runs)
   const char* s16 = std::getenv("MSWM_ST16");
@@ -1100,7 +1112,7 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
     e_nst.resize(nE);
     e_sten.assign(size_t(std::max(sten_max, 1)) * nE, 0);
     e_coef.assign(size_t(std::max(sten_max, 1)) * nE, 0.0);
-    if (use16) e_st16.assign(size_t((std::max(sten_max, 1) + 1) / 2) * nE, 0u);
+    if (use16) e_st16.assign(size_t(n_words) * nE, 0u);
   }
   for (int32_t ne = 0; ne < nE; ++ne) {
     const int32_t e = en[ne];
@@ -1132,7 +1144,46 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
       e_coef[size_t(j) * nE + ne] = d->edge_weight[off + j] * (d->edge_len[e2] * inv_d);
     }
   }
+  // packed copies (kernels.cuh DevMesh): pairs of slots / entries per load
+  std::vector<int2> c_edge2(size_t((deg_max + 1) / 2) * nC, make_int2(0, 0));
+  for (int j = 0; j < deg_max; ++j)
+    for (int32_t i = 0; i < nC; ++i) {
+      int2& p = c_edge2[size_t(j / 2) * nC + i];
+      (j & 1 ? p.y : p.x) = c_edge[size_t(j) * nC + i];
+    }
+  std::vector<int2> v_ce(size_t(3) * nV);
+  std::vector<double2> v_kite01(nV), v_af(nV);
+  for (int32_t v = 0; v < nV; ++v) {
+    for (int k = 0; k < 3; ++k)
+      v_ce[size_t(k) * nV + v] = make_int2(v_cell[size_t(k) * nV + v], v_edge[size_t(k) * nV + v]);
+    v_kite01[v] = make_double2(v_kite[v], v_kite[size_t(nV) + v]);
+    v_af[v] = make_double2(v_area[v], 0.0);  // f_v filled by set_fields
+  }
+  std::vector<double2> e_coef2;
+  if (!e_coef.empty()) {
+    e_coef2.assign(size_t((sten_max + 1) / 2) * nE, make_double2(0.0, 0.0));
+    for (int j = 0; j < sten_max; ++j)
+      for (int32_t e = 0; e < nE; ++e) {
+        double2& p = e_coef2[size_t(j / 2) * nE + e];
+        (j & 1 ? p.y : p.x) = e_coef[size_t(j) * nE + e];
+      }
+    e_coef.clear();
+  }
+  std::vector<uint2> e_st16p;
+  if (!e_st16.empty()) {
+    e_st16p.assign(size_t((n_words + 1) / 2) * nE, make_uint2(0u, 0u));
+    for (int k = 0; k < n_words; ++k)
+      for (int32_t e = 0; e < nE; ++e) {
+        uint2& p = e_st16p[size_t(k / 2) * nE + e];
+        (k & 1 ? p.y : p.x) = e_st16[size_t(k) * nE + e];
+      }
+  }
   cudaStream_t s = c->stream;
+  c->c_edge2.upload(c_edge2, s);
+  c->v_ce.upload(v_ce, s);
+  c->v_kite01.upload(v_kite01, s);
+  c->v_af.upload(v_af, s);
+  c->e_coef2.upload(e_coef2, s);
   c->c_edge.upload(c_edge, s);
   c->c_vert.upload(c_vert, s);
   c->c_nbr.upload(c_nbr, s);
@@ -1155,10 +1206,9 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   c->e_nst.upload(e_nst, s);
   c->e_slots.upload(e_slots, s);
   c->e_sten.upload(e_sten, s);
-  c->e_st16.upload(e_st16, s);
+  c->e_st16.upload(e_st16p, s);
   c->n_sten_wide = 0;
   for (const uint8_t x : e_nst) c->n_sten_wide += x >> 7;
-  c->e_coef.upload(e_coef, s);
   CK(cudaStreamSynchronize(s));  // host vectors die here
 
   // state + workspace, zero-initialised
@@ -2412,6 +2462,10 @@ int mswm_cuda_set_fields(mswm_cuda_ctx* c, const double* b, const double* f_vert
     if (!b || !f_vertex) throw Error(MSWM_E_USAGE, "null field");
     upload_field(c, c->b, b, c->c_new2old, c->nC);
     upload_field(c, c->f, f_vertex, c->v_new2old, c->nV);
+    if (c->nV) {  // (A_v, f_v) pairs of kernel A
+      k_fill_af<<<nblk(c->nV), kBlock, 0, c->stream>>>(c->nV, c->f.p, c->v_af.p);
+      CK(cudaGetLastError());
+    }
     c->gravity = gravity;
     c->have_fields = true;
     CK(cudaStreamSynchronize(c->stream));
