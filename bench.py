@@ -41,6 +41,31 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+def _rss_gb() -> float:
+    try:
+        with open("/proc/self/status") as fh:
+            for line in fh:
+                if line.startswith("VmRSS:"):
+                    return int(line.split()[1]) / 2**20
+    except OSError:
+        pass
+    return float("nan")
+
+
+def start_rss_monitor(period: float = 10.0) -> None:
+    """MSWM_BENCH_RSS=1: log this process's resident set every `period` s
+    (host-memory diagnosis of the largest configurations)."""
+    if os.environ.get("MSWM_BENCH_RSS") != "1":
+        return
+
+    def run():
+        while True:
+            log(f"[rss] {time.strftime('%H:%M:%S')} {_rss_gb():.1f} GB")
+            time.sleep(period)
+
+    threading.Thread(target=run, daemon=True).start()
+
+
 # ---------------------------------------------------------------------------
 # distributed plumbing
 
@@ -203,6 +228,35 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
+def _mem_available() -> float:
+    try:
+        with open("/proc/meminfo") as fh:
+            for line in fh:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024.0
+    except OSError:
+        pass
+    return float("inf")
+
+
+def ref_ranks(wl, threads: int):
+    """Rank count for the reference's ThreadedEvaluator that fits host RAM:
+    it allocates full-size h/u buffers plus scratch per block, 3 blocks per
+    rank (rank_pool.cpp:93-95), ~36 B per (cell + edge) per block (SURVEY.md
+    §8(d)).  Returns (ranks, note); ranks 0 = SerialEvaluator, None = does
+    not fit at all."""
+    per_block = 36.0 * (wl.mesh.n_cells + wl.mesh.n_edges)
+    avail = 0.5 * _mem_available()
+    fit = int(avail // (3 * per_block))
+    if threads > 1 and fit >= 2:
+        r = min(threads, fit)
+        return r, ("" if r == threads else
+                   f"; {r} of {threads} threads: more ranks would exceed host RAM")
+    if 3 * per_block <= avail:
+        return 0, "; SerialEvaluator: ranks would exceed host RAM"
+    return None, "reference needs more host RAM than this box has"
+
+
 def run_reference_arm(args, ws, rank):
     """--impl reference: the reference CPU path on this box's host cores."""
     if rank != 0:
@@ -214,9 +268,13 @@ def run_reference_arm(args, ws, rank):
     wl = make_workload(args.config)
     threads = cpu_threads()
     # the threaded evaluator on every host thread (the reference's parallel
-    # path); each timed "step" is one full LTS3 coarse step, and the number
-    # of timed steps is bounded so the arm ends within a few minutes
-    best = threads if threads > 1 else 0
+    # path) as far as host RAM allows; each timed "step" is one full LTS3
+    # coarse step, and the number of timed steps is bounded so the arm ends
+    # within a few minutes
+    best, note = ref_ranks(wl, threads)
+    if best is None:
+        print(json.dumps({"impl": "reference", "unavailable": f"{args.config}: {note}"}))
+        return
     cores = max(1, best)
     runner = RefRunner(wl, best)
     _, sps0, _ = runner.steps(1)  # warm-up (set caches), also sizes the sample
@@ -269,7 +327,7 @@ def run_ours(args, ws, rank, local):
         ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, device=local, order=args.order,
                           fine_mask=wl.fine_mask, interface_width=wl.width)
         rm = ctx.make_regions(wl.fine_mask, wl.width)
-        log(f"[rank {rank}] groups {rm.group_sizes()}")
+        log(f"[rank {rank}] groups {rm.group_sizes()} (host rss {_rss_gb():.1f} GB)")
         ctx.upload(State(wl.h, wl.u, 0.0))
         io_mesh = wl.mesh
     else:
@@ -388,18 +446,22 @@ def run_ours(args, ws, rank, local):
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         from oracle.oracle import ref_available
-        if ref_available():
-            # bounded sample: 1 warm-up + cpu_steps timed coarse steps with
-            # the reference's ThreadedEvaluator on every host thread
-            threads = cpu_threads()
+        # bounded sample: 1 warm-up + cpu_steps timed coarse steps with the
+        # reference's ThreadedEvaluator on every host thread (as far as host
+        # RAM allows)
+        threads, note = ref_ranks(wl, cpu_threads()) if ref_available() else (None, "")
+        if ref_available() and threads is None:
+            cpu = {"unavailable": f"{args.config}: {note}"}
+        elif ref_available():
             del ctx
-            runner = RefRunner(wl, threads if threads > 1 else 0)
+            runner = RefRunner(wl, threads)
             runner.steps(1)
             rate, sps, _ = runner.steps(args.cpu_steps)
             cpu = {"value": rate, "unit": UNIT, "cores": max(threads, 1), "kind": "reference",
                    "sample": f"{args.cpu_steps} LTS3 coarse step(s) of {args.config} after 1 "
-                             f"warm-up, reference ThreadedEvaluator {threads} ranks "
-                             f"({sps:.3f} s/step)"}
+                             f"warm-up, reference "
+                             f"{'SerialEvaluator' if threads == 0 else f'ThreadedEvaluator {threads} ranks'}"
+                             f" ({sps:.3f} s/step){note}"}
             if not args.no_rk4:
                 rrate, rsps, _ = runner.steps(1, scheme=2, dt=wl.dt / wl.M)
                 cpu["rk4_fine_dt"] = {"edge_evals_per_s": rrate, "s_per_step": rsps,
@@ -445,6 +507,7 @@ def main():
     ap.add_argument("--order", default="regions", choices=["regions", "hilbert", "input"],
                     help="device layout (results are bitwise independent of it)")
     args = ap.parse_args()
+    start_rss_monitor()
     if args.warmup < 3:
         log("note: warmup < 3 violates the timing rules; using 3")
         args.warmup = 3

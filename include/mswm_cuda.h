@@ -214,6 +214,11 @@ int mswm_cuda_layout_info(const mswm_cuda_ctx* ctx, int* kernel_path,
  * table instead (edges_on_edge, mesh.hpp:60-61). */
 int mswm_cuda_stencil_info(const mswm_cuda_ctx* ctx, int* offsets16, int64_t* n_wide);
 
+/* Phases B + C fused per cell tile (k_bc, opt-in MSWM_BC=1 at create,
+ * MSWM_BC_CELLS cells per tile): (F, q~, l) of each tile's edges and halo
+ * in shared memory; all zero when not in use. */
+int mswm_cuda_bc_info(const mswm_cuda_ctx* ctx, int* tile_cells, int* n_tiles, int64_t* smem);
+
 /* Dataflow evaluation (k_flow, opt-in with MSWM_FLOW=1 at create): large
  * masks run as one persistent launch over cell slabs of slab_cells cells;
  * all zero when disabled (the default, small meshes). */

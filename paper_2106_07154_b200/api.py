@@ -361,6 +361,12 @@ class CudaContext:
         self._check(self.lib.mswm_cuda_stencil_info(self.handle, C.byref(o), C.byref(n)))
         return {"offsets16": bool(o.value), "n_wide": n.value}
 
+    def bc_info(self) -> dict:
+        """Fused B + C tile path (k_bc): tile size, tiles, shared memory per CTA."""
+        tc, nt, sm = C.c_int(0), C.c_int(0), C.c_int64(0)
+        self._check(self.lib.mswm_cuda_bc_info(self.handle, C.byref(tc), C.byref(nt), C.byref(sm)))
+        return {"tile_cells": tc.value, "n_tiles": nt.value, "smem": sm.value}
+
     def flow_info(self) -> dict:
         """Dataflow evaluation (k_flow) parameters; slab_cells 0 = disabled."""
         v = [C.c_int(0) for _ in range(4)]

@@ -1323,3 +1323,110 @@ __global__ void k_mark_tiles(const int32_t* __restrict__ clist, int32_t nc,
 }
 
 }  // namespace mswm_dev
+
+namespace mswm_dev {
+
+// ---------------------------------------------------------------------------
+// Phases B + C fused per cell tile (opt-in MSWM_BC=1): (F, q~, l) of the edges
+// a tile needs live in shared memory instead of a round trip through HBM.
+// Tile t = cells [c0, c0+nc) and the edges whose lowest cell lies in them,
+// [e0, e0+ne) (edges are sorted by their cells); its halo = the other edges
+// its cells' rings and its edges' stencils read.  Local ids: owned edge e ->
+// e - e0, halo edge k -> ne + k.  Per-element operation order as
+// item_edge_fq / item_out_sp: bitwise the reference's.
+struct BcTile {
+  int32_t c0, nc, e0, ne, h_off, nh;
+};
+
+struct BcArgs {
+  const BcTile* tiles;
+  const int32_t* list;   // tiles holding outputs of this mask
+  int32_t ntiles;
+  const int32_t* halo;   // halo edge ids, per tile from h_off
+  const uint4* ring;     // [nC] local ids of the ring edges (u16 x 8)
+  const uint2* sten;     // [3][nE] local stencil ids, u16 pairs (as e_st16)
+};
+
+#ifndef MSWM_BC_MINB
+#define MSWM_BC_MINB 6
+#endif
+__global__ void __launch_bounds__(kBlock, MSWM_BC_MINB) k_bc(DevMesh M, BcArgs B,
+                                                               const double* __restrict__ h,
+                                                               const double* __restrict__ u,
+                                                               const double* __restrict__ pv,
+                                                               const double* __restrict__ psi,
+                                                               OutArgs a) {
+  extern __shared__ double2 sFQ[];
+  for (int32_t it = blockIdx.x; it < B.ntiles; it += gridDim.x) {
+    const BcTile T = B.tiles[B.list[it]];
+    const int32_t nl = T.ne + T.nh;
+    double* sL = reinterpret_cast<double*>(sFQ + nl);
+    // phase B on the tile's edges and halo (operators.cpp:61-62, :88-89)
+    for (int32_t k = threadIdx.x; k < nl; k += kBlock) {
+      const int32_t e = k < T.ne ? T.e0 + k : B.halo[T.h_off + k - T.ne];
+      const int2 c = M.e_cells[e];
+      const int2 v = M.e_verts[e];
+      const double F = 0.5 * (h[c.x] + h[c.y]) * u[e];
+      const double q = 0.5 * (pv[v.x] + pv[v.y]);
+      sFQ[k] = make_double2(F, q);
+      sL[k] = M.e_len[e];
+    }
+    __syncthreads();
+    // phase C: dh on the tile's cells, du on its edges, stage update fused
+    for (int32_t t = threadIdx.x; t < T.nc + T.ne; t += kBlock) {
+      if (t < T.nc) {
+        const int32_t i = T.c0 + t;
+        const int g = a.ckey ? a.ckey[i] : 0;
+        if (g > 5 || !((a.mask >> g) & 1u)) continue;
+        const int seg = g <= 2 ? 0 : 1;
+        const uint4 r = B.ring[i];
+        const uint32_t rw[4] = {r.x, r.y, r.z, r.w};
+        const int deg = M.c_deg[i];
+        const uint8_t sb = M.c_sbits[i];
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < kFastDeg; ++j) {
+          const int el = int(j & 1 ? rw[j >> 1] >> 16 : rw[j >> 1] & 0xFFFFu);
+          const double l = sL[el];
+          const double x = ((sb >> j) & 1 ? -l : l) * sFQ[el].x;
+          if (j < deg) acc += x;
+        }
+        apply_op(a.cop[seg], i, -acc / M.c_area[i]);
+      } else {
+        const int32_t k = t - T.nc;
+        const int32_t e = T.e0 + k;
+        const int g = a.ekey ? a.ekey[e] : 0;
+        if (g > 4 || !((a.mask >> (6 + g)) & 1u)) continue;
+        const int seg = g <= 1 ? 0 : 1;
+        const double qt_e = sFQ[k].y;
+        const double inv_d = M.e_invd[e];
+        const int2 cc = M.e_cells[e];
+        const int nst = M.e_nst[e] & 0x7f;
+        uint32_t w[kFastSten / 2 + 1];
+#pragma unroll
+        for (int q = 0; q < (kFastSten / 2 + 1) / 2; ++q) {
+          const uint2 p = B.sten[q * M.nE + e];
+          w[2 * q] = p.x;
+          w[2 * q + 1] = p.y;
+        }
+        double pvflux = 0.0;
+#pragma unroll
+        for (int j = 0; j < kFastSten; j += 2) {
+          const double2 cp = M.e_coef2[(j >> 1) * M.nE + e];
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            const int el = int(b ? w[j >> 1] >> 16 : w[j >> 1] & 0xFFFFu);
+            const double2 fq = sFQ[el];
+            const double x = (b ? cp.y : cp.x) * fq.x * (0.5 * (qt_e + fq.y));
+            if (j + b < nst) pvflux += x;
+          }
+        }
+        const double du = -pvflux - (psi[cc.x] - psi[cc.y]) * inv_d;
+        apply_op(a.eop[seg], e, du);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace mswm_dev

@@ -36,6 +36,7 @@
 #include <stdexcept>
 #include <string>
 #include <tuple>
+#include <type_traits>
 #include <vector>
 
 #include "kernels.cuh"
@@ -105,6 +106,21 @@ struct DArr {
 
 inline int nblk(int64_t n, int b = kBlock) { return int((n + b - 1) / b); }
 
+// MSWM_DEBUG_MEM=1: host resident set at setup milestones (stderr)
+void debug_mem(const char* what) {
+  static const bool on = [] {
+    const char* e = std::getenv("MSWM_DEBUG_MEM");
+    return e && e[0] == '1';
+  }();
+  if (!on) return;
+  long pages = 0, rss = 0;
+  if (FILE* f = std::fopen("/proc/self/statm", "r")) {
+    if (std::fscanf(f, "%ld %ld", &pages, &rss) != 2) rss = 0;
+    std::fclose(f);
+  }
+  std::fprintf(stderr, "[mswm mem] %-40s rss %.2f GB\n", what, double(rss) * 4096.0 / (1 << 30));
+}
+
 __global__ void k_fill_af(int32_t n, const double* __restrict__ f, double2* __restrict__ af) {
   const int32_t v = blockIdx.x * kBlock + threadIdx.x;
   if (v < n) af[v].y = f[v];
@@ -135,6 +151,8 @@ struct MaskPlan {
   DArr<uint32_t> vmask;  // closure bitmask for the dense dry-vertex check
   DArr<int32_t> tiles;   // fused path: tiles holding outputs of this mask
   int32_t ntiles = 0;
+  DArr<int32_t> bc_tiles;  // k_bc: cell tiles holding outputs of this mask
+  int32_t n_bc = 0;
   bool use_tiles = false;
   bool use_coop = false;  // small mask: one cooperative launch (k_fused_eval)
   bool use_flow = false;  // large mask: one dataflow launch (k_flow)
@@ -250,6 +268,14 @@ struct mswm_cuda_ctx {
   DArr<ushort2> t_er_vloc, t_oe_c1;
 
   int32_t n_tiles = 0, tile_cells = 0;
+  // phases B + C fused per cell tile (k_bc, opt-in MSWM_BC=1; see build_bc)
+  bool bc_ok = false;
+  int32_t bc_cells = 0, bc_ntiles = 0, bc_grid = 0;
+  size_t bc_smem = 0;
+  DArr<BcTile> bc_tiles;
+  DArr<int32_t> bc_halo, bc_e_tile;
+  DArr<uint4> bc_ring;
+  DArr<uint2> bc_sten;
   // L2-blocked slabs of the three-kernel path (see build_slabs)
   struct Slab {
     int32_t c0, nc, e0, ne, v0, nv;
@@ -534,6 +560,94 @@ void make_orders(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell_
   for (int32_t k = 0; k < nE && ident; ++k) ident = c->e_new2old[k] == k;
   for (int32_t k = 0; k < nV && ident; ++k) ident = c->v_new2old[k] == k;
   c->identity = ident;
+}
+
+// Cell tiles of k_bc (phases B + C fused): tile t = cells [t*TC, (t+1)*TC)
+// and the edges whose lowest cell lies in them (a contiguous range: edges
+// are sorted by their cells); the halo = the other edges the tile's rings
+// and stencils read.  Local ids are u16 (owned edges first, then the halo).
+// Needs hexagon/pentagon meshes (kFastDeg / kFastSten) and explicit tables.
+bool build_bc(mswm_cuda_ctx* c, const std::vector<int32_t>& c_edge,
+              const std::vector<uint8_t>& c_deg, const std::vector<int2>& e_cells,
+              const std::vector<int32_t>& e_sten, const std::vector<uint8_t>& e_nst) {
+  const int32_t nC = c->nC, nE = c->nE;
+  if (c->deg_max != kFastDeg || c->sten_max != kFastSten || e_sten.empty()) return false;
+  int32_t TC = 256;
+  if (const char* ts = std::getenv("MSWM_BC_CELLS")) TC = std::max(16, std::min(4096, std::atoi(ts)));
+  const int32_t nT = (nC + TC - 1) / TC;
+  std::vector<int32_t> e_tile(nE), e_first(size_t(nT) + 1, nE);
+  int32_t prev = -1;
+  for (int32_t e = 0; e < nE; ++e) {
+    const int32_t t = std::min(e_cells[e].x, e_cells[e].y) / TC;
+    if (t < prev) return false;
+    for (int32_t q = prev + 1; q <= t; ++q) e_first[q] = e;
+    prev = t;
+    e_tile[e] = t;
+  }
+  std::vector<BcTile> tiles(nT);
+  std::vector<int32_t> halo, emark(nE, -1), eloc(nE, 0), hl;
+  std::vector<uint4> ring(nC, make_uint4(0, 0, 0, 0));
+  std::vector<uint2> sten(size_t(3) * nE, make_uint2(0u, 0u));
+  size_t smem_max = 0;
+  for (int32_t t = 0; t < nT; ++t) {
+    BcTile& m = tiles[t];
+    m.c0 = t * TC;
+    m.nc = std::min(TC, nC - m.c0);
+    m.e0 = e_first[t];
+    m.ne = e_first[t + 1] - e_first[t];
+    for (int32_t e = m.e0; e < m.e0 + m.ne; ++e) {
+      emark[e] = t;
+      eloc[e] = e - m.e0;
+    }
+    hl.clear();
+    auto need = [&](int32_t e) {
+      if (emark[e] != t) {
+        emark[e] = t;
+        hl.push_back(e);
+      }
+    };
+    for (int32_t i = m.c0; i < m.c0 + m.nc; ++i)
+      for (int j = 0; j < c_deg[i]; ++j) need(c_edge[size_t(j) * nC + i]);
+    for (int32_t e = m.e0; e < m.e0 + m.ne; ++e)
+      for (int j = 0; j < (e_nst[e] & 0x7f); ++j) need(e_sten[size_t(j) * nE + e]);
+    std::sort(hl.begin(), hl.end());
+    if (m.ne + int64_t(hl.size()) > 65535) return false;
+    m.h_off = int32_t(halo.size());
+    m.nh = int32_t(hl.size());
+    for (size_t k = 0; k < hl.size(); ++k) {
+      eloc[hl[k]] = m.ne + int32_t(k);
+      halo.push_back(hl[k]);
+    }
+    for (int32_t i = m.c0; i < m.c0 + m.nc; ++i) {
+      uint32_t w[4] = {0, 0, 0, 0};
+      for (int j = 0; j < c_deg[i]; ++j)
+        w[j >> 1] |= uint32_t(eloc[c_edge[size_t(j) * nC + i]]) << (16 * (j & 1));
+      ring[i] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    for (int32_t e = m.e0; e < m.e0 + m.ne; ++e) {
+      uint32_t w[6] = {0, 0, 0, 0, 0, 0};
+      for (int j = 0; j < (e_nst[e] & 0x7f); ++j)
+        w[j >> 1] |= uint32_t(eloc[e_sten[size_t(j) * nE + e]]) << (16 * (j & 1));
+      for (int q = 0; q < 3; ++q) sten[size_t(q) * nE + e] = make_uint2(w[2 * q], w[2 * q + 1]);
+    }
+    smem_max = std::max(smem_max, size_t(m.ne + m.nh) * 24);
+  }
+  if (smem_max > 200 * 1024) return false;
+  cudaStream_t s = c->stream;
+  c->bc_tiles.upload(tiles, s);
+  c->bc_halo.upload(halo, s);
+  c->bc_e_tile.upload(e_tile, s);
+  c->bc_ring.upload(ring, s);
+  c->bc_sten.upload(sten, s);
+  CK(cudaFuncSetAttribute(k_bc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_max)));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bc, kBlock, smem_max));
+  c->bc_grid = std::max(1, per_sm) * c->n_sm;
+  c->bc_smem = smem_max;
+  c->bc_cells = TC;
+  c->bc_ntiles = nT;
+  CK(cudaStreamSynchronize(s));
+  return true;
 }
 
 // Is the caller's stencil the ring walk of mesh_build.cpp:133-154 with the
@@ -1100,8 +1214,10 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   std::vector<double> e_len(nE), e_ld(nE), e_dual(nE), e_invd(nE);
   std::vector<uint8_t> e_nst, e_slots;
   std::vector<int32_t> e_sten;
-  std::vector<uint32_t> e_st16;
-  std::vector<double> e_coef;
+  // built directly in their packed layouts (no int32 / f64 staging copies:
+  // C5's tables are ~10 GB each on the host)
+  std::vector<uint2> e_st16p;     // [(W+1)/2][nE] u32 word pairs, W = n_words
+  std::vector<double2> e_coef2;   // [(sten_max+1)/2][nE] coefficient pairs
   const int n_words = (std::max(sten_max, 1) + 1) / 2;
   // 16-bit stencil offsets (kernels.cuh item_out_sp); MSWM_ST16=0 keeps the
   // int32 table only (A/B runs)
@@ -1111,8 +1227,8 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   if (need_explicit) {
     e_nst.resize(nE);
     e_sten.assign(size_t(std::max(sten_max, 1)) * nE, 0);
-    e_coef.assign(size_t(std::max(sten_max, 1)) * nE, 0.0);
-    if (use16) e_st16.assign(size_t(n_words) * nE, 0u);
+    e_coef2.assign(size_t((std::max(sten_max, 1) + 1) / 2) * nE, make_double2(0.0, 0.0));
+    if (use16) e_st16p.assign(size_t((n_words + 1) / 2) * nE, make_uint2(0u, 0u));
   }
   for (int32_t ne = 0; ne < nE; ++ne) {
     const int32_t e = en[ne];
@@ -1137,78 +1253,77 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
       const int32_t dlt = eo[e2] - ne;
       if (dlt < INT16_MIN || dlt > INT16_MAX)
         e_nst[ne] |= 0x80;
-      else if (use16)
-        e_st16[size_t(j / 2) * nE + ne] |= (uint32_t(dlt) & 0xFFFFu) << (16 * (j & 1));
+      else if (use16) {
+        // entry j -> word j/2 (half j&1) -> pair word/2 (component word&1)
+        uint2& pw = e_st16p[size_t(j / 4) * nE + ne];
+        ((j / 2) & 1 ? pw.y : pw.x) |= (uint32_t(dlt) & 0xFFFFu) << (16 * (j & 1));
+      }
       // operators.cpp:109: weights[j] * (edge_len[e2] * inv_d), the first
       // two factors of the stencil term -- mesh constants.
-      e_coef[size_t(j) * nE + ne] = d->edge_weight[off + j] * (d->edge_len[e2] * inv_d);
+      double2& cp = e_coef2[size_t(j / 2) * nE + ne];
+      (j & 1 ? cp.y : cp.x) = d->edge_weight[off + j] * (d->edge_len[e2] * inv_d);
     }
-  }
-  // packed copies (kernels.cuh DevMesh): pairs of slots / entries per load
-  std::vector<int2> c_edge2(size_t((deg_max + 1) / 2) * nC, make_int2(0, 0));
-  for (int j = 0; j < deg_max; ++j)
-    for (int32_t i = 0; i < nC; ++i) {
-      int2& p = c_edge2[size_t(j / 2) * nC + i];
-      (j & 1 ? p.y : p.x) = c_edge[size_t(j) * nC + i];
-    }
-  std::vector<int2> v_ce(size_t(3) * nV);
-  std::vector<double2> v_kite01(nV), v_af(nV);
-  for (int32_t v = 0; v < nV; ++v) {
-    for (int k = 0; k < 3; ++k)
-      v_ce[size_t(k) * nV + v] = make_int2(v_cell[size_t(k) * nV + v], v_edge[size_t(k) * nV + v]);
-    v_kite01[v] = make_double2(v_kite[v], v_kite[size_t(nV) + v]);
-    v_af[v] = make_double2(v_area[v], 0.0);  // f_v filled by set_fields
-  }
-  std::vector<double2> e_coef2;
-  if (!e_coef.empty()) {
-    e_coef2.assign(size_t((sten_max + 1) / 2) * nE, make_double2(0.0, 0.0));
-    for (int j = 0; j < sten_max; ++j)
-      for (int32_t e = 0; e < nE; ++e) {
-        double2& p = e_coef2[size_t(j / 2) * nE + e];
-        (j & 1 ? p.y : p.x) = e_coef[size_t(j) * nE + e];
-      }
-    e_coef.clear();
-  }
-  std::vector<uint2> e_st16p;
-  if (!e_st16.empty()) {
-    e_st16p.assign(size_t((n_words + 1) / 2) * nE, make_uint2(0u, 0u));
-    for (int k = 0; k < n_words; ++k)
-      for (int32_t e = 0; e < nE; ++e) {
-        uint2& p = e_st16p[size_t(k / 2) * nE + e];
-        (k & 1 ? p.y : p.x) = e_st16[size_t(k) * nE + e];
-      }
   }
   cudaStream_t s = c->stream;
-  c->c_edge2.upload(c_edge2, s);
-  c->v_ce.upload(v_ce, s);
-  c->v_kite01.upload(v_kite01, s);
-  c->v_af.upload(v_af, s);
-  c->e_coef2.upload(e_coef2, s);
-  c->c_edge.upload(c_edge, s);
-  c->c_vert.upload(c_vert, s);
-  c->c_nbr.upload(c_nbr, s);
-  c->c_deg.upload(c_deg, s);
-  c->c_sbits.upload(c_sbits, s);
-  c->c_area.upload(c_area, s);
-  c->c_ratio.upload(c_ratio, s);
-  c->v_cell.upload(v_cell, s);
-  c->v_edge.upload(v_edge, s);
-  c->v_orig.upload(v_orig, s);
-  c->v_kite.upload(v_kite, s);
-  c->v_area.upload(v_area, s);
-  c->v_sbits.upload(v_sbits, s);
-  c->e_cells.upload(e_cells, s);
-  c->e_verts.upload(e_verts, s);
-  c->e_len.upload(e_len, s);
-  c->e_ld.upload(e_ld, s);
-  c->e_dual.upload(e_dual, s);
-  c->e_invd.upload(e_invd, s);
-  c->e_nst.upload(e_nst, s);
-  c->e_slots.upload(e_slots, s);
-  c->e_sten.upload(e_sten, s);
-  c->e_st16.upload(e_st16p, s);
+  // upload, then release the host copy at once (C5's tables total tens of GB
+  // on the host; keeping them all alive until the end ran the box out of
+  // memory)
+  auto put = [&](auto& dst, auto& vec) {
+    dst.upload(vec, s);
+    CK(cudaStreamSynchronize(s));
+    std::remove_reference_t<decltype(vec)>().swap(vec);
+  };
+  put(c->e_coef2, e_coef2);
   c->n_sten_wide = 0;
   for (const uint8_t x : e_nst) c->n_sten_wide += x >> 7;
+  put(c->e_st16, e_st16p);
+  if (const char* bc = std::getenv("MSWM_BC"))
+    if (bc[0] == '1' && !c->tile_path && !c->ring_derived && !c->hybrid)
+      c->bc_ok = build_bc(c, c_edge, c_deg, e_cells, e_sten, e_nst);
+  put(c->e_sten, e_sten);
+  put(c->e_nst, e_nst);
+  {
+    // packed copies (kernels.cuh DevMesh): pairs of slots / entries per load
+    std::vector<int2> c_edge2(size_t((deg_max + 1) / 2) * nC, make_int2(0, 0));
+    for (int j = 0; j < deg_max; ++j)
+      for (int32_t i = 0; i < nC; ++i) {
+        int2& p = c_edge2[size_t(j / 2) * nC + i];
+        (j & 1 ? p.y : p.x) = c_edge[size_t(j) * nC + i];
+      }
+    put(c->c_edge2, c_edge2);
+    std::vector<int2> v_ce(size_t(3) * nV);
+    for (int32_t v = 0; v < nV; ++v)
+      for (int k = 0; k < 3; ++k)
+        v_ce[size_t(k) * nV + v] = make_int2(v_cell[size_t(k) * nV + v], v_edge[size_t(k) * nV + v]);
+    put(c->v_ce, v_ce);
+    std::vector<double2> v_kite01(nV), v_af(nV);
+    for (int32_t v = 0; v < nV; ++v) {
+      v_kite01[v] = make_double2(v_kite[v], v_kite[size_t(nV) + v]);
+      v_af[v] = make_double2(v_area[v], 0.0);  // f_v filled by set_fields
+    }
+    put(c->v_kite01, v_kite01);
+    put(c->v_af, v_af);
+  }
+  put(c->c_edge, c_edge);
+  put(c->c_vert, c_vert);
+  put(c->c_nbr, c_nbr);
+  put(c->c_deg, c_deg);
+  put(c->c_sbits, c_sbits);
+  put(c->c_area, c_area);
+  put(c->c_ratio, c_ratio);
+  put(c->v_cell, v_cell);
+  put(c->v_edge, v_edge);
+  put(c->v_orig, v_orig);
+  put(c->v_kite, v_kite);
+  put(c->v_area, v_area);
+  put(c->v_sbits, v_sbits);
+  put(c->e_cells, e_cells);
+  put(c->e_verts, e_verts);
+  put(c->e_len, e_len);
+  put(c->e_ld, e_ld);
+  put(c->e_dual, e_dual);
+  put(c->e_invd, e_invd);
+  put(c->e_slots, e_slots);
   CK(cudaStreamSynchronize(s));  // host vectors die here
 
   // state + workspace, zero-initialised
@@ -1333,6 +1448,7 @@ MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
   if (mask & ~unsigned(MSWM_MASK_ALL)) throw Error(MSWM_E_USAGE, "mask has unknown group bits");
   auto p = std::make_unique<MaskPlan>();
   p->mask = mask;
+  debug_mem("plan_for: start");
   cudaStream_t s = c->stream;
   if (!c->have_regions) {
     // integrators.cpp:139-142
@@ -1404,6 +1520,7 @@ MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
   p->nk = int32_t(compact(c, key.p, c->nC, 1, p->kclos)[0]);
   k_flag_key<<<nblk(c->nV), kBlock, 0, s>>>(c->nV, mv.p, key.p);
   p->nv = int32_t(compact(c, key.p, c->nV, 1, p->vclos)[0]);
+  debug_mem("plan_for: closures");
   p->dense_v = p->nv >= int64_t(c->nV) * 85 / 100;
   p->dense_k = p->nk >= int64_t(c->nC) * 85 / 100;
   p->dense_fq = p->nec >= int64_t(c->nE) * 85 / 100;
@@ -1413,6 +1530,7 @@ MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
   make_span(c, p->eclos.p, p->nec, c->nE, 0.85, p->se);
   make_span(c, p->cells, p->nc, c->nC, 0.5, p->sc_out);
   make_span(c, p->edges, p->ne, c->nE, 0.5, p->se_out);
+  debug_mem("plan_for: spans");
   // supersets need the closure bitmask for the dry check
   if (p->sv.n() > p->nv) p->dense_v = true;
   p->use_coop = c->coop_blocks > 0 && !c->tile_path &&
@@ -1457,6 +1575,20 @@ MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
     k_flag_key<<<nblk(c->n_tiles), kBlock, 0, s>>>(c->n_tiles, tflag.p, key.p);
     p->ntiles = int32_t(compact(c, key.p, c->n_tiles, 1, p->tiles)[0]);
   }
+  if (c->bc_ok && !p->use_tiles && !p->use_coop && !p->use_flow) {
+    DArr<uint8_t> tflag, key;
+    tflag.alloc(size_t(c->bc_ntiles));
+    tflag.zero(s);
+    key.alloc(size_t(c->bc_ntiles));
+    if (int64_t(p->nc) + p->ne > 0) {
+      k_mark_tiles<<<nblk(int64_t(p->nc) + p->ne), kBlock, 0, s>>>(p->cells, p->nc, p->edges, p->ne,
+                                                                  c->bc_e_tile.p, tflag.p,
+                                                                  c->bc_cells);
+      CK(cudaGetLastError());
+    }
+    k_flag_key<<<nblk(c->bc_ntiles), kBlock, 0, s>>>(c->bc_ntiles, tflag.p, key.p);
+    p->n_bc = int32_t(compact(c, key.p, c->bc_ntiles, 1, p->bc_tiles)[0]);
+  }
   if (p->dense_v && p->nv < c->nV) {
     p->vmask.alloc((size_t(c->nV) + 31) / 32);
     k_pack_bits<<<nblk((int64_t(c->nV) + 31) / 32), kBlock, 0, s>>>(c->nV, mv.p, p->vmask.p);
@@ -1476,6 +1608,7 @@ MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
   }
   auto& slot = c->plans[mask];
   slot = std::move(p);
+  debug_mem("plan_for: done");
   return *slot;
 }
 
@@ -1690,6 +1823,29 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
                                                  c->dry_vertex.p, p.vmask.p);
     CK(cudaGetLastError());
     ++c->launches;
+  }
+  if (p.n_bc > 0) {
+    BcArgs B;
+    B.tiles = c->bc_tiles.p;
+    B.list = p.bc_tiles.p;
+    B.ntiles = p.n_bc;
+    B.halo = c->bc_halo.p;
+    B.ring = c->bc_ring.p;
+    B.sten = c->bc_sten.p;
+    OutArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.mask = p.mask;
+    a.ckey = c->have_regions ? c->ckey.p : nullptr;
+    a.ekey = c->have_regions ? c->ekey.p : nullptr;
+    a.cop[0] = cop[0];
+    a.cop[1] = cop[1];
+    a.eop[0] = eop[0];
+    a.eop[1] = eop[1];
+    k_bc<<<std::min(p.n_bc, c->bc_grid), kBlock, c->bc_smem, s>>>(M, B, h, u, c->pv.p, c->K.p, a);
+    CK(cudaGetLastError());
+    ++c->launches;
+    if (rec) CK(cudaEventRecordWithFlags(rec->stop, s, cudaEventRecordExternal));
+    return;
   }
   if (p.se.n() > 0) {
     k_edge_fq<<<sgrid(c, p.se.n(), 1), kBlock, 0, s>>>(M, h, u, c->pv.p, es, c->FQ.p);
@@ -2253,6 +2409,7 @@ mswm_cuda_ctx::Graph capture_step(std::vector<mswm_cuda_ctx*>& cs, cudaStream_t 
     c->launches = 0;
   }
   cs[0]->capture_records = profile ? &gr.records : nullptr;
+  debug_mem("capture_step: plans built");
   CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
   try {
     enqueue_step(cs, scheme, dt, M);
@@ -2271,7 +2428,9 @@ mswm_cuda_ctx::Graph capture_step(std::vector<mswm_cuda_ctx*>& cs, cudaStream_t 
     c->capture_records = nullptr;
   }
   CK(cudaStreamEndCapture(stream, &g));
+  debug_mem("capture_step: captured");
   cudaError_t e = cudaGraphInstantiate(&gr.exec, g, 0);
+  debug_mem("capture_step: instantiated");
   cudaGraphDestroy(g);
   if (e != cudaSuccess) throw Error(MSWM_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
   return gr;
@@ -2696,6 +2855,14 @@ int mswm_cuda_stencil_info(const mswm_cuda_ctx* c, int* offsets16, int64_t* n_wi
   if (!c) return MSWM_E_USAGE;
   if (offsets16) *offsets16 = c->e_st16.p ? 1 : 0;
   if (n_wide) *n_wide = c->n_sten_wide;
+  return MSWM_OK;
+}
+
+int mswm_cuda_bc_info(const mswm_cuda_ctx* c, int* tile_cells, int* n_tiles, int64_t* smem) {
+  if (!c) return MSWM_E_USAGE;
+  if (tile_cells) *tile_cells = c->bc_ok ? c->bc_cells : 0;
+  if (n_tiles) *n_tiles = c->bc_ok ? c->bc_ntiles : 0;
+  if (smem) *smem = c->bc_ok ? int64_t(c->bc_smem) : 0;
   return MSWM_OK;
 }
 

@@ -489,6 +489,34 @@ def test_wide_interfaces_bitwise(width):
             assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref), (order, scheme)
 
 
+@pytest.mark.parametrize("cells", ["256", "64"])
+def test_fused_bc_tiles_bitwise(cells, monkeypatch):
+    """Phases B + C fused per cell tile (k_bc, (F, q~, l) in shared memory):
+    every LTS3 mask and LTS3 / RK4 steps bitwise equal to the oracle."""
+    monkeypatch.setenv("MSWM_BC", "1")
+    monkeypatch.setenv("MSWM_BC_CELLS", cells)
+    wl = W.small_sphere(6, seed=37, cap_deg=25.0)
+    o = _oracle_for(wl)
+    ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order="regions", fine_mask=wl.fine_mask)
+    info = ctx.bc_info()
+    assert info["tile_cells"] == int(cells) and info["n_tiles"] > 0
+    ctx.make_regions(wl.fine_mask, wl.width)
+    ev = CudaEvaluator(ctx)
+    for mask in LTS3_MASKS:
+        dh1 = np.full(wl.mesh.n_cells, SENTINEL)
+        du1 = np.full(wl.mesh.n_edges, SENTINEL)
+        dh2, du2 = dh1.copy(), du1.copy()
+        ev.eval(wl.h, wl.u, mask, dh1, du1)
+        o.eval(wl.h, wl.u, mask, dh2, du2)
+        assert bits_equal(dh1, dh2) and bits_equal(du1, du2)
+    for scheme, n, dt in [(Scheme.LTS3, 3, wl.dt), (Scheme.RK4, 2, wl.dt / wl.M)]:
+        h_ref, u_ref, _ = o.step(int(scheme), wl.h, wl.u, 0.0, dt, wl.M, n)
+        ctx.upload(State(wl.h, wl.u, 0.0))
+        ctx.advance(scheme, dt, wl.M, n)
+        st = ctx.download()
+        assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref), scheme
+
+
 @pytest.mark.parametrize("st16", ["1", "0"])
 def test_stencil_offsets16_bitwise(st16, monkeypatch):
     """16-bit stencil offsets (default) with edges whose offsets overflow
