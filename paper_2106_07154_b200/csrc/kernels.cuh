@@ -136,9 +136,16 @@ struct Op {
   double* acc;
   const double* a1;
   const double* a2;
+  // elements whose bit is set in altbits are written to alt[i] instead of
+  // dst[i] (null altbits: never) -- the concurrent coarse step of the LTS3
+  // schedule parks the values the substeps still read as h_old
+  double* alt;
+  const uint32_t* altbits;
 };
 
-__device__ __forceinline__ void apply_op(const Op& op, int32_t i, double d) {
+__device__ __forceinline__ void apply_op(const Op& op_in, int32_t i, double d) {
+  Op op = op_in;
+  if (op.altbits && ((op.altbits[i >> 5] >> (i & 31)) & 1u)) op.dst = op.alt;
   switch (op.kind) {
     case OP_STORE:
       op.dst[i] = d;
@@ -1426,6 +1433,26 @@ __global__ void __launch_bounds__(kBlock, MSWM_BC_MINB) k_bc(DevMesh M, BcArgs B
       }
     }
     __syncthreads();
+  }
+}
+
+}  // namespace mswm_dev
+
+namespace mswm_dev {
+
+// Move the parked coarse values of the concurrent LTS3 coarse step into the
+// state (see Op::alt): dst[i] = src[i] on the band lists.
+__global__ void k_copy_band(const int32_t* __restrict__ cl, int32_t nc,
+                            const double* __restrict__ hsrc, double* __restrict__ hdst,
+                            const int32_t* __restrict__ el, int32_t ne,
+                            const double* __restrict__ usrc, double* __restrict__ udst) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nc) {
+    const int32_t i = cl[t];
+    hdst[i] = hsrc[i];
+  } else if (t - nc < ne) {
+    const int32_t e = el[t - nc];
+    udst[e] = usrc[e];
   }
 }
 

@@ -299,6 +299,20 @@ struct mswm_cuda_ctx {
   DArr<double> Dh, Du;              // eval ABI outputs
   DArr<double> pv, K;
   DArr<double2> FQ;
+  // concurrent LTS3 coarse step (enqueue_lts3, MSWM_FORK): a second launch
+  // stream, its own intermediates, and the "band" -- coarse elements the
+  // substep evaluations read as h_old, which the coarse step parks in
+  // T1h / T1u until the substeps are done
+  cudaStream_t ls2 = nullptr, lsh = nullptr;  // coarse step (low), substeps (high priority)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join_h = nullptr;
+  int fork_ctas = 6;  // resident CTAs per SM of the concurrent coarse step
+  DArr<double> pv2, K2;
+  DArr<double2> FQ2;
+  DArr<uint32_t> band_cbits, band_ebits;
+  DArr<int32_t> band_cells, band_edges;
+  int32_t n_band_c = 0, n_band_e = 0;
+  int fork_state = 0;  // 0 not prepared, 1 ready, -1 not eligible
+  cudaStream_t stream_of_capture = nullptr;
   DArr<int32_t> d_c_n2o, d_e_n2o;  // internal -> original ids (device permutes)
   DArr<double> io_h, io_u;          // staging for permuted uploads / downloads
   double time = 0.0;
@@ -353,6 +367,11 @@ struct mswm_cuda_ctx {
   ~mswm_cuda_ctx() {
     drop_graphs();
     if (nccl_comm) nccl().CommDestroy(nccl_comm);
+    if (ls2) cudaStreamDestroy(ls2);
+    if (lsh) cudaStreamDestroy(lsh);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (ev_join_h) cudaEventDestroy(ev_join_h);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -1391,6 +1410,7 @@ bool read_dry(mswm_cuda_ctx* c) {
 void invalidate(mswm_cuda_ctx* c) {
   c->plans.clear();
   c->drop_graphs();
+  c->fork_state = 0;  // the band depends on the plans
 }
 
 // Launch set for a sorted id list: its longest run of consecutive ids as a
@@ -1630,9 +1650,26 @@ Op op_none() {
   return o;
 }
 
+// Where a launch_eval goes: stream and intermediates (null: the context's).
+struct Side {
+  cudaStream_t s;
+  double* pv;
+  double* K;
+  double2* FQ;
+  int ctas_per_sm;  // resident-grid size of the streamed kernels (0: default)
+};
+
 void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const double* u,
-                 const Op cop[2], const Op eop[2], const PredArgs* pred = nullptr) {
-  cudaStream_t s = c->ls;
+                 const Op cop[2], const Op eop[2], const PredArgs* pred = nullptr,
+                 const Side* side = nullptr) {
+  cudaStream_t s = side ? side->s : c->ls;
+  double* const pv = side ? side->pv : c->pv.p;
+  double* const Kp = side ? side->K : c->K.p;
+  double2* const FQ = side ? side->FQ : c->FQ.p;
+  auto grid = [&](int64_t n, int kernel) {
+    const int g = sgrid(c, n, kernel);
+    return side && side->ctas_per_sm > 0 ? std::min(g, side->ctas_per_sm * c->n_sm) : g;
+  };
   if (pred && !(p.use_coop && !p.use_tiles) && int64_t(pred->nc) + pred->ne > 0) {
     k_predict<<<nblk(int64_t(pred->nc) + pred->ne), kBlock, 0, s>>>(
         pred->clist, pred->nc, pred->elist, pred->ne, pred->c0, pred->c1, pred->c2, pred->hs0,
@@ -1819,7 +1856,7 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
     return;
   }
   if (na > 0) {
-    k_vertex_cell<<<sgrid(c, na, 0), kBlock, 0, s>>>(M, h, u, vs, ks, c->pv.p, c->K.p,
+    k_vertex_cell<<<grid(na, 0), kBlock, 0, s>>>(M, h, u, vs, ks, pv, Kp,
                                                  c->dry_vertex.p, p.vmask.p);
     CK(cudaGetLastError());
     ++c->launches;
@@ -1841,14 +1878,14 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
     a.cop[1] = cop[1];
     a.eop[0] = eop[0];
     a.eop[1] = eop[1];
-    k_bc<<<std::min(p.n_bc, c->bc_grid), kBlock, c->bc_smem, s>>>(M, B, h, u, c->pv.p, c->K.p, a);
+    k_bc<<<std::min(p.n_bc, c->bc_grid), kBlock, c->bc_smem, s>>>(M, B, h, u, pv, Kp, a);
     CK(cudaGetLastError());
     ++c->launches;
     if (rec) CK(cudaEventRecordWithFlags(rec->stop, s, cudaEventRecordExternal));
     return;
   }
   if (p.se.n() > 0) {
-    k_edge_fq<<<sgrid(c, p.se.n(), 1), kBlock, 0, s>>>(M, h, u, c->pv.p, es, c->FQ.p);
+    k_edge_fq<<<grid(p.se.n(), 1), kBlock, 0, s>>>(M, h, u, pv, es, FQ);
     CK(cudaGetLastError());
     ++c->launches;
   }
@@ -1865,7 +1902,7 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
     a.cop[1] = cop[1];
     a.eop[0] = eop[0];
     a.eop[1] = eop[1];
-    k_out<<<sgrid(c, nout, 2), kBlock, 0, s>>>(M, h, c->K.p, c->FQ.p, a);
+    k_out<<<grid(nout, 2), kBlock, 0, s>>>(M, h, Kp, FQ, a);
     CK(cudaGetLastError());
     ++c->launches;
   }
@@ -2072,6 +2109,77 @@ void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us, unsigned ma
 
 // One LTS3 coarse step (see the file header for the aliasing argument) for
 // every rank context of the executor.
+// The LTS3 coarse step (step 4) runs concurrently with the substeps when
+// one context steps alone on the streamed path: it reads (h2, u2) only on
+// coarse and interface-2 elements and h_old only on its own outputs, none of
+// which the substeps write; the substeps read h_old on a thin band of
+// coarse elements next to interface 2, which step 4 therefore writes to
+// T1h / T1u (Op::alt) and k_copy_band moves into the state after the join.
+// Separate intermediates (pv2, K2, FQ2) keep the two evaluations apart.
+// MSWM_FORK=0 keeps the sequential order.  Bitwise either way (evaluations
+// are pure functions of their inputs).
+void prepare_fork(mswm_cuda_ctx* c) {
+  if (c->fork_state != 0) return;
+  c->fork_state = -1;
+  const char* fe = std::getenv("MSWM_FORK");
+  if ((fe && fe[0] == '0') || c->halo.active() || !c->have_regions) return;
+  MaskPlan& ps = plan_for(c, kMaskSub);
+  MaskPlan& pc = plan_for(c, kMaskCoarseOnly);
+  if (pc.use_tiles || pc.use_coop || pc.use_flow || ps.use_flow || !c->slabs.empty()) return;
+  if (const char* fc = std::getenv("MSWM_FORK_CTAS")) c->fork_ctas = std::max(0, std::atoi(fc));
+  cudaStream_t s = c->stream;
+  DArr<uint8_t> cr, er;
+  cr.alloc(c->nC);
+  er.alloc(c->nE);
+  cr.zero(s);
+  er.zero(s);
+  const int64_t n = int64_t(ps.nv) + ps.nk + ps.nf + ps.ne;
+  if (n > 0) {
+    k_mark_reads<<<nblk(n), kBlock, 0, s>>>(c->dev(), ps.vclos.p, ps.nv, ps.kclos.p, ps.nk,
+                                            ps.fclos.p, ps.nf, ps.edges, ps.ne, cr.p, er.p);
+    CK(cudaGetLastError());
+  }
+  std::vector<uint8_t> hc(c->nC), he(c->nE), kc(c->nC), ke(c->nE);
+  CK(cudaMemcpyAsync(hc.data(), cr.p, size_t(c->nC), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(he.data(), er.p, size_t(c->nE), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(kc.data(), c->ckey.p, size_t(c->nC), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(ke.data(), c->ekey.p, size_t(c->nE), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  std::vector<int32_t> bc, be;
+  std::vector<uint32_t> cb((size_t(c->nC) + 31) / 32, 0u), eb((size_t(c->nE) + 31) / 32, 0u);
+  for (int32_t i = 0; i < c->nC; ++i)
+    if (hc[i] && kc[i] == 5) {  // read by a substep, written by step 4 (coarse)
+      bc.push_back(i);
+      cb[i >> 5] |= 1u << (i & 31);
+    }
+  for (int32_t e = 0; e < c->nE; ++e)
+    if (he[e] && ke[e] == 4) {
+      be.push_back(e);
+      eb[e >> 5] |= 1u << (e & 31);
+    }
+  c->band_cbits.upload(cb, s);
+  c->band_ebits.upload(eb, s);
+  c->band_cells.upload(bc, s);
+  c->band_edges.upload(be, s);
+  c->n_band_c = int32_t(bc.size());
+  c->n_band_e = int32_t(be.size());
+  c->pv2.alloc(c->nV);
+  c->pv2.zero(s);
+  c->K2.alloc(c->nC);
+  c->K2.zero(s);
+  c->FQ2.alloc(c->nE);
+  c->FQ2.zero(s);
+  int lo = 0, hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  if (!c->ls2) CK(cudaStreamCreateWithPriority(&c->ls2, cudaStreamNonBlocking, lo));
+  if (!c->lsh) CK(cudaStreamCreateWithPriority(&c->lsh, cudaStreamNonBlocking, hi));
+  if (!c->ev_fork) CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  if (!c->ev_join) CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  if (!c->ev_join_h) CK(cudaEventCreateWithFlags(&c->ev_join_h, cudaEventDisableTiming));
+  CK(cudaStreamSynchronize(s));
+  c->fork_state = 1;
+}
+
 void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
   const double delta = dt / M;
   bool fuse_pred = true;
@@ -2094,6 +2202,30 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
     Op co[2] = {mk_op(OP_WCOMB, H2, H, 0.75, H1, 0.25, cr), mk_op(OP_WCOMB, H2, H, 0.75, H1, 0.25, cr)};
     Op eo[2] = {mk_op(OP_WCOMB, U2, U, 0.75, U1, 0.25, cr), mk_op(OP_WCOMB, U2, U, 0.75, U1, 0.25, cr)};
     launch_eval(c, plan_for(c, kMaskIfCoarse), H1, U1, co, eo);
+  }
+  // Step 4 forked onto the second stream (prepare_fork)
+  const bool fork = cs.size() == 1 && cs[0]->fork_state == 1;
+  if (fork) {
+    mswm_cuda_ctx* c = cs[0];
+    c->stream_of_capture = c->ls;
+    CK(cudaEventRecord(c->ev_fork, c->ls));
+    CK(cudaStreamWaitEvent(c->ls2, c->ev_fork, 0));
+    const double cr = two3 * dt;
+    double *H = c->H.p, *U = c->U.p, *H2 = c->H2.p, *U2 = c->U2.p;
+    Op co = mk_op(OP_WCOMB, H, H, third, H2, two3, cr);
+    Op eo = mk_op(OP_WCOMB, U, U, third, U2, two3, cr);
+    co.alt = c->T1h.p;
+    co.altbits = c->band_cbits.p;
+    eo.alt = c->T1u.p;
+    eo.altbits = c->band_ebits.p;
+    Op cos[2] = {co, co}, eos[2] = {eo, eo};
+    const Side side{c->ls2, c->pv2.p, c->K2.p, c->FQ2.p, c->fork_ctas};
+    launch_eval(c, plan_for(c, kMaskCoarseOnly), H2, U2, cos, eos, nullptr, &side);
+    CK(cudaEventRecord(c->ev_join, c->ls2));
+    // the substeps on the high-priority stream: their CTAs take SM slots
+    // ahead of the coarse step's as slots free up
+    CK(cudaStreamWaitEvent(c->lsh, c->ev_fork, 0));
+    c->ls = c->lsh;
   }
   // Substep prologue: save I1 u I2 old values, I1 stage values, predict
   // stage 1 of substep 0 into the state (ha == state).
@@ -2167,6 +2299,21 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
   // With full halos the H2/U2 copies are current (the last exchange
   // refreshed them; only fine/I1 entries, never read here, changed since);
   // restricted halos refreshed only the substep's read set.
+  if (fork) {
+    mswm_cuda_ctx* c = cs[0];
+    CK(cudaEventRecord(c->ev_join_h, c->lsh));
+    c->ls = c->stream_of_capture;
+    CK(cudaStreamWaitEvent(c->ls, c->ev_join_h, 0));
+    CK(cudaStreamWaitEvent(c->ls, c->ev_join, 0));
+    const int64_t nb = int64_t(c->n_band_c) + c->n_band_e;
+    if (nb > 0) {
+      k_copy_band<<<nblk(nb), kBlock, 0, c->ls>>>(c->band_cells.p, c->n_band_c, c->T1h.p, c->H.p,
+                                                  c->band_edges.p, c->n_band_e, c->T1u.p, c->U.p);
+      CK(cudaGetLastError());
+      ++c->launches;
+    }
+    return;
+  }
   if (restricted(cs)) exchange(cs, &C::H2, &C::U2, kMaskCoarseOnly);
   for (auto* c : cs) {
     const double cr = two3 * dt;
@@ -2398,6 +2545,7 @@ mswm_cuda_ctx::Graph capture_step(std::vector<mswm_cuda_ctx*>& cs, cudaStream_t 
       plan_for(c, kMaskIfCoarse);
       plan_for(c, kMaskSub);
       plan_for(c, kMaskCoarseOnly);
+      if (scheme == MSWM_LTS3 && cs.size() == 1) prepare_fork(c);
     } else {
       plan_for(c, MSWM_MASK_ALL);
     }
@@ -2429,7 +2577,8 @@ mswm_cuda_ctx::Graph capture_step(std::vector<mswm_cuda_ctx*>& cs, cudaStream_t 
   }
   CK(cudaStreamEndCapture(stream, &g));
   debug_mem("capture_step: captured");
-  cudaError_t e = cudaGraphInstantiate(&gr.exec, g, 0);
+  // per-node priorities (the concurrent coarse step / substeps, enqueue_lts3)
+  cudaError_t e = cudaGraphInstantiate(&gr.exec, g, cudaGraphInstantiateFlagUseNodePriority);
   debug_mem("capture_step: instantiated");
   cudaGraphDestroy(g);
   if (e != cudaSuccess) throw Error(MSWM_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));

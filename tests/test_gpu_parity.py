@@ -489,6 +489,25 @@ def test_wide_interfaces_bitwise(width):
             assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref), (order, scheme)
 
 
+@pytest.mark.parametrize("fork", ["1", "0"])
+@pytest.mark.parametrize("order", ["regions", "hilbert"])
+def test_concurrent_coarse_step_bitwise(fork, order, monkeypatch):
+    """LTS3 with the coarse step (step 4) on a second stream concurrent with
+    the substeps (default) and in sequence (MSWM_FORK=0): bitwise equal to
+    the oracle over several coarse steps, M = 2 and 4."""
+    monkeypatch.setenv("MSWM_FORK", fork)
+    wl = W.small_sphere(6, seed=41, cap_deg=25.0)
+    o = _oracle_for(wl)
+    ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order, fine_mask=wl.fine_mask)
+    ctx.make_regions(wl.fine_mask, wl.width)
+    for M in (4, 2):
+        h_ref, u_ref, _ = o.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, M, 5)
+        ctx.upload(State(wl.h, wl.u, 0.0))
+        ctx.advance(Scheme.LTS3, wl.dt, M, 5)
+        st = ctx.download()
+        assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref), M
+
+
 @pytest.mark.parametrize("cells", ["256", "64"])
 def test_fused_bc_tiles_bitwise(cells, monkeypatch):
     """Phases B + C fused per cell tile (k_bc, (F, q~, l) in shared memory):
