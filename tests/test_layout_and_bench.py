@@ -59,3 +59,23 @@ def test_bench_ours_fails_loudly_without_gpu():
     r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--config", "c1", "--steps", "2"],
                        capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert r.returncode != 0 and "CUDA" in (r.stderr + r.stdout)
+
+
+def test_bench_reference_ranks_fit_host_memory(monkeypatch):
+    """The CPU baseline sizes the reference's ThreadedEvaluator to host RAM
+    (3 full-size blocks per rank, rank_pool.cpp:93-95): all threads when they
+    fit, fewer ranks, SerialEvaluator, or 'unavailable' -- never an OOM kill."""
+    from types import SimpleNamespace as NS
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+    c4 = NS(mesh=NS(n_cells=10485762, n_edges=31457280))
+    c5 = NS(mesh=NS(n_cells=41943042, n_edges=125829120))
+    monkeypatch.setattr(bench, "_mem_available", lambda: 196e9)
+    assert bench.ref_ranks(c4, 16) == (16, "")
+    r, note = bench.ref_ranks(c5, 16)
+    assert 2 <= r < 16 and "host RAM" in note
+    assert 3 * r * 36.0 * (c5.mesh.n_cells + c5.mesh.n_edges) <= 0.5 * 196e9
+    monkeypatch.setattr(bench, "_mem_available", lambda: 62e9)
+    assert bench.ref_ranks(c5, 16)[0] == 0
+    monkeypatch.setattr(bench, "_mem_available", lambda: 8e9)
+    assert bench.ref_ranks(c5, 16)[0] is None
