@@ -305,7 +305,7 @@ struct mswm_cuda_ctx {
   // T1h / T1u until the substeps are done
   cudaStream_t ls2 = nullptr, lsh = nullptr;  // coarse step (low), substeps (high priority)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join_h = nullptr;
-  int fork_ctas = 6;  // resident CTAs per SM of the concurrent coarse step
+  int fork_ctas[3] = {6, 6, 6};  // resident CTAs per SM of the concurrent coarse step (A, B, C)
   DArr<double> pv2, K2;
   DArr<double2> FQ2;
   DArr<uint32_t> band_cbits, band_ebits;
@@ -1656,7 +1656,7 @@ struct Side {
   double* pv;
   double* K;
   double2* FQ;
-  int ctas_per_sm;  // resident-grid size of the streamed kernels (0: default)
+  int ctas_per_sm[3];  // resident-grid size of kernels A, B, C (0: default)
 };
 
 void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const double* u,
@@ -1668,7 +1668,8 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
   double2* const FQ = side ? side->FQ : c->FQ.p;
   auto grid = [&](int64_t n, int kernel) {
     const int g = sgrid(c, n, kernel);
-    return side && side->ctas_per_sm > 0 ? std::min(g, side->ctas_per_sm * c->n_sm) : g;
+    return side && side->ctas_per_sm[kernel] > 0 ? std::min(g, side->ctas_per_sm[kernel] * c->n_sm)
+                                                 : g;
   };
   if (pred && !(p.use_coop && !p.use_tiles) && int64_t(pred->nc) + pred->ne > 0) {
     k_predict<<<nblk(int64_t(pred->nc) + pred->ne), kBlock, 0, s>>>(
@@ -2126,7 +2127,11 @@ void prepare_fork(mswm_cuda_ctx* c) {
   MaskPlan& ps = plan_for(c, kMaskSub);
   MaskPlan& pc = plan_for(c, kMaskCoarseOnly);
   if (pc.use_tiles || pc.use_coop || pc.use_flow || ps.use_flow || !c->slabs.empty()) return;
-  if (const char* fc = std::getenv("MSWM_FORK_CTAS")) c->fork_ctas = std::max(0, std::atoi(fc));
+  if (const char* fc = std::getenv("MSWM_FORK_CTAS")) {  // "n" or "a,b,c"
+    int v[3];
+    const int k = std::sscanf(fc, "%d,%d,%d", &v[0], &v[1], &v[2]);
+    for (int j = 0; j < 3; ++j) c->fork_ctas[j] = std::max(0, k == 3 ? v[j] : v[0]);
+  }
   cudaStream_t s = c->stream;
   DArr<uint8_t> cr, er;
   cr.alloc(c->nC);
@@ -2219,7 +2224,8 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
     eo.alt = c->T1u.p;
     eo.altbits = c->band_ebits.p;
     Op cos[2] = {co, co}, eos[2] = {eo, eo};
-    const Side side{c->ls2, c->pv2.p, c->K2.p, c->FQ2.p, c->fork_ctas};
+    const Side side{c->ls2, c->pv2.p, c->K2.p, c->FQ2.p,
+                    {c->fork_ctas[0], c->fork_ctas[1], c->fork_ctas[2]}};
     launch_eval(c, plan_for(c, kMaskCoarseOnly), H2, U2, cos, eos, nullptr, &side);
     CK(cudaEventRecord(c->ev_join, c->ls2));
     // the substeps on the high-priority stream: their CTAs take SM slots
