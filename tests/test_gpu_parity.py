@@ -565,3 +565,45 @@ def test_stencil_offsets16_bitwise(st16, monkeypatch):
         ctx.advance(Scheme.LTS3, wl.dt, wl.M, 2)
         st = ctx.download()
         assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
+
+
+def test_c4_full_size_against_reference():
+    """north_star's target mesh at full size (BASELINE configs[3]: icosahedral
+    level 10, 10,485,762 cells, 20-degree cap, M = 4) against the unmodified
+    reference (oracle/_ref, ThreadedEvaluator -- bitwise partition-invariant,
+    acceptance.cpp:205-244): region labels and the 11 group lists bit-exact,
+    every LTS3 mask's tendencies bitwise, and h, u after 2 coarse LTS3 steps
+    bitwise (so within north_star's 1e-11 relative max-norm, also asserted)."""
+    import os
+    from oracle.oracle import RefEvaluator, RefMesh, RefRegions, ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    wl = W.config4(n_steps=2)
+    nC, nE = wl.mesh.n_cells, wl.mesh.n_edges
+    rm = RefMesh.from_mesh(wl.mesh)
+    rr = RefRegions(rm, wl.fine_mask, wl.width)
+    ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order="regions", fine_mask=wl.fine_mask)
+    ctx.make_regions(wl.fine_mask, wl.width)
+    cl, cs, el = rr.labels(nC, nE)
+    assert np.array_equal(ctx.regions.cell_label, cl)
+    assert np.array_equal(ctx.regions.cell_sublabel, cs)
+    assert np.array_equal(ctx.regions.edge_label, el)
+    for a, b in zip(ctx.regions.groups, rr.groups()):
+        assert np.array_equal(a, b)
+    # full-size host arrays per rank block: keep the rank count inside host RAM
+    ranks = max(1, min(8, len(os.sched_getaffinity(0))))
+    ref = RefEvaluator(rm, rr, wl.b, wl.f, wl.gravity, nranks=ranks)
+    ev = CudaEvaluator(ctx)
+    for mask in LTS3_MASKS:
+        dh1 = np.full(nC, SENTINEL)
+        du1 = np.full(nE, SENTINEL)
+        dh2, du2 = dh1.copy(), du1.copy()
+        ev.eval(wl.h, wl.u, mask, dh1, du1)
+        ref.eval(wl.h, wl.u, mask, dh2, du2)
+        assert bits_equal(dh1, dh2) and bits_equal(du1, du2), mask
+    h_ref, u_ref, _, _ = ref.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, wl.M, 2)
+    ctx.upload(State(wl.h, wl.u, 0.0))
+    ctx.advance(Scheme.LTS3, wl.dt, wl.M, 2)
+    st = ctx.download()
+    assert max_rel(st.h, h_ref) <= 1e-11 and max_rel(st.u, u_ref) <= 1e-11
+    assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
