@@ -567,18 +567,21 @@ def test_stencil_offsets16_bitwise(st16, monkeypatch):
         assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
 
 
-def test_c4_full_size_against_reference():
-    """north_star's target mesh at full size (BASELINE configs[3]: icosahedral
-    level 10, 10,485,762 cells, 20-degree cap, M = 4) against the unmodified
-    reference (oracle/_ref, ThreadedEvaluator -- bitwise partition-invariant,
-    acceptance.cpp:205-244): region labels and the 11 group lists bit-exact,
-    every LTS3 mask's tendencies bitwise, and h, u after 2 coarse LTS3 steps
-    bitwise (so within north_star's 1e-11 relative max-norm, also asserted)."""
+@pytest.mark.parametrize("config", ["c4", "c3"])
+def test_full_size_against_reference(config):
+    """BASELINE configs at full size against the unmodified reference
+    (oracle/_ref, ThreadedEvaluator -- bitwise partition-invariant,
+    acceptance.cpp:205-244): C4 = north_star's target mesh (icosahedral level
+    10, 10,485,762 cells, 20-degree cap, M = 4), C3 = planar 2048^2 (4.2M
+    cells, four fine circles, beta-plane, M = 8).  Region labels and the 11
+    group lists bit-exact, every LTS3 mask's tendencies bitwise, h, u after 2
+    coarse LTS3 steps bitwise (so within north_star's 1e-11 relative
+    max-norm, also asserted)."""
     import os
     from oracle.oracle import RefEvaluator, RefMesh, RefRegions, ref_available
     if not ref_available():
         pytest.skip("oracle/_ref not built")
-    wl = W.config4(n_steps=2)
+    wl = W.CONFIGS[config](n_steps=2)
     nC, nE = wl.mesh.n_cells, wl.mesh.n_edges
     rm = RefMesh.from_mesh(wl.mesh)
     rr = RefRegions(rm, wl.fine_mask, wl.width)
