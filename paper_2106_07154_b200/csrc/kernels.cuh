@@ -23,10 +23,15 @@ constexpr int kMaxSten = 2 * kMaxDeg - 2;
 constexpr int kFastDeg = 6;
 constexpr int kFastSten = 10;
 constexpr int kBlock = 256;
+// threads per CTA of the three streamed evaluation kernels
+#ifndef MSWM_SBLOCK
+#define MSWM_SBLOCK 256
+#endif
+constexpr int kSBlock = MSWM_SBLOCK;
 // minimum resident CTAs per SM requested from ptxas (register budget) for
-// the streamed kernels; tuned on B200 (profiles/r1_*)
+// the streamed kernels; tuned on B200 (profiles/r1_*): a full SM of 2048 threads
 #ifndef MSWM_KA_MINB
-#define MSWM_KA_MINB 8
+#define MSWM_KA_MINB (2048 / MSWM_SBLOCK)
 #endif
 #ifndef MSWM_VCE
 #define MSWM_VCE 1
@@ -38,17 +43,17 @@ constexpr int kBlock = 256;
 #define MSWM_KOUT_BATCH 3   // coefficient pairs per batch
 #endif
 #ifndef MSWM_KOUT_MINB
-#define MSWM_KOUT_MINB 8
+#define MSWM_KOUT_MINB (2048 / MSWM_SBLOCK)
 #endif
 #if MSWM_KA_MINB > 0
-#define MSWM_KA_BOUNDS __launch_bounds__(kBlock, MSWM_KA_MINB)
+#define MSWM_KA_BOUNDS __launch_bounds__(kSBlock, MSWM_KA_MINB)
 #else
-#define MSWM_KA_BOUNDS __launch_bounds__(kBlock)
+#define MSWM_KA_BOUNDS __launch_bounds__(kSBlock)
 #endif
 #if MSWM_KOUT_MINB > 0
-#define MSWM_KOUT_BOUNDS __launch_bounds__(kBlock, MSWM_KOUT_MINB)
+#define MSWM_KOUT_BOUNDS __launch_bounds__(kSBlock, MSWM_KOUT_MINB)
 #else
-#define MSWM_KOUT_BOUNDS __launch_bounds__(kBlock)
+#define MSWM_KOUT_BOUNDS __launch_bounds__(kSBlock)
 #endif
 
 // Device mesh tables in internal numbering.  Slot-major SoA ([slot][elem])
@@ -277,7 +282,7 @@ __global__ void MSWM_KA_BOUNDS k_vertex_cell(DevMesh M, const double* __restrict
                                              int32_t* __restrict__ dry,
                                              const uint32_t* __restrict__ vmask) {
   const int32_t n = vs.n() + ks.n();
-  for (int32_t t = blockIdx.x * kBlock + threadIdx.x; t < n; t += gridDim.x * kBlock)
+  for (int32_t t = blockIdx.x * kSBlock + threadIdx.x; t < n; t += gridDim.x * kSBlock)
     item_vertex_cell(M, h, u, vs, ks, pv, K, dry, vmask, t);
 }
 
@@ -308,12 +313,12 @@ __device__ __forceinline__ void item_edge_fq(const DevMesh& M, const double* __r
   FQ[e] = make_double2(F, q);
 }
 
-__global__ void __launch_bounds__(kBlock) k_edge_fq(DevMesh M, const double* __restrict__ h,
+__global__ void __launch_bounds__(kSBlock) k_edge_fq(DevMesh M, const double* __restrict__ h,
                                                    const double* __restrict__ u,
                                                    const double* __restrict__ pv, Span es,
                                                    double2* __restrict__ FQ) {
   const int32_t n = es.n();
-  for (int32_t t = blockIdx.x * kBlock + threadIdx.x; t < n; t += gridDim.x * kBlock)
+  for (int32_t t = blockIdx.x * kSBlock + threadIdx.x; t < n; t += gridDim.x * kSBlock)
     item_edge_fq(M, h, u, pv, es, FQ, t);
 }
 
@@ -487,7 +492,7 @@ __global__ void MSWM_KOUT_BOUNDS k_out(DevMesh M, const double* __restrict__ h,
                                      const double* __restrict__ K,
                                      const double2* __restrict__ FQ, OutArgs a) {
   const int32_t n = a.cs.n() + a.es.n();
-  for (int32_t t = blockIdx.x * kBlock + threadIdx.x; t < n; t += gridDim.x * kBlock)
+  for (int32_t t = blockIdx.x * kSBlock + threadIdx.x; t < n; t += gridDim.x * kSBlock)
     item_out(M, h, K, FQ, a, t);
 }
 

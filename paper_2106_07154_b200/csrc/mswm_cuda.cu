@@ -260,7 +260,7 @@ struct mswm_cuda_ctx {
   // full occupancy at 32 registers) looping over their elements: 3.7 % faster
   // C4 steps than one CTA per 256 elements (CTA churn capped occupancy at
   // ~70 %); MSWM_PERSIST=0 restores one element per thread
-  int persist_ctas[3] = {8, 8, 8}, n_sm = 148;  // kernels A, B, C
+  int persist_ctas[3] = {2048 / kSBlock, 2048 / kSBlock, 2048 / kSBlock}, n_sm = 148;  // A, B, C
   // fused tile kernel structures (k_tile)
   DArr<TileMeta> t_meta;
   DArr<int32_t> t_c1_ids, t_er_ids, t_vr_ids, t_e_tile;
@@ -305,7 +305,8 @@ struct mswm_cuda_ctx {
   // T1h / T1u until the substeps are done
   cudaStream_t ls2 = nullptr, lsh = nullptr;  // coarse step (low), substeps (high priority)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join_h = nullptr;
-  int fork_ctas[3] = {6, 6, 6};  // resident CTAs per SM of the concurrent coarse step (A, B, C)
+  // resident CTAs per SM of the concurrent coarse step (A, B, C): 3/4 of an SM
+  int fork_ctas[3] = {1536 / kSBlock, 1536 / kSBlock, 1536 / kSBlock};
   DArr<double> pv2, K2;
   DArr<double2> FQ2;
   DArr<uint32_t> band_cbits, band_ebits;
@@ -1638,7 +1639,7 @@ MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
 // Grid of a streamed kernel: one element per thread, or at most
 // `persist_ctas` CTAs per SM looping over the elements (MSWM_PERSIST).
 int sgrid(const mswm_cuda_ctx* c, int64_t n, int kernel) {
-  const int64_t b = nblk(n);
+  const int64_t b = nblk(n, kSBlock);
   const int p = c->persist_ctas[kernel];
   return int(p > 0 ? std::min<int64_t>(b, int64_t(p) * c->n_sm) : b);
 }
@@ -1730,10 +1731,10 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
       const Span ks{sl.c0, sl.nc, sl.khalo.p, int32_t(sl.khalo.n)};
       const Span es{sl.e0, sl.ne, sl.ehalo.p, int32_t(sl.ehalo.n)};
       const int64_t na = int64_t(vs.n_range) + vs.n_list + ks.n_range + ks.n_list;
-      k_vertex_cell<<<nblk(na), kBlock, 0, s>>>(M, h, u, vs, ks, c->pv.p, c->K.p, c->dry_vertex.p,
+      k_vertex_cell<<<nblk(na, kSBlock), kSBlock, 0, s>>>(M, h, u, vs, ks, c->pv.p, c->K.p, c->dry_vertex.p,
                                                p.vmask.p);
       const int64_t nb_ = int64_t(es.n_range) + es.n_list;
-      k_edge_fq<<<nblk(nb_), kBlock, 0, s>>>(M, h, u, c->pv.p, es, c->FQ.p);
+      k_edge_fq<<<nblk(nb_, kSBlock), kSBlock, 0, s>>>(M, h, u, c->pv.p, es, c->FQ.p);
       OutArgs a;
       std::memset(&a, 0, sizeof(a));
       a.mask = p.mask;
@@ -1745,7 +1746,7 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
       a.cop[1] = cop[1];
       a.eop[0] = eop[0];
       a.eop[1] = eop[1];
-      k_out<<<nblk(int64_t(sl.nc) + sl.ne), kBlock, 0, s>>>(M, h, c->K.p, c->FQ.p, a);
+      k_out<<<nblk(int64_t(sl.nc) + sl.ne, kSBlock), kSBlock, 0, s>>>(M, h, c->K.p, c->FQ.p, a);
       CK(cudaGetLastError());
       c->launches += 3;
       if (c->l2_discard) {
@@ -1857,7 +1858,7 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
     return;
   }
   if (na > 0) {
-    k_vertex_cell<<<grid(na, 0), kBlock, 0, s>>>(M, h, u, vs, ks, pv, Kp,
+    k_vertex_cell<<<grid(na, 0), kSBlock, 0, s>>>(M, h, u, vs, ks, pv, Kp,
                                                  c->dry_vertex.p, p.vmask.p);
     CK(cudaGetLastError());
     ++c->launches;
@@ -1886,7 +1887,7 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
     return;
   }
   if (p.se.n() > 0) {
-    k_edge_fq<<<grid(p.se.n(), 1), kBlock, 0, s>>>(M, h, u, pv, es, FQ);
+    k_edge_fq<<<grid(p.se.n(), 1), kSBlock, 0, s>>>(M, h, u, pv, es, FQ);
     CK(cudaGetLastError());
     ++c->launches;
   }
@@ -1903,7 +1904,7 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
     a.cop[1] = cop[1];
     a.eop[0] = eop[0];
     a.eop[1] = eop[1];
-    k_out<<<grid(nout, 2), kBlock, 0, s>>>(M, h, Kp, FQ, a);
+    k_out<<<grid(nout, 2), kSBlock, 0, s>>>(M, h, Kp, FQ, a);
     CK(cudaGetLastError());
     ++c->launches;
   }
