@@ -176,12 +176,17 @@ int mswm_cuda_ledger(mswm_cuda_ctx* ctx, int64_t cell_evals[16],
                      int64_t edge_evals[16], int64_t* steps);
 int mswm_cuda_ledger_reset(mswm_cuda_ctx* ctx);
 
-/* Original id of the vertex of the last DryVertexError, -1 if none.  The
- * step output is reserved (always 0): a dry vertex inside a replayed step
- * batch is reported when the batch synchronises. */
+/* Original id of the vertex of the last DryVertexError, -1 if none; *step =
+ * the 1-based step of the mswm_cuda_step batch it happened in (the
+ * reference's "during step k of n", harness.cpp:183-190), 0 for an eval
+ * call.  Kernel A records (step, vertex) on the device; an asynchronous batch
+ * reports it at the next synchronous call (step with sync=1, eval, sync,
+ * state_download -- which still writes the state), and the earliest step
+ * wins.  The flag is cleared only once reported. */
 int mswm_cuda_dry_vertex(const mswm_cuda_ctx* ctx, int64_t* step);
 
-/* Synchronise the context's stream; returns any pending error. */
+/* Synchronise the context's stream; returns any pending error
+ * (MSWM_E_DRY_VERTEX from an asynchronous step batch). */
 int mswm_cuda_sync(mswm_cuda_ctx* ctx);
 /* The cudaStream_t every kernel of ctx is launched on (for event timing). */
 void* mswm_cuda_stream(mswm_cuda_ctx* ctx);
@@ -199,12 +204,9 @@ int mswm_cuda_eval_profile(mswm_cuda_ctx* ctx, float* eval_ms,
                            int64_t* out_cells, int64_t* out_edges, int cap,
                            int* n);
 
-/* Layout chosen at create: kernel_path 2 = fused tile kernel (stencil and
- * weights rebuilt from the cell rings on chip), 1 = three kernels walking the
- * rings through L1, 0 = three kernels streaming explicit stencil tables
- * (always used when the mesh's stencil is not the reference builder's ring
- * walk); selectable with MSWM_KERNELS=tile|ringwalk|explicit.
- * identity_order = 1 when the internal numbering equals the caller's. */
+/* Layout chosen at create: kernel_path 0 = three streamed kernels over the
+ * explicit stencil tables (the only path); identity_order = 1 when the
+ * internal numbering equals the caller's. */
 int mswm_cuda_layout_info(const mswm_cuda_ctx* ctx, int* kernel_path,
                           int* identity_order);
 
@@ -213,17 +215,6 @@ int mswm_cuda_layout_info(const mswm_cuda_ctx* ctx, int* kernel_path,
  * n_wide = edges with an offset outside int16, whose warps read the int32
  * table instead (edges_on_edge, mesh.hpp:60-61). */
 int mswm_cuda_stencil_info(const mswm_cuda_ctx* ctx, int* offsets16, int64_t* n_wide);
-
-/* Phases B + C fused per cell tile (k_bc, opt-in MSWM_BC=1 at create,
- * MSWM_BC_CELLS cells per tile): (F, q~, l) of each tile's edges and halo
- * in shared memory; all zero when not in use. */
-int mswm_cuda_bc_info(const mswm_cuda_ctx* ctx, int* tile_cells, int* n_tiles, int64_t* smem);
-
-/* Dataflow evaluation (k_flow, opt-in with MSWM_FLOW=1 at create): large
- * masks run as one persistent launch over cell slabs of slab_cells cells;
- * all zero when disabled (the default, small meshes). */
-int mswm_cuda_flow_info(const mswm_cuda_ctx* ctx, int* slab_cells, int* n_slabs,
-                        int* lag, int* grid);
 
 /* Number of this library's kernels one replay of the most recently used
  * step graph launches (the bench's gpu_launches evidence). */

@@ -37,9 +37,12 @@ class TopologyError(Error):
 
 
 class DryVertexError(Error):
-    def __init__(self, msg, vertex):
+    """errors.hpp:45-49; ``step`` is the 1-based step of the advance() batch
+    it happened in (harness.cpp:183-190), 0 for an eval call."""
+    def __init__(self, msg, vertex, step=0):
         super().__init__(msg)
         self.vertex = vertex
+        self.step = step
 
 
 class CudaError(Error):
@@ -50,11 +53,11 @@ _STATUS = {1: ConfigError, 2: UsageError, 3: TopologyError, 5: CudaError, 6: Cud
            7: CudaError}
 
 
-def _raise(rc: int, msg: str, vertex: int = -1):
+def _raise(rc: int, msg: str, vertex: int = -1, step: int = 0):
     if rc == 0:
         return
     if rc == 4:
-        raise DryVertexError(msg, vertex)
+        raise DryVertexError(msg, vertex, step)
     raise _STATUS.get(rc, Error)(msg)
 
 
@@ -246,10 +249,22 @@ class CudaContext:
     def _check(self, rc: int):
         if rc:
             msg = self.lib.mswm_cuda_last_error(self.handle).decode()
-            v = -1
+            v, st = -1, C.c_int64(0)
             if rc == 4:
-                v = self.lib.mswm_cuda_dry_vertex(self.handle, None)
-            _raise(rc, msg, v)
+                v = self.lib.mswm_cuda_dry_vertex(self.handle, C.byref(st))
+            _raise(rc, msg, v, st.value)
+
+    def _f64(self, a, n: int, what: str, writable: bool = False) -> np.ndarray:
+        """The native side reads / writes exactly n doubles: check before the call."""
+        if writable:
+            if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous \
+                    or not a.flags.writeable:
+                raise UsageError(f"{what} must be a writable contiguous float64 array")
+        else:
+            a = np.ascontiguousarray(a, np.float64)
+        if a.shape != (n,):
+            raise UsageError(f"{what} has shape {a.shape}, expected ({n},)")
+        return a
 
     # -- setup ---------------------------------------------------------------
     def set_fields(self, b, f_vertex, gravity: float):
@@ -297,8 +312,8 @@ class CudaContext:
 
     # -- device-resident stepping ------------------------------------------
     def upload(self, state: State):
-        h = np.ascontiguousarray(state.h, np.float64)
-        u = np.ascontiguousarray(state.u, np.float64)
+        h = self._f64(state.h, self.mesh.n_cells, "h")
+        u = self._f64(state.u, self.mesh.n_edges, "u")
         self._check(self.lib.mswm_cuda_state_upload(self.handle, _p(h, _lib.f64p),
                                                     _p(u, _lib.f64p), float(state.time)))
 
@@ -306,6 +321,8 @@ class CudaContext:
         m = self.mesh
         if state is None:
             state = State(np.zeros(m.n_cells), np.zeros(m.n_edges), 0.0)
+        self._f64(state.h, m.n_cells, "state.h", writable=True)
+        self._f64(state.u, m.n_edges, "state.u", writable=True)
         t = C.c_double(0.0)
         self._check(self.lib.mswm_cuda_state_download(self.handle, _p(state.h, _lib.f64p),
                                                       _p(state.u, _lib.f64p), C.byref(t)))
@@ -352,7 +369,7 @@ class CudaContext:
     def layout_info(self) -> dict:
         kp, ident = C.c_int(0), C.c_int(0)
         self._check(self.lib.mswm_cuda_layout_info(self.handle, C.byref(kp), C.byref(ident)))
-        return {"kernel_path": {0: "explicit", 1: "ringwalk", 2: "tile", 3: "auto"}[kp.value],
+        return {"kernel_path": {0: "explicit"}[kp.value],
                 "input_order": bool(ident.value)}
 
     def stencil_info(self) -> dict:
@@ -360,18 +377,6 @@ class CudaContext:
         o, n = C.c_int(0), C.c_int64(0)
         self._check(self.lib.mswm_cuda_stencil_info(self.handle, C.byref(o), C.byref(n)))
         return {"offsets16": bool(o.value), "n_wide": n.value}
-
-    def bc_info(self) -> dict:
-        """Fused B + C tile path (k_bc): tile size, tiles, shared memory per CTA."""
-        tc, nt, sm = C.c_int(0), C.c_int(0), C.c_int64(0)
-        self._check(self.lib.mswm_cuda_bc_info(self.handle, C.byref(tc), C.byref(nt), C.byref(sm)))
-        return {"tile_cells": tc.value, "n_tiles": nt.value, "smem": sm.value}
-
-    def flow_info(self) -> dict:
-        """Dataflow evaluation (k_flow) parameters; slab_cells 0 = disabled."""
-        v = [C.c_int(0) for _ in range(4)]
-        self._check(self.lib.mswm_cuda_flow_info(self.handle, *[C.byref(x) for x in v]))
-        return dict(zip(["slab_cells", "n_slabs", "lag", "grid"], [x.value for x in v]))
 
     def kernels_per_step(self) -> int:
         n = C.c_int64(0)
@@ -420,11 +425,11 @@ class CudaEvaluator:
 
     def eval(self, h, u, mask: int, dh: np.ndarray, du: np.ndarray):
         c = self.ctx
-        if dh.dtype != np.float64 or du.dtype != np.float64 or not dh.flags.c_contiguous \
-                or not du.flags.c_contiguous:
-            raise UsageError("dh/du must be contiguous float64 arrays")
-        h = np.ascontiguousarray(h, np.float64)
-        u = np.ascontiguousarray(u, np.float64)
+        m = c.mesh
+        c._f64(dh, m.n_cells, "dh", writable=True)
+        c._f64(du, m.n_edges, "du", writable=True)
+        h = c._f64(h, m.n_cells, "h")
+        u = c._f64(u, m.n_edges, "u")
         c._check(c.lib.mswm_cuda_eval(c.handle, _p(h, _lib.f64p), _p(u, _lib.f64p), int(mask),
                                       _p(dh, _lib.f64p), _p(du, _lib.f64p)))
 

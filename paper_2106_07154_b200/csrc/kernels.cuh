@@ -9,12 +9,9 @@
 #pragma once
 
 #include <cstdint>
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 namespace mswm_dev {
-
-namespace cg = cooperative_groups;
 
 constexpr int kMaxDeg = 8;               // ring size bound (hexagons 6, pentagons 5)
 constexpr int kMaxSten = 2 * kMaxDeg - 2;
@@ -32,12 +29,6 @@ constexpr int kSBlock = MSWM_SBLOCK;
 // the streamed kernels; tuned on B200 (profiles/r1_*): a full SM of 2048 threads
 #ifndef MSWM_KA_MINB
 #define MSWM_KA_MINB (2048 / MSWM_SBLOCK)
-#endif
-#ifndef MSWM_VCE
-#define MSWM_VCE 1
-#endif
-#ifndef MSWM_KITE01
-#define MSWM_KITE01 0
 #endif
 #ifndef MSWM_KOUT_BATCH
 #define MSWM_KOUT_BATCH 3   // coefficient pairs per batch
@@ -66,8 +57,6 @@ struct DevMesh {
   const uint8_t* __restrict__ c_deg;     // [nC]
   const uint8_t* __restrict__ c_sbits;   // [nC] bit j: cell_sign(ring edge j, i) < 0
   const double* __restrict__ c_area;     // [nC] A_i
-  const double* __restrict__ c_ratio;    // [deg_max][nC] kite_area / A_i per ring slot
-                                         // (ring-derived stencil; null = explicit tables)
   // vertices
   const int32_t* __restrict__ v_cell;    // [3][nV]
   const int32_t* __restrict__ v_edge;    // [3][nV]
@@ -82,8 +71,6 @@ struct DevMesh {
   const double* __restrict__ e_ld;       // l_e * d_e (the K product's first rounding)
   const double* __restrict__ e_dual;     // d_e
   const double* __restrict__ e_invd;     // 1.0 / d_e
-  const uint8_t* __restrict__ e_slots;   // ring-derived stencil: bits 0-2 slot of e in
-                                         // ring(c0), 3-5 in ring(c1), 6/7 anchor sign < 0
   const uint8_t* __restrict__ e_nst;     // stencil length; bit 7: some e' - e outside int16
   const int32_t* __restrict__ e_sten;    // [sten_max][nE] edges_on_edge
   const uint2* __restrict__ e_st16;      // [(W+1)/2][nE], W = (sten_max+1)/2 u32 words of
@@ -95,7 +82,6 @@ struct DevMesh {
   // coalescing: consecutive threads still read consecutive 8/16 B)
   const int2* __restrict__ c_edge2;      // [(deg_max+1)/2][nC] ring edges (2k, 2k+1)
   const int2* __restrict__ v_ce;         // [3][nV] (vertex_cells k, vertex_edges k)
-  const double2* __restrict__ v_kite01;  // [nV] (kite 0, kite 1); kite 2 in v_kite
   const double2* __restrict__ v_af;      // [nV] (A_v, f_v)
   // fields
   const double* __restrict__ b;          // [nC]
@@ -200,7 +186,8 @@ __device__ __forceinline__ void apply_op(const Op& op_in, int32_t i, double d) {
 __device__ __forceinline__ void item_vertex_cell(const DevMesh& M, const double* __restrict__ h,
                                                  const double* __restrict__ u, const Span& vs,
                                                  const Span& ks, double* __restrict__ pv,
-                                                 double* __restrict__ K, int32_t* __restrict__ dry,
+                                                 double* __restrict__ K, unsigned long long* __restrict__ dry,
+                                                 const int64_t* __restrict__ step_ctr,
                                                  const uint32_t* __restrict__ vmask, int32_t t) {
   // Spans may be supersets of the closure (dense ranges, slabs); the dry
   // check then consults the closure bitmask vmask so only closure vertices
@@ -210,23 +197,11 @@ __device__ __forceinline__ void item_vertex_cell(const DevMesh& M, const double*
     const int32_t v = vs.at(t);
     const uint8_t sb = M.v_sbits[v];
     int2 ce[3];
-#if MSWM_VCE
 #pragma unroll
     for (int k = 0; k < 3; ++k) ce[k] = M.v_ce[k * M.nV + v];
-#else
-#pragma unroll
-    for (int k = 0; k < 3; ++k) ce[k] = make_int2(M.v_cell[k * M.nV + v], M.v_edge[k * M.nV + v]);
-#endif
     double hv = 0.0, circ = 0.0;
-#if MSWM_KITE01
-    const double2 k01 = M.v_kite01[v];
-    const double kite[3] = {k01.x, k01.y, M.v_kite[2 * M.nV + v]};
-#pragma unroll
-    for (int k = 0; k < 3; ++k) hv += kite[k] * h[ce[k].x];
-#else
 #pragma unroll
     for (int k = 0; k < 3; ++k) hv += M.v_kite[k * M.nV + v] * h[ce[k].x];
-#endif
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       const double d = M.e_dual[ce[k].y];
@@ -235,7 +210,12 @@ __device__ __forceinline__ void item_vertex_cell(const DevMesh& M, const double*
     const double2 af = M.v_af[v];
     hv /= af.x;
     if (!(hv > 0.0)) {
-      if (!vmask || ((vmask[v >> 5] >> (v & 31)) & 1u)) atomicMin(dry, M.v_orig[v]);
+      // (step << 32 | vertex): the earliest step wins, then the lowest id
+      // (the reference reports the first dry vertex it meets; the tests
+      // only require an adjacent valid id, test_operators.cpp:236-240)
+      if (!vmask || ((vmask[v >> 5] >> (v & 31)) & 1u))
+        atomicMin(dry, (static_cast<unsigned long long>(*step_ctr) << 32) |
+                           static_cast<uint32_t>(M.v_orig[v]));
       pv[v] = 0.0;
       return;
     }
@@ -279,27 +259,17 @@ __device__ __forceinline__ void item_vertex_cell(const DevMesh& M, const double*
 __global__ void MSWM_KA_BOUNDS k_vertex_cell(DevMesh M, const double* __restrict__ h,
                                              const double* __restrict__ u, Span vs, Span ks,
                                              double* __restrict__ pv, double* __restrict__ K,
-                                             int32_t* __restrict__ dry,
+                                             unsigned long long* __restrict__ dry,
+                                             const int64_t* __restrict__ step_ctr,
                                              const uint32_t* __restrict__ vmask) {
   const int32_t n = vs.n() + ks.n();
   for (int32_t t = blockIdx.x * kSBlock + threadIdx.x; t < n; t += gridDim.x * kSBlock)
-    item_vertex_cell(M, h, u, vs, ks, pv, K, dry, vmask, t);
+    item_vertex_cell(M, h, u, vs, ks, pv, K, dry, step_ctr, vmask, t);
 }
 
 // Phase B: thickness flux F_e (operators.cpp:61-62) and q~_e (:88-89) on the
 // union of the flux and q~ closures, packed as (F, q~) so the stencil loop
 // of phase C reads both with one 16-byte gather.
-// Loads of intermediates written earlier in the same launch (k_flow) bypass
-// L1, which is not coherent with other SMs' writes.
-template <bool CG, class T>
-__device__ __forceinline__ T ldx(const T* p) {
-  if constexpr (CG)
-    return __ldcg(p);
-  else
-    return *p;
-}
-
-template <bool CG = false>
 __device__ __forceinline__ void item_edge_fq(const DevMesh& M, const double* __restrict__ h,
                                              const double* __restrict__ u,
                                              const double* __restrict__ pv, const Span& es,
@@ -309,7 +279,7 @@ __device__ __forceinline__ void item_edge_fq(const DevMesh& M, const double* __r
   const int2 c = M.e_cells[e];
   const int2 v = M.e_verts[e];
   const double F = 0.5 * (h[c.x] + h[c.y]) * u[e];
-  const double q = 0.5 * (ldx<CG>(pv + v.x) + ldx<CG>(pv + v.y));
+  const double q = 0.5 * (pv[v.x] + pv[v.y]);
   FQ[e] = make_double2(F, q);
 }
 
@@ -336,7 +306,6 @@ struct OutArgs {
   Op eop[2];
 };
 
-template <bool CG = false>
 __device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __restrict__ h,
                                             const double* __restrict__ K,
                                             const double2* __restrict__ FQ, const Span& cs,
@@ -361,7 +330,7 @@ __device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __re
 #pragma unroll
       for (int j = 0; j < kFastDeg; ++j) {
         const double l = M.e_len[ce[j]];
-        const double x = ((sb >> j) & 1 ? -l : l) * ldx<CG>(FQ + ce[j]).x;
+        const double x = ((sb >> j) & 1 ? -l : l) * FQ[ce[j]].x;
         if (j < deg) acc += x;
       }
     } else {
@@ -370,7 +339,7 @@ __device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __re
         if (j < deg) {
           const int32_t e = M.c_edge[j * M.nC + i];
           const double l = M.e_len[e];
-          acc += ((sb >> j) & 1 ? -l : l) * ldx<CG>(FQ + e).x;
+          acc += ((sb >> j) & 1 ? -l : l) * FQ[e].x;
         }
       }
     }
@@ -381,43 +350,11 @@ __device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __re
     const int g = a.ekey ? a.ekey[e] : 0;
     if (g > 4 || !((a.mask >> (6 + g)) & 1u)) return;
     const int seg = g <= 1 ? 0 : 1;
-    const double qt_e = ldx<CG>(FQ + e).y;
+    const double qt_e = FQ[e].y;
     const double inv_d = M.e_invd[e];
     const int2 cc = M.e_cells[e];
     double pvflux = 0.0;
-    if (!M.e_sten) {  // no explicit tables: ring walk
-      // Ring-derived stencil (mesh_build.cpp:133-154 walk, weights
-      // :343-362): for each side, walk the cell's ring counterclockwise
-      // from just after e; w = (cell_sign * anchor) * (frac - 0.5) with
-      // frac the running sum of kite/A -- bitwise the stored edge_weight
-      // (verified at create), so the stencil tables never leave the chip.
-      const uint8_t sl = M.e_slots[e];
-#pragma unroll
-      for (int side = 0; side < 2; ++side) {
-        const int32_t c = side ? cc.y : cc.x;
-        const int p = side ? ((sl >> 3) & 7) : (sl & 7);
-        const unsigned aneg = (sl >> (6 + side)) & 1u;
-        const int deg = M.c_deg[c];
-        const uint8_t sb = M.c_sbits[c];
-        double frac = 0.0;
-#pragma unroll
-        for (int k = 1; k < kMaxDeg; ++k) {
-          if (k < deg) {
-            int sp = p + k - 1;
-            if (sp >= deg) sp -= deg;
-            int s = p + k;
-            if (s >= deg) s -= deg;
-            frac += M.c_ratio[sp * M.nC + c];
-            const int32_t e2 = M.c_edge[s * M.nC + c];
-            const double x = frac - 0.5;
-            const double w = (((sb >> s) & 1u) ^ aneg) ? -x : x;
-            const double coef = w * (M.e_len[e2] * inv_d);
-            const double2 fq = ldx<CG>(FQ + e2);
-            pvflux += coef * fq.x * (0.5 * (qt_e + fq.y));
-          }
-        }
-      }
-    } else {
+    {
       // Stencil ids as 16-bit offsets from e (20 B/edge instead of 40 B);
       // a warp holding any edge whose offsets do not fit (bit 7 of e_nst:
       // ~1 % of edges, along the curve's seams) reads the int32 table
@@ -448,7 +385,7 @@ __device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __re
               if (!(b & 1)) c[b >> 1] = M.e_coef2[(j >> 1) * M.nE + e];
               const int32_t e2 = e + (j & 1 ? int32_t(w[j >> 1]) >> 16
                                             : int32_t(w[j >> 1] << 16) >> 16);
-              fq[b] = ldx<CG>(FQ + e2);
+              fq[b] = FQ[e2];
             }
           }
 #pragma unroll
@@ -468,14 +405,14 @@ __device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __re
             const int32_t e2 = M.e_sten[j * M.nE + e];
             const double2 cp = M.e_coef2[(j >> 1) * M.nE + e];
             const double c = j & 1 ? cp.y : cp.x;
-            const double2 fq = ldx<CG>(FQ + e2);
+            const double2 fq = FQ[e2];
             pvflux += c * fq.x * (0.5 * (qt_e + fq.y));
           }
         }
       }
     }
-    const double psi_lo = ldx<CG>(K + cc.x);  // psi (phase A)
-    const double psi_hi = ldx<CG>(K + cc.y);
+    const double psi_lo = K[cc.x];  // psi (phase A)
+    const double psi_hi = K[cc.y];
     const double du = -pvflux - (psi_lo - psi_hi) * inv_d;
     apply_op(a.eop[seg], e, du);
   }
@@ -485,7 +422,7 @@ __device__ __forceinline__ void item_out(const DevMesh& M, const double* __restr
                                          const double* __restrict__ K,
                                          const double2* __restrict__ FQ, const OutArgs& a,
                                          int32_t t) {
-  item_out_sp<false>(M, h, K, FQ, a.cs, a.es, a, t);
+  item_out_sp(M, h, K, FQ, a.cs, a.es, a, t);
 }
 
 __global__ void MSWM_KOUT_BOUNDS k_out(DevMesh M, const double* __restrict__ h,
@@ -586,166 +523,8 @@ __device__ __forceinline__ void item_predict(const PredArgs& p, int32_t t) {
   }
 }
 
-// A whole small evaluation in one cooperative launch: [prediction] | PV, K |
-// F, q~ | dh, du + epilogue, phases separated by grid-wide barriers (all
-// CTAs are co-resident by construction of the cooperative launch).  Used
-// for the LTS substeps, whose three-launch cost is mostly launch latency.
-struct FusedArgs {
-  DevMesh M;
-  const double* h;
-  const double* u;
-  Span vs, ks, es;
-  double *pv, *K;
-  double2* FQ;
-  int32_t* dry;
-  const uint32_t* vmask;
-  OutArgs out;
-  PredArgs pred;
-  int has_pred;
-};
-
-__global__ void __launch_bounds__(kBlock) k_fused_eval(FusedArgs f) {
-  cg::grid_group grid = cg::this_grid();
-  const int32_t stride = gridDim.x * kBlock;
-  const int32_t t0 = blockIdx.x * kBlock + threadIdx.x;
-  if (f.has_pred) {
-    const int32_t n = f.pred.nc + f.pred.ne;
-    for (int32_t t = t0; t < n; t += stride) item_predict(f.pred, t);
-    grid.sync();
-  }
-  {
-    const int32_t n = f.vs.n() + f.ks.n();
-    for (int32_t t = t0; t < n; t += stride)
-      item_vertex_cell(f.M, f.h, f.u, f.vs, f.ks, f.pv, f.K, f.dry, f.vmask, t);
-  }
-  grid.sync();
-  {
-    const int32_t n = f.es.n();
-    for (int32_t t = t0; t < n; t += stride) item_edge_fq(f.M, f.h, f.u, f.pv, f.es, f.FQ, t);
-  }
-  grid.sync();
-  {
-    const int32_t n = f.out.cs.n() + f.out.es.n();
-    for (int32_t t = t0; t < n; t += stride) item_out(f.M, f.h, f.K, f.FQ, f.out, t);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Dataflow evaluation (k_flow): the three phases of one evaluation as one
-// persistent launch whose work items are (phase, cell slab) pairs.  Slab k =
-// cells [kS, (k+1)S) plus the edges and vertices whose lowest cell lies in
-// it (edges and vertices are sorted by their cells).  A warp takes items
-// from a fixed topological order, waits for the completion flags of the
-// items it reads from, and publishes its own completion:
-//   A_k (PV, K)  reads only h, u;
-//   B_k (F, q~)  reads PV of the vertices of its edges;
-//   C_k (dh, du) reads (F, q~) of the ring edges of its cells and of both
-//                cells of its edges (stencils are inside those rings), and K
-//                of both cells of its edges.
-// Dependencies are slab sets computed at create over all elements of a
-// slab, so they hold for every mask.
-// The order keeps producers a fixed lag ahead of their consumers, so PV, K
-// and (F, q~) are read back from L2 instead of HBM and the h, u and edge
-// tables the three phases share are fetched from HBM once.  Per-element
-// arithmetic is the item_* functions of the three-kernel path: bitwise the
-// same results.
-struct FlowSpan {
-  int32_t base, n_range;  // the span's range part
-  const int32_t* list;    // its list part, ascending
-  const int32_t* lofs;    // [nS+1] offsets of each slab's entries in list (null: no list)
-};
-
-__device__ __forceinline__ Span slab_span(const FlowSpan& f, int32_t lo, int32_t hi, int32_t k) {
-  Span s;
-  const int32_t a = max(f.base, lo), b = min(f.base + f.n_range, hi);
-  s.base = a;
-  s.n_range = b > a ? b - a : 0;
-  if (f.lofs) {
-    const int32_t o = f.lofs[k];
-    s.list = f.list + o;
-    s.n_list = f.lofs[k + 1] - o;
-  } else {
-    s.list = nullptr;
-    s.n_list = 0;
-  }
-  return s;
-}
-
-struct FlowArgs {
-  DevMesh M;
-  const double* h;
-  const double* u;
-  FlowSpan vs, ks, es, cs, eo;  // closure spans (A: vs, ks; B: es), outputs (C: cs, eo)
-  const int32_t* slab_v0;       // [nS+1] first vertex of each slab
-  const int32_t* slab_e0;       // [nS+1] first edge of each slab
-  const int32_t* dep_off;       // [2 nS + 1] dependencies of B_k at [k], of C_k at [nS + k]
-  const int32_t* dep;           // flag indices (A slab j: j, B slab j: nS + j)
-  const int32_t* order;         // item codes: phase << 28 | slab
-  int32_t S, nS, n_items;
-  int32_t* flags;  // [2][nS] A / B slab complete (zeroed before the launch)
-  double* pv;
-  double* K;
-  double2* FQ;
-  int32_t* dry;
-  const uint32_t* vmask;
-  OutArgs out;
-};
-
-__device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
-  int32_t v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Completion protocol: a producer warp publishes flags[slab] = 1 after a
-// fence (release); a consumer warp's lanes acquire-load the flags of the
-// exact slabs its item reads (dep lists, built at create) and the warp
-// barrier orders those acquisitions before every lane's reads.
-__device__ __forceinline__ void flow_wait(const FlowArgs& f, int32_t d0, int32_t d1, int lane) {
-  for (int32_t d = d0 + lane; d < d1; d += 32) {
-    const int32_t* fl = f.flags + f.dep[d];
-    while (ld_acquire(fl) == 0) __nanosleep(64);
-  }
-  __syncwarp();
-}
-
-template <int MINB>
-__global__ void __launch_bounds__(kBlock, MINB) k_flow(const __grid_constant__ FlowArgs f) {
-  const int lane = threadIdx.x & 31;
-  const int32_t nwarps = gridDim.x * (kBlock / 32);
-  for (int32_t q = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); q < f.n_items; q += nwarps) {
-    const int32_t code = f.order[q];
-    const int ph = code >> 28;
-    const int32_t k = code & 0x0FFFFFFF;
-    const int32_t c_lo = k * f.S, c_hi = min(c_lo + f.S, f.M.nC);
-    if (ph == 0) {
-      const Span vs = slab_span(f.vs, f.slab_v0[k], f.slab_v0[k + 1], k);
-      const Span ks = slab_span(f.ks, c_lo, c_hi, k);
-      const int32_t n = vs.n() + ks.n();
-      for (int32_t t = lane; t < n; t += 32)
-        item_vertex_cell(f.M, f.h, f.u, vs, ks, f.pv, f.K, f.dry, f.vmask, t);
-    } else if (ph == 1) {
-      flow_wait(f, f.dep_off[k], f.dep_off[k + 1], lane);
-      const Span es = slab_span(f.es, f.slab_e0[k], f.slab_e0[k + 1], k);
-      const int32_t n = es.n();
-      for (int32_t t = lane; t < n; t += 32) item_edge_fq<true>(f.M, f.h, f.u, f.pv, es, f.FQ, t);
-    } else {
-      flow_wait(f, f.dep_off[f.nS + k], f.dep_off[f.nS + k + 1], lane);
-      const Span cs = slab_span(f.cs, c_lo, c_hi, k);
-      const Span eo = slab_span(f.eo, f.slab_e0[k], f.slab_e0[k + 1], k);
-      const int32_t n = cs.n() + eo.n();
-      for (int32_t t = lane; t < n; t += 32) item_out_sp<true>(f.M, f.h, f.K, f.FQ, cs, eo, f.out, t);
-    }
-    if (ph < 2) {
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence();
-        atomicExch(f.flags + ph * f.nS + k, 1);
-      }
-    }
-  }
-}
-
+// First node of every step graph: the 1-based index of the coarse step in
+// flight since the context was created (dry-vertex reports, harness.cpp:183-190).
 __global__ void k_step_counter(int64_t* ctr) { ++*ctr; }
 
 // Halo exchange pack/unpack: code >= 0 is a cell id (h array), code < 0 is
@@ -1131,319 +910,6 @@ __global__ void __launch_bounds__(kBlock) k_compact_scatter(const uint8_t* __res
   }
 }
 
-}  // namespace mswm_dev
-
-namespace mswm_dev {
-
-// ---------------------------------------------------------------------------
-// Fused tile evaluation.  A tile is kTileCells consecutive internal cells
-// (a compact blob along the Hilbert curve); its CTA evaluates everything the
-// tile's outputs need from h and u, keeping the intermediates on chip:
-//   P1  q_v on V_req = ring vertices of C1 (operators.cpp:74-86)
-//   P2  K on C1 = tile cells + their ring neighbours (:64-72), and the
-//       kite/A ring rows of C1 for the weight walk
-//   P3  F, q~ (and l) on E_req = ring edges of C1 (:61-62, :88-89)
-//   P4  dh on the tile's cells (:91-99)
-//   P5  du on the edges the tile owns (min-rank cell in the tile) (:101-116),
-//       stencil and weights rebuilt from the C1 rings (mesh_build.cpp:133-154,
-//       343-362; verified bitwise at create)
-// each followed by the fused stage epilogue.  Values computed for halo
-// elements are never outputs, so per-element results equal the reference.
-constexpr int kTileCells = 128;  // default; MSWM_TILE_CELLS overrides at create
-constexpr int kTileThreads = 256;
-// shared-memory row stride of the per-cell kite/A rows: 9 doubles (odd) so
-// lanes reading different cells' rows hit different banks (a stride of 8
-// doubles = 16 banks folded every lane pair onto two bank groups)
-#ifndef MSWM_RSTRIDE
-#define MSWM_RSTRIDE (kMaxDeg + 1)
-#endif
-constexpr int kRStride = MSWM_RSTRIDE;
-
-struct TileMeta {
-  // owned ranges first (no index lists), then the halo from the lists:
-  // C1 = cells [c0, c0+nc) + c1_ids[c1_off .. nc1-nc); E_req = edges
-  // [e0, e0+ne) + er_ids[..]; V_req = vertices [v0, v0+nvo) + vr_ids[..]
-  int32_t c0, nc, nc1, c1h_off, c1r_off;
-  int32_t e0, ne, ner, erh_off, erv_off;
-  int32_t v0, nvo, nvr, vrh_off;
-};
-
-struct TileArgs {
-  const TileMeta* meta;
-  const int32_t* list;      // tiles to run (those with outputs in the mask)
-  const int32_t* c1_ids;    // per tile: C1 halo cells
-  const uint4* c1_ring;     // per C1 cell: ring edges as E_req-local uint16 x 8
-  const int32_t* er_ids;    // per tile: E_req halo edges
-  const ushort2* er_vloc;   // per E_req edge: V_req-local ids of its vertices
-  const int32_t* vr_ids;    // per tile: V_req halo vertices
-  const ushort2* oe_c1;     // per edge: C1-local ids of edge_cells[e][0], [1] in its tile
-  const uint32_t* vmask;    // closure bitmask of the mask (dry check filter), null = all
-  int32_t* dry;
-};
-
-__device__ __forceinline__ int ring16(const uint4& r, int s) {
-  const uint32_t w = s < 4 ? (s < 2 ? r.x : r.y) : (s < 6 ? r.z : r.w);
-  return (s & 1) ? int(w >> 16) : int(w & 0xFFFFu);
-}
-
-__global__ void __launch_bounds__(kTileThreads, 4) k_tile(DevMesh M, TileArgs T,
-                                                      const double* __restrict__ h,
-                                                      const double* __restrict__ u, OutArgs a) {
-  extern __shared__ double sm[];
-  const TileMeta tm = T.meta[T.list[blockIdx.x]];
-  double* sPV = sm;
-  double* sK = sPV + tm.nvr;
-  double* sR = sK + tm.nc1;
-  double* sF = sR + size_t(tm.nc1) * kRStride;
-  double* sQ = sF + tm.ner;
-  double* sL = sQ + tm.ner;
-
-  // P1: potential vorticity on V_req
-#pragma unroll 2
-  for (int k = threadIdx.x; k < tm.nvr; k += kTileThreads) {
-    const int32_t v = k < tm.nvo ? tm.v0 + k : T.vr_ids[tm.vrh_off + k - tm.nvo];
-    const uint8_t sb = M.v_sbits[v];
-    double hv = 0.0, circ = 0.0;
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      hv += M.v_kite[j * M.nV + v] * h[M.v_cell[j * M.nV + v]];
-      const int32_t e = M.v_edge[j * M.nV + v];
-      const double d = M.e_dual[e];
-      circ += ((sb >> j) & 1 ? -d : d) * u[e];
-    }
-    hv /= M.v_area[v];
-    if (!(hv > 0.0)) {
-      if (!T.vmask || ((T.vmask[v >> 5] >> (v & 31)) & 1u)) atomicMin(T.dry, M.v_orig[v]);
-      sPV[k] = 0.0;
-    } else {
-      sPV[k] = (M.f[v] + circ / M.v_area[v]) / hv;
-    }
-  }
-  // P2: kinetic energy and kite/A rows on C1
-#pragma unroll 2
-  for (int k = threadIdx.x; k < tm.nc1; k += kTileThreads) {
-    const int32_t i = k < tm.nc ? tm.c0 + k : T.c1_ids[tm.c1h_off + k - tm.nc];
-    const int deg = M.c_deg[i];
-    double acc = 0.0;
-#pragma unroll
-    for (int j = 0; j < kMaxDeg; ++j) {
-      if (j < deg) {
-        const int32_t e = M.c_edge[j * M.nC + i];
-        const double ue = u[e];
-        acc += M.e_ld[e] * ue * ue;
-        sR[k * kRStride + j] = M.c_ratio[j * M.nC + i];
-      }
-    }
-    sK[k] = acc / (4.0 * M.c_area[i]);
-  }
-  __syncthreads();
-  // P3: F, q~ and l on E_req
-#pragma unroll 2
-  for (int k = threadIdx.x; k < tm.ner; k += kTileThreads) {
-    const int32_t e = k < tm.ne ? tm.e0 + k : T.er_ids[tm.erh_off + k - tm.ne];
-    const int2 c = M.e_cells[e];
-    const ushort2 vl = T.er_vloc[tm.erv_off + k];
-    sF[k] = 0.5 * (h[c.x] + h[c.y]) * u[e];
-    sQ[k] = 0.5 * (sPV[vl.x] + sPV[vl.y]);
-    sL[k] = M.e_len[e];
-  }
-  __syncthreads();
-  // P4: thickness tendency on the tile's cells
-  for (int k = threadIdx.x; k < tm.nc; k += kTileThreads) {
-    const int32_t i = tm.c0 + k;
-    const int g = a.ckey ? a.ckey[i] : 0;
-    if (g > 5 || !((a.mask >> g) & 1u)) continue;
-    const int seg = g <= 2 ? 0 : 1;
-    const uint4 ring = T.c1_ring[tm.c1r_off + k];
-    const int deg = M.c_deg[i];
-    const uint8_t sb = M.c_sbits[i];
-    double acc = 0.0;
-#pragma unroll
-    for (int j = 0; j < kMaxDeg; ++j) {
-      if (j < deg) {
-        const int el = ring16(ring, j);
-        const double l = sL[el];
-        acc += ((sb >> j) & 1 ? -l : l) * sF[el];
-      }
-    }
-    apply_op(a.cop[seg], i, -acc / M.c_area[i]);
-  }
-  // P5: momentum tendency on the edges the tile owns
-#pragma unroll 2
-  for (int k = threadIdx.x; k < tm.ne; k += kTileThreads) {
-    const int32_t e = tm.e0 + k;
-    const int g = a.ekey ? a.ekey[e] : 0;
-    if (g > 4 || !((a.mask >> (6 + g)) & 1u)) continue;
-    const int seg = g <= 1 ? 0 : 1;
-    const ushort2 cl = T.oe_c1[e];
-    const double qt_e = sQ[k];
-    const double inv_d = M.e_invd[e];
-    const int2 cc = M.e_cells[e];
-    const uint8_t sl = M.e_slots[e];
-    double pvflux = 0.0;
-#pragma unroll
-    for (int side = 0; side < 2; ++side) {
-      const int32_t c = side ? cc.y : cc.x;
-      const int lc = side ? cl.y : cl.x;
-      const int p = side ? ((sl >> 3) & 7) : (sl & 7);
-      const unsigned aneg = (sl >> (6 + side)) & 1u;
-      const int deg = M.c_deg[c];
-      const uint8_t sb = M.c_sbits[c];
-      const uint4 ring = T.c1_ring[tm.c1r_off + lc];
-      const double* rr = sR + lc * kRStride;
-      double frac = 0.0;
-#pragma unroll
-      for (int kk = 1; kk < kMaxDeg; ++kk) {
-        if (kk < deg) {
-          int sp = p + kk - 1;
-          if (sp >= deg) sp -= deg;
-          int s = p + kk;
-          if (s >= deg) s -= deg;
-          frac += rr[sp];
-          const int el = ring16(ring, s);
-          const double x = frac - 0.5;
-          const double w = (((sb >> s) & 1u) ^ aneg) ? -x : x;
-          const double coef = w * (sL[el] * inv_d);
-          pvflux += coef * sF[el] * (0.5 * (qt_e + sQ[el]));
-        }
-      }
-    }
-    const double psi_lo = M.g * (h[cc.x] + M.b[cc.x]) + sK[cl.x];
-    const double psi_hi = M.g * (h[cc.y] + M.b[cc.y]) + sK[cl.y];
-    apply_op(a.eop[seg], e, -pvflux - (psi_lo - psi_hi) * inv_d);
-  }
-}
-
-// Drop dead intermediate lines from L2 without writing them back
-// (discard.global.L2, 128-byte lines): every evaluation rewrites PV, K and
-// (F, q~) before reading them.
-__global__ void k_discard(char* base, int64_t lines) {
-  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k < lines) asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + 128 * k) : "memory");
-}
-
-// tiles holding at least one output of a mask
-__global__ void k_mark_tiles(const int32_t* __restrict__ clist, int32_t nc,
-                             const int32_t* __restrict__ elist, int32_t ne,
-                             const int32_t* __restrict__ e_tile, uint8_t* __restrict__ flag,
-                             int32_t tile_cells) {
-  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < nc)
-    flag[clist[t] / tile_cells] = 1;
-  else if (t - nc < ne)
-    flag[e_tile[elist[t - nc]]] = 1;
-}
-
-}  // namespace mswm_dev
-
-namespace mswm_dev {
-
-// ---------------------------------------------------------------------------
-// Phases B + C fused per cell tile (opt-in MSWM_BC=1): (F, q~, l) of the edges
-// a tile needs live in shared memory instead of a round trip through HBM.
-// Tile t = cells [c0, c0+nc) and the edges whose lowest cell lies in them,
-// [e0, e0+ne) (edges are sorted by their cells); its halo = the other edges
-// its cells' rings and its edges' stencils read.  Local ids: owned edge e ->
-// e - e0, halo edge k -> ne + k.  Per-element operation order as
-// item_edge_fq / item_out_sp: bitwise the reference's.
-struct BcTile {
-  int32_t c0, nc, e0, ne, h_off, nh;
-};
-
-struct BcArgs {
-  const BcTile* tiles;
-  const int32_t* list;   // tiles holding outputs of this mask
-  int32_t ntiles;
-  const int32_t* halo;   // halo edge ids, per tile from h_off
-  const uint4* ring;     // [nC] local ids of the ring edges (u16 x 8)
-  const uint2* sten;     // [3][nE] local stencil ids, u16 pairs (as e_st16)
-};
-
-#ifndef MSWM_BC_MINB
-#define MSWM_BC_MINB 6
-#endif
-__global__ void __launch_bounds__(kBlock, MSWM_BC_MINB) k_bc(DevMesh M, BcArgs B,
-                                                               const double* __restrict__ h,
-                                                               const double* __restrict__ u,
-                                                               const double* __restrict__ pv,
-                                                               const double* __restrict__ psi,
-                                                               OutArgs a) {
-  extern __shared__ double2 sFQ[];
-  for (int32_t it = blockIdx.x; it < B.ntiles; it += gridDim.x) {
-    const BcTile T = B.tiles[B.list[it]];
-    const int32_t nl = T.ne + T.nh;
-    double* sL = reinterpret_cast<double*>(sFQ + nl);
-    // phase B on the tile's edges and halo (operators.cpp:61-62, :88-89)
-    for (int32_t k = threadIdx.x; k < nl; k += kBlock) {
-      const int32_t e = k < T.ne ? T.e0 + k : B.halo[T.h_off + k - T.ne];
-      const int2 c = M.e_cells[e];
-      const int2 v = M.e_verts[e];
-      const double F = 0.5 * (h[c.x] + h[c.y]) * u[e];
-      const double q = 0.5 * (pv[v.x] + pv[v.y]);
-      sFQ[k] = make_double2(F, q);
-      sL[k] = M.e_len[e];
-    }
-    __syncthreads();
-    // phase C: dh on the tile's cells, du on its edges, stage update fused
-    for (int32_t t = threadIdx.x; t < T.nc + T.ne; t += kBlock) {
-      if (t < T.nc) {
-        const int32_t i = T.c0 + t;
-        const int g = a.ckey ? a.ckey[i] : 0;
-        if (g > 5 || !((a.mask >> g) & 1u)) continue;
-        const int seg = g <= 2 ? 0 : 1;
-        const uint4 r = B.ring[i];
-        const uint32_t rw[4] = {r.x, r.y, r.z, r.w};
-        const int deg = M.c_deg[i];
-        const uint8_t sb = M.c_sbits[i];
-        double acc = 0.0;
-#pragma unroll
-        for (int j = 0; j < kFastDeg; ++j) {
-          const int el = int(j & 1 ? rw[j >> 1] >> 16 : rw[j >> 1] & 0xFFFFu);
-          const double l = sL[el];
-          const double x = ((sb >> j) & 1 ? -l : l) * sFQ[el].x;
-          if (j < deg) acc += x;
-        }
-        apply_op(a.cop[seg], i, -acc / M.c_area[i]);
-      } else {
-        const int32_t k = t - T.nc;
-        const int32_t e = T.e0 + k;
-        const int g = a.ekey ? a.ekey[e] : 0;
-        if (g > 4 || !((a.mask >> (6 + g)) & 1u)) continue;
-        const int seg = g <= 1 ? 0 : 1;
-        const double qt_e = sFQ[k].y;
-        const double inv_d = M.e_invd[e];
-        const int2 cc = M.e_cells[e];
-        const int nst = M.e_nst[e] & 0x7f;
-        uint32_t w[kFastSten / 2 + 1];
-#pragma unroll
-        for (int q = 0; q < (kFastSten / 2 + 1) / 2; ++q) {
-          const uint2 p = B.sten[q * M.nE + e];
-          w[2 * q] = p.x;
-          w[2 * q + 1] = p.y;
-        }
-        double pvflux = 0.0;
-#pragma unroll
-        for (int j = 0; j < kFastSten; j += 2) {
-          const double2 cp = M.e_coef2[(j >> 1) * M.nE + e];
-#pragma unroll
-          for (int b = 0; b < 2; ++b) {
-            const int el = int(b ? w[j >> 1] >> 16 : w[j >> 1] & 0xFFFFu);
-            const double2 fq = sFQ[el];
-            const double x = (b ? cp.y : cp.x) * fq.x * (0.5 * (qt_e + fq.y));
-            if (j + b < nst) pvflux += x;
-          }
-        }
-        const double du = -pvflux - (psi[cc.x] - psi[cc.y]) * inv_d;
-        apply_op(a.eop[seg], e, du);
-      }
-    }
-    __syncthreads();
-  }
-}
-
-}  // namespace mswm_dev
-
-namespace mswm_dev {
 
 // Move the parked coarse values of the concurrent LTS3 coarse step into the
 // state (see Op::alt): dst[i] = src[i] on the band lists.

@@ -143,19 +143,10 @@ struct MaskPlan {
     int32_t base = 0, n_range = 0, n_list = 0;
     const int32_t* list = nullptr;
     DArr<int32_t> own;
-    std::vector<int32_t> host_list;  // the list part, ascending
-    DArr<int32_t> lofs;              // dataflow path: per-slab offsets into list
     Span dev() const { return Span{base, n_range, list, n_list}; }
     int64_t n() const { return int64_t(n_range) + n_list; }
   } sv, sk, se, sc_out, se_out;
   DArr<uint32_t> vmask;  // closure bitmask for the dense dry-vertex check
-  DArr<int32_t> tiles;   // fused path: tiles holding outputs of this mask
-  int32_t ntiles = 0;
-  DArr<int32_t> bc_tiles;  // k_bc: cell tiles holding outputs of this mask
-  int32_t n_bc = 0;
-  bool use_tiles = false;
-  bool use_coop = false;  // small mask: one cooperative launch (k_fused_eval)
-  bool use_flow = false;  // large mask: one dataflow launch (k_flow)
   std::vector<int32_t> host_cells, host_edges;  // original ids, same order as device lists
 };
 
@@ -246,49 +237,16 @@ struct mswm_cuda_ctx {
   // device mesh
   DArr<int32_t> c_edge, c_vert, c_nbr, v_cell, v_edge, v_orig, e_sten;
   DArr<uint2> e_st16;
-  DArr<double2> e_coef2, v_kite01, v_af;
+  DArr<double2> e_coef2, v_af;
   DArr<int2> c_edge2, v_ce;
   int64_t n_sten_wide = 0;
-  DArr<uint8_t> c_deg, c_sbits, v_sbits, e_nst, e_slots;
-  DArr<double> c_area, c_ratio, v_kite, v_area, e_len, e_ld, e_dual, e_invd, e_coef, b, f;
-  bool ring_derived = false;
-  bool tile_path = false;
-  bool hybrid = false;
-  int32_t coop_blocks = 0;  // co-resident CTAs of k_fused_eval (0 = disabled)
-  bool l2_discard = true;
+  DArr<uint8_t> c_deg, c_sbits, v_sbits, e_nst;
+  DArr<double> c_area, v_kite, v_area, e_len, e_ld, e_dual, e_invd, b, f;
   // streamed kernels run a resident grid (persist_ctas CTAs per SM, 8 =
   // full occupancy at 32 registers) looping over their elements: 3.7 % faster
   // C4 steps than one CTA per 256 elements (CTA churn capped occupancy at
   // ~70 %); MSWM_PERSIST=0 restores one element per thread
   int persist_ctas[3] = {2048 / kSBlock, 2048 / kSBlock, 2048 / kSBlock}, n_sm = 148;  // A, B, C
-  // fused tile kernel structures (k_tile)
-  DArr<TileMeta> t_meta;
-  DArr<int32_t> t_c1_ids, t_er_ids, t_vr_ids, t_e_tile;
-  DArr<uint4> t_c1_ring;
-  DArr<ushort2> t_er_vloc, t_oe_c1;
-
-  int32_t n_tiles = 0, tile_cells = 0;
-  // phases B + C fused per cell tile (k_bc, opt-in MSWM_BC=1; see build_bc)
-  bool bc_ok = false;
-  int32_t bc_cells = 0, bc_ntiles = 0, bc_grid = 0;
-  size_t bc_smem = 0;
-  DArr<BcTile> bc_tiles;
-  DArr<int32_t> bc_halo, bc_e_tile;
-  DArr<uint4> bc_ring;
-  DArr<uint2> bc_sten;
-  // L2-blocked slabs of the three-kernel path (see build_slabs)
-  struct Slab {
-    int32_t c0, nc, e0, ne, v0, nv;
-    DArr<int32_t> khalo, ehalo, vhalo;
-  };
-  std::vector<Slab> slabs;
-  size_t tile_smem = 0;
-  // dataflow evaluation (k_flow): cell slabs, dependencies, item order
-  bool flow_ok = false;
-  int32_t flow_S = 0, flow_nS = 0, flow_grid = 0, flow_lag = 0;
-  const void* flow_fn = nullptr;
-  std::vector<int32_t> h_flow_v0, h_flow_e0;
-  DArr<int32_t> flow_v0, flow_e0, flow_dep_off, flow_dep, flow_order, flow_sync;
   DArr<int2> e_cells, e_verts;
   double gravity = 9.80616;
   bool have_fields = false;
@@ -317,12 +275,15 @@ struct mswm_cuda_ctx {
   DArr<int32_t> d_c_n2o, d_e_n2o;  // internal -> original ids (device permutes)
   DArr<double> io_h, io_u;          // staging for permuted uploads / downloads
   double time = 0.0;
-  DArr<int32_t> dry_vertex;
-  DArr<unsigned long long> dry_step;
-  DArr<int64_t> step_ctr;
+  // dry-vertex flag: (step << 32 | original vertex), ~0 = none; set by kernel
+  // A, cleared only after a synchronous check has reported it
+  DArr<unsigned long long> dry_flag;
+  DArr<int64_t> step_ctr;  // device copy of steps_issued (k_step_counter)
   int last_dry_vertex = -1;
-  int64_t last_dry_step = 0;
+  int64_t last_dry_step = 0;  // 1-based step of the batch it happened in, 0: an eval call
   int64_t steps_issued = 0;
+  // step batches issued since the flag was last consumed: (first global step, count)
+  std::vector<std::pair<int64_t, int64_t>> batches;
 
   // regions
   bool have_regions = false;
@@ -353,7 +314,13 @@ struct mswm_cuda_ctx {
   int64_t last_kernels_per_step = 0;
   const std::vector<EvalRecord>* last_records = nullptr;
 
+  // configuration generation: bumped whenever captured graphs may hold stale
+  // pointers or arguments (plans, halos, fields, communicators); group graphs
+  // (mswm_cuda_group) compare it to recapture
+  uint64_t gen = 0;
+
   void drop_graphs() {
+    ++gen;
     for (auto& kv : graphs) {
       cudaGraphExecDestroy(kv.second.exec);
       for (auto& r : kv.second.records) {
@@ -387,7 +354,6 @@ struct mswm_cuda_ctx {
     M.c_deg = c_deg.p;
     M.c_sbits = c_sbits.p;
     M.c_area = c_area.p;
-    M.c_ratio = (ring_derived || tile_path || hybrid) ? c_ratio.p : nullptr;
     M.v_cell = v_cell.p;
     M.v_edge = v_edge.p;
     M.v_kite = v_kite.p;
@@ -401,13 +367,11 @@ struct mswm_cuda_ctx {
     M.e_dual = e_dual.p;
     M.e_invd = e_invd.p;
     M.e_nst = e_nst.p;
-    M.e_slots = (ring_derived || tile_path || hybrid) ? e_slots.p : nullptr;
     M.e_sten = e_sten.p;
     M.e_st16 = e_st16.p;
     M.e_coef2 = e_coef2.p;
     M.c_edge2 = c_edge2.p;
     M.v_ce = v_ce.p;
-    M.v_kite01 = v_kite01.p;
     M.v_af = v_af.p;
     M.b = b.p;
     M.f = f.p;
@@ -573,532 +537,11 @@ void make_orders(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell_
       c->v_old2new[key[k].v] = k;
     }
   }
-  // (edges and vertices are always sorted by their cells so the tiles of
-  // the fused kernel own contiguous edge ranges)
   bool ident = true;
   for (int32_t k = 0; k < nC && ident; ++k) ident = c->c_new2old[k] == k;
   for (int32_t k = 0; k < nE && ident; ++k) ident = c->e_new2old[k] == k;
   for (int32_t k = 0; k < nV && ident; ++k) ident = c->v_new2old[k] == k;
   c->identity = ident;
-}
-
-// Cell tiles of k_bc (phases B + C fused): tile t = cells [t*TC, (t+1)*TC)
-// and the edges whose lowest cell lies in them (a contiguous range: edges
-// are sorted by their cells); the halo = the other edges the tile's rings
-// and stencils read.  Local ids are u16 (owned edges first, then the halo).
-// Needs hexagon/pentagon meshes (kFastDeg / kFastSten) and explicit tables.
-bool build_bc(mswm_cuda_ctx* c, const std::vector<int32_t>& c_edge,
-              const std::vector<uint8_t>& c_deg, const std::vector<int2>& e_cells,
-              const std::vector<int32_t>& e_sten, const std::vector<uint8_t>& e_nst) {
-  const int32_t nC = c->nC, nE = c->nE;
-  if (c->deg_max != kFastDeg || c->sten_max != kFastSten || e_sten.empty()) return false;
-  int32_t TC = 256;
-  if (const char* ts = std::getenv("MSWM_BC_CELLS")) TC = std::max(16, std::min(4096, std::atoi(ts)));
-  const int32_t nT = (nC + TC - 1) / TC;
-  std::vector<int32_t> e_tile(nE), e_first(size_t(nT) + 1, nE);
-  int32_t prev = -1;
-  for (int32_t e = 0; e < nE; ++e) {
-    const int32_t t = std::min(e_cells[e].x, e_cells[e].y) / TC;
-    if (t < prev) return false;
-    for (int32_t q = prev + 1; q <= t; ++q) e_first[q] = e;
-    prev = t;
-    e_tile[e] = t;
-  }
-  std::vector<BcTile> tiles(nT);
-  std::vector<int32_t> halo, emark(nE, -1), eloc(nE, 0), hl;
-  std::vector<uint4> ring(nC, make_uint4(0, 0, 0, 0));
-  std::vector<uint2> sten(size_t(3) * nE, make_uint2(0u, 0u));
-  size_t smem_max = 0;
-  for (int32_t t = 0; t < nT; ++t) {
-    BcTile& m = tiles[t];
-    m.c0 = t * TC;
-    m.nc = std::min(TC, nC - m.c0);
-    m.e0 = e_first[t];
-    m.ne = e_first[t + 1] - e_first[t];
-    for (int32_t e = m.e0; e < m.e0 + m.ne; ++e) {
-      emark[e] = t;
-      eloc[e] = e - m.e0;
-    }
-    hl.clear();
-    auto need = [&](int32_t e) {
-      if (emark[e] != t) {
-        emark[e] = t;
-        hl.push_back(e);
-      }
-    };
-    for (int32_t i = m.c0; i < m.c0 + m.nc; ++i)
-      for (int j = 0; j < c_deg[i]; ++j) need(c_edge[size_t(j) * nC + i]);
-    for (int32_t e = m.e0; e < m.e0 + m.ne; ++e)
-      for (int j = 0; j < (e_nst[e] & 0x7f); ++j) need(e_sten[size_t(j) * nE + e]);
-    std::sort(hl.begin(), hl.end());
-    if (m.ne + int64_t(hl.size()) > 65535) return false;
-    m.h_off = int32_t(halo.size());
-    m.nh = int32_t(hl.size());
-    for (size_t k = 0; k < hl.size(); ++k) {
-      eloc[hl[k]] = m.ne + int32_t(k);
-      halo.push_back(hl[k]);
-    }
-    for (int32_t i = m.c0; i < m.c0 + m.nc; ++i) {
-      uint32_t w[4] = {0, 0, 0, 0};
-      for (int j = 0; j < c_deg[i]; ++j)
-        w[j >> 1] |= uint32_t(eloc[c_edge[size_t(j) * nC + i]]) << (16 * (j & 1));
-      ring[i] = make_uint4(w[0], w[1], w[2], w[3]);
-    }
-    for (int32_t e = m.e0; e < m.e0 + m.ne; ++e) {
-      uint32_t w[6] = {0, 0, 0, 0, 0, 0};
-      for (int j = 0; j < (e_nst[e] & 0x7f); ++j)
-        w[j >> 1] |= uint32_t(eloc[e_sten[size_t(j) * nE + e]]) << (16 * (j & 1));
-      for (int q = 0; q < 3; ++q) sten[size_t(q) * nE + e] = make_uint2(w[2 * q], w[2 * q + 1]);
-    }
-    smem_max = std::max(smem_max, size_t(m.ne + m.nh) * 24);
-  }
-  if (smem_max > 200 * 1024) return false;
-  cudaStream_t s = c->stream;
-  c->bc_tiles.upload(tiles, s);
-  c->bc_halo.upload(halo, s);
-  c->bc_e_tile.upload(e_tile, s);
-  c->bc_ring.upload(ring, s);
-  c->bc_sten.upload(sten, s);
-  CK(cudaFuncSetAttribute(k_bc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_max)));
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bc, kBlock, smem_max));
-  c->bc_grid = std::max(1, per_sm) * c->n_sm;
-  c->bc_smem = smem_max;
-  c->bc_cells = TC;
-  c->bc_ntiles = nT;
-  CK(cudaStreamSynchronize(s));
-  return true;
-}
-
-// Is the caller's stencil the ring walk of mesh_build.cpp:133-154 with the
-// weight rule of :343-362?  If so (bitwise, every entry), the kernels
-// rebuild both from per-cell rows and the 120 B/edge stencil tables are not
-// needed.  Returns the per-cell kite/A rows and per-edge slot bytes.
-bool derive_ring_stencil(const mswm_mesh_desc* d, std::vector<double>& kite_of_slot,
-                         std::vector<uint8_t>& slots) {
-  const int32_t nC = d->n_cells, nE = d->n_edges;
-  const int32_t total = d->cell_offset[nC];
-  kite_of_slot.assign(total, 0.0);
-  // kite_area per ring slot from vertex_kite (mesh_build.cpp:330-341 inverted)
-  for (int32_t i = 0; i < nC; ++i)
-    for (int32_t j = d->cell_offset[i]; j < d->cell_offset[i + 1]; ++j) {
-      const int32_t v = d->cell_vertices[j];
-      int k = 0;
-      while (k < 3 && d->vertex_cells[3 * v + k] != i) ++k;
-      if (k == 3) return false;
-      kite_of_slot[j] = d->vertex_kite[3 * v + k];
-    }
-  slots.assign(nE, 0);
-  for (int32_t e = 0; e < nE; ++e) {
-    int pos = d->edge_edge_offset[e];
-    uint8_t sl = 0;
-    for (int side = 0; side < 2; ++side) {
-      const int32_t i = d->edge_cells[2 * e + side];
-      const int off = d->cell_offset[i], mm = d->cell_offset[i + 1] - off;
-      int p = 0;
-      while (p < mm && d->cell_edges[off + p] != e) ++p;
-      if (p == mm) return false;
-      const int32_t av = d->cell_vertices[off + p];
-      const double anchor = d->edge_vertices[2 * e] == av ? double(d->edge_vertex_sign[2 * e])
-                                                          : double(d->edge_vertex_sign[2 * e + 1]);
-      double frac = 0.0;
-      for (int k = 1; k < mm; ++k) {
-        frac += kite_of_slot[off + (p + k - 1) % mm] / d->cell_area[i];
-        const int32_t ep = d->cell_edges[off + (p + k) % mm];
-        const double cs = d->edge_cells[2 * ep] == i ? double(d->edge_cell_sign[2 * ep])
-                                                     : double(d->edge_cell_sign[2 * ep + 1]);
-        const double w = cs * anchor * (frac - 0.5);
-        if (pos >= d->edge_edge_offset[e + 1] || d->edge_edges[pos] != ep) return false;
-        if (std::memcmp(&w, &d->edge_weight[pos], 8) != 0) return false;
-        ++pos;
-      }
-      if (p > 7) return false;
-      sl |= uint8_t(p << (3 * side));
-      if (anchor < 0) sl |= uint8_t(1u << (6 + side));
-    }
-    if (pos != d->edge_edge_offset[e + 1]) return false;
-    slots[e] = sl;
-  }
-  return true;
-}
-
-// Tiles of the fused kernel: kTileCells consecutive internal cells; C1 = the
-// tile's cells plus their ring neighbours; E_req / V_req = ring edges /
-// vertices of C1; owned edges = edges whose lower internal cell is in the
-// tile (a contiguous range, edges being sorted by their cells).  Local ids
-// are uint16.
-// Tiles of the fused kernel: TC consecutive internal cells.  C1 = the tile's
-// cells plus their ring neighbours; E_req / V_req = ring edges / vertices of
-// C1.  The tile owns the edges and vertices whose lowest internal cell is in
-// the tile -- contiguous ranges, edges and vertices being sorted by their
-// cells -- and lists them first in its local numbering, so only halo elements
-// need index lists.  Local ids are uint16.  Returns false (three-kernel path)
-// when a closure does not fit (cell order without locality).
-bool build_tiles(mswm_cuda_ctx* c, const std::vector<int32_t>& c_edge,
-                 const std::vector<int32_t>& c_vert, const std::vector<int32_t>& c_nbr,
-                 const std::vector<uint8_t>& c_deg, const std::vector<int2>& e_cells,
-                 const std::vector<int2>& e_verts) {
-  const int32_t nC = c->nC, nE = c->nE, nV = c->nV;
-  int32_t TC = kTileCells;
-  if (const char* ts = std::getenv("MSWM_TILE_CELLS")) TC = std::max(32, std::min(1024, std::atoi(ts)));
-  const int32_t nT = (nC + TC - 1) / TC;
-  // owned ranges: first edge / vertex of every tile
-  auto ranges = [&](int32_t n, auto tile_of, std::vector<int32_t>& first) {
-    first.assign(nT + 1, n);
-    int32_t prev = -1;
-    for (int32_t x = 0; x < n; ++x) {
-      const int32_t t = tile_of(x);
-      if (t < prev) return false;
-      for (int32_t q = prev + 1; q <= t; ++q) first[q] = x;
-      prev = t;
-    }
-    for (int32_t q = prev + 1; q <= nT; ++q) first[q] = n;
-    return true;
-  };
-  // vertex -> min internal cell needs the vertex cells; recover them from the rings
-  std::vector<int32_t> vmin(nV, INT32_MAX);
-  for (int32_t i = 0; i < nC; ++i)
-    for (int j = 0; j < c_deg[i]; ++j) {
-      const int32_t v = c_vert[size_t(j) * nC + i];
-      vmin[v] = std::min(vmin[v], i);
-    }
-  std::vector<int32_t> e_first, v_first, e_tile(nE);
-  if (!ranges(nE, [&](int32_t e) { return std::min(e_cells[e].x, e_cells[e].y) / TC; }, e_first))
-    return false;
-  if (!ranges(nV, [&](int32_t v) { return vmin[v] / TC; }, v_first)) return false;
-  for (int32_t e = 0; e < nE; ++e) e_tile[e] = std::min(e_cells[e].x, e_cells[e].y) / TC;
-  std::vector<TileMeta> meta(nT);
-  std::vector<int32_t> c1h, erh, vrh;
-  std::vector<uint4> c1_ring;
-  std::vector<ushort2> er_vloc, oe_c1(nE);
-  std::vector<int32_t> cmark(nC, -1), emark(nE, -1), vmark(nV, -1);
-  std::vector<int32_t> cloc(nC, 0), eloc(nE, 0), vloc(nV, 0);
-  size_t smem_max = 0;
-  std::vector<int32_t> halo, ers, vrs;
-  for (int32_t t = 0; t < nT; ++t) {
-    TileMeta& m = meta[t];
-    m.c0 = t * TC;
-    m.nc = std::min(TC, nC - m.c0);
-    m.e0 = e_first[t];
-    m.ne = e_first[t + 1] - e_first[t];
-    m.v0 = v_first[t];
-    m.nvo = v_first[t + 1] - v_first[t];
-    // C1: tile cells, then halo (ascending)
-    for (int32_t i = m.c0; i < m.c0 + m.nc; ++i) {
-      cmark[i] = t;
-      cloc[i] = i - m.c0;
-    }
-    halo.clear();
-    for (int32_t i = m.c0; i < m.c0 + m.nc; ++i)
-      for (int j = 0; j < c_deg[i]; ++j) {
-        const int32_t nb = c_nbr[size_t(j) * nC + i];
-        if (cmark[nb] != t) {
-          cmark[nb] = t;
-          halo.push_back(nb);
-        }
-      }
-    std::sort(halo.begin(), halo.end());
-    m.c1h_off = int32_t(c1h.size());
-    for (size_t k = 0; k < halo.size(); ++k) {
-      cloc[halo[k]] = m.nc + int32_t(k);
-      c1h.push_back(halo[k]);
-    }
-    m.nc1 = m.nc + int32_t(halo.size());
-    // E_req / V_req: owned ranges first, then the rest ascending
-    for (int32_t e = m.e0; e < m.e0 + m.ne; ++e) {
-      emark[e] = t;
-      eloc[e] = e - m.e0;
-    }
-    for (int32_t v = m.v0; v < m.v0 + m.nvo; ++v) {
-      vmark[v] = t;
-      vloc[v] = v - m.v0;
-    }
-    ers.clear();
-    vrs.clear();
-    auto c1_cell = [&](int32_t k) { return k < m.nc ? m.c0 + k : halo[k - m.nc]; };
-    for (int32_t k = 0; k < m.nc1; ++k) {
-      const int32_t i = c1_cell(k);
-      for (int j = 0; j < c_deg[i]; ++j) {
-        const int32_t e = c_edge[size_t(j) * nC + i], v = c_vert[size_t(j) * nC + i];
-        if (emark[e] != t) {
-          emark[e] = t;
-          ers.push_back(e);
-        }
-        if (vmark[v] != t) {
-          vmark[v] = t;
-          vrs.push_back(v);
-        }
-      }
-    }
-    std::sort(ers.begin(), ers.end());
-    std::sort(vrs.begin(), vrs.end());
-    m.ner = m.ne + int32_t(ers.size());
-    m.nvr = m.nvo + int32_t(vrs.size());
-    if (m.nc1 > 65535 || m.ner > 65535 || m.nvr > 65535) return false;
-    m.erh_off = int32_t(erh.size());
-    for (size_t k = 0; k < ers.size(); ++k) {
-      eloc[ers[k]] = m.ne + int32_t(k);
-      erh.push_back(ers[k]);
-    }
-    m.vrh_off = int32_t(vrh.size());
-    for (size_t k = 0; k < vrs.size(); ++k) {
-      vloc[vrs[k]] = m.nvo + int32_t(k);
-      vrh.push_back(vrs[k]);
-    }
-    m.erv_off = int32_t(er_vloc.size());
-    for (int32_t k = 0; k < m.ner; ++k) {
-      const int32_t e = k < m.ne ? m.e0 + k : ers[k - m.ne];
-      const int2 v = e_verts[e];
-      if (vmark[v.x] != t || vmark[v.y] != t) return false;
-      er_vloc.push_back(make_ushort2(uint16_t(vloc[v.x]), uint16_t(vloc[v.y])));
-    }
-    m.c1r_off = int32_t(c1_ring.size());
-    for (int32_t k = 0; k < m.nc1; ++k) {
-      const int32_t i = c1_cell(k);
-      uint16_t r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int j = 0; j < c_deg[i]; ++j) r[j] = uint16_t(eloc[c_edge[size_t(j) * nC + i]]);
-      c1_ring.push_back(make_uint4(r[0] | (uint32_t(r[1]) << 16), r[2] | (uint32_t(r[3]) << 16),
-                                   r[4] | (uint32_t(r[5]) << 16), r[6] | (uint32_t(r[7]) << 16)));
-    }
-    for (int32_t e = m.e0; e < m.e0 + m.ne; ++e) {
-      const int2 cc = e_cells[e];
-      if (cmark[cc.x] != t || cmark[cc.y] != t) return false;
-      oe_c1[e] = make_ushort2(uint16_t(cloc[cc.x]), uint16_t(cloc[cc.y]));
-    }
-    const size_t smem = 8 * (size_t(m.nvr) + m.nc1 + size_t(m.nc1) * kRStride + 3 * size_t(m.ner));
-    smem_max = std::max(smem_max, smem);
-  }
-  if (smem_max > 200 * 1024) return false;  // poor locality: use the three-kernel path
-  cudaStream_t s = c->stream;
-  c->n_tiles = nT;
-  c->tile_cells = TC;
-  c->tile_smem = smem_max;
-  c->t_meta.upload(meta, s);
-  c->t_c1_ids.upload(c1h, s);
-  c->t_c1_ring.upload(c1_ring, s);
-  c->t_er_ids.upload(erh, s);
-  c->t_er_vloc.upload(er_vloc, s);
-  c->t_vr_ids.upload(vrh, s);
-  c->t_oe_c1.upload(oe_c1, s);
-  c->t_e_tile.upload(e_tile, s);
-  CK(cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_max)));
-  CK(cudaStreamSynchronize(s));
-  return true;
-}
-
-// L2 blocking of the three-kernel path: slabs of SC consecutive internal
-// cells (a compact region along the Hilbert curve).  A slab owns its cells,
-// the edges and vertices whose lowest internal cell it holds (contiguous
-// ranges) and lists the halo it additionally needs: K on the cells' ring
-// neighbours, (F, q~) on every ring edge of those cells, PV on their ring
-// vertices.  Evaluating a dense mask slab by slab (A, B, C per slab) keeps
-// each slab's intermediates and inputs L2-resident between the kernels.
-void build_slabs(mswm_cuda_ctx* c, const std::vector<int32_t>& c_edge,
-                 const std::vector<int32_t>& c_vert, const std::vector<int32_t>& c_nbr,
-                 const std::vector<uint8_t>& c_deg, const std::vector<int2>& e_cells) {
-  const int32_t nC = c->nC, nE = c->nE, nV = c->nV;
-  // Opt-in (MSWM_SLAB_CELLS): measured slower than one pass on C4 -- the
-  // kernel boundaries cost more than the L2 reuse saves (profiles/r1_*).
-  const char* ss = std::getenv("MSWM_SLAB_CELLS");
-  if (!ss) return;
-  const int32_t SC = std::max(1024, std::atoi(ss));
-  if (const char* dd = std::getenv("MSWM_L2_DISCARD")) c->l2_discard = dd[0] != '0';
-  c->slabs.clear();
-  const int32_t nS = (nC + SC - 1) / SC;
-  if (nS < 2) return;
-  std::vector<int32_t> vmin(nV, INT32_MAX);
-  for (int32_t i = 0; i < nC; ++i)
-    for (int j = 0; j < c_deg[i]; ++j) {
-      const int32_t v = c_vert[size_t(j) * nC + i];
-      vmin[v] = std::min(vmin[v], i);
-    }
-  // owned ranges (edges / vertices are sorted by their lowest cell)
-  std::vector<int32_t> ef(nS + 1, nE), vf(nS + 1, nV);
-  {
-    int32_t prev = -1;
-    for (int32_t e = 0; e < nE; ++e) {
-      const int32_t t = std::min(e_cells[e].x, e_cells[e].y) / SC;
-      if (t < prev) return;  // not sorted: no slabs
-      for (int32_t q = prev + 1; q <= t; ++q) ef[q] = e;
-      prev = t;
-    }
-    for (int32_t q = prev + 1; q <= nS; ++q) ef[q] = nE;
-    prev = -1;
-    for (int32_t v = 0; v < nV; ++v) {
-      const int32_t t = vmin[v] / SC;
-      if (t < prev) return;
-      for (int32_t q = prev + 1; q <= t; ++q) vf[q] = v;
-      prev = t;
-    }
-    for (int32_t q = prev + 1; q <= nS; ++q) vf[q] = nV;
-  }
-  std::vector<int32_t> cmark(nC, -1), emark(nE, -1), vmark(nV, -1);
-  std::vector<int32_t> kh, eh, vh;
-  c->slabs.resize(nS);
-  for (int32_t t = 0; t < nS; ++t) {
-    auto& sl = c->slabs[t];
-    sl.c0 = t * SC;
-    sl.nc = std::min(SC, nC - sl.c0);
-    sl.e0 = ef[t];
-    sl.ne = ef[t + 1] - ef[t];
-    sl.v0 = vf[t];
-    sl.nv = vf[t + 1] - vf[t];
-    kh.clear();
-    eh.clear();
-    vh.clear();
-    auto own_c = [&](int32_t i) { return i >= sl.c0 && i < sl.c0 + sl.nc; };
-    auto own_e = [&](int32_t e) { return e >= sl.e0 && e < sl.e0 + sl.ne; };
-    auto own_v = [&](int32_t v) { return v >= sl.v0 && v < sl.v0 + sl.nv; };
-    auto visit = [&](int32_t i) {  // ring edges / vertices of a C1 cell
-      for (int j = 0; j < c_deg[i]; ++j) {
-        const int32_t e = c_edge[size_t(j) * nC + i], v = c_vert[size_t(j) * nC + i];
-        if (!own_e(e) && emark[e] != t) {
-          emark[e] = t;
-          eh.push_back(e);
-        }
-        if (!own_v(v) && vmark[v] != t) {
-          vmark[v] = t;
-          vh.push_back(v);
-        }
-      }
-    };
-    for (int32_t i = sl.c0; i < sl.c0 + sl.nc; ++i) {
-      visit(i);
-      for (int j = 0; j < c_deg[i]; ++j) {
-        const int32_t nb = c_nbr[size_t(j) * nC + i];
-        if (!own_c(nb) && cmark[nb] != t) {
-          cmark[nb] = t;
-          kh.push_back(nb);
-        }
-      }
-    }
-    for (int32_t nb : kh) visit(nb);
-    std::sort(kh.begin(), kh.end());
-    std::sort(eh.begin(), eh.end());
-    std::sort(vh.begin(), vh.end());
-    sl.khalo.upload(kh, c->stream);
-    sl.ehalo.upload(eh, c->stream);
-    sl.vhalo.upload(vh, c->stream);
-    CK(cudaStreamSynchronize(c->stream));
-  }
-}
-
-// Dataflow evaluation (k_flow, kernels.cuh): cell slabs of S cells, the
-// edge / vertex range of each slab, each B / C item's dependency slabs and
-// the item order.  Needs edges and vertices sorted by their lowest cell
-// (make_orders guarantees it).  Opt-in (MSWM_FLOW=1; MSWM_FLOW_SLAB,
-// MSWM_FLOW_LAG, MSWM_FLOW_MINB tune): measured 1.7x slower than the three
-// streamed kernels on C4 (profiles/r1_fusion_experiments.md).
-void build_flow(mswm_cuda_ctx* c, const std::vector<int32_t>& v_cell,
-                const std::vector<int2>& e_cells, const std::vector<int2>& e_verts,
-                const std::vector<int32_t>& c_edge, const std::vector<uint8_t>& c_deg) {
-  c->flow_ok = false;
-  const char* fe = std::getenv("MSWM_FLOW");
-  if (!fe || fe[0] != '1') return;
-  const int32_t nC = c->nC, nE = c->nE, nV = c->nV;
-  int32_t S = 64;
-  if (const char* ss = std::getenv("MSWM_FLOW_SLAB")) S = std::max(8, std::atoi(ss));
-  const int32_t nS = (nC + S - 1) / S;
-  if (nS < 64) return;  // small meshes: launch latency, not traffic, dominates
-  std::vector<int32_t> e0(nS + 1, nE), v0(nS + 1, nV), vslab(nV);
-  int32_t prev = -1;
-  for (int32_t e = 0; e < nE; ++e) {
-    const int32_t t = std::min(e_cells[e].x, e_cells[e].y) / S;
-    if (t < prev) return;
-    for (int32_t q = prev + 1; q <= t; ++q) e0[q] = e;
-    prev = t;
-  }
-  for (int32_t q = prev + 1; q <= nS; ++q) e0[q] = nE;
-  prev = -1;
-  for (int32_t v = 0; v < nV; ++v) {
-    const int32_t t =
-        std::min(v_cell[v], std::min(v_cell[size_t(nV) + v], v_cell[2 * size_t(nV) + v])) / S;
-    if (t < prev) return;
-    vslab[v] = t;
-    for (int32_t q = prev + 1; q <= t; ++q) v0[q] = v;
-    prev = t;
-  }
-  for (int32_t q = prev + 1; q <= nS; ++q) v0[q] = nV;
-  auto eslab = [&](int32_t e) { return std::min(e_cells[e].x, e_cells[e].y) / S; };
-  // dependency lists: B_k at [k], C_k at [nS + k]; entries are flag indices
-  std::vector<int32_t> dep_off(2 * size_t(nS) + 1, 0), dep, mark(2 * size_t(nS), -1);
-  std::vector<int32_t> maxdep(2 * size_t(nS), 0);
-  dep.reserve(12 * size_t(nS));
-  int32_t item = 0;
-  auto add = [&](int32_t flag) {
-    if (mark[flag] == item) return;
-    mark[flag] = item;
-    dep.push_back(flag);
-    maxdep[item] = std::max(maxdep[item], flag % nS);
-  };
-  for (int32_t k = 0; k < nS; ++k, ++item) {
-    dep_off[item] = int32_t(dep.size());
-    for (int32_t e = e0[k]; e < e0[k + 1]; ++e) {
-      add(vslab[e_verts[e].x]);
-      add(vslab[e_verts[e].y]);
-    }
-  }
-  auto ring = [&](int32_t i) {
-    for (int j = 0; j < c_deg[i]; ++j) add(nS + eslab(c_edge[size_t(j) * nC + i]));
-  };
-  for (int32_t k = 0; k < nS; ++k, ++item) {
-    dep_off[item] = int32_t(dep.size());
-    for (int32_t i = k * S; i < std::min(nC, (k + 1) * S); ++i) ring(i);
-    for (int32_t e = e0[k]; e < e0[k + 1]; ++e)
-      for (int32_t i : {e_cells[e].x, e_cells[e].y}) {
-        add(i / S);
-        ring(i);
-      }
-  }
-  dep_off[item] = int32_t(dep.size());
-  int per_sm = 0, n_sm = 0;
-  int minb = 8;
-  if (const char* mb = std::getenv("MSWM_FLOW_MINB")) minb = std::atoi(mb);
-  c->flow_fn = minb >= 8 ? reinterpret_cast<const void*>(k_flow<8>)
-               : minb >= 6 ? reinterpret_cast<const void*>(k_flow<6>)
-                           : reinterpret_cast<const void*>(k_flow<4>);
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->flow_fn, kBlock, 0));
-  CK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, c->device));
-  if (per_sm < 1) return;
-  c->flow_grid = per_sm * n_sm;
-  // Producers run `lag` slabs ahead of their consumers -- about a third of
-  // the warps in flight -- so a consumer's inputs are complete when it starts.
-  int32_t lag = c->flow_grid * (kBlock / 32) / 3;
-  if (const char* sl = std::getenv("MSWM_FLOW_LAG")) lag = std::max(1, std::atoi(sl));
-  lag = std::min(lag, nS);
-  // B_k follows A_{max(k, deps) + lag}; C_k follows B_{max deps + lag}
-  std::vector<std::vector<int32_t>> bq(nS), cq(nS);
-  for (int32_t k = 0; k < nS; ++k) {
-    bq[std::min(nS - 1, std::max(k, maxdep[k]) + lag)].push_back(k);
-    cq[std::min(nS - 1, std::max(k, maxdep[nS + k]) + lag)].push_back(k);
-  }
-  // B buckets are keyed by k + lag, so B slabs come out in index order and
-  // C_k, emitted right after B_m, finds every B slab <= m (and every A slab
-  // <= m, which precede B_m) already in the order: the order is topological.
-  std::vector<int32_t> order;
-  order.reserve(3 * size_t(nS));
-  for (int32_t k = 0; k < nS; ++k) {
-    order.push_back(k);
-    for (int32_t b : bq[k]) {
-      order.push_back((1 << 28) | b);
-      for (int32_t j : cq[b]) order.push_back((2 << 28) | j);
-    }
-  }
-  if (int32_t(order.size()) != 3 * nS) throw Error(MSWM_E_CONFIG, "flow order construction");
-  cudaStream_t s = c->stream;
-  c->flow_v0.upload(v0, s);
-  c->flow_e0.upload(e0, s);
-  c->flow_dep_off.upload(dep_off, s);
-  c->flow_dep.upload(dep, s);
-  c->flow_order.upload(order, s);
-  c->flow_sync.alloc(2 * size_t(nS));
-  CK(cudaStreamSynchronize(s));
-  c->h_flow_v0 = std::move(v0);
-  c->h_flow_e0 = std::move(e0);
-  c->flow_S = S;
-  c->flow_nS = nS;
-  c->flow_lag = lag;
-  c->flow_ok = true;
 }
 
 void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell_order) {
@@ -1145,39 +588,18 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   const auto& eo = c->e_old2new;
   const auto& vo = c->v_old2new;
 
-  std::vector<double> kite_of_slot;
-  std::vector<uint8_t> slots;
-  // Evaluation path (MSWM_KERNELS): "explicit" (default); "auto" = "explicit" for
-  // near-full masks and "tile" for small ones; "explicit" = three kernels
-  // streaming the stencil tables (DRAM-roofline-bound, profiles/); "tile" = the fused tile
-  // kernel, needs the ring-derived stencil; "explicit" = three kernels with
-  // the stencil tables streamed; "ringwalk" = three kernels walking the
-  // rings through L1.  Meshes whose stencil is not the reference builder's
-  // ring walk always take "explicit".  Tests cover all three.
   if (const char* pe = std::getenv("MSWM_PERSIST")) {  // "n" or "a,b,c"
     int v[3];
     const int k = std::sscanf(pe, "%d,%d,%d", &v[0], &v[1], &v[2]);
     for (int j = 0; j < 3; ++j) c->persist_ctas[j] = std::max(0, k == 3 ? v[j] : v[0]);
   }
   CK(cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, c->device));
-  const bool eligible = derive_ring_stencil(d, kite_of_slot, slots);
-  const char* kv = std::getenv("MSWM_KERNELS");
-  const std::string kind = kv ? kv : "explicit";
-  c->tile_path = eligible && kind == "tile";
-  c->ring_derived = eligible && kind == "ringwalk";
-  // "auto": three streamed kernels for near-full masks, the one-launch tile
-  // kernel for small masks (the LTS substeps), where launches dominate
-  c->hybrid = eligible && kind == "auto";
-  const bool need_ratio = c->tile_path || c->ring_derived || c->hybrid;
-  bool need_explicit = !(c->tile_path || c->ring_derived);
 
   // cells
   std::vector<int32_t> c_edge(size_t(deg_max) * nC, 0), c_vert(size_t(deg_max) * nC, 0),
       c_nbr(size_t(deg_max) * nC, 0);
   std::vector<uint8_t> c_deg(nC), c_sbits(nC, 0);
   std::vector<double> c_area(nC);
-  std::vector<double> c_ratio;
-  if (need_ratio) c_ratio.assign(size_t(deg_max) * nC, 0.0);
   for (int32_t ni = 0; ni < nC; ++ni) {
     const int32_t i = cn[ni];
     const int off = d->cell_offset[i], deg = d->cell_offset[i + 1] - off;
@@ -1193,8 +615,6 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
       // cell_sign(e, i) (mesh.hpp:89-92)
       const int8_t sg = d->edge_cells[2 * e] == i ? d->edge_cell_sign[2 * e] : d->edge_cell_sign[2 * e + 1];
       if (sg < 0) c_sbits[ni] |= uint8_t(1u << j);
-      // mesh_build.cpp:354: kite_area[slot] / cell_area[i]
-      if (need_ratio) c_ratio[size_t(j) * nC + ni] = kite_of_slot[off + j] / d->cell_area[i];
     }
   }
   c->h_cell_area.assign(d->cell_area, d->cell_area + nC);
@@ -1224,15 +644,8 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
     e_cells[ne] = make_int2(co[d->edge_cells[2 * e]], co[d->edge_cells[2 * e + 1]]);
     e_verts[ne] = make_int2(vo[d->edge_vertices[2 * e]], vo[d->edge_vertices[2 * e + 1]]);
   }
-  if ((c->tile_path || c->hybrid) && !build_tiles(c, c_edge, c_vert, c_nbr, c_deg, e_cells, e_verts)) {
-    c->tile_path = false;  // closures too large for shared memory (poor cell order)
-    c->hybrid = false;
-    need_explicit = true;
-  }
-  if (!c->tile_path) build_slabs(c, c_edge, c_vert, c_nbr, c_deg, e_cells);
-  if (!c->tile_path) build_flow(c, v_cell, e_cells, e_verts, c_edge, c_deg);
   std::vector<double> e_len(nE), e_ld(nE), e_dual(nE), e_invd(nE);
-  std::vector<uint8_t> e_nst, e_slots;
+  std::vector<uint8_t> e_nst;
   std::vector<int32_t> e_sten;
   // built directly in their packed layouts (no int32 / f64 staging copies:
   // C5's tables are ~10 GB each on the host)
@@ -1243,13 +656,10 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   // int32 table only (A/B runs)
   const char* s16 = std::getenv("MSWM_ST16");
   const bool use16 = sten_max < 0x80 && !(s16 && s16[0] == '0');
-  if (need_ratio) e_slots.resize(nE);
-  if (need_explicit) {
-    e_nst.resize(nE);
-    e_sten.assign(size_t(std::max(sten_max, 1)) * nE, 0);
-    e_coef2.assign(size_t((std::max(sten_max, 1) + 1) / 2) * nE, make_double2(0.0, 0.0));
-    if (use16) e_st16p.assign(size_t((n_words + 1) / 2) * nE, make_uint2(0u, 0u));
-  }
+  e_nst.resize(nE);
+  e_sten.assign(size_t(std::max(sten_max, 1)) * nE, 0);
+  e_coef2.assign(size_t((std::max(sten_max, 1) + 1) / 2) * nE, make_double2(0.0, 0.0));
+  if (use16) e_st16p.assign(size_t((n_words + 1) / 2) * nE, make_uint2(0u, 0u));
   for (int32_t ne = 0; ne < nE; ++ne) {
     const int32_t e = en[ne];
     const int32_t c0 = d->edge_cells[2 * e], c1 = d->edge_cells[2 * e + 1];
@@ -1262,8 +672,6 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
     e_ld[ne] = l * dd;              // operators.cpp:70, first product
     const double inv_d = 1.0 / dd;  // operators.cpp:103
     e_invd[ne] = inv_d;
-    if (need_ratio) e_slots[ne] = slots[e];
-    if (!need_explicit) continue;
     const int off = d->edge_edge_offset[e], n = d->edge_edge_offset[e + 1] - off;
     e_nst[ne] = uint8_t(n);
     for (int j = 0; j < n; ++j) {
@@ -1297,9 +705,6 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   c->n_sten_wide = 0;
   for (const uint8_t x : e_nst) c->n_sten_wide += x >> 7;
   put(c->e_st16, e_st16p);
-  if (const char* bc = std::getenv("MSWM_BC"))
-    if (bc[0] == '1' && !c->tile_path && !c->ring_derived && !c->hybrid)
-      c->bc_ok = build_bc(c, c_edge, c_deg, e_cells, e_sten, e_nst);
   put(c->e_sten, e_sten);
   put(c->e_nst, e_nst);
   {
@@ -1316,12 +721,8 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
       for (int k = 0; k < 3; ++k)
         v_ce[size_t(k) * nV + v] = make_int2(v_cell[size_t(k) * nV + v], v_edge[size_t(k) * nV + v]);
     put(c->v_ce, v_ce);
-    std::vector<double2> v_kite01(nV), v_af(nV);
-    for (int32_t v = 0; v < nV; ++v) {
-      v_kite01[v] = make_double2(v_kite[v], v_kite[size_t(nV) + v]);
-      v_af[v] = make_double2(v_area[v], 0.0);  // f_v filled by set_fields
-    }
-    put(c->v_kite01, v_kite01);
+    std::vector<double2> v_af(nV);
+    for (int32_t v = 0; v < nV; ++v) v_af[v] = make_double2(v_area[v], 0.0);  // f_v: set_fields
     put(c->v_af, v_af);
   }
   put(c->c_edge, c_edge);
@@ -1330,7 +731,6 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   put(c->c_deg, c_deg);
   put(c->c_sbits, c_sbits);
   put(c->c_area, c_area);
-  put(c->c_ratio, c_ratio);
   put(c->v_cell, v_cell);
   put(c->v_edge, v_edge);
   put(c->v_orig, v_orig);
@@ -1343,7 +743,6 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   put(c->e_ld, e_ld);
   put(c->e_dual, e_dual);
   put(c->e_invd, e_invd);
-  put(c->e_slots, e_slots);
   CK(cudaStreamSynchronize(s));  // host vectors die here
 
   // state + workspace, zero-initialised
@@ -1374,8 +773,8 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   c->b.zero(s);
   c->f.alloc(nV);
   c->f.zero(s);
-  c->dry_vertex.alloc(1);
-  c->dry_step.alloc(1);
+  c->dry_flag.alloc(1);
+  CK(cudaMemsetAsync(c->dry_flag.p, 0xFF, 8, s));
   c->step_ctr.alloc(1);
   c->step_ctr.zero(s);
   // identity lists for evaluation without regions
@@ -1387,22 +786,29 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   CK(cudaStreamSynchronize(s));
 }
 
-void reset_dry(mswm_cuda_ctx* c) {
-  const int32_t big = INT_MAX;
-  const unsigned long long none = ~0ull;
-  CK(cudaMemcpyAsync(c->dry_vertex.p, &big, 4, cudaMemcpyHostToDevice, c->stream));
-  CK(cudaMemcpyAsync(c->dry_step.p, &none, 8, cudaMemcpyHostToDevice, c->stream));
+// Synchronise and consume the dry-vertex flag: if kernel A hit a dry vertex
+// since the last check, clear the flag and throw DryVertexError with the step
+// ("during step k of n" of the batch it happened in, harness.cpp:183-190).
+void check_dry(mswm_cuda_ctx* c, const char* who = nullptr) {
+  unsigned long long v = ~0ull;
+  CK(cudaMemcpyAsync(&v, c->dry_flag.p, 8, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-}
-
-// Reads the dry flag; returns true if a dry vertex was hit.
-bool read_dry(mswm_cuda_ctx* c) {
-  int32_t v = INT_MAX;
-  CK(cudaMemcpyAsync(&v, c->dry_vertex.p, 4, cudaMemcpyDeviceToHost, c->stream));
+  const auto batches = std::move(c->batches);
+  c->batches.clear();
+  if (v == ~0ull) return;
+  CK(cudaMemsetAsync(c->dry_flag.p, 0xFF, 8, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  if (v == INT_MAX) return false;
-  c->last_dry_vertex = v;
-  return true;
+  c->last_dry_vertex = int(uint32_t(v & 0xFFFFFFFFu));
+  const int64_t gstep = int64_t(v >> 32);
+  std::string msg = (who ? std::string(who) + ": " : std::string()) + "vertex " +
+                    std::to_string(c->last_dry_vertex) + " has non-positive thickness";
+  c->last_dry_step = 0;
+  for (const auto& b : batches)
+    if (gstep > b.first && gstep <= b.first + b.second) {
+      c->last_dry_step = gstep - b.first;
+      msg += " (during step " + std::to_string(gstep - b.first) + " of " + std::to_string(b.second) + ")";
+    }
+  throw Error(MSWM_E_DRY_VERTEX, msg);
 }
 
 // ---------------------------------------------------------------------------
@@ -1449,7 +855,6 @@ void make_span(mswm_cuda_ctx* c, const int32_t* d_list, int32_t n, int32_t unive
     if (!rest.empty()) {
       out.own.upload(rest, c->stream);
       out.list = out.own.p;
-      out.host_list = std::move(rest);
     }
     return;
   }
@@ -1460,7 +865,6 @@ void make_span(mswm_cuda_ctx* c, const int32_t* d_list, int32_t n, int32_t unive
   out.own.upload(h, c->stream);
   out.list = out.own.p;
   out.n_list = n;
-  out.host_list = std::move(h);
 }
 
 MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
@@ -1554,62 +958,6 @@ MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
   debug_mem("plan_for: spans");
   // supersets need the closure bitmask for the dry check
   if (p->sv.n() > p->nv) p->dense_v = true;
-  p->use_coop = c->coop_blocks > 0 && !c->tile_path &&
-                int64_t(p->nc) + p->ne < (int64_t(c->nC) + c->nE) / 5;
-  p->use_tiles = c->tile_path ||
-                 (c->hybrid && int64_t(p->nc) + p->ne < (int64_t(c->nC) + c->nE) / 5);
-  p->use_flow = c->flow_ok && !p->use_tiles && !p->use_coop && c->slabs.empty() &&
-                int64_t(p->nc) + p->ne >= (int64_t(c->nC) + c->nE) / 4;
-  if (p->use_flow) {
-    // per-slab offsets of the spans' list parts (kind 0 cells, 1 edges, 2 vertices)
-    const int32_t nS = c->flow_nS, S = c->flow_S;
-    auto lofs = [&](MaskPlan::HSpan& sp, int kind) {
-      if (!sp.n_list) return;
-      std::vector<int32_t> o(size_t(nS) + 1);
-      for (int32_t k = 0; k < nS; ++k) {
-        const int32_t bound = kind == 0 ? k * S : kind == 1 ? c->h_flow_e0[k] : c->h_flow_v0[k];
-        o[k] = int32_t(std::lower_bound(sp.host_list.begin(), sp.host_list.end(), bound) -
-                       sp.host_list.begin());
-      }
-      o[nS] = sp.n_list;
-      sp.lofs.upload(o, s);
-    };
-    lofs(p->sv, 2);
-    lofs(p->sk, 0);
-    lofs(p->se, 1);
-    lofs(p->sc_out, 0);
-    lofs(p->se_out, 1);
-  }
-  if (p->use_tiles) {
-    // tiles with outputs; the tiles compute closure supersets, so the dry
-    // check always consults the closure bitmask
-    p->dense_v = true;
-    DArr<uint8_t> tflag;
-    tflag.alloc(size_t(c->n_tiles));
-    tflag.zero(s);
-    if (int64_t(p->nc) + p->ne > 0) {
-      k_mark_tiles<<<nblk(int64_t(p->nc) + p->ne), kBlock, 0, s>>>(p->cells, p->nc, p->edges, p->ne,
-                                                                  c->t_e_tile.p, tflag.p,
-                                                                  c->tile_cells);
-      CK(cudaGetLastError());
-    }
-    k_flag_key<<<nblk(c->n_tiles), kBlock, 0, s>>>(c->n_tiles, tflag.p, key.p);
-    p->ntiles = int32_t(compact(c, key.p, c->n_tiles, 1, p->tiles)[0]);
-  }
-  if (c->bc_ok && !p->use_tiles && !p->use_coop && !p->use_flow) {
-    DArr<uint8_t> tflag, key;
-    tflag.alloc(size_t(c->bc_ntiles));
-    tflag.zero(s);
-    key.alloc(size_t(c->bc_ntiles));
-    if (int64_t(p->nc) + p->ne > 0) {
-      k_mark_tiles<<<nblk(int64_t(p->nc) + p->ne), kBlock, 0, s>>>(p->cells, p->nc, p->edges, p->ne,
-                                                                  c->bc_e_tile.p, tflag.p,
-                                                                  c->bc_cells);
-      CK(cudaGetLastError());
-    }
-    k_flag_key<<<nblk(c->bc_ntiles), kBlock, 0, s>>>(c->bc_ntiles, tflag.p, key.p);
-    p->n_bc = int32_t(compact(c, key.p, c->bc_ntiles, 1, p->bc_tiles)[0]);
-  }
   if (p->dense_v && p->nv < c->nV) {
     p->vmask.alloc((size_t(c->nV) + 31) / 32);
     k_pack_bits<<<nblk((int64_t(c->nV) + 31) / 32), kBlock, 0, s>>>(c->nV, mv.p, p->vmask.p);
@@ -1672,7 +1020,7 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
     return side && side->ctas_per_sm[kernel] > 0 ? std::min(g, side->ctas_per_sm[kernel] * c->n_sm)
                                                  : g;
   };
-  if (pred && !(p.use_coop && !p.use_tiles) && int64_t(pred->nc) + pred->ne > 0) {
+  if (pred && int64_t(pred->nc) + pred->ne > 0) {
     k_predict<<<nblk(int64_t(pred->nc) + pred->ne), kBlock, 0, s>>>(
         pred->clist, pred->nc, pred->elist, pred->ne, pred->c0, pred->c1, pred->c2, pred->hs0,
         pred->hs1, pred->hs2, pred->hdst, pred->us0, pred->us1, pred->us2, pred->udst);
@@ -1693,198 +1041,13 @@ void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const dou
     rec->ne = p.ne;
     CK(cudaEventRecordWithFlags(rec->start, s, cudaEventRecordExternal));
   }
-  if (p.use_tiles) {
-    if (p.ntiles > 0) {
-      TileArgs T;
-      T.meta = c->t_meta.p;
-      T.list = p.tiles.p;
-      T.c1_ids = c->t_c1_ids.p;
-      T.c1_ring = c->t_c1_ring.p;
-      T.er_ids = c->t_er_ids.p;
-      T.er_vloc = c->t_er_vloc.p;
-      T.vr_ids = c->t_vr_ids.p;
-      T.oe_c1 = c->t_oe_c1.p;
-      T.vmask = p.vmask.p;
-      T.dry = c->dry_vertex.p;
-      OutArgs a;
-      std::memset(&a, 0, sizeof(a));
-      a.mask = p.mask;
-      a.ckey = c->have_regions ? c->ckey.p : nullptr;
-      a.ekey = c->have_regions ? c->ekey.p : nullptr;
-      a.cop[0] = cop[0];
-      a.cop[1] = cop[1];
-      a.eop[0] = eop[0];
-      a.eop[1] = eop[1];
-      k_tile<<<p.ntiles, kTileThreads, c->tile_smem, s>>>(M, T, h, u, a);
-      CK(cudaGetLastError());
-      ++c->launches;
-    }
-    if (rec) CK(cudaEventRecordWithFlags(rec->stop, s, cudaEventRecordExternal));
-    return;
-  }
-  if (p.dense_v && p.dense_k && p.dense_fq && p.dense_out && c->slabs.size() > 1) {
-    // L2-blocked: A, B, C per slab so a slab's intermediates and re-read
-    // inputs are still in L2 when the next kernel reads them; then drop the
-    // slab's dead intermediates from L2 without write-back.
-    for (auto& sl : c->slabs) {
-      const Span vs{sl.v0, sl.nv, sl.vhalo.p, int32_t(sl.vhalo.n)};
-      const Span ks{sl.c0, sl.nc, sl.khalo.p, int32_t(sl.khalo.n)};
-      const Span es{sl.e0, sl.ne, sl.ehalo.p, int32_t(sl.ehalo.n)};
-      const int64_t na = int64_t(vs.n_range) + vs.n_list + ks.n_range + ks.n_list;
-      k_vertex_cell<<<nblk(na, kSBlock), kSBlock, 0, s>>>(M, h, u, vs, ks, c->pv.p, c->K.p, c->dry_vertex.p,
-                                               p.vmask.p);
-      const int64_t nb_ = int64_t(es.n_range) + es.n_list;
-      k_edge_fq<<<nblk(nb_, kSBlock), kSBlock, 0, s>>>(M, h, u, c->pv.p, es, c->FQ.p);
-      OutArgs a;
-      std::memset(&a, 0, sizeof(a));
-      a.mask = p.mask;
-      a.ckey = c->have_regions ? c->ckey.p : nullptr;
-      a.ekey = c->have_regions ? c->ekey.p : nullptr;
-      a.cs = Span{sl.c0, sl.nc, nullptr, 0};
-      a.es = Span{sl.e0, sl.ne, nullptr, 0};
-      a.cop[0] = cop[0];
-      a.cop[1] = cop[1];
-      a.eop[0] = eop[0];
-      a.eop[1] = eop[1];
-      k_out<<<nblk(int64_t(sl.nc) + sl.ne, kSBlock), kSBlock, 0, s>>>(M, h, c->K.p, c->FQ.p, a);
-      CK(cudaGetLastError());
-      c->launches += 3;
-      if (c->l2_discard) {
-        auto drop = [&](void* base, size_t bytes_lo, size_t bytes_hi) {
-          const size_t lo = (bytes_lo + 127) / 128, hi = bytes_hi / 128;
-          if (hi > lo) {
-            k_discard<<<nblk(int64_t(hi - lo)), kBlock, 0, s>>>(static_cast<char*>(base) + 128 * lo,
-                                                              int64_t(hi - lo));
-            ++c->launches;
-          }
-        };
-        drop(c->FQ.p, size_t(sl.e0) * 16, size_t(sl.e0 + sl.ne) * 16);
-        drop(c->pv.p, size_t(sl.v0) * 8, size_t(sl.v0 + sl.nv) * 8);
-        drop(c->K.p, size_t(sl.c0) * 8, size_t(sl.c0 + sl.nc) * 8);
-        CK(cudaGetLastError());
-      }
-    }
-    if (rec) CK(cudaEventRecordWithFlags(rec->stop, s, cudaEventRecordExternal));
-    return;
-  }
-  // The dataflow launch overlaps the phases, so a stage update must not
-  // write the arrays the evaluation reads.
-  bool flow = p.use_flow;
-  for (int g = 0; g < 2 && flow; ++g)
-    for (const Op* o : {&cop[g], &eop[g]})
-      flow &= o->dst != h && o->dst != u && o->acc != h && o->acc != u;
-  if (flow) {
-    auto fspan = [](const MaskPlan::HSpan& sp) {
-      return FlowSpan{sp.base, sp.n_range, sp.list, sp.n_list ? sp.lofs.p : nullptr};
-    };
-    FlowArgs fa;
-    std::memset(&fa, 0, sizeof(fa));
-    fa.M = M;
-    fa.h = h;
-    fa.u = u;
-    fa.vs = fspan(p.sv);
-    fa.ks = fspan(p.sk);
-    fa.es = fspan(p.se);
-    fa.cs = fspan(p.sc_out);
-    fa.eo = fspan(p.se_out);
-    fa.slab_v0 = c->flow_v0.p;
-    fa.slab_e0 = c->flow_e0.p;
-    fa.dep_off = c->flow_dep_off.p;
-    fa.dep = c->flow_dep.p;
-    fa.order = c->flow_order.p;
-    fa.S = c->flow_S;
-    fa.nS = c->flow_nS;
-    fa.n_items = int32_t(c->flow_order.n);
-    fa.flags = c->flow_sync.p;
-    fa.pv = c->pv.p;
-    fa.K = c->K.p;
-    fa.FQ = c->FQ.p;
-    fa.dry = c->dry_vertex.p;
-    fa.vmask = p.vmask.p;
-    fa.out.mask = p.mask;
-    fa.out.ckey = c->have_regions ? c->ckey.p : nullptr;
-    fa.out.ekey = c->have_regions ? c->ekey.p : nullptr;
-    fa.out.cop[0] = cop[0];
-    fa.out.cop[1] = cop[1];
-    fa.out.eop[0] = eop[0];
-    fa.out.eop[1] = eop[1];
-    CK(cudaMemsetAsync(c->flow_sync.p, 0, c->flow_sync.n * sizeof(int32_t), s));
-    void* args[] = {&fa};
-    // cooperative: every CTA is resident, so a warp never waits on an item
-    // held by a CTA that has not started
-    CK(cudaLaunchCooperativeKernel(c->flow_fn, dim3(c->flow_grid), dim3(kBlock),
-                                   args, 0, s));
-    ++c->launches;
-    if (rec) CK(cudaEventRecordWithFlags(rec->stop, s, cudaEventRecordExternal));
-    return;
-  }
   const Span vs = p.sv.dev(), ks = p.sk.dev(), es = p.se.dev();
   const int64_t na = p.sv.n() + p.sk.n();
-  if (p.use_coop) {
-    FusedArgs f;
-    std::memset(&f, 0, sizeof(f));
-    f.M = M;
-    f.h = h;
-    f.u = u;
-    f.vs = vs;
-    f.ks = ks;
-    f.es = es;
-    f.pv = c->pv.p;
-    f.K = c->K.p;
-    f.FQ = c->FQ.p;
-    f.dry = c->dry_vertex.p;
-    f.vmask = p.vmask.p;
-    f.out.cs = p.sc_out.dev();
-    f.out.es = p.se_out.dev();
-    f.out.mask = p.mask;
-    f.out.ckey = c->have_regions ? c->ckey.p : nullptr;
-    f.out.ekey = c->have_regions ? c->ekey.p : nullptr;
-    f.out.cop[0] = cop[0];
-    f.out.cop[1] = cop[1];
-    f.out.eop[0] = eop[0];
-    f.out.eop[1] = eop[1];
-    int64_t work = std::max<int64_t>(std::max<int64_t>(na, p.se.n()), p.sc_out.n() + p.se_out.n());
-    if (pred) {
-      f.pred = *pred;
-      f.has_pred = 1;
-      work = std::max<int64_t>(work, int64_t(pred->nc) + pred->ne);
-    }
-    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(c->coop_blocks, nblk(work))));
-    void* args[] = {&f};
-    CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_fused_eval), dim3(grid), dim3(kBlock),
-                                   args, 0, s));
-    ++c->launches;
-    if (rec) CK(cudaEventRecordWithFlags(rec->stop, s, cudaEventRecordExternal));
-    return;
-  }
   if (na > 0) {
     k_vertex_cell<<<grid(na, 0), kSBlock, 0, s>>>(M, h, u, vs, ks, pv, Kp,
-                                                 c->dry_vertex.p, p.vmask.p);
+                                                 c->dry_flag.p, c->step_ctr.p, p.vmask.p);
     CK(cudaGetLastError());
     ++c->launches;
-  }
-  if (p.n_bc > 0) {
-    BcArgs B;
-    B.tiles = c->bc_tiles.p;
-    B.list = p.bc_tiles.p;
-    B.ntiles = p.n_bc;
-    B.halo = c->bc_halo.p;
-    B.ring = c->bc_ring.p;
-    B.sten = c->bc_sten.p;
-    OutArgs a;
-    std::memset(&a, 0, sizeof(a));
-    a.mask = p.mask;
-    a.ckey = c->have_regions ? c->ckey.p : nullptr;
-    a.ekey = c->have_regions ? c->ekey.p : nullptr;
-    a.cop[0] = cop[0];
-    a.cop[1] = cop[1];
-    a.eop[0] = eop[0];
-    a.eop[1] = eop[1];
-    k_bc<<<std::min(p.n_bc, c->bc_grid), kBlock, c->bc_smem, s>>>(M, B, h, u, pv, Kp, a);
-    CK(cudaGetLastError());
-    ++c->launches;
-    if (rec) CK(cudaEventRecordWithFlags(rec->stop, s, cudaEventRecordExternal));
-    return;
   }
   if (p.se.n() > 0) {
     k_edge_fq<<<grid(p.se.n(), 1), kSBlock, 0, s>>>(M, h, u, pv, es, FQ);
@@ -2127,7 +1290,6 @@ void prepare_fork(mswm_cuda_ctx* c) {
   if ((fe && fe[0] == '0') || c->halo.active() || !c->have_regions) return;
   MaskPlan& ps = plan_for(c, kMaskSub);
   MaskPlan& pc = plan_for(c, kMaskCoarseOnly);
-  if (pc.use_tiles || pc.use_coop || pc.use_flow || ps.use_flow || !c->slabs.empty()) return;
   if (const char* fc = std::getenv("MSWM_FORK_CTAS")) {  // "n" or "a,b,c"
     int v[3];
     const int k = std::sscanf(fc, "%d,%d,%d", &v[0], &v[1], &v[2]);
@@ -2740,15 +1902,6 @@ int mswm_cuda_create(const mswm_mesh_desc* mesh, int device, const int32_t* cell
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->ls = c->stream;
     build_tables(c.get(), mesh, cell_order);
-    {
-      const char* cv = std::getenv("MSWM_COOP");
-      int nb = 0, nsm = 0, coop = 0;
-      CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
-      CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fused_eval, kBlock, 0));
-      // opt-in (MSWM_COOP=1): measured slower than three launches (profiles/)
-      c->coop_blocks = (coop && cv && cv[0] == '1') ? nb * nsm : 0;
-    }
   } catch (const Error& e) {
     g_create_error = e.what();
     return e.status;
@@ -2851,19 +2004,14 @@ int mswm_cuda_eval(mswm_cuda_ctx* c, const double* h, const double* u, unsigned 
     check_ctx(c);
     if (!h || !u || !dh || !du) throw Error(MSWM_E_USAGE, "null array");
     if (!c->have_fields) throw Error(MSWM_E_USAGE, "set_fields must be called before eval");
+    check_dry(c);  // a pending error of an earlier step batch surfaces first
     MaskPlan& p = plan_for(c, mask);
     upload_field(c, c->T1h, h, c->c_new2old, c->nC);
     upload_field(c, c->T1u, u, c->e_new2old, c->nE);
-    reset_dry(c);
     Op co[2] = {mk_op(OP_STORE, c->Dh.p), mk_op(OP_STORE, c->Dh.p)};
     Op eo[2] = {mk_op(OP_STORE, c->Du.p), mk_op(OP_STORE, c->Du.p)};
     launch_eval(c, p, c->T1h.p, c->T1u.p, co, eo);
-    CK(cudaStreamSynchronize(c->stream));
-    if (read_dry(c)) {
-      c->last_dry_step = 0;
-      throw Error(MSWM_E_DRY_VERTEX, "vertex " + std::to_string(c->last_dry_vertex) +
-                                         " has non-positive thickness");
-    }
+    check_dry(c);
     // Gather the masked entries and scatter them into the caller's arrays;
     // everything else is left untouched (integrators.hpp:63-67).
     std::vector<double> tmp(std::max(c->nC, c->nE));
@@ -2905,6 +2053,7 @@ int mswm_cuda_state_download(mswm_cuda_ctx* c, double* h, double* u, double* tim
     if (h) download_field(c, c->H, h, c->c_new2old, c->nC);
     if (u) download_field(c, c->U, u, c->e_new2old, c->nE);
     if (time) *time = c->time;
+    check_dry(c);  // the state is written either way; a pending error is reported
     return int(MSWM_OK);
   });
 }
@@ -2915,20 +2064,14 @@ int mswm_cuda_step(mswm_cuda_ctx* c, int scheme, double dt, int M, int64_t n_ste
     check_step_args(c, scheme, dt, M, n_steps);
     if (n_steps == 0) return int(MSWM_OK);
     cudaGraphExec_t g = graph_for(c, scheme, dt, M);
-    reset_dry(c);
-    CK(cudaMemcpyAsync(c->step_ctr.p, &c->steps_issued, 8, cudaMemcpyHostToDevice, c->stream));
+    c->batches.emplace_back(c->steps_issued, n_steps);
     for (int64_t k = 0; k < n_steps; ++k) {
       CK(cudaGraphLaunch(g, c->stream));
       tally_step(c, scheme, M);
       c->time += dt;
     }
     c->steps_issued += n_steps;
-    if (sync) {
-      CK(cudaStreamSynchronize(c->stream));
-      if (read_dry(c))
-        throw Error(MSWM_E_DRY_VERTEX, "vertex " + std::to_string(c->last_dry_vertex) +
-                                           " has non-positive thickness (during the step batch)");
-    }
+    if (sync) check_dry(c);
     return int(MSWM_OK);
   });
 }
@@ -2961,10 +2104,7 @@ int mswm_cuda_dry_vertex(const mswm_cuda_ctx* c, int64_t* step) {
 int mswm_cuda_sync(mswm_cuda_ctx* c) {
   return guard(c, [&] {
     check_ctx(c);
-    CK(cudaStreamSynchronize(c->stream));
-    if (read_dry(c))
-      throw Error(MSWM_E_DRY_VERTEX,
-                  "vertex " + std::to_string(c->last_dry_vertex) + " has non-positive thickness");
+    check_dry(c);
     return int(MSWM_OK);
   });
 }
@@ -3002,7 +2142,7 @@ int mswm_cuda_eval_profile(mswm_cuda_ctx* c, float* eval_ms, int64_t* out_cells,
 
 int mswm_cuda_layout_info(const mswm_cuda_ctx* c, int* kernel_path, int* identity_order) {
   if (!c) return MSWM_E_USAGE;
-  if (kernel_path) *kernel_path = c->tile_path ? 2 : (c->ring_derived ? 1 : (c->hybrid ? 3 : 0));
+  if (kernel_path) *kernel_path = 0;
   if (identity_order) *identity_order = c->identity ? 1 : 0;
   return MSWM_OK;
 }
@@ -3011,24 +2151,6 @@ int mswm_cuda_stencil_info(const mswm_cuda_ctx* c, int* offsets16, int64_t* n_wi
   if (!c) return MSWM_E_USAGE;
   if (offsets16) *offsets16 = c->e_st16.p ? 1 : 0;
   if (n_wide) *n_wide = c->n_sten_wide;
-  return MSWM_OK;
-}
-
-int mswm_cuda_bc_info(const mswm_cuda_ctx* c, int* tile_cells, int* n_tiles, int64_t* smem) {
-  if (!c) return MSWM_E_USAGE;
-  if (tile_cells) *tile_cells = c->bc_ok ? c->bc_cells : 0;
-  if (n_tiles) *n_tiles = c->bc_ok ? c->bc_ntiles : 0;
-  if (smem) *smem = c->bc_ok ? int64_t(c->bc_smem) : 0;
-  return MSWM_OK;
-}
-
-int mswm_cuda_flow_info(const mswm_cuda_ctx* c, int* slab_cells, int* n_slabs, int* lag,
-                        int* grid) {
-  if (!c) return MSWM_E_USAGE;
-  if (slab_cells) *slab_cells = c->flow_ok ? c->flow_S : 0;
-  if (n_slabs) *n_slabs = c->flow_ok ? c->flow_nS : 0;
-  if (lag) *lag = c->flow_ok ? c->flow_lag : 0;
-  if (grid) *grid = c->flow_ok ? c->flow_grid : 0;
   return MSWM_OK;
 }
 
@@ -3341,9 +2463,14 @@ struct mswm_cuda_group {
   std::vector<mswm_cuda_ctx*> members;
   cudaStream_t stream = nullptr;
   std::map<std::tuple<int, double, int>, mswm_cuda_ctx::Graph> graphs;
+  std::vector<uint64_t> gens;  // members' configuration generations the graphs were captured at
   std::string last_error;
-  ~mswm_cuda_group() {
+  void drop_graphs() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
+    graphs.clear();
+  }
+  ~mswm_cuda_group() {
+    drop_graphs();
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -3388,13 +2515,21 @@ int mswm_cuda_group_step(mswm_cuda_group* g, int scheme, double dt, int M, int64
       CK(cudaStreamSynchronize(c->stream));  // uploads were issued on member streams
     }
     if (n_steps == 0) return int(MSWM_OK);
+    // a member reconfigured since capture (restrict_halos, relabel, fields):
+    // its buffers and plans may have moved, so every group graph is stale
+    std::vector<uint64_t> now;
+    for (auto* c : g->members) now.push_back(c->gen);
+    if (now != g->gens) {
+      g->drop_graphs();
+      g->gens = now;
+    }
     const auto key = std::make_tuple(scheme, dt, (scheme == MSWM_LTS3 || scheme == MSWM_LTS2) ? M : 0);
     auto it = g->graphs.find(key);
     if (it == g->graphs.end()) {
       auto gr = capture_step(g->members, g->stream, scheme, dt, M, false);
       it = g->graphs.emplace(key, std::move(gr)).first;
     }
-    for (auto* c : g->members) reset_dry(c);
+    for (auto* c : g->members) c->batches.emplace_back(c->steps_issued, n_steps);
     for (int64_t k = 0; k < n_steps; ++k) {
       CK(cudaGraphLaunch(it->second.exec, g->stream));
       for (auto* c : g->members) {
@@ -3403,11 +2538,10 @@ int mswm_cuda_group_step(mswm_cuda_group* g, int scheme, double dt, int M, int64
       }
     }
     CK(cudaStreamSynchronize(g->stream));
-    for (auto* c : g->members)
-      if (read_dry(c))
-        throw Error(MSWM_E_DRY_VERTEX, "rank " + std::to_string(c->rank) + ": vertex " +
-                                           std::to_string(c->last_dry_vertex) +
-                                           " has non-positive thickness (during the step batch)");
+    for (auto* c : g->members) {
+      c->steps_issued += n_steps;
+      check_dry(c, ("rank " + std::to_string(c->rank)).c_str());
+    }
     return int(MSWM_OK);
   });
   if (rc) g->last_error = c0->last_error;

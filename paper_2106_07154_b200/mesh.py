@@ -98,7 +98,8 @@ class Mesh:
         d.n_cells, d.n_edges, d.n_vertices = self.n_cells, self.n_edges, self.n_vertices
         for name, ptype, dtype, _kind in _lib.DESC_TABLES:
             arr = self.tables[name]
-            assert arr.dtype == dtype
+            if not isinstance(arr, np.ndarray) or arr.dtype != dtype or not arr.flags.c_contiguous:
+                raise ValueError(f"mesh table {name} must be a contiguous {np.dtype(dtype)} array")
             setattr(d, name, _lib.as_ptr(arr, ptype))
         return d
 

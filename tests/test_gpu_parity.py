@@ -240,6 +240,53 @@ def test_dry_vertex_reported():
     assert 0 <= v < m.n_vertices and 4 in m.vertex_cells[v]
 
 
+def _draining_workload():
+    """A fine cell with a strong outward flow: the reference's LTS3 raises
+    DryVertexError in step 3 (found with the oracle)."""
+    wl = W.small_sphere(4, seed=5, cap_deg=30.0)
+    T = wl.mesh.tables
+    i = int(np.nonzero(wl.fine_mask)[0][len(np.nonzero(wl.fine_mask)[0]) // 2])
+    off, ce = T["cell_offset"], T["cell_edges"]
+    ec, es = T["edge_cells"].reshape(-1, 2), T["edge_cell_sign"].reshape(-1, 2)
+    u = wl.u.copy()
+    for k in range(off[i], off[i + 1]):
+        e = ce[k]
+        u[e] = 250.0 * (es[e, 0] if ec[e, 0] == i else es[e, 1])
+    return wl, u
+
+
+@pytest.mark.parametrize("sync", [True, False])
+def test_dry_vertex_step_reported(sync):
+    """harness.cpp:183-190: the error names the step of the batch in which
+    the vertex went dry (kernel A records (step, vertex) on the device); an
+    asynchronous batch reports it at the next synchronous call, once."""
+    from oracle.oracle import OracleError
+    wl, u = _draining_workload()
+    o = _oracle_for(wl)
+    hh, uu, k_ref, v_ref = wl.h, u, None, None
+    for k in range(1, 7):
+        try:
+            hh, uu, _ = o.step(int(Scheme.LTS3), hh, uu, 0.0, wl.dt, wl.M, 1)
+        except OracleError as ex:
+            k_ref, v_ref = k, ex.vertex
+            break
+    assert k_ref == 3
+    ctx = _ctx(wl.mesh, wl.b, wl.f, wl.gravity, wl.fine_mask)
+    ctx.upload(State(wl.h, u, 0.0))
+    ctx.advance(Scheme.LTS3, wl.dt, wl.M, 1)   # a clean batch first: steps are per batch
+    with pytest.raises(DryVertexError) as err:
+        ctx.advance(Scheme.LTS3, wl.dt, wl.M, 5, sync=sync)
+        if not sync:
+            ctx.download()
+    assert err.value.step == k_ref - 1, str(err.value)
+    assert f"during step {k_ref - 1} of 5" in str(err.value)
+    v = err.value.vertex
+    vc = wl.mesh.tables["vertex_cells"].reshape(-1, 3)
+    assert 0 <= v < wl.mesh.n_vertices
+    assert set(vc[v]) & set(vc[v_ref]), (v, v_ref)   # next to the drained cell
+    ctx.sync()                                        # reported once, then cleared
+
+
 def test_usage_and_config_errors():
     wl = W.small_sphere(3)
     ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity)
@@ -269,12 +316,12 @@ def test_stepper_drop_in_interface():
     assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
 
 
-@pytest.mark.parametrize("path", ["auto", "tile", "explicit", "ringwalk"])
-def test_layouts_are_bitwise_equivalent(path, monkeypatch):
+@pytest.mark.parametrize("st16", ["1", "0"])
+def test_layouts_are_bitwise_equivalent(st16, monkeypatch):
     """Results are independent of the device numbering (input, Hilbert,
-    random) and of the evaluation path (fused tile kernel, explicit stencil
-    tables, ring walk through L1)."""
-    monkeypatch.setenv("MSWM_KERNELS", path)
+    region-major, random) and of the stencil-id table (16-bit offsets or
+    the int32 table)."""
+    monkeypatch.setenv("MSWM_ST16", st16)
     wl = W.small_sphere(5, seed=13, cap_deg=20.0)
     o = _oracle_for(wl)
     h_ref, u_ref, _ = o.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, wl.M, 4)
@@ -282,11 +329,8 @@ def test_layouts_are_bitwise_equivalent(path, monkeypatch):
     for order in ["input", "hilbert", "regions",
                   rng.permutation(wl.mesh.n_cells).astype(np.int32)]:
         ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order, fine_mask=wl.fine_mask)
-        info = ctx.layout_info()
-        # a random numbering has no locality: the tile path declines it
-        assert info["kernel_path"] == path or (path in ("tile", "auto")
-                                               and not isinstance(order, str)
-                                               and info["kernel_path"] == "explicit")
+        assert ctx.layout_info()["kernel_path"] == "explicit"
+        assert ctx.stencil_info()["offsets16"] == (st16 == "1")
         ctx.make_regions(wl.fine_mask, wl.width)
         for a, b in zip(ctx.regions.groups, o.groups()):
             assert np.array_equal(a, b)
@@ -302,7 +346,7 @@ def test_layouts_are_bitwise_equivalent(path, monkeypatch):
         assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref), str(order)[:20]
 
 
-def test_planar_ring_derived_and_rk4_full_mesh():
+def test_planar_rk4_full_mesh():
     wl = W.config1(n_steps=3)
     o = _oracle_for(wl)
     ctx = _ctx(wl.mesh, wl.b, wl.f, wl.gravity, wl.fine_mask)
@@ -333,82 +377,6 @@ def test_reference_stepper_drives_cuda_evaluator():
     c1, e1, _ = serial.ledger()
     c2, e2, _ = cuda.ledger()
     assert np.array_equal(c1, c2) and np.array_equal(e1, e2)
-
-
-@pytest.mark.parametrize("env", [{"MSWM_COOP": "1"}, {"MSWM_SLAB_CELLS": "2000"},
-                                 {"MSWM_KERNELS": "tile", "MSWM_TILE_CELLS": "64"},
-                                 {"MSWM_KERNELS": "auto"}, {"MSWM_KERNELS": "ringwalk"}])
-def test_optional_evaluation_paths_bitwise(env, monkeypatch):
-    """Every opt-in evaluation strategy (cooperative one-launch small evals,
-    L2-blocked slabs, fused tiles, hybrid, ring walk) stays bitwise equal."""
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
-    wl = W.small_sphere(5, seed=29, cap_deg=25.0)
-    o = _oracle_for(wl)
-    ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order="regions", fine_mask=wl.fine_mask)
-    ctx.make_regions(wl.fine_mask, wl.width)
-    for scheme, n, dt in [(Scheme.LTS3, 4, wl.dt), (Scheme.RK4, 2, wl.dt / wl.M)]:
-        h_ref, u_ref, _ = o.step(int(scheme), wl.h, wl.u, 0.0, dt, wl.M, n)
-        ctx.upload(State(wl.h, wl.u, 0.0))
-        ctx.advance(scheme, dt, wl.M, n)
-        st = ctx.download()
-        assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref), (env, scheme)
-
-
-@pytest.mark.parametrize("slab,lag,order", [(16, 1, "hilbert"), (64, 8, "regions"),
-                                            (256, 3, "hilbert"), (32, 100000, "regions")])
-def test_dataflow_evaluation_bitwise(slab, lag, order, monkeypatch):
-    """k_flow (one persistent launch per large evaluation, phases overlapped
-    through per-slab completion flags) stays bitwise equal for any slab size,
-    producer lag and numbering -- lag 1 makes consumers wait on producers."""
-    monkeypatch.setenv("MSWM_FLOW", "1")
-    monkeypatch.setenv("MSWM_FLOW_SLAB", str(slab))
-    monkeypatch.setenv("MSWM_FLOW_LAG", str(lag))
-    wl = W.small_sphere(6, seed=31, cap_deg=20.0)
-    o = _oracle_for(wl)
-    ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order, fine_mask=wl.fine_mask)
-    info = ctx.flow_info()
-    assert info["slab_cells"] == slab and info["n_slabs"] == -(-wl.mesh.n_cells // slab)
-    ctx.make_regions(wl.fine_mask, wl.width)
-    ev = CudaEvaluator(ctx)
-    for mask in LTS3_MASKS + [kMaskAll]:
-        dh1 = np.full(wl.mesh.n_cells, SENTINEL)
-        du1 = np.full(wl.mesh.n_edges, SENTINEL)
-        dh2, du2 = dh1.copy(), du1.copy()
-        ev.eval(wl.h, wl.u, mask, dh1, du1)
-        o.eval(wl.h, wl.u, mask, dh2, du2)
-        assert bits_equal(dh1, dh2) and bits_equal(du1, du2), hex(mask)
-    for scheme, n, dt in [(Scheme.LTS3, 5, wl.dt), (Scheme.RK4, 3, wl.dt / wl.M),
-                          (Scheme.SSPRK3, 2, wl.dt / wl.M), (Scheme.LTS2, 3, wl.dt)]:
-        h_ref, u_ref, _ = o.step(int(scheme), wl.h, wl.u, 0.0, dt, wl.M, n)
-        ctx.upload(State(wl.h, wl.u, 0.0))
-        ctx.advance(scheme, dt, wl.M, n)
-        st = ctx.download()
-        assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref), scheme
-    # the large evaluations are one launch each
-    ctx.upload(State(wl.h, wl.u, 0.0))
-    ctx.advance(Scheme.LTS3, wl.dt, wl.M, 1)
-    monkeypatch.setenv("MSWM_FLOW", "0")
-    c0 = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order, fine_mask=wl.fine_mask)
-    c0.make_regions(wl.fine_mask, wl.width)
-    c0.upload(State(wl.h, wl.u, 0.0))
-    c0.advance(Scheme.LTS3, wl.dt, wl.M, 1)
-    assert ctx.kernels_per_step() < c0.kernels_per_step()
-
-
-def test_dataflow_disabled_matches(monkeypatch):
-    """Without MSWM_FLOW=1 the three-kernel path runs (same bits)."""
-    monkeypatch.delenv("MSWM_FLOW", raising=False)
-    wl = W.small_sphere(6, seed=31, cap_deg=20.0)
-    ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, fine_mask=wl.fine_mask)
-    assert ctx.flow_info()["slab_cells"] == 0
-    o = _oracle_for(wl)
-    ctx.make_regions(wl.fine_mask, wl.width)
-    h_ref, u_ref, _ = o.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, wl.M, 3)
-    ctx.upload(State(wl.h, wl.u, 0.0))
-    ctx.advance(Scheme.LTS3, wl.dt, wl.M, 3)
-    st = ctx.download()
-    assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
 
 
 @pytest.mark.parametrize("order", ["hilbert", "input"])
@@ -506,34 +474,6 @@ def test_concurrent_coarse_step_bitwise(fork, order, monkeypatch):
         ctx.advance(Scheme.LTS3, wl.dt, M, 5)
         st = ctx.download()
         assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref), M
-
-
-@pytest.mark.parametrize("cells", ["256", "64"])
-def test_fused_bc_tiles_bitwise(cells, monkeypatch):
-    """Phases B + C fused per cell tile (k_bc, (F, q~, l) in shared memory):
-    every LTS3 mask and LTS3 / RK4 steps bitwise equal to the oracle."""
-    monkeypatch.setenv("MSWM_BC", "1")
-    monkeypatch.setenv("MSWM_BC_CELLS", cells)
-    wl = W.small_sphere(6, seed=37, cap_deg=25.0)
-    o = _oracle_for(wl)
-    ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order="regions", fine_mask=wl.fine_mask)
-    info = ctx.bc_info()
-    assert info["tile_cells"] == int(cells) and info["n_tiles"] > 0
-    ctx.make_regions(wl.fine_mask, wl.width)
-    ev = CudaEvaluator(ctx)
-    for mask in LTS3_MASKS:
-        dh1 = np.full(wl.mesh.n_cells, SENTINEL)
-        du1 = np.full(wl.mesh.n_edges, SENTINEL)
-        dh2, du2 = dh1.copy(), du1.copy()
-        ev.eval(wl.h, wl.u, mask, dh1, du1)
-        o.eval(wl.h, wl.u, mask, dh2, du2)
-        assert bits_equal(dh1, dh2) and bits_equal(du1, du2)
-    for scheme, n, dt in [(Scheme.LTS3, 3, wl.dt), (Scheme.RK4, 2, wl.dt / wl.M)]:
-        h_ref, u_ref, _ = o.step(int(scheme), wl.h, wl.u, 0.0, dt, wl.M, n)
-        ctx.upload(State(wl.h, wl.u, 0.0))
-        ctx.advance(scheme, dt, wl.M, n)
-        st = ctx.download()
-        assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref), scheme
 
 
 @pytest.mark.parametrize("st16", ["1", "0"])
