@@ -115,8 +115,10 @@ def allreduce_max(x: float, ws: int) -> float:
 # ---------------------------------------------------------------------------
 # workload + algorithmic bytes
 
-def make_workload(name: str):
+def make_workload(name: str, level: int | None = None):
     from paper_2106_07154_b200 import workloads as W
+    if level is not None and name in W.SPHERE_LEVEL:
+        return W.CONFIGS[name](level=level)
     return W.CONFIGS[name]()
 
 
@@ -199,12 +201,14 @@ class Clocks:
 class RefRunner:
     """The reference's own LTS3 path (oracle/_ref = unmodified proj/src):
     Stepper::lts_step(3) with SerialEvaluator (nranks=0) or ThreadedEvaluator
-    over partition_multiconstraint + make_block_plan (nranks ranks)."""
+    over partition_multiconstraint + make_block_plan (nranks ranks).
+    ``rm``: a reference VoronoiMesh already built (the reference arm's own
+    builder); default: the workload's tables loaded into one."""
 
-    def __init__(self, wl, nranks: int):
+    def __init__(self, wl, nranks: int, rm=None):
         from oracle.oracle import RefEvaluator, RefMesh, RefRegions
         self.wl = wl
-        self.rm = RefMesh.from_mesh(wl.mesh)
+        self.rm = RefMesh.from_mesh(wl.mesh) if rm is None else rm
         self.rr = RefRegions(self.rm, wl.fine_mask, wl.width)
         self.ev = RefEvaluator(self.rm, self.rr, wl.b, wl.f, wl.gravity, nranks=nranks)
         self.h, self.u, self.t = wl.h, wl.u, 0.0
@@ -219,6 +223,25 @@ class RefRunner:
         _, e1, s1 = self.ev.ledger()
         per = int(e1.sum() - e0.sum()) // max(s1 - s0, 1)
         return per * n / secs, secs / n, per
+
+
+def host_info() -> dict:
+    """CPU model, logical CPUs and RAM of this box."""
+    model, mem = None, None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as fh:
+            for line in fh:
+                if line.startswith("MemTotal:"):
+                    mem = round(int(line.split()[1]) / 2**20, 1)
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "threads_available": cpu_threads(),
+            "ram_gb": mem}
 
 
 def cpu_threads():
@@ -257,42 +280,91 @@ def ref_ranks(wl, threads: int):
     return None, "reference needs more host RAM than this box has"
 
 
+def loaded_repo_libraries() -> list:
+    """Shared objects of this repo mapped into the process (/proc/self/maps)."""
+    out = set()
+    try:
+        with open("/proc/self/maps") as fh:
+            for line in fh:
+                path = line.split()[-1]
+                if path.endswith(".so") and str(ROOT) in path:
+                    out.add(os.path.relpath(path, ROOT))
+    except OSError:
+        pass
+    return sorted(out)
+
+
+def reference_workload(name: str, level: int | None = None):
+    """The workload with its mesh built by the REFERENCE's own generator
+    (build_voronoi_mesh(subdivide_icosahedron(L)), proj/src/mesh_build.cpp:
+    185-366, via oracle/_ref) for the spherical configurations, so the
+    reference arm maps no product library; its tables equal ours bitwise
+    (tests/test_reference_arm.py).  The planar configurations have no
+    reference generator (it is sphere-only): their tables come from our
+    planar builder, the table adapter SURVEY.md §8(c) names."""
+    from paper_2106_07154_b200 import workloads as W
+    if name not in W.SPHERE_LEVEL:
+        return W.CONFIGS[name](), None, "planar tables from the repo's builder (the reference has no planar generator)"
+    from oracle.oracle import RefMesh
+    level = level or W.SPHERE_LEVEL[name]
+    t0 = time.time()
+    rm = RefMesh.icosahedral(level, W.EARTH_RADIUS)
+    mesh = rm.as_mesh()
+    note = f"reference build_voronoi_mesh(subdivide_icosahedron({level})) in {time.time() - t0:.0f} s"
+    return W.CONFIGS[name](mesh=mesh, level=level), rm, note
+
+
 def run_reference_arm(args, ws, rank):
-    """--impl reference: the reference CPU path on this box's host cores."""
+    """--impl reference: the reference's own CPU LTS3 path on this box's host
+    cores, same config / metric / step count as the GPU arm.  Only oracle/_ref
+    (the unmodified reference + its C shim) is loaded."""
     if rank != 0:
         return
     from oracle.oracle import ref_available
     if not ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
-    wl = make_workload(args.config)
+    wl, rm, mesh_note = reference_workload(args.config, args.level)
+    log(f"reference arm: {mesh_note}")
     threads = cpu_threads()
-    # the threaded evaluator on every host thread (the reference's parallel
-    # path) as far as host RAM allows; each timed "step" is one full LTS3
-    # coarse step, and the number of timed steps is bounded so the arm ends
-    # within a few minutes
+    # ThreadedEvaluator on every host thread (the reference's parallel path)
+    # as far as host RAM allows
     best, note = ref_ranks(wl, threads)
     if best is None:
         print(json.dumps({"impl": "reference", "unavailable": f"{args.config}: {note}"}))
         return
     cores = max(1, best)
-    runner = RefRunner(wl, best)
-    _, sps0, _ = runner.steps(1)  # warm-up (set caches), also sizes the sample
-    log(f"reference {cores} threads: {sps0:.3f} s/step (warm-up)")
-    budget = 90.0
-    n = max(1, min(args.steps, int(budget / max(sps0, 1e-9))))
-    if args.warmup > 1 and sps0 * (args.warmup - 1) < 30:
-        runner.steps(args.warmup - 1)
+    runner = RefRunner(wl, best, rm)
+    for _ in range(args.warmup):
+        _, sps0, _ = runner.steps(1)
+        log(f"reference {cores} threads: {sps0:.3f} s/step (warm-up)")
+        if sps0 * args.steps > 1800:  # keep the arm's wall time bounded (C5)
+            break
+    n = args.steps if sps0 * args.steps <= 1800 else max(1, int(1800 / sps0))
     rate, sps, per = runner.steps(n)
+    del runner
+    # SerialEvaluator on one core: one coarse step (BASELINE.md §2 (a))
+    serial = None
+    if not args.no_serial and ref_ranks(wl, 1)[0] is not None:
+        sr = RefRunner(wl, 0, rm)
+        srate, ssps, _ = sr.steps(1)
+        serial = {"edge_evals_per_s": srate, "s_per_step": ssps, "cores": 1,
+                  "sample": "1 LTS3 coarse step, SerialEvaluator"}
+        del sr
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": ws,
-        "steps": n, "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": sps * 1e3,
+        "steps": n, "warmup": args.warmup, "ms_per_step": sps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload_config(wl, args.config, ws),
+        "coarse_steps_per_s": 1.0 / sps,
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": f"{n} LTS3 coarse steps of {args.config} "
-                                   f"({'SerialEvaluator' if best == 0 else f'ThreadedEvaluator {best} ranks'})"},
+                         "sample": f"{n} LTS3 coarse steps of {args.config} after {args.warmup} "
+                                   f"warm-up, reference "
+                                   f"{'SerialEvaluator' if best == 0 else f'ThreadedEvaluator {best} ranks'}"
+                                   f"{note}; mesh: {mesh_note}",
+                         "serial_1core": serial, "host": host_info()},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "repo_libraries_loaded": loaded_repo_libraries(),
     }
     print(json.dumps(line), flush=True)
 
@@ -319,7 +391,7 @@ def run_ours(args, ws, rank, local):
         raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
     torch.cuda.set_device(local)
     t0 = time.time()
-    wl = make_workload(args.config)
+    wl = make_workload(args.config, args.level)
     log(f"[rank {rank}] workload {args.config}: {wl.mesh.n_cells} cells, {wl.mesh.n_edges} edges, "
         f"built in {time.time() - t0:.1f}s")
     rc = None
@@ -458,6 +530,7 @@ def run_ours(args, ws, rank, local):
             runner.steps(1)
             rate, sps, _ = runner.steps(args.cpu_steps)
             cpu = {"value": rate, "unit": UNIT, "cores": max(threads, 1), "kind": "reference",
+                   "host": host_info(),
                    "sample": f"{args.cpu_steps} LTS3 coarse step(s) of {args.config} after 1 "
                              f"warm-up, reference "
                              f"{'SerialEvaluator' if threads == 0 else f'ThreadedEvaluator {threads} ranks'}"
@@ -497,13 +570,17 @@ def run_ours(args, ws, rank, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--level", type=int, default=None,
+                    help="icosahedral level override of c4/c5 (tests; default: the config's)")
     ap.add_argument("--cpu-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rk4", action="store_true")
+    ap.add_argument("--no-serial", action="store_true",
+                    help="reference arm: skip the 1-core SerialEvaluator leg")
     ap.add_argument("--order", default="regions", choices=["regions", "hilbert", "input"],
                     help="device layout (results are bitwise independent of it)")
     args = ap.parse_args()

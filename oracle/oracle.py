@@ -21,7 +21,8 @@ from paper_2106_07154_b200 import _lib
 from paper_2106_07154_b200.mesh import Mesh
 
 HERE = Path(__file__).resolve().parent
-REF_LIB = HERE / "_ref" / "libmswm_ref.so"
+REF_LIB = HERE / "_ref" / "libmswm_ref.so"          # the pure reference (no product link)
+DROPIN_LIB = HERE / "_ref" / "libmswm_dropin.so"    # + mswm::CudaEvaluator (tests only)
 ORACLE_LIB = HERE / "_build" / "libmswm_oracle.so"
 
 vp = C.c_void_p
@@ -40,11 +41,28 @@ class OracleError(RuntimeError):
 
 
 _ref = None
+_dropin = None
 _orc = None
 
 
 def ref_available() -> bool:
     return REF_LIB.exists()
+
+
+def dropin() -> C.CDLL:
+    """libmswm_dropin.so: the C++ drop-in over the product's C ABI (tests only;
+    loading it maps libmswm_cuda.so)."""
+    global _dropin
+    if _dropin is None:
+        ref()
+        if not DROPIN_LIB.exists():
+            raise RuntimeError(f"{DROPIN_LIB} not built (make -C oracle ref)")
+        lib = C.CDLL(str(DROPIN_LIB))
+        lib.ref_cuda_eval_create.restype = vp
+        lib.ref_cuda_eval_create.argtypes = [vp, vp, f64p, f64p, C.c_double, C.c_int, C.c_char_p,
+                                             C.c_int]
+        _dropin = lib
+    return _dropin
 
 
 def ref() -> C.CDLL:
@@ -75,7 +93,6 @@ def ref() -> C.CDLL:
             "ref_regions_validate": (C.c_int, [vp, vp]),
             "ref_eval_create": (vp, [vp, vp, f64p, f64p, C.c_double, C.c_int, C.c_uint64] + E),
             "ref_eval_free": (None, [vp]),
-            "ref_cuda_eval_create": (vp, [vp, vp, f64p, f64p, C.c_double, C.c_int] + E),
             "ref_eval": (C.c_int, [vp, f64p, f64p, C.c_uint, f64p, f64p] + E
                          + [C.POINTER(C.c_int)]),
             "ref_closure": (C.c_int, [vp, f64p, f64p, C.c_uint, C.c_int, i32p, i64p] + E),
@@ -252,7 +269,7 @@ class RefEvaluator:
         obj.b = np.ascontiguousarray(b, np.float64)
         obj.f = np.ascontiguousarray(f, np.float64)
         buf = _err()
-        obj.handle = ref().ref_cuda_eval_create(mesh.handle, regions.handle if regions else None,
+        obj.handle = dropin().ref_cuda_eval_create(mesh.handle, regions.handle if regions else None,
                                                 _p(obj.b, f64p), _p(obj.f, f64p), gravity, device,
                                                 buf, ERRLEN)
         if not obj.handle:

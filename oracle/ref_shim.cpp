@@ -1,4 +1,5 @@
-// ORACLE / TEST INFRASTRUCTURE ONLY -- never linked into the product.
+// ORACLE / TEST INFRASTRUCTURE ONLY -- never linked into the product, and links
+// nothing of the product (the timed reference arm of bench.py maps only this).
 //
 // extern "C" shim over the UNMODIFIED reference library (/root/reference/
 // proj/src/*.cpp compiled by oracle/Makefile into oracle/_ref/).  It lets the
@@ -29,58 +30,12 @@
 #include "mswm/rank_pool.hpp"
 #include "mswm/regions.hpp"
 #include "mswm_cuda.h"
-#include "drop_in_evaluator.hpp"
 
-using namespace mswm;
+#include "ref_shim.hpp"
+
+using namespace mswm_shim;
 
 namespace {
-
-void put_err(char* buf, int n, const std::string& s) {
-  if (!buf || n <= 0) return;
-  std::strncpy(buf, s.c_str(), size_t(n - 1));
-  buf[n - 1] = 0;
-}
-
-// Runs f, translating reference exceptions into mswm_status codes.
-template <class F>
-int guarded(char* err, int errlen, int* dry_vertex, F&& f) {
-  try {
-    f();
-    return MSWM_OK;
-  } catch (const DryVertexError& e) {
-    if (dry_vertex) *dry_vertex = e.vertex;
-    put_err(err, errlen, e.what());
-    return MSWM_E_DRY_VERTEX;
-  } catch (const ConfigError& e) {
-    put_err(err, errlen, e.what());
-    return MSWM_E_CONFIG;
-  } catch (const UsageError& e) {
-    put_err(err, errlen, e.what());
-    return MSWM_E_USAGE;
-  } catch (const TopologyError& e) {
-    put_err(err, errlen, e.what());
-    return MSWM_E_TOPOLOGY;
-  } catch (const std::exception& e) {
-    put_err(err, errlen, e.what());
-    return MSWM_E_CONFIG;
-  }
-}
-
-struct Evaluator {
-  const VoronoiMesh* mesh;
-  const RegionMap* map;
-  CellField b;
-  VertexField f;
-  double gravity;
-  std::unique_ptr<PartitionPlan> plan;
-  std::unique_ptr<TendencyEvaluator> ev;
-};
-
-struct StepperBox {
-  WorkLedger ledger;
-  std::unique_ptr<Stepper> stepper;
-  const VoronoiMesh* mesh;
-};
 
 std::vector<int> union_sets(const RegionMap& map, unsigned mask, bool cells) {
   static const unsigned cbits[6] = {kCellsFinePlain, kCellsUF1, kCellsUF2,
@@ -343,28 +298,6 @@ void* ref_eval_create(void* mp, void* rp, const double* b, const double* f, doub
 }
 
 void ref_eval_free(void* e) { delete static_cast<Evaluator*>(e); }
-
-// The drop-in: the reference's own Stepper driving the GPU through
-// mswm::CudaEvaluator (drop_in_evaluator.hpp) -- one C-ABI eval() per stage.
-void* ref_cuda_eval_create(void* mp, void* rp, const double* b, const double* f, double gravity,
-                           int device, char* err, int errlen) {
-  auto* m = static_cast<VoronoiMesh*>(mp);
-  auto* r = static_cast<RegionMap*>(rp);
-  Evaluator* out = nullptr;
-  guarded(err, errlen, nullptr, [&] {
-    auto ev = std::make_unique<Evaluator>();
-    ev->mesh = m;
-    ev->map = r;
-    ev->b = CellField(m->n_cells);
-    ev->f = VertexField(m->n_vertices);
-    std::copy(b, b + m->n_cells, ev->b.data.begin());
-    std::copy(f, f + m->n_vertices, ev->f.data.begin());
-    ev->gravity = gravity;
-    ev->ev = std::make_unique<CudaEvaluator>(*m, r, ev->b, ev->f, gravity, device);
-    out = ev.release();
-  });
-  return out;
-}
 
 int ref_eval(void* ep, const double* h, const double* u, unsigned mask, double* dh, double* du,
              char* err, int errlen, int* dry_vertex) {

@@ -103,6 +103,22 @@ class Mesh:
             setattr(d, name, _lib.as_ptr(arr, ptype))
         return d
 
+    def digest(self, geometry: bool = True) -> str:
+        """sha256 of the hot-path tables (and positions / kite areas): equal
+        digests = bitwise equal meshes, whichever builder made them."""
+        import hashlib
+        h = hashlib.sha256()
+        for name in sorted(self.tables):
+            h.update(name.encode())
+            h.update(np.ascontiguousarray(self.tables[name]).tobytes())
+        if geometry:
+            for name in ("cell_xyz", "vertex_xyz", "edge_xyz", "kite_area"):
+                a = getattr(self, name)
+                if a is not None:
+                    h.update(name.encode())
+                    h.update(np.ascontiguousarray(a).tobytes())
+        return h.hexdigest()
+
     @property
     def n_ring(self) -> int:
         return int(self.tables["cell_offset"][-1])

@@ -193,8 +193,12 @@ def _cap_mask(mesh: Mesh, centers, radius_rad: float) -> np.ndarray:
 
 
 def _spherical(name: str, level: int, seed: int, caps: int, cap_deg: float, M: int,
-               n_steps: int) -> Workload:
-    mesh = Mesh.icosahedral(level, EARTH_RADIUS)
+               n_steps: int, mesh: Mesh | None = None) -> Workload:
+    """``mesh``: the icosahedral level-``level`` mesh from another builder
+    (the reference arm passes the reference's own build_voronoi_mesh, whose
+    tables equal ours bitwise); default: ours."""
+    if mesh is None:
+        mesh = Mesh.icosahedral(level, EARTH_RADIUS)
     rng = _rng(seed)
     H = 4000.0
     waves = _sphere_waves(rng, 32.0, 64)
@@ -215,14 +219,18 @@ def _spherical(name: str, level: int, seed: int, caps: int, cap_deg: float, M: i
                     meta={"mesh": f"icosahedral L{level}", "caps": caps, "cap_deg": cap_deg})
 
 
-def config4(seed: int = 4, n_steps: int = 100, level: int = 10) -> Workload:
+def config4(seed: int = 4, n_steps: int = 100, level: int = 10, mesh: Mesh | None = None) -> Workload:
     """BASELINE configs[3]: icosahedral L10, 20 degree cap, M=4."""
-    return _spherical("C4", level, seed, 1, 20.0, 4, n_steps)
+    return _spherical("C4", level, seed, 1, 20.0, 4, n_steps, mesh)
 
 
-def config5(seed: int = 5, n_steps: int = 20, level: int = 11) -> Workload:
+def config5(seed: int = 5, n_steps: int = 20, level: int = 11, mesh: Mesh | None = None) -> Workload:
     """BASELINE configs[4]: icosahedral L11, three 10 degree caps, M=8."""
-    return _spherical("C5", level, seed, 3, 10.0, 8, n_steps)
+    return _spherical("C5", level, seed, 3, 10.0, 8, n_steps, mesh)
+
+
+# icosahedral level of the spherical configurations (reference-built meshes)
+SPHERE_LEVEL = {"c4": 10, "c5": 11}
 
 
 CONFIGS = {"c1": config1, "c2": config2, "c3": config3, "c4": config4, "c5": config5}

@@ -52,6 +52,38 @@ def test_bench_reference_arm_json_line():
     assert d["e2e"]["h2d_bytes_per_step"] == 0
 
 
+def test_bench_reference_arm_maps_no_product_library():
+    """The spherical reference arm builds its mesh with the reference's own
+    generator and runs the reference's Stepper: only oracle/ libraries are
+    mapped (no libmswm_cuda / libmswm_host), and it runs the requested step
+    count plus the 1-core SerialEvaluator leg."""
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--config",
+                        "c4", "--level", "4", "--steps", "3", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+    libs = d["repo_libraries_loaded"]
+    assert libs and all(p.startswith("oracle/") for p in libs), libs
+    assert not any("dropin" in p for p in libs), libs
+    assert d["steps"] == 3 and d["warmup"] == 3
+    assert d["cpu_baseline"]["serial_1core"]["cores"] == 1
+    assert d["cpu_baseline"]["host"]["nproc"] >= 1
+    assert "reference build_voronoi_mesh" in d["cpu_baseline"]["sample"]
+
+
+@pytest.mark.slow
+def test_reference_builder_equals_ours_at_level10():
+    """The reference arm's C4 mesh (the reference's build_voronoi_mesh at
+    level 10) is bitwise the mesh our builder gives the GPU path."""
+    from oracle.oracle import RefMesh, ref_available
+    from paper_2106_07154_b200.mesh import Mesh
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    ours = Mesh.icosahedral(10, W.EARTH_RADIUS).digest()
+    theirs = RefMesh.icosahedral(10, W.EARTH_RADIUS).as_mesh().digest()
+    assert ours == theirs
+
+
 def test_bench_ours_fails_loudly_without_gpu():
     import torch
     if torch.cuda.is_available():
