@@ -316,12 +316,20 @@ def test_stepper_drop_in_interface():
     assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
 
 
-@pytest.mark.parametrize("st16", ["1", "0"])
-def test_layouts_are_bitwise_equivalent(st16, monkeypatch):
+@pytest.mark.parametrize("kout,env", [("ringtile", {}),
+                                      ("ringtile", {"MSWM_RW_CELLS": "16"}),
+                                      ("ringtile", {"MSWM_RW_STAGE_KB": "8"}),
+                                      ("explicit", {"MSWM_KOUT": "explicit", "MSWM_ST16": "1"}),
+                                      ("explicit", {"MSWM_KOUT": "explicit", "MSWM_ST16": "0"})])
+def test_layouts_are_bitwise_equivalent(kout, env, monkeypatch):
     """Results are independent of the device numbering (input, Hilbert,
-    region-major, random) and of the stencil-id table (16-bit offsets or
-    the int32 table)."""
-    monkeypatch.setenv("MSWM_ST16", st16)
+    region-major, random) and of the output kernel: k_out_rw (cell tiles in
+    shared memory, ring-walk weights; tile sizes and stage capacities that
+    force tile splitting) or k_out over the explicit stencil tables (16-bit
+    offsets or the int32 table)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    st16 = env.get("MSWM_ST16", "1")
     wl = W.small_sphere(5, seed=13, cap_deg=20.0)
     o = _oracle_for(wl)
     h_ref, u_ref, _ = o.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, wl.M, 4)
@@ -329,7 +337,7 @@ def test_layouts_are_bitwise_equivalent(st16, monkeypatch):
     for order in ["input", "hilbert", "regions",
                   rng.permutation(wl.mesh.n_cells).astype(np.int32)]:
         ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order, fine_mask=wl.fine_mask)
-        assert ctx.layout_info()["kernel_path"] == "explicit"
+        assert ctx.layout_info()["kernel_path"] == kout
         assert ctx.stencil_info()["offsets16"] == (st16 == "1")
         ctx.make_regions(wl.fine_mask, wl.width)
         for a, b in zip(ctx.regions.groups, o.groups()):
@@ -457,13 +465,16 @@ def test_wide_interfaces_bitwise(width):
             assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref), (order, scheme)
 
 
+@pytest.mark.parametrize("kout", ["ringtile", "explicit"])
 @pytest.mark.parametrize("fork", ["1", "0"])
 @pytest.mark.parametrize("order", ["regions", "hilbert"])
-def test_concurrent_coarse_step_bitwise(fork, order, monkeypatch):
+def test_concurrent_coarse_step_bitwise(kout, fork, order, monkeypatch):
     """LTS3 with the coarse step (step 4) on a second stream concurrent with
     the substeps (default) and in sequence (MSWM_FORK=0): bitwise equal to
     the oracle over several coarse steps, M = 2 and 4."""
     monkeypatch.setenv("MSWM_FORK", fork)
+    if kout == "explicit":
+        monkeypatch.setenv("MSWM_KOUT", "explicit")
     wl = W.small_sphere(6, seed=41, cap_deg=25.0)
     o = _oracle_for(wl)
     ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order, fine_mask=wl.fine_mask)
@@ -482,6 +493,7 @@ def test_stencil_offsets16_bitwise(st16, monkeypatch):
     int16 (a random numbering of a level-6 sphere: 123k edges, most offsets
     wide, warps mixing both kinds) and the int32-only table: bitwise equal."""
     monkeypatch.setenv("MSWM_ST16", st16)
+    monkeypatch.setenv("MSWM_KOUT", "explicit")
     wl = W.small_sphere(6, seed=31, cap_deg=20.0)
     o = _oracle_for(wl)
     h_ref, u_ref, _ = o.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, wl.M, 2)
