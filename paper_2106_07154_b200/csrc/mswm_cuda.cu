@@ -684,7 +684,7 @@ bool build_rw(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const std::vector<int32
     }
     const int32_t nx = int32_t(x_loc.size());
     if (nh > idx_cap || nx > idx_cap || ne + nx > 65535 ||
-        rw_stage_bytes(ne + nx + 1, nc + nh + 1) > cap) {
+        rw_stage_bytes(ne + nx + 1, nc + nh + 3) > cap) {
       if (b - a == 1) throw Error(MSWM_E_TOPOLOGY, "k_out_rw: one cell overflows a tile stage");
       return false;
     }
@@ -724,8 +724,10 @@ bool build_rw(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const std::vector<int32
     cover(m, b);
   };
   for (int32_t a = 0; a < nC; a += T) cover(a, std::min(nC, a + T));
+  // stage offsets (RwStage) stay 16 B aligned: 24 emax needs emax even, the
+  // second stage at 24 emax + 76 cmax needs cmax a multiple of 4
   emax += emax & 1;
-  cmax += cmax & 1;
+  cmax = (cmax + 3) & ~3;
   // per-cell rows: kite_area / A_i per ring slot (mesh_build.cpp:354, the
   // rounding derive_ring_stencil verified) and degree / sign bits
   const auto& cn = c->c_new2old;
