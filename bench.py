@@ -391,11 +391,11 @@ def run_ours(args, ws, rank, local):
         raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
     torch.cuda.set_device(local)
     t0 = time.time()
-    wl = make_workload(args.config, args.level)
-    log(f"[rank {rank}] workload {args.config}: {wl.mesh.n_cells} cells, {wl.mesh.n_edges} edges, "
-        f"built in {time.time() - t0:.1f}s")
     rc = None
     if ws == 1:
+        wl = make_workload(args.config, args.level)
+        log(f"[rank {rank}] workload {args.config}: {wl.mesh.n_cells} cells, {wl.mesh.n_edges} edges, "
+            f"built in {time.time() - t0:.1f}s")
         ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, device=local, order=args.order,
                           fine_mask=wl.fine_mask, interface_width=wl.width)
         rm = ctx.make_regions(wl.fine_mask, wl.width)
@@ -403,17 +403,23 @@ def run_ours(args, ws, rank, local):
         ctx.upload(State(wl.h, wl.u, 0.0))
         io_mesh = wl.mesh
     else:
-        # partitioned (strong scaling): global labels from a device
-        # make_regions, this rank's local mesh + halo plan, NCCL p2p halos
+        # partitioned (strong scaling).  Rank 0 alone builds the global mesh,
+        # labels it on its device and publishes it as a binary store in
+        # /dev/shm; every rank memory-maps the store (one page-cache copy per
+        # node) and materialises only its own local mesh + halo plan.
         import torch.distributed as dist
-        from paper_2106_07154_b200.dist import DistributedLayout, RankContext
-        g = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, device=local)
-        rm = g.make_regions(wl.fine_mask, wl.width)
-        g.close()
-        del g
+        from paper_2106_07154_b200.dist import RankContext, layout_from_store, publish_store
+        store_dir = Path(os.environ.get("MSWM_STORE_DIR", "/dev/shm")) / \
+            f"mswm_bench_{args.config}_{os.environ.get('MASTER_PORT', '0')}"
+        if rank == 0:
+            wl0 = make_workload(args.config, args.level)
+            log(f"[rank 0] workload {args.config}: {wl0.mesh.n_cells} cells, built in "
+                f"{time.time() - t0:.1f}s")
+            publish_store(store_dir, wl0, device=local)
+            del wl0
+        barrier(ws)
         t1 = time.time()
-        lay = DistributedLayout(wl.mesh, rm.cell_label, rm.cell_sublabel, rm.edge_label, ws,
-                                only=rank)
+        wl, lay = layout_from_store(store_dir, rank, ws)
         rc = RankContext(lay, rank, wl.b, wl.f, wl.gravity, wl.width, device=local)
         uid = [RankContext.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -422,10 +428,15 @@ def run_ours(args, ws, rank, local):
         from paper_2106_07154_b200.api import LTS3_MASKS, kMaskAll
         rc.restrict_halos(LTS3_MASKS + [kMaskAll])
         rc.upload(wl.h, wl.u)
+        barrier(ws)
+        if rank == 0:
+            import shutil
+            shutil.rmtree(store_dir, ignore_errors=True)
         ctx = rc.ctx
         io_mesh = rc.local_mesh
         log(f"[rank {rank}] local mesh {rc.lm.n_cells} cells ({rc.lm.n_owned_cells} owned), "
-            f"{len(lay.locals[rank].send_cells)} peers, set up in {time.time() - t1:.1f}s")
+            f"{len(lay.locals[rank].send_cells)} peers, set up in {time.time() - t1:.1f}s "
+            f"(host rss {_rss_gb():.1f} GB)")
     ctx.set_profiling(2)  # events around the dominant (first full-mesh) evaluation only
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=local)
 

@@ -39,6 +39,35 @@ def swap_needs(rank: int, n_ranks: int, needs: dict) -> dict:
     return {int(q): allv[int(q)].get(rank, np.zeros(0, np.int32)) for q in needs}
 
 
+def publish_store(store_dir, wl, device: int = 0) -> dict:
+    """Rank 0 of a multi-GPU job: device region labels of the global mesh
+    (one global context, closed again), the locality order, then the whole
+    workload + labels written as a binary store (store.py) that every rank
+    memory-maps.  Returns the extra arrays written."""
+    from . import store
+    g = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, device=device)
+    rm = g.make_regions(wl.fine_mask, wl.width)
+    g.close()
+    del g
+    extra = {"cell_label": np.asarray(rm.cell_label, np.uint8),
+             "cell_sub": np.asarray(rm.cell_sublabel, np.uint8),
+             "edge_label": np.asarray(rm.edge_label, np.uint8),
+             "order": np.asarray(wl.mesh.locality_order(), np.int32)}
+    store.save_workload(store_dir, wl, extra, digest=False)
+    return extra
+
+
+def layout_from_store(store_dir, rank: int, n_ranks: int):
+    """(workload, DistributedLayout for ``rank`` alone) from a published
+    store: the global tables are shared read-only maps, only this rank's
+    local mesh and halo plan are materialised."""
+    from . import store
+    wl, extra = store.load_workload(store_dir, mmap=True)
+    lay = DistributedLayout(wl.mesh, extra["cell_label"], extra["cell_sub"], extra["edge_label"],
+                            n_ranks, order=np.asarray(extra["order"]), only=rank)
+    return wl, lay
+
+
 class DistributedLayout:
     """Partition + local meshes of a global mesh with given region labels."""
 
