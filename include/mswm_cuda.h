@@ -223,6 +223,19 @@ int mswm_cuda_stencil_info(const mswm_cuda_ctx* ctx, int* offsets16, int64_t* n_
  * step graph launches (the bench's gpu_launches evidence). */
 int mswm_cuda_kernels_per_step(mswm_cuda_ctx* ctx, int64_t* n);
 
+/* Cost replication (SchemeConfig::replication, integrators.hpp:33-39;
+ * SerialEvaluator's `replication`, integrators.cpp:117-129): every
+ * evaluation repeats the tendency arithmetic `replication` times
+ * (operators.cpp:60) -- results unchanged, ledger counts scaled by it
+ * (integrators.cpp:302-335).  MSWM_E_CONFIG when < 1. */
+int mswm_cuda_set_replication(mswm_cuda_ctx* ctx, int replication);
+
+/* LTS3 schedule of the most recent step graph: concurrent_coarse = 1 when
+ * the coarse stage (integrators.cpp:557-563) ran on its own stream
+ * concurrently with the substeps (with ranks: its halo exchange too, on a
+ * second communicator), 0 in sequence, -1 not yet captured. */
+int mswm_cuda_schedule_info(const mswm_cuda_ctx* ctx, int* concurrent_coarse);
+
 /* Device diagnostics: total_mass (proj/src/harness.cpp:99-105) of the
  * device state, summed in ascending original cell id order (bitwise equal
  * to the reference). */

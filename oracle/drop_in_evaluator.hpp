@@ -16,6 +16,7 @@
 
 #include "mswm/errors.hpp"
 #include "mswm/integrators.hpp"
+#include "mswm/ledger.hpp"
 #include "mswm/mesh.hpp"
 #include "mswm/regions.hpp"
 #include "mswm_cuda.h"
@@ -95,6 +96,95 @@ class CudaEvaluator : public TendencyEvaluator {
 
  private:
   mswm_cuda_ctx* ctx_ = nullptr;
+};
+
+// The device-resident counterpart of Stepper (integrators.hpp:136-160):
+// same step entry points and the same ledger, but the whole coarse step --
+// every stage, prediction, accumulation and correction -- runs on the GPU as
+// one graph replay (mswm_cuda_step) instead of one eval() per stage.  The
+// caller's State is uploaded, stepped and downloaded per call; advance()
+// runs n steps between one upload and one download.  Errors map to the
+// reference's exceptions (ConfigError for dt <= 0 / M < 1 / missing map,
+// DryVertexError with its step, integrators.cpp:413-421, harness.cpp:183-190).
+class CudaStepper {
+ public:
+  CudaStepper(const VoronoiMesh& mesh, const RegionMap* map, const CellField& b,
+              const VertexField& f_vertex, double gravity, WorkLedger* ledger,
+              int replication = 1, int device = 0, const int32_t* cell_order = nullptr)
+      : ledger_(ledger), n_cells_(mesh.n_cells), n_edges_(mesh.n_edges) {
+    const mswm_mesh_desc d = cuda_mesh_desc(mesh);
+    if (mswm_cuda_create(&d, device, cell_order, &ctx_) != MSWM_OK)
+      throw Error(std::string("mswm_cuda_create: ") + mswm_cuda_last_error(nullptr));
+    try {
+      cuda_check(mswm_cuda_set_fields(ctx_, b.ptr(), f_vertex.ptr(), gravity), ctx_);
+      cuda_check(mswm_cuda_set_replication(ctx_, replication), ctx_);
+      if (map) {
+        std::vector<uint8_t> fine(mesh.n_cells);
+        for (int i = 0; i < mesh.n_cells; ++i) fine[i] = map->cell_label[i] == CellRegion::Fine;
+        cuda_check(mswm_cuda_set_regions(ctx_, fine.data(), map->interface_width, nullptr,
+                                         nullptr, nullptr, nullptr, nullptr),
+                   ctx_);
+      }
+    } catch (...) {
+      mswm_cuda_destroy(ctx_);
+      throw;
+    }
+  }
+  ~CudaStepper() { mswm_cuda_destroy(ctx_); }
+  CudaStepper(const CudaStepper&) = delete;
+  CudaStepper& operator=(const CudaStepper&) = delete;
+
+  void ssprk_step(int order, State& state, double dt) {
+    if (order != 2 && order != 3) throw UsageError("SSPRK order must be 2 or 3");
+    run(order == 2 ? MSWM_SSPRK2 : MSWM_SSPRK3, state, dt, 1, 1);
+  }
+  void rk4_step(State& state, double dt) { run(MSWM_RK4, state, dt, 1, 1); }
+  void lts_step(int order, State& state, double dt, int substeps) {
+    if (order != 2 && order != 3) throw UsageError("LTS order must be 2 or 3");
+    run(order == 2 ? MSWM_LTS2 : MSWM_LTS3, state, dt, substeps, 1);
+  }
+  void step(State& state, const SchemeConfig& cfg) { advance(state, cfg, 1); }
+
+  // n_steps of cfg.scheme with the state resident on the GPU in between.
+  void advance(State& state, const SchemeConfig& cfg, int64_t n_steps) {
+    run(scheme_of(cfg.scheme), state, cfg.dt, cfg.substeps, n_steps);
+  }
+
+  mswm_cuda_ctx* context() { return ctx_; }
+
+ private:
+  static int scheme_of(Scheme s) {
+    switch (s) {
+      case Scheme::SSPRK2: return MSWM_SSPRK2;
+      case Scheme::SSPRK3: return MSWM_SSPRK3;
+      case Scheme::RK4: return MSWM_RK4;
+      case Scheme::LTS2: return MSWM_LTS2;
+      case Scheme::LTS3: return MSWM_LTS3;
+    }
+    throw UsageError("unknown scheme");
+  }
+
+  void run(int scheme, State& st, double dt, int M, int64_t n) {
+    if (st.h.size() != std::size_t(n_cells_) || st.u.size() != std::size_t(n_edges_))
+      throw UsageError("state size does not match the mesh");
+    cuda_check(mswm_cuda_state_upload(ctx_, st.h.ptr(), st.u.ptr(), st.time), ctx_);
+    int64_t c0[16], e0[16], s0 = 0;
+    cuda_check(mswm_cuda_ledger(ctx_, c0, e0, &s0), ctx_);
+    cuda_check(mswm_cuda_step(ctx_, scheme, dt, M, n, 1), ctx_);
+    cuda_check(mswm_cuda_state_download(ctx_, st.h.ptr(), st.u.ptr(), &st.time), ctx_);
+    if (!ledger_) return;
+    int64_t c1[16], e1[16], s1 = 0;
+    cuda_check(mswm_cuda_ledger(ctx_, c1, e1, &s1), ctx_);
+    for (int r = 0; r < kLedgerRegionCount; ++r)
+      for (int k = 0; k < kLedgerStageCount; ++k) {
+        ledger_->add_cells(r, k, c1[4 * r + k] - c0[4 * r + k]);
+        ledger_->add_edges(r, k, e1[4 * r + k] - e0[4 * r + k]);
+      }
+  }
+
+  WorkLedger* ledger_;
+  mswm_cuda_ctx* ctx_ = nullptr;
+  int n_cells_, n_edges_;
 };
 
 }  // namespace mswm

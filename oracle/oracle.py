@@ -61,6 +61,17 @@ def dropin() -> C.CDLL:
         lib.ref_cuda_eval_create.restype = vp
         lib.ref_cuda_eval_create.argtypes = [vp, vp, f64p, f64p, C.c_double, C.c_int, C.c_char_p,
                                              C.c_int]
+        lib.ref_cuda_stepper_create.restype = vp
+        lib.ref_cuda_stepper_create.argtypes = [vp, vp, f64p, f64p, C.c_double, C.c_int, C.c_int,
+                                                C.c_char_p, C.c_int]
+        lib.ref_cuda_stepper_free.restype = None
+        lib.ref_cuda_stepper_free.argtypes = [vp]
+        lib.ref_cuda_stepper_run.restype = C.c_int
+        lib.ref_cuda_stepper_run.argtypes = [vp, C.c_int, f64p, f64p, f64p, C.c_double, C.c_int,
+                                             C.c_int64, C.c_int, C.c_char_p, C.c_int,
+                                             C.POINTER(C.c_int)]
+        lib.ref_cuda_stepper_ledger.restype = None
+        lib.ref_cuda_stepper_ledger.argtypes = [vp, i64p, i64p]
         _dropin = lib
     return _dropin
 
@@ -91,7 +102,7 @@ def ref() -> C.CDLL:
             "ref_regions_labels": (None, [vp, u8p, u8p, u8p]),
             "ref_regions_group": (C.c_int64, [vp, C.c_int, i32p]),
             "ref_regions_validate": (C.c_int, [vp, vp]),
-            "ref_eval_create": (vp, [vp, vp, f64p, f64p, C.c_double, C.c_int, C.c_uint64] + E),
+            "ref_eval_create": (vp, [vp, vp, f64p, f64p, C.c_double, C.c_int, C.c_uint64, C.c_int] + E),
             "ref_eval_free": (None, [vp]),
             "ref_eval": (C.c_int, [vp, f64p, f64p, C.c_uint, f64p, f64p] + E
                          + [C.POINTER(C.c_int)]),
@@ -249,13 +260,13 @@ class RefEvaluator:
     """SerialEvaluator (nranks=0) or ThreadedEvaluator (nranks>=1)."""
 
     def __init__(self, mesh: RefMesh, regions: RefRegions | None, b, f, gravity, nranks=0,
-                 seed=12345):
+                 seed=12345, replication=1):
         self.b = np.ascontiguousarray(b, np.float64)
         self.f = np.ascontiguousarray(f, np.float64)
         buf = _err()
         self.handle = ref().ref_eval_create(mesh.handle, regions.handle if regions else None,
                                             _p(self.b, f64p), _p(self.f, f64p), gravity, nranks,
-                                            seed, buf, ERRLEN)
+                                            seed, replication, buf, ERRLEN)
         if not self.handle:
             raise OracleError(1, buf.value.decode())
         self.mesh, self.regions = mesh, regions
@@ -328,6 +339,46 @@ class RefEvaluator:
         s = C.c_int64(0)
         ref().ref_ledger(self.stepper, _p(c, i64p), _p(e, i64p), C.byref(s))
         return c.reshape(4, 4), e.reshape(4, 4), s.value
+
+
+class CudaStepperRef:
+    """mswm::CudaStepper (oracle/drop_in_evaluator.hpp), the C++
+    device-resident Stepper over the C ABI, on a reference mesh / map."""
+
+    def __init__(self, mesh: RefMesh, regions: RefRegions | None, b, f, gravity, replication=1,
+                 device=0):
+        self.b = np.ascontiguousarray(b, np.float64)
+        self.f = np.ascontiguousarray(f, np.float64)
+        buf = _err()
+        self.handle = dropin().ref_cuda_stepper_create(
+            mesh.handle, regions.handle if regions else None, _p(self.b, f64p), _p(self.f, f64p),
+            gravity, replication, device, buf, ERRLEN)
+        if not self.handle:
+            raise OracleError(5, buf.value.decode())
+        self.mesh, self.regions = mesh, regions
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            dropin().ref_cuda_stepper_free(self.handle)
+            self.handle = None
+
+    def run(self, scheme, h, u, time, dt, M, n_steps, per_call=True):
+        h = np.array(h, np.float64, copy=True)
+        u = np.array(u, np.float64, copy=True)
+        t = C.c_double(time)
+        dv = C.c_int(-1)
+        buf = _err()
+        rc = dropin().ref_cuda_stepper_run(self.handle, scheme, _p(h, f64p), _p(u, f64p),
+                                           C.byref(t), dt, M, n_steps, int(per_call), buf, ERRLEN,
+                                           C.byref(dv))
+        _check(rc, buf, dv.value)
+        return h, u, t.value
+
+    def ledger(self):
+        c = np.zeros(16, np.int64)
+        e = np.zeros(16, np.int64)
+        dropin().ref_cuda_stepper_ledger(self.handle, _p(c, i64p), _p(e, i64p))
+        return c.reshape(4, 4), e.reshape(4, 4)
 
 
 def ref_lts_coeffs(order, stage, k, M):

@@ -270,7 +270,7 @@ int ref_regions_validate(void* mp, void* rp) {
 // partition_multiconstraint(build_cell_graph(mesh, map), nranks, seed) and
 // make_block_plan -- the reference's emulated-rank path (mswm.cpp:319-323).
 void* ref_eval_create(void* mp, void* rp, const double* b, const double* f, double gravity,
-                      int nranks, uint64_t seed, char* err, int errlen) {
+                      int nranks, uint64_t seed, int replication, char* err, int errlen) {
   auto* m = static_cast<VoronoiMesh*>(mp);
   auto* r = static_cast<RegionMap*>(rp);
   Evaluator* out = nullptr;
@@ -283,14 +283,16 @@ void* ref_eval_create(void* mp, void* rp, const double* b, const double* f, doub
     std::copy(b, b + m->n_cells, ev->b.data.begin());
     std::copy(f, f + m->n_vertices, ev->f.data.begin());
     ev->gravity = gravity;
+    ev->replication = replication;
     if (nranks <= 0) {
-      ev->ev = std::make_unique<SerialEvaluator>(*m, r, ev->b, ev->f, gravity, 1);
+      ev->ev = std::make_unique<SerialEvaluator>(*m, r, ev->b, ev->f, gravity, replication);
     } else {
       if (!r) throw UsageError("threaded evaluator needs a region map");
       const CellGraph g = build_cell_graph(*m, r);
       const std::vector<int> labels = partition_multiconstraint(g, nranks, seed, nullptr);
       ev->plan = std::make_unique<PartitionPlan>(make_block_plan(*m, *r, labels, nranks));
-      ev->ev = std::make_unique<ThreadedEvaluator>(*m, *r, *ev->plan, ev->b, ev->f, gravity, 1);
+      ev->ev = std::make_unique<ThreadedEvaluator>(*m, *r, *ev->plan, ev->b, ev->f, gravity,
+                                                   replication);
     }
     out = ev.release();
   });
@@ -339,7 +341,7 @@ void* ref_stepper_create(void* ep) {
   auto* e = static_cast<Evaluator*>(ep);
   auto* s = new StepperBox();
   s->mesh = e->mesh;
-  s->stepper = std::make_unique<Stepper>(*e->mesh, e->map, *e->ev, &s->ledger, 1);
+  s->stepper = std::make_unique<Stepper>(*e->mesh, e->map, *e->ev, &s->ledger, e->replication);
   return s;
 }
 

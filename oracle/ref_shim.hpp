@@ -61,6 +61,7 @@ struct Evaluator {
   CellField b;
   VertexField f;
   double gravity;
+  int replication = 1;  // SerialEvaluator / ThreadedEvaluator / Stepper cost replication
   std::unique_ptr<PartitionPlan> plan;
   std::unique_ptr<TendencyEvaluator> ev;
 };

@@ -166,6 +166,8 @@ def cuda() -> C.CDLL:
             "mswm_cuda_halo_needs": (C.c_int, [vp, C.c_uint, i64p, i32p]),
             "mswm_cuda_set_halo_mask": (C.c_int, [vp, C.c_uint, i64p, i32p, i64p, i32p]),
             "mswm_cuda_kernels_per_step": (C.c_int, [vp, i64p]),
+            "mswm_cuda_schedule_info": (C.c_int, [vp, C.POINTER(C.c_int)]),
+            "mswm_cuda_set_replication": (C.c_int, [vp, C.c_int]),
             "mswm_cuda_layout_info": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
             "mswm_cuda_stencil_info": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int64)]),
             "mswm_cuda_set_labels": (C.c_int, [vp, u8p, u8p, u8p, u8p, u8p, C.c_int]),

@@ -383,6 +383,19 @@ class CudaContext:
         self._check(self.lib.mswm_cuda_kernels_per_step(self.handle, C.byref(n)))
         return n.value
 
+    def set_replication(self, replication: int) -> None:
+        """Cost replication (SchemeConfig::replication): the tendency
+        arithmetic repeated per evaluation (operators.cpp:60), results
+        unchanged, ledger counts scaled."""
+        self._check(self.lib.mswm_cuda_set_replication(self.handle, int(replication)))
+
+    def concurrent_coarse(self) -> int:
+        """1: the last captured LTS3 step ran its coarse stage concurrently
+        with the substeps; 0: in sequence; -1: no LTS3 step captured yet."""
+        v = C.c_int(0)
+        self._check(self.lib.mswm_cuda_schedule_info(self.handle, C.byref(v)))
+        return v.value
+
     def total_mass(self) -> float:
         out = C.c_double(0.0)
         self._check(self.lib.mswm_cuda_total_mass(self.handle, C.byref(out)))

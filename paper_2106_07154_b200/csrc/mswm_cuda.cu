@@ -151,6 +151,12 @@ struct MaskPlan {
   DArr<int32_t> rw_list;  // k_out_rw tiles holding outputs (null: every tile)
   int32_t rw_n = 0;
   std::vector<int32_t> host_cells, host_edges;  // original ids, same order as device lists
+  // drop-in eval I/O (mswm_cuda_eval): the h / u entries the evaluation
+  // reads, original ids on the host and internal ids on the device (built on
+  // first use); full_* = the read set covers most of the mesh, upload whole
+  bool io_ready = false, io_full_c = false, io_full_e = false;
+  std::vector<int32_t> io_rc_orig, io_re_orig;
+  DArr<int32_t> io_rc, io_re;
 };
 
 // Halo exchange plan of one rank: per peer slot, the owned values it sends
@@ -179,6 +185,8 @@ struct NcclApi {
   ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  // optional (NCCL >= 2.18): a second communicator for the forked coarse step
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, void*) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -200,6 +208,7 @@ NcclApi& nccl() {
     a.Send = reinterpret_cast<decltype(a.Send)>(sym("ncclSend"));
     a.Recv = reinterpret_cast<decltype(a.Recv)>(sym("ncclRecv"));
     a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
+    a.CommSplit = reinterpret_cast<decltype(a.CommSplit)>(sym("ncclCommSplit"));
     a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.GroupStart && a.GroupEnd &&
            a.Send && a.Recv && a.GetErrorString;
     if (!a.ok) a.why = "libnccl.so.2 lacks the p2p API";
@@ -231,6 +240,7 @@ struct mswm_cuda_ctx {
   // §8(e)); masks without one exchange the full halo
   std::map<unsigned, Halo> halo_mask;
   ncclComm_t nccl_comm = nullptr;
+  ncclComm_t nccl_comm2 = nullptr;  // the concurrent coarse step's exchanges (ncclCommSplit)
   std::string last_error;
   int32_t nC = 0, nE = 0, nV = 0, deg_max = 0, sten_max = 0;
   bool identity = true;
@@ -286,9 +296,13 @@ struct mswm_cuda_ctx {
   DArr<int32_t> band_cells, band_edges;
   int32_t n_band_c = 0, n_band_e = 0;
   int fork_state = 0;  // 0 not prepared, 1 ready, -1 not eligible
+  int replication = 1;  // SchemeConfig::replication (operators.cpp:60)
   cudaStream_t stream_of_capture = nullptr;
   DArr<int32_t> d_c_n2o, d_e_n2o;  // internal -> original ids (device permutes)
   DArr<double> io_h, io_u;          // staging for permuted uploads / downloads
+  double* pin = nullptr;            // pinned host staging of mswm_cuda_eval (packed reads / outputs)
+  size_t pin_n = 0;
+  DArr<double> io_pack;             // its device twin
   double time = 0.0;
   // dry-vertex flag: (step << 32 | original vertex), ~0 = none; set by kernel
   // A, cleared only after a synchronous check has reported it
@@ -349,6 +363,7 @@ struct mswm_cuda_ctx {
 
   ~mswm_cuda_ctx() {
     drop_graphs();
+    if (nccl_comm2) nccl().CommDestroy(nccl_comm2);
     if (nccl_comm) nccl().CommDestroy(nccl_comm);
     if (ls2) cudaStreamDestroy(ls2);
     if (lsh) cudaStreamDestroy(lsh);
@@ -356,6 +371,7 @@ struct mswm_cuda_ctx {
     if (ev_join) cudaEventDestroy(ev_join);
     if (ev_join_h) cudaEventDestroy(ev_join_h);
     if (stream) cudaStreamDestroy(stream);
+    if (pin) cudaFreeHost(pin);
   }
 
   DevMesh dev() const {
@@ -1246,9 +1262,9 @@ struct Side {
   int ctas_per_sm[3];  // resident-grid size of kernels A, B, C (0: default)
 };
 
-void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const double* u,
-                 const Op cop[2], const Op eop[2], const PredArgs* pred = nullptr,
-                 const Side* side = nullptr) {
+void launch_eval_once(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const double* u,
+                      const Op cop[2], const Op eop[2], const PredArgs* pred,
+                      const Side* side) {
   cudaStream_t s = side ? side->s : c->ls;
   double* const pv = side ? side->pv : c->pv.p;
   double* const Kp = side ? side->K : c->K.p;
@@ -1362,21 +1378,38 @@ Op mk_op(int kind, double* dst, const double* y0 = nullptr, double c0 = 0, const
   return o;
 }
 
+// One masked evaluation with its fused stage update.  With a replication
+// factor R > 1 (SchemeConfig::replication, operators.cpp:60: the kernel
+// arithmetic repeated to emulate more vertical layers) the three kernels run
+// R times; the first R - 1 passes store into the eval scratch (Dh / Du) and
+// only the last applies the stage update, so results are unchanged.
+void launch_eval(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, const double* u,
+                 const Op cop[2], const Op eop[2], const PredArgs* pred = nullptr,
+                 const Side* side = nullptr) {
+  for (int r = 1; r < c->replication; ++r) {
+    const Op so[2] = {mk_op(OP_STORE, c->Dh.p), mk_op(OP_STORE, c->Dh.p)};
+    const Op se[2] = {mk_op(OP_STORE, c->Du.p), mk_op(OP_STORE, c->Du.p)};
+    launch_eval_once(c, p, h, u, so, se, r == 1 ? pred : nullptr, side);
+  }
+  launch_eval_once(c, p, h, u, cop, eop, c->replication > 1 ? nullptr : pred, side);
+}
+
 // ---------------------------------------------------------------------------
 // ledger (Stepper::tally, integrators.cpp:302-335)
 
 void tally(mswm_cuda_ctx* c, unsigned mask, int stage) {
+  const int64_t L = c->replication;  // counts scale with the replication (integrators.cpp:304)
   if (!c->have_regions) {
-    if (mask & MSWM_CELLS_ALL) c->ledger_cell[0][stage] += c->nC;
-    if (mask & MSWM_EDGES_ALL) c->ledger_edge[0][stage] += c->nE;
+    if (mask & MSWM_CELLS_ALL) c->ledger_cell[0][stage] += L * c->nC;
+    if (mask & MSWM_EDGES_ALL) c->ledger_edge[0][stage] += L * c->nE;
     return;
   }
   static const int cell_region[6] = {0, 0, 0, 1, 2, 3};
   static const int edge_region[5] = {0, 0, 1, 2, 3};
   for (int g = 0; g < 6; ++g)
-    if (mask & (1u << g)) c->ledger_cell[cell_region[g]][stage] += c->gsize[g];
+    if (mask & (1u << g)) c->ledger_cell[cell_region[g]][stage] += L * c->gsize[g];
   for (int g = 0; g < 5; ++g)
-    if (mask & (1u << (6 + g))) c->ledger_edge[edge_region[g]][stage] += c->gsize[6 + g];
+    if (mask & (1u << (6 + g))) c->ledger_edge[edge_region[g]][stage] += L * c->gsize[6 + g];
 }
 
 constexpr unsigned kMaskCoarseOnly = MSWM_CELLS_COARSE | MSWM_EDGES_COARSE;
@@ -1487,7 +1520,8 @@ bool restricted(const std::vector<mswm_cuda_ctx*>& cs) {
   return false;
 }
 
-void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us, unsigned mask) {
+void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us, unsigned mask,
+              bool second_comm = false) {
   bool any = false;
   for (auto* c : cs) any |= c->halo.active();
   if (!any) return;
@@ -1499,18 +1533,29 @@ void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us, unsigned ma
       ++c->launches;
     }
   }
-  if (cs.size() == 1) {
+  static const bool dry_run = [] {
+    const char* e = std::getenv("MSWM_HALO_DRYRUN");
+    return e && e[0] == '1';
+  }();
+  if (cs.size() == 1 && dry_run) {
+    // timing aid only (results are wrong): one rank of a partition stepped
+    // alone on one GPU -- pack and unpack run, the transfer is skipped
+  } else if (cs.size() == 1) {
     mswm_cuda_ctx* c = cs[0];
     Halo& x = halo_for(c, mask);
     if (!c->nccl_comm) throw Error(MSWM_E_USAGE, "halo set but no communicator (mswm_cuda_comm_init)");
+    // the forked coarse step exchanges on its own stream: a communicator of
+    // its own keeps the two streams' NCCL operations independent
+    ncclComm_t comm = second_comm ? c->nccl_comm2 : c->nccl_comm;
+    if (!comm) throw Error(MSWM_E_NCCL, "no second communicator for the concurrent coarse step");
     nccl_check(nccl().GroupStart());
     for (size_t j = 0; j < x.peer.size(); ++j) {
       if (x.scnt[j])
         nccl_check(nccl().Send(x.sbuf.p + x.soff[j], size_t(x.scnt[j]), ncclFloat64, x.peer[j],
-                               c->nccl_comm, c->ls));
+                               comm, c->ls));
       if (x.rcnt[j])
         nccl_check(nccl().Recv(x.rbuf.p + x.roff[j], size_t(x.rcnt[j]), ncclFloat64, x.peer[j],
-                               c->nccl_comm, c->ls));
+                               comm, c->ls));
     }
     nccl_check(nccl().GroupEnd());
   } else {
@@ -1556,7 +1601,15 @@ void prepare_fork(mswm_cuda_ctx* c) {
   if (c->fork_state != 0) return;
   c->fork_state = -1;
   const char* fe = std::getenv("MSWM_FORK");
-  if ((fe && fe[0] == '0') || c->halo.active() || !c->have_regions) return;
+  if ((fe && fe[0] == '0') || !c->have_regions) return;
+  if (c->halo.active()) {
+    // ranks: the coarse step's exchange runs on the fork stream concurrently
+    // with the substeps' exchanges, so both need buffers of their own
+    // (per-mask restricted halos) and, between processes, the second
+    // communicator
+    if (!c->halo_mask.count(kMaskSub) || !c->halo_mask.count(kMaskCoarseOnly)) return;
+    if (c->nccl_comm && !c->nccl_comm2) return;
+  }
   MaskPlan& ps = plan_for(c, kMaskSub);
   MaskPlan& pc = plan_for(c, kMaskCoarseOnly);
   if (const char* fc = std::getenv("MSWM_FORK_CTAS")) {  // "n" or "a,b,c"
@@ -1582,6 +1635,15 @@ void prepare_fork(mswm_cuda_ctx* c) {
   CK(cudaMemcpyAsync(kc.data(), c->ckey.p, size_t(c->nC), cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(ke.data(), c->ekey.p, size_t(c->nE), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  // ranks: the substeps' exchanges also read h_old / u_old (the state) on
+  // the owned elements they send
+  if (c->halo.active()) {
+    const Halo& xs = halo_for(c, kMaskSub);
+    for (const int32_t code : xs.h_scode) {
+      if (code >= 0) hc[code] = 1;
+      else he[~code] = 1;
+    }
+  }
   std::vector<int32_t> bc, be;
   std::vector<uint32_t> cb((size_t(c->nC) + 31) / 32, 0u), eb((size_t(c->nE) + 31) / 32, 0u);
   for (int32_t i = 0; i < c->nC; ++i)
@@ -1640,30 +1702,37 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
     Op eo[2] = {mk_op(OP_WCOMB, U2, U, 0.75, U1, 0.25, cr), mk_op(OP_WCOMB, U2, U, 0.75, U1, 0.25, cr)};
     launch_eval(c, plan_for(c, kMaskIfCoarse), H1, U1, co, eo);
   }
-  // Step 4 forked onto the second stream (prepare_fork)
-  const bool fork = cs.size() == 1 && cs[0]->fork_state == 1;
+  // Step 4 forked onto the second stream (prepare_fork); with ranks, its
+  // (restricted) halo exchange of h2/u2 rides on that stream too.  The
+  // streams and events of member 0 serve the whole group.
+  bool fork = true;
+  for (auto* c : cs) fork &= c->fork_state == 1;
+  mswm_cuda_ctx* const c0 = cs[0];
+  cudaStream_t capture_stream = c0->ls;
   if (fork) {
-    mswm_cuda_ctx* c = cs[0];
-    c->stream_of_capture = c->ls;
-    CK(cudaEventRecord(c->ev_fork, c->ls));
-    CK(cudaStreamWaitEvent(c->ls2, c->ev_fork, 0));
-    const double cr = two3 * dt;
-    double *H = c->H.p, *U = c->U.p, *H2 = c->H2.p, *U2 = c->U2.p;
-    Op co = mk_op(OP_WCOMB, H, H, third, H2, two3, cr);
-    Op eo = mk_op(OP_WCOMB, U, U, third, U2, two3, cr);
-    co.alt = c->T1h.p;
-    co.altbits = c->band_cbits.p;
-    eo.alt = c->T1u.p;
-    eo.altbits = c->band_ebits.p;
-    Op cos[2] = {co, co}, eos[2] = {eo, eo};
-    const Side side{c->ls2, c->pv2.p, c->K2.p, c->FQ2.p,
-                    {c->fork_ctas[0], c->fork_ctas[1], c->fork_ctas[2]}};
-    launch_eval(c, plan_for(c, kMaskCoarseOnly), H2, U2, cos, eos, nullptr, &side);
-    CK(cudaEventRecord(c->ev_join, c->ls2));
+    CK(cudaEventRecord(c0->ev_fork, capture_stream));
+    CK(cudaStreamWaitEvent(c0->ls2, c0->ev_fork, 0));
+    for (auto* c : cs) c->ls = c0->ls2;
+    if (restricted(cs)) exchange(cs, &C::H2, &C::U2, kMaskCoarseOnly, true);
+    for (auto* c : cs) {
+      const double cr = two3 * dt;
+      double *H = c->H.p, *U = c->U.p, *H2 = c->H2.p, *U2 = c->U2.p;
+      Op co = mk_op(OP_WCOMB, H, H, third, H2, two3, cr);
+      Op eo = mk_op(OP_WCOMB, U, U, third, U2, two3, cr);
+      co.alt = c->T1h.p;
+      co.altbits = c->band_cbits.p;
+      eo.alt = c->T1u.p;
+      eo.altbits = c->band_ebits.p;
+      Op cos[2] = {co, co}, eos[2] = {eo, eo};
+      const Side side{c0->ls2, c->pv2.p, c->K2.p, c->FQ2.p,
+                      {c->fork_ctas[0], c->fork_ctas[1], c->fork_ctas[2]}};
+      launch_eval(c, plan_for(c, kMaskCoarseOnly), H2, U2, cos, eos, nullptr, &side);
+    }
+    CK(cudaEventRecord(c0->ev_join, c0->ls2));
     // the substeps on the high-priority stream: their CTAs take SM slots
     // ahead of the coarse step's as slots free up
-    CK(cudaStreamWaitEvent(c->lsh, c->ev_fork, 0));
-    c->ls = c->lsh;
+    CK(cudaStreamWaitEvent(c0->lsh, c0->ev_fork, 0));
+    for (auto* c : cs) c->ls = c0->lsh;
   }
   // Substep prologue: save I1 u I2 old values, I1 stage values, predict
   // stage 1 of substep 0 into the state (ha == state).
@@ -1738,17 +1807,18 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
   // refreshed them; only fine/I1 entries, never read here, changed since);
   // restricted halos refreshed only the substep's read set.
   if (fork) {
-    mswm_cuda_ctx* c = cs[0];
-    CK(cudaEventRecord(c->ev_join_h, c->lsh));
-    c->ls = c->stream_of_capture;
-    CK(cudaStreamWaitEvent(c->ls, c->ev_join_h, 0));
-    CK(cudaStreamWaitEvent(c->ls, c->ev_join, 0));
-    const int64_t nb = int64_t(c->n_band_c) + c->n_band_e;
-    if (nb > 0) {
-      k_copy_band<<<nblk(nb), kBlock, 0, c->ls>>>(c->band_cells.p, c->n_band_c, c->T1h.p, c->H.p,
-                                                  c->band_edges.p, c->n_band_e, c->T1u.p, c->U.p);
-      CK(cudaGetLastError());
-      ++c->launches;
+    CK(cudaEventRecord(c0->ev_join_h, c0->lsh));
+    for (auto* c : cs) c->ls = capture_stream;
+    CK(cudaStreamWaitEvent(capture_stream, c0->ev_join_h, 0));
+    CK(cudaStreamWaitEvent(capture_stream, c0->ev_join, 0));
+    for (auto* c : cs) {
+      const int64_t nb = int64_t(c->n_band_c) + c->n_band_e;
+      if (nb > 0) {
+        k_copy_band<<<nblk(nb), kBlock, 0, c->ls>>>(c->band_cells.p, c->n_band_c, c->T1h.p, c->H.p,
+                                                    c->band_edges.p, c->n_band_e, c->T1u.p, c->U.p);
+        CK(cudaGetLastError());
+        ++c->launches;
+      }
     }
     return;
   }
@@ -1983,7 +2053,7 @@ mswm_cuda_ctx::Graph capture_step(std::vector<mswm_cuda_ctx*>& cs, cudaStream_t 
       plan_for(c, kMaskIfCoarse);
       plan_for(c, kMaskSub);
       plan_for(c, kMaskCoarseOnly);
-      if (scheme == MSWM_LTS3 && cs.size() == 1) prepare_fork(c);
+      if (scheme == MSWM_LTS3) prepare_fork(c);
     } else {
       plan_for(c, MSWM_MASK_ALL);
     }
@@ -2267,6 +2337,62 @@ int mswm_cuda_get_closure(mswm_cuda_ctx* c, unsigned mask, int kind, int32_t* id
   });
 }
 
+// Read set of a mask plan for the drop-in eval (k_mark_reads over its
+// closure lists, operators.cpp:61-86) as original / internal id lists.
+void build_eval_io(mswm_cuda_ctx* c, MaskPlan& p) {
+  if (p.io_ready) return;
+  cudaStream_t s = c->stream;
+  DArr<uint8_t> cr, er;
+  cr.alloc(c->nC);
+  er.alloc(c->nE);
+  cr.zero(s);
+  er.zero(s);
+  const int64_t n = int64_t(p.nv) + p.nk + p.nf + p.ne;
+  if (n > 0) {
+    k_mark_reads<<<nblk(n), kBlock, 0, s>>>(c->dev(), p.vclos.p, p.nv, p.kclos.p, p.nk, p.fclos.p,
+                                            p.nf, p.edges, p.ne, cr.p, er.p);
+    CK(cudaGetLastError());
+  }
+  std::vector<uint8_t> hc(c->nC), he(c->nE);
+  CK(cudaMemcpyAsync(hc.data(), cr.p, size_t(c->nC), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(he.data(), er.p, size_t(c->nE), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  std::vector<int32_t> ci, ei;
+  p.io_rc_orig.clear();
+  p.io_re_orig.clear();
+  for (int32_t o = 0; o < c->nC; ++o) {
+    const int32_t ni = c->identity ? o : c->c_old2new[o];
+    if (hc[ni]) {
+      p.io_rc_orig.push_back(o);
+      ci.push_back(ni);
+    }
+  }
+  for (int32_t o = 0; o < c->nE; ++o) {
+    const int32_t ni = c->identity ? o : c->e_old2new[o];
+    if (he[ni]) {
+      p.io_re_orig.push_back(o);
+      ei.push_back(ni);
+    }
+  }
+  // packing pays while the read set is a minority of the mesh
+  p.io_full_c = 2 * ci.size() > size_t(c->nC);
+  p.io_full_e = 2 * ei.size() > size_t(c->nE);
+  if (!p.io_full_c && !ci.empty()) p.io_rc.upload(ci, s);
+  if (!p.io_full_e && !ei.empty()) p.io_re.upload(ei, s);
+  CK(cudaStreamSynchronize(s));
+  p.io_ready = true;
+}
+
+void ensure_pin(mswm_cuda_ctx* c, size_t n) {
+  if (c->pin_n >= n) return;
+  if (c->pin) CK(cudaFreeHost(c->pin));
+  c->pin = nullptr;
+  c->pin_n = 0;
+  CK(cudaMallocHost(&c->pin, n * 8));
+  c->pin_n = n;
+  c->io_pack.alloc(n);
+}
+
 int mswm_cuda_eval(mswm_cuda_ctx* c, const double* h, const double* u, unsigned mask, double* dh,
                    double* du) {
   return guard(c, [&] {
@@ -2275,31 +2401,49 @@ int mswm_cuda_eval(mswm_cuda_ctx* c, const double* h, const double* u, unsigned 
     if (!c->have_fields) throw Error(MSWM_E_USAGE, "set_fields must be called before eval");
     check_dry(c);  // a pending error of an earlier step batch surfaces first
     MaskPlan& p = plan_for(c, mask);
-    upload_field(c, c->T1h, h, c->c_new2old, c->nC);
-    upload_field(c, c->T1u, u, c->e_new2old, c->nE);
+    build_eval_io(c, p);
+    cudaStream_t s = c->stream;
+    // inputs: only the h / u entries the evaluation reads cross PCIe (packed
+    // through pinned staging), unless they are most of the mesh
+    if (c->T1h.n != size_t(c->nC)) c->T1h.alloc(c->nC);
+    if (c->T1u.n != size_t(c->nE)) c->T1u.alloc(c->nE);
+    const size_t nrc = p.io_full_c ? 0 : p.io_rc_orig.size();
+    const size_t nre = p.io_full_e ? 0 : p.io_re_orig.size();
+    const size_t nout = size_t(p.nc) + p.ne;
+    ensure_pin(c, std::max<size_t>(1, std::max(nrc + nre, nout)));
+    if (p.io_full_c) upload_field(c, c->T1h, h, c->c_new2old, c->nC);
+    if (p.io_full_e) upload_field(c, c->T1u, u, c->e_new2old, c->nE);
+    if (nrc + nre > 0) {
+      for (size_t k = 0; k < nrc; ++k) c->pin[k] = h[p.io_rc_orig[k]];
+      for (size_t k = 0; k < nre; ++k) c->pin[nrc + k] = u[p.io_re_orig[k]];
+      CK(cudaMemcpyAsync(c->io_pack.p, c->pin, (nrc + nre) * 8, cudaMemcpyHostToDevice, s));
+      if (nrc)
+        k_scatter_perm<<<nblk(int64_t(nrc)), kBlock, 0, s>>>(int32_t(nrc), p.io_rc.p, c->io_pack.p,
+                                                             c->T1h.p);
+      if (nre)
+        k_scatter_perm<<<nblk(int64_t(nre)), kBlock, 0, s>>>(int32_t(nre), p.io_re.p,
+                                                             c->io_pack.p + nrc, c->T1u.p);
+      CK(cudaGetLastError());
+    }
     Op co[2] = {mk_op(OP_STORE, c->Dh.p), mk_op(OP_STORE, c->Dh.p)};
     Op eo[2] = {mk_op(OP_STORE, c->Du.p), mk_op(OP_STORE, c->Du.p)};
     launch_eval(c, p, c->T1h.p, c->T1u.p, co, eo);
+    // outputs: gathered on the device in the plan's order, one packed copy
+    // back, scattered into the caller's arrays; everything else is left
+    // untouched (integrators.hpp:63-67)
+    if (nout > 0) {
+      if (p.nc)
+        k_gather_perm<<<nblk(int64_t(p.nc)), kBlock, 0, s>>>(p.nc, p.cells, c->Dh.p, c->io_pack.p);
+      if (p.ne)
+        k_gather_perm<<<nblk(int64_t(p.ne)), kBlock, 0, s>>>(p.ne, p.edges, c->Du.p,
+                                                             c->io_pack.p + p.nc);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(c->pin, c->io_pack.p, nout * 8, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
     check_dry(c);
-    // Gather the masked entries and scatter them into the caller's arrays;
-    // everything else is left untouched (integrators.hpp:63-67).
-    std::vector<double> tmp(std::max(c->nC, c->nE));
-    if (p.nc) {
-      CK(cudaMemcpyAsync(tmp.data(), c->Dh.p, size_t(c->nC) * 8, cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaStreamSynchronize(c->stream));
-      for (int32_t k = 0; k < p.nc; ++k) {
-        const int32_t orig = p.host_cells[k];
-        dh[orig] = tmp[c->identity ? orig : c->c_old2new[orig]];
-      }
-    }
-    if (p.ne) {
-      CK(cudaMemcpyAsync(tmp.data(), c->Du.p, size_t(c->nE) * 8, cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaStreamSynchronize(c->stream));
-      for (int32_t k = 0; k < p.ne; ++k) {
-        const int32_t orig = p.host_edges[k];
-        du[orig] = tmp[c->identity ? orig : c->e_old2new[orig]];
-      }
-    }
+    for (int32_t k = 0; k < p.nc; ++k) dh[p.host_cells[k]] = c->pin[k];
+    for (int32_t k = 0; k < p.ne; ++k) du[p.host_edges[k]] = c->pin[p.nc + k];
     return int(MSWM_OK);
   });
 }
@@ -2426,6 +2570,25 @@ int mswm_cuda_stencil_info(const mswm_cuda_ctx* c, int* offsets16, int64_t* n_wi
 int mswm_cuda_kernels_per_step(mswm_cuda_ctx* c, int64_t* n) {
   if (!c || !n) return MSWM_E_USAGE;
   *n = c->last_kernels_per_step;
+  return MSWM_OK;
+}
+
+int mswm_cuda_set_replication(mswm_cuda_ctx* c, int replication) {
+  return guard(c, [&] {
+    check_ctx(c);
+    // integrators.cpp:128-129
+    if (replication < 1) throw Error(MSWM_E_CONFIG, "cost replication factor must be >= 1");
+    if (replication != c->replication) {
+      c->replication = replication;
+      c->drop_graphs();
+    }
+    return int(MSWM_OK);
+  });
+}
+
+int mswm_cuda_schedule_info(const mswm_cuda_ctx* c, int* concurrent_coarse) {
+  if (!c || !concurrent_coarse) return MSWM_E_USAGE;
+  *concurrent_coarse = c->fork_state == 0 ? -1 : (c->fork_state == 1 ? 1 : 0);
   return MSWM_OK;
 }
 
@@ -2722,7 +2885,13 @@ int mswm_cuda_comm_init(mswm_cuda_ctx* c, const void* unique_id, int rank, int n
       nccl().CommDestroy(c->nccl_comm);
       c->nccl_comm = nullptr;
     }
+    if (c->nccl_comm2) {
+      nccl().CommDestroy(c->nccl_comm2);
+      c->nccl_comm2 = nullptr;
+    }
     nccl_check(nccl().CommInitRank(&c->nccl_comm, n_ranks, id, rank));
+    if (nccl().CommSplit) nccl_check(nccl().CommSplit(c->nccl_comm, 0, rank, &c->nccl_comm2, nullptr));
+    c->fork_state = 0;  // the concurrent coarse step may use the new communicators
     c->drop_graphs();
     return int(MSWM_OK);
   });

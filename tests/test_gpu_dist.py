@@ -91,3 +91,32 @@ def test_group_restricted_halos_bitwise(n_ranks, scheme):
     for rc in ranks:
         rc.download_owned(h, u)
     assert bits_equal(h, h_ref) and bits_equal(u, u_ref)
+
+
+@pytest.mark.parametrize("fork", ["1", "0"])
+@pytest.mark.parametrize("n_ranks,M", [(2, 4), (3, 2), (4, 4)])
+def test_group_concurrent_coarse_step_bitwise(fork, n_ranks, M, monkeypatch):
+    """The coarse stage on its own stream with its own (restricted) halo
+    exchange, concurrent with the substeps and their exchanges, on every
+    rank: bitwise equal to the oracle over several coarse steps, and to the
+    sequential schedule (MSWM_FORK=0)."""
+    monkeypatch.setenv("MSWM_FORK", fork)
+    wl = W.small_sphere(6, seed=41, cap_deg=25.0, M=M)
+    o = Oracle(wl.mesh, wl.b, wl.f, wl.gravity)
+    o.set_regions(wl.fine_mask, wl.width)
+    cl, cs, el = o.labels()
+    h_ref, u_ref, _ = o.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, M, 3)
+    lay = DistributedLayout(wl.mesh, cl, cs, el, n_ranks)
+    ranks = [RankContext(lay, r, wl.b, wl.f, wl.gravity) for r in range(n_ranks)]
+    grp = CudaGroup(ranks)
+    grp.restrict_halos(LTS3_MASKS + [kMaskAll])
+    for rc in ranks:
+        rc.upload(wl.h, wl.u)
+    grp.advance(Scheme.LTS3, wl.dt, M, 3)
+    for rc in ranks:
+        assert rc.ctx.concurrent_coarse() == (1 if fork == "1" else 0)
+    h = np.full(wl.mesh.n_cells, np.nan)
+    u = np.full(wl.mesh.n_edges, np.nan)
+    for rc in ranks:
+        rc.download_owned(h, u)
+    assert bits_equal(h, h_ref) and bits_equal(u, u_ref)
