@@ -434,6 +434,134 @@ __global__ void MSWM_KOUT_BOUNDS k_out(DevMesh M, const double* __restrict__ h,
 }
 
 // ---------------------------------------------------------------------------
+// Phase C with the stencil rebuilt from cell rows (k_out_cr): the default
+// wherever the mesh's stencil is the reference builder's ring walk
+// (mesh_build.cpp:133-154, weights :343-362; verified bitwise at create).
+//
+// k_out streams 104 B/edge of explicit stencil tables (16-bit id offsets +
+// coefficient pairs).  But an edge's stencil is the rest of the rings of its
+// two cells, walked from the edge's slot, and its weights are running sums
+// of the ring's kite_area / A_i, minus 1/2, signed (edge_weight's rule).  So
+// one 128-byte row per cell -- ring edge ids, degree / sign bits, the kite
+// ratios and the ring edges' lengths -- serves all ~6 edges that touch the
+// cell (L1 / L2 hits after the first), and the per-edge tables shrink to
+// one slot byte.  The weight is rebuilt as (frac - 0.5) with the sign of
+// cell_sign * anchor, the coefficient as w * (l_e' * (1/d_e)): the exact
+// roundings of edge_weight and of k_out's coefficient table, so results are
+// bitwise the reference's (operators.cpp:91-116).
+struct __align__(16) CellRow {
+  int32_t id[6];   // ring edges (internal ids; padding slots hold 0)
+  uint32_t info;   // degree | cell_sign(ring edge j) < 0 at bit 8 + j
+  uint32_t pad;
+  double rat[6];   // kite_area / A_i per ring slot
+  double l[6];     // l of the ring edges
+};
+static_assert(sizeof(CellRow) == 128, "one 128-byte line per cell");
+
+template <class T>
+__device__ __forceinline__ T pick6(const T (&v)[6], int s) {
+  T r = v[0];
+  r = s == 1 ? v[1] : r;
+  r = s == 2 ? v[2] : r;
+  r = s == 3 ? v[3] : r;
+  r = s == 4 ? v[4] : r;
+  r = s == 5 ? v[5] : r;
+  return r;
+}
+
+// ring ids and info of one row (the first 32 bytes: two 16-byte loads)
+__device__ __forceinline__ void load_ids(const CellRow* __restrict__ rows, int32_t c,
+                                         int32_t (&id)[6], uint32_t& info) {
+  const int4* q = reinterpret_cast<const int4*>(rows + c);
+  const int4 a = q[0], b = q[1];
+  id[0] = a.x;
+  id[1] = a.y;
+  id[2] = a.z;
+  id[3] = a.w;
+  id[4] = b.x;
+  id[5] = b.y;
+  info = uint32_t(b.z);
+}
+
+#ifndef MSWM_KCR_MINB
+#define MSWM_KCR_MINB 6
+#endif
+
+__global__ void __launch_bounds__(kSBlock, MSWM_KCR_MINB)
+    k_out_cr(DevMesh M, const double* __restrict__ K, const double2* __restrict__ FQ,
+             const CellRow* __restrict__ rows, const uint8_t* __restrict__ e_slots, OutArgs a) {
+  const int32_t ncs = a.cs.n();
+  const int32_t n = ncs + a.es.n();
+  for (int32_t t = blockIdx.x * kSBlock + threadIdx.x; t < n; t += gridDim.x * kSBlock) {
+    if (t < ncs) {
+      // dh (operators.cpp:91-99)
+      const int32_t i = a.cs.at(t);
+      const int g = a.ckey ? a.ckey[i] : 0;
+      if (g > 5 || !((a.mask >> g) & 1u)) continue;
+      int32_t id[6];
+      uint32_t info;
+      load_ids(rows, i, id, info);
+      const int deg = info & 0xFF;
+      const double* lr = rows[i].l;
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < kFastDeg; ++j) {
+        const double l = lr[j];
+        const double x = ((info >> (8 + j)) & 1u ? -l : l) * FQ[id[j]].x;
+        if (j < deg) acc += x;
+      }
+      apply_op(a.cop[g <= 2 ? 0 : 1], i, -acc / M.c_area[i]);
+    } else {
+      // du (operators.cpp:101-116), stencil walked over the two cell rows
+      const int32_t e = a.es.at(t - ncs);
+      const int g = a.ekey ? a.ekey[e] : 0;
+      if (g > 4 || !((a.mask >> (6 + g)) & 1u)) continue;
+      const int2 cc = M.e_cells[e];
+      const uint32_t sl = e_slots[e];
+      const double inv_d = M.e_invd[e];
+      const double qt_e = FQ[e].y;
+      double pvflux = 0.0;
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const int32_t c = side ? cc.y : cc.x;
+        int32_t id[6];
+        uint32_t info;
+        load_ids(rows, c, id, info);
+        const int deg = info & 0xFF;
+        const int p = side ? ((sl >> 3) & 7) : (sl & 7);
+        const uint32_t aneg = (sl >> (6 + side)) & 1u;
+        const double* rr = rows[c].rat;
+        const double* lr = rows[c].l;
+        // the side's gathers first (ids known), then the walk
+        double2 fq[kFastDeg - 1];
+#pragma unroll
+        for (int k = 1; k < kFastDeg; ++k) {
+          int s = p + k;
+          if (s >= deg) s -= deg;
+          fq[k - 1] = FQ[pick6(id, s)];
+        }
+        double frac = 0.0;
+#pragma unroll
+        for (int k = 1; k < kFastDeg; ++k) {
+          if (k < deg) {
+            int s = p + k;
+            if (s >= deg) s -= deg;
+            const int sp = s == 0 ? deg - 1 : s - 1;
+            frac += rr[sp];
+            const double x = frac - 0.5;
+            const double w = (((info >> (8 + s)) & 1u) ^ aneg) ? -x : x;
+            const double coef = w * (lr[s] * inv_d);
+            pvflux += coef * fq[k - 1].x * (0.5 * (qt_e + fq[k - 1].y));
+          }
+        }
+      }
+      const double du = -pvflux - (K[cc.x] - K[cc.y]) * inv_d;
+      apply_op(a.eop[g <= 1 ? 0 : 1], e, du);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Phase C on cell tiles with ring-walk weights (k_out_rw): the default
 // wherever the mesh's stencil is the reference builder's ring walk
 // (mesh_build.cpp:133-154, weights :343-362; verified bitwise at create).

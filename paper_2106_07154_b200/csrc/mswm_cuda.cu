@@ -264,6 +264,9 @@ struct mswm_cuda_ctx {
   // tiled ring-walk phase C (k_out_rw, build_rw): tiles, their staged-set
   // lists, per-edge local ids / slots, per-cell kite/A rows and ring info
   bool rw_ok = false;
+  // phase C over per-cell rows (k_out_cr, build_cr): 128 B per cell + a slot byte per edge
+  bool cr_ok = false;
+  DArr<CellRow> c_rows;
   int32_t rw_ntiles = 0, rw_emax = 0, rw_cmax = 0, rw_blocks = 0;
   size_t rw_smem = 0;
   DArr<RwTile> rw_tiles;
@@ -628,6 +631,40 @@ bool derive_ring_stencil(const mswm_mesh_desc* d, std::vector<double>& kite_of_s
   return true;
 }
 
+// Rows of k_out_cr (kernels.cuh): per internal cell its ring edge ids,
+// degree / sign bits, kite ratios (kite_area / A_i, the rounding
+// derive_ring_stencil verified) and ring edge lengths; per internal edge its
+// slot byte.  Returns false (explicit k_out) when the mesh's stencil is not
+// the ring walk or rings exceed 6 edges.
+bool build_cr(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const std::vector<int32_t>& c_edge,
+              const std::vector<uint8_t>& c_deg, const std::vector<uint8_t>& c_sbits) {
+  if (c->deg_max > kFastDeg) return false;
+  std::vector<double> kite_of_slot;
+  std::vector<uint8_t> slots;
+  if (!derive_ring_stencil(d, kite_of_slot, slots)) return false;
+  const int32_t nC = c->nC, nE = c->nE;
+  std::vector<CellRow> rows(nC);
+  for (int32_t ni = 0; ni < nC; ++ni) {
+    const int32_t i = c->c_new2old[ni];
+    const int off = d->cell_offset[i];
+    CellRow& r = rows[ni];
+    std::memset(&r, 0, sizeof(r));
+    r.info = uint32_t(c_deg[ni]) | (uint32_t(c_sbits[ni]) << 8);
+    for (int j = 0; j < c_deg[ni]; ++j) {
+      r.id[j] = c_edge[size_t(j) * nC + ni];
+      r.rat[j] = kite_of_slot[off + j] / d->cell_area[i];
+      r.l[j] = d->edge_len[d->cell_edges[off + j]];
+    }
+  }
+  std::vector<uint8_t> e_slots(nE);
+  for (int32_t ne = 0; ne < nE; ++ne) e_slots[ne] = slots[c->e_new2old[ne]];
+  cudaStream_t s = c->stream;
+  c->c_rows.upload(rows, s);
+  c->e_slots.upload(e_slots, s);
+  CK(cudaStreamSynchronize(s));
+  return true;
+}
+
 // Tiles of k_out_rw (kernels.cuh): runs of consecutive internal cells; a tile
 // owns the edges whose lower internal cell lies in it (a contiguous range,
 // edges being sorted by their cells).  C_req = tile cells + the far cells of
@@ -638,8 +675,6 @@ bool derive_ring_stencil(const mswm_mesh_desc* d, std::vector<double>& kite_of_s
 bool build_rw(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const std::vector<int32_t>& c_edge,
               const std::vector<uint8_t>& c_deg, const std::vector<uint8_t>& c_sbits,
               const std::vector<int2>& e_cells) {
-  if (const char* k = std::getenv("MSWM_KOUT"))
-    if (std::string(k) == "explicit") return false;
   if (c->deg_max > kFastDeg) return false;
   std::vector<double> kite_of_slot;
   std::vector<uint8_t> slots;
@@ -966,7 +1001,15 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
     for (int32_t v = 0; v < nV; ++v) v_af[v] = make_double2(v_area[v], 0.0);  // f_v: set_fields
     put(c->v_af, v_af);
   }
-  c->rw_ok = build_rw(c, d, c_edge, c_deg, c_sbits, e_cells);
+  {
+    // phase C kernel: k_out_cr (cell rows) by default, k_out_rw (cell tiles)
+    // or k_out (explicit tables) on request or when the stencil is not the
+    // ring walk
+    const char* k = std::getenv("MSWM_KOUT");
+    const std::string kout = k ? k : "";
+    if (kout == "ringtile") c->rw_ok = build_rw(c, d, c_edge, c_deg, c_sbits, e_cells);
+    else if (kout != "explicit") c->cr_ok = build_cr(c, d, c_edge, c_deg, c_sbits);
+  }
   put(c->c_edge, c_edge);
   put(c->c_vert, c_vert);
   put(c->c_nbr, c_nbr);
@@ -1340,6 +1383,21 @@ void launch_eval_once(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, cons
       CK(cudaGetLastError());
       ++c->launches;
     }
+  } else if (nout > 0 && c->cr_ok) {
+    OutArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.cs = p.sc_out.dev();
+    a.es = p.se_out.dev();
+    a.mask = p.mask;
+    a.ckey = c->have_regions ? c->ckey.p : nullptr;
+    a.ekey = c->have_regions ? c->ekey.p : nullptr;
+    a.cop[0] = cop[0];
+    a.cop[1] = cop[1];
+    a.eop[0] = eop[0];
+    a.eop[1] = eop[1];
+    k_out_cr<<<grid(nout, 2), kSBlock, 0, s>>>(M, Kp, FQ, c->c_rows.p, c->e_slots.p, a);
+    CK(cudaGetLastError());
+    ++c->launches;
   } else if (nout > 0) {
     OutArgs a;
     std::memset(&a, 0, sizeof(a));
@@ -1509,6 +1567,18 @@ PredArgs make_pred(mswm_cuda_ctx* c, int stage, int k, int M, double* hdst, doub
 
 using ArrSel = DArr<double> mswm_cuda_ctx::*;
 
+// MSWM_HALO_DRYRUN=1: timing aid for one rank of a partition stepped alone
+// on one GPU (scripts/rank_timing.py) -- exchanges pack and unpack but skip
+// the transfer; the receive buffers keep the halo values of the uploaded
+// state, so the (wrong) results stay physical.
+bool halo_dry_run() {
+  static const bool on = [] {
+    const char* e = std::getenv("MSWM_HALO_DRYRUN");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 Halo& halo_for(mswm_cuda_ctx* c, unsigned mask) {
   auto it = c->halo_mask.find(mask);
   return it == c->halo_mask.end() ? c->halo : it->second;
@@ -1533,11 +1603,7 @@ void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us, unsigned ma
       ++c->launches;
     }
   }
-  static const bool dry_run = [] {
-    const char* e = std::getenv("MSWM_HALO_DRYRUN");
-    return e && e[0] == '1';
-  }();
-  if (cs.size() == 1 && dry_run) {
+  if (cs.size() == 1 && halo_dry_run()) {
     // timing aid only (results are wrong): one rank of a partition stepped
     // alone on one GPU -- pack and unpack run, the transfer is skipped
   } else if (cs.size() == 1) {
@@ -2455,6 +2521,16 @@ int mswm_cuda_state_upload(mswm_cuda_ctx* c, const double* h, const double* u, d
     upload_field(c, c->H, h, c->c_new2old, c->nC);
     upload_field(c, c->U, u, c->e_new2old, c->nE);
     c->time = time;
+    if (halo_dry_run()) {
+      std::vector<Halo*> hs{&c->halo};
+      for (auto& kv : c->halo_mask) hs.push_back(&kv.second);
+      for (Halo* x : hs)
+        if (x->nr > 0) {
+          k_pack<<<nblk(x->nr), kBlock, 0, c->stream>>>(x->nr, x->rcode.p, c->H.p, c->U.p,
+                                                        x->rbuf.p);
+          CK(cudaGetLastError());
+        }
+    }
     CK(cudaStreamSynchronize(c->stream));
     return int(MSWM_OK);
   });
@@ -2555,7 +2631,7 @@ int mswm_cuda_eval_profile(mswm_cuda_ctx* c, float* eval_ms, int64_t* out_cells,
 
 int mswm_cuda_layout_info(const mswm_cuda_ctx* c, int* kernel_path, int* identity_order) {
   if (!c) return MSWM_E_USAGE;
-  if (kernel_path) *kernel_path = c->rw_ok ? 1 : 0;
+  if (kernel_path) *kernel_path = c->cr_ok ? 2 : (c->rw_ok ? 1 : 0);
   if (identity_order) *identity_order = c->identity ? 1 : 0;
   return MSWM_OK;
 }

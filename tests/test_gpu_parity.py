@@ -316,9 +316,10 @@ def test_stepper_drop_in_interface():
     assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
 
 
-@pytest.mark.parametrize("kout,env", [("ringtile", {}),
-                                      ("ringtile", {"MSWM_RW_CELLS": "16"}),
-                                      ("ringtile", {"MSWM_RW_STAGE_KB": "8"}),
+@pytest.mark.parametrize("kout,env", [("cellrow", {}),
+                                      ("ringtile", {"MSWM_KOUT": "ringtile"}),
+                                      ("ringtile", {"MSWM_KOUT": "ringtile", "MSWM_RW_CELLS": "16"}),
+                                      ("ringtile", {"MSWM_KOUT": "ringtile", "MSWM_RW_STAGE_KB": "8"}),
                                       ("explicit", {"MSWM_KOUT": "explicit", "MSWM_ST16": "1"}),
                                       ("explicit", {"MSWM_KOUT": "explicit", "MSWM_ST16": "0"})])
 def test_layouts_are_bitwise_equivalent(kout, env, monkeypatch):
@@ -465,7 +466,7 @@ def test_wide_interfaces_bitwise(width):
             assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref), (order, scheme)
 
 
-@pytest.mark.parametrize("kout", ["ringtile", "explicit"])
+@pytest.mark.parametrize("kout", ["cellrow", "ringtile", "explicit"])
 @pytest.mark.parametrize("fork", ["1", "0"])
 @pytest.mark.parametrize("order", ["regions", "hilbert"])
 def test_concurrent_coarse_step_bitwise(kout, fork, order, monkeypatch):
@@ -473,8 +474,8 @@ def test_concurrent_coarse_step_bitwise(kout, fork, order, monkeypatch):
     the substeps (default) and in sequence (MSWM_FORK=0): bitwise equal to
     the oracle over several coarse steps, M = 2 and 4."""
     monkeypatch.setenv("MSWM_FORK", fork)
-    if kout == "explicit":
-        monkeypatch.setenv("MSWM_KOUT", "explicit")
+    if kout != "cellrow":
+        monkeypatch.setenv("MSWM_KOUT", kout)
     wl = W.small_sphere(6, seed=41, cap_deg=25.0)
     o = _oracle_for(wl)
     ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order, fine_mask=wl.fine_mask)
