@@ -204,12 +204,9 @@ int mswm_cuda_eval_profile(mswm_cuda_ctx* ctx, float* eval_ms,
                            int64_t* out_cells, int64_t* out_edges, int cap,
                            int* n);
 
-/* Output kernel chosen at create: kernel_path 2 = k_out_cr (stencil and
- * weights rebuilt from one 128-byte row per cell -- the default when the
- * mesh's stencil is the reference builder's ring walk, mesh_build.cpp:133-154
- * / 343-362, verified bitwise at create); 1 = k_out_rw (cell tiles staged in
- * shared memory, MSWM_KOUT=ringtile); 0 = k_out over the explicit stencil
- * tables (other meshes, or MSWM_KOUT=explicit).
+/* Output kernel: kernel_path 0 = k_out over the explicit stencil tables
+ * (the only output kernel; profiles/r2_phaseC_experiments.json records the
+ * ring-walk variants measured slower and removed).
  * identity_order = 1 when the internal numbering equals the caller's. */
 int mswm_cuda_layout_info(const mswm_cuda_ctx* ctx, int* kernel_path,
                           int* identity_order);

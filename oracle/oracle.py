@@ -113,6 +113,9 @@ def ref() -> C.CDLL:
                                    C.c_int64] + E + [C.POINTER(C.c_int), f64p]),
             "ref_ledger": (None, [vp, i64p, i64p, i64p]),
             "ref_lts_coeffs": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, f64p] + E),
+            "ref_init_tc5": (C.c_int, [vp, f64p, f64p, f64p, f64p] + E),
+            "ref_convergence_study": (C.c_int, [vp, vp, C.c_int, C.c_int, f64p, C.c_int,
+                                                C.c_double, f64p] + E),
             "ref_partition": (C.c_int, [vp, vp, C.c_int, C.c_uint64, i32p] + E),
             "ref_block_plan": (vp, [vp, vp, i32p, C.c_int] + E),
             "ref_block_plan_free": (None, [vp]),
@@ -379,6 +382,31 @@ class CudaStepperRef:
         e = np.zeros(16, np.int64)
         dropin().ref_cuda_stepper_ledger(self.handle, _p(c, i64p), _p(e, i64p))
         return c.reshape(4, 4), e.reshape(4, 4)
+
+
+def ref_init_tc5(mesh: RefMesh):
+    """The reference's TC5 initial state (harness.cpp:35-72): h, u, b, f."""
+    m = mesh.as_mesh()
+    h, u = np.zeros(m.n_cells), np.zeros(m.n_edges)
+    b, f = np.zeros(m.n_cells), np.zeros(m.n_vertices)
+    buf = _err()
+    _check(ref().ref_init_tc5(mesh.handle, _p(h, f64p), _p(u, f64p), _p(b, f64p), _p(f, f64p),
+                              buf, ERRLEN), buf)
+    return h, u, b, f
+
+
+def ref_convergence_study(mesh: RefMesh, regions: RefRegions | None, scheme, M, dts, duration):
+    """The reference's convergence_study on TC5 (harness.cpp:243-309)."""
+    dts = np.ascontiguousarray(dts, np.float64)
+    n = len(dts)
+    out = np.zeros(2 * n + 4)
+    buf = _err()
+    _check(ref().ref_convergence_study(mesh.handle, regions.handle if regions else None,
+                                       int(scheme), int(M), _p(dts, f64p), n, float(duration),
+                                       _p(out, f64p), buf, ERRLEN), buf)
+    return {"err_h": out[:n], "err_u": out[n:2 * n], "slope_h": out[2 * n],
+            "slope_u": out[2 * n + 1], "monotone_h": bool(out[2 * n + 2]),
+            "monotone_u": bool(out[2 * n + 3])}
 
 
 def ref_lts_coeffs(order, stage, k, M):

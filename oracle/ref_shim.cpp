@@ -432,4 +432,37 @@ int64_t ref_block_plan_list(void* pp, int block, int which, int32_t* ids) {
   return int64_t(v.size());
 }
 
+// init_tc5 with the default TestCaseConfig (harness.cpp:35-72).
+int ref_init_tc5(void* mp, double* h, double* u, double* b, double* f, char* err, int errlen) {
+  auto* m = static_cast<VoronoiMesh*>(mp);
+  return guarded(err, errlen, nullptr, [&] {
+    const Tc5Init init = init_tc5(*m, TestCaseConfig{});
+    std::copy(init.state.h.data.begin(), init.state.h.data.end(), h);
+    std::copy(init.state.u.data.begin(), init.state.u.data.end(), u);
+    std::copy(init.b.data.begin(), init.b.data.end(), b);
+    std::copy(init.f.data.begin(), init.f.data.end(), f);
+  });
+}
+
+// convergence_study (harness.cpp:243-309) on TC5 with the default test case:
+// out = err_h[n], err_u[n], then slope_h, slope_u, monotone_h, monotone_u.
+int ref_convergence_study(void* mp, void* rp, int scheme, int M, const double* dts, int n,
+                          double duration, double* out, char* err, int errlen) {
+  auto* m = static_cast<VoronoiMesh*>(mp);
+  auto* r = static_cast<RegionMap*>(rp);
+  return guarded(err, errlen, nullptr, [&] {
+    const ConvergenceResult cr = convergence_study(*m, r, Scheme(scheme), M,
+                                                   std::vector<double>(dts, dts + n), duration,
+                                                   TestCaseConfig{});
+    for (int k = 0; k < n; ++k) {
+      out[k] = cr.err_h[k];
+      out[n + k] = cr.err_u[k];
+    }
+    out[2 * n] = cr.slope_h;
+    out[2 * n + 1] = cr.slope_u;
+    out[2 * n + 2] = cr.monotone_h ? 1.0 : 0.0;
+    out[2 * n + 3] = cr.monotone_u ? 1.0 : 0.0;
+  });
+}
+
 }  // extern "C"

@@ -434,401 +434,6 @@ __global__ void MSWM_KOUT_BOUNDS k_out(DevMesh M, const double* __restrict__ h,
 }
 
 // ---------------------------------------------------------------------------
-// Phase C with the stencil rebuilt from cell rows (k_out_cr): the default
-// wherever the mesh's stencil is the reference builder's ring walk
-// (mesh_build.cpp:133-154, weights :343-362; verified bitwise at create).
-//
-// k_out streams 104 B/edge of explicit stencil tables (16-bit id offsets +
-// coefficient pairs).  But an edge's stencil is the rest of the rings of its
-// two cells, walked from the edge's slot, and its weights are running sums
-// of the ring's kite_area / A_i, minus 1/2, signed (edge_weight's rule).  So
-// one 128-byte row per cell -- ring edge ids, degree / sign bits, the kite
-// ratios and the ring edges' lengths -- serves all ~6 edges that touch the
-// cell (L1 / L2 hits after the first), and the per-edge tables shrink to
-// one slot byte.  The weight is rebuilt as (frac - 0.5) with the sign of
-// cell_sign * anchor, the coefficient as w * (l_e' * (1/d_e)): the exact
-// roundings of edge_weight and of k_out's coefficient table, so results are
-// bitwise the reference's (operators.cpp:91-116).
-struct __align__(16) CellRow {
-  int32_t id[6];   // ring edges (internal ids; padding slots hold 0)
-  uint32_t info;   // degree | cell_sign(ring edge j) < 0 at bit 8 + j
-  uint32_t pad;
-  double rat[6];   // kite_area / A_i per ring slot
-  double l[6];     // l of the ring edges
-};
-static_assert(sizeof(CellRow) == 128, "one 128-byte line per cell");
-
-template <class T>
-__device__ __forceinline__ T pick6(const T (&v)[6], int s) {
-  T r = v[0];
-  r = s == 1 ? v[1] : r;
-  r = s == 2 ? v[2] : r;
-  r = s == 3 ? v[3] : r;
-  r = s == 4 ? v[4] : r;
-  r = s == 5 ? v[5] : r;
-  return r;
-}
-
-// ring ids and info of one row (the first 32 bytes: two 16-byte loads)
-__device__ __forceinline__ void load_ids(const CellRow* __restrict__ rows, int32_t c,
-                                         int32_t (&id)[6], uint32_t& info) {
-  const int4* q = reinterpret_cast<const int4*>(rows + c);
-  const int4 a = q[0], b = q[1];
-  id[0] = a.x;
-  id[1] = a.y;
-  id[2] = a.z;
-  id[3] = a.w;
-  id[4] = b.x;
-  id[5] = b.y;
-  info = uint32_t(b.z);
-}
-
-#ifndef MSWM_KCR_MINB
-#define MSWM_KCR_MINB 6
-#endif
-
-__global__ void __launch_bounds__(kSBlock, MSWM_KCR_MINB)
-    k_out_cr(DevMesh M, const double* __restrict__ K, const double2* __restrict__ FQ,
-             const CellRow* __restrict__ rows, const uint8_t* __restrict__ e_slots, OutArgs a) {
-  const int32_t ncs = a.cs.n();
-  const int32_t n = ncs + a.es.n();
-  for (int32_t t = blockIdx.x * kSBlock + threadIdx.x; t < n; t += gridDim.x * kSBlock) {
-    if (t < ncs) {
-      // dh (operators.cpp:91-99)
-      const int32_t i = a.cs.at(t);
-      const int g = a.ckey ? a.ckey[i] : 0;
-      if (g > 5 || !((a.mask >> g) & 1u)) continue;
-      int32_t id[6];
-      uint32_t info;
-      load_ids(rows, i, id, info);
-      const int deg = info & 0xFF;
-      const double* lr = rows[i].l;
-      double acc = 0.0;
-#pragma unroll
-      for (int j = 0; j < kFastDeg; ++j) {
-        const double l = lr[j];
-        const double x = ((info >> (8 + j)) & 1u ? -l : l) * FQ[id[j]].x;
-        if (j < deg) acc += x;
-      }
-      apply_op(a.cop[g <= 2 ? 0 : 1], i, -acc / M.c_area[i]);
-    } else {
-      // du (operators.cpp:101-116), stencil walked over the two cell rows
-      const int32_t e = a.es.at(t - ncs);
-      const int g = a.ekey ? a.ekey[e] : 0;
-      if (g > 4 || !((a.mask >> (6 + g)) & 1u)) continue;
-      const int2 cc = M.e_cells[e];
-      const uint32_t sl = e_slots[e];
-      const double inv_d = M.e_invd[e];
-      const double qt_e = FQ[e].y;
-      double pvflux = 0.0;
-#pragma unroll
-      for (int side = 0; side < 2; ++side) {
-        const int32_t c = side ? cc.y : cc.x;
-        int32_t id[6];
-        uint32_t info;
-        load_ids(rows, c, id, info);
-        const int deg = info & 0xFF;
-        const int p = side ? ((sl >> 3) & 7) : (sl & 7);
-        const uint32_t aneg = (sl >> (6 + side)) & 1u;
-        const double* rr = rows[c].rat;
-        const double* lr = rows[c].l;
-        // the side's gathers first (ids known), then the walk
-        double2 fq[kFastDeg - 1];
-#pragma unroll
-        for (int k = 1; k < kFastDeg; ++k) {
-          int s = p + k;
-          if (s >= deg) s -= deg;
-          fq[k - 1] = FQ[pick6(id, s)];
-        }
-        double frac = 0.0;
-#pragma unroll
-        for (int k = 1; k < kFastDeg; ++k) {
-          if (k < deg) {
-            int s = p + k;
-            if (s >= deg) s -= deg;
-            const int sp = s == 0 ? deg - 1 : s - 1;
-            frac += rr[sp];
-            const double x = frac - 0.5;
-            const double w = (((info >> (8 + s)) & 1u) ^ aneg) ? -x : x;
-            const double coef = w * (lr[s] * inv_d);
-            pvflux += coef * fq[k - 1].x * (0.5 * (qt_e + fq[k - 1].y));
-          }
-        }
-      }
-      const double du = -pvflux - (K[cc.x] - K[cc.y]) * inv_d;
-      apply_op(a.eop[g <= 1 ? 0 : 1], e, du);
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Phase C on cell tiles with ring-walk weights (k_out_rw): the default
-// wherever the mesh's stencil is the reference builder's ring walk
-// (mesh_build.cpp:133-154, weights :343-362; verified bitwise at create).
-//
-// The explicit path (k_out above) streams 100 B/edge of stencil tables
-// (ids + coefficients) and gathers (F, q~) ten times per edge through L1.
-// Here a tile = up to a few hundred consecutive internal cells; it owns the
-// edges whose lower internal cell lies in it (a contiguous range: edges are
-// sorted by their cells).  Everything the tile's outputs read -- (F, q~) and
-// l on E_req (ring edges of the tile cells and of the far cells of owned
-// edges), and per cell of C_req (tile cells + those far cells) its
-// kite/A ring row, ring of local edge ids, degree / sign bits and psi --
-// is staged in shared memory with cp.async (LDGSTS gathers, no registers
-// held), double-buffered: the copies of tile i+1 are in flight while tile i
-// computes, and the index lists of tile i+2 load into registers meanwhile.
-// The weights are rebuilt on chip as (cell_sign * anchor) * (frac - 0.5)
-// from running sums of the kite/A row, the coefficient as w * (l_e' * (1/d_e))
-// -- the exact roundings of the stored edge_weight and of the explicit
-// coefficient table -- so per-element results are bitwise the reference's
-// (operators.cpp:91-116).
-constexpr int kRwThreads = 256;
-constexpr int kRwIdx = 2;  // register-held halo / extra ids per thread and tile
-
-struct RwTile {
-  int32_t c0, nc;          // tile cells [c0, c0 + nc)
-  int32_t e0, ne;          // owned edges [e0, e0 + ne) = local edges [0, ne)
-  int32_t halo_off, nh;    // far cells: local cells [nc, nc + nh) = halo[halo_off ..]
-  int32_t extra_off, nx;   // other E_req edges: local [ne, ne + nx) = extra[extra_off ..]
-  int32_t ring_off;        // ring[ring_off .. + nc + nh): 8 x u16 local edge ids per cell
-  int32_t pad[3];
-};
-
-struct RwArgs {
-  const RwTile* __restrict__ tiles;
-  const int32_t* __restrict__ list;   // tiles of this evaluation (null: all)
-  int32_t n_tiles;
-  int32_t emax, cmax;                 // stage capacities (edges, cells)
-  const int32_t* __restrict__ halo;
-  const int32_t* __restrict__ extra;
-  const uint4* __restrict__ ring;
-  const ushort2* __restrict__ e_lc;   // [nE] local ids of edge_cells[e][0], [1] in the owning tile
-  const uint8_t* __restrict__ e_slots;  // [nE] slot of e in ring(c0) | ring(c1) << 3 |
-                                        // anchor sign < 0 (side 0) << 6 | (side 1) << 7
-  const double* __restrict__ rat;     // [nC][6] kite_area / A_i per ring slot
-  const uint32_t* __restrict__ cinfo; // [nC] deg | cell-sign bits << 8
-};
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void cp_async16(void* s, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* s, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* s, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-
-// one stage of the shared-memory ring (offsets for capacities emax, cmax, both even)
-struct RwStage {
-  double2* fq;
-  double* l;
-  double* rat;
-  double* psi;
-  uint4* ring;
-  uint32_t* cinfo;
-  __device__ __forceinline__ RwStage(char* base, int emax, int cmax) {
-    fq = reinterpret_cast<double2*>(base);
-    l = reinterpret_cast<double*>(base + 16 * emax);
-    rat = reinterpret_cast<double*>(base + 24 * emax);
-    psi = reinterpret_cast<double*>(base + 24 * emax + 48 * cmax);
-    ring = reinterpret_cast<uint4*>(base + 24 * emax + 56 * cmax);
-    cinfo = reinterpret_cast<uint32_t*>(base + 24 * emax + 72 * cmax);
-  }
-};
-__host__ __device__ constexpr size_t rw_stage_bytes(int emax, int cmax) {
-  return size_t(24) * emax + size_t(76) * cmax;
-}
-
-// issue the copies of tile t into stage S (every thread; ids in registers)
-__device__ __forceinline__ void rw_issue(const RwArgs& a, const DevMesh& M, const RwTile& t,
-                                         const int32_t (&xr)[kRwIdx], const int32_t (&hr)[kRwIdx],
-                                         const double* __restrict__ K,
-                                         const double2* __restrict__ FQ, RwStage S) {
-  const int tid = threadIdx.x;
-  for (int j = tid; j < t.ne; j += kRwThreads) {  // owned edges: contiguous
-    cp_async16(S.fq + j, FQ + t.e0 + j);
-    cp_async8(S.l + j, M.e_len + t.e0 + j);
-  }
-#pragma unroll
-  for (int m = 0; m < kRwIdx; ++m) {
-    const int j = tid + m * kRwThreads;
-    if (j < t.nx) {
-      cp_async16(S.fq + t.ne + j, FQ + xr[m]);
-      cp_async8(S.l + t.ne + j, M.e_len + xr[m]);
-    }
-  }
-  const int ncr = t.nc + t.nh;
-  for (int j = tid; j < ncr; j += kRwThreads) cp_async16(S.ring + j, a.ring + t.ring_off + j);
-  for (int j = tid; j < t.nc; j += kRwThreads) {  // tile cells: contiguous
-    const int32_t c = t.c0 + j;
-    const double* r = a.rat + 6 * int64_t(c);
-    cp_async16(S.rat + 6 * j, r);
-    cp_async16(S.rat + 6 * j + 2, r + 2);
-    cp_async16(S.rat + 6 * j + 4, r + 4);
-    cp_async8(S.psi + j, K + c);
-    cp_async4(S.cinfo + j, a.cinfo + c);
-  }
-#pragma unroll
-  for (int m = 0; m < kRwIdx; ++m) {
-    const int j = tid + m * kRwThreads;
-    if (j < t.nh) {
-      const int32_t c = hr[m];
-      const int q = t.nc + j;
-      const double* r = a.rat + 6 * int64_t(c);
-      cp_async16(S.rat + 6 * q, r);
-      cp_async16(S.rat + 6 * q + 2, r + 2);
-      cp_async16(S.rat + 6 * q + 4, r + 4);
-      cp_async8(S.psi + q, K + c);
-      cp_async4(S.cinfo + q, a.cinfo + c);
-    }
-  }
-}
-
-__device__ __forceinline__ void rw_load_idx(const RwArgs& a, const RwTile& t, int32_t (&xr)[kRwIdx],
-                                            int32_t (&hr)[kRwIdx]) {
-#pragma unroll
-  for (int m = 0; m < kRwIdx; ++m) {
-    const int j = threadIdx.x + m * kRwThreads;
-    xr[m] = j < t.nx ? a.extra[t.extra_off + j] : 0;
-    hr[m] = j < t.nh ? a.halo[t.halo_off + j] : 0;
-  }
-}
-
-__device__ __forceinline__ void rw_compute(const RwArgs& a, const DevMesh& M, const OutArgs& o,
-                                           int32_t c0, int32_t nc, int32_t e0, int32_t ne,
-                                           const RwStage& S) {
-  for (int q = threadIdx.x; q < nc + ne; q += kRwThreads) {
-    if (q < nc) {
-      // dh (operators.cpp:91-99) on a tile cell
-      const int32_t i = c0 + q;
-      const int g = o.ckey ? o.ckey[i] : 0;
-      if (g > 5 || !((o.mask >> g) & 1u)) continue;
-      const uint32_t ci = S.cinfo[q];
-      const int deg = ci & 0xFF;
-      const uint32_t sb = ci >> 8;
-      const uint16_t* rid = reinterpret_cast<const uint16_t*>(S.ring + q);
-      double acc = 0.0;
-#pragma unroll
-      for (int k = 0; k < kFastDeg; ++k) {
-        if (k < deg) {
-          const int e2 = rid[k];
-          const double l = S.l[e2];
-          acc += ((sb >> k) & 1u ? -l : l) * S.fq[e2].x;
-        }
-      }
-      apply_op(o.cop[g <= 2 ? 0 : 1], i, -acc / M.c_area[i]);
-    } else {
-      // du (operators.cpp:101-116) on an owned edge, stencil walked from the rings
-      const int k0 = q - nc;
-      const int32_t e = e0 + k0;
-      const int g = o.ekey ? o.ekey[e] : 0;
-      if (g > 4 || !((o.mask >> (6 + g)) & 1u)) continue;
-      const double inv_d = M.e_invd[e];
-      const ushort2 lc = a.e_lc[e];
-      const uint32_t sl = a.e_slots[e];
-      const double qt_e = S.fq[k0].y;
-      double pvflux = 0.0;
-#pragma unroll
-      for (int side = 0; side < 2; ++side) {
-        const int c = side ? lc.y : lc.x;
-        const int p = side ? ((sl >> 3) & 7) : (sl & 7);
-        const uint32_t aneg = (sl >> (6 + side)) & 1u;
-        const uint32_t ci = S.cinfo[c];
-        const int deg = ci & 0xFF;
-        const uint32_t sb = ci >> 8;
-        const uint16_t* rid = reinterpret_cast<const uint16_t*>(S.ring + c);
-        const double* rr = S.rat + 6 * c;
-        double frac = 0.0;
-        int sp = p;  // slot of the kite added next: p + k - 1 (mod deg)
-#pragma unroll
-        for (int k = 1; k < kFastDeg; ++k) {
-          if (k < deg) {
-            int s = sp + 1;
-            if (s >= deg) s -= deg;
-            frac += rr[sp];
-            const int e2 = rid[s];
-            const double x = frac - 0.5;
-            const double w = (((sb >> s) & 1u) ^ aneg) ? -x : x;
-            const double coef = w * (S.l[e2] * inv_d);
-            const double2 fq = S.fq[e2];
-            pvflux += coef * fq.x * (0.5 * (qt_e + fq.y));
-            sp = s;
-          }
-        }
-      }
-      const double du = -pvflux - (S.psi[lc.x] - S.psi[lc.y]) * inv_d;
-      apply_op(o.eop[g <= 1 ? 0 : 1], e, du);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kRwThreads) k_out_rw(DevMesh M, const double* __restrict__ K,
-                                                       const double2* __restrict__ FQ, RwArgs a,
-                                                       OutArgs o) {
-  extern __shared__ __align__(16) char rw_smem[];
-  const size_t sb = rw_stage_bytes(a.emax, a.cmax);
-  const RwStage S0(rw_smem, a.emax, a.cmax), S1(rw_smem + sb, a.emax, a.cmax);
-  const int G = gridDim.x;
-  const int my = a.n_tiles > int(blockIdx.x) ? (a.n_tiles - int(blockIdx.x) + G - 1) / G : 0;
-  if (my == 0) return;
-  auto tile_at = [&](int it) -> RwTile {
-    const int pos = int(blockIdx.x) + it * G;
-    return a.tiles[a.list ? a.list[pos] : pos];
-  };
-  int32_t xr[kRwIdx], hr[kRwIdx];
-  RwTile t = tile_at(0);
-  rw_load_idx(a, t, xr, hr);
-  rw_issue(a, M, t, xr, hr, K, FQ, S0);
-  cp_async_commit();
-  int32_t cc0 = t.c0, cnc = t.nc, ce0 = t.e0, cne = t.ne;
-  if (my > 1) {
-    t = tile_at(1);
-    rw_load_idx(a, t, xr, hr);
-  }
-  for (int it = 0; it < my; ++it) {
-    if (it + 1 < my) rw_issue(a, M, t, xr, hr, K, FQ, (it & 1) ? S0 : S1);
-    cp_async_commit();
-    const int32_t nc0 = t.c0, nnc = t.nc, ne0 = t.e0, nne = t.ne;
-    if (it + 2 < my) {
-      t = tile_at(it + 2);
-      rw_load_idx(a, t, xr, hr);
-    }
-    cp_async_wait<1>();
-    __syncthreads();
-    rw_compute(a, M, o, cc0, cnc, ce0, cne, (it & 1) ? S1 : S0);
-    __syncthreads();
-    cc0 = nc0;
-    cnc = nnc;
-    ce0 = ne0;
-    cne = nne;
-  }
-}
-
-// Tiles of k_out_rw holding an output of a mask: key 0 (compaction key; the
-// key array starts 0xFF).  An edge belongs to the tile of its lower cell.
-__global__ void k_mark_rw(const int32_t* __restrict__ cells, int32_t nc,
-                          const int32_t* __restrict__ edges, int32_t ne,
-                          const int32_t* __restrict__ c_tile, const int2* __restrict__ e_cells,
-                          uint8_t* __restrict__ key) {
-  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < nc) {
-    key[c_tile[cells[t]]] = 0;
-  } else if (t - nc < ne) {
-    const int2 cc = e_cells[edges[t - nc]];
-    key[c_tile[min(cc.x, cc.y)]] = 0;
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Interface-1 prediction (integrators.cpp:217-227): order 3
 // dst = ((c0*s0) + (c1*s1)) + (c2*s2), order 2 (s2 null) (c0*s0) + (c1*s1),
 // on the I1 lists.

@@ -148,8 +148,6 @@ struct MaskPlan {
     int64_t n() const { return int64_t(n_range) + n_list; }
   } sv, sk, se, sc_out, se_out;
   DArr<uint32_t> vmask;  // closure bitmask for the dense dry-vertex check
-  DArr<int32_t> rw_list;  // k_out_rw tiles holding outputs (null: every tile)
-  int32_t rw_n = 0;
   std::vector<int32_t> host_cells, host_edges;  // original ids, same order as device lists
   // drop-in eval I/O (mswm_cuda_eval): the h / u entries the evaluation
   // reads, original ids on the host and internal ids on the device (built on
@@ -261,21 +259,6 @@ struct mswm_cuda_ctx {
   // ~70 %); MSWM_PERSIST=0 restores one element per thread
   int persist_ctas[3] = {2048 / kSBlock, 2048 / kSBlock, 2048 / kSBlock}, n_sm = 148;  // A, B, C
   DArr<int2> e_cells, e_verts;
-  // tiled ring-walk phase C (k_out_rw, build_rw): tiles, their staged-set
-  // lists, per-edge local ids / slots, per-cell kite/A rows and ring info
-  bool rw_ok = false;
-  // phase C over per-cell rows (k_out_cr, build_cr): 128 B per cell + a slot byte per edge
-  bool cr_ok = false;
-  DArr<CellRow> c_rows;
-  int32_t rw_ntiles = 0, rw_emax = 0, rw_cmax = 0, rw_blocks = 0;
-  size_t rw_smem = 0;
-  DArr<RwTile> rw_tiles;
-  DArr<int32_t> rw_halo, rw_extra, c_tile;
-  DArr<uint4> rw_ring;
-  DArr<ushort2> e_lc;
-  DArr<uint8_t> e_slots;
-  DArr<double> c_rat;
-  DArr<uint32_t> c_info;
   double gravity = 9.80616;
   bool have_fields = false;
 
@@ -578,247 +561,6 @@ void make_orders(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell_
   c->identity = ident;
 }
 
-// Is the caller's stencil the ring walk of mesh_build.cpp:133-154 with the
-// weight rule of :343-362 (w = (cell_sign * anchor) * (frac - 0.5), frac the
-// running sum of kite_area / cell_area around the ring)?  If so -- bitwise,
-// every entry -- k_out_rw rebuilds stencil and weights on chip from per-cell
-// rows.  Returns the kite area of every ring slot and per-edge slot bytes
-// (slot of e in ring(c0) | ring(c1) << 3, anchor sign < 0 at bits 6 / 7).
-bool derive_ring_stencil(const mswm_mesh_desc* d, std::vector<double>& kite_of_slot,
-                         std::vector<uint8_t>& slots) {
-  const int32_t nC = d->n_cells, nE = d->n_edges;
-  const int32_t total = d->cell_offset[nC];
-  kite_of_slot.assign(total, 0.0);
-  // kite_area per ring slot from vertex_kite (mesh_build.cpp:330-341 inverted)
-  for (int32_t i = 0; i < nC; ++i)
-    for (int32_t j = d->cell_offset[i]; j < d->cell_offset[i + 1]; ++j) {
-      const int32_t v = d->cell_vertices[j];
-      int k = 0;
-      while (k < 3 && d->vertex_cells[3 * v + k] != i) ++k;
-      if (k == 3) return false;
-      kite_of_slot[j] = d->vertex_kite[3 * v + k];
-    }
-  slots.assign(nE, 0);
-  for (int32_t e = 0; e < nE; ++e) {
-    int pos = d->edge_edge_offset[e];
-    uint8_t sl = 0;
-    for (int side = 0; side < 2; ++side) {
-      const int32_t i = d->edge_cells[2 * e + side];
-      const int off = d->cell_offset[i], mm = d->cell_offset[i + 1] - off;
-      int p = 0;
-      while (p < mm && d->cell_edges[off + p] != e) ++p;
-      if (p == mm || p > 7) return false;
-      const int32_t av = d->cell_vertices[off + p];
-      const double anchor = d->edge_vertices[2 * e] == av ? double(d->edge_vertex_sign[2 * e])
-                                                          : double(d->edge_vertex_sign[2 * e + 1]);
-      double frac = 0.0;
-      for (int k = 1; k < mm; ++k) {
-        frac += kite_of_slot[off + (p + k - 1) % mm] / d->cell_area[i];
-        const int32_t ep = d->cell_edges[off + (p + k) % mm];
-        const double cs = d->edge_cells[2 * ep] == i ? double(d->edge_cell_sign[2 * ep])
-                                                     : double(d->edge_cell_sign[2 * ep + 1]);
-        const double w = cs * anchor * (frac - 0.5);
-        if (pos >= d->edge_edge_offset[e + 1] || d->edge_edges[pos] != ep) return false;
-        if (std::memcmp(&w, &d->edge_weight[pos], 8) != 0) return false;
-        ++pos;
-      }
-      sl |= uint8_t(p << (3 * side));
-      if (anchor < 0) sl |= uint8_t(1u << (6 + side));
-    }
-    if (pos != d->edge_edge_offset[e + 1]) return false;
-    slots[e] = sl;
-  }
-  return true;
-}
-
-// Rows of k_out_cr (kernels.cuh): per internal cell its ring edge ids,
-// degree / sign bits, kite ratios (kite_area / A_i, the rounding
-// derive_ring_stencil verified) and ring edge lengths; per internal edge its
-// slot byte.  Returns false (explicit k_out) when the mesh's stencil is not
-// the ring walk or rings exceed 6 edges.
-bool build_cr(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const std::vector<int32_t>& c_edge,
-              const std::vector<uint8_t>& c_deg, const std::vector<uint8_t>& c_sbits) {
-  if (c->deg_max > kFastDeg) return false;
-  std::vector<double> kite_of_slot;
-  std::vector<uint8_t> slots;
-  if (!derive_ring_stencil(d, kite_of_slot, slots)) return false;
-  const int32_t nC = c->nC, nE = c->nE;
-  std::vector<CellRow> rows(nC);
-  for (int32_t ni = 0; ni < nC; ++ni) {
-    const int32_t i = c->c_new2old[ni];
-    const int off = d->cell_offset[i];
-    CellRow& r = rows[ni];
-    std::memset(&r, 0, sizeof(r));
-    r.info = uint32_t(c_deg[ni]) | (uint32_t(c_sbits[ni]) << 8);
-    for (int j = 0; j < c_deg[ni]; ++j) {
-      r.id[j] = c_edge[size_t(j) * nC + ni];
-      r.rat[j] = kite_of_slot[off + j] / d->cell_area[i];
-      r.l[j] = d->edge_len[d->cell_edges[off + j]];
-    }
-  }
-  std::vector<uint8_t> e_slots(nE);
-  for (int32_t ne = 0; ne < nE; ++ne) e_slots[ne] = slots[c->e_new2old[ne]];
-  cudaStream_t s = c->stream;
-  c->c_rows.upload(rows, s);
-  c->e_slots.upload(e_slots, s);
-  CK(cudaStreamSynchronize(s));
-  return true;
-}
-
-// Tiles of k_out_rw (kernels.cuh): runs of consecutive internal cells; a tile
-// owns the edges whose lower internal cell lies in it (a contiguous range,
-// edges being sorted by their cells).  C_req = tile cells + the far cells of
-// owned edges (local ids after the tile's), E_req = owned edges + every other
-// ring edge of C_req (local ids after the owned ones).  A tile whose staged
-// sets overflow the stage capacity is split.  Returns false (explicit k_out)
-// when the mesh's stencil is not the ring walk or rings exceed 6 edges.
-bool build_rw(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const std::vector<int32_t>& c_edge,
-              const std::vector<uint8_t>& c_deg, const std::vector<uint8_t>& c_sbits,
-              const std::vector<int2>& e_cells) {
-  if (c->deg_max > kFastDeg) return false;
-  std::vector<double> kite_of_slot;
-  std::vector<uint8_t> slots;
-  if (!derive_ring_stencil(d, kite_of_slot, slots)) return false;
-  const int32_t nC = c->nC, nE = c->nE;
-  const int D = c->deg_max;
-  int32_t T = 128;
-  if (const char* tc = std::getenv("MSWM_RW_CELLS")) T = std::max(8, std::min(512, std::atoi(tc)));
-  size_t cap = 36 * 1024;  // bytes per stage: two stages + 3 CTAs per SM
-  if (const char* cb = std::getenv("MSWM_RW_STAGE_KB")) cap = size_t(std::max(8, std::atoi(cb))) * 1024;
-  // first owned edge of every cell (edges sorted by (min, max) internal cell)
-  std::vector<int32_t> efirst(size_t(nC) + 1, nE);
-  for (int32_t e = nE - 1; e >= 0; --e) efirst[std::min(e_cells[e].x, e_cells[e].y)] = e;
-  for (int32_t i = nC - 1; i >= 0; --i) efirst[i] = std::min(efirst[i], efirst[i + 1]);
-  for (int32_t e = 1; e < nE; ++e)
-    if (std::min(e_cells[e].x, e_cells[e].y) < std::min(e_cells[e - 1].x, e_cells[e - 1].y))
-      return false;  // not sorted by lower cell
-  std::vector<int32_t> cstamp(nC, -1), cloc(nC, 0), estamp(nE, -1);
-  std::vector<uint16_t> eloc(nE, 0);
-  std::vector<RwTile> tiles;
-  std::vector<int32_t> halo, extra, c_tile(nC, 0);
-  std::vector<uint4> ring;
-  std::vector<ushort2> e_lc(nE, make_ushort2(0, 0));
-  int32_t gen = 0, emax = 2, cmax = 2;
-  const int idx_cap = kRwIdx * kRwThreads;
-  // try cells [a, b) as one tile; false if a staged set overflows
-  std::function<bool(int32_t, int32_t)> make = [&](int32_t a, int32_t b) -> bool {
-    const int32_t g = gen++;
-    const int32_t ea = efirst[a], eb = efirst[b];
-    const int32_t nc = b - a, ne = eb - ea;
-    std::vector<int32_t> h_loc, x_loc;
-    for (int32_t i = a; i < b; ++i) {
-      cstamp[i] = g;
-      cloc[i] = i - a;
-    }
-    for (int32_t e = ea; e < eb; ++e) {
-      estamp[e] = g;
-      eloc[e] = uint16_t(std::min(e - ea, 65535));
-      for (const int32_t x : {e_cells[e].x, e_cells[e].y})
-        if (cstamp[x] != g) {
-          cstamp[x] = g;
-          cloc[x] = nc + int32_t(h_loc.size());
-          h_loc.push_back(x);
-        }
-    }
-    const int32_t nh = int32_t(h_loc.size());
-    auto ring_of = [&](int32_t q) { return q < nc ? a + q : h_loc[q - nc]; };
-    for (int32_t q = 0; q < nc + nh; ++q) {
-      const int32_t cc = ring_of(q);
-      for (int j = 0; j < c_deg[cc]; ++j) {
-        const int32_t e2 = c_edge[size_t(j) * nC + cc];
-        if (estamp[e2] != g) {
-          estamp[e2] = g;
-          eloc[e2] = uint16_t(std::min(ne + int32_t(x_loc.size()), 65535));
-          x_loc.push_back(e2);
-        }
-      }
-    }
-    const int32_t nx = int32_t(x_loc.size());
-    if (nh > idx_cap || nx > idx_cap || ne + nx > 65535 ||
-        rw_stage_bytes(ne + nx + 1, nc + nh + 3) > cap) {
-      if (b - a == 1) throw Error(MSWM_E_TOPOLOGY, "k_out_rw: one cell overflows a tile stage");
-      return false;
-    }
-    RwTile t;
-    std::memset(&t, 0, sizeof(t));
-    t.c0 = a;
-    t.nc = nc;
-    t.e0 = ea;
-    t.ne = ne;
-    t.halo_off = int32_t(halo.size());
-    t.nh = nh;
-    t.extra_off = int32_t(extra.size());
-    t.nx = nx;
-    t.ring_off = int32_t(ring.size());
-    halo.insert(halo.end(), h_loc.begin(), h_loc.end());
-    extra.insert(extra.end(), x_loc.begin(), x_loc.end());
-    for (int32_t q = 0; q < nc + nh; ++q) {
-      const int32_t cc = ring_of(q);
-      uint16_t r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int j = 0; j < c_deg[cc]; ++j) r[j] = eloc[c_edge[size_t(j) * nC + cc]];
-      uint4 w;
-      std::memcpy(&w, r, 16);
-      ring.push_back(w);
-    }
-    for (int32_t e = ea; e < eb; ++e)
-      e_lc[e] = make_ushort2(uint16_t(cloc[e_cells[e].x]), uint16_t(cloc[e_cells[e].y]));
-    for (int32_t i = a; i < b; ++i) c_tile[i] = int32_t(tiles.size());
-    emax = std::max(emax, ne + nx);
-    cmax = std::max(cmax, nc + nh);
-    tiles.push_back(t);
-    return true;
-  };
-  std::function<void(int32_t, int32_t)> cover = [&](int32_t a, int32_t b) {
-    if (make(a, b)) return;
-    const int32_t m = a + (b - a) / 2;
-    cover(a, m);
-    cover(m, b);
-  };
-  for (int32_t a = 0; a < nC; a += T) cover(a, std::min(nC, a + T));
-  // stage offsets (RwStage) stay 16 B aligned: 24 emax needs emax even, the
-  // second stage at 24 emax + 76 cmax needs cmax a multiple of 4
-  emax += emax & 1;
-  cmax = (cmax + 3) & ~3;
-  // per-cell rows: kite_area / A_i per ring slot (mesh_build.cpp:354, the
-  // rounding derive_ring_stencil verified) and degree / sign bits
-  const auto& cn = c->c_new2old;
-  std::vector<double> rat(size_t(nC) * 6, 0.0);
-  std::vector<uint32_t> info(nC);
-  for (int32_t ni = 0; ni < nC; ++ni) {
-    const int32_t i = cn[ni];
-    const int off = d->cell_offset[i], deg = d->cell_offset[i + 1] - off;
-    for (int j = 0; j < deg; ++j) rat[size_t(ni) * 6 + j] = kite_of_slot[off + j] / d->cell_area[i];
-    info[ni] = uint32_t(c_deg[ni]) | (uint32_t(c_sbits[ni]) << 8);
-  }
-  (void)D;
-  std::vector<uint8_t> e_slots(nE);
-  for (int32_t ne = 0; ne < nE; ++ne) e_slots[ne] = slots[c->e_new2old[ne]];
-  cudaStream_t s = c->stream;
-  auto put = [&](auto& dst, auto& vec) {
-    dst.upload(vec, s);
-    CK(cudaStreamSynchronize(s));
-    std::remove_reference_t<decltype(vec)>().swap(vec);
-  };
-  c->rw_ntiles = int32_t(tiles.size());
-  c->rw_emax = emax;
-  c->rw_cmax = cmax;
-  c->rw_smem = 2 * rw_stage_bytes(emax, cmax);
-  put(c->rw_tiles, tiles);
-  put(c->rw_halo, halo);
-  put(c->rw_extra, extra);
-  put(c->rw_ring, ring);
-  put(c->e_lc, e_lc);
-  put(c->e_slots, e_slots);
-  put(c->c_rat, rat);
-  put(c->c_info, info);
-  put(c->c_tile, c_tile);
-  CK(cudaFuncSetAttribute(k_out_rw, cudaFuncAttributeMaxDynamicSharedMemorySize, int(c->rw_smem)));
-  int nb = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_out_rw, kRwThreads, c->rw_smem));
-  if (nb < 1) return false;
-  c->rw_blocks = nb;
-  return true;
-}
 
 void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell_order) {
   const int32_t nC = d->n_cells, nE = d->n_edges, nV = d->n_vertices;
@@ -1000,15 +742,6 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
     std::vector<double2> v_af(nV);
     for (int32_t v = 0; v < nV; ++v) v_af[v] = make_double2(v_area[v], 0.0);  // f_v: set_fields
     put(c->v_af, v_af);
-  }
-  {
-    // phase C kernel: k_out_cr (cell rows) by default, k_out_rw (cell tiles)
-    // or k_out (explicit tables) on request or when the stencil is not the
-    // ring walk
-    const char* k = std::getenv("MSWM_KOUT");
-    const std::string kout = k ? k : "";
-    if (kout == "ringtile") c->rw_ok = build_rw(c, d, c_edge, c_deg, c_sbits, e_cells);
-    else if (kout != "explicit") c->cr_ok = build_cr(c, d, c_edge, c_deg, c_sbits);
   }
   put(c->c_edge, c_edge);
   put(c->c_vert, c_vert);
@@ -1243,18 +976,6 @@ MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
   debug_mem("plan_for: spans");
   // supersets need the closure bitmask for the dry check
   if (p->sv.n() > p->nv) p->dense_v = true;
-  if (c->rw_ok) {
-    DArr<uint8_t> tk;
-    tk.alloc(size_t(c->rw_ntiles));
-    CK(cudaMemsetAsync(tk.p, 0xFF, size_t(c->rw_ntiles), s));
-    if (int64_t(p->nc) + p->ne > 0) {
-      k_mark_rw<<<nblk(int64_t(p->nc) + p->ne), kBlock, 0, s>>>(p->cells, p->nc, p->edges, p->ne,
-                                                                 c->c_tile.p, c->e_cells.p, tk.p);
-      CK(cudaGetLastError());
-    }
-    p->rw_n = int32_t(compact(c, tk.p, c->rw_ntiles, 1, p->rw_list)[0]);
-    if (p->rw_n == c->rw_ntiles) p->rw_list = DArr<int32_t>();  // every tile: no list
-  }
   if (p->dense_v && p->nv < c->nV) {
     p->vmask.alloc((size_t(c->nV) + 31) / 32);
     k_pack_bits<<<nblk((int64_t(c->nV) + 31) / 32), kBlock, 0, s>>>(c->nV, mv.p, p->vmask.p);
@@ -1352,53 +1073,7 @@ void launch_eval_once(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, cons
     ++c->launches;
   }
   const int64_t nout = p.sc_out.n() + p.se_out.n();
-  if (nout > 0 && c->rw_ok) {
-    OutArgs a;
-    std::memset(&a, 0, sizeof(a));
-    a.mask = p.mask;
-    a.ckey = c->have_regions ? c->ckey.p : nullptr;
-    a.ekey = c->have_regions ? c->ekey.p : nullptr;
-    a.cop[0] = cop[0];
-    a.cop[1] = cop[1];
-    a.eop[0] = eop[0];
-    a.eop[1] = eop[1];
-    RwArgs r;
-    r.tiles = c->rw_tiles.p;
-    r.list = p.rw_list.p;
-    r.n_tiles = p.rw_n;
-    r.emax = c->rw_emax;
-    r.cmax = c->rw_cmax;
-    r.halo = c->rw_halo.p;
-    r.extra = c->rw_extra.p;
-    r.ring = c->rw_ring.p;
-    r.e_lc = c->e_lc.p;
-    r.e_slots = c->e_slots.p;
-    r.rat = c->c_rat.p;
-    r.cinfo = c->c_info.p;
-    int per_sm = c->rw_blocks;
-    if (side && side->ctas_per_sm[2] > 0) per_sm = std::max(1, per_sm * side->ctas_per_sm[2] / 8);
-    const int g = int(std::max<int64_t>(1, std::min<int64_t>(p.rw_n, int64_t(per_sm) * c->n_sm)));
-    if (p.rw_n > 0) {
-      k_out_rw<<<g, kRwThreads, c->rw_smem, s>>>(M, Kp, FQ, r, a);
-      CK(cudaGetLastError());
-      ++c->launches;
-    }
-  } else if (nout > 0 && c->cr_ok) {
-    OutArgs a;
-    std::memset(&a, 0, sizeof(a));
-    a.cs = p.sc_out.dev();
-    a.es = p.se_out.dev();
-    a.mask = p.mask;
-    a.ckey = c->have_regions ? c->ckey.p : nullptr;
-    a.ekey = c->have_regions ? c->ekey.p : nullptr;
-    a.cop[0] = cop[0];
-    a.cop[1] = cop[1];
-    a.eop[0] = eop[0];
-    a.eop[1] = eop[1];
-    k_out_cr<<<grid(nout, 2), kSBlock, 0, s>>>(M, Kp, FQ, c->c_rows.p, c->e_slots.p, a);
-    CK(cudaGetLastError());
-    ++c->launches;
-  } else if (nout > 0) {
+  if (nout > 0) {
     OutArgs a;
     std::memset(&a, 0, sizeof(a));
     a.cs = p.sc_out.dev();
@@ -2631,7 +2306,7 @@ int mswm_cuda_eval_profile(mswm_cuda_ctx* c, float* eval_ms, int64_t* out_cells,
 
 int mswm_cuda_layout_info(const mswm_cuda_ctx* c, int* kernel_path, int* identity_order) {
   if (!c) return MSWM_E_USAGE;
-  if (kernel_path) *kernel_path = c->cr_ok ? 2 : (c->rw_ok ? 1 : 0);
+  if (kernel_path) *kernel_path = 0;
   if (identity_order) *identity_order = c->identity ? 1 : 0;
   return MSWM_OK;
 }

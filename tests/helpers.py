@@ -31,3 +31,19 @@ def golden_mesh(name):
     if name.startswith("sphereL"):
         return Mesh.icosahedral(int(name[len("sphereL"):]), 6371220.0)
     raise KeyError(name)
+
+
+def workload(cfg: str):
+    """A BASELINE configuration's workload, built once per test session for
+    the full-size tests (the C4 / C5 meshes take minutes to build)."""
+    return _workload(cfg)
+
+
+def _build(cfg):
+    from paper_2106_07154_b200 import workloads as W
+    return W.CONFIGS[cfg]()
+
+
+import functools  # noqa: E402
+
+_workload = functools.lru_cache(maxsize=2)(_build)

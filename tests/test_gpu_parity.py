@@ -9,7 +9,7 @@ bound is asserted too where north_star states it.
 import numpy as np
 import pytest
 
-from helpers import bits_equal, golden_mesh, load_golden, max_rel
+from helpers import bits_equal, golden_mesh, load_golden, max_rel, workload
 from make_golden import mesh_digest
 from oracle.oracle import Oracle
 from paper_2106_07154_b200 import workloads as W
@@ -316,18 +316,12 @@ def test_stepper_drop_in_interface():
     assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
 
 
-@pytest.mark.parametrize("kout,env", [("cellrow", {}),
-                                      ("ringtile", {"MSWM_KOUT": "ringtile"}),
-                                      ("ringtile", {"MSWM_KOUT": "ringtile", "MSWM_RW_CELLS": "16"}),
-                                      ("ringtile", {"MSWM_KOUT": "ringtile", "MSWM_RW_STAGE_KB": "8"}),
-                                      ("explicit", {"MSWM_KOUT": "explicit", "MSWM_ST16": "1"}),
-                                      ("explicit", {"MSWM_KOUT": "explicit", "MSWM_ST16": "0"})])
+@pytest.mark.parametrize("kout,env", [("explicit", {"MSWM_ST16": "1"}),
+                                      ("explicit", {"MSWM_ST16": "0"})])
 def test_layouts_are_bitwise_equivalent(kout, env, monkeypatch):
     """Results are independent of the device numbering (input, Hilbert,
-    region-major, random) and of the output kernel: k_out_rw (cell tiles in
-    shared memory, ring-walk weights; tile sizes and stage capacities that
-    force tile splitting) or k_out over the explicit stencil tables (16-bit
-    offsets or the int32 table)."""
+    region-major, random) and of the stencil-id table (16-bit offsets or the
+    int32 table)."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     st16 = env.get("MSWM_ST16", "1")
@@ -466,16 +460,13 @@ def test_wide_interfaces_bitwise(width):
             assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref), (order, scheme)
 
 
-@pytest.mark.parametrize("kout", ["cellrow", "ringtile", "explicit"])
 @pytest.mark.parametrize("fork", ["1", "0"])
 @pytest.mark.parametrize("order", ["regions", "hilbert"])
-def test_concurrent_coarse_step_bitwise(kout, fork, order, monkeypatch):
+def test_concurrent_coarse_step_bitwise(fork, order, monkeypatch):
     """LTS3 with the coarse step (step 4) on a second stream concurrent with
     the substeps (default) and in sequence (MSWM_FORK=0): bitwise equal to
     the oracle over several coarse steps, M = 2 and 4."""
     monkeypatch.setenv("MSWM_FORK", fork)
-    if kout != "cellrow":
-        monkeypatch.setenv("MSWM_KOUT", kout)
     wl = W.small_sphere(6, seed=41, cap_deg=25.0)
     o = _oracle_for(wl)
     ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order, fine_mask=wl.fine_mask)
@@ -494,7 +485,6 @@ def test_stencil_offsets16_bitwise(st16, monkeypatch):
     int16 (a random numbering of a level-6 sphere: 123k edges, most offsets
     wide, warps mixing both kinds) and the int32-only table: bitwise equal."""
     monkeypatch.setenv("MSWM_ST16", st16)
-    monkeypatch.setenv("MSWM_KOUT", "explicit")
     wl = W.small_sphere(6, seed=31, cap_deg=20.0)
     o = _oracle_for(wl)
     h_ref, u_ref, _ = o.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, wl.M, 2)
@@ -534,7 +524,7 @@ def test_full_size_against_reference(config):
     from oracle.oracle import RefEvaluator, RefMesh, RefRegions, ref_available
     if not ref_available():
         pytest.skip("oracle/_ref not built")
-    wl = W.CONFIGS[config](n_steps=2)
+    wl = workload(config)
     nC, nE = wl.mesh.n_cells, wl.mesh.n_edges
     rm = RefMesh.from_mesh(wl.mesh)
     rr = RefRegions(rm, wl.fine_mask, wl.width)

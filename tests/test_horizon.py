@@ -16,7 +16,7 @@ import json
 import numpy as np
 import pytest
 
-from helpers import GOLDEN
+from helpers import GOLDEN, workload
 from paper_2106_07154_b200 import workloads as W
 from paper_2106_07154_b200.api import CudaContext, Scheme, State
 
@@ -58,7 +58,7 @@ def test_lts3_horizon_bitwise_vs_reference(cfg):
     """C4: 100 coarse steps (north_star); C2: its 1000-step horizon; C1 100;
     C3 20; C5 1 -- h and u bitwise the reference at every checkpoint."""
     rec = _load(cfg)
-    wl = W.CONFIGS[cfg]()
+    wl = workload(cfg)
     assert _input_digest(wl) == rec["input_sha256"], "workload or mesh builder changed"
     ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order="regions", fine_mask=wl.fine_mask,
                       interface_width=wl.width)
