@@ -15,10 +15,14 @@
 #include <array>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <exception>
+#include <mutex>
 #include <numeric>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "mswm_host.h"
@@ -26,6 +30,95 @@
 namespace {
 
 thread_local std::string g_last_error;
+
+// --- host threads -----------------------------------------------------------
+// The builder's per-element loops run on all host cores (MSWM_HOST_THREADS
+// overrides); every element's arithmetic is unchanged, so the tables are
+// bitwise those of the serial build.
+int host_threads() {
+  static const int n = [] {
+    if (const char* e = std::getenv("MSWM_HOST_THREADS")) return std::max(1, std::atoi(e));
+    return std::max(1, int(std::thread::hardware_concurrency()));
+  }();
+  return n;
+}
+
+// f(lo, hi) over [0, n) in contiguous chunks; the first exception is rethrown.
+template <class F>
+void par_for(int64_t n, F&& f, int64_t grain = 16384) {
+  const int64_t T = std::min<int64_t>(host_threads(), std::max<int64_t>(1, n / grain));
+  if (T <= 1) {
+    if (n > 0) f(int64_t(0), n);
+    return;
+  }
+  std::exception_ptr err;
+  std::mutex mu;
+  std::vector<std::thread> th;
+  for (int64_t k = 0; k < T; ++k)
+    th.emplace_back([&, k] {
+      try {
+        f(n * k / T, n * (k + 1) / T);
+      } catch (...) {
+        std::lock_guard<std::mutex> g(mu);
+        if (!err) err = std::current_exception();
+      }
+    });
+  for (auto& t : th) t.join();
+  if (err) std::rethrow_exception(err);
+}
+
+// Sample sort on all host threads: sorted chunks, splitters from a sorted
+// sample, every chunk cut at the splitters, each bucket gathered and sorted.
+template <class T>
+void par_sort(std::vector<T>& v) {
+  const int64_t n = int64_t(v.size());
+  const int64_t C = std::min<int64_t>(host_threads(), std::max<int64_t>(1, n / 65536));
+  if (C <= 1) {
+    std::sort(v.begin(), v.end());
+    return;
+  }
+  std::vector<int64_t> b(size_t(C) + 1);
+  for (int64_t k = 0; k <= C; ++k) b[k] = n * k / C;
+  par_for(C, [&](int64_t lo, int64_t hi) {
+    for (int64_t k = lo; k < hi; ++k) std::sort(v.begin() + b[k], v.begin() + b[k + 1]);
+  }, 1);
+  const int64_t S = 64 * C;
+  std::vector<T> sample(S);
+  for (int64_t q = 0; q < S; ++q) sample[q] = v[(n - 1) * q / (S - 1)];
+  std::sort(sample.begin(), sample.end());
+  std::vector<T> split(size_t(C) - 1);
+  for (int64_t j = 1; j < C; ++j) split[j - 1] = sample[S * j / C];
+  // cut[k][j]: start of bucket j in chunk k
+  std::vector<int64_t> cut(size_t(C) * (C + 1));
+  par_for(C, [&](int64_t lo, int64_t hi) {
+    for (int64_t k = lo; k < hi; ++k) {
+      cut[k * (C + 1)] = b[k];
+      for (int64_t j = 1; j < C; ++j)
+        cut[k * (C + 1) + j] = std::lower_bound(v.begin() + cut[k * (C + 1) + j - 1],
+                                                v.begin() + b[k + 1], split[j - 1]) - v.begin();
+      cut[k * (C + 1) + C] = b[k + 1];
+    }
+  }, 1);
+  std::vector<int64_t> out(size_t(C) + 1, 0);
+  for (int64_t j = 0; j < C; ++j) {
+    int64_t m = 0;
+    for (int64_t k = 0; k < C; ++k) m += cut[k * (C + 1) + j + 1] - cut[k * (C + 1) + j];
+    out[j + 1] = out[j] + m;
+  }
+  std::vector<T> tmp(v.size());
+  par_for(C, [&](int64_t lo, int64_t hi) {
+    for (int64_t j = lo; j < hi; ++j) {
+      int64_t at = out[j];
+      for (int64_t k = 0; k < C; ++k) {
+        const int64_t x = cut[k * (C + 1) + j], y = cut[k * (C + 1) + j + 1];
+        std::copy(v.begin() + x, v.begin() + y, tmp.begin() + at);
+        at += y - x;
+      }
+      std::sort(tmp.begin() + out[j], tmp.begin() + out[j + 1]);
+    }
+  }, 1);
+  v.swap(tmp);
+}
 
 struct V3 {
   double x, y, z;
@@ -69,33 +162,46 @@ struct Triangulation {
 // Returns side_id[s] in [0, n_unique), ids assigned in ascending order of
 // each side's first occurrence -- the order an insertion-ordered hash map
 // (the reference's edge_of / midpoint maps) produces.
-std::vector<int32_t> number_sides(const std::vector<Tri>& tris, int64_t* n_unique) {
+std::vector<int32_t> number_sides(const std::vector<Tri>& tris, int64_t* n_unique,
+                                  std::vector<uint8_t>* first = nullptr) {
   const int64_t ns = int64_t(tris.size()) * 3;
-  std::vector<uint64_t> key(ns);
-  for (int64_t t = 0; t < int64_t(tris.size()); ++t)
-    for (int k = 0; k < 3; ++k) {
-      uint64_t a = uint32_t(tris[t][k]), b = uint32_t(tris[t][(k + 1) % 3]);
-      if (a > b) std::swap(a, b);
-      key[3 * t + k] = (a << 32) | b;
-    }
-  std::vector<int64_t> order(ns);
-  std::iota(order.begin(), order.end(), 0);
-  std::sort(order.begin(), order.end(), [&](int64_t x, int64_t y) {
-    return key[x] != key[y] ? key[x] < key[y] : x < y;
+  struct KS {
+    uint64_t key;
+    int64_t s;
+    bool operator<(const KS& o) const { return key != o.key ? key < o.key : s < o.s; }
+  };
+  std::vector<KS> ks(ns);
+  par_for(int64_t(tris.size()), [&](int64_t lo, int64_t hi) {
+    for (int64_t t = lo; t < hi; ++t)
+      for (int k = 0; k < 3; ++k) {
+        uint64_t a = uint32_t(tris[t][k]), b = uint32_t(tris[t][(k + 1) % 3]);
+        if (a > b) std::swap(a, b);
+        ks[3 * t + k] = {(a << 32) | b, 3 * t + k};
+      }
   });
-  // rep[s] = first side with the same key.
+  par_sort(ks);
+  // rep[s] = first side with the same key (the run head: sorted by (key, s))
   std::vector<int64_t> rep(ns);
   for (int64_t i = 0; i < ns;) {
     int64_t j = i;
-    while (j < ns && key[order[j]] == key[order[i]]) ++j;
-    for (int64_t q = i; q < j; ++q) rep[order[q]] = order[i];
+    while (j < ns && ks[j].key == ks[i].key) ++j;
+    for (int64_t q = i; q < j; ++q) rep[ks[q].s] = ks[i].s;
     i = j;
   }
+  std::vector<KS>().swap(ks);
   std::vector<int32_t> id(ns, -1);
   int64_t next = 0;
   for (int64_t s = 0; s < ns; ++s)
     if (rep[s] == s) id[s] = int32_t(next++);
-  for (int64_t s = 0; s < ns; ++s) id[s] = id[rep[s]];
+  par_for(ns, [&](int64_t lo, int64_t hi) {
+    for (int64_t s = lo; s < hi; ++s) id[s] = id[rep[s]];
+  });
+  if (first) {
+    first->assign(ns, 0);
+    par_for(ns, [&](int64_t lo, int64_t hi) {
+      for (int64_t s = lo; s < hi; ++s) (*first)[s] = rep[s] == s;
+    });
+  }
   *n_unique = next;
   return id;
 }
@@ -128,28 +234,29 @@ Triangulation subdivide(int level) {
   Triangulation t = icosahedron();
   for (int l = 0; l < level; ++l) {
     int64_t n_mid = 0;
-    const std::vector<int32_t> sid = number_sides(t.tris, &n_mid);
+    std::vector<uint8_t> first;
+    const std::vector<int32_t> sid = number_sides(t.tris, &n_mid, &first);
     const int32_t base = int32_t(t.pts.size());
     t.pts.resize(size_t(base + n_mid));
-    std::vector<char> made(size_t(n_mid), 0);
     std::vector<Tri> next(t.tris.size() * 4);
-    for (size_t tt = 0; tt < t.tris.size(); ++tt) {
-      const Tri f = t.tris[tt];
-      int32_t m[3];
-      for (int k = 0; k < 3; ++k) {
-        const int32_t id = sid[3 * tt + k];
-        if (!made[id]) {
-          made[id] = 1;
-          t.pts[base + id] = unit(add(t.pts[f[k]], t.pts[f[(k + 1) % 3]]));
+    // a midpoint from its first triangle (the reference's insertion order
+    // fixes only its id; add is commutative, so any side gives the same bits)
+    par_for(int64_t(t.tris.size()), [&](int64_t lo, int64_t hi) {
+      for (int64_t tt = lo; tt < hi; ++tt) {
+        const Tri f = t.tris[tt];
+        int32_t m[3];
+        for (int k = 0; k < 3; ++k) {
+          const int32_t id = sid[3 * tt + k];
+          if (first[3 * tt + k]) t.pts[base + id] = unit(add(t.pts[f[k]], t.pts[f[(k + 1) % 3]]));
+          m[k] = base + id;
         }
-        m[k] = base + id;
+        const int32_t ab = m[0], bc = m[1], ca = m[2];
+        next[4 * tt + 0] = {f[0], ab, ca};
+        next[4 * tt + 1] = {f[1], bc, ab};
+        next[4 * tt + 2] = {f[2], ca, bc};
+        next[4 * tt + 3] = {ab, bc, ca};
       }
-      const int32_t ab = m[0], bc = m[1], ca = m[2];
-      next[4 * tt + 0] = {f[0], ab, ca};
-      next[4 * tt + 1] = {f[1], bc, ab};
-      next[4 * tt + 2] = {f[2], ca, bc};
-      next[4 * tt + 3] = {ab, bc, ca};
-    }
+    });
     t.tris.swap(next);
   }
   return t;
@@ -250,7 +357,8 @@ void dualise_topology(const Triangulation& tri, mswm_mesh& m, bool check_euler) 
   m.cell_edges.assign(total, -1);
   m.cell_vertices.assign(total, -1);
   m.cell_cells.assign(total, -1);
-  for (int32_t i = 0; i < nP; ++i) {
+  par_for(nP, [&](int64_t lo, int64_t hi) {
+  for (int32_t i = int32_t(lo); i < int32_t(hi); ++i) {
     const int32_t mm = deg[i], off = m.cell_offset[i];
     if (mm < 3) throw std::runtime_error("degenerate Voronoi cell " + std::to_string(i));
     const Succ* s = succ.data() + off;
@@ -272,11 +380,13 @@ void dualise_topology(const Triangulation& tri, mswm_mesh& m, bool check_euler) 
     }
     if (cur != start) throw std::runtime_error("fan does not close around cell " + std::to_string(i));
   }
+  });
 
   // Vertex tables, smallest cell first (mesh_build.cpp:249-258).
   m.vertex_cells.assign(3 * nT, -1);
   m.vertex_edges.assign(3 * nT, -1);
-  for (int64_t v = 0; v < nT; ++v) {
+  par_for(nT, [&](int64_t lo, int64_t hi) {
+  for (int64_t v = lo; v < hi; ++v) {
     Tri f = tri.tris[v];
     int rot = 0;
     while (f[0] > f[1] || f[0] > f[2]) {
@@ -288,6 +398,7 @@ void dualise_topology(const Triangulation& tri, mswm_mesh& m, bool check_euler) 
       m.vertex_edges[3 * v + k] = side_edge[3 * v + (k + rot) % 3];
     }
   }
+  });
 
   // Edge stencil (mesh_build.cpp:133-154): both cells' rings, lower cell
   // first, each walked counterclockwise starting just after e.
@@ -296,7 +407,8 @@ void dualise_topology(const Triangulation& tri, mswm_mesh& m, bool check_euler) 
     m.ee_offset[e + 1] =
         m.ee_offset[e] + m.ring(m.edge_cells[2 * e]) + m.ring(m.edge_cells[2 * e + 1]) - 2;
   m.edge_edges.assign(m.ee_offset[nE], -1);
-  for (int64_t e = 0; e < nE; ++e) {
+  par_for(nE, [&](int64_t lo, int64_t hi) {
+  for (int64_t e = lo; e < hi; ++e) {
     int pos = m.ee_offset[e];
     for (int side = 0; side < 2; ++side) {
       const int32_t c = m.edge_cells[2 * e + side];
@@ -305,11 +417,13 @@ void dualise_topology(const Triangulation& tri, mswm_mesh& m, bool check_euler) 
       for (int k = 1; k < mm; ++k) m.edge_edges[pos++] = m.cell_edges[off + (p + k) % mm];
     }
   }
+  });
 
   // Orientation signs (mesh_build.cpp:156-183).
   m.edge_cell_sign.assign(2 * nE, 0);
   m.edge_vertex_sign.assign(2 * nE, 0);
-  for (int64_t e = 0; e < nE; ++e) {
+  par_for(nE, [&](int64_t lo, int64_t hi) {
+  for (int64_t e = lo; e < hi; ++e) {
     m.edge_cell_sign[2 * e] = -1;
     m.edge_cell_sign[2 * e + 1] = +1;
     const int32_t c0 = m.edge_cells[2 * e];
@@ -325,13 +439,15 @@ void dualise_topology(const Triangulation& tri, mswm_mesh& m, bool check_euler) 
       throw std::runtime_error("edge ring vertex does not match its endpoints");
     }
   }
+  });
 }
 
 // vertex_kite (mesh_build.cpp:330-341) and TRiSK weights (:343-362), from
 // kite_area / cell_area already filled in.
 void finish_kites_and_weights(mswm_mesh& m) {
   m.vertex_kite.assign(size_t(3) * m.nV, 0.0);
-  for (int32_t v = 0; v < m.nV; ++v)
+  par_for(m.nV, [&](int64_t lo, int64_t hi) {
+  for (int32_t v = int32_t(lo); v < int32_t(hi); ++v)
     for (int k = 0; k < 3; ++k) {
       const int32_t c = m.vertex_cells[3 * v + k];
       const int off = m.cell_offset[c], mm = m.ring(c);
@@ -344,8 +460,10 @@ void finish_kites_and_weights(mswm_mesh& m) {
       if (slot < 0) throw std::runtime_error("vertex missing from ring of its cell");
       m.vertex_kite[3 * v + k] = m.kite_area[off + slot];
     }
+  });
   m.edge_weight.assign(m.edge_edges.size(), 0.0);
-  for (int32_t e = 0; e < m.nE; ++e) {
+  par_for(m.nE, [&](int64_t lo, int64_t hi) {
+  for (int32_t e = int32_t(lo); e < int32_t(hi); ++e) {
     int pos = m.ee_offset[e];
     for (int side = 0; side < 2; ++side) {
       const int32_t c = m.edge_cells[2 * e + side];
@@ -360,6 +478,7 @@ void finish_kites_and_weights(mswm_mesh& m) {
       }
     }
   }
+  });
 }
 
 void put3(std::vector<double>& dst, int64_t i, const V3& p) {
@@ -373,10 +492,13 @@ V3 get3(const std::vector<double>& src, int64_t i) { return {src[3 * i], src[3 *
 void sphere_geometry(const Triangulation& tri, mswm_mesh& m, double R) {
   const double R2 = R * R;
   m.cell_xyz.assign(size_t(3) * m.nC, 0.0);
-  for (int32_t i = 0; i < m.nC; ++i) put3(m.cell_xyz, i, unit(tri.pts[i]));
+  par_for(m.nC, [&](int64_t lo, int64_t hi) {
+    for (int32_t i = int32_t(lo); i < int32_t(hi); ++i) put3(m.cell_xyz, i, unit(tri.pts[i]));
+  });
   m.vertex_xyz.assign(size_t(3) * m.nV, 0.0);
   m.vertex_area.assign(m.nV, 0.0);
-  for (int32_t v = 0; v < m.nV; ++v) {
+  par_for(m.nV, [&](int64_t lo, int64_t hi) {
+  for (int32_t v = int32_t(lo); v < int32_t(hi); ++v) {
     const V3 a = get3(m.cell_xyz, m.vertex_cells[3 * v]);
     const V3 b = get3(m.cell_xyz, m.vertex_cells[3 * v + 1]);
     const V3 c = get3(m.cell_xyz, m.vertex_cells[3 * v + 2]);
@@ -390,10 +512,12 @@ void sphere_geometry(const Triangulation& tri, mswm_mesh& m, double R) {
     if (!(area > 0.0)) throw std::runtime_error("non-positive vertex area at " + std::to_string(v));
     m.vertex_area[v] = area;
   }
+  });
   m.edge_xyz.assign(size_t(3) * m.nE, 0.0);
   m.edge_len.assign(m.nE, 0.0);
   m.edge_dual_len.assign(m.nE, 0.0);
-  for (int32_t e = 0; e < m.nE; ++e) {
+  par_for(m.nE, [&](int64_t lo, int64_t hi) {
+  for (int32_t e = int32_t(lo); e < int32_t(hi); ++e) {
     const V3 c0 = get3(m.cell_xyz, m.edge_cells[2 * e]);
     const V3 c1 = get3(m.cell_xyz, m.edge_cells[2 * e + 1]);
     const V3 v0 = get3(m.vertex_xyz, m.edge_vertices[2 * e]);
@@ -404,10 +528,12 @@ void sphere_geometry(const Triangulation& tri, mswm_mesh& m, double R) {
     if (!(m.edge_len[e] > R * 1e-14) || !(m.edge_dual_len[e] > R * 1e-14))
       throw std::runtime_error("zero-length edge " + std::to_string(e));
   }
+  });
   const int64_t total = m.cell_offset[m.nC];
   m.kite_area.assign(total, 0.0);
   m.cell_area.assign(m.nC, 0.0);
-  for (int32_t i = 0; i < m.nC; ++i) {
+  par_for(m.nC, [&](int64_t lo, int64_t hi) {
+  for (int32_t i = int32_t(lo); i < int32_t(hi); ++i) {
     const int off = m.cell_offset[i], mm = m.ring(i);
     const V3 xi = get3(m.cell_xyz, i);
     double acc = 0.0;
@@ -422,6 +548,7 @@ void sphere_geometry(const Triangulation& tri, mswm_mesh& m, double R) {
     if (!(acc > 0.0)) throw std::runtime_error("non-positive cell area at " + std::to_string(i));
     m.cell_area[i] = acc;
   }
+  });
 }
 
 // --- planar periodic hexagonal mesh ---------------------------------------
@@ -570,7 +697,8 @@ uint64_t hilbert2(uint32_t n, uint32_t x, uint32_t y) {
 void locality_order(const mswm_mesh& m, int32_t* order) {
   const uint32_t n = 1u << 20;
   std::vector<std::pair<uint64_t, int32_t>> key(m.nC);
-  for (int32_t i = 0; i < m.nC; ++i) {
+  par_for(m.nC, [&](int64_t lo, int64_t hi) {
+  for (int32_t i = int32_t(lo); i < int32_t(hi); ++i) {
     const double* p = &m.cell_xyz[3 * size_t(i)];
     uint64_t k;
     if (!m.spherical) {
@@ -600,7 +728,8 @@ void locality_order(const mswm_mesh& m, int32_t* order) {
     }
     key[i] = {k, i};
   }
-  std::sort(key.begin(), key.end());
+  });
+  par_sort(key);
   for (int32_t k = 0; k < m.nC; ++k) order[k] = key[k].second;
 }
 

@@ -6,3 +6,4 @@ REF_RANKS=4 timeout 3300 python tests/make_horizon_digests.py c5 > gpurun_out/c5
 tail -5 gpurun_out/c5digest.log
 cp tests/golden/horizon_c5.json gpurun_out/ 2>/dev/null
 timeout 1200 python -m pytest tests/test_horizon.py -q -k c5 > gpurun_out/c5_test.log 2>&1; echo "c5 test rc=$?"; tail -3 gpurun_out/c5_test.log
+timeout 600 python -m pytest tests/test_gpu_study.py tests/test_gpu_parity.py -q -x -k "study or layouts or concurrent or stencil" > gpurun_out/c5_study.log 2>&1; echo "study rc=$?"; tail -3 gpurun_out/c5_study.log

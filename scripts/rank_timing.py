@@ -67,11 +67,19 @@ def main():
         for r, rc in enumerate(ranks):
             send = {q: needs[m][q].get(r, np.zeros(0, np.int32)) for q in needs[m][r]}
             rc.set_halo_mask(int(m), send, needs[m][r])
-    per_rank, fork = [], []
+    per_rank, fork, evals = [], [], []
     for rc in ranks:
         rc.upload(wl.h, wl.u)
         per_rank.append(time_steps(rc.ctx, wl, steps))
         fork.append(rc.ctx.concurrent_coarse())
+        # per-evaluation device times of one profiled step (events around
+        # every evaluation: step 1, step 2, the 3M substeps, the coarse step)
+        rc.ctx.set_profiling(1)
+        rc.ctx.advance(Scheme.LTS3, wl.dt, wl.M, 2)
+        ms, nc, ne = rc.ctx.eval_profile()
+        evals.append({"ms": [round(float(x), 4) for x in ms], "cells": [int(x) for x in nc],
+                      "edges": [int(x) for x in ne]})
+        rc.ctx.set_profiling(0)
     # bytes received per exchange (8 B per value) per rank and mask, and peers
     xbytes = {hex(int(m)): [int(8 * sum(len(v) for v in needs[m][r].values())) for r in range(n)]
               for m in masks}
@@ -81,7 +89,7 @@ def main():
         "config": cfg, "n_ranks": n, "steps": steps, "single_ms_per_step": t_single,
         "rank_ms_per_step": per_rank, "max_rank_ms": max(per_rank),
         "ideal_ms": t_single / n, "compute_efficiency": t_single / (n * max(per_rank)),
-        "concurrent_coarse": fork, "owned_cells": [rc.lm.n_owned_cells for rc in ranks],
+        "concurrent_coarse": fork, "evals_per_rank": evals, "owned_cells": [rc.lm.n_owned_cells for rc in ranks],
         "local_cells": [rc.lm.n_cells for rc in ranks],
         "recv_bytes_per_exchange": xbytes, "peers_per_exchange": xpeers,
         "setup_s": time.time() - t0}))
