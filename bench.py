@@ -502,6 +502,34 @@ def run_ours(args, ws, rank, local):
 
     launches = ctx.kernels_per_step() * args.steps
 
+    # the per-stage drop-in (mswm::CudaEvaluator under the reference's own
+    # Stepper, one C-ABI eval() per stage): the 3M+3 eval calls of one LTS3
+    # coarse step with pageable host arrays, as the reference issues them
+    # (integrators.cpp:483-563); the reference's host-side stage combines
+    # are not part of this number
+    dropin = None
+    if ws == 1:
+        from paper_2106_07154_b200.api import (MASK_COARSE_ONLY, MASK_IF_COARSE, MASK_STEP1,
+                                               MASK_SUB, CudaEvaluator)
+        ev = CudaEvaluator(ctx)
+        hh, uu = np.array(st0.h), np.array(st0.u)
+        dh, du = np.zeros_like(hh), np.zeros_like(uu)
+        seq = [MASK_STEP1, MASK_IF_COARSE] + [MASK_SUB] * (3 * wl.M) + [MASK_COARSE_ONLY]
+        for m in dict.fromkeys(seq):  # first call per mask builds its plan / read set
+            ev.eval(hh, uu, int(m), dh, du)
+        n_di = 2
+        t = time.perf_counter()
+        for _ in range(n_di):
+            for m in seq:
+                ev.eval(hh, uu, int(m), dh, du)
+        di_s = (time.perf_counter() - t) / n_di
+        dropin = {"value": edge_per_step / di_s, "unit": UNIT, "ms_per_coarse_step": di_s * 1e3,
+                  "eval_calls_per_step": len(seq),
+                  "d2h_bytes_per_step": int(8 * (edge_per_step + cell_per_step)),
+                  "note": "C-ABI eval() per stage with host arrays (inputs: the masked read set "
+                          "only; outputs: the masked entries only); excludes the reference "
+                          "Stepper's own host-side stage combines"}
+
     # the comparison strategy (north_star): global RK4 at the fine step dt/M,
     # M steps per coarse interval, timed the same way
     rk4 = None
@@ -570,6 +598,7 @@ def run_ours(args, ws, rank, local):
                          "share_of_step": float(evms.sum() / ms_step)},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": io_bytes,
                     "d2h_bytes_per_step": io_bytes, "steps": n_e2e},
+            "e2e_dropin_eval": dropin,
             "cpu_baseline": cpu,
             "rk4_fine_dt": rk4,
             "gpu_launches": int(launches),

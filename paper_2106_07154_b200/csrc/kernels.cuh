@@ -671,6 +671,69 @@ __global__ void k_mark_closure(DevMesh M, const int32_t* __restrict__ c_vert,
   }
 }
 
+// Halo dependence of a rank's evaluations (interior / boundary split of the
+// multi-rank schedule).  A halo element is one this rank does not own
+// (key 0xFF); every value computed from one is "tainted".
+// tv[v]: q_v reads h / u of a halo element (operators.cpp:74-86).
+__global__ void k_taint_vertices(DevMesh M, const uint8_t* __restrict__ ckey,
+                                 const uint8_t* __restrict__ ekey, uint8_t* __restrict__ tv) {
+  const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= M.nV) return;
+  uint8_t t = 0;
+  for (int k = 0; k < 3; ++k)
+    t |= (ckey[M.v_cell[k * M.nV + v]] == 0xFF) | (ekey[M.v_edge[k * M.nV + v]] == 0xFF);
+  tv[v] = t;
+}
+// tf[e]: F_e or q~_e is tainted (:61-62, :88-89); tp[i]: psi_i is (:64-72, :112).
+__global__ void k_taint_fp(DevMesh M, const uint8_t* __restrict__ ckey,
+                           const uint8_t* __restrict__ ekey, const uint8_t* __restrict__ tv,
+                           uint8_t* __restrict__ tf, uint8_t* __restrict__ tp) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < M.nE) {
+    const int2 c = M.e_cells[t];
+    const int2 v = M.e_verts[t];
+    tf[t] = (ekey[t] == 0xFF) | (ckey[c.x] == 0xFF) | (ckey[c.y] == 0xFF) | tv[v.x] | tv[v.y];
+  } else if (t - M.nE < M.nC) {
+    const int32_t i = t - M.nE;
+    uint8_t x = ckey[i] == 0xFF;
+    for (int j = 0; j < M.c_deg[i]; ++j) x |= ekey[M.c_edge[j * M.nC + i]] == 0xFF;
+    tp[i] = x;
+  }
+}
+// Boundary outputs: dh_i reads (F, q~) of its ring (:91-99); du_e reads its
+// own q~, (F, q~) of its stencil = the rest of both cells' rings, and psi of
+// both cells (:101-116).  Everything else is interior: computable before
+// the halo exchange lands.
+__global__ void k_mark_boundary(DevMesh M, const uint8_t* __restrict__ tf,
+                                const uint8_t* __restrict__ tp, uint8_t* __restrict__ cb,
+                                uint8_t* __restrict__ eb) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < M.nC) {
+    uint8_t x = 0;
+    for (int j = 0; j < M.c_deg[t]; ++j) x |= tf[M.c_edge[j * M.nC + t]];
+    cb[t] = x;
+  } else if (t - M.nC < M.nE) {
+    const int32_t e = t - M.nC;
+    const int2 c = M.e_cells[e];
+    uint8_t x = tf[e] | tp[c.x] | tp[c.y];
+    for (int side = 0; side < 2; ++side) {
+      const int32_t i = side ? c.y : c.x;
+      for (int j = 0; j < M.c_deg[i]; ++j) x |= tf[M.c_edge[j * M.nC + i]];
+    }
+    eb[e] = x;
+  }
+}
+// Compaction key of one part of a mask's outputs: owned, in the mask, and
+// boundary flag == want.
+__global__ void k_part_key(int32_t n, const uint8_t* __restrict__ key, int shift, uint32_t mask,
+                           int gmax, const uint8_t* __restrict__ bnd, uint8_t want,
+                           uint8_t* __restrict__ out) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int g = key[i];
+  out[i] = (g <= gmax && ((mask >> (shift + g)) & 1u) && bnd[i] == want) ? 0 : 0xFF;
+}
+
 // Elements whose h (cells) or u (edges) one masked evaluation reads
 // (operators.cpp:61-86 over the closure lists): cells and edges of the PV
 // vertices, ring edges of the K cells, flux edges and their cells, and the

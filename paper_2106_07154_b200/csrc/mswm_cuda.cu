@@ -283,6 +283,11 @@ struct mswm_cuda_ctx {
   int32_t n_band_c = 0, n_band_e = 0;
   int fork_state = 0;  // 0 not prepared, 1 ready, -1 not eligible
   int replication = 1;  // SchemeConfig::replication (operators.cpp:60)
+  // interior / boundary split of ranked evaluations (plan_part)
+  bool bnd_ready = false;
+  DArr<uint8_t> cbnd, ebnd;
+  cudaStream_t lx = nullptr;         // halo exchanges overlapping the interior evaluation
+  cudaEvent_t ev_x0 = nullptr, ev_x1 = nullptr;
   cudaStream_t stream_of_capture = nullptr;
   DArr<int32_t> d_c_n2o, d_e_n2o;  // internal -> original ids (device permutes)
   DArr<double> io_h, io_u;          // staging for permuted uploads / downloads
@@ -356,6 +361,9 @@ struct mswm_cuda_ctx {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (ev_join_h) cudaEventDestroy(ev_join_h);
+    if (lx) cudaStreamDestroy(lx);
+    if (ev_x0) cudaEventDestroy(ev_x0);
+    if (ev_x1) cudaEventDestroy(ev_x1);
     if (stream) cudaStreamDestroy(stream);
     if (pin) cudaFreeHost(pin);
   }
@@ -834,6 +842,7 @@ void check_dry(mswm_cuda_ctx* c, const char* who = nullptr) {
 
 void invalidate(mswm_cuda_ctx* c) {
   c->plans.clear();
+  c->bnd_ready = false;
   c->drop_graphs();
   c->fork_state = 0;  // the band depends on the plans
 }
@@ -884,6 +893,8 @@ void make_span(mswm_cuda_ctx* c, const int32_t* d_list, int32_t n, int32_t unive
   out.list = out.own.p;
   out.n_list = n;
 }
+
+void finish_plan(mswm_cuda_ctx* c, MaskPlan* p, double out_dense_frac);
 
 MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
   auto it = c->plans.find(mask);
@@ -937,6 +948,18 @@ MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
     build(0, 5, c->cell_groups, p->own_cells, p->cells, p->nc, p->csplit, 2);
     build(6, 10, c->edge_groups, p->own_edges, p->edges, p->ne, p->esplit, 7);
   }
+  finish_plan(c, p.get(), 0.5);
+  auto& slot = c->plans[mask];
+  slot = std::move(p);
+  debug_mem("plan_for: done");
+  return *slot;
+}
+
+// Closures, launch spans and host id lists of a plan whose output lists are
+// set.  out_dense_frac > 1: the output spans are never dense supersets (a
+// part plan must not touch the other part's outputs).
+void finish_plan(mswm_cuda_ctx* c, MaskPlan* p, double out_dense_frac) {
+  cudaStream_t s = c->stream;
   // Closure marks (operators.cpp:35-58) and their compaction.
   DArr<uint8_t> mf, mq, mk, mv, key;
   mf.alloc(c->nE);
@@ -971,8 +994,8 @@ MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
   make_span(c, p->vclos.p, p->nv, c->nV, 0.85, p->sv);
   make_span(c, p->kclos.p, p->nk, c->nC, 0.85, p->sk);
   make_span(c, p->eclos.p, p->nec, c->nE, 0.85, p->se);
-  make_span(c, p->cells, p->nc, c->nC, 0.5, p->sc_out);
-  make_span(c, p->edges, p->ne, c->nE, 0.5, p->se_out);
+  make_span(c, p->cells, p->nc, c->nC, out_dense_frac, p->sc_out);
+  make_span(c, p->edges, p->ne, c->nE, out_dense_frac, p->se_out);
   debug_mem("plan_for: spans");
   // supersets need the closure bitmask for the dry check
   if (p->sv.n() > p->nv) p->dense_v = true;
@@ -993,9 +1016,56 @@ MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
     for (auto& i : p->host_cells) i = c->c_new2old[i];
     for (auto& e : p->host_edges) e = c->e_new2old[e];
   }
-  auto& slot = c->plans[mask];
+}
+
+// Boundary flags of a rank's outputs (k_taint_*, k_mark_boundary): the
+// outputs whose evaluation reads a halo value, directly or through PV, psi
+// or (F, q~).
+void ensure_boundary(mswm_cuda_ctx* c) {
+  if (c->bnd_ready) return;
+  cudaStream_t s = c->stream;
+  DArr<uint8_t> tv, tf, tp;
+  tv.alloc(c->nV);
+  tf.alloc(c->nE);
+  tp.alloc(c->nC);
+  c->cbnd.alloc(c->nC);
+  c->ebnd.alloc(c->nE);
+  const DevMesh M = c->dev();
+  k_taint_vertices<<<nblk(c->nV), kBlock, 0, s>>>(M, c->ckey.p, c->ekey.p, tv.p);
+  k_taint_fp<<<nblk(int64_t(c->nE) + c->nC), kBlock, 0, s>>>(M, c->ckey.p, c->ekey.p, tv.p, tf.p,
+                                                              tp.p);
+  k_mark_boundary<<<nblk(int64_t(c->nC) + c->nE), kBlock, 0, s>>>(M, tf.p, tp.p, c->cbnd.p,
+                                                                   c->ebnd.p);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  c->bnd_ready = true;
+}
+
+// The interior (part 1: reads no halo value) or boundary (part 2) outputs of
+// a mask, as a plan of their own.
+MaskPlan& plan_part(mswm_cuda_ctx* c, unsigned mask, int part) {
+  const unsigned key = mask | (unsigned(part) << 16);
+  auto it = c->plans.find(key);
+  if (it != c->plans.end()) return *it->second;
+  plan_for(c, mask);  // validates the mask
+  ensure_boundary(c);
+  auto p = std::make_unique<MaskPlan>();
+  p->mask = mask;
+  cudaStream_t s = c->stream;
+  const uint8_t want = part == 2 ? 1 : 0;
+  DArr<uint8_t> k;
+  k.alloc(std::max(c->nC, c->nE));
+  k_part_key<<<nblk(c->nC), kBlock, 0, s>>>(c->nC, c->ckey.p, 0, mask, 5, c->cbnd.p, want, k.p);
+  CK(cudaGetLastError());
+  p->nc = int32_t(compact(c, k.p, c->nC, 1, p->own_cells)[0]);
+  p->cells = p->nc ? p->own_cells.p : nullptr;
+  k_part_key<<<nblk(c->nE), kBlock, 0, s>>>(c->nE, c->ekey.p, 6, mask, 4, c->ebnd.p, want, k.p);
+  CK(cudaGetLastError());
+  p->ne = int32_t(compact(c, k.p, c->nE, 1, p->own_edges)[0]);
+  p->edges = p->ne ? p->own_edges.p : nullptr;
+  finish_plan(c, p.get(), 2.0);
+  auto& slot = c->plans[key];
   slot = std::move(p);
-  debug_mem("plan_for: done");
   return *slot;
 }
 
@@ -1327,6 +1397,46 @@ void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us, unsigned ma
   }
 }
 
+// An evaluation preceded by its halo exchange.  With ranks (and
+// MSWM_OVERLAP unset or 1) the exchange runs on a side stream while the
+// interior outputs -- those whose closure reads no halo value -- evaluate,
+// and the boundary outputs follow once the halo has landed: the transfer
+// hides behind the interior work.  Both parts are pure functions of their
+// inputs, so the split changes no bits.  `eval(c, plan)` launches one
+// member's evaluation with its fused stage update.
+template <class F>
+void exchange_eval(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us, unsigned mask, F&& eval) {
+  bool halos = false;
+  for (auto* c : cs) halos |= c->halo.active();
+  mswm_cuda_ctx* const c0 = cs[0];
+  if (!halos || !c0->lx) {
+    exchange(cs, hs, us, mask);
+    for (auto* c : cs) eval(c, plan_for(c, mask));
+    return;
+  }
+  cudaStream_t main = c0->ls;
+  CK(cudaEventRecord(c0->ev_x0, main));
+  CK(cudaStreamWaitEvent(c0->lx, c0->ev_x0, 0));
+  for (auto* c : cs) c->ls = c0->lx;
+  exchange(cs, hs, us, mask);
+  CK(cudaEventRecord(c0->ev_x1, c0->lx));
+  for (auto* c : cs) c->ls = main;
+  for (auto* c : cs) eval(c, plan_part(c, mask, 1));
+  CK(cudaStreamWaitEvent(main, c0->ev_x1, 0));
+  for (auto* c : cs) eval(c, plan_part(c, mask, 2));
+}
+
+void prepare_overlap(mswm_cuda_ctx* c) {
+  if (!c->halo.active() || c->lx) return;
+  const char* e = std::getenv("MSWM_OVERLAP");
+  if (e && e[0] == '0') return;
+  int lo = 0, hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  CK(cudaStreamCreateWithPriority(&c->lx, cudaStreamNonBlocking, hi));
+  CK(cudaEventCreateWithFlags(&c->ev_x0, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_x1, cudaEventDisableTiming));
+}
+
 // One LTS3 coarse step (see the file header for the aliasing argument) for
 // every rank context of the executor.
 // The LTS3 coarse step (step 4) runs concurrently with the substeps when
@@ -1427,22 +1537,20 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
   const double third = 1.0 / 3.0, two3 = 2.0 / 3.0;
   using C = mswm_cuda_ctx;
   // Step 1 (:483-487): h1 = h_old + dt*dh on UF1 u UF2 u I1 u I2 u C.
-  exchange(cs, &C::H, &C::U, kMaskStep1);
-  for (auto* c : cs) {
+  exchange_eval(cs, &C::H, &C::U, kMaskStep1, [&](mswm_cuda_ctx* c, const MaskPlan& p) {
     double *H = c->H.p, *U = c->U.p, *H1 = c->H1.p, *U1 = c->U1.p;
     Op co[2] = {mk_op(OP_EULER, H1, H, dt), mk_op(OP_EULER, H1, H, dt)};
     Op eo[2] = {mk_op(OP_EULER, U1, U, dt), mk_op(OP_EULER, U1, U, dt)};
-    launch_eval(c, plan_for(c, kMaskStep1), H, U, co, eo);
-  }
+    launch_eval(c, p, H, U, co, eo);
+  });
   // Step 2 (:491-500): h2 = 0.75 h_old + 0.25 h1 + (0.25 dt) dh on I u C.
-  exchange(cs, &C::H1, &C::U1, kMaskIfCoarse);
-  for (auto* c : cs) {
+  exchange_eval(cs, &C::H1, &C::U1, kMaskIfCoarse, [&](mswm_cuda_ctx* c, const MaskPlan& p) {
     double *H = c->H.p, *U = c->U.p, *H1 = c->H1.p, *U1 = c->U1.p, *H2 = c->H2.p, *U2 = c->U2.p;
     const double cr = 0.25 * dt;
     Op co[2] = {mk_op(OP_WCOMB, H2, H, 0.75, H1, 0.25, cr), mk_op(OP_WCOMB, H2, H, 0.75, H1, 0.25, cr)};
     Op eo[2] = {mk_op(OP_WCOMB, U2, U, 0.75, U1, 0.25, cr), mk_op(OP_WCOMB, U2, U, 0.75, U1, 0.25, cr)};
-    launch_eval(c, plan_for(c, kMaskIfCoarse), H1, U1, co, eo);
-  }
+    launch_eval(c, p, H1, U1, co, eo);
+  });
   // Step 4 forked onto the second stream (prepare_fork); with ranks, its
   // (restricted) halo exchange of h2/u2 rides on that stream too.  The
   // streams and events of member 0 serve the whole group.
@@ -1497,35 +1605,31 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
     // has to propagate them first (multi-rank)
     if (k > 0 && !fuse_pred)
       for (auto* c : cs) launch_predict(c, 1, k, M, c->H.p, c->U.p);
-    exchange(cs, &C::H, &C::U, kMaskSub);
-    for (auto* c : cs) {
+    exchange_eval(cs, &C::H, &C::U, kMaskSub, [&](mswm_cuda_ctx* c, const MaskPlan& p) {
       const PredArgs pa = make_pred(c, 1, k, M, c->H.p, c->U.p);
       Op co[2] = {mk_op(OP_EULER, c->H1.p, c->H.p, delta),
                   mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A1h.p, first)};
       Op eo[2] = {mk_op(OP_EULER, c->U1.p, c->U.p, delta),
                   mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A1u.p, first)};
-      launch_eval(c, plan_for(c, kMaskSub), c->H.p, c->U.p, co, eo,
-                  (k > 0 && fuse_pred) ? &pa : nullptr);
-    }
+      launch_eval(c, p, c->H.p, c->U.p, co, eo, (k > 0 && fuse_pred) ? &pa : nullptr);
+    });
     // stage 2: fine hc = 0.75 ha + 0.25 hb + (0.25 delta) d; acc2 += d   (:532-541)
     if (!fuse_pred)
       for (auto* c : cs) launch_predict(c, 2, k, M, c->H1.p, c->U1.p);
-    exchange(cs, &C::H1, &C::U1, kMaskSub);
-    for (auto* c : cs) {
+    exchange_eval(cs, &C::H1, &C::U1, kMaskSub, [&](mswm_cuda_ctx* c, const MaskPlan& p) {
       const PredArgs pa = make_pred(c, 2, k, M, c->H1.p, c->U1.p);
       const double cr = 0.25 * delta;
       Op co[2] = {mk_op(OP_WCOMB, c->H2.p, c->H.p, 0.75, c->H1.p, 0.25, cr),
                   mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A2h.p, first)};
       Op eo[2] = {mk_op(OP_WCOMB, c->U2.p, c->U.p, 0.75, c->U1.p, 0.25, cr),
                   mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A2u.p, first)};
-      launch_eval(c, plan_for(c, kMaskSub), c->H1.p, c->U1.p, co, eo, fuse_pred ? &pa : nullptr);
-    }
+      launch_eval(c, p, c->H1.p, c->U1.p, co, eo, fuse_pred ? &pa : nullptr);
+    });
     // stage 3: fine ha = 1/3 ha + 2/3 hc + (2/3 delta) d; acc3 += d, and on
     // the last substep the interface correction (:542-553, :231-274).
     if (!fuse_pred)
       for (auto* c : cs) launch_predict(c, 3, k, M, c->H2.p, c->U2.p);
-    exchange(cs, &C::H2, &C::U2, kMaskSub);
-    for (auto* c : cs) {
+    exchange_eval(cs, &C::H2, &C::U2, kMaskSub, [&](mswm_cuda_ctx* c, const MaskPlan& p) {
       const PredArgs pa = make_pred(c, 3, k, M, c->H2.p, c->U2.p);
       const double cr = two3 * delta;
       Op co[2], eo[2];
@@ -1540,8 +1644,8 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
         eo[1] = mk_op(OP_ACC_CORR, c->U.p, c->S0u.p, delta, nullptr, 1.0 / 6.0, two3, c->A3u.p,
                       first, c->A1u.p, c->A2u.p);
       }
-      launch_eval(c, plan_for(c, kMaskSub), c->H2.p, c->U2.p, co, eo, fuse_pred ? &pa : nullptr);
-    }
+      launch_eval(c, p, c->H2.p, c->U2.p, co, eo, fuse_pred ? &pa : nullptr);
+    });
   }
   // Step 4 (:557-563): coarse h = 1/3 h_old + 2/3 h2 + (2/3 dt) dh, in place.
   // With full halos the H2/U2 copies are current (the last exchange
@@ -1795,6 +1899,14 @@ mswm_cuda_ctx::Graph capture_step(std::vector<mswm_cuda_ctx*>& cs, cudaStream_t 
       plan_for(c, kMaskSub);
       plan_for(c, kMaskCoarseOnly);
       if (scheme == MSWM_LTS3) prepare_fork(c);
+      prepare_overlap(c);
+      if (c->halo.active() && scheme == MSWM_LTS3) {
+        // part plans are built outside the capture too
+        for (unsigned m : {kMaskStep1, kMaskIfCoarse, kMaskSub}) {
+          plan_part(c, m, 1);
+          plan_part(c, m, 2);
+        }
+      }
     } else {
       plan_for(c, MSWM_MASK_ALL);
     }
