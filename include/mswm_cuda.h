@@ -311,6 +311,13 @@ int mswm_cuda_group_create(mswm_cuda_ctx* const* members, int n,
 void mswm_cuda_group_destroy(mswm_cuda_group* group);
 int mswm_cuda_group_step(mswm_cuda_group* group, int scheme, double dt, int M,
                          int64_t n_steps);
+/* Group halo copies through NCCL instead of device copies: a one-rank
+ * communicator (two: the concurrent coarse step has its own) on the group's
+ * device, every copy an ncclSend to self matched by the ncclRecv issued
+ * after it -- the NCCL transport's calls, buffers and graph capture,
+ * exercised on one GPU without kernels that wait on one another. */
+int mswm_cuda_group_nccl_loopback(mswm_cuda_group* g);
+
 const char* mswm_cuda_group_last_error(const mswm_cuda_group* group);
 
 #ifdef __cplusplus

@@ -177,6 +177,7 @@ def cuda() -> C.CDLL:
             "mswm_cuda_group_create": (C.c_int, [C.POINTER(vp), C.c_int, C.POINTER(vp)]),
             "mswm_cuda_group_destroy": (None, [vp]),
             "mswm_cuda_group_step": (C.c_int, [vp, C.c_int, C.c_double, C.c_int, C.c_int64]),
+            "mswm_cuda_group_nccl_loopback": (C.c_int, [vp]),
             "mswm_cuda_group_last_error": (C.c_char_p, [vp]),
         }
         for name, (res, args) in sig.items():

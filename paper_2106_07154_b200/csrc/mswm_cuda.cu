@@ -239,6 +239,9 @@ struct mswm_cuda_ctx {
   std::map<unsigned, Halo> halo_mask;
   ncclComm_t nccl_comm = nullptr;
   ncclComm_t nccl_comm2 = nullptr;  // the concurrent coarse step's exchanges (ncclCommSplit)
+  // in-process group over a one-rank NCCL communicator (owned by the group,
+  // mswm_cuda_group_nccl_loopback): halo copies as NCCL send/recv to self
+  ncclComm_t loop_comm = nullptr, loop_comm2 = nullptr;
   std::string last_error;
   int32_t nC = 0, nE = 0, nV = 0, deg_max = 0, sten_max = 0;
   bool identity = true;
@@ -1367,6 +1370,28 @@ void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us, unsigned ma
       if (x.rcnt[j])
         nccl_check(nccl().Recv(x.rbuf.p + x.roff[j], size_t(x.rcnt[j]), ncclFloat64, x.peer[j],
                                comm, c->ls));
+    }
+    nccl_check(nccl().GroupEnd());
+  } else if (cs[0]->loop_comm) {
+    // in-process group over a one-rank communicator: every halo copy is an
+    // NCCL send to self matched, in issue order, by the receive after it --
+    // the NCCL transport's calls, buffers and graph capture on one GPU
+    ncclComm_t comm = second_comm ? cs[0]->loop_comm2 : cs[0]->loop_comm;
+    nccl_check(nccl().GroupStart());
+    for (auto* c : cs) {
+      Halo& x = halo_for(c, mask);
+      for (size_t j = 0; j < x.peer.size(); ++j) {
+        if (!x.rcnt[j]) continue;
+        mswm_cuda_ctx* src = cs[x.peer[j]];
+        const Halo& y = halo_for(src, mask);
+        size_t k = 0;
+        while (k < y.peer.size() && y.peer[k] != c->rank) ++k;
+        if (k == y.peer.size() || y.scnt[k] != x.rcnt[j])
+          throw Error(MSWM_E_USAGE, "inconsistent halo plans between ranks " +
+                                        std::to_string(c->rank) + " and " + std::to_string(x.peer[j]));
+        nccl_check(nccl().Send(y.sbuf.p + y.soff[k], size_t(x.rcnt[j]), ncclFloat64, 0, comm, c->ls));
+        nccl_check(nccl().Recv(x.rbuf.p + x.roff[j], size_t(x.rcnt[j]), ncclFloat64, 0, comm, c->ls));
+      }
     }
     nccl_check(nccl().GroupEnd());
   } else {
@@ -2763,6 +2788,7 @@ int mswm_cuda_comm_init(mswm_cuda_ctx* c, const void* unique_id, int rank, int n
 struct mswm_cuda_group {
   std::vector<mswm_cuda_ctx*> members;
   cudaStream_t stream = nullptr;
+  ncclComm_t loop = nullptr, loop2 = nullptr;  // one-rank communicators (nccl_loopback)
   std::map<std::tuple<int, double, int>, mswm_cuda_ctx::Graph> graphs;
   std::vector<uint64_t> gens;  // members' configuration generations the graphs were captured at
   std::string last_error;
@@ -2772,6 +2798,9 @@ struct mswm_cuda_group {
   }
   ~mswm_cuda_group() {
     drop_graphs();
+    if (stream) cudaStreamSynchronize(stream);
+    if (loop2) nccl().CommDestroy(loop2);
+    if (loop) nccl().CommDestroy(loop);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -2790,6 +2819,7 @@ int mswm_cuda_group_create(mswm_cuda_ctx* const* members, int n, mswm_cuda_group
         throw Error(MSWM_E_USAGE, "group members must share a device");
       g->members.push_back(members[r]);
     }
+    for (auto* c : g->members) c->loop_comm = c->loop_comm2 = nullptr;  // a previous group's
     CK(cudaSetDevice(members[0]->device));
     CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
   } catch (const Error& e) {
@@ -2843,6 +2873,30 @@ int mswm_cuda_group_step(mswm_cuda_group* g, int scheme, double dt, int M, int64
       c->steps_issued += n_steps;
       check_dry(c, ("rank " + std::to_string(c->rank)).c_str());
     }
+    return int(MSWM_OK);
+  });
+  if (rc) g->last_error = c0->last_error;
+  return rc;
+}
+
+int mswm_cuda_group_nccl_loopback(mswm_cuda_group* g) {
+  if (!g) return MSWM_E_USAGE;
+  mswm_cuda_ctx* c0 = g->members[0];
+  const int rc = guard(c0, [&] {
+    CK(cudaSetDevice(c0->device));
+    if (!g->loop) {
+      ncclUniqueId id1, id2;
+      nccl_check(nccl().GetUniqueId(&id1));
+      nccl_check(nccl().CommInitRank(&g->loop, 1, id1, 0));
+      nccl_check(nccl().GetUniqueId(&id2));
+      nccl_check(nccl().CommInitRank(&g->loop2, 1, id2, 0));
+    }
+    for (auto* c : g->members) {
+      c->loop_comm = g->loop;
+      c->loop_comm2 = g->loop2;
+      c->drop_graphs();
+    }
+    g->drop_graphs();
     return int(MSWM_OK);
   });
   if (rc) g->last_error = c0->last_error;

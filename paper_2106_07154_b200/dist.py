@@ -220,6 +220,13 @@ class CudaGroup:
                 send = {q: needs[q].get(r, np.zeros(0, np.int32)) for q in needs[r]}
                 rc.set_halo_mask(int(m), send, needs[r])
 
+    def use_nccl_loopback(self):
+        """Halo copies as NCCL send/recv to self over a one-rank communicator
+        (the NCCL transport's code path on one GPU)."""
+        rc = self.lib.mswm_cuda_group_nccl_loopback(self.handle)
+        if rc:
+            _raise(rc, self.lib.mswm_cuda_group_last_error(self.handle).decode())
+
     def advance(self, scheme, dt: float, substeps: int = 1, n_steps: int = 1):
         rc = self.lib.mswm_cuda_group_step(self.handle, int(scheme), float(dt), int(substeps),
                                            int(n_steps))

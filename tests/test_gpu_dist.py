@@ -124,3 +124,32 @@ def test_group_concurrent_coarse_step_bitwise(fork, overlap, n_ranks, M, monkeyp
     for rc in ranks:
         rc.download_owned(h, u)
     assert bits_equal(h, h_ref) and bits_equal(u, u_ref)
+
+
+@pytest.mark.parametrize("scheme", [Scheme.LTS3, Scheme.RK4])
+def test_group_over_nccl_loopback_bitwise(scheme):
+    """The halo copies of a 3-rank group as NCCL send/recv (to self, over
+    one-rank communicators: the NCCL transport's calls, buffers and graph
+    capture on one GPU), with the concurrent coarse step on the second
+    communicator and the interior / boundary overlap: bitwise the oracle."""
+    wl = W.small_sphere(6, seed=43, cap_deg=25.0)
+    o = Oracle(wl.mesh, wl.b, wl.f, wl.gravity)
+    o.set_regions(wl.fine_mask, wl.width)
+    cl, cs, el = o.labels()
+    dt = wl.dt if scheme == Scheme.LTS3 else wl.dt / wl.M
+    h_ref, u_ref, _ = o.step(int(scheme), wl.h, wl.u, 0.0, dt, wl.M, 3)
+    lay = DistributedLayout(wl.mesh, cl, cs, el, 3)
+    ranks = [RankContext(lay, r, wl.b, wl.f, wl.gravity) for r in range(3)]
+    grp = CudaGroup(ranks)
+    grp.use_nccl_loopback()
+    grp.restrict_halos(LTS3_MASKS + [kMaskAll])
+    for rc in ranks:
+        rc.upload(wl.h, wl.u)
+    grp.advance(scheme, dt, wl.M, 3)
+    if scheme == Scheme.LTS3:
+        assert all(rc.ctx.concurrent_coarse() == 1 for rc in ranks)
+    h = np.full(wl.mesh.n_cells, np.nan)
+    u = np.full(wl.mesh.n_edges, np.nan)
+    for rc in ranks:
+        rc.download_owned(h, u)
+    assert bits_equal(h, h_ref) and bits_equal(u, u_ref)
