@@ -155,6 +155,10 @@ struct MaskPlan {
   bool io_ready = false, io_full_c = false, io_full_e = false;
   std::vector<int32_t> io_rc_orig, io_re_orig;
   DArr<int32_t> io_rc, io_re;
+  // outputs in ascending original id (the host scatter streams): original
+  // ids on the host, internal ids on the device
+  std::vector<int32_t> io_oc_orig, io_oe_orig;
+  DArr<int32_t> io_oc, io_oe;
 };
 
 // Halo exchange plan of one rank: per peer slot, the owned values it sends
@@ -290,6 +294,7 @@ struct mswm_cuda_ctx {
   bool bnd_ready = false;
   DArr<uint8_t> cbnd, ebnd;
   cudaStream_t lx = nullptr;         // halo exchanges overlapping the interior evaluation
+  int overlap_level = 0;             // 1: steps 1-2, 2: every evaluation (MSWM_OVERLAP)
   cudaEvent_t ev_x0 = nullptr, ev_x1 = nullptr;
   cudaStream_t stream_of_capture = nullptr;
   DArr<int32_t> d_c_n2o, d_e_n2o;  // internal -> original ids (device permutes)
@@ -1429,12 +1434,18 @@ void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us, unsigned ma
 // hides behind the interior work.  Both parts are pure functions of their
 // inputs, so the split changes no bits.  `eval(c, plan)` launches one
 // member's evaluation with its fused stage update.
+// The split costs a launch-latency floor for the boundary part (~10 us per
+// evaluation, measured on the 8-way C4 partition, scripts/rank_timing.py),
+// about what it hides of a small exchange: it pays on the large
+// evaluations (steps 1 and 2, big_eval) and is used for the substeps only
+// with MSWM_OVERLAP=2.
 template <class F>
-void exchange_eval(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us, unsigned mask, F&& eval) {
+void exchange_eval(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us, unsigned mask,
+                   bool big_eval, F&& eval) {
   bool halos = false;
   for (auto* c : cs) halos |= c->halo.active();
   mswm_cuda_ctx* const c0 = cs[0];
-  if (!halos || !c0->lx) {
+  if (!halos || !c0->lx || (!big_eval && c0->overlap_level < 2)) {
     exchange(cs, hs, us, mask);
     for (auto* c : cs) eval(c, plan_for(c, mask));
     return;
@@ -1455,6 +1466,7 @@ void prepare_overlap(mswm_cuda_ctx* c) {
   if (!c->halo.active() || c->lx) return;
   const char* e = std::getenv("MSWM_OVERLAP");
   if (e && e[0] == '0') return;
+  c->overlap_level = (e && e[0] == '2') ? 2 : 1;
   int lo = 0, hi = 0;
   CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   CK(cudaStreamCreateWithPriority(&c->lx, cudaStreamNonBlocking, hi));
@@ -1562,14 +1574,14 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
   const double third = 1.0 / 3.0, two3 = 2.0 / 3.0;
   using C = mswm_cuda_ctx;
   // Step 1 (:483-487): h1 = h_old + dt*dh on UF1 u UF2 u I1 u I2 u C.
-  exchange_eval(cs, &C::H, &C::U, kMaskStep1, [&](mswm_cuda_ctx* c, const MaskPlan& p) {
+  exchange_eval(cs, &C::H, &C::U, kMaskStep1, true, [&](mswm_cuda_ctx* c, const MaskPlan& p) {
     double *H = c->H.p, *U = c->U.p, *H1 = c->H1.p, *U1 = c->U1.p;
     Op co[2] = {mk_op(OP_EULER, H1, H, dt), mk_op(OP_EULER, H1, H, dt)};
     Op eo[2] = {mk_op(OP_EULER, U1, U, dt), mk_op(OP_EULER, U1, U, dt)};
     launch_eval(c, p, H, U, co, eo);
   });
   // Step 2 (:491-500): h2 = 0.75 h_old + 0.25 h1 + (0.25 dt) dh on I u C.
-  exchange_eval(cs, &C::H1, &C::U1, kMaskIfCoarse, [&](mswm_cuda_ctx* c, const MaskPlan& p) {
+  exchange_eval(cs, &C::H1, &C::U1, kMaskIfCoarse, true, [&](mswm_cuda_ctx* c, const MaskPlan& p) {
     double *H = c->H.p, *U = c->U.p, *H1 = c->H1.p, *U1 = c->U1.p, *H2 = c->H2.p, *U2 = c->U2.p;
     const double cr = 0.25 * dt;
     Op co[2] = {mk_op(OP_WCOMB, H2, H, 0.75, H1, 0.25, cr), mk_op(OP_WCOMB, H2, H, 0.75, H1, 0.25, cr)};
@@ -1630,7 +1642,7 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
     // has to propagate them first (multi-rank)
     if (k > 0 && !fuse_pred)
       for (auto* c : cs) launch_predict(c, 1, k, M, c->H.p, c->U.p);
-    exchange_eval(cs, &C::H, &C::U, kMaskSub, [&](mswm_cuda_ctx* c, const MaskPlan& p) {
+    exchange_eval(cs, &C::H, &C::U, kMaskSub, false, [&](mswm_cuda_ctx* c, const MaskPlan& p) {
       const PredArgs pa = make_pred(c, 1, k, M, c->H.p, c->U.p);
       Op co[2] = {mk_op(OP_EULER, c->H1.p, c->H.p, delta),
                   mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A1h.p, first)};
@@ -1641,7 +1653,7 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
     // stage 2: fine hc = 0.75 ha + 0.25 hb + (0.25 delta) d; acc2 += d   (:532-541)
     if (!fuse_pred)
       for (auto* c : cs) launch_predict(c, 2, k, M, c->H1.p, c->U1.p);
-    exchange_eval(cs, &C::H1, &C::U1, kMaskSub, [&](mswm_cuda_ctx* c, const MaskPlan& p) {
+    exchange_eval(cs, &C::H1, &C::U1, kMaskSub, false, [&](mswm_cuda_ctx* c, const MaskPlan& p) {
       const PredArgs pa = make_pred(c, 2, k, M, c->H1.p, c->U1.p);
       const double cr = 0.25 * delta;
       Op co[2] = {mk_op(OP_WCOMB, c->H2.p, c->H.p, 0.75, c->H1.p, 0.25, cr),
@@ -1654,7 +1666,7 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
     // the last substep the interface correction (:542-553, :231-274).
     if (!fuse_pred)
       for (auto* c : cs) launch_predict(c, 3, k, M, c->H2.p, c->U2.p);
-    exchange_eval(cs, &C::H2, &C::U2, kMaskSub, [&](mswm_cuda_ctx* c, const MaskPlan& p) {
+    exchange_eval(cs, &C::H2, &C::U2, kMaskSub, false, [&](mswm_cuda_ctx* c, const MaskPlan& p) {
       const PredArgs pa = make_pred(c, 3, k, M, c->H2.p, c->U2.p);
       const double cr = two3 * delta;
       Op co[2], eo[2];
@@ -2257,6 +2269,16 @@ void build_eval_io(mswm_cuda_ctx* c, MaskPlan& p) {
   p.io_full_e = 2 * ei.size() > size_t(c->nE);
   if (!p.io_full_c && !ci.empty()) p.io_rc.upload(ci, s);
   if (!p.io_full_e && !ei.empty()) p.io_re.upload(ei, s);
+  auto sorted_out = [&](const std::vector<int32_t>& orig, const std::vector<int32_t>& o2n,
+                        std::vector<int32_t>& so, DArr<int32_t>& dev) {
+    so = orig;
+    std::sort(so.begin(), so.end());
+    std::vector<int32_t> ni(so.size());
+    for (size_t k = 0; k < so.size(); ++k) ni[k] = c->identity ? so[k] : o2n[so[k]];
+    if (!ni.empty()) dev.upload(ni, s);
+  };
+  sorted_out(p.host_cells, c->c_old2new, p.io_oc_orig, p.io_oc);
+  sorted_out(p.host_edges, c->e_old2new, p.io_oe_orig, p.io_oe);
   CK(cudaStreamSynchronize(s));
   p.io_ready = true;
 }
@@ -2311,17 +2333,17 @@ int mswm_cuda_eval(mswm_cuda_ctx* c, const double* h, const double* u, unsigned 
     // untouched (integrators.hpp:63-67)
     if (nout > 0) {
       if (p.nc)
-        k_gather_perm<<<nblk(int64_t(p.nc)), kBlock, 0, s>>>(p.nc, p.cells, c->Dh.p, c->io_pack.p);
+        k_gather_perm<<<nblk(int64_t(p.nc)), kBlock, 0, s>>>(p.nc, p.io_oc.p, c->Dh.p, c->io_pack.p);
       if (p.ne)
-        k_gather_perm<<<nblk(int64_t(p.ne)), kBlock, 0, s>>>(p.ne, p.edges, c->Du.p,
+        k_gather_perm<<<nblk(int64_t(p.ne)), kBlock, 0, s>>>(p.ne, p.io_oe.p, c->Du.p,
                                                              c->io_pack.p + p.nc);
       CK(cudaGetLastError());
       CK(cudaMemcpyAsync(c->pin, c->io_pack.p, nout * 8, cudaMemcpyDeviceToHost, s));
     }
     CK(cudaStreamSynchronize(s));
     check_dry(c);
-    for (int32_t k = 0; k < p.nc; ++k) dh[p.host_cells[k]] = c->pin[k];
-    for (int32_t k = 0; k < p.ne; ++k) du[p.host_edges[k]] = c->pin[p.nc + k];
+    for (int32_t k = 0; k < p.nc; ++k) dh[p.io_oc_orig[k]] = c->pin[k];
+    for (int32_t k = 0; k < p.ne; ++k) du[p.io_oe_orig[k]] = c->pin[p.nc + k];
     return int(MSWM_OK);
   });
 }

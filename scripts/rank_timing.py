@@ -57,6 +57,11 @@ def main():
     rm = g.make_regions(wl.fine_mask, wl.width)
     g.upload(State(wl.h, wl.u, 0.0))
     t_single = time_steps(g, wl, steps)
+    g.set_profiling(1)
+    g.advance(Scheme.LTS3, wl.dt, wl.M, 2)
+    ms1, nc1, ne1 = g.eval_profile()
+    single_evals = {"ms": [round(float(x), 4) for x in ms1], "cells": [int(x) for x in nc1],
+                    "edges": [int(x) for x in ne1]}
     g.close()
     del g
     lay = DistributedLayout(wl.mesh, rm.cell_label, rm.cell_sublabel, rm.edge_label, n)
@@ -87,7 +92,7 @@ def main():
               for m in masks}
     print(json.dumps({
         "config": cfg, "n_ranks": n, "steps": steps, "single_ms_per_step": t_single,
-        "rank_ms_per_step": per_rank, "max_rank_ms": max(per_rank),
+        "single_evals": single_evals, "rank_ms_per_step": per_rank, "max_rank_ms": max(per_rank),
         "ideal_ms": t_single / n, "compute_efficiency": t_single / (n * max(per_rank)),
         "concurrent_coarse": fork, "evals_per_rank": evals, "owned_cells": [rc.lm.n_owned_cells for rc in ranks],
         "local_cells": [rc.lm.n_cells for rc in ranks],

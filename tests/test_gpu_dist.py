@@ -93,15 +93,15 @@ def test_group_restricted_halos_bitwise(n_ranks, scheme):
     assert bits_equal(h, h_ref) and bits_equal(u, u_ref)
 
 
-@pytest.mark.parametrize("overlap", ["1", "0"])
+@pytest.mark.parametrize("overlap", ["2", "1", "0"])
 @pytest.mark.parametrize("fork", ["1", "0"])
 @pytest.mark.parametrize("n_ranks,M", [(2, 4), (3, 2), (4, 4)])
 def test_group_concurrent_coarse_step_bitwise(fork, overlap, n_ranks, M, monkeypatch):
     """The coarse stage on its own stream with its own (restricted) halo
     exchange, concurrent with the substeps and their exchanges, on every
     rank; and every other exchange on a side stream while the interior
-    outputs evaluate (MSWM_OVERLAP=1, the boundary outputs after the halo
-    lands): bitwise equal to the oracle over several coarse steps, and to
+    outputs evaluate (MSWM_OVERLAP=1: steps 1 and 2, 2: every evaluation;
+    the boundary outputs after the halo lands): bitwise equal to the oracle over several coarse steps, and to
     the sequential schedule (MSWM_FORK=0, MSWM_OVERLAP=0)."""
     monkeypatch.setenv("MSWM_FORK", fork)
     monkeypatch.setenv("MSWM_OVERLAP", overlap)
