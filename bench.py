@@ -415,7 +415,7 @@ def run_ours(args, ws, rank, local):
             wl0 = make_workload(args.config, args.level)
             log(f"[rank 0] workload {args.config}: {wl0.mesh.n_cells} cells, built in "
                 f"{time.time() - t0:.1f}s")
-            publish_store(store_dir, wl0, device=local)
+            publish_store(store_dir, wl0, device=local, n_ranks=ws)
             del wl0
         barrier(ws)
         t1 = time.time()

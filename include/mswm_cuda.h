@@ -261,6 +261,15 @@ int mswm_cuda_courant(mswm_cuda_ctx* ctx, double dt, int M, double* fine,
  * refreshed before every evaluation (the device form of ThreadedEvaluator's
  * per-eval copy-in, rank_pool.cpp:133-135). */
 
+/* Halo plan of a partition on the device (make_block_plan's 2-hop halo,
+ * partition.cpp:355-392, for every rank at once): for each cell / edge /
+ * vertex (caller ids) the bit set of the ranks whose local mesh -- owned
+ * cells plus the cells within two hops, their ring edges and vertices --
+ * holds it.  rank_of_cell[nC] in [0, n_ranks), n_ranks <= 64; null outputs
+ * are skipped. */
+int mswm_cuda_halo_reach(mswm_cuda_ctx* ctx, const int32_t* rank_of_cell, int n_ranks,
+                         uint64_t* cell_reach, uint64_t* edge_reach, uint64_t* vertex_reach);
+
 /* Region labels from the global RegionMap (regions.hpp:27-29 values),
  * indexed by local ids; outputs restricted to cell_owned / edge_owned
  * (NULL = all).  Replaces mswm_cuda_set_regions on a rank context. */

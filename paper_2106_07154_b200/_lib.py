@@ -22,6 +22,7 @@ i8p = C.POINTER(C.c_int8)
 f64p = C.POINTER(C.c_double)
 u8p = C.POINTER(C.c_uint8)
 i64p = C.POINTER(C.c_int64)
+u64p = C.POINTER(C.c_uint64)
 
 
 class MeshDesc(C.Structure):
@@ -177,6 +178,7 @@ def cuda() -> C.CDLL:
             "mswm_cuda_group_create": (C.c_int, [C.POINTER(vp), C.c_int, C.POINTER(vp)]),
             "mswm_cuda_group_destroy": (None, [vp]),
             "mswm_cuda_group_step": (C.c_int, [vp, C.c_int, C.c_double, C.c_int, C.c_int64]),
+            "mswm_cuda_halo_reach": (C.c_int, [vp, i32p, C.c_int, u64p, u64p, u64p]),
             "mswm_cuda_group_nccl_loopback": (C.c_int, [vp]),
             "mswm_cuda_group_last_error": (C.c_char_p, [vp]),
         }

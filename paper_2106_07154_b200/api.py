@@ -383,6 +383,21 @@ class CudaContext:
         self._check(self.lib.mswm_cuda_kernels_per_step(self.handle, C.byref(n)))
         return n.value
 
+    def halo_reach(self, rank_of_cell, n_ranks: int):
+        """Device halo plan of a partition (partition.cpp:355-392): uint64 bit
+        sets of the ranks whose local mesh holds each cell / edge / vertex."""
+        m = self.mesh
+        r = np.ascontiguousarray(rank_of_cell, np.int32)
+        if r.shape != (m.n_cells,):
+            raise UsageError(f"rank_of_cell must have shape ({m.n_cells},)")
+        cr = np.zeros(m.n_cells, np.uint64)
+        er = np.zeros(m.n_edges, np.uint64)
+        vr = np.zeros(m.n_vertices, np.uint64)
+        self._check(self.lib.mswm_cuda_halo_reach(self.handle, _p(r, _lib.i32p), int(n_ranks),
+                                                  _p(cr, _lib.u64p), _p(er, _lib.u64p),
+                                                  _p(vr, _lib.u64p)))
+        return cr, er, vr
+
     def set_replication(self, replication: int) -> None:
         """Cost replication (SchemeConfig::replication): the tendency
         arithmetic repeated per evaluation (operators.cpp:60), results

@@ -671,6 +671,36 @@ __global__ void k_mark_closure(DevMesh M, const int32_t* __restrict__ c_vert,
   }
 }
 
+// Halo plan of a partition (make_block_plan's 2-hop rule, partition.cpp:
+// 355-392) for every rank at once: reach[c] = bit set of the ranks whose
+// local mesh (owned cells + cells within two hops) holds c.  One OR over the
+// ring neighbours per hop; an edge / vertex belongs to the local mesh of every
+// rank that holds one of its cells.
+__global__ void k_reach_init(int32_t nC, const int32_t* __restrict__ rank_of_cell,
+                             uint64_t* __restrict__ reach) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nC) reach[i] = uint64_t(1) << rank_of_cell[i];
+}
+__global__ void k_reach_hop(DevMesh M, const int32_t* __restrict__ c_nbr,
+                            const uint64_t* __restrict__ in, uint64_t* __restrict__ out) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M.nC) return;
+  uint64_t r = in[i];
+  for (int j = 0; j < M.c_deg[i]; ++j) r |= in[c_nbr[j * M.nC + i]];
+  out[i] = r;
+}
+__global__ void k_reach_ev(DevMesh M, const uint64_t* __restrict__ cr, uint64_t* __restrict__ er,
+                           uint64_t* __restrict__ vr) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < M.nE) {
+    const int2 c = M.e_cells[t];
+    er[t] = cr[c.x] | cr[c.y];
+  } else if (t - M.nE < M.nV) {
+    const int32_t v = t - M.nE;
+    vr[v] = cr[M.v_cell[v]] | cr[M.v_cell[M.nV + v]] | cr[M.v_cell[2 * M.nV + v]];
+  }
+}
+
 // Halo dependence of a rank's evaluations (interior / boundary split of the
 // multi-rank schedule).  A halo element is one this rank does not own
 // (key 0xFF); every value computed from one is "tainted".

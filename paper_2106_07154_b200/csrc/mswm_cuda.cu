@@ -2587,6 +2587,46 @@ int mswm_cuda_courant(mswm_cuda_ctx* c, double dt, int M, double* fine, double* 
 
 // ---- multi-rank --------------------------------------------------------------
 
+int mswm_cuda_halo_reach(mswm_cuda_ctx* c, const int32_t* rank_of_cell, int n_ranks,
+                         uint64_t* cell_reach, uint64_t* edge_reach, uint64_t* vertex_reach) {
+  return guard(c, [&] {
+    check_ctx(c);
+    if (!rank_of_cell) throw Error(MSWM_E_USAGE, "rank_of_cell is null");
+    if (n_ranks < 1 || n_ranks > 64) throw Error(MSWM_E_USAGE, "n_ranks must lie in [1, 64]");
+    cudaStream_t s = c->stream;
+    std::vector<int32_t> r(c->nC);
+    for (int32_t ni = 0; ni < c->nC; ++ni) {
+      const int32_t q = rank_of_cell[c->identity ? ni : c->c_new2old[ni]];
+      if (q < 0 || q >= n_ranks) throw Error(MSWM_E_USAGE, "rank out of range");
+      r[ni] = q;
+    }
+    DArr<int32_t> dr;
+    dr.upload(r, s);
+    DArr<uint64_t> a, b, er, vr;
+    a.alloc(c->nC);
+    b.alloc(c->nC);
+    er.alloc(c->nE);
+    vr.alloc(c->nV);
+    const DevMesh M = c->dev();
+    k_reach_init<<<nblk(c->nC), kBlock, 0, s>>>(c->nC, dr.p, a.p);
+    k_reach_hop<<<nblk(c->nC), kBlock, 0, s>>>(M, c->c_nbr.p, a.p, b.p);
+    k_reach_hop<<<nblk(c->nC), kBlock, 0, s>>>(M, c->c_nbr.p, b.p, a.p);
+    k_reach_ev<<<nblk(int64_t(c->nE) + c->nV), kBlock, 0, s>>>(M, a.p, er.p, vr.p);
+    CK(cudaGetLastError());
+    auto down = [&](const DArr<uint64_t>& d, uint64_t* out, int32_t n, const std::vector<int32_t>& n2o) {
+      if (!out) return;
+      std::vector<uint64_t> h(n);
+      CK(cudaMemcpyAsync(h.data(), d.p, size_t(n) * 8, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (int32_t k = 0; k < n; ++k) out[c->identity ? k : n2o[k]] = h[k];
+    };
+    down(a, cell_reach, c->nC, c->c_new2old);
+    down(er, edge_reach, c->nE, c->e_new2old);
+    down(vr, vertex_reach, c->nV, c->v_new2old);
+    return int(MSWM_OK);
+  });
+}
+
 int mswm_cuda_set_labels(mswm_cuda_ctx* c, const uint8_t* cell_label, const uint8_t* cell_sub,
                          const uint8_t* edge_label, const uint8_t* cell_owned,
                          const uint8_t* edge_owned, int interface_width) {

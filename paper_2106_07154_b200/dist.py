@@ -39,20 +39,26 @@ def swap_needs(rank: int, n_ranks: int, needs: dict) -> dict:
     return {int(q): allv[int(q)].get(rank, np.zeros(0, np.int32)) for q in needs}
 
 
-def publish_store(store_dir, wl, device: int = 0) -> dict:
-    """Rank 0 of a multi-GPU job: device region labels of the global mesh
-    (one global context, closed again), the locality order, then the whole
-    workload + labels written as a binary store (store.py) that every rank
-    memory-maps.  Returns the extra arrays written."""
+def publish_store(store_dir, wl, device: int = 0, n_ranks: int | None = None) -> dict:
+    """Rank 0 of a multi-GPU job: on one global context (closed again) the
+    device region labels of the global mesh and, for ``n_ranks``, the
+    partition's halo plan (halo_reach bit sets); then the whole workload,
+    labels, locality order and plan written as a binary store (store.py)
+    that every rank memory-maps.  Returns the extra arrays written."""
     from . import store
     g = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, device=device)
     rm = g.make_regions(wl.fine_mask, wl.width)
-    g.close()
-    del g
     extra = {"cell_label": np.asarray(rm.cell_label, np.uint8),
              "cell_sub": np.asarray(rm.cell_sublabel, np.uint8),
              "edge_label": np.asarray(rm.edge_label, np.uint8),
              "order": np.asarray(wl.mesh.locality_order(), np.int32)}
+    if n_ranks:
+        roc = partition_cells(extra["order"], extra["cell_label"], n_ranks)
+        cr, er, vr = g.halo_reach(roc, n_ranks)
+        extra.update({"rank_of_cell": roc, "cell_reach": cr, "edge_reach": er,
+                      "vertex_reach": vr})
+    g.close()
+    del g
     store.save_workload(store_dir, wl, extra, digest=False)
     return extra
 
@@ -63,8 +69,11 @@ def layout_from_store(store_dir, rank: int, n_ranks: int):
     local mesh and halo plan are materialised."""
     from . import store
     wl, extra = store.load_workload(store_dir, mmap=True)
+    reach = None
+    if "cell_reach" in extra and int(np.max(extra["rank_of_cell"])) == n_ranks - 1:
+        reach = (extra["cell_reach"], extra["edge_reach"], extra["vertex_reach"])
     lay = DistributedLayout(wl.mesh, extra["cell_label"], extra["cell_sub"], extra["edge_label"],
-                            n_ranks, order=np.asarray(extra["order"]), only=rank)
+                            n_ranks, order=np.asarray(extra["order"]), only=rank, reach=reach)
     return wl, lay
 
 
@@ -72,7 +81,8 @@ class DistributedLayout:
     """Partition + local meshes of a global mesh with given region labels."""
 
     def __init__(self, mesh: Mesh, cell_label, cell_sub, edge_label, n_ranks: int,
-                 order: np.ndarray | None = None, only: int | None = None):
+                 order: np.ndarray | None = None, only: int | None = None, ctx=None,
+                 reach=None):
         self.mesh = mesh
         self.n_ranks = n_ranks
         self.cell_label = np.asarray(cell_label, np.uint8)
@@ -82,7 +92,8 @@ class DistributedLayout:
         self.rank_of_cell = partition_cells(self.order, self.cell_label, n_ranks)
         self.locals: list[LocalMesh] = build_local_meshes(mesh, self.cell_label, self.cell_sub,
                                                           self.edge_label, self.rank_of_cell,
-                                                          n_ranks, only=only)
+                                                          n_ranks, only=only, ctx=ctx,
+                                                          reach=reach)
         hr = np.empty(mesh.n_cells, np.int64)
         hr[self.order] = np.arange(mesh.n_cells)
         self.hilbert_rank = hr

@@ -124,43 +124,58 @@ class LocalMesh:
         return np.concatenate([x[self.vertices], [0.0]])
 
 
-def _two_hop(mesh: Mesh, seed_mask: np.ndarray) -> np.ndarray:
-    rows, nbr, _, _ = ring_neighbours(mesh)
-    m = seed_mask.copy()
+def halo_reach(mesh: Mesh, rank_of_cell: np.ndarray, n_ranks: int, ctx=None):
+    """Local-mesh membership of every rank at once (make_block_plan's 2-hop
+    halo, partition.cpp:355-392): uint64 bit sets per cell / edge / vertex of
+    the ranks whose local mesh (owned cells + cells within two hops, their
+    ring edges and ring vertices) holds it.  ``ctx`` (a CudaContext on the
+    mesh): computed on the device (mswm_cuda_halo_reach); else vectorised
+    on the host.  Two OR passes over the ring neighbours replace one BFS per
+    rank."""
+    if not 1 <= n_ranks <= 64:
+        raise ValueError("n_ranks must lie in [1, 64]")
+    if ctx is not None:
+        return ctx.halo_reach(rank_of_cell, n_ranks)
+    co = np.asarray(mesh.cell_offset, np.int64)
+    nbr = np.asarray(mesh.cell_cells)
+    r = np.left_shift(np.uint64(1), np.asarray(rank_of_cell, np.uint64))
     for _ in range(2):
-        hit = np.zeros(mesh.n_cells, bool)
-        hit[nbr[m[rows]]] = True
-        m |= hit
-    return m
+        r = r | np.bitwise_or.reduceat(r[nbr], co[:-1])
+    ec = np.asarray(mesh.edge_cells)
+    vc = np.asarray(mesh.vertex_cells)
+    return r, r[ec[:, 0]] | r[ec[:, 1]], r[vc[:, 0]] | r[vc[:, 1]] | r[vc[:, 2]]
+
+
+def _has(bits: np.ndarray, q: int) -> np.ndarray:
+    return (bits >> np.uint64(q)) & np.uint64(1) == np.uint64(1)
 
 
 def build_local_meshes(mesh: Mesh, cell_label, cell_sub, edge_label, rank_of_cell: np.ndarray,
-                       n_ranks: int, only: int | None = None) -> list:
-    """Local meshes and halo plans (host setup).  With ``only`` = r, the
-    tables are built for rank r alone (the others are None) -- what one
-    process of a multi-GPU run needs."""
+                       n_ranks: int, only: int | None = None, ctx=None, reach=None) -> list:
+    """Local meshes and halo plans.  With ``only`` = r, the tables are built
+    for rank r alone (the others are None) -- what one process of a
+    multi-GPU run needs.  The membership bit sets come from the device when
+    ``ctx`` (a CudaContext on ``mesh``) is given (halo_reach), or precomputed
+    as ``reach``."""
     own_e = edge_owner(mesh, cell_label, edge_label, rank_of_cell)
-    rows, nbr, redges, rverts = ring_neighbours(mesh)
     co = mesh.cell_offset
-    # local cell / edge sets of every rank (needed for the send lists)
-    sets = []
-    for r in range(n_ranks):
+    cr, er, vr = reach if reach is not None else halo_reach(mesh, rank_of_cell, n_ranks, ctx)
+
+    def sets_of(r):
         owned_c = rank_of_cell == r
-        lc_mask = _two_hop(mesh, owned_c)
-        e_mask = np.zeros(mesh.n_edges, bool)
-        e_mask[redges[lc_mask[rows]]] = True
         owned_e = own_e == r
+        e_mask = _has(er, r)
         if np.any(owned_e & ~e_mask):
             raise AssertionError("an owned edge is not a ring edge of a local cell")
-        sets.append((owned_c, lc_mask, owned_e, e_mask))
+        return owned_c, _has(cr, r), owned_e, e_mask
+
     build = range(n_ranks) if only is None else [only]
     out = [None] * n_ranks
     for r in build:
-        owned_c, lc_mask, owned_e, e_mask = sets[r]
+        owned_c, lc_mask, owned_e, e_mask = sets_of(r)
         # cells: owned first, then halo, each ascending
         cells = np.concatenate([np.nonzero(owned_c)[0], np.nonzero(lc_mask & ~owned_c)[0]])
-        v_mask = np.zeros(mesh.n_vertices, bool)
-        v_mask[rverts[lc_mask[rows]]] = True
+        v_mask = _has(vr, r)
         edges = np.concatenate([np.nonzero(owned_e)[0], np.nonzero(e_mask & ~owned_e)[0]])
         verts = np.nonzero(v_mask)[0]
         nC, nE, nV = len(cells) + 1, len(edges) + 1, len(verts) + 1
@@ -220,7 +235,8 @@ def build_local_meshes(mesh: Mesh, cell_label, cell_sub, edge_label, rank_of_cel
         for p in range(n_ranks):
             if p == r:
                 continue
-            p_owned_c, p_lc, p_owned_e, p_e = sets[p]
+            p_owned_c, p_lc = rank_of_cell == p, _has(cr, p)
+            p_owned_e, p_e = own_e == p, _has(er, p)
             rc_ = np.nonzero(lc_mask & p_owned_c)[0]
             re_ = np.nonzero(e_mask & p_owned_e)[0]
             sc_ = np.nonzero(owned_c & p_lc)[0]

@@ -153,3 +153,30 @@ def test_group_over_nccl_loopback_bitwise(scheme):
     for rc in ranks:
         rc.download_owned(h, u)
     assert bits_equal(h, h_ref) and bits_equal(u, u_ref)
+
+
+@pytest.mark.parametrize("n_ranks", [2, 5, 8])
+def test_device_halo_plan_equals_host(n_ranks):
+    """The partition's halo plan computed on the device (mswm_cuda_halo_reach:
+    2-hop reach bit sets of every rank at once, partition.cpp:355-392) equals
+    the host computation, and so do the local meshes built from it."""
+    from paper_2106_07154_b200.api import CudaContext
+    from paper_2106_07154_b200.partition import halo_reach, partition_cells
+    wl = W.small_sphere(6, seed=47, cap_deg=20.0)
+    o = Oracle(wl.mesh, wl.b, wl.f, wl.gravity)
+    o.set_regions(wl.fine_mask, wl.width)
+    cl, cs, el = o.labels()
+    order = wl.mesh.locality_order()
+    roc = partition_cells(order, cl, n_ranks)
+    ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order="hilbert")
+    dev = halo_reach(wl.mesh, roc, n_ranks, ctx)
+    host = halo_reach(wl.mesh, roc, n_ranks)
+    for a, b in zip(dev, host):
+        assert np.array_equal(a, b)
+    la = DistributedLayout(wl.mesh, cl, cs, el, n_ranks, order=order, ctx=ctx)
+    lb = DistributedLayout(wl.mesh, cl, cs, el, n_ranks, order=order)
+    for x, y in zip(la.locals, lb.locals):
+        assert np.array_equal(x.cells, y.cells) and np.array_equal(x.edges, y.edges)
+        assert all(np.array_equal(x.tables[k], y.tables[k]) for k in x.tables)
+        assert {q: v.tolist() for q, v in x.send_cells.items()} == \
+            {q: v.tolist() for q, v in y.send_cells.items()}
