@@ -63,7 +63,7 @@ def test_store_rejects_damage(tmp_path):
         store.load_workload(tmp_path / "s")
 
 
-def _shard_worker(rank, world, port, root, q):
+def _shard_worker(rank, world, port, root, q, with_reach=False):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -74,8 +74,15 @@ def _shard_worker(rank, world, port, root, q):
             # in for the device labelling (no GPU here)
             wl = W.small_sphere(5, seed=21, cap_deg=25.0)
             cl, cs, el = _labels(wl)
-            store.save_workload(root, wl, {"cell_label": cl, "cell_sub": cs, "edge_label": el,
-                                           "order": wl.mesh.locality_order()})
+            extra = {"cell_label": cl, "cell_sub": cs, "edge_label": el,
+                     "order": wl.mesh.locality_order()}
+            if with_reach:  # what publish_store adds from the device
+                from paper_2106_07154_b200.partition import halo_reach, partition_cells
+                roc = partition_cells(extra["order"], cl, world)
+                cr, er, vr = halo_reach(wl.mesh, roc, world)
+                extra.update({"rank_of_cell": roc, "cell_reach": cr, "edge_reach": er,
+                              "vertex_reach": vr})
+            store.save_workload(root, wl, extra)
         dist.barrier()
         wl, lay = layout_from_store(root, rank, world)
         lm = lay.locals[rank]
@@ -89,7 +96,8 @@ def _shard_worker(rank, world, port, root, q):
         dist.destroy_process_group()
 
 
-def test_rank_local_setup_from_store_gloo(tmp_path):
+@pytest.mark.parametrize("with_reach", [False, True])
+def test_rank_local_setup_from_store_gloo(tmp_path, with_reach):
     """world_size 2: rank 0 publishes the store, each rank builds only its
     own local mesh + halo plan from the shared maps; both equal the
     single-process DistributedLayout."""
@@ -98,7 +106,8 @@ def test_rank_local_setup_from_store_gloo(tmp_path):
     q = ctx.Queue()
     port = _free_port()
     root = str(tmp_path / "store")
-    ps = [ctx.Process(target=_shard_worker, args=(r, world, port, root, q)) for r in range(world)]
+    ps = [ctx.Process(target=_shard_worker, args=(r, world, port, root, q, with_reach))
+          for r in range(world)]
     for p in ps:
         p.start()
     got = [q.get(timeout=300) for _ in range(world)]
