@@ -204,10 +204,9 @@ int mswm_cuda_eval_profile(mswm_cuda_ctx* ctx, float* eval_ms,
                            int64_t* out_cells, int64_t* out_edges, int cap,
                            int* n);
 
-/* Output kernel: kernel_path 0 = k_out over the explicit stencil tables;
- * 1 = the contiguous range of each evaluation's edge outputs through
- * k_out_bulk (the same tables streamed into shared memory by bulk copies,
- * MSWM_BULK=1 at create), the rest through k_out.
+/* Output kernel: kernel_path 0 = k_out over the explicit stencil tables
+ * (the only output kernel; profiles/r2_phaseC_experiments.json records the
+ * variants measured slower and removed).
  * identity_order = 1 when the internal numbering equals the caller's. */
 int mswm_cuda_layout_info(const mswm_cuda_ctx* ctx, int* kernel_path,
                           int* identity_order);

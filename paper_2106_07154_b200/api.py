@@ -369,7 +369,7 @@ class CudaContext:
     def layout_info(self) -> dict:
         kp, ident = C.c_int(0), C.c_int(0)
         self._check(self.lib.mswm_cuda_layout_info(self.handle, C.byref(kp), C.byref(ident)))
-        return {"kernel_path": {0: "explicit", 1: "bulk"}[kp.value],
+        return {"kernel_path": {0: "explicit"}[kp.value],
                 "input_order": bool(ident.value)}
 
     def stencil_info(self) -> dict:

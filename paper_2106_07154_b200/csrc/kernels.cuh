@@ -434,229 +434,6 @@ __global__ void MSWM_KOUT_BOUNDS k_out(DevMesh M, const double* __restrict__ h,
 }
 
 // ---------------------------------------------------------------------------
-// Phase C, edge outputs over a contiguous range, with the per-edge tables
-// streamed by the copy engine (k_out_bulk).  One producer warp issues, per
-// tile of kBT edges, the bulk copies (cp.async.bulk -> UBLKCP) of the
-// stencil-id words, coefficient pairs, edge cells, 1/d, stencil lengths,
-// group keys and the edges' own (F, q~) into a shared-memory ring whose
-// stages are handed over with mbarriers (expect_tx / complete_tx); the
-// consumer warps, one thread per edge, read their ids and coefficients from
-// shared memory and issue all (F, q~) and psi gathers at once -- the table
-// stream no longer sits in front of the gathers' dependency chain.  Same
-// per-element arithmetic as item_out_sp (operators.cpp:101-116): bitwise.
-constexpr int kBT = 256;     // edges per tile = consumer threads
-constexpr int kBStages = 2;  // ring depth
-constexpr int kBCopies = 12;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// One streamed array of a tile: a 16-byte-aligned window of global memory
-// copied to a 16-byte-aligned shared slot; `shift` bytes of lead-in.
-struct BulkSlot {
-  uint32_t off;    // shared offset of the slot within a stage
-  uint32_t bytes;  // slot capacity (kBT elements + 32 bytes)
-};
-__host__ __device__ constexpr uint32_t bslot(uint32_t elem) { return kBT * elem + 32; }
-// slot order: st16 x3 (8 B), coef x5 (16 B), cells (8), invd (8), own FQ (16), nst (1), key (1)
-__host__ __device__ constexpr uint32_t bulk_stage_bytes() {
-  return 3 * bslot(8) + 5 * bslot(16) + bslot(8) + bslot(8) + bslot(16) + bslot(1) + bslot(1);
-}
-
-struct BulkArgs {
-  int32_t base, n;  // edge range [base, base + n)
-};
-
-__device__ __forceinline__ uint32_t bulk_window(char* stage, uint32_t off, const void* gsrc,
-                                                int64_t elem_index, uint32_t elem, uint32_t count,
-                                                uint64_t* bar, uint32_t& shift) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(gsrc) + uintptr_t(elem_index) * elem;
-  const uintptr_t a0 = a & ~uintptr_t(15);
-  const uintptr_t a1 = (a + uintptr_t(count) * elem + 15) & ~uintptr_t(15);
-  shift = uint32_t(a - a0);
-  const uint32_t bytes = uint32_t(a1 - a0);
-  bulk_g2s(stage + off, reinterpret_cast<const void*>(a0), bytes, bar);
-  return bytes;
-}
-
-__global__ void __launch_bounds__(kBT + 32) k_out_bulk(DevMesh M, const double* __restrict__ K,
-                                                       const double2* __restrict__ FQ, BulkArgs r,
-                                                       OutArgs a) {
-  extern __shared__ __align__(128) char bsm[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(bsm);
-  uint64_t* empty = full + kBStages;
-  char* ring = bsm + 128;
-  constexpr uint32_t SB = bulk_stage_bytes();
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  constexpr int kConsumerWarps = kBT / 32;
-  if (tid == 0) {
-    for (int s = 0; s < kBStages; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, kConsumerWarps);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-  const int n_tiles = (r.n + kBT - 1) / kBT;
-  const int G = gridDim.x;
-  const int my = n_tiles > int(blockIdx.x) ? (n_tiles - int(blockIdx.x) + G - 1) / G : 0;
-  // slot offsets (same in every stage)
-  uint32_t off[kBCopies];
-  {
-    uint32_t o = 0;
-    const uint32_t el[kBCopies] = {8, 8, 8, 16, 16, 16, 16, 16, 8, 8, 16, 1};
-#pragma unroll
-    for (int k = 0; k < kBCopies; ++k) {
-      off[k] = o;
-      o += bslot(el[k]);
-    }
-    (void)o;
-  }
-  const uint32_t off_key = off[kBCopies - 1] + bslot(1);
-  const int W = (M.sten_max + 1) / 2;  // u32 words of st16 per edge; rows of uint2 = (W + 1) / 2
-  if (warp == kConsumerWarps) {
-    // producer
-    if (lane == 0) {
-      for (int i = 0; i < my; ++i) {
-        const int s = i % kBStages;
-        if (i >= kBStages) mbar_wait(empty + s, ((i / kBStages) - 1) & 1);
-        const int t = int(blockIdx.x) + i * G;
-        const int32_t e0 = r.base + t * kBT;
-        const uint32_t cnt = uint32_t(min(kBT, r.base + r.n - e0));
-        char* st = ring + size_t(s) * SB;
-        uint32_t sh, total = 0;
-        // expected bytes first (the copies complete against it)
-        uint32_t bytes[kBCopies + 1];
-        auto win = [&](const void* g, int64_t idx, uint32_t el) {
-          const uintptr_t x = reinterpret_cast<uintptr_t>(g) + uintptr_t(idx) * el;
-          return uint32_t(((x + uintptr_t(cnt) * el + 15) & ~uintptr_t(15)) - (x & ~uintptr_t(15)));
-        };
-        for (int k = 0; k < 3; ++k) bytes[k] = win(M.e_st16, int64_t(k) * M.nE + e0, 8);
-        for (int k = 0; k < 5; ++k) bytes[3 + k] = win(M.e_coef2, int64_t(k) * M.nE + e0, 16);
-        bytes[8] = win(M.e_cells, e0, 8);
-        bytes[9] = win(M.e_invd, e0, 8);
-        bytes[10] = win(FQ, e0, 16);
-        bytes[11] = win(M.e_nst, e0, 1);
-        bytes[12] = a.ekey ? win(a.ekey, e0, 1) : 0;
-        for (int k = 0; k <= kBCopies; ++k) total += bytes[k];
-        mbar_expect_tx(full + s, total);
-        for (int k = 0; k < 3; ++k) bulk_window(st, off[k], M.e_st16, int64_t(k) * M.nE + e0, 8, cnt, full + s, sh);
-        for (int k = 0; k < 5; ++k)
-          bulk_window(st, off[3 + k], M.e_coef2, int64_t(k) * M.nE + e0, 16, cnt, full + s, sh);
-        bulk_window(st, off[8], M.e_cells, e0, 8, cnt, full + s, sh);
-        bulk_window(st, off[9], M.e_invd, e0, 8, cnt, full + s, sh);
-        bulk_window(st, off[10], FQ, e0, 16, cnt, full + s, sh);
-        bulk_window(st, off[11], M.e_nst, e0, 1, cnt, full + s, sh);
-        if (a.ekey) bulk_window(st, off_key, a.ekey, e0, 1, cnt, full + s, sh);
-      }
-    }
-    return;
-  }
-  (void)W;
-  // consumers: thread tid <-> edge e0 + tid
-  for (int i = 0; i < my; ++i) {
-    const int s = i % kBStages;
-    mbar_wait(full + s, (i / kBStages) & 1);
-    const int t = int(blockIdx.x) + i * G;
-    const int32_t e0 = r.base + t * kBT;
-    const int32_t e = e0 + tid;
-    const char* st = ring + size_t(s) * SB;
-    // lead-in shift of every window (recomputed from the addresses)
-    auto sh = [&](const void* g, int64_t idx, uint32_t el) {
-      return uint32_t((reinterpret_cast<uintptr_t>(g) + uintptr_t(idx) * el) & 15u);
-    };
-    if (e < r.base + r.n) {
-      const uint8_t nstw = *reinterpret_cast<const uint8_t*>(st + off[11] + sh(M.e_nst, e0, 1) + tid);
-      const int g = a.ekey ? *reinterpret_cast<const uint8_t*>(st + off_key + sh(a.ekey, e0, 1) + tid) : 0;
-      const bool out = g <= 4 && ((a.mask >> (6 + g)) & 1u);
-      const bool wide = !M.e_st16 || __any_sync(__activemask(), nstw & 0x80);
-      if (out) {
-        const int nst = nstw & 0x7f;
-        const double2 own =
-            *reinterpret_cast<const double2*>(st + off[10] + sh(FQ, e0, 16) + 16 * tid);
-        const double qt_e = own.y;
-        const double inv_d = *reinterpret_cast<const double*>(st + off[9] + sh(M.e_invd, e0, 8) + 8 * tid);
-        const int2 cc = *reinterpret_cast<const int2*>(st + off[8] + sh(M.e_cells, e0, 8) + 8 * tid);
-        const double psi_lo = K[cc.x];
-        const double psi_hi = K[cc.y];
-        double pvflux = 0.0;
-        if (!wide && M.sten_max == kFastSten) {
-          uint32_t w[kFastSten / 2 + 1];
-#pragma unroll
-          for (int k = 0; k < (kFastSten / 2 + 1) / 2; ++k) {
-            const uint2 p = *reinterpret_cast<const uint2*>(
-                st + off[k] + sh(M.e_st16, int64_t(k) * M.nE + e0, 8) + 8 * tid);
-            w[2 * k] = p.x;
-            w[2 * k + 1] = p.y;
-          }
-          double2 fq[kFastSten];
-#pragma unroll
-          for (int j = 0; j < kFastSten; ++j) {
-            const int32_t e2 = e + (j & 1 ? int32_t(w[j >> 1]) >> 16 : int32_t(w[j >> 1] << 16) >> 16);
-            fq[j] = FQ[e2];
-          }
-#pragma unroll
-          for (int j = 0; j < kFastSten; ++j) {
-            const double2 cp = *reinterpret_cast<const double2*>(
-                st + off[3 + (j >> 1)] + sh(M.e_coef2, int64_t(j >> 1) * M.nE + e0, 16) + 16 * tid);
-            const double cj = j & 1 ? cp.y : cp.x;
-            const double x = cj * fq[j].x * (0.5 * (qt_e + fq[j].y));
-            if (j < nst) pvflux += x;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < kMaxSten; ++j) {
-            if (j < nst) {
-              const int32_t e2 = M.e_sten[j * M.nE + e];
-              const double2 cp = *reinterpret_cast<const double2*>(
-                  st + off[3 + (j >> 1)] + sh(M.e_coef2, int64_t(j >> 1) * M.nE + e0, 16) + 16 * tid);
-              const double c = j & 1 ? cp.y : cp.x;
-              const double2 fq = FQ[e2];
-              pvflux += c * fq.x * (0.5 * (qt_e + fq.y));
-            }
-          }
-        }
-        const double du = -pvflux - (psi_lo - psi_hi) * inv_d;
-        apply_op(a.eop[g <= 1 ? 0 : 1], e, du);
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty + s);
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Interface-1 prediction (integrators.cpp:217-227): order 3
 // dst = ((c0*s0) + (c1*s1)) + (c2*s2), order 2 (s2 null) (c0*s0) + (c1*s1),
 // on the I1 lists.

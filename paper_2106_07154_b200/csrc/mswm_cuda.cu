@@ -90,9 +90,7 @@ struct DArr {
     p = nullptr;
     n = count;
     if (count) {
-      // +64 bytes: 16-byte-aligned bulk copies (k_out_bulk) may round a
-      // window's end up past the last element
-      cudaError_t e = cudaMalloc(&p, count * sizeof(T) + 64);
+      cudaError_t e = cudaMalloc(&p, count * sizeof(T));
       if (e != cudaSuccess)
         throw Error(MSWM_E_NOMEM, "cudaMalloc of " + std::to_string(count * sizeof(T)) +
                                       " bytes: " + cudaGetErrorString(e));
@@ -162,9 +160,6 @@ struct MaskPlan {
   std::vector<int32_t> io_oc_orig, io_oe_orig;
   DArr<int32_t> io_oc, io_oe;
 };
-
-constexpr int32_t kBulkMinEdges = 1 << 16;  // edge ranges below this stay on k_out
-constexpr size_t kBulkSmem = 128 + size_t(kBStages) * bulk_stage_bytes();
 
 // Halo exchange plan of one rank: per peer slot, the owned values it sends
 // and the halo values it receives, as flat codes into the (h, u) arrays
@@ -295,7 +290,6 @@ struct mswm_cuda_ctx {
   int32_t n_band_c = 0, n_band_e = 0;
   int fork_state = 0;  // 0 not prepared, 1 ready, -1 not eligible
   int replication = 1;  // SchemeConfig::replication (operators.cpp:60)
-  int bulk_blocks = 0;  // resident CTAs/SM of k_out_bulk (0: not used, MSWM_BULK)
   // interior / boundary split of ranked evaluations (plan_part)
   bool bnd_ready = false;
   DArr<uint8_t> cbnd, ebnd;
@@ -747,13 +741,6 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   put(c->e_st16, e_st16p);
   put(c->e_sten, e_sten);
   put(c->e_nst, e_nst);
-  if (const char* bk = std::getenv("MSWM_BULK");
-      bk && bk[0] == '1' && sten_max == kFastSten && c->e_st16.p) {
-    CK(cudaFuncSetAttribute(k_out_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBulkSmem)));
-    int nb = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_out_bulk, kBT + 32, kBulkSmem));
-    c->bulk_blocks = nb;
-  }
   {
     // packed copies (kernels.cuh DevMesh): pairs of slots / entries per load
     std::vector<int2> c_edge2(size_t((deg_max + 1) / 2) * nC, make_int2(0, 0));
@@ -1176,26 +1163,9 @@ void launch_eval_once(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, cons
     a.cop[1] = cop[1];
     a.eop[0] = eop[0];
     a.eop[1] = eop[1];
-    // the contiguous range of the edge outputs through k_out_bulk (tables
-    // streamed by the copy engine), cells and the list part through k_out
-    const Span es_all = a.es;
-    const bool bulk = c->bulk_blocks > 0 && es_all.n_range >= kBulkMinEdges;
-    if (bulk) a.es = Span{es_all.base, 0, es_all.list, es_all.n_list};
-    const int64_t n_rest = int64_t(a.cs.n()) + a.es.n();
-    if (n_rest > 0) {
-      k_out<<<grid(n_rest, 2), kSBlock, 0, s>>>(M, h, Kp, FQ, a);
-      CK(cudaGetLastError());
-      ++c->launches;
-    }
-    if (bulk) {
-      int per_sm = c->bulk_blocks;
-      if (side && side->ctas_per_sm[2] > 0) per_sm = std::max(1, per_sm * side->ctas_per_sm[2] / 8);
-      const int64_t tiles = (int64_t(es_all.n_range) + kBT - 1) / kBT;
-      const int g = int(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(per_sm) * c->n_sm)));
-      k_out_bulk<<<g, kBT + 32, kBulkSmem, s>>>(M, Kp, FQ, BulkArgs{es_all.base, es_all.n_range}, a);
-      CK(cudaGetLastError());
-      ++c->launches;
-    }
+    k_out<<<grid(nout, 2), kSBlock, 0, s>>>(M, h, Kp, FQ, a);
+    CK(cudaGetLastError());
+    ++c->launches;
   }
   if (rec) CK(cudaEventRecordWithFlags(rec->stop, s, cudaEventRecordExternal));
 }
@@ -2495,7 +2465,7 @@ int mswm_cuda_eval_profile(mswm_cuda_ctx* c, float* eval_ms, int64_t* out_cells,
 
 int mswm_cuda_layout_info(const mswm_cuda_ctx* c, int* kernel_path, int* identity_order) {
   if (!c) return MSWM_E_USAGE;
-  if (kernel_path) *kernel_path = c->bulk_blocks > 0 ? 1 : 0;
+  if (kernel_path) *kernel_path = 0;
   if (identity_order) *identity_order = c->identity ? 1 : 0;
   return MSWM_OK;
 }

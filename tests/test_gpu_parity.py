@@ -317,8 +317,7 @@ def test_stepper_drop_in_interface():
 
 
 @pytest.mark.parametrize("kout,env", [("explicit", {"MSWM_ST16": "1"}),
-                                      ("explicit", {"MSWM_ST16": "0"}),
-                                      ("bulk", {"MSWM_BULK": "1"})])
+                                      ("explicit", {"MSWM_ST16": "0"})])
 def test_layouts_are_bitwise_equivalent(kout, env, monkeypatch):
     """Results are independent of the device numbering (input, Hilbert,
     region-major, random) and of the stencil-id table (16-bit offsets or the
@@ -461,15 +460,13 @@ def test_wide_interfaces_bitwise(width):
             assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref), (order, scheme)
 
 
-@pytest.mark.parametrize("bulk", ["0", "1"])
 @pytest.mark.parametrize("fork", ["1", "0"])
 @pytest.mark.parametrize("order", ["regions", "hilbert"])
-def test_concurrent_coarse_step_bitwise(fork, order, bulk, monkeypatch):
+def test_concurrent_coarse_step_bitwise(fork, order, monkeypatch):
     """LTS3 with the coarse step (step 4) on a second stream concurrent with
     the substeps (default) and in sequence (MSWM_FORK=0): bitwise equal to
     the oracle over several coarse steps, M = 2 and 4."""
     monkeypatch.setenv("MSWM_FORK", fork)
-    monkeypatch.setenv("MSWM_BULK", bulk)
     wl = W.small_sphere(6, seed=41, cap_deg=25.0)
     o = _oracle_for(wl)
     ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order, fine_mask=wl.fine_mask)
