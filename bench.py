@@ -76,7 +76,11 @@ def dist_init():
     if ws > 1:
         import torch
         import torch.distributed as dist
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            # more ranks than GPUs only for the dry-run check (MSWM_HALO_DRYRUN=1)
+            local %= torch.cuda.device_count()
+        backend = os.environ.get("MSWM_DIST_BACKEND",
+                                 "nccl" if torch.cuda.is_available() else "gloo")
         if backend == "nccl":
             torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -95,7 +99,7 @@ def allreduce_sum(x: float, ws: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
     t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
@@ -106,7 +110,7 @@ def allreduce_max(x: float, ws: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
     t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -385,6 +389,9 @@ def workload_config(wl, name, ws):
 
 def run_ours(args, ws, rank, local):
     import torch
+    # MSWM_HALO_DRYRUN=1 (checks of the multi-rank bench path on one GPU:
+    # ranks step independently, halo transfers skipped, results invalid)
+    dry_run = os.environ.get("MSWM_HALO_DRYRUN") == "1"
     from paper_2106_07154_b200.api import CudaContext, Scheme, State
 
     if not torch.cuda.is_available():
@@ -421,9 +428,10 @@ def run_ours(args, ws, rank, local):
         t1 = time.time()
         wl, lay = layout_from_store(store_dir, rank, ws)
         rc = RankContext(lay, rank, wl.b, wl.f, wl.gravity, wl.width, device=local)
-        uid = [RankContext.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        rc.init_nccl(uid[0])
+        if not dry_run:
+            uid = [RankContext.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            rc.init_nccl(uid[0])
         # exchange only what each evaluation reads (setup-time position swap)
         from paper_2106_07154_b200.api import LTS3_MASKS, kMaskAll
         rc.restrict_halos(LTS3_MASKS + [kMaskAll])
@@ -604,6 +612,8 @@ def run_ours(args, ws, rank, local):
             "gpu_launches": int(launches),
             "clocks": ck,
         }
+        if dry_run:
+            line["dry_run"] = "MSWM_HALO_DRYRUN=1: halo transfers skipped -- a check of the path, not a measurement"
         print(json.dumps(line), flush=True)
 
 
