@@ -425,32 +425,12 @@ __device__ __forceinline__ void item_out(const DevMesh& M, const double* __restr
   item_out_sp(M, h, K, FQ, a.cs, a.es, a, t);
 }
 
-#ifndef MSWM_KOUT_PREFETCH
-#define MSWM_KOUT_PREFETCH 0
-#endif
-__device__ __forceinline__ void pf_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
-}
-
 __global__ void MSWM_KOUT_BOUNDS k_out(DevMesh M, const double* __restrict__ h,
                                      const double* __restrict__ K,
                                      const double2* __restrict__ FQ, OutArgs a) {
   const int32_t n = a.cs.n() + a.es.n();
-  const int32_t stride = gridDim.x * kSBlock;
-  for (int32_t t = blockIdx.x * kSBlock + threadIdx.x; t < n; t += stride) {
-#if MSWM_KOUT_PREFETCH
-    // the next element's stencil tables into L2 while this one gathers
-    const int32_t tn = t + stride - a.cs.n();
-    if (tn >= 0 && tn < a.es.n() && M.e_st16) {
-      const int32_t en = a.es.at(tn);
-#pragma unroll
-      for (int k = 0; k < 3; ++k) pf_l2(M.e_st16 + int64_t(k) * M.nE + en);
-#pragma unroll
-      for (int k = 0; k < 5; ++k) pf_l2(M.e_coef2 + int64_t(k) * M.nE + en);
-    }
-#endif
+  for (int32_t t = blockIdx.x * kSBlock + threadIdx.x; t < n; t += gridDim.x * kSBlock)
     item_out(M, h, K, FQ, a, t);
-  }
 }
 
 // ---------------------------------------------------------------------------

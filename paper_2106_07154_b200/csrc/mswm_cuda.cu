@@ -1835,13 +1835,15 @@ void enqueue_rk4(std::vector<mswm_cuda_ctx*>& cs, double dt) {
                         {&C::T1h, &C::T1u, &C::T2h, &C::T2u, OP_RK4_MID, half},
                         {&C::T2h, &C::T2u, &C::T1h, &C::T1u, OP_RK4_MID, dt},
                         {&C::T1h, &C::T1u, &C::H, &C::U, OP_RK4_LAST, sixth}};
+  // every stage reads one buffer pair and writes another (or, last, the
+  // state at its own outputs only): the exchange of the read pair can
+  // overlap the interior evaluation (exchange_eval)
   for (const St& st : stages) {
-    exchange(cs, st.rh, st.ru, MSWM_MASK_ALL);
-    for (auto* c : cs) {
+    exchange_eval(cs, st.rh, st.ru, MSWM_MASK_ALL, true, [&](mswm_cuda_ctx* c, const MaskPlan& p) {
       auto co = both(mk_op(st.kind, (c->*st.wh).p, c->H.p, st.c0, nullptr, 0, 0, c->A1h.p));
       auto eo = both(mk_op(st.kind, (c->*st.wu).p, c->U.p, st.c0, nullptr, 0, 0, c->A1u.p));
-      launch_eval(c, plan_for(c, MSWM_MASK_ALL), (c->*st.rh).p, (c->*st.ru).p, co.data(), eo.data());
-    }
+      launch_eval(c, p, (c->*st.rh).p, (c->*st.ru).p, co.data(), eo.data());
+    });
   }
 }
 
@@ -1946,6 +1948,11 @@ mswm_cuda_ctx::Graph capture_step(std::vector<mswm_cuda_ctx*>& cs, cudaStream_t 
       }
     } else {
       plan_for(c, MSWM_MASK_ALL);
+      prepare_overlap(c);
+      if (c->halo.active() && scheme == MSWM_RK4) {
+        plan_part(c, MSWM_MASK_ALL, 1);
+        plan_part(c, MSWM_MASK_ALL, 2);
+      }
     }
   }
   mswm_cuda_ctx::Graph gr;
