@@ -33,7 +33,7 @@ OUT = ROOT / "tests" / "golden"
 # checkpoints (coarse LTS3 steps): north_star's 100 steps on C4, the configs'
 # own horizons on C2 (1000) and, bounded by the reference's CPU time, C3/C5
 CHECKPOINTS = {"c1": [1, 10, 100], "c2": [1, 10, 100, 1000], "c3": [1, 10, 20],
-               "c4": [1, 10, 100], "c5": [1]}
+               "c4": [1, 10, 100], "c5": [1, 10]}
 SAMPLE = 4099  # stride of the stored samples (prime: no alignment with the numbering)
 
 

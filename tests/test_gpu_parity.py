@@ -553,3 +553,42 @@ def test_full_size_against_reference(config):
     st = ctx.download()
     assert max_rel(st.h, h_ref) <= 1e-11 and max_rel(st.u, u_ref) <= 1e-11
     assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
+
+
+def test_region_edge_cases_match_reference(ref_lib):
+    """make_regions on degenerate inputs (regions.cpp:69-105): every fine
+    predicate the reference rejects raises ConfigError on the device too
+    (no fine cell, every cell fine, interface layers exhausting the non-fine
+    cells, an empty layer, width 0); the ones it accepts -- a single fine
+    cell, fine cells that touch no interface (underline layers empty, with
+    its warnings) -- give bit-exact labels and groups."""
+    wl = W.small_sphere(3, seed=8)
+    n = wl.mesh.n_cells
+    rm = ref_lib.RefMesh.from_mesh(wl.mesh)
+    rng = np.random.default_rng(3)
+    one = np.zeros(n, np.uint8)
+    one[7] = 1
+    almost = np.ones(n, np.uint8)
+    almost[rng.choice(n, 3, replace=False)] = 0
+    cases = [(np.zeros(n, np.uint8), 1), (np.ones(n, np.uint8), 1), (almost, 1), (one, 1),
+             (one, 2), (one, 4), (wl.fine_mask, 3), (wl.fine_mask, 0),
+             ((rng.random(n) < 0.3).astype(np.uint8), 1)]
+    for mask, width in cases:
+        try:
+            rr = ref_lib.RefRegions(rm, mask, width)
+            ref_err = None
+        except ref_lib.OracleError as e:
+            ref_err = e
+        ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity)
+        if ref_err is not None:
+            assert ref_err.status == 1
+            with pytest.raises(ConfigError):
+                ctx.make_regions(mask, width)
+            continue
+        got = ctx.make_regions(mask, width)
+        cl, cs, el = rr.labels(n, wl.mesh.n_edges)
+        assert np.array_equal(got.cell_label, cl) and np.array_equal(got.cell_sublabel, cs)
+        assert np.array_equal(got.edge_label, el)
+        for a, b in zip(got.groups, rr.groups()):
+            assert np.array_equal(a, b)
+        assert len(got.warnings) == rr.n_warnings, (width, got.warnings)
