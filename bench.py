@@ -612,7 +612,7 @@ def run_ours(args, ws, rank, local):
             "gpu_launches": int(launches),
             "clocks": ck,
         }
-        if dry_run:
+        if dry_run and ws > 1:
             line["dry_run"] = "MSWM_HALO_DRYRUN=1: halo transfers skipped -- a check of the path, not a measurement"
         print(json.dumps(line), flush=True)
 
