@@ -546,6 +546,24 @@ __global__ void k_unpack(int64_t n, const int32_t* __restrict__ code, const doub
   else
     u[~c] = buf[k];
 }
+// Unpack fused with the next stage's interface-1 prediction (ranks: the
+// prediction writes the next stage's input array on I1, which neither this
+// exchange nor this stage's evaluation touches) -- one launch fewer per
+// substep stage on the latency-bound chain.
+__global__ void k_unpack_pred(int64_t n, const int32_t* __restrict__ code,
+                              const double* __restrict__ buf, double* __restrict__ h,
+                              double* __restrict__ u, PredArgs pa) {
+  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < n) {
+    const int32_t c = code[k];
+    if (c >= 0)
+      h[c] = buf[k];
+    else
+      u[~c] = buf[k];
+  } else if (k - n < int64_t(pa.nc) + pa.ne) {
+    item_predict(pa, int32_t(k - n));
+  }
+}
 
 // Boundary permutations between the caller's numbering and the internal one.
 __global__ void k_gather_perm(int32_t n, const int32_t* __restrict__ n2o,

@@ -1343,11 +1343,16 @@ bool restricted(const std::vector<mswm_cuda_ctx*>& cs) {
   return false;
 }
 
+// `preds` (one per member, or null): the next stage's interface-1
+// prediction, fused into the unpack launch (k_unpack_pred).
 void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us, unsigned mask,
-              bool second_comm = false) {
+              bool second_comm = false, const std::vector<PredArgs>* preds = nullptr) {
   bool any = false;
   for (auto* c : cs) any |= c->halo.active();
-  if (!any) return;
+  if (!any) {
+    if (preds) throw Error(MSWM_E_USAGE, "fused prediction without a halo exchange");
+    return;
+  }
   for (auto* c : cs) {
     Halo& x = halo_for(c, mask);
     if (x.ns > 0) {
@@ -1417,9 +1422,17 @@ void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us, unsigned ma
       }
     }
   }
-  for (auto* c : cs) {
+  for (size_t m = 0; m < cs.size(); ++m) {
+    mswm_cuda_ctx* c = cs[m];
     Halo& x = halo_for(c, mask);
-    if (x.nr > 0) {
+    const PredArgs* pa = preds ? &(*preds)[m] : nullptr;
+    const int64_t np = pa ? int64_t(pa->nc) + pa->ne : 0;
+    if (np > 0) {
+      k_unpack_pred<<<nblk(x.nr + np), kBlock, 0, c->ls>>>(x.nr, x.rcode.p, x.rbuf.p, (c->*hs).p,
+                                                            (c->*us).p, *pa);
+      CK(cudaGetLastError());
+      ++c->launches;
+    } else if (x.nr > 0) {
       k_unpack<<<nblk(x.nr), kBlock, 0, c->ls>>>(x.nr, x.rcode.p, x.rbuf.p, (c->*hs).p, (c->*us).p);
       CK(cudaGetLastError());
       ++c->launches;
@@ -1441,12 +1454,12 @@ void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us, unsigned ma
 // with MSWM_OVERLAP=2.
 template <class F>
 void exchange_eval(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us, unsigned mask,
-                   bool big_eval, F&& eval) {
+                   bool big_eval, F&& eval, const std::vector<PredArgs>* preds = nullptr) {
   bool halos = false;
   for (auto* c : cs) halos |= c->halo.active();
   mswm_cuda_ctx* const c0 = cs[0];
   if (!halos || !c0->lx || (!big_eval && c0->overlap_level < 2)) {
-    exchange(cs, hs, us, mask);
+    exchange(cs, hs, us, mask, false, preds);
     for (auto* c : cs) eval(c, plan_for(c, mask));
     return;
   }
@@ -1454,7 +1467,7 @@ void exchange_eval(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us, unsign
   CK(cudaEventRecord(c0->ev_x0, main));
   CK(cudaStreamWaitEvent(c0->lx, c0->ev_x0, 0));
   for (auto* c : cs) c->ls = c0->lx;
-  exchange(cs, hs, us, mask);
+  exchange(cs, hs, us, mask, false, preds);
   CK(cudaEventRecord(c0->ev_x1, c0->lx));
   for (auto* c : cs) c->ls = main;
   for (auto* c : cs) eval(c, plan_part(c, mask, 1));
@@ -1640,8 +1653,15 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
     // stage 1: fine hb = ha + delta*d; interfaces acc1 += d   (:521-531)
     // predictions ride in the evaluation's launch unless a halo exchange
     // has to propagate them first (multi-rank)
-    if (k > 0 && !fuse_pred)
-      for (auto* c : cs) launch_predict(c, 1, k, M, c->H.p, c->U.p);
+    // ranks: each stage's exchange carries the next stage's prediction in its
+    // unpack launch (k_unpack_pred; substep 0's stage 1 is the prologue's)
+    std::vector<PredArgs> pred2, pred3, pred1n;
+    if (!fuse_pred)
+      for (auto* c : cs) {
+        pred2.push_back(make_pred(c, 2, k, M, c->H1.p, c->U1.p));
+        pred3.push_back(make_pred(c, 3, k, M, c->H2.p, c->U2.p));
+        if (k + 1 < M) pred1n.push_back(make_pred(c, 1, k + 1, M, c->H.p, c->U.p));
+      }
     exchange_eval(cs, &C::H, &C::U, kMaskSub, false, [&](mswm_cuda_ctx* c, const MaskPlan& p) {
       const PredArgs pa = make_pred(c, 1, k, M, c->H.p, c->U.p);
       Op co[2] = {mk_op(OP_EULER, c->H1.p, c->H.p, delta),
@@ -1649,10 +1669,8 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
       Op eo[2] = {mk_op(OP_EULER, c->U1.p, c->U.p, delta),
                   mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A1u.p, first)};
       launch_eval(c, p, c->H.p, c->U.p, co, eo, (k > 0 && fuse_pred) ? &pa : nullptr);
-    });
+    }, fuse_pred ? nullptr : &pred2);
     // stage 2: fine hc = 0.75 ha + 0.25 hb + (0.25 delta) d; acc2 += d   (:532-541)
-    if (!fuse_pred)
-      for (auto* c : cs) launch_predict(c, 2, k, M, c->H1.p, c->U1.p);
     exchange_eval(cs, &C::H1, &C::U1, kMaskSub, false, [&](mswm_cuda_ctx* c, const MaskPlan& p) {
       const PredArgs pa = make_pred(c, 2, k, M, c->H1.p, c->U1.p);
       const double cr = 0.25 * delta;
@@ -1661,11 +1679,9 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
       Op eo[2] = {mk_op(OP_WCOMB, c->U2.p, c->U.p, 0.75, c->U1.p, 0.25, cr),
                   mk_op(OP_ACC, nullptr, nullptr, 0, nullptr, 0, 0, c->A2u.p, first)};
       launch_eval(c, p, c->H1.p, c->U1.p, co, eo, fuse_pred ? &pa : nullptr);
-    });
+    }, fuse_pred ? nullptr : &pred3);
     // stage 3: fine ha = 1/3 ha + 2/3 hc + (2/3 delta) d; acc3 += d, and on
     // the last substep the interface correction (:542-553, :231-274).
-    if (!fuse_pred)
-      for (auto* c : cs) launch_predict(c, 3, k, M, c->H2.p, c->U2.p);
     exchange_eval(cs, &C::H2, &C::U2, kMaskSub, false, [&](mswm_cuda_ctx* c, const MaskPlan& p) {
       const PredArgs pa = make_pred(c, 3, k, M, c->H2.p, c->U2.p);
       const double cr = two3 * delta;
@@ -1682,7 +1698,7 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
                       first, c->A1u.p, c->A2u.p);
       }
       launch_eval(c, p, c->H2.p, c->U2.p, co, eo, fuse_pred ? &pa : nullptr);
-    });
+    }, (fuse_pred || k + 1 == M) ? nullptr : &pred1n);
   }
   // Step 4 (:557-563): coarse h = 1/3 h_old + 2/3 h2 + (2/3 dt) dh, in place.
   // With full halos the H2/U2 copies are current (the last exchange
