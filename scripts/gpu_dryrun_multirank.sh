@@ -1,4 +1,4 @@
-# Round-2: the multi-rank bench path end to end on one GPU in dry-run mode (ranks step
+# The multi-rank bench path end to end on one GPU in dry-run mode (ranks step
 # independently, halo transfers skipped -- no kernels wait on one another), plus a test subset.
 set -u
 mkdir -p gpurun_out

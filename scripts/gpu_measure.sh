@@ -1,4 +1,4 @@
-# Round-2 measurement: bench lines C1-C3, C5, the reference arm on C4, the ncu launch list and
+# Measurement on one B200 (under gpurun): bench lines C1-C3, C5, the reference arm on C4, the ncu launch list and
 # one full capture of the step-1 evaluation kernels (each profiled command ran without ncu first).
 set -u
 mkdir -p gpurun_out
