@@ -23,7 +23,7 @@ def main():
     t1 = rec["single_ms_per_step"]
     tmax = rec["max_rank_ms"]
     sub_mask = "0x3df"  # MASK_SUB
-    m_sub = 3 * 4  # 3M substep exchanges at M = 4 (C4)
+    m_sub = 3 * rec.get("M", 4)  # 3M substep exchanges per coarse step
     kb = max(rec["recv_bytes_per_exchange"][sub_mask]) / 1e3
     print(f"{rec['config']} on {n} ranks: T1 {t1:.3f} ms, max rank {tmax:.3f} ms "
           f"(compute efficiency {t1 / (n * tmax):.3f}); {m_sub} substep exchanges of "

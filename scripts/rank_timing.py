@@ -91,7 +91,7 @@ def main():
     xpeers = {hex(int(m)): [int(sum(1 for v in needs[m][r].values() if len(v))) for r in range(n)]
               for m in masks}
     print(json.dumps({
-        "config": cfg, "n_ranks": n, "steps": steps, "single_ms_per_step": t_single,
+        "config": cfg, "n_ranks": n, "M": wl.M, "steps": steps, "single_ms_per_step": t_single,
         "single_evals": single_evals, "rank_ms_per_step": per_rank, "max_rank_ms": max(per_rank),
         "ideal_ms": t_single / n, "compute_efficiency": t_single / (n * max(per_rank)),
         "concurrent_coarse": fork, "evals_per_rank": evals, "owned_cells": [rc.lm.n_owned_cells for rc in ranks],
