@@ -36,6 +36,7 @@
 #include <numeric>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <type_traits>
 #include <vector>
@@ -151,8 +152,8 @@ struct MaskPlan {
   std::vector<int32_t> host_cells, host_edges;  // original ids, same order as device lists
   // drop-in eval I/O (mswm_cuda_eval): the h / u entries the evaluation
   // reads, original ids on the host and internal ids on the device (built on
-  // first use); full_* = the read set covers most of the mesh, upload whole
-  bool io_ready = false, io_full_c = false, io_full_e = false;
+  // first use)
+  bool io_ready = false;
   std::vector<int32_t> io_rc_orig, io_re_orig;
   DArr<int32_t> io_rc, io_re;
   // outputs in ascending original id (the host scatter streams): original
@@ -2137,6 +2138,22 @@ int guard(mswm_cuda_ctx* c, F&& f) {
 
 }  // namespace
 
+// f(lo, hi) over [0, n) on the host cores (the drop-in eval's pack and
+// scatter loops: independent elements).
+template <class F>
+void host_par_for(int64_t n, F&& f) {
+  static const int64_t T = std::max(1u, std::thread::hardware_concurrency());
+  const int64_t t = std::min<int64_t>(T, std::max<int64_t>(1, n / (1 << 18)));
+  if (t <= 1) {
+    if (n > 0) f(int64_t(0), n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int64_t k = 1; k < t; ++k) th.emplace_back([&, k] { f(n * k / t, n * (k + 1) / t); });
+  f(0, n / t);
+  for (auto& x : th) x.join();
+}
+
 // ===========================================================================
 // C ABI
 
@@ -2287,11 +2304,11 @@ void build_eval_io(mswm_cuda_ctx* c, MaskPlan& p) {
       ei.push_back(ni);
     }
   }
-  // packing pays while the read set is a minority of the mesh
-  p.io_full_c = 2 * ci.size() > size_t(c->nC);
-  p.io_full_e = 2 * ei.size() > size_t(c->nE);
-  if (!p.io_full_c && !ci.empty()) p.io_rc.upload(ci, s);
-  if (!p.io_full_e && !ei.empty()) p.io_re.upload(ei, s);
+  // inputs always go through pinned staging (packed on all host cores; a
+  // pageable copy of the whole array is slower even when the read set is
+  // most of the mesh)
+  if (!ci.empty()) p.io_rc.upload(ci, s);
+  if (!ei.empty()) p.io_re.upload(ei, s);
   auto sorted_out = [&](const std::vector<int32_t>& orig, const std::vector<int32_t>& o2n,
                         std::vector<int32_t>& so, DArr<int32_t>& dev) {
     so = orig;
@@ -2326,19 +2343,24 @@ int mswm_cuda_eval(mswm_cuda_ctx* c, const double* h, const double* u, unsigned 
     MaskPlan& p = plan_for(c, mask);
     build_eval_io(c, p);
     cudaStream_t s = c->stream;
-    // inputs: only the h / u entries the evaluation reads cross PCIe (packed
-    // through pinned staging), unless they are most of the mesh
+    // inputs: only the h / u entries the evaluation reads cross PCIe, packed
+    // on the host cores into pinned staging
     if (c->T1h.n != size_t(c->nC)) c->T1h.alloc(c->nC);
     if (c->T1u.n != size_t(c->nE)) c->T1u.alloc(c->nE);
-    const size_t nrc = p.io_full_c ? 0 : p.io_rc_orig.size();
-    const size_t nre = p.io_full_e ? 0 : p.io_re_orig.size();
+    const size_t nrc = p.io_rc_orig.size();
+    const size_t nre = p.io_re_orig.size();
     const size_t nout = size_t(p.nc) + p.ne;
     ensure_pin(c, std::max<size_t>(1, std::max(nrc + nre, nout)));
-    if (p.io_full_c) upload_field(c, c->T1h, h, c->c_new2old, c->nC);
-    if (p.io_full_e) upload_field(c, c->T1u, u, c->e_new2old, c->nE);
     if (nrc + nre > 0) {
-      for (size_t k = 0; k < nrc; ++k) c->pin[k] = h[p.io_rc_orig[k]];
-      for (size_t k = 0; k < nre; ++k) c->pin[nrc + k] = u[p.io_re_orig[k]];
+      double* pin = c->pin;
+      const int32_t* rc = p.io_rc_orig.data();
+      const int32_t* re = p.io_re_orig.data();
+      host_par_for(int64_t(nrc), [&](int64_t lo, int64_t hi) {
+        for (int64_t k = lo; k < hi; ++k) pin[k] = h[rc[k]];
+      });
+      host_par_for(int64_t(nre), [&](int64_t lo, int64_t hi) {
+        for (int64_t k = lo; k < hi; ++k) pin[nrc + k] = u[re[k]];
+      });
       CK(cudaMemcpyAsync(c->io_pack.p, c->pin, (nrc + nre) * 8, cudaMemcpyHostToDevice, s));
       if (nrc)
         k_scatter_perm<<<nblk(int64_t(nrc)), kBlock, 0, s>>>(int32_t(nrc), p.io_rc.p, c->io_pack.p,
@@ -2365,8 +2387,18 @@ int mswm_cuda_eval(mswm_cuda_ctx* c, const double* h, const double* u, unsigned 
     }
     CK(cudaStreamSynchronize(s));
     check_dry(c);
-    for (int32_t k = 0; k < p.nc; ++k) dh[p.io_oc_orig[k]] = c->pin[k];
-    for (int32_t k = 0; k < p.ne; ++k) du[p.io_oe_orig[k]] = c->pin[p.nc + k];
+    {
+      const double* pin = c->pin;
+      const int32_t* oc = p.io_oc_orig.data();
+      const int32_t* oe = p.io_oe_orig.data();
+      const int64_t nc = p.nc;
+      host_par_for(nc, [&](int64_t lo, int64_t hi) {
+        for (int64_t k = lo; k < hi; ++k) dh[oc[k]] = pin[k];
+      });
+      host_par_for(int64_t(p.ne), [&](int64_t lo, int64_t hi) {
+        for (int64_t k = lo; k < hi; ++k) du[oe[k]] = pin[nc + k];
+      });
+    }
     return int(MSWM_OK);
   });
 }
