@@ -398,6 +398,30 @@ __device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __re
             }
           }
         }
+      } else if (M.sten_max == kFastSten) {
+        // the int32 ids (~9 % of warps on C4), same straight-line batches
+#pragma unroll
+        for (int j0 = 0; j0 < kFastSten; j0 += 2 * MSWM_KOUT_BATCH) {
+          double2 c[MSWM_KOUT_BATCH];
+          double2 fq[2 * MSWM_KOUT_BATCH];
+#pragma unroll
+          for (int b = 0; b < 2 * MSWM_KOUT_BATCH; ++b) {
+            const int j = j0 + b;
+            if (j < kFastSten) {
+              if (!(b & 1)) c[b >> 1] = M.e_coef2[(j >> 1) * M.nE + e];
+              fq[b] = FQ[M.e_sten[j * M.nE + e]];
+            }
+          }
+#pragma unroll
+          for (int b = 0; b < 2 * MSWM_KOUT_BATCH; ++b) {
+            const int j = j0 + b;
+            if (j < kFastSten) {
+              const double cj = b & 1 ? c[b >> 1].y : c[b >> 1].x;
+              const double x = cj * fq[b].x * (0.5 * (qt_e + fq[b].y));
+              if (j < nst) pvflux += x;
+            }
+          }
+        }
       } else {
 #pragma unroll
         for (int j = 0; j < kMaxSten; ++j) {
