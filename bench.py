@@ -398,14 +398,20 @@ def run_ours(args, ws, rank, local):
         raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
     torch.cuda.set_device(local)
     t0 = time.time()
+    setup = {}
     rc = None
     if ws == 1:
         wl = make_workload(args.config, args.level)
+        setup["workload_s"] = time.time() - t0
         log(f"[rank {rank}] workload {args.config}: {wl.mesh.n_cells} cells, {wl.mesh.n_edges} edges, "
             f"built in {time.time() - t0:.1f}s")
+        t1 = time.time()
         ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, device=local, order=args.order,
                           fine_mask=wl.fine_mask, interface_width=wl.width)
+        setup["context_s"] = time.time() - t1
+        t1 = time.time()
         rm = ctx.make_regions(wl.fine_mask, wl.width)
+        setup["regions_s"] = time.time() - t1
         log(f"[rank {rank}] groups {rm.group_sizes()} (host rss {_rss_gb():.1f} GB)")
         ctx.upload(State(wl.h, wl.u, 0.0))
         io_mesh = wl.mesh
@@ -422,7 +428,10 @@ def run_ours(args, ws, rank, local):
             wl0 = make_workload(args.config, args.level)
             log(f"[rank 0] workload {args.config}: {wl0.mesh.n_cells} cells, built in "
                 f"{time.time() - t0:.1f}s")
+            setup["workload_s"] = time.time() - t0
+            t1 = time.time()
             publish_store(store_dir, wl0, device=local, n_ranks=ws)
+            setup["publish_s"] = time.time() - t1
             del wl0
         barrier(ws)
         t1 = time.time()
@@ -442,6 +451,7 @@ def run_ours(args, ws, rank, local):
             shutil.rmtree(store_dir, ignore_errors=True)
         ctx = rc.ctx
         io_mesh = rc.local_mesh
+        setup["rank_local_s"] = time.time() - t1
         log(f"[rank {rank}] local mesh {rc.lm.n_cells} cells ({rc.lm.n_owned_cells} owned), "
             f"{len(lay.locals[rank].send_cells)} peers, set up in {time.time() - t1:.1f}s "
             f"(host rss {_rss_gb():.1f} GB)")
@@ -449,7 +459,10 @@ def run_ours(args, ws, rank, local):
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=local)
 
     # warm-up (also captures the step graph)
+    t1 = time.time()
     ctx.advance(Scheme.LTS3, wl.dt, wl.M, max(args.warmup, 1))
+    setup["plans_capture_warmup_s"] = time.time() - t1
+    setup["total_s"] = time.time() - t0
     ctx.reset_ledger()
 
     clocks = Clocks(local)
@@ -610,6 +623,7 @@ def run_ours(args, ws, rank, local):
             "cpu_baseline": cpu,
             "rk4_fine_dt": rk4,
             "gpu_launches": int(launches),
+            "setup": {k: round(v, 2) for k, v in setup.items()},
             "clocks": ck,
         }
         if dry_run and ws > 1:
