@@ -217,6 +217,14 @@ int mswm_cuda_layout_info(const mswm_cuda_ctx* ctx, int* kernel_path,
  * table instead (edges_on_edge, mesh.hpp:60-61). */
 int mswm_cuda_stencil_info(const mswm_cuda_ctx* ctx, int* offsets16, int64_t* n_wide);
 
+/* 16-bit index records of the evaluation kernels (kernels.cuh DevMesh
+ * v_rec / c_rec / e_cv16 / e_c16): packed16 bit 0 = in use (MSWM_PACK16 != 0),
+ * bit 1 = the cell records too (ring size <= 6 meshes); the counts are the
+ * vertices, cells and edges with an id offset outside int16, which their
+ * warps read from the int32 tables instead. */
+int mswm_cuda_index_info(const mswm_cuda_ctx* ctx, int* packed16, int64_t* n_wide_vertices,
+                         int64_t* n_wide_cells, int64_t* n_wide_edges);
+
 /* Number of this library's kernels one replay of the most recently used
  * step graph launches (the bench's gpu_launches evidence). */
 int mswm_cuda_kernels_per_step(mswm_cuda_ctx* ctx, int64_t* n);
@@ -260,6 +268,19 @@ int mswm_cuda_courant(mswm_cuda_ctx* ctx, double dt, int M, double* fine,
  * numbering; outputs are the owned elements only and halo copies are
  * refreshed before every evaluation (the device form of ThreadedEvaluator's
  * per-eval copy-in, rank_pool.cpp:133-135). */
+
+/* Partition of the mesh for n_parts ranks on the device (replaces
+ * partition_multiconstraint's per-class split, partition.cpp:219-231, and
+ * make_block_plan's edge ownership, partition.cpp:338-353): every region class
+ * (fine incl. underline, coarse, interface) is cut into n_parts near-equal
+ * consecutive runs of `sweep_order` (a permutation of the caller's cell ids,
+ * e.g. a space-filling curve); an edge goes to the rank of its first cell
+ * (edge_cells order) of the edge's own class.  Needs the region map of
+ * mswm_cuda_set_regions.  Outputs in caller ids (either may be null);
+ * MSWM_E_USAGE for a bad order / n_parts, MSWM_E_TOPOLOGY for an edge with no
+ * cell of its class. */
+int mswm_cuda_partition(mswm_cuda_ctx* ctx, const int32_t* sweep_order, int n_parts,
+                        int32_t* rank_of_cell, int32_t* edge_owner);
 
 /* Halo plan of a partition on the device (make_block_plan's 2-hop halo,
  * partition.cpp:355-392, for every rank at once): for each cell / edge /

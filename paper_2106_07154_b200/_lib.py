@@ -171,6 +171,8 @@ def cuda() -> C.CDLL:
             "mswm_cuda_set_replication": (C.c_int, [vp, C.c_int]),
             "mswm_cuda_layout_info": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
             "mswm_cuda_stencil_info": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int64)]),
+            "mswm_cuda_index_info": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int64),
+                                               C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
             "mswm_cuda_set_labels": (C.c_int, [vp, u8p, u8p, u8p, u8p, u8p, C.c_int]),
             "mswm_cuda_set_halo": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, i32p, i64p, i32p]),
             "mswm_cuda_nccl_unique_id": (C.c_int, [vp]),
@@ -179,6 +181,7 @@ def cuda() -> C.CDLL:
             "mswm_cuda_group_destroy": (None, [vp]),
             "mswm_cuda_group_step": (C.c_int, [vp, C.c_int, C.c_double, C.c_int, C.c_int64]),
             "mswm_cuda_halo_reach": (C.c_int, [vp, i32p, C.c_int, u64p, u64p, u64p]),
+            "mswm_cuda_partition": (C.c_int, [vp, i32p, C.c_int, i32p, i32p]),
             "mswm_cuda_group_nccl_loopback": (C.c_int, [vp]),
             "mswm_cuda_group_last_error": (C.c_char_p, [vp]),
         }

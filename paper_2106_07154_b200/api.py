@@ -378,10 +378,34 @@ class CudaContext:
         self._check(self.lib.mswm_cuda_stencil_info(self.handle, C.byref(o), C.byref(n)))
         return {"offsets16": bool(o.value), "n_wide": n.value}
 
+    def index_info(self) -> dict:
+        """16-bit index records of kernels A, B, C in use, and the vertices /
+        cells / edges whose warps read the int32 tables instead."""
+        p = C.c_int(0)
+        n = [C.c_int64(0) for _ in range(3)]
+        self._check(self.lib.mswm_cuda_index_info(self.handle, C.byref(p), *[C.byref(x) for x in n]))
+        return {"packed16": bool(p.value & 1), "cell_records": bool(p.value & 2),
+                "n_wide_vertices": n[0].value, "n_wide_cells": n[1].value,
+                "n_wide_edges": n[2].value}
+
     def kernels_per_step(self) -> int:
         n = C.c_int64(0)
         self._check(self.lib.mswm_cuda_kernels_per_step(self.handle, C.byref(n)))
         return n.value
+
+    def partition(self, sweep_order, n_parts: int):
+        """Device partition (partition.cpp:219-231, 338-353): (rank of every
+        cell, owner rank of every edge) -- each region class cut into n_parts
+        near-equal runs of ``sweep_order``.  Needs make_regions first."""
+        m = self.mesh
+        o = np.ascontiguousarray(sweep_order, np.int32)
+        if o.shape != (m.n_cells,):
+            raise UsageError(f"sweep_order must have shape ({m.n_cells},)")
+        roc = np.zeros(m.n_cells, np.int32)
+        own = np.zeros(m.n_edges, np.int32)
+        self._check(self.lib.mswm_cuda_partition(self.handle, _p(o, _lib.i32p), int(n_parts),
+                                                 _p(roc, _lib.i32p), _p(own, _lib.i32p)))
+        return roc, own
 
     def halo_reach(self, rank_of_cell, n_ranks: int):
         """Device halo plan of a partition (partition.cpp:355-392): uint64 bit

@@ -83,11 +83,45 @@ struct DevMesh {
   const int2* __restrict__ c_edge2;      // [(deg_max+1)/2][nC] ring edges (2k, 2k+1)
   const int2* __restrict__ v_ce;         // [3][nV] (vertex_cells k, vertex_edges k)
   const double2* __restrict__ v_af;      // [nV] (A_v, f_v)
+  // 16-bit index records (null: the int32 tables above only).  Each id is
+  // stored as an int16 offset from a base proportional to the issuing
+  // element's own id (pbase: edges, cells and vertices follow the same
+  // space-filling curve, so an element's neighbours sit near id * n_to /
+  // n_from); an element with an offset outside int16 (region seams, ~0.3 %)
+  // is flagged "wide", and a warp holding one reads the int32 tables
+  // instead (warp-uniform vote: the gathers stay back to back).
+  const uint4* __restrict__ v_rec;       // [nV] 3 cells, 3 edges; w: bits 0-2 v_sbits, bit 7 wide
+  const uint4* __restrict__ c_rec;       // [nC] 6 ring edges; w: byte 0 deg | wide << 7, byte 1 c_sbits
+                                         // (deg_max == 6 meshes only)
+  const uint2* __restrict__ e_cv16;      // [nE] (c0, c1), (v0, v1); a half 0x8000: wide
+  const uint32_t* __restrict__ e_c16;    // [nE] (c0, c1) for kernel C; wide: e_nst bit 6
+                                         // (also in e_st16's sixth word when sten_max == 10)
+  uint32_t rq_ce, rf_ce;                 // base ratios n_to / n_from as q + f / 2^32:
+  uint32_t rq_ve, rf_ve;                 //   cells per edge, vertices per edge,
+  uint32_t rq_cv, rf_cv;                 //   cells per vertex, edges per vertex,
+  uint32_t rq_ev, rf_ev;                 //   edges per cell
+  uint32_t rq_ec, rf_ec;
   // fields
   const double* __restrict__ b;          // [nC]
   const double* __restrict__ f;          // [nV]
   double g;
 };
+
+// base id of a 16-bit offset record (host twin: pbase_host in mswm_cuda.cu)
+__device__ __forceinline__ int32_t pbase(int32_t x, uint32_t q, uint32_t f) {
+  return int32_t(q * uint32_t(x) + __umulhi(uint32_t(x), f));
+}
+__device__ __forceinline__ int32_t lo16(uint32_t w) { return int32_t(w << 16) >> 16; }
+__device__ __forceinline__ int32_t hi16(uint32_t w) { return int32_t(w) >> 16; }
+__device__ __forceinline__ bool has_sentinel16(uint32_t w) {
+  return (w & 0xFFFFu) == 0x8000u || (w >> 16) == 0x8000u;
+}
+
+// (c0, c1) of edge e from its 16-bit record word
+__device__ __forceinline__ int2 c16_cells(const DevMesh& M, int32_t e, uint32_t r) {
+  const int32_t bc = pbase(e, M.rq_ce, M.rf_ce);
+  return make_int2(bc + lo16(r), bc + hi16(r));
+}
 
 // A set of elements: the range [base, base+n_range) followed by list[0..n_list).
 struct Span {
@@ -178,6 +212,39 @@ __device__ __forceinline__ void apply_op(const Op& op_in, int32_t i, double d) {
   }
 }
 
+// Ring edge ids (six slots), ring size and sign bits of cell i on a
+// deg_max == 6 mesh: from the 16-bit record unless the warp holds a wide cell.
+__device__ __forceinline__ void ring_ids(const DevMesh& M, int32_t i, int32_t (&ce)[kFastDeg],
+                                         int& deg, uint8_t* sbits = nullptr) {
+  bool wide = true;
+  if (M.c_rec) {
+    const uint4 r = M.c_rec[i];
+    deg = int(r.w & 0x7Fu);
+    if (sbits) *sbits = uint8_t(r.w >> 8);
+    wide = __any_sync(__activemask(), r.w & 0x80u);
+    if (!wide) {
+      const int32_t be = pbase(i, M.rq_ec, M.rf_ec);
+      ce[0] = be + lo16(r.x);
+      ce[1] = be + hi16(r.x);
+      ce[2] = be + lo16(r.y);
+      ce[3] = be + hi16(r.y);
+      ce[4] = be + lo16(r.z);
+      ce[5] = be + hi16(r.z);
+    }
+  } else {
+    deg = M.c_deg[i];
+    if (sbits) *sbits = M.c_sbits[i];
+  }
+  if (wide) {
+#pragma unroll
+    for (int k = 0; k < kFastDeg / 2; ++k) {
+      const int2 p = M.c_edge2[k * M.nC + i];
+      ce[2 * k] = p.x;
+      ce[2 * k + 1] = p.y;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Phase A: potential vorticity on the closure vertices (operators.cpp:74-86)
 // and kinetic energy -> Bernoulli potential psi on the closure cells
@@ -195,10 +262,25 @@ __device__ __forceinline__ void item_vertex_cell(const DevMesh& M, const double*
   const int32_t nv = vs.n();
   if (t < nv) {
     const int32_t v = vs.at(t);
-    const uint8_t sb = M.v_sbits[v];
+    uint8_t sb;
     int2 ce[3];
+    if (M.v_rec) {
+      const uint4 r = M.v_rec[v];
+      sb = uint8_t(r.w & 7u);
+      if (!__any_sync(__activemask(), r.w & 0x80u)) {
+        const int32_t bc = pbase(v, M.rq_cv, M.rf_cv), be = pbase(v, M.rq_ev, M.rf_ev);
+        ce[0] = make_int2(bc + lo16(r.x), be + hi16(r.y));
+        ce[1] = make_int2(bc + hi16(r.x), be + lo16(r.z));
+        ce[2] = make_int2(bc + lo16(r.y), be + hi16(r.z));
+      } else {
 #pragma unroll
-    for (int k = 0; k < 3; ++k) ce[k] = M.v_ce[k * M.nV + v];
+        for (int k = 0; k < 3; ++k) ce[k] = M.v_ce[k * M.nV + v];
+      }
+    } else {
+      sb = M.v_sbits[v];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) ce[k] = M.v_ce[k * M.nV + v];
+    }
     double hv = 0.0, circ = 0.0;
 #pragma unroll
     for (int k = 0; k < 3; ++k) hv += M.v_kite[k * M.nV + v] * h[ce[k].x];
@@ -222,19 +304,14 @@ __device__ __forceinline__ void item_vertex_cell(const DevMesh& M, const double*
     pv[v] = (af.y + circ / af.x) / hv;
   } else if (t - nv < ks.n()) {
     const int32_t i = ks.at(t - nv);
-    const int deg = M.c_deg[i];
+    int deg;
     double acc = 0.0;
     if (M.deg_max == kFastDeg) {
       // all ring ids first, then all gathers: the loads of one cell are
       // independent and issue back to back (padding slots hold id 0, a
       // valid edge, and are not accumulated)
       int32_t ce[kFastDeg];
-#pragma unroll
-      for (int k = 0; k < kFastDeg / 2; ++k) {
-        const int2 p = M.c_edge2[k * M.nC + i];
-        ce[2 * k] = p.x;
-        ce[2 * k + 1] = p.y;
-      }
+      ring_ids(M, i, ce, deg);
 #pragma unroll
       for (int j = 0; j < kFastDeg; ++j) {
         const double ue = u[ce[j]];
@@ -242,6 +319,7 @@ __device__ __forceinline__ void item_vertex_cell(const DevMesh& M, const double*
         if (j < deg) acc += x;
       }
     } else {
+      deg = M.c_deg[i];
       for (int j = 0; j < deg; ++j) {
         const int32_t e = M.c_edge[j * M.nC + i];
         const double ue = u[e];
@@ -276,8 +354,21 @@ __device__ __forceinline__ void item_edge_fq(const DevMesh& M, const double* __r
                                              double2* __restrict__ FQ, int32_t t) {
   if (t >= es.n()) return;
   const int32_t e = es.at(t);
-  const int2 c = M.e_cells[e];
-  const int2 v = M.e_verts[e];
+  int2 c, v;
+  bool wide = true;
+  if (M.e_cv16) {
+    const uint2 r = M.e_cv16[e];
+    wide = __any_sync(__activemask(), has_sentinel16(r.x) || has_sentinel16(r.y));
+    if (!wide) {
+      const int32_t bc = pbase(e, M.rq_ce, M.rf_ce), bv = pbase(e, M.rq_ve, M.rf_ve);
+      c = make_int2(bc + lo16(r.x), bc + hi16(r.x));
+      v = make_int2(bv + lo16(r.y), bv + hi16(r.y));
+    }
+  }
+  if (wide) {
+    c = M.e_cells[e];
+    v = M.e_verts[e];
+  }
   const double F = 0.5 * (h[c.x] + h[c.y]) * u[e];
   const double q = 0.5 * (pv[v.x] + pv[v.y]);
   FQ[e] = make_double2(F, q);
@@ -316,17 +407,12 @@ __device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __re
     const int g = a.ckey ? a.ckey[i] : 0;
     if (g > 5 || !((a.mask >> g) & 1u)) return;  // 0xFF: not an output of this rank
     const int seg = g <= 2 ? 0 : 1;
-    const int deg = M.c_deg[i];
-    const uint8_t sb = M.c_sbits[i];
+    int deg;
+    uint8_t sb;
     double acc = 0.0;
     if (M.deg_max == kFastDeg) {
       int32_t ce[kFastDeg];
-#pragma unroll
-      for (int k = 0; k < kFastDeg / 2; ++k) {
-        const int2 p = M.c_edge2[k * M.nC + i];
-        ce[2 * k] = p.x;
-        ce[2 * k + 1] = p.y;
-      }
+      ring_ids(M, i, ce, deg, &sb);
 #pragma unroll
       for (int j = 0; j < kFastDeg; ++j) {
         const double l = M.e_len[ce[j]];
@@ -334,6 +420,8 @@ __device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __re
         if (j < deg) acc += x;
       }
     } else {
+      deg = M.c_deg[i];
+      sb = M.c_sbits[i];
 #pragma unroll
       for (int j = 0; j < kMaxDeg; ++j) {
         if (j < deg) {
@@ -352,7 +440,12 @@ __device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __re
     const int seg = g <= 1 ? 0 : 1;
     const double qt_e = FQ[e].y;
     const double inv_d = M.e_invd[e];
-    const int2 cc = M.e_cells[e];
+    const int nstw = M.e_nst[e];  // bits 0-5 stencil length, 6: e_c16 wide, 7: e_st16 wide
+    // (c0, c1) for psi: 16-bit offsets (e_c16, or the spare sixth word of
+    // the e_st16 row on ten-entry stencils) unless the warp holds an edge
+    // whose offsets do not fit (e_nst bit 6)
+    const bool wide_c = !M.e_c16 || __any_sync(__activemask(), nstw & 0x40);
+    int2 cc;
     double pvflux = 0.0;
     {
       // Stencil ids as 16-bit offsets from e (20 B/edge instead of 40 B);
@@ -360,8 +453,7 @@ __device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __re
       // ~1 % of edges, along the curve's seams) reads the int32 table
       // instead.  The vote keeps the path warp-uniform, so the ten gathers
       // stay back to back.
-      const int nstw = M.e_nst[e];
-      const int nst = nstw & 0x7f;
+      const int nst = nstw & 0x3f;
       const bool wide = !M.e_st16 || __any_sync(__activemask(), nstw & 0x80);
       if (!wide && M.sten_max == kFastSten) {
         // straight line: three 8 B loads of packed id words, then batches
@@ -369,10 +461,12 @@ __device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __re
         // accumulation (padding entries hold valid ids and are skipped)
         uint32_t w[kFastSten / 2 + 1];
 #pragma unroll
-        for (int k = 0; k < (kFastSten / 2 + 1) / 2; ++k) {
+        for (int k = (kFastSten / 2 + 1) / 2 - 1; k >= 0; --k) {
           const uint2 p = M.e_st16[k * M.nE + e];
           w[2 * k] = p.x;
           w[2 * k + 1] = p.y;
+          if (k == (kFastSten / 2 + 1) / 2 - 1)
+            cc = wide_c ? M.e_cells[e] : c16_cells(M, e, w[kFastSten / 2]);
         }
 #pragma unroll
         for (int j0 = 0; j0 < kFastSten; j0 += 2 * MSWM_KOUT_BATCH) {
@@ -400,6 +494,7 @@ __device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __re
         }
       } else if (M.sten_max == kFastSten) {
         // the int32 ids (~9 % of warps on C4), same straight-line batches
+        cc = wide_c ? M.e_cells[e] : c16_cells(M, e, M.e_c16[e]);
 #pragma unroll
         for (int j0 = 0; j0 < kFastSten; j0 += 2 * MSWM_KOUT_BATCH) {
           double2 c[MSWM_KOUT_BATCH];
@@ -423,6 +518,7 @@ __device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __re
           }
         }
       } else {
+        cc = wide_c ? M.e_cells[e] : c16_cells(M, e, M.e_c16[e]);
 #pragma unroll
         for (int j = 0; j < kMaxSten; ++j) {
           if (j < nst) {
@@ -740,6 +836,57 @@ __global__ void k_reach_ev(DevMesh M, const uint64_t* __restrict__ cr, uint64_t*
   } else if (t - M.nE < M.nV) {
     const int32_t v = t - M.nE;
     vr[v] = cr[M.v_cell[v]] | cr[M.v_cell[M.nV + v]] | cr[M.v_cell[2 * M.nV + v]];
+  }
+}
+
+// Partition of the mesh for N ranks (partition.cpp:219-231, 338-353).
+// Region class of a cell: 0 fine (incl. underline), 1 coarse, 2 interface
+// (partition.cpp:16-25); of an edge: 0 fine / underline fine, 1 coarse, 2
+// interfaces (:27-37).
+__device__ __forceinline__ uint8_t part_cell_class(uint8_t label) {
+  return label == 0 ? 0 : (label == 3 ? 1 : 2);
+}
+// key[k] = class of the k-th cell of the sweep (ord: internal ids)
+__global__ void k_part_class(int32_t n, const int32_t* __restrict__ ord,
+                             const uint8_t* __restrict__ label, uint8_t* __restrict__ key) {
+  const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) key[k] = part_cell_class(label[ord[k]]);
+}
+// lst: sweep positions grouped by class (ascending inside each, sizes t[3]);
+// position p of its class's run goes to part p * N / t (partition.cpp:219-231)
+__global__ void k_part_assign(int32_t n, const int32_t* __restrict__ lst,
+                              const int32_t* __restrict__ ord, int64_t t0, int64_t t1, int64_t t2,
+                              int n_parts, int32_t* __restrict__ rank) {
+  const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  int64_t base = 0, t = t0;
+  if (j >= t0 + t1) {
+    base = t0 + t1;
+    t = t2;
+  } else if (j >= t0) {
+    base = t0;
+    t = t1;
+  }
+  rank[ord[lst[j]]] = int32_t((int64_t(j) - base) * n_parts / t);
+}
+// owner of an edge: the rank of its first cell (edge_cells order) whose class
+// is the edge's (partition.cpp:338-353); bad = lowest edge without one
+__global__ void k_part_edge_owner(DevMesh M, const uint8_t* __restrict__ clabel,
+                                  const uint8_t* __restrict__ elabel,
+                                  const int32_t* __restrict__ rank, int32_t* __restrict__ owner,
+                                  int32_t* __restrict__ bad) {
+  const int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= M.nE) return;
+  const uint8_t el = elabel[e];
+  const uint8_t ec = el <= 1 ? 0 : (el == 4 ? 1 : 2);
+  const int2 c = M.e_cells[e];
+  if (part_cell_class(clabel[c.x]) == ec) {
+    owner[e] = rank[c.x];
+  } else if (part_cell_class(clabel[c.y]) == ec) {
+    owner[e] = rank[c.y];
+  } else {
+    owner[e] = -1;
+    atomicMin(bad, e);
   }
 }
 

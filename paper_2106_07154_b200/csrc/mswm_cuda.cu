@@ -258,6 +258,12 @@ struct mswm_cuda_ctx {
   DArr<uint2> e_st16;
   DArr<double2> e_coef2, v_af;
   DArr<int2> c_edge2, v_ce;
+  DArr<uint4> v_rec, c_rec;      // 16-bit index records (kernels.cuh DevMesh)
+  DArr<uint2> e_cv16;
+  DArr<uint32_t> e_c16;
+  bool pack16 = false;
+  int64_t n_wide16[3] = {0, 0, 0};  // vertices, cells, edges with an offset outside int16
+  uint32_t rq[5] = {0}, rf[5] = {0};  // base ratios: ce, ve, cv, ev, ec
   int64_t n_sten_wide = 0;
   DArr<uint8_t> c_deg, c_sbits, v_sbits, e_nst;
   DArr<double> c_area, v_kite, v_area, e_len, e_ld, e_dual, e_invd, b, f;
@@ -407,6 +413,15 @@ struct mswm_cuda_ctx {
     M.c_edge2 = c_edge2.p;
     M.v_ce = v_ce.p;
     M.v_af = v_af.p;
+    M.v_rec = pack16 ? v_rec.p : nullptr;
+    M.c_rec = pack16 && c_rec.p ? c_rec.p : nullptr;
+    M.e_cv16 = pack16 ? e_cv16.p : nullptr;
+    M.e_c16 = pack16 ? e_c16.p : nullptr;
+    M.rq_ce = rq[0]; M.rf_ce = rf[0];
+    M.rq_ve = rq[1]; M.rf_ve = rf[1];
+    M.rq_cv = rq[2]; M.rf_cv = rf[2];
+    M.rq_ev = rq[3]; M.rf_ev = rf[3];
+    M.rq_ec = rq[4]; M.rf_ec = rf[4];
     M.b = b.p;
     M.f = f.p;
     M.g = gravity;
@@ -418,6 +433,11 @@ namespace {
 
 // ---------------------------------------------------------------------------
 // helpers
+
+// host twin of kernels.cuh pbase: q * x + floor(x * f / 2^32), mod 2^32
+int32_t pbase_host(int32_t x, uint32_t q, uint32_t f) {
+  return int32_t(q * uint32_t(x) + uint32_t((uint64_t(uint32_t(x)) * f) >> 32));
+}
 
 void check_ctx(mswm_cuda_ctx* c) {
   if (!c) throw Error(MSWM_E_USAGE, "null context");
@@ -691,6 +711,36 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   // int32 table only (A/B runs)
   const char* s16 = std::getenv("MSWM_ST16");
   const bool use16 = sten_max < 0x80 && !(s16 && s16[0] == '0');
+  // 16-bit index records (kernels.cuh DevMesh: v_rec, c_rec, e_cv16, e_c16);
+  // MSWM_PACK16=0 keeps the int32 tables only (A/B runs)
+  const char* p16 = std::getenv("MSWM_PACK16");
+  c->pack16 = !(p16 && p16[0] == '0');
+  {
+    const int64_t n_of[3] = {nC, nE, nV};  // 0 cells, 1 edges, 2 vertices
+    const int pairs[5][2] = {{0, 1}, {2, 1}, {0, 2}, {1, 2}, {1, 0}};  // (to, from)
+    for (int k = 0; k < 5; ++k) {
+      const uint64_t num = uint64_t(n_of[pairs[k][0]]), den = uint64_t(n_of[pairs[k][1]]);
+      c->rq[k] = uint32_t(num / den);
+      c->rf[k] = uint32_t(((num % den) << 32) / den);
+    }
+  }
+  // offset of id from the base of x under ratio k; 0x8000 (and a wide flag)
+  // when it does not fit
+  auto off16 = [&](int32_t id, int32_t x, int k, bool& wide) -> uint32_t {
+    const int32_t base = pbase_host(x, c->rq[k], c->rf[k]);
+    const int64_t dd = int64_t(id) - base;
+    if (dd < -32767 || dd > 32767) {
+      wide = true;
+      return 0x8000u;
+    }
+    return uint32_t(dd) & 0xFFFFu;
+  };
+  std::vector<uint2> e_cv16;
+  std::vector<uint32_t> e_c16;
+  if (c->pack16) {
+    e_cv16.resize(nE);
+    e_c16.resize(nE);
+  }
   e_nst.resize(nE);
   e_sten.assign(size_t(std::max(sten_max, 1)) * nE, 0);
   e_coef2.assign(size_t((std::max(sten_max, 1) + 1) / 2) * nE, make_double2(0.0, 0.0));
@@ -709,6 +759,18 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
     e_invd[ne] = inv_d;
     const int off = d->edge_edge_offset[e], n = d->edge_edge_offset[e + 1] - off;
     e_nst[ne] = uint8_t(n);
+    if (c->pack16) {
+      bool wc = false, wv = false;
+      const uint32_t a = off16(e_cells[ne].x, ne, 0, wc), b2 = off16(e_cells[ne].y, ne, 0, wc);
+      const uint32_t x = off16(e_verts[ne].x, ne, 1, wv), y = off16(e_verts[ne].y, ne, 1, wv);
+      e_cv16[ne] = make_uint2(a | b2 << 16, x | y << 16);
+      e_c16[ne] = a | b2 << 16;
+      // ten-entry stencils use five of the six words of the e_st16 row: the
+      // sixth carries (c0, c1) for kernel C
+      if (use16 && sten_max == kFastSten) e_st16p[size_t(2) * nE + ne].y = a | b2 << 16;
+      if (wc) e_nst[ne] |= 0x40;
+      c->n_wide16[2] += wc || wv;
+    }
     for (int j = 0; j < n; ++j) {
       const int32_t e2 = d->edge_edges[off + j];
       need(e2 >= 0 && e2 < nE, "stencil id out of range");
@@ -742,6 +804,10 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   put(c->e_st16, e_st16p);
   put(c->e_sten, e_sten);
   put(c->e_nst, e_nst);
+  if (c->pack16) {
+    put(c->e_cv16, e_cv16);
+    put(c->e_c16, e_c16);
+  }
   {
     // packed copies (kernels.cuh DevMesh): pairs of slots / entries per load
     std::vector<int2> c_edge2(size_t((deg_max + 1) / 2) * nC, make_int2(0, 0));
@@ -756,6 +822,35 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
       for (int k = 0; k < 3; ++k)
         v_ce[size_t(k) * nV + v] = make_int2(v_cell[size_t(k) * nV + v], v_edge[size_t(k) * nV + v]);
     put(c->v_ce, v_ce);
+    // 16-bit index records of vertices and cells (e_cv16 / e_c16 above)
+    if (c->pack16) {
+      std::vector<uint4> v_rec(nV);
+      for (int32_t v = 0; v < nV; ++v) {
+        bool w = false;
+        uint32_t o[6];
+        for (int k = 0; k < 3; ++k) {
+          o[k] = off16(v_cell[size_t(k) * nV + v], v, 2, w);
+          o[3 + k] = off16(v_edge[size_t(k) * nV + v], v, 3, w);
+        }
+        c->n_wide16[0] += w;
+        v_rec[v] = make_uint4(o[0] | o[1] << 16, o[2] | o[3] << 16, o[4] | o[5] << 16,
+                              uint32_t(v_sbits[v]) | (w ? 0x80u : 0u));
+      }
+      put(c->v_rec, v_rec);
+      if (deg_max == kFastDeg) {
+        std::vector<uint4> c_rec(nC);
+        for (int32_t i = 0; i < nC; ++i) {
+          bool w = false;
+          uint32_t o[6];
+          for (int j = 0; j < 6; ++j)
+            o[j] = j < c_deg[i] ? off16(c_edge[size_t(j) * nC + i], i, 4, w) : 0u;
+          c->n_wide16[1] += w;
+          c_rec[i] = make_uint4(o[0] | o[1] << 16, o[2] | o[3] << 16, o[4] | o[5] << 16,
+                                uint32_t(c_deg[i]) | (w ? 0x80u : 0u) | uint32_t(c_sbits[i]) << 8);
+        }
+        put(c->c_rec, c_rec);
+      }
+    }
     std::vector<double2> v_af(nV);
     for (int32_t v = 0; v < nV; ++v) v_af[v] = make_double2(v_area[v], 0.0);  // f_v: set_fields
     put(c->v_af, v_af);
@@ -2532,6 +2627,16 @@ int mswm_cuda_stencil_info(const mswm_cuda_ctx* c, int* offsets16, int64_t* n_wi
   return MSWM_OK;
 }
 
+int mswm_cuda_index_info(const mswm_cuda_ctx* c, int* packed16, int64_t* n_wide_vertices,
+                         int64_t* n_wide_cells, int64_t* n_wide_edges) {
+  if (!c) return MSWM_E_USAGE;
+  if (packed16) *packed16 = (c->pack16 ? 1 : 0) | (c->c_rec.p ? 2 : 0);
+  if (n_wide_vertices) *n_wide_vertices = c->n_wide16[0];
+  if (n_wide_cells) *n_wide_cells = c->n_wide16[1];
+  if (n_wide_edges) *n_wide_edges = c->n_wide16[2];
+  return MSWM_OK;
+}
+
 int mswm_cuda_kernels_per_step(mswm_cuda_ctx* c, int64_t* n) {
   if (!c || !n) return MSWM_E_USAGE;
   *n = c->last_kernels_per_step;
@@ -2678,6 +2783,63 @@ int mswm_cuda_halo_reach(mswm_cuda_ctx* c, const int32_t* rank_of_cell, int n_ra
     down(a, cell_reach, c->nC, c->c_new2old);
     down(er, edge_reach, c->nE, c->e_new2old);
     down(vr, vertex_reach, c->nV, c->v_new2old);
+    return int(MSWM_OK);
+  });
+}
+
+int mswm_cuda_partition(mswm_cuda_ctx* c, const int32_t* sweep_order, int n_parts,
+                        int32_t* rank_of_cell, int32_t* edge_owner) {
+  return guard(c, [&] {
+    check_ctx(c);
+    if (!sweep_order) throw Error(MSWM_E_USAGE, "sweep_order is null");
+    if (!c->have_regions || !c->cell_label.p || !c->edge_label.p)
+      throw Error(MSWM_E_USAGE, "partition needs the region map of mswm_cuda_set_regions");
+    const int32_t nC = c->nC, nE = c->nE;
+    if (n_parts < 1 || n_parts > nC) throw Error(MSWM_E_USAGE, "n_parts out of range");
+    cudaStream_t s = c->stream;
+    // sweep in internal ids (and a permutation check)
+    std::vector<int32_t> ord(nC);
+    {
+      std::vector<uint8_t> seen(nC, 0);
+      for (int32_t k = 0; k < nC; ++k) {
+        const int32_t x = sweep_order[k];
+        if (x < 0 || x >= nC || seen[x]) throw Error(MSWM_E_USAGE, "sweep_order is not a permutation");
+        seen[x] = 1;
+        ord[k] = c->identity ? x : c->c_old2new[x];
+      }
+    }
+    DArr<int32_t> d_ord, lst, rank, owner, bad;
+    DArr<uint8_t> key;
+    d_ord.upload(ord, s);
+    key.alloc(nC);
+    k_part_class<<<nblk(nC), kBlock, 0, s>>>(nC, d_ord.p, c->cell_label.p, key.p);
+    CK(cudaGetLastError());
+    const std::vector<int64_t> t = compact(c, key.p, nC, 3, lst);
+    rank.alloc(nC);
+    k_part_assign<<<nblk(nC), kBlock, 0, s>>>(nC, lst.p, d_ord.p, t[0], t[1], t[2], n_parts,
+                                              rank.p);
+    owner.alloc(nE);
+    const int32_t none = INT32_MAX;
+    bad.alloc(1);
+    CK(cudaMemcpyAsync(bad.p, &none, 4, cudaMemcpyHostToDevice, s));
+    k_part_edge_owner<<<nblk(nE), kBlock, 0, s>>>(c->dev(), c->cell_label.p, c->edge_label.p,
+                                                  rank.p, owner.p, bad.p);
+    CK(cudaGetLastError());
+    int32_t first_bad = none;
+    CK(cudaMemcpyAsync(&first_bad, bad.p, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (first_bad != none)
+      throw Error(MSWM_E_TOPOLOGY, "edge " + std::to_string(c->e_new2old[first_bad]) +
+                                       " has no adjacent cell of its own region class");
+    auto down = [&](const DArr<int32_t>& d, int32_t* out, int32_t n, const std::vector<int32_t>& n2o) {
+      if (!out) return;
+      std::vector<int32_t> h(n);
+      CK(cudaMemcpyAsync(h.data(), d.p, size_t(n) * 4, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (int32_t k = 0; k < n; ++k) out[c->identity ? k : n2o[k]] = h[k];
+    };
+    down(rank, rank_of_cell, nC, c->c_new2old);
+    down(owner, edge_owner, nE, c->e_new2old);
     return int(MSWM_OK);
   });
 }

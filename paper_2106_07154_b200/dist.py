@@ -53,10 +53,12 @@ def publish_store(store_dir, wl, device: int = 0, n_ranks: int | None = None) ->
              "edge_label": np.asarray(rm.edge_label, np.uint8),
              "order": np.asarray(wl.mesh.locality_order(), np.int32)}
     if n_ranks:
-        roc = partition_cells(extra["order"], extra["cell_label"], n_ranks)
+        # partition and halo plan on the device (partition.cpp:219-231,
+        # 338-353, 355-392)
+        roc, own = g.partition(extra["order"], n_ranks)
         cr, er, vr = g.halo_reach(roc, n_ranks)
-        extra.update({"rank_of_cell": roc, "cell_reach": cr, "edge_reach": er,
-                      "vertex_reach": vr})
+        extra.update({"rank_of_cell": roc, "edge_owner": own, "cell_reach": cr,
+                      "edge_reach": er, "vertex_reach": vr})
     g.close()
     del g
     store.save_workload(store_dir, wl, extra, digest=False)
@@ -69,11 +71,14 @@ def layout_from_store(store_dir, rank: int, n_ranks: int):
     local mesh and halo plan are materialised."""
     from . import store
     wl, extra = store.load_workload(store_dir, mmap=True)
-    reach = None
+    reach = part = None
     if "cell_reach" in extra and int(np.max(extra["rank_of_cell"])) == n_ranks - 1:
         reach = (extra["cell_reach"], extra["edge_reach"], extra["vertex_reach"])
+        if "edge_owner" in extra:
+            part = (np.asarray(extra["rank_of_cell"]), np.asarray(extra["edge_owner"]))
     lay = DistributedLayout(wl.mesh, extra["cell_label"], extra["cell_sub"], extra["edge_label"],
-                            n_ranks, order=np.asarray(extra["order"]), only=rank, reach=reach)
+                            n_ranks, order=np.asarray(extra["order"]), only=rank, reach=reach,
+                            partition=part)
     return wl, lay
 
 
@@ -82,18 +87,25 @@ class DistributedLayout:
 
     def __init__(self, mesh: Mesh, cell_label, cell_sub, edge_label, n_ranks: int,
                  order: np.ndarray | None = None, only: int | None = None, ctx=None,
-                 reach=None):
+                 reach=None, partition=None):
+        """``partition``: precomputed (rank_of_cell, edge_owner), e.g. the
+        device partition published by rank 0; else partition_cells on the
+        host."""
         self.mesh = mesh
         self.n_ranks = n_ranks
         self.cell_label = np.asarray(cell_label, np.uint8)
         self.cell_sub = np.asarray(cell_sub, np.uint8)
         self.edge_label = np.asarray(edge_label, np.uint8)
         self.order = mesh.locality_order() if order is None else np.asarray(order)
-        self.rank_of_cell = partition_cells(self.order, self.cell_label, n_ranks)
+        own = None
+        if partition is not None:
+            self.rank_of_cell, own = partition
+        else:
+            self.rank_of_cell = partition_cells(self.order, self.cell_label, n_ranks)
         self.locals: list[LocalMesh] = build_local_meshes(mesh, self.cell_label, self.cell_sub,
                                                           self.edge_label, self.rank_of_cell,
                                                           n_ranks, only=only, ctx=ctx,
-                                                          reach=reach)
+                                                          reach=reach, own_edges=own)
         hr = np.empty(mesh.n_cells, np.int64)
         hr[self.order] = np.arange(mesh.n_cells)
         self.hilbert_rank = hr

@@ -56,6 +56,14 @@ def partition_cells(order: np.ndarray, cell_label: np.ndarray, n_parts: int) -> 
     return rank
 
 
+def partition_device(ctx, order: np.ndarray, n_parts: int):
+    """(rank_of_cell, edge_owner) computed on the device by a CudaContext on
+    the global mesh with its region map (mswm_cuda_partition): the same rules
+    as partition_cells and edge_owner, run as a class-keyed order-preserving
+    compaction of the sweep plus one pass over the edges."""
+    return ctx.partition(order, n_parts)
+
+
 def edge_owner(mesh: Mesh, cell_label: np.ndarray, edge_label: np.ndarray,
                rank_of_cell: np.ndarray) -> np.ndarray:
     """Rank owning each edge (partition.cpp:338-353)."""
@@ -151,13 +159,15 @@ def _has(bits: np.ndarray, q: int) -> np.ndarray:
 
 
 def build_local_meshes(mesh: Mesh, cell_label, cell_sub, edge_label, rank_of_cell: np.ndarray,
-                       n_ranks: int, only: int | None = None, ctx=None, reach=None) -> list:
+                       n_ranks: int, only: int | None = None, ctx=None, reach=None,
+                       own_edges: np.ndarray | None = None) -> list:
     """Local meshes and halo plans.  With ``only`` = r, the tables are built
     for rank r alone (the others are None) -- what one process of a
     multi-GPU run needs.  The membership bit sets come from the device when
     ``ctx`` (a CudaContext on ``mesh``) is given (halo_reach), or precomputed
     as ``reach``."""
-    own_e = edge_owner(mesh, cell_label, edge_label, rank_of_cell)
+    own_e = (edge_owner(mesh, cell_label, edge_label, rank_of_cell) if own_edges is None
+             else np.asarray(own_edges))
     co = mesh.cell_offset
     cr, er, vr = reach if reach is not None else halo_reach(mesh, rank_of_cell, n_ranks, ctx)
 

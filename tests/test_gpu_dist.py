@@ -180,3 +180,40 @@ def test_device_halo_plan_equals_host(n_ranks):
         assert all(np.array_equal(x.tables[k], y.tables[k]) for k in x.tables)
         assert {q: v.tolist() for q, v in x.send_cells.items()} == \
             {q: v.tolist() for q, v in y.send_cells.items()}
+
+
+@pytest.mark.parametrize("n_ranks", [1, 3, 8])
+def test_device_partition_equals_host(n_ranks):
+    """The partition computed on the device (mswm_cuda_partition: class-keyed
+    order-preserving compaction of the sweep, partition.cpp:219-231; edge
+    ownership, :338-353) equals partition_cells / edge_owner on the host, on
+    the region-major and the input numbering; bad arguments are usage errors."""
+    from paper_2106_07154_b200.api import CudaContext, UsageError
+    from paper_2106_07154_b200.partition import edge_owner, partition_cells, partition_device
+    for wl in [W.small_sphere(6, seed=47, cap_deg=20.0), W.config1(n_steps=1)]:
+        o = Oracle(wl.mesh, wl.b, wl.f, wl.gravity)
+        o.set_regions(wl.fine_mask, wl.width)
+        cl, cs, el = o.labels()
+        order = wl.mesh.locality_order()
+        roc = partition_cells(order, cl, n_ranks)
+        own = edge_owner(wl.mesh, cl, el, roc)
+        for layout in ["regions", "input"]:
+            ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=layout,
+                              fine_mask=wl.fine_mask)
+            ctx.make_regions(wl.fine_mask, wl.width)
+            droc, down = partition_device(ctx, order, n_ranks)
+            assert np.array_equal(droc, roc) and np.array_equal(down, own)
+            # every class split evenly
+            for k in range(3):
+                sel = np.isin(cl, [0] if k == 0 else ([3] if k == 1 else [1, 2]))
+                cnt = np.bincount(droc[sel], minlength=n_ranks)
+                assert cnt.max() - cnt.min() <= 1
+        with pytest.raises(UsageError):
+            ctx.partition(np.concatenate([order[:-1], order[:1]]), n_ranks)  # not a permutation
+        with pytest.raises(UsageError):
+            ctx.partition(order, 0)
+    lay = DistributedLayout(wl.mesh, cl, cs, el, n_ranks, order=order,
+                            partition=partition_device(ctx, order, n_ranks))
+    ref = DistributedLayout(wl.mesh, cl, cs, el, n_ranks, order=order)
+    for x, y in zip(lay.locals, ref.locals):
+        assert np.array_equal(x.cells, y.cells) and np.array_equal(x.edges, y.edges)

@@ -317,7 +317,8 @@ def test_stepper_drop_in_interface():
 
 
 @pytest.mark.parametrize("kout,env", [("explicit", {"MSWM_ST16": "1"}),
-                                      ("explicit", {"MSWM_ST16": "0"})])
+                                      ("explicit", {"MSWM_ST16": "0"}),
+                                      ("explicit", {"MSWM_ST16": "1", "MSWM_PACK16": "0"})])
 def test_layouts_are_bitwise_equivalent(kout, env, monkeypatch):
     """Results are independent of the device numbering (input, Hilbert,
     region-major, random) and of the stencil-id table (16-bit offsets or the
@@ -508,6 +509,42 @@ def test_stencil_offsets16_bitwise(st16, monkeypatch):
         ctx.advance(Scheme.LTS3, wl.dt, wl.M, 2)
         st = ctx.download()
         assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
+
+
+@pytest.mark.parametrize("pack16", ["1", "0"])
+def test_index_records16_bitwise(pack16, monkeypatch):
+    """16-bit index records of kernels A, B, C (default) against the int32
+    tables: bitwise equal on the region-major numbering (a few wide elements
+    at region seams) and on a random numbering (most elements wide, warps
+    mixing both kinds), sphere (pentagons: padded ring slots) and plane."""
+    monkeypatch.setenv("MSWM_PACK16", pack16)
+    rng = np.random.default_rng(5)
+    for wl in [W.small_sphere(6, seed=37, cap_deg=20.0), W.config1(n_steps=2)]:
+        o = _oracle_for(wl)
+        h_ref, u_ref, _ = o.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, wl.M, 2)
+        for order in ["regions", rng.permutation(wl.mesh.n_cells).astype(np.int32)]:
+            ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order,
+                              fine_mask=wl.fine_mask)
+            info = ctx.index_info()
+            assert info["packed16"] == (pack16 == "1")
+            if pack16 == "1":
+                assert info["cell_records"]
+                if not isinstance(order, str) and wl.mesh.n_edges > 1 << 16:
+                    for k in ("n_wide_vertices", "n_wide_cells", "n_wide_edges"):
+                        assert 0 < info[k], k
+            ctx.make_regions(wl.fine_mask, wl.width)
+            ev = CudaEvaluator(ctx)
+            for mask in LTS3_MASKS:
+                dh1 = np.full(wl.mesh.n_cells, SENTINEL)
+                du1 = np.full(wl.mesh.n_edges, SENTINEL)
+                dh2, du2 = dh1.copy(), du1.copy()
+                ev.eval(wl.h, wl.u, mask, dh1, du1)
+                o.eval(wl.h, wl.u, mask, dh2, du2)
+                assert bits_equal(dh1, dh2) and bits_equal(du1, du2)
+            ctx.upload(State(wl.h, wl.u, 0.0))
+            ctx.advance(Scheme.LTS3, wl.dt, wl.M, 2)
+            st = ctx.download()
+            assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
 
 
 @pytest.mark.parametrize("config", ["c4", "c3"])
