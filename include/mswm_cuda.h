@@ -136,6 +136,21 @@ int mswm_cuda_set_regions(mswm_cuda_ctx* ctx, const uint8_t* fine_mask,
                           uint8_t* cell_sublabel, uint8_t* edge_label,
                           int64_t group_size[11], int* warnings);
 
+/* Check label arrays the caller supplies (caller ids; does not change the
+ * context's own region map) on the device.  Replaces the label checks of
+ * validate_regions (proj/src/regions.cpp:173-288): band distances from the
+ * label-0 set (:213-244), underline sublabels (:247-262; cell_sublabel NULL =
+ * not assigned) and the fine-side-wins edge rule (:265-286; edge_label NULL =
+ * not assigned).  Per check kind k -- 0 value out of range, 1 Interface1
+ * outside 1..w, 2 Interface2 outside w+1..2w, 3 coarse within 2w, 4 wrong
+ * underline sublabel, 5 wrong edge label -- counts[k] = offending elements and
+ * first[k] = the lowest offending id (the one the reference names first), -1
+ * if none.  The group lists of this library are compactions of the labels,
+ * so validate_regions' list-cover checks have no counterpart. */
+int mswm_cuda_validate_labels(mswm_cuda_ctx* ctx, const uint8_t* cell_label,
+                              const uint8_t* cell_sublabel, const uint8_t* edge_label,
+                              int interface_width, int64_t counts[6], int32_t first[6]);
+
 /* Ascending original ids of group g (GroupBit index 0..10), the
  * RegionMap::cells_* / edges_* lists (regions.hpp:35-42). */
 int mswm_cuda_get_group(mswm_cuda_ctx* ctx, int group, int32_t* ids);

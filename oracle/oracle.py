@@ -102,6 +102,7 @@ def ref() -> C.CDLL:
             "ref_regions_labels": (None, [vp, u8p, u8p, u8p]),
             "ref_regions_group": (C.c_int64, [vp, C.c_int, i32p]),
             "ref_regions_validate": (C.c_int, [vp, vp]),
+            "ref_regions_validate_labels": (C.c_int, [vp, vp, u8p, u8p, u8p, C.c_char_p, C.c_int]),
             "ref_eval_create": (vp, [vp, vp, f64p, f64p, C.c_double, C.c_int, C.c_uint64, C.c_int] + E),
             "ref_eval_free": (None, [vp]),
             "ref_eval": (C.c_int, [vp, f64p, f64p, C.c_uint, f64p, f64p] + E
@@ -257,6 +258,18 @@ class RefRegions:
 
     def validate(self):
         return ref().ref_regions_validate(self.mesh.handle, self.handle)
+
+    def validate_labels(self, cell_label, cell_sub, edge_label):
+        """validate_regions on these labels (lists rebuilt from them): its messages."""
+        cl = np.ascontiguousarray(cell_label, np.uint8)
+        cs = np.ascontiguousarray(cell_sub, np.uint8)
+        el = np.ascontiguousarray(edge_label, np.uint8)
+        buf = C.create_string_buffer(1 << 16)
+        n = ref().ref_regions_validate_labels(self.mesh.handle, self.handle, _p(cl, u8p),
+                                              _p(cs, u8p), _p(el, u8p), buf, len(buf))
+        msgs = [x for x in buf.value.decode().split("\n") if x]
+        assert n == len(msgs) or len(buf.value) >= len(buf) - 2
+        return msgs
 
 
 class RefEvaluator:

@@ -264,6 +264,29 @@ int ref_regions_validate(void* mp, void* rp) {
                  .violations.size());
 }
 
+// validate_regions on a copy of the map with the given labels (lists rebuilt
+// from them): the number of violations, messages joined by '\n' in msgs.
+int ref_regions_validate_labels(void* mp, void* rp, const uint8_t* cell_label,
+                                const uint8_t* cell_sub, const uint8_t* edge_label, char* msgs,
+                                int len) {
+  auto* m = static_cast<VoronoiMesh*>(mp);
+  RegionMap r = *static_cast<RegionMap*>(rp);
+  for (int i = 0; i < m->n_cells; ++i) {
+    r.cell_label[i] = CellRegion(cell_label[i]);
+    r.cell_sublabel[i] = CellSub(cell_sub[i]);
+  }
+  for (int e = 0; e < m->n_edges; ++e) r.edge_label[e] = EdgeRegion(edge_label[e]);
+  r.rebuild_groups(m->n_cells, m->n_edges);
+  const RegionReport rep = validate_regions(*m, r);
+  std::string all;
+  for (const auto& v : rep.violations) all += v + "\n";
+  if (msgs && len > 0) {
+    std::strncpy(msgs, all.c_str(), size_t(len) - 1);
+    msgs[len - 1] = 0;
+  }
+  return int(rep.violations.size());
+}
+
 // ---- evaluators -------------------------------------------------------------
 
 // nranks == 0: SerialEvaluator.  nranks >= 1: ThreadedEvaluator over

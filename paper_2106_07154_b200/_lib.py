@@ -174,6 +174,7 @@ def cuda() -> C.CDLL:
             "mswm_cuda_index_info": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int64),
                                                C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
             "mswm_cuda_set_labels": (C.c_int, [vp, u8p, u8p, u8p, u8p, u8p, C.c_int]),
+            "mswm_cuda_validate_labels": (C.c_int, [vp, u8p, u8p, u8p, C.c_int, i64p, i32p]),
             "mswm_cuda_set_halo": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, i32p, i64p, i32p]),
             "mswm_cuda_nccl_unique_id": (C.c_int, [vp]),
             "mswm_cuda_comm_init": (C.c_int, [vp, vp, C.c_int, C.c_int]),

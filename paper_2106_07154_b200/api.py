@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -195,6 +195,23 @@ class RegionMap:
         return [len(g) for g in self.groups]
 
 
+@dataclass
+class RegionReport:
+    """regions.hpp:74-79."""
+    n_fine: int = 0
+    n_if1: int = 0
+    n_if2: int = 0
+    n_coarse: int = 0
+    n_uf1: int = 0
+    n_uf2: int = 0
+    violations: list = field(default_factory=list)
+    counts: list = field(default_factory=list)   # offending elements per check kind
+    first: list = field(default_factory=list)    # lowest offending id per check kind, -1: none
+
+    def ok(self) -> bool:
+        return not self.violations
+
+
 _WARN_TEXT = {1: "no fine cell touches Interface1; underline layers are empty",
               2: "fine region is one layer thick; second underline layer is empty "
                  "(third-order interface prediction degrades)",
@@ -300,6 +317,71 @@ class CudaContext:
         warnings = [_WARN_TEXT[warn.value]] if warn.value else []
         self.regions = RegionMap(cl, cs, el, interface_width, groups, warnings)
         return self.regions
+
+    def validate_regions(self, regions: RegionMap | None = None) -> RegionReport:
+        """validate_regions (regions.cpp:173-288): the label checks on the device
+        (mswm_cuda_validate_labels), the list-cover checks on the group lists."""
+        m = self.mesh
+        r = regions if regions is not None else self.regions
+        if r is None:
+            raise UsageError("no region map to validate")
+        rep = RegionReport()
+        cl = np.ascontiguousarray(r.cell_label, np.uint8)
+        if cl.shape != (m.n_cells,):
+            rep.violations.append("cell label array size mismatch")
+            return rep
+        g = r.groups
+        rep.n_fine = sum(len(x) for x in g[0:3])
+        rep.n_uf1, rep.n_uf2 = len(g[1]), len(g[2])
+        rep.n_if1, rep.n_if2, rep.n_coarse = len(g[3]), len(g[4]), len(g[5])
+
+        def cover(lists, n, what):
+            ids = np.concatenate([np.asarray(x, np.int64) for x in lists]) if lists else \
+                np.zeros(0, np.int64)
+            if ids.size and (ids.min() < 0 or ids.max() >= n):
+                rep.violations.append(f"{what} id out of range in a group list")
+                ids = ids[(ids >= 0) & (ids < n)]
+            seen = np.bincount(ids, minlength=n)
+            bad = np.flatnonzero(seen != 1)
+            if bad.size:
+                i = int(bad[0])
+                rep.violations.append(f"{what} {i} has no region" if seen[i] == 0
+                                      else f"{what} {i} is in several regions")
+
+        cover(g[0:6], m.n_cells, "cell")
+        for k, name in ((1, "1"), (2, "2")):
+            ids = np.asarray(g[k], np.int64)
+            bad = ids[cl[ids] != 0] if ids.size else ids
+            if bad.size:
+                rep.violations.append(
+                    f"underline layer {name} leaves the fine region at cell {int(bad[0])}")
+        cs = None if r.cell_sublabel is None else np.ascontiguousarray(r.cell_sublabel, np.uint8)
+        el = None if r.edge_label is None else np.ascontiguousarray(r.edge_label, np.uint8)
+        if cs is not None and cs.shape != (m.n_cells,):
+            raise UsageError("cell sublabel array size mismatch")
+        if el is not None and el.shape != (m.n_edges,):
+            rep.violations.append("edge label array size mismatch")
+            return rep
+        counts = np.zeros(6, np.int64)
+        first = np.zeros(6, np.int32)
+        self._check(self.lib.mswm_cuda_validate_labels(
+            self.handle, _p(cl, _lib.u8p), None if cs is None else _p(cs, _lib.u8p),
+            None if el is None else _p(el, _lib.u8p), int(r.interface_width),
+            _p(counts, _lib.i64p), _p(first, _lib.i32p)))
+        rep.counts, rep.first = counts.tolist(), first.tolist()
+        w = int(r.interface_width)
+        text = ("cell {i} has an invalid label",
+                f"Interface1 cell {{i}} is not at distance 1..{w} from fine",
+                f"Interface2 cell {{i}} is not at distance {w + 1}..{2 * w} from fine",
+                f"coarse cell {{i}} is too close to fine for width {w}",
+                "fine cell {i} has the wrong underline sublabel",
+                "edge {i} label disagrees with the fine-side-wins rule")
+        for k in range(6):
+            if counts[k]:
+                rep.violations.append(text[k].format(i=int(first[k])))
+        if el is not None:
+            cover(g[6:11], m.n_edges, "edge")
+        return rep
 
     def closure(self, mask: int, kind: int) -> np.ndarray:
         n = C.c_int64(0)

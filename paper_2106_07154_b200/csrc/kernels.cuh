@@ -134,6 +134,29 @@ struct Span {
   }
 };
 
+// Chunk schedule of a two-part launch (kernel A: vertices | cells, kernel C:
+// cells | edges).  Q == 0: part 0's elements, then part 1's.  Otherwise the
+// kSBlock-sized chunks of the two parts are interleaved in proportion --
+// chunk q belongs to part 0 iff c(q + 1) > c(q), c(q) = umulhi(q, ratio) -- so
+// the CTAs resident at any time work on the same stretch of the space-filling
+// curve in both parts and the second part's gathers (u, h; (F, q~)) hit lines
+// the first part's just brought into L2.
+struct Mix {
+  uint32_t ratio;
+  int32_t Q;
+};
+
+// thread's element index under a Mix (-1: none), n0 / n1 = the parts' sizes
+__device__ __forceinline__ int32_t mix_index(const Mix& mx, int32_t q, int32_t n0, int32_t n1) {
+  const uint32_t c0 = __umulhi(uint32_t(q), mx.ratio), c1 = __umulhi(uint32_t(q) + 1u, mx.ratio);
+  if (c1 > c0) {
+    const int32_t t = int32_t(c0) * kSBlock + threadIdx.x;
+    return t < n0 ? t : -1;
+  }
+  const int32_t t = (q - int32_t(c0)) * kSBlock + threadIdx.x;
+  return t < n1 ? n0 + t : -1;
+}
+
 // Stage epilogue fused into the output kernel (integrators.cpp:18-52,
 // 231-274, 370-410).  d is the freshly computed tendency of element i.
 enum OpKind : int {
@@ -334,27 +357,32 @@ __device__ __forceinline__ void item_vertex_cell(const DevMesh& M, const double*
   }
 }
 
+template <bool kMix>
 __global__ void MSWM_KA_BOUNDS k_vertex_cell(DevMesh M, const double* __restrict__ h,
                                              const double* __restrict__ u, Span vs, Span ks,
                                              double* __restrict__ pv, double* __restrict__ K,
                                              unsigned long long* __restrict__ dry,
                                              const int64_t* __restrict__ step_ctr,
-                                             const uint32_t* __restrict__ vmask) {
-  const int32_t n = vs.n() + ks.n();
-  for (int32_t t = blockIdx.x * kSBlock + threadIdx.x; t < n; t += gridDim.x * kSBlock)
-    item_vertex_cell(M, h, u, vs, ks, pv, K, dry, step_ctr, vmask, t);
+                                             const uint32_t* __restrict__ vmask, Mix mx) {
+  if (kMix) {
+    const int32_t n0 = vs.n(), n1 = ks.n();
+    for (int32_t q = blockIdx.x; q < mx.Q; q += gridDim.x) {
+      const int32_t t = mix_index(mx, q, n0, n1);
+      if (t >= 0) item_vertex_cell(M, h, u, vs, ks, pv, K, dry, step_ctr, vmask, t);
+    }
+  } else {
+    const int32_t n = vs.n() + ks.n();
+    for (int32_t t = blockIdx.x * kSBlock + threadIdx.x; t < n; t += gridDim.x * kSBlock)
+      item_vertex_cell(M, h, u, vs, ks, pv, K, dry, step_ctr, vmask, t);
+  }
 }
 
 // Phase B: thickness flux F_e (operators.cpp:61-62) and q~_e (:88-89) on the
 // union of the flux and q~ closures, packed as (F, q~) so the stencil loop
 // of phase C reads both with one 16-byte gather.
-__device__ __forceinline__ void item_edge_fq(const DevMesh& M, const double* __restrict__ h,
-                                             const double* __restrict__ u,
-                                             const double* __restrict__ pv, const Span& es,
-                                             double2* __restrict__ FQ, int32_t t) {
-  if (t >= es.n()) return;
-  const int32_t e = es.at(t);
-  int2 c, v;
+// ids of edge e's two cells and two vertices: 16-bit records unless the warp
+// holds a wide edge
+__device__ __forceinline__ void edge_cv(const DevMesh& M, int32_t e, int2& c, int2& v) {
   bool wide = true;
   if (M.e_cv16) {
     const uint2 r = M.e_cv16[e];
@@ -369,18 +397,63 @@ __device__ __forceinline__ void item_edge_fq(const DevMesh& M, const double* __r
     c = M.e_cells[e];
     v = M.e_verts[e];
   }
+}
+
+__device__ __forceinline__ void item_edge_fq(const DevMesh& M, const double* __restrict__ h,
+                                             const double* __restrict__ u,
+                                             const double* __restrict__ pv, const Span& es,
+                                             double2* __restrict__ FQ, int32_t t) {
+  if (t >= es.n()) return;
+  const int32_t e = es.at(t);
+  int2 c, v;
+  edge_cv(M, e, c, v);
   const double F = 0.5 * (h[c.x] + h[c.y]) * u[e];
   const double q = 0.5 * (pv[v.x] + pv[v.y]);
   FQ[e] = make_double2(F, q);
 }
+
+// edges per thread and loop trip of kernel B (independent loads of several
+// edges in flight: B has two dependent load levels and little else to hide them)
+#ifndef MSWM_KB_UNROLL
+#define MSWM_KB_UNROLL 1
+#endif
 
 __global__ void __launch_bounds__(kSBlock) k_edge_fq(DevMesh M, const double* __restrict__ h,
                                                    const double* __restrict__ u,
                                                    const double* __restrict__ pv, Span es,
                                                    double2* __restrict__ FQ) {
   const int32_t n = es.n();
+#if MSWM_KB_UNROLL > 1
+  constexpr int U = MSWM_KB_UNROLL;
+  for (int32_t t0 = blockIdx.x * (kSBlock * U) + threadIdx.x; t0 < n; t0 += gridDim.x * (kSBlock * U)) {
+    int32_t e[U];
+    int2 c[U], v[U];
+    double h0[U], h1[U], ue[U], p0[U], p1[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int32_t t = t0 + k * kSBlock;
+      e[k] = t < n ? es.at(t) : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (e[k] >= 0) edge_cv(M, e[k], c[k], v[k]);
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (e[k] >= 0) {
+        h0[k] = h[c[k].x];
+        h1[k] = h[c[k].y];
+        ue[k] = u[e[k]];
+        p0[k] = pv[v[k].x];
+        p1[k] = pv[v[k].y];
+      }
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (e[k] >= 0) FQ[e[k]] = make_double2(0.5 * (h0[k] + h1[k]) * ue[k], 0.5 * (p0[k] + p1[k]));
+  }
+#else
   for (int32_t t = blockIdx.x * kSBlock + threadIdx.x; t < n; t += gridDim.x * kSBlock)
     item_edge_fq(M, h, u, pv, es, FQ, t);
+#endif
 }
 
 // Phase C: the output tendencies -- dh on out cells (operators.cpp:91-99),
@@ -395,15 +468,12 @@ struct OutArgs {
   uint32_t mask;
   Op cop[2];             // segment 0 = fine groups, 1 = the rest
   Op eop[2];
+  Mix mix;               // chunk schedule of cells | edges
 };
 
-__device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __restrict__ h,
-                                            const double* __restrict__ K,
-                                            const double2* __restrict__ FQ, const Span& cs,
-                                            const Span& es, const OutArgs& a, int32_t t) {
-  const int32_t ncs = cs.n();
-  if (t < ncs) {
-    const int32_t i = cs.at(t);
+__device__ __forceinline__ void item_out_cell(const DevMesh& M, const double2* __restrict__ FQ,
+                                              const OutArgs& a, int32_t i) {
+  {
     const int g = a.ckey ? a.ckey[i] : 0;
     if (g > 5 || !((a.mask >> g) & 1u)) return;  // 0xFF: not an output of this rank
     const int seg = g <= 2 ? 0 : 1;
@@ -433,8 +503,13 @@ __device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __re
     }
     const double dh = -acc / M.c_area[i];
     apply_op(a.cop[seg], i, dh);
-  } else if (t - ncs < es.n()) {
-    const int32_t e = es.at(t - ncs);
+  }
+}
+
+__device__ __forceinline__ void item_out_edge(const DevMesh& M, const double* __restrict__ K,
+                                              const double2* __restrict__ FQ, const OutArgs& a,
+                                              int32_t e) {
+  {
     const int g = a.ekey ? a.ekey[e] : 0;
     if (g > 4 || !((a.mask >> (6 + g)) & 1u)) return;
     const int seg = g <= 1 ? 0 : 1;
@@ -538,19 +613,30 @@ __device__ __forceinline__ void item_out_sp(const DevMesh& M, const double* __re
   }
 }
 
-__device__ __forceinline__ void item_out(const DevMesh& M, const double* __restrict__ h,
-                                         const double* __restrict__ K,
+__device__ __forceinline__ void item_out(const DevMesh& M, const double* __restrict__ K,
                                          const double2* __restrict__ FQ, const OutArgs& a,
                                          int32_t t) {
-  item_out_sp(M, h, K, FQ, a.cs, a.es, a, t);
+  const int32_t ncs = a.cs.n();
+  if (t < ncs)
+    item_out_cell(M, FQ, a, a.cs.at(t));
+  else if (t - ncs < a.es.n())
+    item_out_edge(M, K, FQ, a, a.es.at(t - ncs));
 }
 
 __global__ void MSWM_KOUT_BOUNDS k_out(DevMesh M, const double* __restrict__ h,
                                      const double* __restrict__ K,
                                      const double2* __restrict__ FQ, OutArgs a) {
+  if (a.mix.Q) {
+    const int32_t n0 = a.cs.n(), n1 = a.es.n();
+    for (int32_t q = blockIdx.x; q < a.mix.Q; q += gridDim.x) {
+      const int32_t t = mix_index(a.mix, q, n0, n1);
+      if (t >= 0) item_out(M, K, FQ, a, t);
+    }
+    return;
+  }
   const int32_t n = a.cs.n() + a.es.n();
   for (int32_t t = blockIdx.x * kSBlock + threadIdx.x; t < n; t += gridDim.x * kSBlock)
-    item_out(M, h, K, FQ, a, t);
+    item_out(M, K, FQ, a, t);
 }
 
 // ---------------------------------------------------------------------------
@@ -773,6 +859,68 @@ __global__ void k_edge_labels_and_keys(DevMesh M, const uint8_t* __restrict__ la
   if (t < M.nC) {
     const uint8_t l = label[t], s = sub[t];
     ckey[t] = l == 0 ? s : uint8_t(l + 2);  // 0 plain, 1 uf1, 2 uf2, 3 if1, 4 if2, 5 coarse
+  }
+}
+
+// validate_regions (regions.cpp:173-288) for label arrays the caller supplies:
+// band distances (:213-244), underline sublabels (:247-262, sub null: not
+// assigned) and the fine-side-wins edge rule (:265-286, elabel null: not
+// assigned).  dist holds the BFS layers 1..2w from the label-0 set (-1:
+// farther).  Per check kind the number of offending elements and the lowest
+// original id (the one the reference reports first).
+enum ValidateKind : int {
+  VK_VALUE = 0,    // label / sublabel value out of range, sublabel on a non-fine cell
+  VK_IF1,          // Interface1 cell outside distance 1..w
+  VK_IF2,          // Interface2 cell outside w+1..2w
+  VK_COARSE,       // coarse cell within 2w
+  VK_UNDERLINE,    // fine cell with the wrong underline sublabel
+  VK_EDGE,         // edge label disagrees with the fine-side-wins rule
+  VK_COUNT
+};
+
+__device__ __forceinline__ void validate_hit(int kind, int32_t orig, unsigned long long* count,
+                                             int32_t* first) {
+  atomicAdd(count + kind, 1ull);
+  atomicMin(first + kind, orig);
+}
+
+__global__ void k_validate_labels(DevMesh M, const int32_t* __restrict__ c_nbr,
+                                  const int32_t* __restrict__ dist, int w,
+                                  const uint8_t* __restrict__ label, const uint8_t* __restrict__ sub,
+                                  const uint8_t* __restrict__ elabel,
+                                  const int32_t* __restrict__ c_new2old,
+                                  const int32_t* __restrict__ e_new2old,
+                                  unsigned long long* count, int32_t* first) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < M.nC) {
+    const int l = label[t];
+    const int s = sub ? sub[t] : 0;
+    const int32_t orig = c_new2old[t];
+    if (l > 3 || s > 2 || (l != 0 && s != 0)) {
+      validate_hit(VK_VALUE, orig, count, first);
+    } else {
+      const int d = dist[t] == -1 ? INT32_MAX : dist[t];
+      if (l == 1 && (d < 1 || d > w)) validate_hit(VK_IF1, orig, count, first);
+      if (l == 2 && (d <= w || d > 2 * w)) validate_hit(VK_IF2, orig, count, first);
+      if (l == 3 && d <= 2 * w) validate_hit(VK_COARSE, orig, count, first);
+      if (l == 0 && sub) {
+        bool touch_i1 = false, touch_uf1 = false;
+        const int deg = M.c_deg[t];
+        for (int j = 0; j < deg; ++j) {
+          const int32_t nb = c_nbr[j * M.nC + t];
+          if (label[nb] == 1) touch_i1 = true;
+          if (label[nb] == 0 && sub[nb] == 1) touch_uf1 = true;
+        }
+        const int want = touch_i1 ? 1 : (touch_uf1 ? 2 : 0);
+        if (s != want) validate_hit(VK_UNDERLINE, orig, count, first);
+      }
+    }
+  }
+  if (elabel && t < M.nE) {
+    const int2 c = M.e_cells[t];
+    const int r0 = cell_rank(label[c.x], sub ? sub[c.x] : 0);
+    const int r1 = cell_rank(label[c.y], sub ? sub[c.y] : 0);
+    if (elabel[t] != (r0 < r1 ? r0 : r1)) validate_hit(VK_EDGE, e_new2old[t], count, first);
   }
 }
 

@@ -272,6 +272,10 @@ struct mswm_cuda_ctx {
   // C4 steps than one CTA per 256 elements (CTA churn capped occupancy at
   // ~70 %); MSWM_PERSIST=0 restores one element per thread
   int persist_ctas[3] = {2048 / kSBlock, 2048 / kSBlock, 2048 / kSBlock}, n_sm = 148;  // A, B, C
+  // interleaved chunk schedules (MSWM_MIX): bit 0 kernel A, bit 1 kernel C.
+  // Measured on C4 (profiles/r2_s4_mix_sweep_c4.log): A gains ~1.5 % of the
+  // step (u and h are read once instead of twice), C loses ~2 %.
+  int mix = 1;
   DArr<int2> e_cells, e_verts;
   double gravity = 9.80616;
   bool have_fields = false;
@@ -707,8 +711,9 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   std::vector<uint2> e_st16p;     // [(W+1)/2][nE] u32 word pairs, W = n_words
   std::vector<double2> e_coef2;   // [(sten_max+1)/2][nE] coefficient pairs
   const int n_words = (std::max(sten_max, 1) + 1) / 2;
-  // 16-bit stencil offsets (kernels.cuh item_out_sp); MSWM_ST16=0 keeps the
+  // 16-bit stencil offsets (kernels.cuh item_out_edge); MSWM_ST16=0 keeps the
   // int32 table only (A/B runs)
+  if (const char* me = std::getenv("MSWM_MIX")) c->mix = std::atoi(me);
   const char* s16 = std::getenv("MSWM_ST16");
   const bool use16 = sten_max < 0x80 && !(s16 && s16[0] == '0');
   // 16-bit index records (kernels.cuh DevMesh: v_rec, c_rec, e_cv16, e_c16);
@@ -1184,6 +1189,20 @@ int sgrid(const mswm_cuda_ctx* c, int64_t n, int kernel) {
   return int(p > 0 ? std::min<int64_t>(b, int64_t(p) * c->n_sm) : b);
 }
 
+// Interleaved chunk schedule of a two-part launch (kernels.cuh Mix): ratio =
+// ceil(C0 2^32 / (C0 + C1)) for C0 / C1 chunks of the two parts, Q = the
+// first chunk count that covers both parts.
+Mix make_mix(int64_t n0, int64_t n1) {
+  const uint64_t C0 = uint64_t(nblk(n0, kSBlock)), C1 = uint64_t(nblk(n1, kSBlock));
+  if (C0 == 0 || C1 == 0) return Mix{0u, 0};
+  const uint64_t T = C0 + C1;
+  const uint64_t ratio = ((C0 << 32) + T - 1) / T;  // < 2^32: C0 < T
+  auto c_of = [&](uint64_t q) { return (q * ratio) >> 32; };
+  uint64_t Q = T;
+  while (c_of(Q) < C0 || Q - c_of(Q) < C1) ++Q;
+  return Mix{uint32_t(ratio), int32_t(Q)};
+}
+
 Op op_none() {
   Op o;
   std::memset(&o, 0, sizeof(o));
@@ -1236,8 +1255,13 @@ void launch_eval_once(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, cons
   const Span vs = p.sv.dev(), ks = p.sk.dev(), es = p.se.dev();
   const int64_t na = p.sv.n() + p.sk.n();
   if (na > 0) {
-    k_vertex_cell<<<grid(na, 0), kSBlock, 0, s>>>(M, h, u, vs, ks, pv, Kp,
-                                                 c->dry_flag.p, c->step_ctr.p, p.vmask.p);
+    const Mix mx = (c->mix & 1) ? make_mix(p.sv.n(), p.sk.n()) : Mix{0u, 0};
+    if (mx.Q)
+      k_vertex_cell<true><<<grid(na, 0), kSBlock, 0, s>>>(M, h, u, vs, ks, pv, Kp, c->dry_flag.p,
+                                                         c->step_ctr.p, p.vmask.p, mx);
+    else
+      k_vertex_cell<false><<<grid(na, 0), kSBlock, 0, s>>>(M, h, u, vs, ks, pv, Kp, c->dry_flag.p,
+                                                          c->step_ctr.p, p.vmask.p, mx);
     CK(cudaGetLastError());
     ++c->launches;
   }
@@ -1259,6 +1283,7 @@ void launch_eval_once(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, cons
     a.cop[1] = cop[1];
     a.eop[0] = eop[0];
     a.eop[1] = eop[1];
+    a.mix = (c->mix & 2) ? make_mix(p.sc_out.n(), p.se_out.n()) : Mix{0u, 0};
     k_out<<<grid(nout, 2), kSBlock, 0, s>>>(M, h, Kp, FQ, a);
     CK(cudaGetLastError());
     ++c->launches;
@@ -2883,6 +2908,73 @@ int mswm_cuda_set_labels(mswm_cuda_ctx* c, const uint8_t* cell_label, const uint
     }
     c->width = interface_width;
     c->have_regions = true;
+    return int(MSWM_OK);
+  });
+}
+
+int mswm_cuda_validate_labels(mswm_cuda_ctx* c, const uint8_t* cell_label, const uint8_t* cell_sub,
+                              const uint8_t* edge_label, int interface_width, int64_t counts[6],
+                              int32_t first[6]) {
+  return guard(c, [&] {
+    check_ctx(c);
+    if (!cell_label || !counts || !first) throw Error(MSWM_E_USAGE, "null label or output array");
+    if (interface_width < 1) throw Error(MSWM_E_CONFIG, "interface width must be >= 1");
+    const int32_t nC = c->nC, nE = c->nE;
+    const int w = interface_width;
+    cudaStream_t s = c->stream;
+    // labels in internal order; dist = 0 on the label-0 set, -1 elsewhere
+    std::vector<uint8_t> cl(nC), cb(cell_sub ? nC : 0), el(edge_label ? nE : 0);
+    std::vector<int32_t> dist0(nC);
+    host_par_for(nC, [&](int64_t lo, int64_t hi) {
+      for (int64_t ni = lo; ni < hi; ++ni) {
+        const int32_t i = c->c_new2old[ni];
+        cl[ni] = cell_label[i];
+        if (cell_sub) cb[ni] = cell_sub[i];
+        dist0[ni] = cell_label[i] == 0 ? 0 : -1;
+      }
+    });
+    if (edge_label)
+      host_par_for(nE, [&](int64_t lo, int64_t hi) {
+        for (int64_t ne = lo; ne < hi; ++ne) el[ne] = edge_label[c->e_new2old[ne]];
+      });
+    DArr<uint8_t> d_cl, d_cb, d_el;
+    DArr<int32_t> dist, layer_count, d_first, ident_c;
+    DArr<unsigned long long> d_count;
+    d_cl.upload(cl, s);
+    if (cell_sub) d_cb.upload(cb, s);
+    if (edge_label) d_el.upload(el, s);
+    dist.upload(dist0, s);
+    layer_count.alloc(size_t(2 * w) + 1);
+    layer_count.zero(s);
+    const DevMesh M = c->dev();
+    for (int level = 1; level <= 2 * w; ++level) {
+      k_bfs_layer<<<nblk(nC), kBlock, 0, s>>>(M, c->c_nbr.p, dist.p, level, layer_count.p + level);
+      CK(cudaGetLastError());
+    }
+    const int32_t *n2o_c = c->d_c_n2o.p, *n2o_e = c->d_e_n2o.p;
+    if (c->identity) {
+      std::vector<int32_t> id(size_t(std::max(nC, nE)));
+      for (size_t k = 0; k < id.size(); ++k) id[k] = int32_t(k);
+      ident_c.upload(id, s);
+      n2o_c = n2o_e = ident_c.p;
+    }
+    d_count.alloc(VK_COUNT);
+    d_count.zero(s);
+    std::vector<int32_t> f0(VK_COUNT, INT32_MAX);
+    d_first.upload(f0, s);
+    k_validate_labels<<<nblk(std::max(nC, nE)), kBlock, 0, s>>>(
+        M, c->c_nbr.p, dist.p, w, d_cl.p, cell_sub ? d_cb.p : nullptr,
+        edge_label ? d_el.p : nullptr, n2o_c, n2o_e, d_count.p, d_first.p);
+    CK(cudaGetLastError());
+    unsigned long long hc[VK_COUNT];
+    int32_t hf[VK_COUNT];
+    CK(cudaMemcpyAsync(hc, d_count.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hf, d_first.p, sizeof(hf), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int k = 0; k < VK_COUNT; ++k) {
+      counts[k] = int64_t(hc[k]);
+      first[k] = hc[k] ? hf[k] : -1;
+    }
     return int(MSWM_OK);
   });
 }

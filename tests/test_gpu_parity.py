@@ -629,3 +629,75 @@ def test_region_edge_cases_match_reference(ref_lib):
         for a, b in zip(got.groups, rr.groups()):
             assert np.array_equal(a, b)
         assert len(got.warnings) == rr.n_warnings, (width, got.warnings)
+
+
+def _first_ids(msgs):
+    """validate_regions messages -> {check kind: first offending id} (regions.cpp:213-286)."""
+    import re
+    pat = [(1, r"^Interface1 cell (\d+) at distance"), (2, r"^Interface2 cell (\d+) at distance"),
+           (3, r"^coarse cell (\d+) at distance"),
+           (4, r"^fine cell (\d+) has the wrong underline sublabel"),
+           (5, r"^edge (\d+) label disagrees")]
+    out = {}
+    for m in msgs:
+        for kind, p in pat:
+            hit = re.match(p, m)
+            if hit:
+                out.setdefault(kind, int(hit.group(1)))
+    return out
+
+
+@pytest.mark.parametrize("width", [1, 2])
+def test_validate_regions_matches_reference(ref_lib, width):
+    """validate_regions (regions.cpp:173-288) on the device: a valid map
+    passes; labels corrupted one check kind at a time (and all at once) are
+    flagged for the kinds the reference flags, naming the same first element."""
+    from paper_2106_07154_b200.api import RegionMap
+    wl = W.small_sphere(4, seed=5)
+    nC, nE = wl.mesh.n_cells, wl.mesh.n_edges
+    rm = ref_lib.RefMesh.from_mesh(wl.mesh)
+    rr = ref_lib.RefRegions(rm, wl.fine_mask, width)
+    for order in ("input", "hilbert"):  # identity and permuted internal numbering
+        ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order)
+        good = ctx.make_regions(wl.fine_mask, width)
+        rep = ctx.validate_regions()
+        assert rep.ok() and rep.counts == [0] * 6 and rep.first == [-1] * 6
+        assert rr.validate() == 0
+        assert (rep.n_fine, rep.n_if1, rep.n_if2, rep.n_coarse, rep.n_uf1, rep.n_uf2) == (
+            sum(len(g) for g in good.groups[0:3]), len(good.groups[3]), len(good.groups[4]),
+            len(good.groups[5]), len(good.groups[1]), len(good.groups[2]))
+        rng = np.random.default_rng(17)
+
+        def corrupt(kinds):
+            cl, cs, el = good.cell_label.copy(), good.cell_sublabel.copy(), good.edge_label.copy()
+            if 1 in kinds:   # coarse cells relabelled Interface1
+                cl[rng.choice(np.flatnonzero(good.cell_label == 3), 3, replace=False)] = 1
+            if 2 in kinds:   # Interface1 cells relabelled Interface2
+                cl[rng.choice(np.flatnonzero(good.cell_label == 1), 2, replace=False)] = 2
+            if 3 in kinds:   # Interface2 cells relabelled coarse
+                cl[rng.choice(np.flatnonzero(good.cell_label == 2), 4, replace=False)] = 3
+            if 4 in kinds:   # underline layer 1 cells demoted
+                cs[rng.choice(np.flatnonzero(good.cell_sublabel == 1), 2, replace=False)] = 0
+            if 5 in kinds:   # edge labels changed
+                e = rng.choice(nE, 5, replace=False)
+                el[e] = (el[e] + 1) % 5
+            return cl, cs, el
+
+        for kinds in ([1], [2], [3], [4], [5], [1, 2, 3, 4, 5]):
+            cl, cs, el = corrupt(kinds)
+            want = _first_ids(rr.validate_labels(cl, cs, el))
+            assert want, kinds
+            # lists rebuilt from the labels, as the reference shim does
+            ckey = np.where(cl == 0, cs, cl + 2)
+            groups = [np.flatnonzero(ckey == k).astype(np.int32) for k in range(6)] + \
+                     [np.flatnonzero(el == k).astype(np.int32) for k in range(5)]
+            rep = ctx.validate_regions(RegionMap(cl, cs, el, width, groups, []))
+            got = {k: rep.first[k] for k in range(1, 6) if rep.counts[k]}
+            assert got == want, (kinds, got, want)
+            assert not rep.ok() and rep.counts[0] == 0
+    # value checks: a label outside the enum, a sublabel on a non-fine cell
+    cl, cs, el = good.cell_label.copy(), good.cell_sublabel.copy(), good.edge_label.copy()
+    cl[11] = 7
+    cs[int(np.flatnonzero(good.cell_label == 3)[5])] = 1
+    rep = ctx.validate_regions(RegionMap(cl, cs, el, width, good.groups, []))
+    assert rep.counts[0] == 2 and rep.first[0] == min(11, int(np.flatnonzero(good.cell_label == 3)[5]))
