@@ -437,13 +437,18 @@ def run_ours(args, ws, rank, local):
         t1 = time.time()
         wl, lay = layout_from_store(store_dir, rank, ws)
         rc = RankContext(lay, rank, wl.b, wl.f, wl.gravity, wl.width, device=local)
-        if not dry_run:
+        # MSWM_TRANSPORT=nccl (default): ncclSend / ncclRecv inside the step graph;
+        # =peer: stores into the neighbours' IPC-mapped buffers + device flags
+        transport = os.environ.get("MSWM_TRANSPORT", "nccl")
+        if not dry_run and transport == "nccl":
             uid = [RankContext.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(uid, src=0)
             rc.init_nccl(uid[0])
         # exchange only what each evaluation reads (setup-time position swap)
         from paper_2106_07154_b200.api import LTS3_MASKS, kMaskAll
         rc.restrict_halos(LTS3_MASKS + [kMaskAll])
+        if not dry_run and transport == "peer":
+            rc.init_peer()
         rc.upload(wl.h, wl.u)
         barrier(ws)
         if rank == 0:
@@ -626,6 +631,8 @@ def run_ours(args, ws, rank, local):
             "setup": {k: round(v, 2) for k, v in setup.items()},
             "clocks": ck,
         }
+        if ws > 1:
+            line["transport"] = os.environ.get("MSWM_TRANSPORT", "nccl")
         if dry_run and ws > 1:
             line["dry_run"] = "MSWM_HALO_DRYRUN=1: halo transfers skipped -- a check of the path, not a measurement"
         print(json.dumps(line), flush=True)

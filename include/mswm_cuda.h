@@ -363,6 +363,35 @@ int mswm_cuda_group_step(mswm_cuda_group* group, int scheme, double dt, int M,
  * exercised on one GPU without kernels that wait on one another. */
 int mswm_cuda_group_nccl_loopback(mswm_cuda_group* g);
 
+/* ---- peer-store halo transport --------------------------------------------
+ * Halo exchanges without a communication library: the pack kernel stores
+ * into the neighbours' receive buffers through peer-mapped pointers (CUDA IPC
+ * between the processes of one box, NVLink / NVSwitch peer access) and raises
+ * a device flag at every neighbour; the unpack kernel waits for its
+ * neighbours' flags (bounded polling: a silent neighbour is reported as
+ * MSWM_E_NCCL by the next synchronous call).  Two launches per exchange inside
+ * the step graph.  Replaces the copy-in of ThreadedEvaluator's ranks
+ * (rank_pool.cpp:127-176) like the NCCL transport does.  Setup, after the
+ * halo plans (mswm_cuda_set_halo, mswm_cuda_set_halo_mask) are final: every rank exports, imports each neighbour's
+ * export (moved by the host, e.g. torch.distributed all_gather_object) and
+ * enables.  A later change of the halo plans drops the transport. */
+
+/* This rank's arena as a 64-byte cudaIpcMemHandle_t (NULL: skip) and the rows
+ * (mask or -1 for the full halo, sending rank, byte offset, bytes between the
+ * two halves, count) of where each neighbour's values land in it.  rows NULL:
+ * query *n_rows. */
+int mswm_cuda_peer_export(mswm_cuda_ctx* ctx, void* ipc_handle, int64_t* rows,
+                          int64_t cap_rows, int64_t* n_rows);
+int mswm_cuda_peer_import(mswm_cuda_ctx* ctx, int peer_rank, const void* ipc_handle,
+                          const int64_t* rows, int64_t n_rows);
+int mswm_cuda_peer_enable(mswm_cuda_ctx* ctx, int on);
+/* One full-halo exchange of the state arrays in two host-ordered halves
+ * (phase 0: pack + store + signal; phase 1: wait + unpack), synchronous. */
+int mswm_cuda_peer_exchange(mswm_cuda_ctx* ctx, int phase);
+/* The same transport between the members of an in-process group (plain
+ * device pointers instead of IPC mappings). */
+int mswm_cuda_group_peer(mswm_cuda_group* group, int on);
+
 const char* mswm_cuda_group_last_error(const mswm_cuda_group* group);
 
 #ifdef __cplusplus

@@ -184,6 +184,11 @@ def cuda() -> C.CDLL:
             "mswm_cuda_halo_reach": (C.c_int, [vp, i32p, C.c_int, u64p, u64p, u64p]),
             "mswm_cuda_partition": (C.c_int, [vp, i32p, C.c_int, i32p, i32p]),
             "mswm_cuda_group_nccl_loopback": (C.c_int, [vp]),
+            "mswm_cuda_group_peer": (C.c_int, [vp, C.c_int]),
+            "mswm_cuda_peer_export": (C.c_int, [vp, vp, i64p, C.c_int64, i64p]),
+            "mswm_cuda_peer_import": (C.c_int, [vp, C.c_int, vp, i64p, C.c_int64]),
+            "mswm_cuda_peer_enable": (C.c_int, [vp, C.c_int]),
+            "mswm_cuda_peer_exchange": (C.c_int, [vp, C.c_int]),
             "mswm_cuda_group_last_error": (C.c_char_p, [vp]),
         }
         for name, (res, args) in sig.items():

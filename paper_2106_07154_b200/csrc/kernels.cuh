@@ -412,48 +412,16 @@ __device__ __forceinline__ void item_edge_fq(const DevMesh& M, const double* __r
   FQ[e] = make_double2(F, q);
 }
 
-// edges per thread and loop trip of kernel B (independent loads of several
-// edges in flight: B has two dependent load levels and little else to hide them)
-#ifndef MSWM_KB_UNROLL
-#define MSWM_KB_UNROLL 1
-#endif
-
+// (2 and 4 edges per thread -- more independent loads in flight, 40 registers
+// -- measured slower on C4: 6.12 / 6.34 vs 5.93 ms per step,
+// profiles/r2_s4_kernelB_unroll_sweep_c4.log)
 __global__ void __launch_bounds__(kSBlock) k_edge_fq(DevMesh M, const double* __restrict__ h,
                                                    const double* __restrict__ u,
                                                    const double* __restrict__ pv, Span es,
                                                    double2* __restrict__ FQ) {
   const int32_t n = es.n();
-#if MSWM_KB_UNROLL > 1
-  constexpr int U = MSWM_KB_UNROLL;
-  for (int32_t t0 = blockIdx.x * (kSBlock * U) + threadIdx.x; t0 < n; t0 += gridDim.x * (kSBlock * U)) {
-    int32_t e[U];
-    int2 c[U], v[U];
-    double h0[U], h1[U], ue[U], p0[U], p1[U];
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int32_t t = t0 + k * kSBlock;
-      e[k] = t < n ? es.at(t) : -1;
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k)
-      if (e[k] >= 0) edge_cv(M, e[k], c[k], v[k]);
-#pragma unroll
-    for (int k = 0; k < U; ++k)
-      if (e[k] >= 0) {
-        h0[k] = h[c[k].x];
-        h1[k] = h[c[k].y];
-        ue[k] = u[e[k]];
-        p0[k] = pv[v[k].x];
-        p1[k] = pv[v[k].y];
-      }
-#pragma unroll
-    for (int k = 0; k < U; ++k)
-      if (e[k] >= 0) FQ[e[k]] = make_double2(0.5 * (h0[k] + h1[k]) * ue[k], 0.5 * (p0[k] + p1[k]));
-  }
-#else
   for (int32_t t = blockIdx.x * kSBlock + threadIdx.x; t < n; t += gridDim.x * kSBlock)
     item_edge_fq(M, h, u, pv, es, FQ, t);
-#endif
 }
 
 // Phase C: the output tendencies -- dh on out cells (operators.cpp:91-99),
@@ -766,6 +734,102 @@ __global__ void k_unpack_pred(int64_t n, const int32_t* __restrict__ code,
       h[c] = buf[k];
     else
       u[~c] = buf[k];
+  } else if (k - n < int64_t(pa.nc) + pa.ne) {
+    item_predict(pa, int32_t(k - n));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Peer-store halo transport: the pack kernel stores straight into the
+// receivers' buffers through peer-mapped pointers (CUDA IPC between processes,
+// NVLink / NVSwitch peer access; plain pointers inside an in-process group)
+// and then raises a flag at every neighbour; the unpack kernel waits for its
+// neighbours' flags.  One exchange = two launches and no library call.
+//
+// Protocol (per channel: 0 = main schedule, 1 = the concurrent coarse stage):
+// every rank performs the same sequence of exchanges on a channel, and every
+// exchange signals and awaits ALL neighbours (also those it has no data for), so
+// an exchange is a neighbourhood barrier.  seq = 1, 2, ... counts the channel's
+// exchanges in a device counter (graph replays need no patched arguments);
+// receive regions are double buffered on seq & 1: a sender can run at most
+// one exchange ahead of a neighbour (it needs that neighbour's flag of
+// exchange n + 1, raised after the neighbour's unpack of n in stream order,
+// before it may store exchange n + 2 into the half n used).
+struct PeerSlot {
+  double* dst;                 // the neighbour's receive region for this rank's values (half 0)
+  int64_t stride;              // doubles between the two halves of that region
+  unsigned long long* flag;    // the neighbour's flag word for (channel 0, this rank)
+  int64_t soff;                // first send item of this slot
+};
+
+__device__ __forceinline__ unsigned long long ld_flag(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_flag(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// pack + store into the neighbours' buffers + signal.  chan[0] = seq of the
+// channel's last finished exchange, chan[1] = block arrival counter (as u64).
+__global__ void k_push(int64_t n, const int32_t* __restrict__ code, const uint8_t* __restrict__ sslot,
+                       const double* __restrict__ h, const double* __restrict__ u,
+                       const PeerSlot* __restrict__ slots, int np, int flag_stride,
+                       unsigned long long* chan) {
+  __shared__ bool last;
+  const unsigned long long seq = chan[0] + 1;
+  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < n) {
+    const int32_t c = code[k];
+    const PeerSlot s = slots[sslot[k]];
+    s.dst[int64_t(seq & 1) * s.stride + (k - s.soff)] = c >= 0 ? h[c] : u[~c];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(chan + 1, 1ull) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  // every block's stores are fenced: publish
+  __threadfence_system();
+  for (int j = threadIdx.x; j < np; j += blockDim.x) st_flag(slots[j].flag + flag_stride, seq);
+  if (threadIdx.x == 0) {
+    chan[1] = 0;
+    chan[0] = seq;
+  }
+}
+
+// wait for every neighbour's flag of this exchange, then unpack (and the
+// fused interface-1 prediction, as k_unpack_pred).  flags: this rank's flag
+// words of the channel, indexed by rank; a neighbour that does not answer within
+// the poll budget sets *err (reported as MSWM_E_NCCL by the next synchronous
+// call) instead of hanging the device.
+__global__ void k_wait_unpack(int64_t n, const int32_t* __restrict__ code, const double* rbuf,
+                              int64_t stride, double* __restrict__ h, double* __restrict__ u,
+                              PredArgs pa, const unsigned long long* flags,
+                              const int32_t* __restrict__ peers, int np,
+                              const unsigned long long* chan, int* err) {
+  const unsigned long long seq = chan[0];
+  if (threadIdx.x < np) {
+    const unsigned long long* f = flags + peers[threadIdx.x];
+    unsigned polls = 0;
+    while (ld_flag(f) < seq) {
+      __nanosleep(64);
+      if (++polls > (1u << 24)) {
+        atomicExch(err, 1 + peers[threadIdx.x]);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < n) {
+    const int32_t c = code[k];
+    const double v = __ldcg(rbuf + int64_t(seq & 1) * stride + k);
+    if (c >= 0)
+      h[c] = v;
+    else
+      u[~c] = v;
   } else if (k - n < int64_t(pa.nc) + pa.ne) {
     item_predict(pa, int32_t(k - n));
   }

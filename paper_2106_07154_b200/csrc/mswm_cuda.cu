@@ -173,6 +173,14 @@ struct Halo {
   DArr<int32_t> scode, rcode;
   DArr<double> sbuf, rbuf;
   int64_t ns = 0, nr = 0;
+  // peer-store transport (mswm_cuda_peer_*): this halo's receive region in the
+  // context's arena (two halves of pstride doubles) and, per peer slot, where
+  // this rank's values go in the neighbour's arena
+  double* prbuf = nullptr;
+  int64_t pstride = 0;
+  std::vector<PeerSlot> h_pslots;
+  DArr<PeerSlot> pslots;
+  DArr<uint8_t> sslot;  // peer slot of every send item
   bool active() const { return !peer.empty(); }
 };
 
@@ -247,6 +255,16 @@ struct mswm_cuda_ctx {
   // in-process group over a one-rank NCCL communicator (owned by the group,
   // mswm_cuda_group_nccl_loopback): halo copies as NCCL send/recv to self
   ncclComm_t loop_comm = nullptr, loop_comm2 = nullptr;
+  // peer-store transport: one arena per rank -- flag words [channel][rank],
+  // then every halo's double-buffered receive region -- exported to the
+  // neighbours (CUDA IPC between processes, plain pointers inside a group)
+  int transport = 0;  // 0: NCCL / device copies, 1: peer stores
+  DArr<unsigned char> arena;
+  std::vector<unsigned char*> peer_base;  // neighbours' arenas as mapped here, by rank
+  std::vector<char> peer_ipc;             // opened with cudaIpcOpenMemHandle (to close)
+  DArr<unsigned long long> xchan;         // per channel: exchanges done, block arrivals
+  DArr<int> xerr;                         // 1 + rank of a neighbour that did not signal
+  DArr<int32_t> d_peers;
   std::string last_error;
   int32_t nC = 0, nE = 0, nV = 0, deg_max = 0, sten_max = 0;
   bool identity = true;
@@ -373,6 +391,8 @@ struct mswm_cuda_ctx {
 
   ~mswm_cuda_ctx() {
     drop_graphs();
+    for (size_t r = 0; r < peer_base.size(); ++r)
+      if (peer_base[r] && peer_ipc[r]) cudaIpcCloseMemHandle(peer_base[r]);
     if (nccl_comm2) nccl().CommDestroy(nccl_comm2);
     if (nccl_comm) nccl().CommDestroy(nccl_comm);
     if (ls2) cudaStreamDestroy(ls2);
@@ -928,6 +948,15 @@ void check_dry(mswm_cuda_ctx* c, const char* who = nullptr) {
   unsigned long long v = ~0ull;
   CK(cudaMemcpyAsync(&v, c->dry_flag.p, 8, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  if (c->xerr.p) {
+    int xe = 0;
+    CK(cudaMemcpy(&xe, c->xerr.p, sizeof(xe), cudaMemcpyDeviceToHost));
+    if (xe) {
+      CK(cudaMemset(c->xerr.p, 0, sizeof(xe)));
+      throw Error(MSWM_E_NCCL, "peer-store halo exchange: rank " + std::to_string(xe - 1) +
+                                   " did not signal within the poll budget");
+    }
+  }
   const auto batches = std::move(c->batches);
   c->batches.clear();
   if (v == ~0ull) return;
@@ -1472,6 +1501,36 @@ void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us, unsigned ma
   for (auto* c : cs) any |= c->halo.active();
   if (!any) {
     if (preds) throw Error(MSWM_E_USAGE, "fused prediction without a halo exchange");
+    return;
+  }
+  if (cs[0]->transport == 1 && !(cs.size() == 1 && halo_dry_run())) {
+    // peer stores: pack into the neighbours' buffers and signal; wait and
+    // unpack.  Both launch on every rank for every exchange (the protocol's
+    // neighbourhood barrier, kernels.cuh), also with nothing to move.
+    const int ch = second_comm ? 1 : 0;
+    for (auto* c : cs) {
+      Halo& x = halo_for(c, mask);
+      if (c->transport != 1 || !x.pslots.p) throw Error(MSWM_E_USAGE, "peer transport not enabled on every rank");
+      k_push<<<unsigned(std::max<int64_t>(1, nblk(x.ns))), kBlock, 0, c->ls>>>(
+          x.ns, x.scode.p, x.sslot.p, (c->*hs).p, (c->*us).p, x.pslots.p, int(x.peer.size()),
+          ch * c->n_ranks, c->xchan.p + 2 * ch);
+      CK(cudaGetLastError());
+      ++c->launches;
+    }
+    for (size_t m = 0; m < cs.size(); ++m) {
+      mswm_cuda_ctx* c = cs[m];
+      Halo& x = halo_for(c, mask);
+      PredArgs pa;
+      std::memset(&pa, 0, sizeof(pa));
+      if (preds) pa = (*preds)[m];
+      const int64_t np = int64_t(pa.nc) + pa.ne;
+      k_wait_unpack<<<unsigned(std::max<int64_t>(1, nblk(x.nr + np))), kBlock, 0, c->ls>>>(
+          x.nr, x.rcode.p, x.prbuf, x.pstride, (c->*hs).p, (c->*us).p, pa,
+          reinterpret_cast<const unsigned long long*>(c->arena.p) + ch * c->n_ranks, c->d_peers.p,
+          int(x.peer.size()), c->xchan.p + 2 * ch, c->xerr.p);
+      CK(cudaGetLastError());
+      ++c->launches;
+    }
     return;
   }
   for (auto* c : cs) {
@@ -3030,6 +3089,8 @@ int mswm_cuda_set_halo(mswm_cuda_ctx* c, int rank, int n_ranks, int n_peers, con
     h.rbuf.alloc(size_t(std::max<int64_t>(h.nr, 1)));
     CK(cudaStreamSynchronize(c->stream));
     c->drop_graphs();
+    c->arena.alloc(0);  // the peer-store arena follows the halo plans
+    c->transport = 0;
     c->halo = std::move(h);
     c->halo_mask.clear();
     c->rank = rank;
@@ -3116,7 +3177,197 @@ int mswm_cuda_set_halo_mask(mswm_cuda_ctx* c, unsigned mask, const int64_t* send
     h.h_scode = std::move(sc);
     h.h_rcode = std::move(rc);
     c->drop_graphs();
+    c->arena.alloc(0);
+    c->transport = 0;
+    c->halo.prbuf = nullptr;
+    for (auto& kv : c->halo_mask) kv.second.prbuf = nullptr;
     c->halo_mask[mask] = std::move(h);
+    return int(MSWM_OK);
+  });
+}
+
+
+}  // extern "C"
+
+namespace {
+
+constexpr size_t kArenaAlign = 256;
+size_t arena_align(size_t n) { return (n + kArenaAlign - 1) / kArenaAlign * kArenaAlign; }
+
+// the context's halos in export order: the full halo (key -1), then the
+// per-mask restrictions by ascending mask
+std::vector<std::pair<int64_t, Halo*>> peer_halos(mswm_cuda_ctx* c) {
+  std::vector<std::pair<int64_t, Halo*>> v;
+  v.emplace_back(-1, &c->halo);
+  for (auto& kv : c->halo_mask) v.emplace_back(int64_t(kv.first), &kv.second);
+  return v;
+}
+
+// allocate the arena for the current halo plans (idempotent until they change)
+void peer_prepare(mswm_cuda_ctx* c) {
+  if (!c->halo.active()) throw Error(MSWM_E_USAGE, "peer transport needs a halo plan (mswm_cuda_set_halo)");
+  if (c->arena.p) return;
+  size_t off = arena_align(size_t(2) * c->n_ranks * 8);
+  std::vector<size_t> at;
+  for (auto& kh : peer_halos(c)) {
+    at.push_back(off);
+    off += arena_align(size_t(2) * std::max<int64_t>(kh.second->nr, 1) * 8);
+  }
+  c->arena.alloc(off);
+  c->arena.zero(c->stream);
+  size_t k = 0;
+  for (auto& kh : peer_halos(c)) {
+    kh.second->prbuf = reinterpret_cast<double*>(c->arena.p + at[k++]);
+    kh.second->pstride = std::max<int64_t>(kh.second->nr, 1);
+    kh.second->h_pslots.assign(kh.second->peer.size(), PeerSlot{nullptr, 0, nullptr, 0});
+  }
+  c->xchan.alloc(4);
+  c->xchan.zero(c->stream);
+  c->xerr.alloc(1);
+  c->xerr.zero(c->stream);
+  std::vector<int32_t> peers(c->halo.peer.begin(), c->halo.peer.end());
+  c->d_peers.upload(peers, c->stream);
+  for (size_t r = 0; r < c->peer_base.size(); ++r)
+    if (c->peer_base[r] && c->peer_ipc[r]) cudaIpcCloseMemHandle(c->peer_base[r]);
+  c->peer_base.assign(size_t(c->n_ranks), nullptr);
+  c->peer_ipc.assign(size_t(c->n_ranks), 0);
+  CK(cudaStreamSynchronize(c->stream));
+}
+
+// rows of (mask or -1, sending rank, byte offset, stride bytes, count): where
+// each neighbour's values land in this rank's arena
+std::vector<int64_t> peer_rows(mswm_cuda_ctx* c) {
+  std::vector<int64_t> rows;
+  for (auto& kh : peer_halos(c)) {
+    const Halo& x = *kh.second;
+    for (size_t j = 0; j < x.peer.size(); ++j) {
+      rows.push_back(kh.first);
+      rows.push_back(x.peer[j]);
+      rows.push_back(int64_t(reinterpret_cast<unsigned char*>(x.prbuf + x.roff[j]) - c->arena.p));
+      rows.push_back(x.pstride * 8);
+      rows.push_back(x.rcnt[j]);
+    }
+  }
+  return rows;
+}
+
+void peer_attach(mswm_cuda_ctx* c, int peer_rank, unsigned char* base, bool ipc, const int64_t* rows,
+                 int64_t n_rows) {
+  if (peer_rank < 0 || peer_rank >= c->n_ranks || peer_rank == c->rank)
+    throw Error(MSWM_E_USAGE, "bad peer rank");
+  c->peer_base[size_t(peer_rank)] = base;
+  c->peer_ipc[size_t(peer_rank)] = ipc;
+  for (auto& kh : peer_halos(c)) {
+    Halo& x = *kh.second;
+    for (size_t j = 0; j < x.peer.size(); ++j) {
+      if (x.peer[j] != peer_rank) continue;
+      const int64_t* hit = nullptr;
+      for (int64_t r = 0; r < n_rows; ++r)
+        if (rows[5 * r] == kh.first && rows[5 * r + 1] == c->rank) hit = rows + 5 * r;
+      if (!hit || hit[4] != x.scnt[j])
+        throw Error(MSWM_E_USAGE, "inconsistent halo plans between ranks " + std::to_string(c->rank) +
+                                      " and " + std::to_string(peer_rank));
+      x.h_pslots[j] = PeerSlot{reinterpret_cast<double*>(base + hit[2]), hit[3] / 8,
+                               reinterpret_cast<unsigned long long*>(base) + c->rank, x.soff[j]};
+    }
+  }
+}
+
+void peer_enable(mswm_cuda_ctx* c, bool on) {
+  if (on) {
+    if (!c->arena.p) throw Error(MSWM_E_USAGE, "peer transport: export and import first");
+    for (auto& kh : peer_halos(c)) {
+      Halo& x = *kh.second;
+      std::vector<uint8_t> ss(size_t(std::max<int64_t>(x.ns, 1)), 0);
+      for (size_t j = 0; j < x.peer.size(); ++j) {
+        if (!x.h_pslots[j].dst)
+          throw Error(MSWM_E_USAGE, "peer transport: rank " + std::to_string(x.peer[j]) + " not imported");
+        for (int64_t k = 0; k < x.scnt[j]; ++k) ss[size_t(x.soff[j] + k)] = uint8_t(j);
+      }
+      if (x.peer.size() > 255) throw Error(MSWM_E_USAGE, "peer transport: more than 255 neighbours");
+      x.pslots.upload(x.h_pslots, c->stream);
+      x.sslot.upload(ss, c->stream);
+    }
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  c->transport = on ? 1 : 0;
+  c->fork_state = 0;
+  c->drop_graphs();
+}
+
+}  // namespace
+
+extern "C" {
+
+int mswm_cuda_peer_export(mswm_cuda_ctx* c, void* ipc_handle, int64_t* rows, int64_t cap_rows,
+                          int64_t* n_rows) {
+  return guard(c, [&] {
+    check_ctx(c);
+    if (!n_rows) throw Error(MSWM_E_USAGE, "null row count");
+    peer_prepare(c);
+    const std::vector<int64_t> r = peer_rows(c);
+    *n_rows = int64_t(r.size() / 5);
+    if (rows) {
+      if (cap_rows < *n_rows) throw Error(MSWM_E_USAGE, "row buffer too small");
+      std::copy(r.begin(), r.end(), rows);
+    }
+    if (ipc_handle) {
+      cudaIpcMemHandle_t hnd;
+      CK(cudaIpcGetMemHandle(&hnd, c->arena.p));
+      static_assert(sizeof(hnd) == 64, "cudaIpcMemHandle_t is 64 bytes");
+      std::memcpy(ipc_handle, &hnd, sizeof(hnd));
+    }
+    return int(MSWM_OK);
+  });
+}
+
+int mswm_cuda_peer_import(mswm_cuda_ctx* c, int peer_rank, const void* ipc_handle, const int64_t* rows,
+                          int64_t n_rows) {
+  return guard(c, [&] {
+    check_ctx(c);
+    if (!ipc_handle || (n_rows && !rows)) throw Error(MSWM_E_USAGE, "null handle or rows");
+    peer_prepare(c);
+    if (peer_rank >= 0 && peer_rank < c->n_ranks && c->peer_base[size_t(peer_rank)] &&
+        c->peer_ipc[size_t(peer_rank)]) {
+      cudaIpcCloseMemHandle(c->peer_base[size_t(peer_rank)]);
+      c->peer_base[size_t(peer_rank)] = nullptr;
+    }
+    cudaIpcMemHandle_t hnd;
+    std::memcpy(&hnd, ipc_handle, sizeof(hnd));
+    void* base = nullptr;
+    CK(cudaIpcOpenMemHandle(&base, hnd, cudaIpcMemLazyEnablePeerAccess));
+    peer_attach(c, peer_rank, static_cast<unsigned char*>(base), true, rows, n_rows);
+    return int(MSWM_OK);
+  });
+}
+
+int mswm_cuda_peer_enable(mswm_cuda_ctx* c, int on) {
+  return guard(c, [&] {
+    check_ctx(c);
+    peer_enable(c, on != 0);
+    return int(MSWM_OK);
+  });
+}
+
+int mswm_cuda_peer_exchange(mswm_cuda_ctx* c, int phase) {
+  return guard(c, [&] {
+    check_ctx(c);
+    if (c->transport != 1) throw Error(MSWM_E_USAGE, "peer transport not enabled");
+    if (phase != 0 && phase != 1) throw Error(MSWM_E_USAGE, "phase must be 0 (push) or 1 (wait + unpack)");
+    Halo& x = c->halo;
+    if (phase == 0) {
+      k_push<<<unsigned(std::max<int64_t>(1, nblk(x.ns))), kBlock, 0, c->stream>>>(
+          x.ns, x.scode.p, x.sslot.p, c->H.p, c->U.p, x.pslots.p, int(x.peer.size()), 0, c->xchan.p);
+    } else {
+      PredArgs pa;
+      std::memset(&pa, 0, sizeof(pa));
+      k_wait_unpack<<<unsigned(std::max<int64_t>(1, nblk(x.nr))), kBlock, 0, c->stream>>>(
+          x.nr, x.rcode.p, x.prbuf, x.pstride, c->H.p, c->U.p, pa,
+          reinterpret_cast<const unsigned long long*>(c->arena.p), c->d_peers.p, int(x.peer.size()),
+          c->xchan.p, c->xerr.p);
+    }
+    CK(cudaGetLastError());
+    check_dry(c);
     return int(MSWM_OK);
   });
 }
@@ -3266,6 +3517,34 @@ int mswm_cuda_group_nccl_loopback(mswm_cuda_group* g) {
       c->loop_comm = g->loop;
       c->loop_comm2 = g->loop2;
       c->drop_graphs();
+    }
+    g->drop_graphs();
+    return int(MSWM_OK);
+  });
+  if (rc) g->last_error = c0->last_error;
+  return rc;
+}
+
+int mswm_cuda_group_peer(mswm_cuda_group* g, int on) {
+  if (!g) return MSWM_E_USAGE;
+  mswm_cuda_ctx* c0 = g->members[0];
+  const int rc = guard(c0, [&] {
+    CK(cudaSetDevice(c0->device));
+    if (on) {
+      for (auto* c : g->members) peer_prepare(c);
+      for (auto* c : g->members)
+        for (auto* d : g->members) {
+          if (c == d) continue;
+          bool nb = false;
+          for (int p : c->halo.peer) nb |= p == d->rank;
+          if (!nb) continue;
+          const std::vector<int64_t> rows = peer_rows(d);
+          peer_attach(c, d->rank, d->arena.p, false, rows.data(), int64_t(rows.size() / 5));
+        }
+    }
+    for (auto* c : g->members) {
+      peer_enable(c, on != 0);
+      if (on) c->loop_comm = c->loop_comm2 = nullptr;
     }
     g->drop_graphs();
     return int(MSWM_OK);

@@ -206,6 +206,43 @@ class RankContext:
         self.ctx._check(self.ctx.lib.mswm_cuda_comm_init(
             self.ctx.handle, C.cast(buf, C.c_void_p), self.rank, self.layout.n_ranks))
 
+    # -- peer-store transport ---------------------------------------------------
+    def peer_export(self) -> tuple[bytes, np.ndarray]:
+        """This rank's arena as a CUDA IPC handle plus the table of where each
+        neighbour's values land in it (after restrict_halos: the arena follows
+        the halo plans)."""
+        n = C.c_int64(0)
+        self.ctx._check(self.ctx.lib.mswm_cuda_peer_export(self.ctx.handle, None, None, 0, C.byref(n)))
+        rows = np.zeros((max(n.value, 1), 5), np.int64)
+        buf = (C.c_char * 64)()
+        self.ctx._check(self.ctx.lib.mswm_cuda_peer_export(
+            self.ctx.handle, C.cast(buf, C.c_void_p), _p(rows, _lib.i64p), rows.shape[0], C.byref(n)))
+        return bytes(buf), rows[:n.value]
+
+    def peer_import(self, peer_rank: int, handle: bytes, rows: np.ndarray):
+        buf = (C.c_char * 64).from_buffer_copy(handle)
+        rows = np.ascontiguousarray(rows, np.int64)
+        self.ctx._check(self.ctx.lib.mswm_cuda_peer_import(
+            self.ctx.handle, int(peer_rank), C.cast(buf, C.c_void_p), _p(rows, _lib.i64p),
+            rows.shape[0]))
+
+    def init_peer(self):
+        """Halo exchanges as stores into the neighbours' buffers (CUDA IPC over
+        NVLink peer access) with device flags instead of NCCL send/recv: the
+        handles and tables travel once over torch.distributed."""
+        import torch.distributed as dist
+        allv = [None] * self.layout.n_ranks
+        dist.all_gather_object(allv, self.peer_export())
+        for q in self._peers:
+            self.peer_import(int(q), *allv[int(q)])
+        self.ctx._check(self.ctx.lib.mswm_cuda_peer_enable(self.ctx.handle, 1))
+
+    def peer_exchange(self, phase: int):
+        """One full-halo exchange of the state in two host-ordered halves (0:
+        pack + store + signal, 1: wait + unpack) -- the cross-process test of
+        the mapping; stepping runs them back to back inside the step graph."""
+        self.ctx._check(self.ctx.lib.mswm_cuda_peer_exchange(self.ctx.handle, int(phase)))
+
     # -- state ---------------------------------------------------------------
     def upload(self, h_global, u_global, time: float = 0.0):
         lm = self.lm
@@ -247,6 +284,13 @@ class CudaGroup:
         """Halo copies as NCCL send/recv to self over a one-rank communicator
         (the NCCL transport's code path on one GPU)."""
         rc = self.lib.mswm_cuda_group_nccl_loopback(self.handle)
+        if rc:
+            _raise(rc, self.lib.mswm_cuda_group_last_error(self.handle).decode())
+
+    def use_peer_stores(self, on: bool = True):
+        """Halo exchanges as stores into the neighbours' buffers plus device
+        flags (the peer-store transport with in-process pointers)."""
+        rc = self.lib.mswm_cuda_group_peer(self.handle, int(on))
         if rc:
             _raise(rc, self.lib.mswm_cuda_group_last_error(self.handle).decode())
 

@@ -217,3 +217,65 @@ def test_device_partition_equals_host(n_ranks):
     ref = DistributedLayout(wl.mesh, cl, cs, el, n_ranks, order=order)
     for x, y in zip(lay.locals, ref.locals):
         assert np.array_equal(x.cells, y.cells) and np.array_equal(x.edges, y.edges)
+
+
+@pytest.mark.parametrize("n_ranks,restrict", [(2, True), (3, False), (4, True)])
+@pytest.mark.parametrize("scheme", [Scheme.LTS3, Scheme.RK4, Scheme.LTS2])
+def test_group_over_peer_stores_bitwise(scheme, n_ranks, restrict):
+    """The peer-store transport inside a group (k_push stores into the
+    neighbours' double-buffered regions and raises their flags, k_wait_unpack
+    consumes them; both channels, graph replays over several steps so both
+    buffer halves and the sequence counters cycle): bitwise the oracle."""
+    wl = W.small_sphere(6, seed=47, cap_deg=25.0)
+    o = Oracle(wl.mesh, wl.b, wl.f, wl.gravity)
+    o.set_regions(wl.fine_mask, wl.width)
+    cl, cs, el = o.labels()
+    dt = wl.dt if scheme in (Scheme.LTS3, Scheme.LTS2) else wl.dt / wl.M
+    h_ref, u_ref, _ = o.step(int(scheme), wl.h, wl.u, 0.0, dt, wl.M, 5)
+    lay = DistributedLayout(wl.mesh, cl, cs, el, n_ranks)
+    ranks = [RankContext(lay, r, wl.b, wl.f, wl.gravity) for r in range(n_ranks)]
+    grp = CudaGroup(ranks)
+    if restrict:
+        grp.restrict_halos(LTS3_MASKS + [kMaskAll])
+    grp.use_peer_stores()
+    for rc in ranks:
+        rc.upload(wl.h, wl.u)
+    grp.advance(scheme, dt, wl.M, 2)
+    grp.advance(scheme, dt, wl.M, 3)
+    if scheme == Scheme.LTS3 and restrict:
+        assert all(rc.ctx.concurrent_coarse() == 1 for rc in ranks)
+    h = np.full(wl.mesh.n_cells, np.nan)
+    u = np.full(wl.mesh.n_edges, np.nan)
+    for rc in ranks:
+        rc.download_owned(h, u)
+    assert bits_equal(h, h_ref) and bits_equal(u, u_ref)
+    # back to device copies: the same group keeps stepping (graphs recaptured)
+    grp.use_peer_stores(False)
+    h2_ref, u2_ref, _ = o.step(int(scheme), h_ref, u_ref, 0.0, dt, wl.M, 1)
+    grp.advance(scheme, dt, wl.M, 1)
+    for rc in ranks:
+        rc.download_owned(h, u)
+    assert bits_equal(h, h2_ref) and bits_equal(u, u2_ref)
+
+
+def test_peer_stores_across_processes():
+    """Two processes on one GPU: each rank maps the other's arena through CUDA
+    IPC (handles and tables over gloo), stores its owned values into it and
+    raises the flag; after a host barrier each unpacks what the other stored
+    (no kernel ever waits on another process)."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    root = Path(__file__).resolve().parents[1]
+    cmd = ["timeout", "600", sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           str(root / "tests" / "peer_ipc_worker.py")]
+    env = dict(os.environ, PYTHONPATH=f"{root}:{root / 'tests'}")
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, cwd=root)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert "PEER_IPC_OK rank 0" in out.stdout and "PEER_IPC_OK rank 1" in out.stdout
