@@ -497,8 +497,17 @@ def run_ours(args, ws, rank, local):
     evms, evnc, evne = ctx.eval_profile()
     k = int(np.argmax(evne))
     alg = BE * evne[k] + BC * evnc[k]
+    # the events sit inside the step graph, so they hold the last replay's
+    # times: the timed region's last step, then the same graph replayed step by
+    # step (events read after each) -- the kernel's average over these launches
+    ev_samples = [float(evms[k])]
+    for _ in range(max(args.steps - 1, 0)):
+        ctx.advance(Scheme.LTS3, wl.dt, wl.M, 1)
+        ev_samples.append(float(ctx.eval_profile()[0][k]))
+    ctx.reset_ledger()
+    ev_mean = float(np.mean(ev_samples))
     hbm, peak_kind = peaks()
-    achieved = alg / (evms[k] / 1e3) / 1e9
+    achieved = alg / (ev_mean / 1e3) / 1e9
     step_alg = BE * edge_per_step + BC * cell_per_step
     traffic = None
     tf = ROOT / "profiles" / f"traffic_{args.config}.json"
@@ -620,7 +629,9 @@ def run_ours(args, ws, rank, local):
                          "peak_kind": peak_kind,
                          "kernel": "tendency evaluation (A: PV+K, B: F,q~, C: dh/du + fused "
                                    f"stage update), out {int(evnc[k])} cells / {int(evne[k])} edges",
-                         "algorithmic_bytes": alg, "ms": float(evms[k]),
+                         "algorithmic_bytes": alg, "ms": ev_mean,
+                         "ms_samples": len(ev_samples), "ms_min": float(np.min(ev_samples)),
+                         "ms_max": float(np.max(ev_samples)),
                          "share_of_step": float(evms.sum() / ms_step)},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": io_bytes,
                     "d2h_bytes_per_step": io_bytes, "steps": n_e2e},

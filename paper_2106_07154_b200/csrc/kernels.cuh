@@ -135,27 +135,17 @@ struct Span {
 };
 
 // Chunk schedule of a two-part launch (kernel A: vertices | cells, kernel C:
-// cells | edges).  Q == 0: part 0's elements, then part 1's.  Otherwise the
-// kSBlock-sized chunks of the two parts are interleaved in proportion --
-// chunk q belongs to part 0 iff c(q + 1) > c(q), c(q) = umulhi(q, ratio) -- so
-// the CTAs resident at any time work on the same stretch of the space-filling
-// curve in both parts and the second part's gathers (u, h; (F, q~)) hit lines
-// the first part's just brought into L2.
-struct Mix {
-  uint32_t ratio;
-  int32_t Q;
+// cells | edges): map[q] = index of the first element of the q-th kSBlock-sized
+// chunk to run (part 0's elements are [0, n0), part 1's [n0, n0 + n1); a chunk
+// never straddles the two).  Null: part 0's elements, then part 1's.  The host
+// (chunk_map in mswm_cuda.cu) interleaves the parts' chunks in proportion, or
+// window by window, so the CTAs resident at any time work on the same stretch
+// of the space-filling curve in both parts and the second part's gathers (u,
+// h; (F, q~)) hit lines the first part's just brought into L2.
+struct ChunkMap {
+  const int32_t* map;
+  int32_t nq;
 };
-
-// thread's element index under a Mix (-1: none), n0 / n1 = the parts' sizes
-__device__ __forceinline__ int32_t mix_index(const Mix& mx, int32_t q, int32_t n0, int32_t n1) {
-  const uint32_t c0 = __umulhi(uint32_t(q), mx.ratio), c1 = __umulhi(uint32_t(q) + 1u, mx.ratio);
-  if (c1 > c0) {
-    const int32_t t = int32_t(c0) * kSBlock + threadIdx.x;
-    return t < n0 ? t : -1;
-  }
-  const int32_t t = (q - int32_t(c0)) * kSBlock + threadIdx.x;
-  return t < n1 ? n0 + t : -1;
-}
 
 // Stage epilogue fused into the output kernel (integrators.cpp:18-52,
 // 231-274, 370-410).  d is the freshly computed tendency of element i.
@@ -357,23 +347,22 @@ __device__ __forceinline__ void item_vertex_cell(const DevMesh& M, const double*
   }
 }
 
-template <bool kMix>
 __global__ void MSWM_KA_BOUNDS k_vertex_cell(DevMesh M, const double* __restrict__ h,
                                              const double* __restrict__ u, Span vs, Span ks,
                                              double* __restrict__ pv, double* __restrict__ K,
                                              unsigned long long* __restrict__ dry,
                                              const int64_t* __restrict__ step_ctr,
-                                             const uint32_t* __restrict__ vmask, Mix mx) {
-  if (kMix) {
-    const int32_t n0 = vs.n(), n1 = ks.n();
-    for (int32_t q = blockIdx.x; q < mx.Q; q += gridDim.x) {
-      const int32_t t = mix_index(mx, q, n0, n1);
-      if (t >= 0) item_vertex_cell(M, h, u, vs, ks, pv, K, dry, step_ctr, vmask, t);
+                                             const uint32_t* __restrict__ vmask, ChunkMap cm) {
+  const int32_t n0 = vs.n(), n = n0 + ks.n();
+  const int32_t nt = cm.map ? cm.nq * kSBlock : n;
+  for (int32_t t = blockIdx.x * kSBlock + threadIdx.x; t < nt; t += gridDim.x * kSBlock) {
+    int32_t tt = t;
+    if (cm.map) {
+      const int32_t base = cm.map[t / kSBlock];
+      tt = base + threadIdx.x;
+      if (tt >= (base < n0 ? n0 : n)) continue;
     }
-  } else {
-    const int32_t n = vs.n() + ks.n();
-    for (int32_t t = blockIdx.x * kSBlock + threadIdx.x; t < n; t += gridDim.x * kSBlock)
-      item_vertex_cell(M, h, u, vs, ks, pv, K, dry, step_ctr, vmask, t);
+    item_vertex_cell(M, h, u, vs, ks, pv, K, dry, step_ctr, vmask, tt);
   }
 }
 
@@ -436,7 +425,7 @@ struct OutArgs {
   uint32_t mask;
   Op cop[2];             // segment 0 = fine groups, 1 = the rest
   Op eop[2];
-  Mix mix;               // chunk schedule of cells | edges
+  ChunkMap cm;           // chunk schedule of cells | edges
 };
 
 __device__ __forceinline__ void item_out_cell(const DevMesh& M, const double2* __restrict__ FQ,
@@ -594,17 +583,17 @@ __device__ __forceinline__ void item_out(const DevMesh& M, const double* __restr
 __global__ void MSWM_KOUT_BOUNDS k_out(DevMesh M, const double* __restrict__ h,
                                      const double* __restrict__ K,
                                      const double2* __restrict__ FQ, OutArgs a) {
-  if (a.mix.Q) {
-    const int32_t n0 = a.cs.n(), n1 = a.es.n();
-    for (int32_t q = blockIdx.x; q < a.mix.Q; q += gridDim.x) {
-      const int32_t t = mix_index(a.mix, q, n0, n1);
-      if (t >= 0) item_out(M, K, FQ, a, t);
+  const int32_t n0 = a.cs.n(), n = n0 + a.es.n();
+  const int32_t nt = a.cm.map ? a.cm.nq * kSBlock : n;
+  for (int32_t t = blockIdx.x * kSBlock + threadIdx.x; t < nt; t += gridDim.x * kSBlock) {
+    int32_t tt = t;
+    if (a.cm.map) {
+      const int32_t base = a.cm.map[t / kSBlock];
+      tt = base + threadIdx.x;
+      if (tt >= (base < n0 ? n0 : n)) continue;
     }
-    return;
+    item_out(M, K, FQ, a, tt);
   }
-  const int32_t n = a.cs.n() + a.es.n();
-  for (int32_t t = blockIdx.x * kSBlock + threadIdx.x; t < n; t += gridDim.x * kSBlock)
-    item_out(M, K, FQ, a, t);
 }
 
 // ---------------------------------------------------------------------------

@@ -149,6 +149,7 @@ struct MaskPlan {
     int64_t n() const { return int64_t(n_range) + n_list; }
   } sv, sk, se, sc_out, se_out;
   DArr<uint32_t> vmask;  // closure bitmask for the dense dry-vertex check
+  DArr<int32_t> cmapA, cmapC;  // chunk schedules of kernels A and C (kernels.cuh ChunkMap)
   std::vector<int32_t> host_cells, host_edges;  // original ids, same order as device lists
   // drop-in eval I/O (mswm_cuda_eval): the h / u entries the evaluation
   // reads, original ids on the host and internal ids on the device (built on
@@ -290,10 +291,12 @@ struct mswm_cuda_ctx {
   // C4 steps than one CTA per 256 elements (CTA churn capped occupancy at
   // ~70 %); MSWM_PERSIST=0 restores one element per thread
   int persist_ctas[3] = {2048 / kSBlock, 2048 / kSBlock, 2048 / kSBlock}, n_sm = 148;  // A, B, C
-  // interleaved chunk schedules (MSWM_MIX): bit 0 kernel A, bit 1 kernel C.
-  // Measured on C4 (profiles/r2_s4_mix_sweep_c4.log): A gains ~1.5 % of the
-  // step (u and h are read once instead of twice), C loses ~2 %.
+  // chunk schedules of the two-part launches (MSWM_MIX): bit 0 kernel A, bit
+  // 1 kernel C interleaved in proportion; bits 2 / 3 windowed.  Measured on C4
+  // (profiles/r2_s4_mix_sweep_c4.log): A interleaved gains ~1.5 % of the step
+  // (u and h are read once instead of twice), C interleaved loses ~2 %.
   int mix = 1;
+  int mix_windows = 64;  // window mode (bits 2 / 3 of MSWM_MIX), MSWM_MIX_WIN
   DArr<int2> e_cells, e_verts;
   double gravity = 9.80616;
   bool have_fields = false;
@@ -734,6 +737,7 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   // 16-bit stencil offsets (kernels.cuh item_out_edge); MSWM_ST16=0 keeps the
   // int32 table only (A/B runs)
   if (const char* me = std::getenv("MSWM_MIX")) c->mix = std::atoi(me);
+  if (const char* me = std::getenv("MSWM_MIX_WIN")) c->mix_windows = std::max(1, std::atoi(me));
   const char* s16 = std::getenv("MSWM_ST16");
   const bool use16 = sten_max < 0x80 && !(s16 && s16[0] == '0');
   // 16-bit index records (kernels.cuh DevMesh: v_rec, c_rec, e_cv16, e_c16);
@@ -1033,6 +1037,7 @@ void make_span(mswm_cuda_ctx* c, const int32_t* d_list, int32_t n, int32_t unive
 }
 
 void finish_plan(mswm_cuda_ctx* c, MaskPlan* p, double out_dense_frac);
+std::vector<int32_t> chunk_map(int64_t n0, int64_t n1, int mode, int n_windows);
 
 MaskPlan& plan_for(mswm_cuda_ctx* c, unsigned mask) {
   auto it = c->plans.find(mask);
@@ -1142,6 +1147,15 @@ void finish_plan(mswm_cuda_ctx* c, MaskPlan* p, double out_dense_frac) {
     k_pack_bits<<<nblk((int64_t(c->nV) + 31) / 32), kBlock, 0, s>>>(c->nV, mv.p, p->vmask.p);
     CK(cudaGetLastError());
   }
+  // chunk schedules of the two-part launches (MSWM_MIX: bits 0 / 1 kernel A /
+  // C interleaved, bits 2 / 3 windowed)
+  {
+    const int ma = (c->mix & 4) ? 2 : (c->mix & 1) ? 1 : 0, mc = (c->mix & 8) ? 2 : (c->mix & 2) ? 1 : 0;
+    const std::vector<int32_t> a = chunk_map(p->sv.n(), p->sk.n(), ma, c->mix_windows);
+    const std::vector<int32_t> o = chunk_map(p->sc_out.n(), p->se_out.n(), mc, c->mix_windows);
+    if (!a.empty()) p->cmapA.upload(a, s);
+    if (!o.empty()) p->cmapC.upload(o, s);
+  }
   // host copies of the output lists (original ids) for the eval ABI
   p->host_cells.resize(p->nc);
   p->host_edges.resize(p->ne);
@@ -1218,18 +1232,36 @@ int sgrid(const mswm_cuda_ctx* c, int64_t n, int kernel) {
   return int(p > 0 ? std::min<int64_t>(b, int64_t(p) * c->n_sm) : b);
 }
 
-// Interleaved chunk schedule of a two-part launch (kernels.cuh Mix): ratio =
-// ceil(C0 2^32 / (C0 + C1)) for C0 / C1 chunks of the two parts, Q = the
-// first chunk count that covers both parts.
-Mix make_mix(int64_t n0, int64_t n1) {
-  const uint64_t C0 = uint64_t(nblk(n0, kSBlock)), C1 = uint64_t(nblk(n1, kSBlock));
-  if (C0 == 0 || C1 == 0) return Mix{0u, 0};
-  const uint64_t T = C0 + C1;
-  const uint64_t ratio = ((C0 << 32) + T - 1) / T;  // < 2^32: C0 < T
-  auto c_of = [&](uint64_t q) { return (q * ratio) >> 32; };
-  uint64_t Q = T;
-  while (c_of(Q) < C0 || Q - c_of(Q) < C1) ++Q;
-  return Mix{uint32_t(ratio), int32_t(Q)};
+// Chunk schedule of a two-part launch (kernels.cuh ChunkMap) for parts of n0
+// and n1 elements.  mode 1: the parts' chunks interleaved in proportion (part
+// 0's chunk count among the first q chunks = floor(q C0 / (C0 + C1))); mode 2:
+// n_windows windows along the curve, each running its part-1 chunks and then
+// its part-0 chunks.  Empty: part 0, then part 1 (no map).
+std::vector<int32_t> chunk_map(int64_t n0, int64_t n1, int mode, int n_windows) {
+  std::vector<int32_t> m;
+  const int64_t C0 = nblk(n0, kSBlock), C1 = nblk(n1, kSBlock);
+  if (mode == 0 || C0 == 0 || C1 == 0) return m;
+  m.reserve(size_t(C0 + C1));
+  auto part0 = [&](int64_t k) { m.push_back(int32_t(k * kSBlock)); };
+  auto part1 = [&](int64_t k) { m.push_back(int32_t(n0 + k * kSBlock)); };
+  if (mode == 1) {
+    const int64_t T = C0 + C1;
+    int64_t k0 = 0, k1 = 0;
+    for (int64_t q = 0; q < T; ++q) {
+      if ((q + 1) * C0 / T > q * C0 / T)
+        part0(k0++);
+      else
+        part1(k1++);
+    }
+  } else {
+    const int64_t nw = std::max(1, n_windows);
+    const int64_t w0 = (C0 + nw - 1) / nw, w1 = (C1 + nw - 1) / nw;
+    for (int64_t k0 = 0, k1 = 0; k0 < C0 || k1 < C1;) {
+      for (int64_t j = 0; j < w1 && k1 < C1; ++j) part1(k1++);
+      for (int64_t j = 0; j < w0 && k0 < C0; ++j) part0(k0++);
+    }
+  }
+  return m;
 }
 
 Op op_none() {
@@ -1284,13 +1316,9 @@ void launch_eval_once(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, cons
   const Span vs = p.sv.dev(), ks = p.sk.dev(), es = p.se.dev();
   const int64_t na = p.sv.n() + p.sk.n();
   if (na > 0) {
-    const Mix mx = (c->mix & 1) ? make_mix(p.sv.n(), p.sk.n()) : Mix{0u, 0};
-    if (mx.Q)
-      k_vertex_cell<true><<<grid(na, 0), kSBlock, 0, s>>>(M, h, u, vs, ks, pv, Kp, c->dry_flag.p,
-                                                         c->step_ctr.p, p.vmask.p, mx);
-    else
-      k_vertex_cell<false><<<grid(na, 0), kSBlock, 0, s>>>(M, h, u, vs, ks, pv, Kp, c->dry_flag.p,
-                                                          c->step_ctr.p, p.vmask.p, mx);
+    k_vertex_cell<<<grid(na, 0), kSBlock, 0, s>>>(M, h, u, vs, ks, pv, Kp, c->dry_flag.p,
+                                                 c->step_ctr.p, p.vmask.p,
+                                                 ChunkMap{p.cmapA.p, int32_t(p.cmapA.n)});
     CK(cudaGetLastError());
     ++c->launches;
   }
@@ -1312,7 +1340,7 @@ void launch_eval_once(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, cons
     a.cop[1] = cop[1];
     a.eop[0] = eop[0];
     a.eop[1] = eop[1];
-    a.mix = (c->mix & 2) ? make_mix(p.sc_out.n(), p.se_out.n()) : Mix{0u, 0};
+    a.cm = ChunkMap{p.cmapC.p, int32_t(p.cmapC.n)};
     k_out<<<grid(nout, 2), kSBlock, 0, s>>>(M, h, Kp, FQ, a);
     CK(cudaGetLastError());
     ++c->launches;
