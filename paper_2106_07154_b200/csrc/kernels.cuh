@@ -407,10 +407,13 @@ __device__ __forceinline__ void item_edge_fq(const DevMesh& M, const double* __r
 __global__ void __launch_bounds__(kSBlock) k_edge_fq(DevMesh M, const double* __restrict__ h,
                                                    const double* __restrict__ u,
                                                    const double* __restrict__ pv, Span es,
-                                                   double2* __restrict__ FQ) {
+                                                   double2* __restrict__ FQ, ChunkMap cm) {
   const int32_t n = es.n();
-  for (int32_t t = blockIdx.x * kSBlock + threadIdx.x; t < n; t += gridDim.x * kSBlock)
-    item_edge_fq(M, h, u, pv, es, FQ, t);
+  const int32_t nt = cm.map ? cm.nq * kSBlock : n;
+  for (int32_t t = blockIdx.x * kSBlock + threadIdx.x; t < nt; t += gridDim.x * kSBlock) {
+    const int32_t tt = cm.map ? cm.map[t / kSBlock] + threadIdx.x : t;
+    item_edge_fq(M, h, u, pv, es, FQ, tt);
+  }
 }
 
 // Phase C: the output tendencies -- dh on out cells (operators.cpp:91-99),

@@ -149,7 +149,9 @@ struct MaskPlan {
     int64_t n() const { return int64_t(n_range) + n_list; }
   } sv, sk, se, sc_out, se_out;
   DArr<uint32_t> vmask;  // closure bitmask for the dense dry-vertex check
-  DArr<int32_t> cmapA, cmapC;  // chunk schedules of kernels A and C (kernels.cuh ChunkMap)
+  // chunk schedules of kernels A and C (kernels.cuh ChunkMap) and, for the
+  // ping-pong order (MSWM_MIX bit 4), their reversals and kernel B's
+  DArr<int32_t> cmapA, cmapC, cmapA_r, cmapB_r, cmapC_r;
   std::vector<int32_t> host_cells, host_edges;  // original ids, same order as device lists
   // drop-in eval I/O (mswm_cuda_eval): the h / u entries the evaluation
   // reads, original ids on the host and internal ids on the device (built on
@@ -295,8 +297,14 @@ struct mswm_cuda_ctx {
   // 1 kernel C interleaved in proportion; bits 2 / 3 windowed.  Measured on C4
   // (profiles/r2_s4_mix_sweep_c4.log): A interleaved gains ~1.5 % of the step
   // (u and h are read once instead of twice), C interleaved loses ~2 %.
-  int mix = 1;
-  int mix_windows = 64;  // window mode (bits 2 / 3 of MSWM_MIX), MSWM_MIX_WIN
+  // C windowed gains ~2 % (its cell pass finds the window's (F, q~) in L2:
+  // profiles/r2_s4_mix_windows_sweep_c4.log); A windowed does not.
+  int mix = 9;
+  // window mode: part-0 elements per window (C4: 64 windows of 164k cells,
+  // ~80 MB of traffic each, inside L2), or a fixed window count (MSWM_MIX_WIN)
+  int flip_main = 0, flip_side = 0;  // ping-pong direction of the next evaluation
+  int mix_window_elems = 163840;
+  int mix_windows = 0;
   DArr<int2> e_cells, e_verts;
   double gravity = 9.80616;
   bool have_fields = false;
@@ -1151,10 +1159,29 @@ void finish_plan(mswm_cuda_ctx* c, MaskPlan* p, double out_dense_frac) {
   // C interleaved, bits 2 / 3 windowed)
   {
     const int ma = (c->mix & 4) ? 2 : (c->mix & 1) ? 1 : 0, mc = (c->mix & 8) ? 2 : (c->mix & 2) ? 1 : 0;
-    const std::vector<int32_t> a = chunk_map(p->sv.n(), p->sk.n(), ma, c->mix_windows);
-    const std::vector<int32_t> o = chunk_map(p->sc_out.n(), p->se_out.n(), mc, c->mix_windows);
+    auto windows = [&](int64_t n0) {
+      return c->mix_windows > 0 ? c->mix_windows
+                                : int(std::max<int64_t>(1, (n0 + c->mix_window_elems - 1) / c->mix_window_elems));
+    };
+    const std::vector<int32_t> a = chunk_map(p->sv.n(), p->sk.n(), ma, windows(p->sv.n()));
+    const std::vector<int32_t> o = chunk_map(p->sc_out.n(), p->se_out.n(), mc, windows(p->sc_out.n()));
     if (!a.empty()) p->cmapA.upload(a, s);
     if (!o.empty()) p->cmapC.upload(o, s);
+    if (c->mix & 16) {
+      // reversed schedules: a kernel that starts where its producer just
+      // finished finds that stretch of the producer's output still in L2
+      auto rev = [&](std::vector<int32_t> m, int64_t n0, int64_t n1, DArr<int32_t>& out) {
+        if (m.empty()) {  // part 0's chunks, then part 1's
+          for (int64_t k = 0; k < nblk(n0, kSBlock); ++k) m.push_back(int32_t(k * kSBlock));
+          for (int64_t k = 0; k < nblk(n1, kSBlock); ++k) m.push_back(int32_t(n0 + k * kSBlock));
+        }
+        std::reverse(m.begin(), m.end());
+        if (!m.empty()) out.upload(m, s);
+      };
+      rev(a, p->sv.n(), p->sk.n(), p->cmapA_r);
+      rev(o, p->sc_out.n(), p->se_out.n(), p->cmapC_r);
+      rev({}, p->se.n(), 0, p->cmapB_r);
+    }
   }
   // host copies of the output lists (original ids) for the eval ABI
   p->host_cells.resize(p->nc);
@@ -1300,6 +1327,14 @@ void launch_eval_once(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, cons
     ++c->launches;
   }
   const DevMesh M = c->dev();
+  // ping-pong order (MSWM_MIX bit 4): A forward, B backward, C forward, and
+  // the next evaluation on this stream mirrored (A backward from where C ended)
+  bool flip = false;
+  if (c->mix & 16) {
+    int& par = side ? c->flip_side : c->flip_main;
+    flip = par != 0;
+    par ^= 1;
+  }
   EvalRecord* rec = nullptr;
   if (c->capture_records &&
       (c->profiling != 2 || (c->capture_records->empty() &&
@@ -1316,14 +1351,18 @@ void launch_eval_once(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, cons
   const Span vs = p.sv.dev(), ks = p.sk.dev(), es = p.se.dev();
   const int64_t na = p.sv.n() + p.sk.n();
   if (na > 0) {
+    const DArr<int32_t>& ma = flip ? p.cmapA_r : p.cmapA;
     k_vertex_cell<<<grid(na, 0), kSBlock, 0, s>>>(M, h, u, vs, ks, pv, Kp, c->dry_flag.p,
                                                  c->step_ctr.p, p.vmask.p,
-                                                 ChunkMap{p.cmapA.p, int32_t(p.cmapA.n)});
+                                                 ChunkMap{ma.p, int32_t(ma.n)});
     CK(cudaGetLastError());
     ++c->launches;
   }
   if (p.se.n() > 0) {
-    k_edge_fq<<<grid(p.se.n(), 1), kSBlock, 0, s>>>(M, h, u, pv, es, FQ);
+    // ping-pong: B runs against A's direction, C against B's
+    const DArr<int32_t>* mb = (c->mix & 16) && !flip ? &p.cmapB_r : nullptr;
+    k_edge_fq<<<grid(p.se.n(), 1), kSBlock, 0, s>>>(
+        M, h, u, pv, es, FQ, mb ? ChunkMap{mb->p, int32_t(mb->n)} : ChunkMap{nullptr, 0});
     CK(cudaGetLastError());
     ++c->launches;
   }
@@ -1340,7 +1379,8 @@ void launch_eval_once(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, cons
     a.cop[1] = cop[1];
     a.eop[0] = eop[0];
     a.eop[1] = eop[1];
-    a.cm = ChunkMap{p.cmapC.p, int32_t(p.cmapC.n)};
+    const DArr<int32_t>& mc = flip ? p.cmapC_r : p.cmapC;
+    a.cm = ChunkMap{mc.p, int32_t(mc.n)};
     k_out<<<grid(nout, 2), kSBlock, 0, s>>>(M, h, Kp, FQ, a);
     CK(cudaGetLastError());
     ++c->launches;
