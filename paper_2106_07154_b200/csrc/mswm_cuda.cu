@@ -299,7 +299,9 @@ struct mswm_cuda_ctx {
   // (u and h are read once instead of twice), C interleaved loses ~2 %.
   // C windowed gains ~2 % (its cell pass finds the window's (F, q~) in L2:
   // profiles/r2_s4_mix_windows_sweep_c4.log); A windowed does not.
-  int mix = 9;
+  // Bit 4: ping-pong directions (A forward, B backward, C forward, the next
+  // evaluation mirrored): ~0.5 % (profiles/r2_s4_mix_pingpong_sweep_c4.log).
+  int mix = 25;
   // window mode: part-0 elements per window (C4: 64 windows of 164k cells,
   // ~80 MB of traffic each, inside L2), or a fixed window count (MSWM_MIX_WIN)
   int flip_main = 0, flip_side = 0;  // ping-pong direction of the next evaluation
