@@ -791,25 +791,36 @@ __global__ void k_push(int64_t n, const int32_t* __restrict__ code, const uint8_
   }
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // wait for every neighbour's flag of this exchange, then unpack (and the
 // fused interface-1 prediction, as k_unpack_pred).  flags: this rank's flag
-// words of the channel, indexed by rank; a neighbour that does not answer within
-// the poll budget sets *err (reported as MSWM_E_NCCL by the next synchronous
-// call) instead of hanging the device.
+// words of the channel, indexed by rank.  A neighbour that does not answer
+// within budget_ns sets *err (1 + its rank; reported as MSWM_E_NCCL by the
+// next synchronous call) instead of hanging the device, and once *err is set
+// no later wait polls.
 __global__ void k_wait_unpack(int64_t n, const int32_t* __restrict__ code, const double* rbuf,
                               int64_t stride, double* __restrict__ h, double* __restrict__ u,
                               PredArgs pa, const unsigned long long* flags,
                               const int32_t* __restrict__ peers, int np,
-                              const unsigned long long* chan, int* err) {
+                              const unsigned long long* chan, int* err,
+                              unsigned long long budget_ns) {
   const unsigned long long seq = chan[0];
   if (threadIdx.x < np) {
     const unsigned long long* f = flags + peers[threadIdx.x];
-    unsigned polls = 0;
-    while (ld_flag(f) < seq) {
-      __nanosleep(64);
-      if (++polls > (1u << 24)) {
-        atomicExch(err, 1 + peers[threadIdx.x]);
-        break;
+    if (ld_flag(f) < seq) {
+      const unsigned long long t0 = global_ns();
+      while (ld_flag(f) < seq) {
+        __nanosleep(100);
+        if (*reinterpret_cast<volatile int*>(err)) break;
+        if (global_ns() - t0 > budget_ns) {
+          atomicCAS(err, 0, 1 + peers[threadIdx.x]);
+          break;
+        }
       }
     }
   }

@@ -267,6 +267,10 @@ struct mswm_cuda_ctx {
   std::vector<char> peer_ipc;             // opened with cudaIpcOpenMemHandle (to close)
   DArr<unsigned long long> xchan;         // per channel: exchanges done, block arrivals
   DArr<int> xerr;                         // 1 + rank of a neighbour that did not signal
+  // how long a wait polls for a neighbour's flag (MSWM_PEER_TIMEOUT_MS): long
+  // enough for start-up skew between processes, finite so a dead rank
+  // becomes an error
+  unsigned long long peer_budget_ns = 60000ull * 1000000ull;
   DArr<int32_t> d_peers;
   std::string last_error;
   int32_t nC = 0, nE = 0, nV = 0, deg_max = 0, sten_max = 0;
@@ -960,13 +964,14 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
 // ("during step k of n" of the batch it happened in, harness.cpp:183-190).
 void check_dry(mswm_cuda_ctx* c, const char* who = nullptr) {
   unsigned long long v = ~0ull;
+  int xe = 0;
   CK(cudaMemcpyAsync(&v, c->dry_flag.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  if (c->xerr.p) CK(cudaMemcpyAsync(&xe, c->xerr.p, sizeof(xe), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   if (c->xerr.p) {
-    int xe = 0;
-    CK(cudaMemcpy(&xe, c->xerr.p, sizeof(xe), cudaMemcpyDeviceToHost));
     if (xe) {
-      CK(cudaMemset(c->xerr.p, 0, sizeof(xe)));
+      CK(cudaMemsetAsync(c->xerr.p, 0, sizeof(xe), c->stream));
+      CK(cudaStreamSynchronize(c->stream));
       throw Error(MSWM_E_NCCL, "peer-store halo exchange: rank " + std::to_string(xe - 1) +
                                    " did not signal within the poll budget");
     }
@@ -1322,9 +1327,9 @@ void launch_eval_once(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, cons
                                                  : g;
   };
   if (pred && int64_t(pred->nc) + pred->ne > 0) {
-    k_predict<<<nblk(int64_t(pred->nc) + pred->ne), kBlock, 0, s>>>(
-        pred->clist, pred->nc, pred->elist, pred->ne, pred->c0, pred->c1, pred->c2, pred->hs0,
-        pred->hs1, pred->hs2, pred->hdst, pred->us0, pred->us1, pred->us2, pred->udst);
+    k_predict<<<nblk(int64_t(pred->nc) + pred->ne), kBlock, 0, s>>>(pred->clist, pred->nc,
+        pred->elist, pred->ne, pred->c0, pred->c1, pred->c2, pred->hs0, pred->hs1, pred->hs2,
+        pred->hdst, pred->us0, pred->us1, pred->us2, pred->udst);
     CK(cudaGetLastError());
     ++c->launches;
   }
@@ -1355,16 +1360,15 @@ void launch_eval_once(mswm_cuda_ctx* c, const MaskPlan& p, const double* h, cons
   if (na > 0) {
     const DArr<int32_t>& ma = flip ? p.cmapA_r : p.cmapA;
     k_vertex_cell<<<grid(na, 0), kSBlock, 0, s>>>(M, h, u, vs, ks, pv, Kp, c->dry_flag.p,
-                                                 c->step_ctr.p, p.vmask.p,
-                                                 ChunkMap{ma.p, int32_t(ma.n)});
+        c->step_ctr.p, p.vmask.p, ChunkMap{ma.p, int32_t(ma.n)});
     CK(cudaGetLastError());
     ++c->launches;
   }
   if (p.se.n() > 0) {
     // ping-pong: B runs against A's direction, C against B's
     const DArr<int32_t>* mb = (c->mix & 16) && !flip ? &p.cmapB_r : nullptr;
-    k_edge_fq<<<grid(p.se.n(), 1), kSBlock, 0, s>>>(
-        M, h, u, pv, es, FQ, mb ? ChunkMap{mb->p, int32_t(mb->n)} : ChunkMap{nullptr, 0});
+    k_edge_fq<<<grid(p.se.n(), 1), kSBlock, 0, s>>>(M, h, u, pv, es, FQ,
+        mb ? ChunkMap{mb->p, int32_t(mb->n)} : ChunkMap{nullptr, 0});
     CK(cudaGetLastError());
     ++c->launches;
   }
@@ -1500,8 +1504,7 @@ void launch_predict(mswm_cuda_ctx* c, int stage, int k, int M, double* hdst, dou
   if (n == 0) return;
   const bool o3 = order == 3;
   k_predict<<<nblk(n), kBlock, 0, c->ls>>>(L.c, L.nc1, L.e, L.ne1, w[0], w[1], w[2], c->S0h.p,
-                                           c->S1h.p, o3 ? c->S2h.p : nullptr, hdst, c->S0u.p,
-                                           c->S1u.p, o3 ? c->S2u.p : nullptr, udst);
+      c->S1h.p, o3 ? c->S2h.p : nullptr, hdst, c->S0u.p, c->S1u.p, o3 ? c->S2u.p : nullptr, udst);
   CK(cudaGetLastError());
   ++c->launches;
 }
@@ -1581,9 +1584,9 @@ void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us, unsigned ma
     for (auto* c : cs) {
       Halo& x = halo_for(c, mask);
       if (c->transport != 1 || !x.pslots.p) throw Error(MSWM_E_USAGE, "peer transport not enabled on every rank");
-      k_push<<<unsigned(std::max<int64_t>(1, nblk(x.ns))), kBlock, 0, c->ls>>>(
-          x.ns, x.scode.p, x.sslot.p, (c->*hs).p, (c->*us).p, x.pslots.p, int(x.peer.size()),
-          ch * c->n_ranks, c->xchan.p + 2 * ch);
+      k_push<<<unsigned(std::max<int64_t>(1, nblk(x.ns))), kBlock, 0, c->ls>>>(x.ns, x.scode.p,
+          x.sslot.p, (c->*hs).p, (c->*us).p, x.pslots.p, int(x.peer.size()), ch * c->n_ranks,
+          c->xchan.p + 2 * ch);
       CK(cudaGetLastError());
       ++c->launches;
     }
@@ -1594,10 +1597,10 @@ void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us, unsigned ma
       std::memset(&pa, 0, sizeof(pa));
       if (preds) pa = (*preds)[m];
       const int64_t np = int64_t(pa.nc) + pa.ne;
-      k_wait_unpack<<<unsigned(std::max<int64_t>(1, nblk(x.nr + np))), kBlock, 0, c->ls>>>(
-          x.nr, x.rcode.p, x.prbuf, x.pstride, (c->*hs).p, (c->*us).p, pa,
+      k_wait_unpack<<<unsigned(std::max<int64_t>(1, nblk(x.nr + np))), kBlock, 0, c->ls>>>(x.nr,
+          x.rcode.p, x.prbuf, x.pstride, (c->*hs).p, (c->*us).p, pa,
           reinterpret_cast<const unsigned long long*>(c->arena.p) + ch * c->n_ranks, c->d_peers.p,
-          int(x.peer.size()), c->xchan.p + 2 * ch, c->xerr.p);
+          int(x.peer.size()), c->xchan.p + 2 * ch, c->xerr.p, c->peer_budget_ns);
       CK(cudaGetLastError());
       ++c->launches;
     }
@@ -1679,7 +1682,7 @@ void exchange(std::vector<mswm_cuda_ctx*>& cs, ArrSel hs, ArrSel us, unsigned ma
     const int64_t np = pa ? int64_t(pa->nc) + pa->ne : 0;
     if (np > 0) {
       k_unpack_pred<<<nblk(x.nr + np), kBlock, 0, c->ls>>>(x.nr, x.rcode.p, x.rbuf.p, (c->*hs).p,
-                                                            (c->*us).p, *pa);
+          (c->*us).p, *pa);
       CK(cudaGetLastError());
       ++c->launches;
     } else if (x.nr > 0) {
@@ -1891,9 +1894,9 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
     lts_coeffs(3, 1, 0, M, w);
     const int64_t n = int64_t(L.nc) + L.ne;
     if (n > 0) {
-      k_save_predict<<<nblk(n), kBlock, 0, c->ls>>>(
-          L.c, L.nc, L.nc1, L.e, L.ne, L.ne1, w[0], w[1], w[2], c->H.p, c->H1.p, c->H2.p, c->S0h.p,
-          c->S1h.p, c->S2h.p, c->U.p, c->U1.p, c->U2.p, c->S0u.p, c->S1u.p, c->S2u.p);
+      k_save_predict<<<nblk(n), kBlock, 0, c->ls>>>(L.c, L.nc, L.nc1, L.e, L.ne, L.ne1, w[0], w[1],
+          w[2], c->H.p, c->H1.p, c->H2.p, c->S0h.p, c->S1h.p, c->S2h.p, c->U.p, c->U1.p, c->U2.p,
+          c->S0u.p, c->S1u.p, c->S2u.p);
       CK(cudaGetLastError());
       ++c->launches;
     }
@@ -1963,7 +1966,7 @@ void enqueue_lts3(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
       const int64_t nb = int64_t(c->n_band_c) + c->n_band_e;
       if (nb > 0) {
         k_copy_band<<<nblk(nb), kBlock, 0, c->ls>>>(c->band_cells.p, c->n_band_c, c->T1h.p, c->H.p,
-                                                    c->band_edges.p, c->n_band_e, c->T1u.p, c->U.p);
+            c->band_edges.p, c->n_band_e, c->T1u.p, c->U.p);
         CK(cudaGetLastError());
         ++c->launches;
       }
@@ -2008,9 +2011,9 @@ void enqueue_lts2(std::vector<mswm_cuda_ctx*>& cs, double dt, int M) {
     lts_coeffs(2, 1, 0, M, w);
     const int64_t n = int64_t(L.nc) + L.ne;
     if (n > 0) {
-      k_save_predict<<<nblk(n), kBlock, 0, c->ls>>>(
-          L.c, L.nc, L.nc1, L.e, L.ne, L.ne1, w[0], w[1], w[2], c->H.p, c->H1.p, nullptr, c->S0h.p,
-          c->S1h.p, nullptr, c->U.p, c->U1.p, nullptr, c->S0u.p, c->S1u.p, nullptr);
+      k_save_predict<<<nblk(n), kBlock, 0, c->ls>>>(L.c, L.nc, L.nc1, L.e, L.ne, L.ne1, w[0], w[1],
+          w[2], c->H.p, c->H1.p, nullptr, c->S0h.p, c->S1h.p, nullptr, c->U.p, c->U1.p, nullptr,
+          c->S0u.p, c->S1u.p, nullptr);
       CK(cudaGetLastError());
       ++c->launches;
     }
@@ -2664,8 +2667,7 @@ int mswm_cuda_state_upload(mswm_cuda_ctx* c, const double* h, const double* u, d
       for (auto& kv : c->halo_mask) hs.push_back(&kv.second);
       for (Halo* x : hs)
         if (x->nr > 0) {
-          k_pack<<<nblk(x->nr), kBlock, 0, c->stream>>>(x->nr, x->rcode.p, c->H.p, c->U.p,
-                                                        x->rbuf.p);
+          k_pack<<<nblk(x->nr), kBlock, 0, c->stream>>>(x->nr, x->rcode.p, c->H.p, c->U.p, x->rbuf.p);
           CK(cudaGetLastError());
         }
     }
@@ -3291,6 +3293,8 @@ void peer_prepare(mswm_cuda_ctx* c) {
     kh.second->pstride = std::max<int64_t>(kh.second->nr, 1);
     kh.second->h_pslots.assign(kh.second->peer.size(), PeerSlot{nullptr, 0, nullptr, 0});
   }
+  if (const char* e = std::getenv("MSWM_PEER_TIMEOUT_MS"))
+    c->peer_budget_ns = std::max(1ll, std::atoll(e)) * 1000000ull;
   c->xchan.alloc(4);
   c->xchan.zero(c->stream);
   c->xerr.alloc(1);
@@ -3426,15 +3430,15 @@ int mswm_cuda_peer_exchange(mswm_cuda_ctx* c, int phase) {
     if (phase != 0 && phase != 1) throw Error(MSWM_E_USAGE, "phase must be 0 (push) or 1 (wait + unpack)");
     Halo& x = c->halo;
     if (phase == 0) {
-      k_push<<<unsigned(std::max<int64_t>(1, nblk(x.ns))), kBlock, 0, c->stream>>>(
-          x.ns, x.scode.p, x.sslot.p, c->H.p, c->U.p, x.pslots.p, int(x.peer.size()), 0, c->xchan.p);
+      k_push<<<unsigned(std::max<int64_t>(1, nblk(x.ns))), kBlock, 0, c->stream>>>(x.ns, x.scode.p,
+          x.sslot.p, c->H.p, c->U.p, x.pslots.p, int(x.peer.size()), 0, c->xchan.p);
     } else {
       PredArgs pa;
       std::memset(&pa, 0, sizeof(pa));
-      k_wait_unpack<<<unsigned(std::max<int64_t>(1, nblk(x.nr))), kBlock, 0, c->stream>>>(
-          x.nr, x.rcode.p, x.prbuf, x.pstride, c->H.p, c->U.p, pa,
+      k_wait_unpack<<<unsigned(std::max<int64_t>(1, nblk(x.nr))), kBlock, 0, c->stream>>>(x.nr,
+          x.rcode.p, x.prbuf, x.pstride, c->H.p, c->U.p, pa,
           reinterpret_cast<const unsigned long long*>(c->arena.p), c->d_peers.p, int(x.peer.size()),
-          c->xchan.p, c->xerr.p);
+          c->xchan.p, c->xerr.p, c->peer_budget_ns);
     }
     CK(cudaGetLastError());
     check_dry(c);

@@ -279,3 +279,33 @@ def test_peer_stores_across_processes():
     out = subprocess.run(cmd, capture_output=True, text=True, env=env, cwd=root)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert "PEER_IPC_OK rank 0" in out.stdout and "PEER_IPC_OK rank 1" in out.stdout
+
+
+def test_peer_stores_silent_neighbour_is_an_error(monkeypatch):
+    """A neighbour that never raises its flag ends the bounded wait with an
+    error naming it (no device hang); once it has pushed, the same wait
+    passes and delivers its values."""
+    from paper_2106_07154_b200.api import CudaError, State
+    monkeypatch.setenv("MSWM_PEER_TIMEOUT_MS", "200")
+    wl = W.small_sphere(4, seed=3, cap_deg=25.0)
+    o = Oracle(wl.mesh, wl.b, wl.f, wl.gravity)
+    o.set_regions(wl.fine_mask, wl.width)
+    lay = DistributedLayout(wl.mesh, *o.labels(), 2)
+    ranks = [RankContext(lay, r, wl.b, wl.f, wl.gravity) for r in range(2)]
+    grp = CudaGroup(ranks)
+    grp.use_peer_stores()
+    for rc in ranks:
+        lm = rc.lm
+        hp, up = lm.gather_cells(wl.h), lm.gather_edges(wl.u)
+        hp[lm.n_owned_cells:-1] = np.nan
+        up[lm.n_owned_edges:-1] = np.nan
+        rc.ctx.upload(State(hp, up, 0.0))
+    ranks[0].peer_exchange(0)
+    with pytest.raises(CudaError, match="rank 1 did not signal"):
+        ranks[0].peer_exchange(1)
+    ranks[1].peer_exchange(0)
+    ranks[0].peer_exchange(1)
+    ranks[1].peer_exchange(1)
+    for rc in ranks:
+        st = rc.ctx.download()
+        assert bits_equal(st.h, rc.lm.gather_cells(wl.h)) and bits_equal(st.u, rc.lm.gather_edges(wl.u))
