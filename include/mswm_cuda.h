@@ -106,10 +106,7 @@ typedef struct mswm_cuda_ctx mswm_cuda_ctx;
  * mswm_cuda_set_fields).  cell_order (may be NULL = input order) is a
  * permutation of the cells for the internal memory layout, normally a
  * space-filling curve (mswm_mesh_locality_order); edges and vertices follow
- * it.  Results are bitwise independent of cell_order.  When the stencil and
- * weights are the reference builder's ring walk and weight rule
- * (mesh_build.cpp:133-154, 343-362) -- verified bitwise here -- the kernels
- * rebuild them from per-cell rows instead of streaming the stencil tables.
+ * it.  Results are bitwise independent of cell_order.
  * On failure *out is NULL and the message is available from
  * mswm_cuda_last_error(NULL). */
 int mswm_cuda_create(const mswm_mesh_desc* mesh, int device,

@@ -36,6 +36,7 @@
 #include <numeric>
 #include <stdexcept>
 #include <string>
+#include <atomic>
 #include <thread>
 #include <tuple>
 #include <type_traits>
@@ -576,6 +577,22 @@ std::vector<int64_t> compact(mswm_cuda_ctx* c, const uint8_t* d_key, int32_t n, 
 // ---------------------------------------------------------------------------
 // create
 
+// f(lo, hi) over [0, n) on the host cores (the drop-in eval's pack and
+// scatter loops: independent elements).
+template <class F>
+void host_par_for(int64_t n, F&& f) {
+  static const int64_t T = std::max(1u, std::thread::hardware_concurrency());
+  const int64_t t = std::min<int64_t>(T, std::max<int64_t>(1, n / (1 << 18)));
+  if (t <= 1) {
+    if (n > 0) f(int64_t(0), n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int64_t k = 1; k < t; ++k) th.emplace_back([&, k] { f(n * k / t, n * (k + 1) / t); });
+  f(0, n / t);
+  for (auto& x : th) x.join();
+}
+
 // Internal numbering.  Cells follow `cell_order` (a space-filling curve from
 // the caller, or the input order); edges are sorted by the internal ids of
 // their two cells (min, max) and vertices by their three, so every gather of
@@ -583,6 +600,10 @@ std::vector<int64_t> compact(mswm_cuda_ctx* c, const uint8_t* d_key, int32_t n, 
 // arithmetic does not depend on the numbering (slot orders, edge_cells
 // order and stencil order are carried verbatim), so results are bitwise
 // independent of it (SURVEY.md §0 finding 5).
+struct OrderKey {
+  uint32_t a, b, cc;
+};
+
 void make_orders(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell_order) {
   const int32_t nC = d->n_cells, nE = d->n_edges, nV = d->n_vertices;
   c->c_new2old.resize(nC);
@@ -597,41 +618,64 @@ void make_orders(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell_
     c->c_new2old[k] = i;
   }
   const auto& r = c->c_old2new;
-  {
-    std::vector<std::pair<uint64_t, int32_t>> key(nE);
-    for (int32_t e = 0; e < nE; ++e) {
-      uint32_t a = uint32_t(r[d->edge_cells[2 * e]]), b = uint32_t(r[d->edge_cells[2 * e + 1]]);
-      if (a > b) std::swap(a, b);
-      key[e] = {(uint64_t(a) << 32) | b, e};
-    }
-    std::sort(key.begin(), key.end());
-    c->e_old2new.assign(nE, 0);
-    for (int32_t k = 0; k < nE; ++k) {
-      c->e_new2old[k] = key[k].second;
-      c->e_old2new[key[k].second] = k;
-    }
-  }
-  {
-    struct VK {
-      uint32_t a, b, cc;
-      int32_t v;
-    };
-    std::vector<VK> key(nV);
-    for (int32_t v = 0; v < nV; ++v) {
-      uint32_t x[3] = {uint32_t(r[d->vertex_cells[3 * v]]), uint32_t(r[d->vertex_cells[3 * v + 1]]),
-                       uint32_t(r[d->vertex_cells[3 * v + 2]])};
-      std::sort(x, x + 3);
-      key[v] = {x[0], x[1], x[2], v};
-    }
-    std::sort(key.begin(), key.end(), [](const VK& p, const VK& q) {
-      return std::tie(p.a, p.b, p.cc, p.v) < std::tie(q.a, q.b, q.cc, q.v);
+  // Edges by (min cell, max cell, id) and vertices by (their three cells
+  // ascending, id) in internal cell ids: a bucket pass on the smallest cell
+  // (an element lands in the bucket of one of its <= kMaxDeg-ring cells) and
+  // an insertion sort inside each bucket -- linear, parallel over the cells,
+  // the order a comparison sort of the full keys gives.
+  auto bucket_sort = [&](int32_t n, auto&& key_of, std::vector<int32_t>& new2old,
+                         std::vector<int32_t>& old2new) {
+    // key_of(x) -> {a, b, c}: a = bucket (smallest cell), (b, c) the rest of the key
+    using K = OrderKey;
+    std::vector<K> key(static_cast<size_t>(n));
+    host_par_for(n, [&](int64_t lo, int64_t hi) {
+      for (int64_t x = lo; x < hi; ++x) key[size_t(x)] = key_of(int32_t(x));
     });
-    c->v_old2new.assign(nV, 0);
-    for (int32_t k = 0; k < nV; ++k) {
-      c->v_new2old[k] = key[k].v;
-      c->v_old2new[key[k].v] = k;
-    }
-  }
+    std::vector<int32_t> start(size_t(nC) + 1, 0);
+    for (int32_t x = 0; x < n; ++x) ++start[size_t(key[size_t(x)].a) + 1];
+    for (int32_t i = 0; i < nC; ++i) start[size_t(i) + 1] += start[size_t(i)];
+    std::vector<int32_t> fill(start.begin(), start.end() - 1);
+    for (int32_t x = 0; x < n; ++x) new2old[size_t(fill[key[size_t(x)].a]++)] = x;  // ascending id
+    host_par_for(nC, [&](int64_t lo, int64_t hi) {
+      for (int64_t i = lo; i < hi; ++i) {
+        const int32_t b0 = start[size_t(i)], b1 = start[size_t(i) + 1];
+        for (int32_t p = b0 + 1; p < b1; ++p) {
+          const int32_t x = new2old[size_t(p)];
+          const K kx = key[size_t(x)];
+          int32_t q = p;
+          while (q > b0) {
+            const int32_t y = new2old[size_t(q) - 1];
+            const K ky = key[size_t(y)];
+            if (std::tie(ky.b, ky.cc, y) <= std::tie(kx.b, kx.cc, x)) break;
+            new2old[size_t(q)] = y;
+            --q;
+          }
+          new2old[size_t(q)] = x;
+        }
+      }
+    });
+    old2new.assign(size_t(n), 0);
+    host_par_for(n, [&](int64_t lo, int64_t hi) {
+      for (int64_t k = lo; k < hi; ++k) old2new[size_t(new2old[size_t(k)])] = int32_t(k);
+    });
+  };
+  bucket_sort(
+      nE,
+      [&](int32_t e) {
+        uint32_t a = uint32_t(r[d->edge_cells[2 * e]]), b = uint32_t(r[d->edge_cells[2 * e + 1]]);
+        if (a > b) std::swap(a, b);
+        return OrderKey{a, b, 0u};
+      },
+      c->e_new2old, c->e_old2new);
+  bucket_sort(
+      nV,
+      [&](int32_t v) {
+        uint32_t x[3] = {uint32_t(r[d->vertex_cells[3 * v]]), uint32_t(r[d->vertex_cells[3 * v + 1]]),
+                         uint32_t(r[d->vertex_cells[3 * v + 2]])};
+        std::sort(x, x + 3);
+        return OrderKey{x[0], x[1], x[2]};
+      },
+      c->v_new2old, c->v_old2new);
   bool ident = true;
   for (int32_t k = 0; k < nC && ident; ++k) ident = c->c_new2old[k] == k;
   for (int32_t k = 0; k < nE && ident; ++k) ident = c->e_new2old[k] == k;
@@ -696,50 +740,57 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
       c_nbr(size_t(deg_max) * nC, 0);
   std::vector<uint8_t> c_deg(nC), c_sbits(nC, 0);
   std::vector<double> c_area(nC);
-  for (int32_t ni = 0; ni < nC; ++ni) {
-    const int32_t i = cn[ni];
-    const int off = d->cell_offset[i], deg = d->cell_offset[i + 1] - off;
-    c_deg[ni] = uint8_t(deg);
-    c_area[ni] = d->cell_area[i];
-    for (int j = 0; j < deg; ++j) {
-      const int32_t e = d->cell_edges[off + j], v = d->cell_vertices[off + j],
-                    nb = d->cell_cells[off + j];
-      need(e >= 0 && e < nE && v >= 0 && v < nV && nb >= 0 && nb < nC, "ring id out of range");
-      c_edge[size_t(j) * nC + ni] = eo[e];
-      c_vert[size_t(j) * nC + ni] = vo[v];
-      c_nbr[size_t(j) * nC + ni] = co[nb];
-      // cell_sign(e, i) (mesh.hpp:89-92)
-      const int8_t sg = d->edge_cells[2 * e] == i ? d->edge_cell_sign[2 * e] : d->edge_cell_sign[2 * e + 1];
-      if (sg < 0) c_sbits[ni] |= uint8_t(1u << j);
+  // the per-element loops below run on all host cores (independent elements,
+  // every thread writes its own range); an id out of range is recorded and
+  // raised after the join
+  std::atomic<int> bad_ring{0}, bad_sten{0};
+  host_par_for(nC, [&](int64_t lo, int64_t hi) {
+    for (int32_t ni = int32_t(lo); ni < int32_t(hi); ++ni) {
+      const int32_t i = cn[ni];
+      const int off = d->cell_offset[i], deg = d->cell_offset[i + 1] - off;
+      c_deg[ni] = uint8_t(deg);
+      c_area[ni] = d->cell_area[i];
+      for (int j = 0; j < deg; ++j) {
+        const int32_t e = d->cell_edges[off + j], v = d->cell_vertices[off + j],
+                      nb = d->cell_cells[off + j];
+        if (!(e >= 0 && e < nE && v >= 0 && v < nV && nb >= 0 && nb < nC)) {
+          bad_ring = 1;
+          continue;
+        }
+        c_edge[size_t(j) * nC + ni] = eo[e];
+        c_vert[size_t(j) * nC + ni] = vo[v];
+        c_nbr[size_t(j) * nC + ni] = co[nb];
+        // cell_sign(e, i) (mesh.hpp:89-92)
+        const int8_t sg = d->edge_cells[2 * e] == i ? d->edge_cell_sign[2 * e] : d->edge_cell_sign[2 * e + 1];
+        if (sg < 0) c_sbits[ni] |= uint8_t(1u << j);
+      }
     }
-  }
+  });
+  need(!bad_ring, "ring id out of range");
   c->h_cell_area.assign(d->cell_area, d->cell_area + nC);
   // vertices
   std::vector<int32_t> v_cell(size_t(3) * nV), v_edge(size_t(3) * nV), v_orig(nV);
   std::vector<double> v_kite(size_t(3) * nV), v_area(nV);
   std::vector<uint8_t> v_sbits(nV, 0);
-  for (int32_t nv = 0; nv < nV; ++nv) {
-    const int32_t v = vn[nv];
-    v_orig[nv] = v;
-    v_area[nv] = d->vertex_area[v];
-    for (int k = 0; k < 3; ++k) {
-      const int32_t cc = d->vertex_cells[3 * v + k], e = d->vertex_edges[3 * v + k];
-      v_cell[size_t(k) * nV + nv] = co[cc];
-      v_edge[size_t(k) * nV + nv] = eo[e];
-      v_kite[size_t(k) * nV + nv] = d->vertex_kite[3 * v + k];
-      // vertex_sign(e, v) (mesh.hpp:93-96)
-      const int8_t sg =
-          d->edge_vertices[2 * e] == v ? d->edge_vertex_sign[2 * e] : d->edge_vertex_sign[2 * e + 1];
-      if (sg < 0) v_sbits[nv] |= uint8_t(1u << k);
+  host_par_for(nV, [&](int64_t lo, int64_t hi) {
+    for (int32_t nv = int32_t(lo); nv < int32_t(hi); ++nv) {
+      const int32_t v = vn[nv];
+      v_orig[nv] = v;
+      v_area[nv] = d->vertex_area[v];
+      for (int k = 0; k < 3; ++k) {
+        const int32_t cc = d->vertex_cells[3 * v + k], e = d->vertex_edges[3 * v + k];
+        v_cell[size_t(k) * nV + nv] = co[cc];
+        v_edge[size_t(k) * nV + nv] = eo[e];
+        v_kite[size_t(k) * nV + nv] = d->vertex_kite[3 * v + k];
+        // vertex_sign(e, v) (mesh.hpp:93-96)
+        const int8_t sg =
+            d->edge_vertices[2 * e] == v ? d->edge_vertex_sign[2 * e] : d->edge_vertex_sign[2 * e + 1];
+        if (sg < 0) v_sbits[nv] |= uint8_t(1u << k);
+      }
     }
-  }
+  });
   // edges
   std::vector<int2> e_cells(nE), e_verts(nE);
-  for (int32_t ne = 0; ne < nE; ++ne) {
-    const int32_t e = en[ne];
-    e_cells[ne] = make_int2(co[d->edge_cells[2 * e]], co[d->edge_cells[2 * e + 1]]);
-    e_verts[ne] = make_int2(vo[d->edge_vertices[2 * e]], vo[d->edge_vertices[2 * e + 1]]);
-  }
   std::vector<double> e_len(nE), e_ld(nE), e_dual(nE), e_invd(nE);
   std::vector<uint8_t> e_nst;
   std::vector<int32_t> e_sten;
@@ -788,50 +839,60 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   e_sten.assign(size_t(std::max(sten_max, 1)) * nE, 0);
   e_coef2.assign(size_t((std::max(sten_max, 1) + 1) / 2) * nE, make_double2(0.0, 0.0));
   if (use16) e_st16p.assign(size_t((n_words + 1) / 2) * nE, make_uint2(0u, 0u));
-  for (int32_t ne = 0; ne < nE; ++ne) {
-    const int32_t e = en[ne];
-    const int32_t c0 = d->edge_cells[2 * e], c1 = d->edge_cells[2 * e + 1];
-    const int32_t v0 = d->edge_vertices[2 * e], v1 = d->edge_vertices[2 * e + 1];
-    e_cells[ne] = make_int2(co[c0], co[c1]);
-    e_verts[ne] = make_int2(vo[v0], vo[v1]);
-    const double l = d->edge_len[e], dd = d->edge_dual_len[e];
-    e_len[ne] = l;
-    e_dual[ne] = dd;
-    e_ld[ne] = l * dd;              // operators.cpp:70, first product
-    const double inv_d = 1.0 / dd;  // operators.cpp:103
-    e_invd[ne] = inv_d;
-    const int off = d->edge_edge_offset[e], n = d->edge_edge_offset[e + 1] - off;
-    e_nst[ne] = uint8_t(n);
-    if (c->pack16) {
-      bool wc = false, wv = false;
-      const uint32_t a = off16(e_cells[ne].x, ne, 0, wc), b2 = off16(e_cells[ne].y, ne, 0, wc);
-      const uint32_t x = off16(e_verts[ne].x, ne, 1, wv), y = off16(e_verts[ne].y, ne, 1, wv);
-      e_cv16[ne] = make_uint2(a | b2 << 16, x | y << 16);
-      e_c16[ne] = a | b2 << 16;
-      // ten-entry stencils use five of the six words of the e_st16 row: the
-      // sixth carries (c0, c1) for kernel C
-      if (use16 && sten_max == kFastSten) e_st16p[size_t(2) * nE + ne].y = a | b2 << 16;
-      if (wc) e_nst[ne] |= 0x40;
-      c->n_wide16[2] += wc || wv;
-    }
-    for (int j = 0; j < n; ++j) {
-      const int32_t e2 = d->edge_edges[off + j];
-      need(e2 >= 0 && e2 < nE, "stencil id out of range");
-      e_sten[size_t(j) * nE + ne] = eo[e2];
-      const int32_t dlt = eo[e2] - ne;
-      if (dlt < INT16_MIN || dlt > INT16_MAX)
-        e_nst[ne] |= 0x80;
-      else if (use16) {
-        // entry j -> word j/2 (half j&1) -> pair word/2 (component word&1)
-        uint2& pw = e_st16p[size_t(j / 4) * nE + ne];
-        ((j / 2) & 1 ? pw.y : pw.x) |= (uint32_t(dlt) & 0xFFFFu) << (16 * (j & 1));
+  std::atomic<int64_t> wide_edges{0};
+  host_par_for(nE, [&](int64_t lo, int64_t hi) {
+    int64_t n_wide_local = 0;
+    for (int32_t ne = int32_t(lo); ne < int32_t(hi); ++ne) {
+      const int32_t e = en[ne];
+      const int32_t c0 = d->edge_cells[2 * e], c1 = d->edge_cells[2 * e + 1];
+      const int32_t v0 = d->edge_vertices[2 * e], v1 = d->edge_vertices[2 * e + 1];
+      e_cells[ne] = make_int2(co[c0], co[c1]);
+      e_verts[ne] = make_int2(vo[v0], vo[v1]);
+      const double l = d->edge_len[e], dd = d->edge_dual_len[e];
+      e_len[ne] = l;
+      e_dual[ne] = dd;
+      e_ld[ne] = l * dd;              // operators.cpp:70, first product
+      const double inv_d = 1.0 / dd;  // operators.cpp:103
+      e_invd[ne] = inv_d;
+      const int off = d->edge_edge_offset[e], n = d->edge_edge_offset[e + 1] - off;
+      e_nst[ne] = uint8_t(n);
+      if (c->pack16) {
+        bool wc = false, wv = false;
+        const uint32_t a = off16(e_cells[ne].x, ne, 0, wc), b2 = off16(e_cells[ne].y, ne, 0, wc);
+        const uint32_t x = off16(e_verts[ne].x, ne, 1, wv), y = off16(e_verts[ne].y, ne, 1, wv);
+        e_cv16[ne] = make_uint2(a | b2 << 16, x | y << 16);
+        e_c16[ne] = a | b2 << 16;
+        // ten-entry stencils use five of the six words of the e_st16 row: the
+        // sixth carries (c0, c1) for kernel C
+        if (use16 && sten_max == kFastSten) e_st16p[size_t(2) * nE + ne].y = a | b2 << 16;
+        if (wc) e_nst[ne] |= 0x40;
+        n_wide_local += wc || wv;
       }
-      // operators.cpp:109: weights[j] * (edge_len[e2] * inv_d), the first
-      // two factors of the stencil term -- mesh constants.
-      double2& cp = e_coef2[size_t(j / 2) * nE + ne];
-      (j & 1 ? cp.y : cp.x) = d->edge_weight[off + j] * (d->edge_len[e2] * inv_d);
+      for (int j = 0; j < n; ++j) {
+        const int32_t e2 = d->edge_edges[off + j];
+        if (!(e2 >= 0 && e2 < nE)) {
+          bad_sten = 1;
+          continue;
+        }
+        e_sten[size_t(j) * nE + ne] = eo[e2];
+        const int32_t dlt = eo[e2] - ne;
+        if (dlt < INT16_MIN || dlt > INT16_MAX)
+          e_nst[ne] |= 0x80;
+        else if (use16) {
+          // entry j -> word j/2 (half j&1) -> pair word/2 (component word&1)
+          uint2& pw = e_st16p[size_t(j / 4) * nE + ne];
+          ((j / 2) & 1 ? pw.y : pw.x) |= (uint32_t(dlt) & 0xFFFFu) << (16 * (j & 1));
+        }
+        // operators.cpp:109: weights[j] * (edge_len[e2] * inv_d), the first
+        // two factors of the stencil term -- mesh constants.
+        double2& cp = e_coef2[size_t(j / 2) * nE + ne];
+        (j & 1 ? cp.y : cp.x) = d->edge_weight[off + j] * (d->edge_len[e2] * inv_d);
+      }
     }
-  }
+    wide_edges += n_wide_local;
+  });
+  need(!bad_sten, "stencil id out of range");
+  c->n_wide16[2] += wide_edges;
   cudaStream_t s = c->stream;
   // upload, then release the host copy at once (C5's tables total tens of GB
   // on the host; keeping them all alive until the end ran the box out of
@@ -854,43 +915,59 @@ void build_tables(mswm_cuda_ctx* c, const mswm_mesh_desc* d, const int32_t* cell
   {
     // packed copies (kernels.cuh DevMesh): pairs of slots / entries per load
     std::vector<int2> c_edge2(size_t((deg_max + 1) / 2) * nC, make_int2(0, 0));
-    for (int j = 0; j < deg_max; ++j)
-      for (int32_t i = 0; i < nC; ++i) {
-        int2& p = c_edge2[size_t(j / 2) * nC + i];
-        (j & 1 ? p.y : p.x) = c_edge[size_t(j) * nC + i];
-      }
+    host_par_for(nC, [&](int64_t lo, int64_t hi) {
+      for (int j = 0; j < deg_max; ++j)
+        for (int32_t i = int32_t(lo); i < int32_t(hi); ++i) {
+          int2& p = c_edge2[size_t(j / 2) * nC + i];
+          (j & 1 ? p.y : p.x) = c_edge[size_t(j) * nC + i];
+        }
+    });
     put(c->c_edge2, c_edge2);
     std::vector<int2> v_ce(size_t(3) * nV);
-    for (int32_t v = 0; v < nV; ++v)
-      for (int k = 0; k < 3; ++k)
-        v_ce[size_t(k) * nV + v] = make_int2(v_cell[size_t(k) * nV + v], v_edge[size_t(k) * nV + v]);
+    host_par_for(nV, [&](int64_t lo, int64_t hi) {
+      for (int32_t v = int32_t(lo); v < int32_t(hi); ++v)
+        for (int k = 0; k < 3; ++k)
+          v_ce[size_t(k) * nV + v] = make_int2(v_cell[size_t(k) * nV + v], v_edge[size_t(k) * nV + v]);
+    });
     put(c->v_ce, v_ce);
     // 16-bit index records of vertices and cells (e_cv16 / e_c16 above)
     if (c->pack16) {
       std::vector<uint4> v_rec(nV);
-      for (int32_t v = 0; v < nV; ++v) {
-        bool w = false;
-        uint32_t o[6];
-        for (int k = 0; k < 3; ++k) {
-          o[k] = off16(v_cell[size_t(k) * nV + v], v, 2, w);
-          o[3 + k] = off16(v_edge[size_t(k) * nV + v], v, 3, w);
+      std::atomic<int64_t> wide_v{0};
+      host_par_for(nV, [&](int64_t lo, int64_t hi) {
+        int64_t nw = 0;
+        for (int32_t v = int32_t(lo); v < int32_t(hi); ++v) {
+          bool w = false;
+          uint32_t o[6];
+          for (int k = 0; k < 3; ++k) {
+            o[k] = off16(v_cell[size_t(k) * nV + v], v, 2, w);
+            o[3 + k] = off16(v_edge[size_t(k) * nV + v], v, 3, w);
+          }
+          nw += w;
+          v_rec[v] = make_uint4(o[0] | o[1] << 16, o[2] | o[3] << 16, o[4] | o[5] << 16,
+                                uint32_t(v_sbits[v]) | (w ? 0x80u : 0u));
         }
-        c->n_wide16[0] += w;
-        v_rec[v] = make_uint4(o[0] | o[1] << 16, o[2] | o[3] << 16, o[4] | o[5] << 16,
-                              uint32_t(v_sbits[v]) | (w ? 0x80u : 0u));
-      }
+        wide_v += nw;
+      });
+      c->n_wide16[0] += wide_v;
       put(c->v_rec, v_rec);
       if (deg_max == kFastDeg) {
         std::vector<uint4> c_rec(nC);
-        for (int32_t i = 0; i < nC; ++i) {
-          bool w = false;
-          uint32_t o[6];
-          for (int j = 0; j < 6; ++j)
-            o[j] = j < c_deg[i] ? off16(c_edge[size_t(j) * nC + i], i, 4, w) : 0u;
-          c->n_wide16[1] += w;
-          c_rec[i] = make_uint4(o[0] | o[1] << 16, o[2] | o[3] << 16, o[4] | o[5] << 16,
-                                uint32_t(c_deg[i]) | (w ? 0x80u : 0u) | uint32_t(c_sbits[i]) << 8);
-        }
+        std::atomic<int64_t> wide_c{0};
+        host_par_for(nC, [&](int64_t lo, int64_t hi) {
+          int64_t nw = 0;
+          for (int32_t i = int32_t(lo); i < int32_t(hi); ++i) {
+            bool w = false;
+            uint32_t o[6];
+            for (int j = 0; j < 6; ++j)
+              o[j] = j < c_deg[i] ? off16(c_edge[size_t(j) * nC + i], i, 4, w) : 0u;
+            nw += w;
+            c_rec[i] = make_uint4(o[0] | o[1] << 16, o[2] | o[3] << 16, o[4] | o[5] << 16,
+                                  uint32_t(c_deg[i]) | (w ? 0x80u : 0u) | uint32_t(c_sbits[i]) << 8);
+          }
+          wide_c += nw;
+        });
+        c->n_wide16[1] += wide_c;
         put(c->c_rec, c_rec);
       }
     }
@@ -2390,21 +2467,6 @@ int guard(mswm_cuda_ctx* c, F&& f) {
 
 }  // namespace
 
-// f(lo, hi) over [0, n) on the host cores (the drop-in eval's pack and
-// scatter loops: independent elements).
-template <class F>
-void host_par_for(int64_t n, F&& f) {
-  static const int64_t T = std::max(1u, std::thread::hardware_concurrency());
-  const int64_t t = std::min<int64_t>(T, std::max<int64_t>(1, n / (1 << 18)));
-  if (t <= 1) {
-    if (n > 0) f(int64_t(0), n);
-    return;
-  }
-  std::vector<std::thread> th;
-  for (int64_t k = 1; k < t; ++k) th.emplace_back([&, k] { f(n * k / t, n * (k + 1) / t); });
-  f(0, n / t);
-  for (auto& x : th) x.join();
-}
 
 // ===========================================================================
 // C ABI
