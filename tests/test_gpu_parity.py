@@ -547,6 +547,38 @@ def test_index_records16_bitwise(pack16, monkeypatch):
             assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
 
 
+@pytest.mark.parametrize("mix,win", [("0", None), ("1", None), ("3", None), ("12", "7"),
+                                     ("25", None), ("29", "3"), ("25", "1000")])
+def test_chunk_schedules_bitwise(mix, win, monkeypatch):
+    """Chunk schedules of the evaluation kernels (MSWM_MIX: none, kernel A /
+    C interleaved in proportion, windowed with few / one-chunk windows, ping-pong
+    directions; the default is 25): every order of the same elements gives the
+    same bits -- every LTS3 mask's tendencies and 3 coarse steps against the
+    oracle, on a sphere (hilbert and region-major numbering) and a plane."""
+    monkeypatch.setenv("MSWM_MIX", mix)
+    if win:
+        monkeypatch.setenv("MSWM_MIX_WIN", win)
+    for wl in [W.small_sphere(6, seed=41, cap_deg=20.0), W.config1(n_steps=3)]:
+        o = _oracle_for(wl)
+        h_ref, u_ref, _ = o.step(int(Scheme.LTS3), wl.h, wl.u, 0.0, wl.dt, wl.M, 3)
+        for order in ["hilbert", "regions"]:
+            ctx = CudaContext(wl.mesh, wl.b, wl.f, wl.gravity, order=order,
+                              fine_mask=wl.fine_mask)
+            ctx.make_regions(wl.fine_mask, wl.width)
+            ev = CudaEvaluator(ctx)
+            for mask in LTS3_MASKS + [kMaskAll]:
+                dh1 = np.full(wl.mesh.n_cells, SENTINEL)
+                du1 = np.full(wl.mesh.n_edges, SENTINEL)
+                dh2, du2 = dh1.copy(), du1.copy()
+                ev.eval(wl.h, wl.u, mask, dh1, du1)
+                o.eval(wl.h, wl.u, mask, dh2, du2)
+                assert bits_equal(dh1, dh2) and bits_equal(du1, du2), hex(mask)
+            ctx.upload(State(wl.h, wl.u, 0.0))
+            ctx.advance(Scheme.LTS3, wl.dt, wl.M, 3)
+            st = ctx.download()
+            assert bits_equal(st.h, h_ref) and bits_equal(st.u, u_ref)
+
+
 @pytest.mark.parametrize("config", ["c4", "c3"])
 def test_full_size_against_reference(config):
     """BASELINE configs at full size against the unmodified reference
