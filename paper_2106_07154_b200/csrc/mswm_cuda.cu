@@ -256,6 +256,7 @@ struct mswm_cuda_ctx {
   std::map<unsigned, Halo> halo_mask;
   ncclComm_t nccl_comm = nullptr;
   ncclComm_t nccl_comm2 = nullptr;  // the concurrent coarse step's exchanges (ncclCommSplit)
+  bool nccl_warm = false;           // p2p connections to every neighbour set up (warm_nccl)
   // in-process group over a one-rank NCCL communicator (owned by the group,
   // mswm_cuda_group_nccl_loopback): halo copies as NCCL send/recv to self
   ncclComm_t loop_comm = nullptr, loop_comm2 = nullptr;
@@ -2274,8 +2275,31 @@ void check_step_args(mswm_cuda_ctx* c, int scheme, double dt, int M, int64_t n_s
 }
 
 // Capture one step of every context in `cs` on `stream` into a graph.
+// One eager one-double send / receive with every neighbour on each
+// communicator, so NCCL sets its point-to-point connections up (allocations,
+// handshakes) before the exchanges are captured into the step graph.
+void warm_nccl(mswm_cuda_ctx* c) {
+  if (c->nccl_warm || !c->nccl_comm || !c->halo.active()) return;
+  const size_t np = c->halo.peer.size();
+  DArr<double> buf;
+  buf.alloc(2 * np);
+  buf.zero(c->stream);
+  for (ncclComm_t comm : {c->nccl_comm, c->nccl_comm2}) {
+    if (!comm) continue;
+    nccl_check(nccl().GroupStart());
+    for (size_t j = 0; j < np; ++j) {
+      nccl_check(nccl().Send(buf.p + j, 1, ncclFloat64, c->halo.peer[j], comm, c->stream));
+      nccl_check(nccl().Recv(buf.p + np + j, 1, ncclFloat64, c->halo.peer[j], comm, c->stream));
+    }
+    nccl_check(nccl().GroupEnd());
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  c->nccl_warm = true;
+}
+
 mswm_cuda_ctx::Graph capture_step(std::vector<mswm_cuda_ctx*>& cs, cudaStream_t stream, int scheme,
                                   double dt, int M, bool profile) {
+  if (cs.size() == 1 && cs[0]->transport == 0 && !halo_dry_run()) warm_nccl(cs[0]);
   // Build every plan outside the capture (plan construction synchronises).
   for (auto* c : cs) {
     if (scheme == MSWM_LTS3 || scheme == MSWM_LTS2) {
@@ -3535,6 +3559,7 @@ int mswm_cuda_comm_init(mswm_cuda_ctx* c, const void* unique_id, int rank, int n
       nccl().CommDestroy(c->nccl_comm2);
       c->nccl_comm2 = nullptr;
     }
+    c->nccl_warm = false;
     nccl_check(nccl().CommInitRank(&c->nccl_comm, n_ranks, id, rank));
     if (nccl().CommSplit) nccl_check(nccl().CommSplit(c->nccl_comm, 0, rank, &c->nccl_comm2, nullptr));
     c->fork_state = 0;  // the concurrent coarse step may use the new communicators
