@@ -383,7 +383,8 @@ int mswm_cuda_peer_import(mswm_cuda_ctx* ctx, int peer_rank, const void* ipc_han
                           const int64_t* rows, int64_t n_rows);
 int mswm_cuda_peer_enable(mswm_cuda_ctx* ctx, int on);
 /* One full-halo exchange of the state arrays in two host-ordered halves
- * (phase 0: pack + store + signal; phase 1: wait + unpack), synchronous. */
+ * (phase 0: pack + store + signal; phase 1: wait + unpack), synchronous;
+ * phase 2 enqueues the wait + unpack and returns (mswm_cuda_sync awaits it). */
 int mswm_cuda_peer_exchange(mswm_cuda_ctx* ctx, int phase);
 /* The same transport between the members of an in-process group (plain
  * device pointers instead of IPC mappings). */

@@ -3513,7 +3513,8 @@ int mswm_cuda_peer_exchange(mswm_cuda_ctx* c, int phase) {
   return guard(c, [&] {
     check_ctx(c);
     if (c->transport != 1) throw Error(MSWM_E_USAGE, "peer transport not enabled");
-    if (phase != 0 && phase != 1) throw Error(MSWM_E_USAGE, "phase must be 0 (push) or 1 (wait + unpack)");
+    if (phase < 0 || phase > 2)
+      throw Error(MSWM_E_USAGE, "phase must be 0 (push), 1 (wait + unpack) or 2 (the same, not awaited)");
     Halo& x = c->halo;
     if (phase == 0) {
       k_push<<<unsigned(std::max<int64_t>(1, nblk(x.ns))), kBlock, 0, c->stream>>>(x.ns, x.scode.p,
@@ -3527,7 +3528,7 @@ int mswm_cuda_peer_exchange(mswm_cuda_ctx* c, int phase) {
           c->xchan.p, c->xerr.p, c->peer_budget_ns);
     }
     CK(cudaGetLastError());
-    check_dry(c);
+    if (phase != 2) check_dry(c);  // phase 2 returns at once: mswm_cuda_sync reports
     return int(MSWM_OK);
   });
 }

@@ -309,3 +309,37 @@ def test_peer_stores_silent_neighbour_is_an_error(monkeypatch):
     for rc in ranks:
         st = rc.ctx.download()
         assert bits_equal(st.h, rc.lm.gather_cells(wl.h)) and bits_equal(st.u, rc.lm.gather_edges(wl.u))
+
+
+def test_peer_stores_wait_then_push(monkeypatch):
+    """The wait really waits: rank 0's wait + unpack is enqueued first and polls
+    its flag while rank 1's push is launched afterwards on rank 1's own stream
+    (one block each on an idle device; the poll is bounded, so a failure to
+    overlap is an error, never a hang); the values stored during the poll are
+    the ones unpacked."""
+    from paper_2106_07154_b200.api import State
+    monkeypatch.setenv("MSWM_PEER_TIMEOUT_MS", "5000")
+    wl = W.small_sphere(4, seed=9, cap_deg=25.0)
+    o = Oracle(wl.mesh, wl.b, wl.f, wl.gravity)
+    o.set_regions(wl.fine_mask, wl.width)
+    lay = DistributedLayout(wl.mesh, *o.labels(), 2)
+    ranks = [RankContext(lay, r, wl.b, wl.f, wl.gravity) for r in range(2)]
+    grp = CudaGroup(ranks)
+    grp.use_peer_stores()
+    for rnd in range(4):
+        scale = 1.0 + rnd
+        for rc in ranks:
+            lm = rc.lm
+            hp, up = lm.gather_cells(wl.h) * scale, lm.gather_edges(wl.u) * scale
+            hp[lm.n_owned_cells:-1] = np.nan
+            up[lm.n_owned_edges:-1] = np.nan
+            rc.ctx.upload(State(hp, up, 0.0))
+        ranks[0].peer_exchange(0)      # rank 0's values and flag are out
+        ranks[0].peer_exchange(2)      # enqueued: polls for rank 1's flag
+        ranks[1].peer_exchange(0)      # arrives while rank 0 polls
+        ranks[0].ctx.sync()            # raises if the wait ran out of budget
+        ranks[1].peer_exchange(1)
+        for rc in ranks:
+            st = rc.ctx.download()
+            assert bits_equal(st.h, rc.lm.gather_cells(wl.h) * scale)
+            assert bits_equal(st.u, rc.lm.gather_edges(wl.u) * scale)
