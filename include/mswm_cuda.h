@@ -178,7 +178,8 @@ int mswm_cuda_state_download(mswm_cuda_ctx* ctx, double* h, double* u,
  * (:412-575), RK4 = rk4_step (:370-410), SSPRK3 / SSPRK2 = ssprk_step(3 / 2)
  * (:337-368).
  * Steps are replayed from a captured CUDA graph.  Asynchronous when
- * `sync` is 0 (errors then surface at the next synchronous call). */
+ * `sync` is 0 (errors then surface at the next synchronous call).  n_steps
+ * == 0 prepares only: plans built and the graph captured, nothing launched. */
 int mswm_cuda_step(mswm_cuda_ctx* ctx, int scheme, double dt, int M,
                    int64_t n_steps, int sync);
 

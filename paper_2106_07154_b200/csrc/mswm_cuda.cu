@@ -2777,8 +2777,9 @@ int mswm_cuda_step(mswm_cuda_ctx* c, int scheme, double dt, int M, int64_t n_ste
   return guard(c, [&] {
     check_ctx(c);
     check_step_args(c, scheme, dt, M, n_steps);
-    if (n_steps == 0) return int(MSWM_OK);
+    // n_steps == 0 prepares: plans built, the step graph captured, nothing launched
     cudaGraphExec_t g = graph_for(c, scheme, dt, M);
+    if (n_steps == 0) return int(MSWM_OK);
     c->batches.emplace_back(c->steps_issued, n_steps);
     for (int64_t k = 0; k < n_steps; ++k) {
       CK(cudaGraphLaunch(g, c->stream));

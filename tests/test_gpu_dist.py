@@ -343,3 +343,41 @@ def test_peer_stores_wait_then_push(monkeypatch):
             st = rc.ctx.download()
             assert bits_equal(st.h, rc.lm.gather_cells(wl.h) * scale)
             assert bits_equal(st.u, rc.lm.gather_edges(wl.u) * scale)
+
+
+@pytest.mark.parametrize("scheme,n_ranks", [(Scheme.LTS3, 3), (Scheme.RK4, 2)])
+def test_peer_stores_asynchronous_ranks_bitwise(scheme, n_ranks, monkeypatch):
+    """Every rank steps by itself -- its own stream, its own step graph, launched
+    without waiting for the others, as one process per GPU would -- and only
+    the peer-store flags order the halo exchanges (both channels, double
+    buffering, sequence counters across graph replays).  Small meshes on an
+    idle device, so the ranks' kernels are co-resident; the polls are bounded,
+    so a protocol error would be an error, not a hang.  Bitwise the oracle."""
+    monkeypatch.setenv("MSWM_PEER_TIMEOUT_MS", "20000")
+    wl = W.small_sphere(5, seed=53, cap_deg=25.0)
+    o = Oracle(wl.mesh, wl.b, wl.f, wl.gravity)
+    o.set_regions(wl.fine_mask, wl.width)
+    dt = wl.dt if scheme == Scheme.LTS3 else wl.dt / wl.M
+    h_ref, u_ref, _ = o.step(int(scheme), wl.h, wl.u, 0.0, dt, wl.M, 5)
+    lay = DistributedLayout(wl.mesh, *o.labels(), n_ranks)
+    ranks = [RankContext(lay, r, wl.b, wl.f, wl.gravity) for r in range(n_ranks)]
+    grp = CudaGroup(ranks)                       # only to wire the arenas in-process
+    grp.restrict_halos(LTS3_MASKS + [kMaskAll])
+    grp.use_peer_stores()
+    for rc in ranks:
+        rc.upload(wl.h, wl.u)
+        # plans and the step graph first: building them frees device memory, which
+        # on this one shared device would wait for the other ranks' polling kernels
+        rc.ctx.advance(scheme, dt, wl.M, 0)
+    for n in (2, 3):
+        for rc in ranks:                         # no rank waits for another on the host
+            rc.ctx.advance(scheme, dt, wl.M, n, sync=False)
+        for rc in ranks:
+            rc.ctx.sync()
+    if scheme == Scheme.LTS3:
+        assert all(rc.ctx.concurrent_coarse() == 1 for rc in ranks)
+    h = np.full(wl.mesh.n_cells, np.nan)
+    u = np.full(wl.mesh.n_edges, np.nan)
+    for rc in ranks:
+        rc.download_owned(h, u)
+    assert bits_equal(h, h_ref) and bits_equal(u, u_ref)
