@@ -345,7 +345,8 @@ def test_peer_stores_wait_then_push(monkeypatch):
             assert bits_equal(st.u, rc.lm.gather_edges(wl.u) * scale)
 
 
-@pytest.mark.parametrize("scheme,n_ranks", [(Scheme.LTS3, 3), (Scheme.RK4, 2)])
+@pytest.mark.parametrize("scheme,n_ranks", [(Scheme.LTS3, 3), (Scheme.RK4, 2), (Scheme.LTS2, 4),
+                                            (Scheme.LTS3, 4)])
 def test_peer_stores_asynchronous_ranks_bitwise(scheme, n_ranks, monkeypatch):
     """Every rank steps by itself -- its own stream, its own step graph, launched
     without waiting for the others, as one process per GPU would -- and only
@@ -357,7 +358,7 @@ def test_peer_stores_asynchronous_ranks_bitwise(scheme, n_ranks, monkeypatch):
     wl = W.small_sphere(5, seed=53, cap_deg=25.0)
     o = Oracle(wl.mesh, wl.b, wl.f, wl.gravity)
     o.set_regions(wl.fine_mask, wl.width)
-    dt = wl.dt if scheme == Scheme.LTS3 else wl.dt / wl.M
+    dt = wl.dt if scheme in (Scheme.LTS3, Scheme.LTS2) else wl.dt / wl.M
     h_ref, u_ref, _ = o.step(int(scheme), wl.h, wl.u, 0.0, dt, wl.M, 5)
     lay = DistributedLayout(wl.mesh, *o.labels(), n_ranks)
     ranks = [RankContext(lay, r, wl.b, wl.f, wl.gravity) for r in range(n_ranks)]
